@@ -1,0 +1,139 @@
+/* pmklc_b200 — C ABI of the B200-native PMKLC compress/decompress hot path.
+ *
+ * Drop-in boundary for the reference library's entry points
+ * (/root/reference/proj/core/include/pmklc/pipeline.hpp):
+ *
+ *   pmklc_compress            replaces  pmklc::compress(ByteSpan, const CompressConfig&, PipelineStats*)
+ *                                       pipeline.hpp:64, pipeline.cpp:303-377
+ *   pmklc_decompress          replaces  pmklc::decompress(ByteSpan, const std::string&, uint32_t, PipelineStats*)
+ *                                       pipeline.hpp:66-67, pipeline.cpp:379-450
+ *   pmklc_encode_chunks       replaces  pmklc::encode_chunk_standalone (batched over chunks)
+ *                                       pipeline.hpp:72-76, pipeline.cpp:298-301
+ *   pmklc_skmer_encode        replaces  pmklc::encode(const NucleotideStream&, SkParams, unsigned)
+ *                                       skmer.hpp:39, skmer.cpp:28-61
+ *   pmklc_cfg                 mirrors   pmklc::CompressConfig (pipeline.hpp:12-25), same defaults
+ *   pmklc_stats               mirrors   pmklc::WorkerStats (pipeline.hpp:27-35), one per chunk
+ *
+ * Conventions: plain pointers and sizes only. Return 0 on success, otherwise
+ * 1 + errc in the reference enum order (core/include/pmklc/error.hpp:8-43),
+ * e.g. 16 = ConfigInvalid, 11 = InvalidDistribution, 7 = ChecksumMismatch;
+ * 101 = a CUDA failure (no reference equivalent). pmklc_last_error() returns
+ * the thread-local message ("<ErrcName>: <what>", as error::what()). Output
+ * buffers are allocated by the library and released with pmklc_free(). There
+ * is no CPU fallback: without a usable sm_100 device every compute entry point
+ * fails with 101.
+ */
+#ifndef PMKLC_B200_H
+#define PMKLC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pmklc_cfg {
+  uint32_t s, k;            /* (s,k)-mer step and window, 1 <= s <= k <= 8      */
+  uint32_t t;               /* context length, 1..4096                          */
+  uint32_t bs;              /* substreams per chunk                             */
+  uint32_t workers;         /* data blocks (chunks), 1..max_workers             */
+  uint32_t scale;           /* model width divisor (1 = paper widths)           */
+  uint64_t selector_threshold;
+  uint64_t seed;
+  float smp_fraction;       /* Step-wise Model Passing fraction, [0,1)          */
+  const char* pub_model_path; /* SPuM file or NULL                              */
+  int32_t device;           /* CUDA device ordinal                              */
+  uint32_t max_workers;     /* 0 = reference cap (256, pipeline.cpp:20)         */
+} pmklc_cfg;
+
+typedef struct pmklc_stats {
+  uint64_t tokens, uniform_coded, pub_calls, priv_calls, dyn_calls;
+  uint64_t snapshot_recv_hash, snapshot_sent_hash;
+  double early_loss_bits;
+} pmklc_stats;
+
+typedef struct pmklc_timing {  /* CUDA-event times of the last call, ms */
+  double total_ms, h2d_ms, tokenize_ms, warmup_ms, model_ms, d2h_ms;
+  uint64_t ticks, kernel_launches, chunks, h2d_bytes, d2h_bytes;
+} pmklc_timing;
+
+/* CompressConfig{} defaults: s=k=3, t=32, bs=320, workers=1, threshold 5e8,
+ * smp 0.05, seed 42, scale 4, no public model, device 0. */
+void pmklc_cfg_default(pmklc_cfg* cfg);
+
+/* compress: host input, host container out. stats (nullable) receives one
+ * entry per chunk up to stats_cap; n_chunks (nullable) the chunk count. */
+int pmklc_compress(const uint8_t* in, size_t n, const pmklc_cfg* cfg, uint8_t** out,
+                   size_t* out_n, pmklc_stats* stats, size_t stats_cap, size_t* n_chunks,
+                   pmklc_timing* timing);
+/* same, input already resident in device memory (16-byte aligned) */
+int pmklc_compress_device(const uint8_t* d_in, size_t n, const pmklc_cfg* cfg, uint8_t** out,
+                          size_t* out_n, pmklc_stats* stats, size_t stats_cap, size_t* n_chunks,
+                          pmklc_timing* timing);
+
+/* decompress: host container in, host bytes out. `workers` is accepted for
+ * API parity; it only schedules threads in the reference. */
+int pmklc_decompress(const uint8_t* in, size_t n, const char* pub_model_path, uint32_t workers,
+                     int32_t device, uint8_t** out, size_t* out_n, pmklc_stats* stats,
+                     size_t stats_cap, pmklc_timing* timing);
+/* same, output left in device memory (release with pmklc_device_free) */
+int pmklc_decompress_to_device(const uint8_t* in, size_t n, const char* pub_model_path,
+                               int32_t device, uint8_t** d_out, size_t* out_n,
+                               pmklc_timing* timing);
+
+/* encode_chunk_standalone over n_chunks chunks at once: chunk i codes
+ * tokens[off_i, off_i + chunk_len[i]) (off_i = prefix sum) from inbound
+ * snapshot i (length 0 = seeded init). payloads[i] is library-allocated. */
+int pmklc_encode_chunks(const uint32_t* tokens, const uint64_t* chunk_len, size_t n_chunks,
+                        const uint8_t* const* inbound, const size_t* inbound_len, uint32_t flags,
+                        const char* pub_model_path, uint32_t k, uint32_t t, uint32_t bs,
+                        uint32_t scale, uint64_t dm_seed, int32_t device, uint8_t** payloads,
+                        size_t* payload_lens);
+
+/* one chunk with a probe of its mixed probabilities [max_steps, bs, 4^k]
+ * (diagnostic; mirrors oracle/ pmref_dump_chunk) */
+int pmklc_dump_chunk(const uint32_t* tokens, uint64_t n_tokens, uint32_t flags,
+                     const char* pub_model_path, uint32_t k, uint32_t t, uint32_t bs,
+                     uint32_t scale, uint64_t dm_seed, const uint8_t* inbound, size_t inbound_n,
+                     int32_t device, float* probs, uint64_t max_steps, uint8_t** payload,
+                     size_t* payload_n);
+
+/* (s,k)-mer tokenizer on host base codes 0..3 -> tokens (capacity m) */
+int pmklc_skmer_encode(const uint8_t* codes, uint64_t n, uint32_t s, uint32_t k, int32_t device,
+                       uint32_t* tokens, uint64_t* m);
+/* tokenizer on device buffers: packed 2-bit bases (base i at bits 2*(i%4) of
+ * byte i/4, 16-byte aligned) -> u32 tokens; `stream` is a cudaStream_t */
+int pmklc_skmer_encode_packed_device(const uint8_t* d_packed, uint64_t n_bases, uint32_t s,
+                                     uint32_t k, uint32_t* d_tokens, void* stream);
+
+/* host logic of PMKLC-M block partitioning: plan_chunks (pipeline.cpp:32-52)
+ * and snapshot_step (pipeline.cpp:26-30); arrays of capacity `cap` */
+int pmklc_plan_chunks(uint64_t m, uint32_t workers, uint32_t bs, uint32_t t, uint16_t smp_per_myriad,
+                      uint64_t* starts, uint64_t* lens, uint64_t* snapshot_steps, size_t cap,
+                      size_t* count, uint32_t* bs_out);
+/* Step-wise Model Passing tick schedule for chunks of token length lens[i]
+ * (the device realisation of run_chunks, pipeline.cpp:253-294): per chunk the
+ * tick of its first model step, the chunk its inbound state comes from (-1 =
+ * seeded init), that source's completed model steps, and its own model steps */
+int pmklc_schedule(const uint64_t* lens, size_t n_chunks, uint32_t bs, uint32_t t,
+                   uint16_t smp_per_myriad, int64_t* offset, int64_t* src, uint64_t* src_steps,
+                   uint64_t* model_steps, int64_t* ticks);
+
+void pmklc_free(void* p);
+void pmklc_device_free(void* d_p);
+const char* pmklc_last_error(void);
+const char* pmklc_errc_name(int code);
+const char* pmklc_version(void);
+
+/* synthetic inputs for benchmarks; not on the hot path */
+void pmklc_synth_markov3(uint8_t* out, uint64_t n, uint64_t seed);
+void pmklc_synth_uniform(uint8_t* out, uint64_t n, uint64_t seed);
+void pmklc_synth_genome(uint8_t* out, uint64_t n, uint64_t seed, uint32_t segments);
+void pmklc_synth_species(uint8_t* out, uint64_t n, uint64_t seed, uint64_t block);
+void pmklc_synth_packed_codes(uint8_t* out, uint64_t n_bytes, uint64_t seed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

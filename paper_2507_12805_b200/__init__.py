@@ -1,0 +1,299 @@
+"""pmklc_b200 — B200-native PMKLC compress/decompress hot path.
+
+Python mirror of the reference's public API (core/include/pmklc/pipeline.hpp):
+``CompressConfig`` with the same fields and defaults, ``compress`` /
+``decompress`` with the same argument meaning, ``PmklcError`` carrying the
+reference ``errc`` name (core/include/pmklc/error.hpp). Every call goes
+through the C ABI in include/pmklc_b200.h (lib/libpmklc_b200.so, built in-tree
+by ``__graft_entry__.build()``); there is no CPU fallback — if the library or
+a CUDA device is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import List, Optional, Sequence
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "lib" / "libpmklc_b200.so"
+
+ERRC = [
+    "LengthMismatch", "TokenOutOfRange", "NotOverlapping", "ShapeMismatch", "StaleTape",
+    "ContextLengthMismatch", "ChecksumMismatch", "ArchitectureMismatch", "MissingLogits",
+    "BatchMismatch", "InvalidDistribution", "StreamExhausted", "BadMagic", "UnsupportedVersion",
+    "TableInconsistent", "ConfigInvalid", "IoError", "SpumMissing", "CorruptStream", "CorpusEmpty",
+    "TargetTooShort", "EmptySource", "ZeroTime", "EmptyList", "VerificationFailed",
+]
+
+
+class PmklcError(RuntimeError):
+    """pmklc::error equivalent: ``.errc`` is the reference enum name."""
+
+    def __init__(self, code: int, message: str):
+        self.code = code
+        self.errc = ERRC[code - 1] if 1 <= code <= len(ERRC) else ("CudaError" if code == 101 else "Unknown")
+        super().__init__(message)
+
+
+class _Cfg(C.Structure):
+    _fields_ = [("s", C.c_uint32), ("k", C.c_uint32), ("t", C.c_uint32), ("bs", C.c_uint32),
+                ("workers", C.c_uint32), ("scale", C.c_uint32),
+                ("selector_threshold", C.c_uint64), ("seed", C.c_uint64),
+                ("smp_fraction", C.c_float), ("pub_model_path", C.c_char_p),
+                ("device", C.c_int32), ("max_workers", C.c_uint32)]
+
+
+class Stats(C.Structure):
+    """WorkerStats (pipeline.hpp:27-35), one per chunk."""
+    _fields_ = [("tokens", C.c_uint64), ("uniform_coded", C.c_uint64), ("pub_calls", C.c_uint64),
+                ("priv_calls", C.c_uint64), ("dyn_calls", C.c_uint64),
+                ("snapshot_recv_hash", C.c_uint64), ("snapshot_sent_hash", C.c_uint64),
+                ("early_loss_bits", C.c_double)]
+
+
+class Timing(C.Structure):
+    _fields_ = [("total_ms", C.c_double), ("h2d_ms", C.c_double), ("tokenize_ms", C.c_double),
+                ("warmup_ms", C.c_double), ("model_ms", C.c_double), ("d2h_ms", C.c_double),
+                ("ticks", C.c_uint64), ("kernel_launches", C.c_uint64), ("chunks", C.c_uint64),
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+
+
+# Every symbol include/pmklc_b200.h declares (checked by tests/test_capi.py).
+EXPORTS = [
+    "pmklc_cfg_default", "pmklc_compress", "pmklc_compress_device", "pmklc_decompress",
+    "pmklc_decompress_to_device", "pmklc_encode_chunks", "pmklc_dump_chunk", "pmklc_skmer_encode",
+    "pmklc_skmer_encode_packed_device", "pmklc_free", "pmklc_device_free", "pmklc_last_error",
+    "pmklc_errc_name", "pmklc_version", "pmklc_synth_markov3", "pmklc_synth_uniform",
+    "pmklc_synth_genome", "pmklc_synth_species", "pmklc_synth_packed_codes", "pmklc_plan_chunks",
+    "pmklc_schedule",
+]
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load the in-tree C ABI library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build()")
+        L = C.CDLL(str(LIB_PATH))
+        L.pmklc_last_error.restype = C.c_char_p
+        L.pmklc_errc_name.restype = C.c_char_p
+        L.pmklc_version.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise PmklcError(rc, lib().pmklc_last_error().decode(errors="replace"))
+
+
+def _take(ptr, n: int) -> bytes:
+    b = C.string_at(ptr, n)
+    lib().pmklc_free(ptr)
+    return b
+
+
+@dataclass
+class CompressConfig:
+    """pmklc::CompressConfig (pipeline.hpp:12-25), same defaults."""
+    s: int = 3
+    k: int = 3
+    t: int = 32
+    bs: int = 320
+    workers: int = 1
+    selector_threshold: int = 500_000_000
+    smp_fraction: float = 0.05
+    seed: int = 42
+    scale: int = 4
+    pub_model_path: str = ""
+    device: int = 0
+    max_workers: int = 0  # 0 = the reference's 256 cap
+
+    def _c(self) -> _Cfg:
+        return _Cfg(self.s, self.k, self.t, self.bs, self.workers, self.scale,
+                    self.selector_threshold, self.seed, self.smp_fraction,
+                    self.pub_model_path.encode() if self.pub_model_path else None,
+                    self.device, self.max_workers)
+
+
+@dataclass
+class PipelineStats:
+    workers: List[Stats] = field(default_factory=list)
+    timing: Optional[Timing] = None
+
+
+def compress(raw: bytes, cfg: CompressConfig = CompressConfig(),
+             stats: Optional[PipelineStats] = None) -> bytes:
+    """pmklc::compress — returns the PMKL container (byte-identical to the reference)."""
+    c = cfg._c()
+    out = C.POINTER(C.c_uint8)()
+    n = C.c_size_t()
+    cap = 1 << 16
+    st = (Stats * cap)() if stats is not None else None
+    nch = C.c_size_t()
+    tm = Timing()
+    _check(lib().pmklc_compress(raw, C.c_size_t(len(raw)), C.byref(c), C.byref(out), C.byref(n),
+                                st, C.c_size_t(cap if st is not None else 0), C.byref(nch),
+                                C.byref(tm)))
+    if stats is not None:
+        stats.workers = [st[i] for i in range(nch.value)]
+        stats.timing = tm
+    return _take(out, n.value)
+
+
+def compress_device(d_ptr: int, n: int, cfg: CompressConfig = CompressConfig(),
+                    timing: Optional[Timing] = None) -> bytes:
+    """compress with the input already in device memory (pointer as int)."""
+    c = cfg._c()
+    out = C.POINTER(C.c_uint8)()
+    on = C.c_size_t()
+    tm = timing if timing is not None else Timing()
+    _check(lib().pmklc_compress_device(C.c_void_p(d_ptr), C.c_size_t(n), C.byref(c), C.byref(out),
+                                       C.byref(on), None, C.c_size_t(0), None, C.byref(tm)))
+    return _take(out, on.value)
+
+
+def decompress(container: bytes, pub_model_path: str = "", workers: int = 1,
+               stats: Optional[PipelineStats] = None, device: int = 0) -> bytes:
+    """pmklc::decompress — bit-exact inverse of compress."""
+    out = C.POINTER(C.c_uint8)()
+    n = C.c_size_t()
+    cap = 1 << 16
+    st = (Stats * cap)() if stats is not None else None
+    tm = Timing()
+    _check(lib().pmklc_decompress(container, C.c_size_t(len(container)),
+                                  pub_model_path.encode() if pub_model_path else None, workers,
+                                  device, C.byref(out), C.byref(n), st,
+                                  C.c_size_t(cap if st is not None else 0), C.byref(tm)))
+    if stats is not None:
+        nchunks = int.from_bytes(container[48:52], "little") if len(container) >= 52 else 0
+        stats.workers = [st[i] for i in range(min(nchunks, cap))]
+        stats.timing = tm
+    return _take(out, n.value)
+
+
+def decompress_to_device(container: bytes, pub_model_path: str = "", device: int = 0,
+                         timing: Optional[Timing] = None):
+    """Returns (device_ptr:int, length); free with device_free."""
+    d = C.c_void_p()
+    n = C.c_size_t()
+    tm = timing if timing is not None else Timing()
+    _check(lib().pmklc_decompress_to_device(container, C.c_size_t(len(container)),
+                                            pub_model_path.encode() if pub_model_path else None,
+                                            device, C.byref(d), C.byref(n), C.byref(tm)))
+    return d.value, n.value
+
+
+def device_free(ptr: int) -> None:
+    lib().pmklc_device_free(C.c_void_p(ptr))
+
+
+def encode_chunks(tokens, chunk_lens: Sequence[int], inbound: Sequence[bytes], flags: int, k: int,
+                  t: int, bs: int, scale: int, dm_seed: int, pub_model_path: str = "",
+                  device: int = 0) -> List[bytes]:
+    """Batched pmklc::encode_chunk_standalone."""
+    import numpy as np
+    tokens = np.ascontiguousarray(tokens, dtype=np.uint32)
+    nc = len(chunk_lens)
+    lens = (C.c_uint64 * nc)(*chunk_lens)
+    ib = (C.c_char_p * nc)(*[bytes(b) for b in inbound])
+    ibl = (C.c_size_t * nc)(*[len(b) for b in inbound])
+    pays = (C.POINTER(C.c_uint8) * nc)()
+    pl = (C.c_size_t * nc)()
+    _check(lib().pmklc_encode_chunks(tokens.ctypes.data_as(C.c_void_p), lens, C.c_size_t(nc),
+                                     C.cast(ib, C.c_void_p), ibl, flags,
+                                     pub_model_path.encode() if pub_model_path else None, k, t, bs,
+                                     scale, C.c_uint64(dm_seed), device, pays, pl))
+    return [_take(pays[i], pl[i]) for i in range(nc)]
+
+
+def dump_chunk(tokens, flags: int, k: int, t: int, bs: int, scale: int, dm_seed: int,
+               pub_model_path: str = "", inbound: bytes = b"", max_steps: int = 0, device: int = 0):
+    """One chunk with its first max_steps mixed-probability tables: (payload, probs)."""
+    import numpy as np
+    tokens = np.ascontiguousarray(tokens, dtype=np.uint32)
+    V = 1 << (2 * k)
+    probs = np.zeros((max(max_steps, 1), bs, V), dtype=np.float32)
+    out = C.POINTER(C.c_uint8)()
+    n = C.c_size_t()
+    _check(lib().pmklc_dump_chunk(tokens.ctypes.data_as(C.c_void_p), C.c_uint64(len(tokens)), flags,
+                                  pub_model_path.encode() if pub_model_path else None, k, t, bs,
+                                  scale, C.c_uint64(dm_seed), inbound, C.c_size_t(len(inbound)),
+                                  device, probs.ctypes.data_as(C.c_void_p), C.c_uint64(max_steps),
+                                  C.byref(out), C.byref(n)))
+    return _take(out, n.value), probs[:max_steps]
+
+
+def skmer_encode(codes: bytes, s: int, k: int, device: int = 0):
+    """pmklc::encode on base codes 0..3 -> numpy uint32 tokens."""
+    import numpy as np
+    n = len(codes)
+    mcap = (n - k) // s + 1 if n >= k else 0
+    tok = np.zeros(max(mcap, 1), dtype=np.uint32)
+    m = C.c_uint64()
+    _check(lib().pmklc_skmer_encode(codes, C.c_uint64(n), s, k, device,
+                                    tok.ctypes.data_as(C.c_void_p), C.byref(m)))
+    return tok[: m.value]
+
+
+def skmer_encode_packed_device(d_packed: int, n_bases: int, s: int, k: int, d_tokens: int,
+                               stream: int = 0) -> None:
+    _check(lib().pmklc_skmer_encode_packed_device(C.c_void_p(d_packed), C.c_uint64(n_bases), s, k,
+                                                  C.c_void_p(d_tokens), C.c_void_p(stream)))
+
+
+def plan_chunks(m: int, workers: int, bs: int, t: int, smp_per_myriad: int):
+    """pmklc::plan_chunks (host logic): (starts, lens, bs, snapshot_steps)."""
+    cap = max(workers, 1)
+    st = (C.c_uint64 * cap)()
+    ln = (C.c_uint64 * cap)()
+    sn = (C.c_uint64 * cap)()
+    cnt = C.c_size_t()
+    bso = C.c_uint32()
+    _check(lib().pmklc_plan_chunks(C.c_uint64(m), workers, bs, t, C.c_uint16(smp_per_myriad), st, ln,
+                                   sn, C.c_size_t(cap), C.byref(cnt), C.byref(bso)))
+    n = cnt.value
+    return list(st[:n]), list(ln[:n]), bso.value, list(sn[:n])
+
+
+def schedule(lens: Sequence[int], bs: int, t: int, smp_per_myriad: int):
+    """Tick schedule of Step-wise Model Passing (host logic): per chunk
+    (offset, src, src_steps, model_steps) and the tick count."""
+    nc = len(lens)
+    L = (C.c_uint64 * nc)(*lens)
+    off = (C.c_int64 * nc)()
+    src = (C.c_int64 * nc)()
+    ss = (C.c_uint64 * nc)()
+    ms = (C.c_uint64 * nc)()
+    ticks = C.c_int64()
+    _check(lib().pmklc_schedule(L, C.c_size_t(nc), bs, t, C.c_uint16(smp_per_myriad), off, src, ss,
+                                ms, C.byref(ticks)))
+    return list(off), list(src), list(ss), list(ms), ticks.value
+
+
+def synth(kind: str, n: int, seed: int, extra: int = 0) -> bytes:
+    """Seeded synthetic DNA: markov3 | uniform | genome | species | packed."""
+    buf = (C.c_uint8 * max(n, 1))()
+    L = lib()
+    if kind == "markov3":
+        L.pmklc_synth_markov3(buf, C.c_uint64(n), C.c_uint64(seed))
+    elif kind == "uniform":
+        L.pmklc_synth_uniform(buf, C.c_uint64(n), C.c_uint64(seed))
+    elif kind == "genome":
+        L.pmklc_synth_genome(buf, C.c_uint64(n), C.c_uint64(seed), C.c_uint32(extra or 10))
+    elif kind == "species":
+        L.pmklc_synth_species(buf, C.c_uint64(n), C.c_uint64(seed), C.c_uint64(extra))
+    elif kind == "packed":
+        L.pmklc_synth_packed_codes(buf, C.c_uint64(n), C.c_uint64(seed))
+    else:
+        raise ValueError(kind)
+    return bytes(buf)[:n]
+
+
+def version() -> str:
+    return lib().pmklc_version().decode()

@@ -1,0 +1,271 @@
+// extern "C" boundary (include/pmklc_b200.h) over the B200 engine.
+#include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "../../include/pmklc_b200.h"
+#include "host/engine.hpp"
+#include "host/plan.hpp"
+
+namespace pmklc_b200 {
+void synth_markov3(uint8_t*, uint64_t, uint64_t);
+void synth_uniform(uint8_t*, uint64_t, uint64_t);
+void synth_packed_codes(uint8_t*, uint64_t, uint64_t);
+void synth_genome(uint8_t*, uint64_t, uint64_t, uint32_t);
+void synth_species(uint8_t*, uint64_t, uint64_t, uint64_t);
+}  // namespace pmklc_b200
+
+using namespace pmklc_b200;
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return 1 + int(e.code());
+  } catch (const std::bad_alloc&) {
+    g_err = "CudaError: host allocation failed";
+    return 1 + int(errc::cuda_error);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1 + int(errc::cuda_error);
+  }
+}
+
+uint8_t* dup(const Bytes& v) {
+  uint8_t* p = static_cast<uint8_t*>(std::malloc(v.size() ? v.size() : 1));
+  if (!p) throw std::bad_alloc();
+  if (!v.empty()) std::memcpy(p, v.data(), v.size());
+  return p;
+}
+
+Config to_cfg(const pmklc_cfg* c) {
+  Config cfg;
+  cfg.s = c->s;
+  cfg.k = c->k;
+  cfg.t = c->t;
+  cfg.bs = c->bs;
+  cfg.workers = c->workers;
+  cfg.scale = c->scale;
+  cfg.selector_threshold = c->selector_threshold;
+  cfg.seed = c->seed;
+  cfg.smp_fraction = c->smp_fraction;
+  if (c->pub_model_path) cfg.pub_model_path = c->pub_model_path;
+  cfg.device = c->device;
+  cfg.max_workers = c->max_workers ? c->max_workers : 256;
+  return cfg;
+}
+
+void copy_stats(const std::vector<ChunkStats>& st, pmklc_stats* out, size_t cap) {
+  if (!out) return;
+  for (size_t i = 0; i < st.size() && i < cap; ++i) {
+    const ChunkStats& s = st[i];
+    out[i] = pmklc_stats{s.tokens,    s.uniform_coded,      s.pub_calls,          s.priv_calls,
+                         s.dyn_calls, s.snapshot_recv_hash, s.snapshot_sent_hash, s.early_loss_bits};
+  }
+}
+
+void copy_timing(const Timing& t, pmklc_timing* out) {
+  if (!out) return;
+  *out = pmklc_timing{t.total_ms, t.h2d_ms, t.tokenize_ms, t.warmup_ms, t.model_ms, t.d2h_ms,
+                      t.ticks,    t.kernel_launches, t.chunks, t.h2d_bytes, t.d2h_bytes};
+}
+
+int do_compress(const uint8_t* h, const uint8_t* d, size_t n, const pmklc_cfg* c, uint8_t** out,
+                size_t* out_n, pmklc_stats* stats, size_t cap, size_t* n_chunks, pmklc_timing* tm) {
+  return guard([&] {
+    if (!c) raise(errc::config_invalid, "null config");
+    std::vector<ChunkStats> st;
+    Timing t;
+    CallOptions opt;
+    opt.want_stats = stats != nullptr;
+    opt.stats = &st;
+    opt.timing = &t;
+    Bytes v = h ? compress(h, n, to_cfg(c), opt) : compress_device(d, n, to_cfg(c), opt);
+    copy_stats(st, stats, cap);
+    if (n_chunks) *n_chunks = st.size();
+    copy_timing(t, tm);
+    *out = dup(v);
+    *out_n = v.size();
+  });
+}
+}  // namespace
+
+extern "C" {
+
+void pmklc_cfg_default(pmklc_cfg* c) {
+  *c = pmklc_cfg{3, 3, 32, 320, 1, 4, 500000000ull, 42, 0.05f, nullptr, 0, 0};
+}
+
+int pmklc_compress(const uint8_t* in, size_t n, const pmklc_cfg* cfg, uint8_t** out, size_t* out_n,
+                   pmklc_stats* stats, size_t stats_cap, size_t* n_chunks, pmklc_timing* timing) {
+  static const uint8_t empty = 0;
+  return do_compress(in ? in : &empty, nullptr, n, cfg, out, out_n, stats, stats_cap, n_chunks,
+                     timing);
+}
+
+int pmklc_compress_device(const uint8_t* d_in, size_t n, const pmklc_cfg* cfg, uint8_t** out,
+                          size_t* out_n, pmklc_stats* stats, size_t stats_cap, size_t* n_chunks,
+                          pmklc_timing* timing) {
+  return do_compress(nullptr, d_in, n, cfg, out, out_n, stats, stats_cap, n_chunks, timing);
+}
+
+int pmklc_decompress(const uint8_t* in, size_t n, const char* pub_model_path, uint32_t workers,
+                     int32_t device, uint8_t** out, size_t* out_n, pmklc_stats* stats,
+                     size_t stats_cap, pmklc_timing* timing) {
+  return guard([&] {
+    std::vector<ChunkStats> st;
+    Timing t;
+    CallOptions opt;
+    opt.want_stats = stats != nullptr;
+    opt.stats = &st;
+    opt.timing = &t;
+    Bytes v = decompress(in, n, pub_model_path ? pub_model_path : "", workers, device, opt);
+    copy_stats(st, stats, stats_cap);
+    copy_timing(t, timing);
+    *out = dup(v);
+    *out_n = v.size();
+  });
+}
+
+int pmklc_decompress_to_device(const uint8_t* in, size_t n, const char* pub_model_path,
+                               int32_t device, uint8_t** d_out, size_t* out_n,
+                               pmklc_timing* timing) {
+  return guard([&] {
+    Timing t;
+    CallOptions opt;
+    opt.timing = &t;
+    *d_out = decompress_to_device(in, n, pub_model_path ? pub_model_path : "", device, out_n, opt);
+    copy_timing(t, timing);
+  });
+}
+
+int pmklc_encode_chunks(const uint32_t* tokens, const uint64_t* chunk_len, size_t n_chunks,
+                        const uint8_t* const* inbound, const size_t* inbound_len, uint32_t flags,
+                        const char* pub_model_path, uint32_t k, uint32_t t, uint32_t bs,
+                        uint32_t scale, uint64_t dm_seed, int32_t device, uint8_t** payloads,
+                        size_t* payload_lens) {
+  return guard([&] {
+    std::vector<ChunkJob> jobs(n_chunks);
+    uint64_t off = 0;
+    for (size_t i = 0; i < n_chunks; ++i) {
+      jobs[i].tokens = tokens + off;
+      jobs[i].n_tokens = chunk_len[i];
+      off += chunk_len[i];
+      if (inbound && inbound_len && inbound_len[i])
+        jobs[i].inbound.assign(inbound[i], inbound[i] + inbound_len[i]);
+    }
+    std::vector<Bytes> out = encode_chunks(jobs, uint8_t(flags), pub_model_path ? pub_model_path : "",
+                                           k, t, bs, scale, dm_seed, device);
+    for (size_t i = 0; i < n_chunks; ++i) {
+      payloads[i] = dup(out[i]);
+      payload_lens[i] = out[i].size();
+    }
+  });
+}
+
+int pmklc_dump_chunk(const uint32_t* tokens, uint64_t n_tokens, uint32_t flags,
+                     const char* pub_model_path, uint32_t k, uint32_t t, uint32_t bs,
+                     uint32_t scale, uint64_t dm_seed, const uint8_t* inbound, size_t inbound_n,
+                     int32_t device, float* probs, uint64_t max_steps, uint8_t** payload,
+                     size_t* payload_n) {
+  return guard([&] {
+    std::vector<ChunkJob> jobs(1);
+    jobs[0].tokens = tokens;
+    jobs[0].n_tokens = n_tokens;
+    if (inbound_n) jobs[0].inbound.assign(inbound, inbound + inbound_n);
+    std::vector<float> pr(size_t(max_steps) * bs * (uint64_t(1) << (2 * k)));
+    CallOptions opt;
+    opt.probe_chunk = 0;
+    opt.probe_steps = max_steps;
+    opt.probe = &pr;
+    std::vector<Bytes> out = encode_chunks(jobs, uint8_t(flags), pub_model_path ? pub_model_path : "",
+                                           k, t, bs, scale, dm_seed, device, opt);
+    if (probs && !pr.empty()) std::memcpy(probs, pr.data(), pr.size() * 4);
+    *payload = dup(out[0]);
+    *payload_n = out[0].size();
+  });
+}
+
+int pmklc_skmer_encode(const uint8_t* codes, uint64_t n, uint32_t s, uint32_t k, int32_t device,
+                       uint32_t* tokens, uint64_t* m) {
+  return guard([&] {
+    std::vector<uint32_t> t = skmer_encode_codes(codes, n, s, k, device);
+    *m = t.size();
+    if (tokens && !t.empty()) std::memcpy(tokens, t.data(), t.size() * 4);
+  });
+}
+
+int pmklc_skmer_encode_packed_device(const uint8_t* d_packed, uint64_t n_bases, uint32_t s,
+                                     uint32_t k, uint32_t* d_tokens, void* stream) {
+  return guard([&] { skmer_encode_packed_device(d_packed, n_bases, s, k, d_tokens, stream); });
+}
+
+int pmklc_plan_chunks(uint64_t m, uint32_t workers, uint32_t bs, uint32_t t, uint16_t myriad,
+                      uint64_t* starts, uint64_t* lens, uint64_t* snaps, size_t cap, size_t* count,
+                      uint32_t* bs_out) {
+  return guard([&] {
+    const Plan p = plan_chunks(m, workers, bs, t, myriad);
+    *count = p.len.size();
+    *bs_out = p.bs;
+    for (size_t i = 0; i < p.len.size() && i < cap; ++i) {
+      starts[i] = p.start[i];
+      lens[i] = p.len[i];
+      snaps[i] = p.snapshot_step(i);
+    }
+  });
+}
+
+int pmklc_schedule(const uint64_t* lens, size_t n, uint32_t bs, uint32_t t, uint16_t myriad,
+                   int64_t* offset, int64_t* src, uint64_t* src_steps, uint64_t* model_steps,
+                   int64_t* ticks) {
+  return guard([&] {
+    Plan p;
+    p.bs = bs;
+    p.t = t;
+    p.myriad = myriad;
+    uint64_t s = 0;
+    for (size_t i = 0; i < n; ++i) {
+      p.start.push_back(s);
+      p.len.push_back(lens[i]);
+      s += lens[i];
+    }
+    const Schedule sc = make_schedule(p, myriad > 0);
+    for (size_t i = 0; i < n; ++i) {
+      offset[i] = sc.offset[i];
+      src[i] = sc.src[i];
+      src_steps[i] = sc.src_steps[i];
+      model_steps[i] = sc.M[i];
+    }
+    *ticks = sc.ticks;
+  });
+}
+
+void pmklc_free(void* p) { std::free(p); }
+void pmklc_device_free(void* d_p) {
+  if (d_p) cudaFree(d_p);
+}
+const char* pmklc_last_error(void) { return g_err.c_str(); }
+const char* pmklc_errc_name(int code) { return errc_name(errc(code - 1)); }
+const char* pmklc_version(void) { return "pmklc_b200 0.1 (sm_100a, EXACT mode)"; }
+
+void pmklc_synth_markov3(uint8_t* out, uint64_t n, uint64_t seed) { synth_markov3(out, n, seed); }
+void pmklc_synth_uniform(uint8_t* out, uint64_t n, uint64_t seed) { synth_uniform(out, n, seed); }
+void pmklc_synth_genome(uint8_t* out, uint64_t n, uint64_t seed, uint32_t segments) {
+  synth_genome(out, n, seed, segments);
+}
+void pmklc_synth_species(uint8_t* out, uint64_t n, uint64_t seed, uint64_t block) {
+  synth_species(out, n, seed, block);
+}
+void pmklc_synth_packed_codes(uint8_t* out, uint64_t n_bytes, uint64_t seed) {
+  synth_packed_codes(out, n_bytes, seed);
+}
+
+}  // extern "C"

@@ -1,0 +1,977 @@
+// B200 engine: reference control flow on the host, every per-token stage on
+// the device. See engine.hpp and DESIGN.md.
+#include "engine.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+
+#include "../kernels/kernels.hpp"
+#include "container.hpp"
+#include "plan.hpp"
+#include "rng.hpp"
+
+namespace pmklc_b200 {
+
+namespace {
+
+#define CK(x)                                                                      \
+  do {                                                                             \
+    cudaError_t e_ = (x);                                                          \
+    if (e_ != cudaSuccess)                                                         \
+      raise(errc::cuda_error, std::string(#x) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  void alloc(size_t count) {
+    free();
+    n = count;
+    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { free(); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  void upload(const T* h, size_t count, cudaStream_t st, size_t at = 0) {
+    if (count) CK(cudaMemcpyAsync(p + at, h, count * sizeof(T), cudaMemcpyHostToDevice, st));
+  }
+  void zero(cudaStream_t st) {
+    if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), st));
+  }
+};
+
+struct Stream {
+  cudaStream_t s = nullptr;
+  explicit Stream(int device) {
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  }
+  ~Stream() {
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
+struct Event {
+  cudaEvent_t e = nullptr;
+  Event() { CK(cudaEventCreate(&e)); }
+  ~Event() {
+    if (e) cudaEventDestroy(e);
+  }
+  void record(cudaStream_t s) { CK(cudaEventRecord(e, s)); }
+  static double ms(const Event& a, const Event& b) {
+    float f = 0;
+    CK(cudaEventElapsedTime(&f, a.e, b.e));
+    return double(f);
+  }
+};
+
+void check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) raise(errc::cuda_error, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+uint64_t token_count(uint64_t n, uint32_t s, uint32_t k) { return n < k ? 0 : (n - k) / s + 1; }
+
+// pack_tokens / unpack_tokens (pipeline.cpp:58-92)
+Bytes pack_tokens(const uint32_t* tok, uint64_t n, uint32_t k) {
+  const unsigned bits = 2u * k;
+  Bytes out;
+  uint64_t acc = 0;
+  unsigned fill = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    acc |= uint64_t(tok[i]) << fill;
+    fill += bits;
+    while (fill >= 8) {
+      out.push_back(uint8_t(acc));
+      acc >>= 8;
+      fill -= 8;
+    }
+  }
+  if (fill) out.push_back(uint8_t(acc));
+  return out;
+}
+
+void unpack_tokens(const uint8_t* b, size_t bn, uint32_t k, uint32_t* out, uint64_t n) {
+  const unsigned bits = 2u * k;
+  const uint32_t limit = uint32_t(1) << bits;
+  uint64_t acc = 0;
+  unsigned fill = 0;
+  size_t pos = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    while (fill < bits) {
+      if (pos >= bn) raise(errc::corrupt_stream, "trailer shorter than its token count");
+      acc |= uint64_t(b[pos++]) << fill;
+      fill += 8;
+    }
+    out[i] = uint32_t(acc & (limit - 1));
+    acc >>= bits;
+    fill -= bits;
+  }
+}
+
+// A frozen BiGRU predictor resident on the device.
+struct DevBiGru {
+  BiGru host;
+  DBuf<float> w;
+  DBuf<int64_t> offs;
+  void upload(BiGru m, cudaStream_t st) {
+    host = std::move(m);
+    w.alloc(host.total);
+    w.upload(host.w.data(), host.total, st);
+    std::vector<int64_t> o;
+    for (const ParamDesc& p : host.ps) o.push_back(int64_t(p.off));
+    offs.alloc(o.size());
+    offs.upload(o.data(), o.size(), st);
+    CK(cudaStreamSynchronize(st));
+  }
+  BiGruP params(int R) const {
+    BiGruP p;
+    p.w = w.p;
+    p.offs = offs.p;
+    p.layers = host.layers;
+    p.V = int(host.d.V);
+    p.T = int(host.d.T);
+    p.Es = int(host.d.se);
+    p.Hs = int(host.d.sh);
+    p.B = int(host.d.sb);
+    p.R = R;
+    return p;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Per-call chunk engine: state slots, tapes and the tick loop.
+struct ChunkRun {
+  // inputs
+  Dims dims;
+  uint32_t R = 1, t = 1;
+  uint8_t flags = 4;
+  bool decode = false;
+  const DevBiGru* pub = nullptr;
+  const DevBiGru* priv = nullptr;
+  uint64_t dm_seed = 0;
+  std::vector<uint64_t> start;  // token offset per chunk
+  Schedule sch;
+  std::vector<const DmState*> init_state;  // per chunk; nullptr = seeded / handoff
+  // decode: payload bytes per chunk (host spans)
+  std::vector<const uint8_t*> pay_in;
+  std::vector<uint64_t> pay_in_len;
+  const CallOptions* opt = nullptr;
+  // outputs
+  std::vector<Bytes> payloads;  // encode
+  std::vector<ChunkStats> stats;
+  uint64_t launches = 0;
+  double warm_ms = 0, model_ms = 0;
+};
+
+// Host snapshot of a device state slot (for stats / snapshot hashes).
+DmState fetch_state(const DmLayout& L, const float* w, const float* m, const float* v,
+                    const AdamScalars* sc, int64_t c, cudaStream_t st) {
+  DmState s;
+  s.w.resize(L.total);
+  s.m.resize(L.total);
+  s.v.resize(L.total);
+  AdamScalars a;
+  CK(cudaMemcpyAsync(s.w.data(), w + c * int64_t(L.total), L.total * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(s.m.data(), m + c * int64_t(L.total), L.total * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(s.v.data(), v + c * int64_t(L.total), L.total * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&a, sc + c, sizeof a, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  s.step = a.step;
+  s.b1p = a.b1p;
+  s.b2p = a.b2p;
+  return s;
+}
+
+void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
+  const size_t W = run.start.size();
+  const Dims& d = run.dims;
+  const DmLayout lay(d);
+  const int64_t P = int64_t(lay.total);
+  const int R = int(run.R), T = int(d.T), E = int(d.de), H = int(d.dh), F = int(d.df),
+            V = int(d.V), NH = int(d.heads);
+  const DmDims dd{R, T, E, H, F, V, NH};
+  const Schedule& sch = run.sch;
+  const bool want_stats = run.opt && run.opt->want_stats;
+  run.stats.assign(W, ChunkStats{});
+
+  // ---- geometry
+  std::vector<uint64_t> Lh(sch.L.begin(), sch.L.end());
+  DBuf<uint64_t> d_start(W), d_L(W);
+  DBuf<int64_t> d_off(W);
+  d_start.upload(run.start.data(), W, st);
+  d_L.upload(Lh.data(), W, st);
+  d_off.upload(sch.offset.data(), W, st);
+  const ChunkGeo geo{d_start.p, d_L.p, d_off.p};
+
+  // ---- model state slots (one per chunk)
+  DBuf<float> w(W * P), g(W * P), m(W * P), v(W * P);
+  DBuf<AdamScalars> sc(W);
+  g.zero(st);
+  {
+    const std::vector<float> seeded = lay.seeded(run.dm_seed);
+    DBuf<float> init(P);
+    init.upload(seeded.data(), P, st);
+    std::vector<AdamScalars> hsc(W);
+    for (size_t c = 0; c < W; ++c) {
+      const DmState* s0 = run.init_state.empty() ? nullptr : run.init_state[c];
+      hsc[c] = AdamScalars{0, 1.0f, 1.0f, 0.0f, 0.0f, {0, 0}};
+      if (s0) {
+        w.upload(s0->w.data(), P, st, c * P);
+        m.upload(s0->m.data(), P, st, c * P);
+        v.upload(s0->v.data(), P, st, c * P);
+        hsc[c].step = s0->step;
+        hsc[c].b1p = s0->b1p;
+        hsc[c].b2p = s0->b2p;
+      } else {
+        CK(cudaMemcpyAsync(w.p + c * P, init.p, P * 4, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemsetAsync(m.p + c * P, 0, P * 4, st));
+        CK(cudaMemsetAsync(v.p + c * P, 0, P * 4, st));
+      }
+    }
+    sc.upload(hsc.data(), W, st);
+    CK(cudaStreamSynchronize(st));
+  }
+
+  // ---- tapes (one per chunk that ever steps)
+  const int64_t s_ctx = int64_t(R) * T, s_x = int64_t(R) * T * E, s_kv = int64_t(R) * T * H,
+                s_rh = int64_t(R) * H, s_w = int64_t(R) * NH * T, s_rf = int64_t(R) * F,
+                s_rv = int64_t(R) * V, s_cum = int64_t(R) * (V + 1), s_re = int64_t(R) * E;
+  uint32_t n_step_chunks = 0;
+  for (size_t c = 0; c < W; ++c) n_step_chunks += sch.M[c] ? 1 : 0;
+  const size_t TW = n_step_chunks ? W : 0;  // tapes indexed by chunk id
+  DBuf<uint32_t> ctx(TW * s_ctx), freq(TW * s_rv), cum(TW * s_cum);
+  DBuf<float> x(TW * s_x), kk(TW * s_kv), vv(TW * s_kv), q(TW * s_rh), wts(TW * s_w),
+      cx(TW * s_rh), ao(TW * s_rh), pre(TW * s_rf), fo(TW * s_rh), lm(TW * s_rv),
+      probs(TW * s_rv), dlm(TW * s_rv), dffn(TW * s_rh), dact(TW * s_rf), datt(TW * s_rh),
+      dctx(TW * s_rh), dq(TW * s_rh), dk(TW * s_kv), dv(TW * s_kv), dx(TW * s_x), dxl(TW * s_re);
+  DBuf<float> lu((run.flags & 1) ? TW * s_rv : 0), lr((run.flags & 2) ? TW * s_rv : 0);
+  int64_t s_bw = 0;
+  DBuf<float> bwork;
+  if (run.flags & 3) {
+    size_t mx = 0;
+    if (run.pub) mx = std::max(mx, bigru_work_floats(run.pub->params(R)));
+    if (run.priv) mx = std::max(mx, bigru_work_floats(run.priv->params(R)));
+    s_bw = int64_t(mx);
+    bwork.alloc(TW * mx);
+  }
+
+  // ---- coder
+  std::vector<uint64_t> pay_off(W), pay_cap(W);
+  uint64_t total_cap = 0;
+  for (size_t c = 0; c < W; ++c) {
+    pay_off[c] = total_cap;
+    pay_cap[c] = run.decode ? run.pay_in_len[c] : 2 * uint64_t(R) * sch.L[c] + 16;
+    total_cap += (pay_cap[c] + 15) & ~uint64_t(15);
+  }
+  DBuf<uint8_t> payload(total_cap + 16);
+  DBuf<uint64_t> d_pay_off(W), d_pay_len(W);
+  d_pay_off.upload(pay_off.data(), W, st);
+  d_pay_len.upload(pay_cap.data(), W, st);
+  if (run.decode)
+    for (size_t c = 0; c < W; ++c) payload.upload(run.pay_in[c], run.pay_in_len[c], st, pay_off[c]);
+  DBuf<CoderState> cstate(W);
+  DBuf<int> err(1);
+  err.zero(st);
+  std::vector<uint64_t> warm(W);
+  for (size_t c = 0; c < W; ++c) warm[c] = std::max<uint64_t>(1, (sch.L[c] * 500 + 9999) / 10000);
+  DBuf<uint64_t> d_warm(W);
+  d_warm.upload(warm.data(), W, st);
+  DBuf<double> warm_loss(W);
+  warm_loss.zero(st);
+
+  // ---- schedule lists
+  DBuf<int> d_act(std::max<size_t>(sch.act.size(), 1));
+  if (!sch.act.empty()) d_act.upload(reinterpret_cast<const int*>(sch.act.data()), sch.act.size(), st);
+  DBuf<int2> d_hand(std::max<size_t>(sch.hand.size() / 2, 1));
+  if (!sch.hand.empty())
+    d_hand.upload(reinterpret_cast<const int2*>(sch.hand.data()), sch.hand.size() / 2, st);
+
+  // snapshot hashes for stats: key (src, steps)
+  std::map<std::pair<int64_t, uint64_t>, uint64_t> snap_hash;
+  auto need_snapshot = [&](int64_t src, uint64_t steps) {
+    return want_stats && !snap_hash.count({src, steps});
+  };
+  auto take_snapshot = [&](int64_t src, uint64_t steps) {
+    DmState s;
+    if (src < 0) {
+      s.w = lay.seeded(run.dm_seed);
+      s.m.assign(lay.total, 0.0f);
+      s.v.assign(lay.total, 0.0f);
+    } else {
+      s = fetch_state(lay, w.p, m.p, v.p, sc.p, src, st);
+    }
+    const Bytes b = snapshot_bytes(lay, s);
+    snap_hash[{src, steps}] = fnv1a64(b);
+  };
+  // which (src, steps) snapshots are needed and when they become available
+  std::map<int64_t, std::vector<std::pair<int64_t, uint64_t>>> snap_at;  // tick -> keys
+  if (want_stats) {
+    for (size_t c = 0; c < W; ++c) {
+      if (!sch.inbound_nonempty[c]) continue;
+      const int64_t sr = sch.src[c];
+      const uint64_t stp = sch.src_steps[c];
+      const int64_t at = sr < 0 ? -1 : sch.offset[size_t(sr)] + int64_t(stp);
+      snap_at[at].push_back({sr, stp});
+    }
+  }
+  auto snapshots_for_tick = [&](int64_t tick) {
+    auto it = snap_at.find(tick);
+    if (it == snap_at.end()) return;
+    for (auto& key : it->second)
+      if (need_snapshot(key.first, key.second)) take_snapshot(key.first, key.second);
+  };
+
+  Event e0, e1, e2;
+  e0.record(st);
+  // ---- warm-up symbols of every chunk (uniform distribution)
+  launch_range_uniform(d_tokens, geo, int(run.t), R, V, payload.p, d_pay_off.p, d_pay_len.p,
+                       cstate.p, int(W), run.decode, st);
+  ++run.launches;
+  e1.record(st);
+  snapshots_for_tick(-1);
+
+  const float inv_hd = 1.0f / std::sqrt(float(H / NH));
+  const int64_t oE = int64_t(lay.off(DmLayout::EMB)), oP = int64_t(lay.off(DmLayout::POS)),
+                oA = int64_t(lay.off(DmLayout::ALPHA));
+  auto W_ = [&](DmLayout::Id i) { return w.p + lay.off(i); };
+  auto G_ = [&](DmLayout::Id i) { return g.p + lay.off(i); };
+
+  for (int64_t tick = 0; tick < sch.ticks; ++tick) {
+    snapshots_for_tick(tick);
+    const uint32_t h0 = sch.hand_ptr[size_t(tick)], h1 = sch.hand_ptr[size_t(tick) + 1];
+    if (h1 > h0) {
+      launch_state_copy(w.p, m.p, v.p, sc.p, P, P, d_hand.p + h0, int(h1 - h0), st);
+      ++run.launches;
+    }
+    const uint32_t a0 = sch.act_ptr[size_t(tick)], a1 = sch.act_ptr[size_t(tick) + 1];
+    const int na = int(a1 - a0);
+    if (na == 0) continue;
+    const int* act = d_act.p + a0;
+    auto gemm = [&](GemmP p, bool at, bool bt) {
+      launch_gemm(p, at, bt, act, na, st);
+      ++run.launches;
+    };
+    // ---------------- forward (AttentionModel::forward, models.cpp:122-136)
+    launch_embed(d_tokens, geo, tick, w.p, P, oE, oP, ctx.p, s_ctx, x.p, s_x, dd, act, na, st);
+    ++run.launches;
+    GemmP gp{};
+    // K, V over all R*T rows, q over the last position (layers.cpp:437-445)
+    gp = GemmP{x.p, s_x, E, W_(DmLayout::KW), P, H, kk.p, s_kv, H, W_(DmLayout::KB), P,
+               nullptr, 0, 0, R * T, H, E, 0, 1, 0};
+    gemm(gp, false, false);
+    gp.B = W_(DmLayout::VW);
+    gp.bias = W_(DmLayout::VB);
+    gp.C = vv.p;
+    gemm(gp, false, false);
+    gp = GemmP{x.p + int64_t(T - 1) * E, s_x, int64_t(T) * E, W_(DmLayout::QW), P, H, q.p, s_rh, H,
+               W_(DmLayout::QB), P, nullptr, 0, 0, R, H, E, 0, 1, 0};
+    gemm(gp, false, false);
+    launch_attn_fwd(q.p, kk.p, vv.p, wts.p, cx.p, s_rh, s_kv, s_w, dd, inv_hd, act, na, st);
+    ++run.launches;
+    gemm(GemmP{cx.p, s_rh, H, W_(DmLayout::OW), P, H, ao.p, s_rh, H, W_(DmLayout::OB), P, nullptr,
+               0, 0, R, H, H, 0, 1, 0},
+         false, false);
+    gemm(GemmP{ao.p, s_rh, H, W_(DmLayout::IW), P, F, pre.p, s_rf, F, W_(DmLayout::IB), P, nullptr,
+               0, 0, R, F, H, 0, 1, 0},
+         false, false);
+    gemm(GemmP{pre.p, s_rf, F, W_(DmLayout::UW), P, H, fo.p, s_rh, H, W_(DmLayout::UB), P, nullptr,
+               0, 0, R, H, F, 0, 1, 1},
+         false, false);
+    gemm(GemmP{fo.p, s_rh, H, W_(DmLayout::HW), P, V, lm.p, s_rv, V, W_(DmLayout::HB), P, nullptr,
+               0, 0, R, V, H, 0, 1, 0},
+         false, false);
+    // ---------------- static predictors
+    if (run.flags & 1) {
+      launch_bigru_predict(run.pub->params(R), ctx.p, s_ctx, bwork.p, s_bw, lu.p, s_rv, act, na, st);
+      run.launches += run.pub->host.layers + 2;
+    }
+    if (run.flags & 2) {
+      launch_bigru_predict(run.priv->params(R), ctx.p, s_ctx, bwork.p, s_bw, lr.p, s_rv, act, na, st);
+      run.launches += run.priv->host.layers + 2;
+    }
+    // ---------------- mix + quantize + code
+    MixP mp{lu.p, lr.p, lm.p, s_rv, probs.p, freq.p, cum.p, s_rv, s_cum, w.p, P, oA, sc.p,
+            int(run.flags), R, V, err.p};
+    launch_mix_quantize(mp, act, na, st);
+    ++run.launches;
+    if (run.opt && run.opt->probe && run.opt->probe_chunk >= 0) {
+      const int64_t pc = run.opt->probe_chunk;
+      const int64_t ms = tick - sch.offset[size_t(pc)];
+      if (sch.M[size_t(pc)] && ms >= 0 && uint64_t(ms) < sch.M[size_t(pc)] &&
+          uint64_t(ms) < run.opt->probe_steps) {
+        std::vector<float>& pr = *run.opt->probe;
+        CK(cudaMemcpyAsync(pr.data() + uint64_t(ms) * s_rv, probs.p + pc * s_rv, s_rv * 4,
+                           cudaMemcpyDeviceToHost, st));
+      }
+    }
+    launch_range_step(d_tokens, geo, tick, int(run.t), R, V, freq.p, cum.p, s_rv, s_cum, payload.p,
+                      d_pay_off.p, d_pay_len.p, cstate.p, act, na, run.decode, st);
+    ++run.launches;
+    // ---------------- backward controller (OnlineTrainer::step, mixer.cpp:57-97)
+    launch_bc_dlm(probs.p, d_tokens, geo, tick, int(run.t), w.p, P, oA, dlm.p, s_rv, R, V, act, na,
+                  st);
+    ++run.launches;
+    AlphaP ap{probs.p, lu.p, lr.p, lm.p, s_rv, d_tokens, geo, tick, int(run.t), w.p, m.p, v.p, P, oA,
+              sc.p, warm_loss.p, d_warm.p, int(run.flags), R, V};
+    launch_alpha_step(ap, act, na, st);
+    ++run.launches;
+    // head, ffn, attention output projection (Linear::backward, layers.cpp:176-183)
+    gemm(GemmP{fo.p, s_rh, H, dlm.p, s_rv, V, G_(DmLayout::HW), P, V, nullptr, 0, nullptr, 0, 0, H,
+               V, R, 1, 2, 0},
+         true, false);
+    gemm(GemmP{dlm.p, s_rv, V, W_(DmLayout::HW), P, V, dffn.p, s_rh, H, nullptr, 0, nullptr, 0, 0,
+               R, H, V, 0, 0, 0},
+         false, true);
+    gemm(GemmP{pre.p, s_rf, F, dffn.p, s_rh, H, G_(DmLayout::UW), P, H, nullptr, 0, nullptr, 0, 0,
+               F, H, R, 1, 2, 1},
+         true, false);
+    gemm(GemmP{dffn.p, s_rh, H, W_(DmLayout::UW), P, H, dact.p, s_rf, F, nullptr, 0, pre.p, s_rf, F,
+               R, F, H, 0, 0, 0},
+         false, true);
+    gemm(GemmP{ao.p, s_rh, H, dact.p, s_rf, F, G_(DmLayout::IW), P, F, nullptr, 0, nullptr, 0, 0, H,
+               F, R, 1, 2, 0},
+         true, false);
+    gemm(GemmP{dact.p, s_rf, F, W_(DmLayout::IW), P, F, datt.p, s_rh, H, nullptr, 0, nullptr, 0, 0,
+               R, H, F, 0, 0, 0},
+         false, true);
+    gemm(GemmP{cx.p, s_rh, H, datt.p, s_rh, H, G_(DmLayout::OW), P, H, nullptr, 0, nullptr, 0, 0, H,
+               H, R, 1, 2, 0},
+         true, false);
+    gemm(GemmP{datt.p, s_rh, H, W_(DmLayout::OW), P, H, dctx.p, s_rh, H, nullptr, 0, nullptr, 0, 0,
+               R, H, H, 0, 0, 0},
+         false, true);
+    launch_attn_bwd(q.p, kk.p, vv.p, wts.p, dctx.p, dq.p, dk.p, dv.p, s_rh, s_kv, s_w, dd, inv_hd,
+                    act, na, st);
+    ++run.launches;
+    // q/k/v projections: weight+bias grads, then dx = dk Wk^T + dv Wv^T, dxl = dq Wq^T
+    gemm(GemmP{x.p, s_x, E, dk.p, s_kv, H, G_(DmLayout::KW), P, H, nullptr, 0, nullptr, 0, 0, E, H,
+               R * T, 1, 2, 0},
+         true, false);
+    gemm(GemmP{x.p, s_x, E, dv.p, s_kv, H, G_(DmLayout::VW), P, H, nullptr, 0, nullptr, 0, 0, E, H,
+               R * T, 1, 2, 0},
+         true, false);
+    gemm(GemmP{x.p + int64_t(T - 1) * E, s_x, int64_t(T) * E, dq.p, s_rh, H, G_(DmLayout::QW), P, H,
+               nullptr, 0, nullptr, 0, 0, E, H, R, 1, 2, 0},
+         true, false);
+    gemm(GemmP{dk.p, s_kv, H, W_(DmLayout::KW), P, H, dx.p, s_x, E, nullptr, 0, nullptr, 0, 0,
+               R * T, E, H, 0, 0, 0},
+         false, true);
+    gemm(GemmP{dv.p, s_kv, H, W_(DmLayout::VW), P, H, dx.p, s_x, E, nullptr, 0, nullptr, 0, 0,
+               R * T, E, H, 0, 2, 0},
+         false, true);
+    gemm(GemmP{dq.p, s_rh, H, W_(DmLayout::QW), P, H, dxl.p, s_re, E, nullptr, 0, nullptr, 0, 0, R,
+               E, H, 0, 0, 0},
+         false, true);
+    launch_embed_bwd(ctx.p, s_ctx, dx.p, s_x, dxl.p, s_re, g.p, P, oE, oP, dd, act, na, st);
+    run.launches += 2;
+    // Adam over every DM parameter (alpha was updated by k_alpha_step)
+    launch_adam(w.p, g.p, m.p, v.p, P, P - 1, sc.p, act, na, st);
+    ++run.launches;
+    check_launch();
+  }
+  snapshots_for_tick(sch.ticks);
+  if (!run.decode) {
+    launch_range_finish(payload.p, d_pay_off.p, cstate.p, int(W), st);
+    ++run.launches;
+  }
+  e2.record(st);
+  check_launch();
+  CK(cudaStreamSynchronize(st));
+  run.warm_ms = Event::ms(e0, e1);
+  run.model_ms = Event::ms(e1, e2);
+
+  int h_err = 0;
+  CK(cudaMemcpy(&h_err, err.p, sizeof h_err, cudaMemcpyDeviceToHost));
+  if (h_err) raise(errc::invalid_distribution, "probabilities do not sum to 1");
+  std::vector<CoderState> hcs(W);
+  CK(cudaMemcpy(hcs.data(), cstate.p, W * sizeof(CoderState), cudaMemcpyDeviceToHost));
+  for (size_t c = 0; c < W; ++c)
+    if (hcs[c].err) raise(errc::stream_exhausted, "codestream truncated");
+  if (!run.decode) {
+    run.payloads.resize(W);
+    for (size_t c = 0; c < W; ++c) {
+      run.payloads[c].resize(hcs[c].pos);
+      if (hcs[c].pos > pay_cap[c]) raise(errc::cuda_error, "payload capacity exceeded");
+      CK(cudaMemcpyAsync(run.payloads[c].data(), payload.p + pay_off[c], hcs[c].pos,
+                         cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+  }
+  // stats (WorkerStats semantics, pipeline.cpp:106-220)
+  std::vector<double> wl(W);
+  CK(cudaMemcpy(wl.data(), warm_loss.p, W * sizeof(double), cudaMemcpyDeviceToHost));
+  for (size_t c = 0; c < W; ++c) {
+    ChunkStats& s = run.stats[c];
+    s.tokens = uint64_t(R) * sch.L[c];
+    s.uniform_coded = uint64_t(R) * std::min<uint64_t>(run.t, sch.L[c]);
+    s.dyn_calls = sch.M[c];
+    s.pub_calls = (run.flags & 1) ? sch.M[c] : 0;
+    s.priv_calls = (run.flags & 2) ? sch.M[c] : 0;
+    const uint64_t counted = std::min<uint64_t>(sch.M[c], warm[c]);
+    if (counted) s.early_loss_bits = wl[c] / double(counted * R) / 0.6931471805599453;
+    if (want_stats) {
+      if (sch.inbound_nonempty[c]) s.snapshot_recv_hash = snap_hash[{sch.src[c], sch.src_steps[c]}];
+      if (sch.emits[c]) s.snapshot_sent_hash = snap_hash[{sch.src[c + 1], sch.src_steps[c + 1]}];
+    }
+  }
+}
+
+}  // namespace
+
+void Config::validate() const {
+  // CompressConfig::validate (pipeline.cpp:16-24)
+  if (!(s >= 1 && s <= k && k <= 8)) raise(errc::config_invalid, "window parameters need 1 <= s <= k <= 8");
+  if (t < 1 || t > 4096) raise(errc::config_invalid, "context length out of range");
+  if (bs < 1 || bs > 1'000'000) raise(errc::config_invalid, "substream count out of range");
+  if (workers < 1 || workers > max_workers) raise(errc::config_invalid, "worker count out of range");
+  if (!(smp_fraction >= 0.0f) || smp_fraction >= 1.0f)
+    raise(errc::config_invalid, "handoff fraction must lie in [0, 1)");
+  Dims::make(uint32_t(1) << (2 * k), t, scale);
+}
+
+namespace {
+
+struct Loaded {
+  DevBiGru pub, priv;
+  bool has_pub = false, has_priv = false;
+  uint64_t pub_fingerprint = 0;
+};
+
+void check_model_dims(const BiGru& m, const Dims& want, const char* role) {
+  if (!m.fits(want))
+    raise(errc::architecture_mismatch, std::string(role) + " model does not fit this configuration");
+}
+
+struct Canon {
+  uint64_t n_codes = 0;
+  std::vector<uint64_t> exc_pos;
+  std::vector<uint8_t> exc_byte;
+  DBuf<uint8_t> codes;  // empty when the input is pure ACGT (tokenize from ASCII)
+};
+
+// canonicalize (alphabet.cpp:22-35) on the device
+void canonicalize_device(const uint8_t* d_raw, uint64_t n, Canon& out, cudaStream_t st) {
+  const uint32_t nb = canon_blocks(n);
+  if (n == 0) return;
+  DBuf<uint32_t> counts(nb);
+  launch_canon_count(d_raw, n, counts.p, st);
+  std::vector<uint32_t> hc(nb);
+  CK(cudaMemcpyAsync(hc.data(), counts.p, nb * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<uint64_t> offs(nb + 1, 0);
+  for (uint32_t b = 0; b < nb; ++b) offs[b + 1] = offs[b] + hc[b];
+  const uint64_t ne = offs[nb];
+  out.n_codes = n - ne;
+  if (ne == 0) return;
+  DBuf<uint64_t> d_offs(nb + 1), d_epos(ne);
+  DBuf<uint8_t> d_ebyte(ne);
+  d_offs.upload(offs.data(), nb + 1, st);
+  out.codes.alloc(std::max<uint64_t>(out.n_codes, 1) + 16);
+  launch_canon_scatter(d_raw, n, d_offs.p, out.codes.p, d_epos.p, d_ebyte.p, st);
+  out.exc_pos.resize(ne);
+  out.exc_byte.resize(ne);
+  CK(cudaMemcpyAsync(out.exc_pos.data(), d_epos.p, ne * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out.exc_byte.data(), d_ebyte.p, ne, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+Bytes compress_impl(const uint8_t* h_raw, const uint8_t* d_raw_in, size_t n, const Config& cfg,
+                    const CallOptions& opt) {
+  cfg.validate();
+  CK(cudaSetDevice(cfg.device));
+  Stream stream(cfg.device);
+  cudaStream_t st = stream.s;
+  Event t0, t1, t2, t3;
+  t0.record(st);
+  Rng master(cfg.seed);
+  const uint64_t dm_seed = master.next_u64();
+  const uint64_t sprm_seed = master.next_u64();
+  const uint32_t V = uint32_t(1) << (2 * cfg.k);
+  const Dims dims = Dims::make(V, cfg.t, cfg.scale);
+
+  // input to HBM
+  DBuf<uint8_t> d_raw_own;
+  const uint8_t* d_raw = d_raw_in;
+  uint64_t h2d = 0;
+  if (!d_raw) {
+    d_raw_own.alloc(n + 16);
+    d_raw_own.upload(h_raw, n, st);
+    d_raw = d_raw_own.p;
+    h2d = n;
+  }
+  t1.record(st);
+  Canon canon;
+  canonicalize_device(d_raw, n, canon, st);
+  const uint64_t nc = canon.n_codes == 0 && canon.exc_pos.empty() ? n : canon.n_codes;
+  const uint64_t m = token_count(nc, cfg.s, cfg.k);
+  DBuf<uint32_t> d_tok(m + 8);
+  if (canon.exc_pos.empty())
+    launch_skmer_encode_ascii(d_raw, nc, cfg.s, cfg.k, d_tok.p, m, st);
+  else
+    launch_skmer_encode_codes(canon.codes.p, nc, cfg.s, cfg.k, d_tok.p, m, st);
+  check_launch();
+  // residual: bases after the last full window (skmer.cpp:55-59)
+  const uint64_t covered = m ? (m - 1) * cfg.s + cfg.k : 0;
+  std::vector<uint8_t> residual(nc - covered);
+  if (!residual.empty()) {
+    if (canon.exc_pos.empty()) {
+      CK(cudaMemcpyAsync(residual.data(), d_raw + covered, residual.size(), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (uint8_t& b : residual) b = uint8_t(((b >> 1) ^ (b >> 2)) & 3);
+    } else {
+      CK(cudaMemcpyAsync(residual.data(), canon.codes.p + covered, residual.size(),
+                         cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+  }
+  t2.record(st);
+
+  // selector + static models (pipeline.cpp:313-334)
+  uint8_t flags = n <= cfg.selector_threshold ? 5 : 6;
+  Loaded models;
+  if (!cfg.pub_model_path.empty()) {
+    const Bytes file = read_file(cfg.pub_model_path);
+    BiGru pub = BiGru::deserialize(file.data(), file.size());
+    check_model_dims(pub, dims, "public");
+    models.pub_fingerprint = fnv1a64(file);
+    models.pub.upload(std::move(pub), st);
+    models.has_pub = true;
+  }
+  if ((flags & 1) && !models.has_pub) flags = 4;
+  if ((flags & 2) && m < uint64_t(cfg.t) + 1) flags = 4;
+  if (flags & 2)
+    raise(errc::config_invalid,
+          "private-model pre-pass (pretrain_private) is not implemented on the B200 path yet");
+
+  const uint16_t myriad = uint16_t(std::lround(double(cfg.smp_fraction) * 10000.0));
+  const Plan plan = plan_chunks(m, cfg.workers, cfg.bs, cfg.t, myriad);
+  const size_t W = plan.len.size();
+  ChunkRun run;
+  run.dims = dims;
+  run.R = plan.bs;
+  run.t = cfg.t;
+  run.flags = flags;
+  run.decode = false;
+  run.pub = models.has_pub ? &models.pub : nullptr;
+  run.dm_seed = dm_seed;
+  run.start = plan.start;
+  run.sch = make_schedule(plan, myriad > 0);
+  run.opt = &opt;
+  if (W) run_chunks(run, d_tok.p, st);
+
+  // trailers: leftover tokens of each chunk (len - bs*L)
+  Container c;
+  c.flags = flags;
+  c.s = uint8_t(cfg.s);
+  c.k = uint8_t(cfg.k);
+  c.t = uint16_t(cfg.t);
+  c.bs = plan.bs;
+  c.smp_per_myriad = myriad;
+  c.dm_seed = dm_seed;
+  c.sprm_seed = (flags & 2) ? sprm_seed : uint64_t(cfg.scale);
+  c.pub_fingerprint = (flags & 1) ? models.pub_fingerprint : 0;
+  c.original_len = n;
+  std::vector<Bytes> trailers(W);
+  for (size_t i = 0; i < W; ++i) {
+    const uint64_t used = uint64_t(plan.bs) * run.sch.L[i];
+    const uint64_t left = plan.len[i] - used;
+    std::vector<uint32_t> lt(left);
+    if (left)
+      CK(cudaMemcpyAsync(lt.data(), d_tok.p + plan.start[i] + used, left * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    trailers[i] = pack_tokens(lt.data(), left, cfg.k);
+    ChunkEntry e;
+    e.token_start = plan.start[i];
+    e.token_len = plan.len[i];
+    e.payload_len = run.payloads[i].size();
+    e.trailer_len = uint32_t(trailers[i].size());
+    c.chunks.push_back(e);
+    c.payload_ptr.push_back(run.payloads[i].data());
+    c.trailer_ptr.push_back(trailers[i].data());
+  }
+  c.exc_pos = std::move(canon.exc_pos);
+  c.exc_byte = std::move(canon.exc_byte);
+  c.residual = std::move(residual);
+  Bytes out = write_container(c);
+  t3.record(st);
+  CK(cudaStreamSynchronize(st));
+  if (opt.stats) *opt.stats = run.stats;
+  if (opt.timing) {
+    Timing& tm = *opt.timing;
+    tm.total_ms = Event::ms(t0, t3);
+    tm.h2d_ms = Event::ms(t0, t1);
+    tm.tokenize_ms = Event::ms(t1, t2);
+    tm.warmup_ms = run.warm_ms;
+    tm.model_ms = run.model_ms;
+    tm.ticks = uint64_t(run.sch.ticks);
+    tm.kernel_launches = run.launches + 3;
+    tm.chunks = W;
+    tm.h2d_bytes = h2d;
+    tm.d2h_bytes = out.size();
+  }
+  return out;
+}
+
+struct DecodeResult {
+  DBuf<uint8_t> out;
+  uint64_t len = 0;
+};
+
+void decompress_impl(const uint8_t* blob, size_t n, const std::string& pub_path, int device,
+                     const CallOptions& opt, DecodeResult& res, cudaStream_t st) {
+  Event t0, t1, t2, t3;
+  t0.record(st);
+  const Container c = read_container(blob, n);
+  const uint8_t flags = c.flags;
+  if (!(flags & 4)) raise(errc::table_inconsistent, "dynamic model flag must be set");
+  if (!(c.s >= 1 && c.s <= c.k && c.k <= 8) || c.t < 1 || c.bs < 1)
+    raise(errc::table_inconsistent, "coding parameters");
+  Loaded models;
+  uint32_t scale = 0;
+  BiGru priv;
+  if (flags & 2) {
+    priv = BiGru::deserialize(c.private_model.data(), c.private_model.size());
+    const int64_t se = priv.d.se;
+    if (se < 1 || 16 % se != 0) raise(errc::architecture_mismatch, "private model width");
+    scale = uint32_t(16 / se);
+  } else {
+    if (c.sprm_seed < 1 || c.sprm_seed > 16) raise(errc::table_inconsistent, "model width divisor");
+    scale = uint32_t(c.sprm_seed);
+  }
+  const Dims dims = Dims::make(uint32_t(1) << (2 * c.k), c.t, scale);
+  if (flags & 2) {
+    check_model_dims(priv, dims, "private");
+    models.priv.upload(std::move(priv), st);
+    models.has_priv = true;
+  }
+  if (flags & 1) {
+    if (pub_path.empty()) raise(errc::spum_missing, "container requires the public model file");
+    const Bytes file = read_file(pub_path);
+    if (fnv1a64(file) != c.pub_fingerprint)
+      raise(errc::checksum_mismatch, "public model file does not match the container");
+    BiGru pub = BiGru::deserialize(file.data(), file.size());
+    check_model_dims(pub, dims, "public");
+    models.pub.upload(std::move(pub), st);
+    models.has_pub = true;
+  }
+  uint64_t total = 0;
+  for (const ChunkEntry& e : c.chunks) total += e.token_len;
+  const uint64_t ne = c.exc_pos.size();
+  const uint64_t payload_bases = c.original_len - std::min<uint64_t>(c.original_len, ne);
+  if (token_count(payload_bases, c.s, c.k) != total)
+    raise(errc::corrupt_stream, "token count does not match the original length");
+
+  DBuf<uint32_t> d_tok(total + 8);
+  Plan plan;
+  plan.bs = c.bs;
+  plan.t = c.t;
+  plan.myriad = c.smp_per_myriad;
+  for (const ChunkEntry& e : c.chunks) {
+    plan.start.push_back(e.token_start);
+    plan.len.push_back(e.token_len);
+  }
+  const size_t W = c.chunks.size();
+  ChunkRun run;
+  run.dims = dims;
+  run.R = c.bs;
+  run.t = c.t;
+  run.flags = flags;
+  run.decode = true;
+  run.pub = models.has_pub ? &models.pub : nullptr;
+  run.priv = models.has_priv ? &models.priv : nullptr;
+  run.dm_seed = c.dm_seed;
+  run.start = plan.start;
+  run.sch = make_schedule(plan, c.smp_per_myriad > 0);
+  run.opt = &opt;
+  for (size_t i = 0; i < W; ++i) {
+    run.pay_in.push_back(c.payload_ptr[i]);
+    run.pay_in_len.push_back(c.chunks[i].payload_len);
+  }
+  t1.record(st);
+  if (W) run_chunks(run, d_tok.p, st);
+  // trailers (pipeline.cpp:431-436)
+  for (size_t i = 0; i < W; ++i) {
+    const ChunkEntry& e = c.chunks[i];
+    const uint64_t used = uint64_t(c.bs) * run.sch.L[i];
+    const uint64_t left = e.token_len - used;
+    if ((uint64_t(e.trailer_len) * 8) / (2 * c.k) < left) raise(errc::corrupt_stream, "trailer too short");
+    std::vector<uint32_t> lt(left);
+    unpack_tokens(c.trailer_ptr[i], e.trailer_len, c.k, lt.data(), left);
+    if (left)
+      CK(cudaMemcpyAsync(d_tok.p + e.token_start + used, lt.data(), left * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  t2.record(st);
+  // decode tokens + restore on the device
+  const uint64_t covered = total ? (total - 1) * c.s + c.k : 0;
+  if (covered + c.residual.size() != payload_bases) raise(errc::corrupt_stream, "decoded base count");
+  DBuf<uint8_t> d_res(c.residual.size() + 1);
+  d_res.upload(c.residual.data(), c.residual.size(), st);
+  DBuf<uint64_t> d_epos(ne + 1);
+  DBuf<uint8_t> d_ebyte(ne + 1);
+  d_epos.upload(c.exc_pos.data(), ne, st);
+  d_ebyte.upload(c.exc_byte.data(), ne, st);
+  if (ne) {
+    if (c.exc_pos.back() >= c.original_len)
+      raise(errc::length_mismatch, "exception position beyond original length");
+    if (payload_bases + ne != c.original_len)
+      raise(errc::length_mismatch, "payload + exceptions do not cover the original length");
+  }
+  DBuf<int> err(1);
+  err.zero(st);
+  res.out.alloc(c.original_len + 16);
+  res.len = c.original_len;
+  launch_detokenize_restore(d_tok.p, total, c.s, c.k, d_res.p, c.residual.size(), d_epos.p,
+                            d_ebyte.p, ne, res.out.p, c.original_len, err.p, st);
+  check_launch();
+  int h_err = 0;
+  CK(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
+  t3.record(st);
+  CK(cudaStreamSynchronize(st));
+  if (h_err == 1) raise(errc::token_out_of_range, "token exceeds 4^k");
+  if (h_err) raise(errc::corrupt_stream, "decoded base count");
+  if (opt.stats) *opt.stats = run.stats;
+  if (opt.timing) {
+    Timing& tm = *opt.timing;
+    tm.total_ms = Event::ms(t0, t3);
+    tm.h2d_ms = Event::ms(t0, t1);
+    tm.warmup_ms = run.warm_ms;
+    tm.model_ms = run.model_ms;
+    tm.tokenize_ms = Event::ms(t2, t3);
+    tm.ticks = uint64_t(run.sch.ticks);
+    tm.kernel_launches = run.launches + 1;
+    tm.chunks = W;
+    tm.h2d_bytes = n;
+  }
+}
+
+}  // namespace
+
+Bytes compress(const uint8_t* raw, size_t n, const Config& cfg, const CallOptions& opt) {
+  return compress_impl(raw, nullptr, n, cfg, opt);
+}
+
+Bytes compress_device(const uint8_t* d_raw, size_t n, const Config& cfg, const CallOptions& opt) {
+  return compress_impl(nullptr, d_raw, n, cfg, opt);
+}
+
+Bytes decompress(const uint8_t* blob, size_t n, const std::string& pub_model_path, uint32_t workers,
+                 int device, const CallOptions& opt) {
+  (void)workers;  // scheduling only (pipeline.cpp:379-441); the device runs every chunk
+  CK(cudaSetDevice(device));
+  Stream stream(device);
+  DecodeResult res;
+  decompress_impl(blob, n, pub_model_path, device, opt, res, stream.s);
+  Bytes out(res.len);
+  if (res.len) CK(cudaMemcpy(out.data(), res.out.p, res.len, cudaMemcpyDeviceToHost));
+  if (opt.timing) opt.timing->d2h_bytes = res.len;
+  return out;
+}
+
+uint8_t* decompress_to_device(const uint8_t* blob, size_t n, const std::string& pub_model_path,
+                              int device, size_t* out_len, const CallOptions& opt) {
+  CK(cudaSetDevice(device));
+  Stream stream(device);
+  DecodeResult res;
+  decompress_impl(blob, n, pub_model_path, device, opt, res, stream.s);
+  *out_len = res.len;
+  uint8_t* p = res.out.p;
+  res.out.p = nullptr;  // ownership to caller
+  res.out.n = 0;
+  return p;
+}
+
+std::vector<Bytes> encode_chunks(const std::vector<ChunkJob>& jobs, uint8_t flags,
+                                 const std::string& pub_model_path, uint32_t k, uint32_t t,
+                                 uint32_t bs, uint32_t scale, uint64_t dm_seed, int device,
+                                 const CallOptions& opt) {
+  CK(cudaSetDevice(device));
+  Stream stream(device);
+  cudaStream_t st = stream.s;
+  const Dims dims = Dims::make(uint32_t(1) << (2 * k), t, scale);
+  const DmLayout lay(dims);
+  if (!(flags & 4)) raise(errc::config_invalid, "dynamic model flag must be set");
+  if (flags & 2) raise(errc::config_invalid, "private model not supported by encode_chunks");
+  Loaded models;
+  if (flags & 1) {
+    const Bytes file = read_file(pub_model_path);
+    BiGru pub = BiGru::deserialize(file.data(), file.size());
+    check_model_dims(pub, dims, "public");
+    models.pub.upload(std::move(pub), st);
+    models.has_pub = true;
+  }
+  const size_t W = jobs.size();
+  ChunkRun run;
+  run.dims = dims;
+  run.R = bs;
+  run.t = t;
+  run.flags = flags;
+  run.pub = models.has_pub ? &models.pub : nullptr;
+  run.dm_seed = dm_seed;
+  Plan plan;
+  plan.bs = bs;
+  plan.t = t;
+  plan.myriad = 0;
+  uint64_t total = 0;
+  for (const ChunkJob& j : jobs) {
+    plan.start.push_back(total);
+    plan.len.push_back(j.n_tokens);
+    total += j.n_tokens;
+  }
+  run.start = plan.start;
+  run.sch = make_schedule(plan, false);
+  std::vector<DmState> states(W);
+  run.init_state.assign(W, nullptr);
+  for (size_t i = 0; i < W; ++i)
+    if (!jobs[i].inbound.empty()) {
+      states[i] = parse_snapshot(lay, jobs[i].inbound.data(), jobs[i].inbound.size());
+      run.init_state[i] = &states[i];
+    }
+  run.opt = &opt;
+  DBuf<uint32_t> d_tok(total + 8);
+  for (size_t i = 0; i < W; ++i) d_tok.upload(jobs[i].tokens, jobs[i].n_tokens, st, plan.start[i]);
+  if (W) run_chunks(run, d_tok.p, st);
+  if (opt.stats) *opt.stats = run.stats;
+  return run.payloads;
+}
+
+std::vector<uint32_t> skmer_encode_codes(const uint8_t* codes, uint64_t n, uint32_t s, uint32_t k,
+                                         int device) {
+  if (!(s >= 1 && s <= k && k <= 8)) raise(errc::config_invalid, "invalid (s,k) parameters");
+  CK(cudaSetDevice(device));
+  Stream stream(device);
+  const uint64_t m = token_count(n, s, k);
+  DBuf<uint8_t> d_in(n + 16);
+  d_in.upload(codes, n, stream.s);
+  DBuf<uint32_t> d_tok(m + 8);
+  launch_skmer_encode_codes(d_in.p, n, s, k, d_tok.p, m, stream.s);
+  check_launch();
+  std::vector<uint32_t> out(m);
+  if (m) CK(cudaMemcpyAsync(out.data(), d_tok.p, m * 4, cudaMemcpyDeviceToHost, stream.s));
+  CK(cudaStreamSynchronize(stream.s));
+  return out;
+}
+
+void skmer_encode_packed_device(const uint8_t* d_packed, uint64_t n_bases, uint32_t s, uint32_t k,
+                                uint32_t* d_tokens, void* stream) {
+  if (!(s >= 1 && s <= k && k <= 8)) raise(errc::config_invalid, "invalid (s,k) parameters");
+  const uint64_t m = token_count(n_bases, s, k);
+  launch_skmer_encode_packed(d_packed, n_bases, s, k, d_tokens, m, static_cast<cudaStream_t>(stream));
+  check_launch();
+}
+
+}  // namespace pmklc_b200

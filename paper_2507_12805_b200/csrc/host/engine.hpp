@@ -1,0 +1,80 @@
+// B200 compress/decompress engine: the drop-in for pmklc::compress /
+// pmklc::decompress (core/include/pmklc/pipeline.hpp:12-76). Host C++ keeps
+// the reference's control flow (validate, seeds, selector, fallbacks, plan,
+// container); every per-token stage runs as sm_100a kernels.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "models.hpp"
+
+namespace pmklc_b200 {
+
+// CompressConfig (pipeline.hpp:12-25) plus device selection.
+struct Config {
+  uint32_t s = 3, k = 3, t = 32, bs = 320, workers = 1, scale = 4;
+  uint64_t selector_threshold = 500'000'000ull, seed = 42;
+  float smp_fraction = 0.05f;
+  std::string pub_model_path;
+  int device = 0;
+  uint32_t max_workers = 256;  // validate()'s cap; the C ABI may raise it
+  void validate() const;
+};
+
+// WorkerStats (pipeline.hpp:27-35)
+struct ChunkStats {
+  uint64_t tokens = 0, uniform_coded = 0, pub_calls = 0, priv_calls = 0, dyn_calls = 0;
+  uint64_t snapshot_recv_hash = 0, snapshot_sent_hash = 0;
+  double early_loss_bits = 0;
+};
+
+// Device-side timing of the last call (CUDA events on the engine stream).
+struct Timing {
+  double total_ms = 0, h2d_ms = 0, tokenize_ms = 0, warmup_ms = 0, model_ms = 0, d2h_ms = 0;
+  uint64_t ticks = 0, kernel_launches = 0, chunks = 0;
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;
+};
+
+struct CallOptions {
+  bool want_stats = false;
+  std::vector<ChunkStats>* stats = nullptr;
+  Timing* timing = nullptr;
+  // debug probe: mixed probabilities of chunk `probe_chunk` for its first
+  // `probe_steps` model steps, [steps, R, V] floats
+  int64_t probe_chunk = -1;
+  uint64_t probe_steps = 0;
+  std::vector<float>* probe = nullptr;
+};
+
+// host buffers in / out
+Bytes compress(const uint8_t* raw, size_t n, const Config& cfg, const CallOptions& opt = {});
+Bytes decompress(const uint8_t* blob, size_t n, const std::string& pub_model_path, uint32_t workers,
+                 int device, const CallOptions& opt = {});
+// raw already resident in device memory (bench "value" path)
+Bytes compress_device(const uint8_t* d_raw, size_t n, const Config& cfg, const CallOptions& opt = {});
+// decompress to a device buffer of original_len bytes (caller frees with cudaFree)
+uint8_t* decompress_to_device(const uint8_t* blob, size_t n, const std::string& pub_model_path,
+                              int device, size_t* out_len, const CallOptions& opt = {});
+
+// encode_chunk_standalone (pipeline.cpp:298-301), batched: every chunk is
+// coded independently from its own inbound snapshot (empty = seeded init).
+struct ChunkJob {
+  const uint32_t* tokens = nullptr;  // host, bs*L tokens used
+  uint64_t n_tokens = 0;
+  Bytes inbound;
+};
+std::vector<Bytes> encode_chunks(const std::vector<ChunkJob>& jobs, uint8_t flags,
+                                 const std::string& pub_model_path, uint32_t k, uint32_t t,
+                                 uint32_t bs, uint32_t scale, uint64_t dm_seed, int device,
+                                 const CallOptions& opt = {});
+
+// Stand-alone tokenizer on host buffers of base codes 0..3 (for parity tests)
+std::vector<uint32_t> skmer_encode_codes(const uint8_t* codes, uint64_t n, uint32_t s, uint32_t k,
+                                         int device);
+// Tokenizer on device buffers: packed 2-bit bases -> u32 tokens (bench config 2)
+void skmer_encode_packed_device(const uint8_t* d_packed, uint64_t n_bases, uint32_t s, uint32_t k,
+                                uint32_t* d_tokens, void* stream);
+
+}  // namespace pmklc_b200

@@ -1,0 +1,97 @@
+#include "plan.hpp"
+
+#include <algorithm>
+
+namespace pmklc_b200 {
+
+Plan plan_chunks(uint64_t m, uint32_t workers, uint32_t bs, uint32_t t, uint16_t myriad) {
+  Plan p;
+  p.t = t;
+  p.myriad = myriad;
+  if (m == 0) {
+    p.bs = 1;
+    return p;
+  }
+  const uint64_t per_worker = uint64_t(bs) * (uint64_t(t) + 1);
+  const uint64_t w = std::min<uint64_t>(workers, std::max<uint64_t>(1, m / per_worker));
+  const uint64_t base = m / w, rem = m % w;
+  uint64_t start = 0;
+  for (uint64_t i = 0; i < w; ++i) {
+    const uint64_t len = base + (i < rem ? 1 : 0);
+    p.start.push_back(start);
+    p.len.push_back(len);
+    start += len;
+  }
+  p.bs = uint32_t(std::min<uint64_t>(bs, std::max<uint64_t>(1, base / (uint64_t(t) + 1))));
+  return p;
+}
+
+Schedule make_schedule(const Plan& p, bool smp_on) {
+  Schedule s;
+  const size_t W = p.len.size();
+  s.L.resize(W);
+  s.M.resize(W);
+  s.offset.resize(W);
+  s.src.resize(W);
+  s.src_steps.resize(W);
+  s.inbound_nonempty.resize(W);
+  s.emits.resize(W);
+  for (size_t c = 0; c < W; ++c) {
+    s.L[c] = p.len[c] / p.bs;
+    s.M[c] = s.L[c] > p.t ? s.L[c] - p.t : 0;
+  }
+  for (size_t c = 0; c < W; ++c) {
+    // reference: chunk c emits its snapshot iff SMP is on, it is not the last
+    // chunk, and it reaches step snap (steps_done counts warm-up steps)
+    const uint64_t snap = smp_on ? p.snapshot_step(c) : 0;
+    s.emits[c] = smp_on && c + 1 < W && snap <= s.L[c];
+    if (c == 0 || !smp_on) {
+      s.src[c] = -1;
+      s.src_steps[c] = 0;
+      s.offset[c] = 0;
+      s.inbound_nonempty[c] = 0;
+      continue;
+    }
+    const uint64_t psnap = p.snapshot_step(c - 1);
+    s.inbound_nonempty[c] = s.emits[c - 1] || s.inbound_nonempty[c - 1];
+    if (s.emits[c - 1] && psnap > p.t) {
+      // snapshot after psnap - t model steps of chunk c-1
+      s.src[c] = int64_t(c - 1);
+      s.src_steps[c] = psnap - p.t;
+      s.offset[c] = s.offset[c - 1] + int64_t(psnap - p.t);
+    } else {
+      // snapshot taken during warm-up (== c-1's inbound) or never taken
+      // (inbound forwarded unchanged): same state as chunk c-1 started from
+      s.src[c] = s.src[c - 1];
+      s.src_steps[c] = s.src_steps[c - 1];
+      s.offset[c] = s.offset[c - 1];
+    }
+  }
+  int64_t ticks = 0;
+  for (size_t c = 0; c < W; ++c)
+    if (s.M[c]) ticks = std::max<int64_t>(ticks, s.offset[c] + int64_t(s.M[c]));
+  s.ticks = ticks;
+  // CSR lists
+  std::vector<std::vector<uint32_t>> act(static_cast<size_t>(ticks));
+  std::vector<std::vector<int32_t>> hand(static_cast<size_t>(ticks));
+  for (size_t c = 0; c < W; ++c) {
+    if (!s.M[c]) continue;
+    for (uint64_t q = 0; q < s.M[c]; ++q) act[size_t(s.offset[c] + int64_t(q))].push_back(uint32_t(c));
+    if (s.src[c] >= 0) {
+      hand[size_t(s.offset[c])].push_back(int32_t(s.src[c]));
+      hand[size_t(s.offset[c])].push_back(int32_t(c));
+    }
+  }
+  s.act_ptr.push_back(0);
+  s.hand_ptr.push_back(0);
+  for (int64_t t = 0; t < ticks; ++t) {
+    s.act.insert(s.act.end(), act[size_t(t)].begin(), act[size_t(t)].end());
+    s.act_ptr.push_back(uint32_t(s.act.size()));
+    s.hand.insert(s.hand.end(), hand[size_t(t)].begin(), hand[size_t(t)].end());
+    s.hand_ptr.push_back(uint32_t(s.hand.size() / 2));
+    s.max_active = std::max<uint32_t>(s.max_active, uint32_t(act[size_t(t)].size()));
+  }
+  return s;
+}
+
+}  // namespace pmklc_b200

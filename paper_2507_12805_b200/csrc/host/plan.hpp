@@ -1,0 +1,46 @@
+// Chunk planning (PMKLC-M data-block partitioning) and the tick schedule that
+// realises Step-wise Model Passing on the device.
+//
+// plan_chunks / snapshot_step restate pipeline.cpp:26-52 exactly. The
+// schedule turns the reference's thread-per-chunk promise chain
+// (run_chunks, pipeline.cpp:253-294) into a deterministic global clock: at
+// tick T every chunk whose model phase covers T performs one coded batch step,
+// and a chunk's inbound state is copied from its source chunk at the tick its
+// source reaches the snapshot step. Warm-up positions (j < t) never touch the
+// model, so they are coded for all chunks before tick 0.
+#pragma once
+#include <cstdint>
+#include <vector>
+
+namespace pmklc_b200 {
+
+struct Plan {
+  std::vector<uint64_t> start, len;
+  uint32_t bs = 1, t = 0;
+  uint16_t myriad = 0;
+  uint64_t snapshot_step(size_t i) const {
+    const uint64_t steps = len[i] / bs;
+    const uint64_t s = (uint64_t(myriad) * steps + 9999) / 10000;
+    return s ? s : 1;
+  }
+};
+
+Plan plan_chunks(uint64_t m, uint32_t workers, uint32_t bs, uint32_t t, uint16_t myriad);
+
+struct Schedule {
+  std::vector<uint64_t> L, M;         // batch steps, model steps per chunk
+  std::vector<int64_t> offset;        // tick of the chunk's first model step
+  std::vector<int64_t> src;           // inbound state source chunk, -1 = seeded init
+  std::vector<uint64_t> src_steps;    // model steps the source had completed
+  std::vector<uint8_t> inbound_nonempty, emits;  // reference stats semantics
+  int64_t ticks = 0;
+  std::vector<uint32_t> act_ptr, act;        // CSR: chunks stepping at each tick
+  std::vector<uint32_t> hand_ptr;            // CSR into hand (pairs src,dst)
+  std::vector<int32_t> hand;                 // flattened (src, dst) pairs
+  uint32_t max_active = 0;
+};
+
+// smp_on: myriad > 0 (the container's smp_per_myriad field)
+Schedule make_schedule(const Plan& p, bool smp_on);
+
+}  // namespace pmklc_b200

@@ -1,0 +1,453 @@
+// Mixer + quantizer + range coder + backward-controller scalars on sm_100a.
+//
+//  * k_mix_quantize: one warp per coded row. Eq. 1 mix (mixer.cpp:14-25),
+//    det_softmax with the reference's sequential sum, then the largest-remainder
+//    quantizer (coder.cpp:28-88) in closed form: the reference's stable sorts
+//    become per-element ranks under the same total order (remainder, index), and
+//    its surplus sweep loop becomes "P full passes + a partial pass", both exact.
+//  * range coder (coder.cpp:101-166): 64-bit state, one thread per chunk; the
+//    decoder replaces the 64-bit integer division with a double estimate plus an
+//    exact integer correction.
+//  * k_alpha_step: the single sequential d(alpha) accumulator (mixer.cpp:64-84)
+//    and alpha's Adam update, kept off the main stream's critical path.
+#include <cstdint>
+
+#include "detmath.cuh"
+#include "kernels.hpp"
+
+namespace pmklc_b200 {
+
+namespace {
+
+constexpr uint32_t kTotal = 65536u;
+constexpr uint64_t kRenorm = 1ull << 56;
+
+__device__ __forceinline__ double rem_of(float p, uint32_t& f) {
+  const double v = double(p) * double(kTotal);
+  const double fl = floor(v);
+  f = uint32_t(fl > 1.0 ? fl : 1.0);
+  return v - double(f);
+}
+
+__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t x) {
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+__global__ void k_mix_quantize(MixP p, const int* __restrict__ active) {
+  const int c = active[blockIdx.y];
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // Adam::step scalar prologue (adam.cpp:23-27)
+    AdamScalars s = p.sc[c];
+    s.step += 1;
+    s.b1p = fmul(s.b1p, 0.9f);
+    s.b2p = fmul(s.b2p, 0.999f);
+    s.bc1 = fsub(1.0f, s.b1p);
+    s.bc2 = fsub(1.0f, s.b2p);
+    p.sc[c] = s;
+  }
+  if (row >= p.R) return;
+  const int V = p.V;
+  const int64_t lo = c * p.cs_l + int64_t(row) * V;
+  const float* lu = (p.flags & 1) ? p.lu + lo : nullptr;
+  const float* lr = (p.flags & 2) ? p.lr + lo : nullptr;
+  const float* lm = p.lm + lo;
+  float* pr = p.probs + c * p.cs_p + int64_t(row) * V;
+  uint32_t* fq = p.freq + c * p.cs_p + int64_t(row) * V;
+  uint32_t* cm = p.cum + c * p.cs_c + int64_t(row) * (V + 1);
+
+  const float alpha = det_sigmoid(p.params[c * p.p_cs + p.off_alpha]);
+  const float s0 = (p.flags & 1) ? 1.0f : 0.0f, s1 = (p.flags & 2) ? 1.0f : 0.0f;
+  const float s2 = (p.flags & 4) ? 1.0f : 0.0f;
+  const float wdyn = fmul(fsub(1.0f, alpha), s2);
+  // z = alpha*stat + ((1-alpha)*s2)*lm
+  float mx = -__int_as_float(0x7f800000);
+  for (int i = lane; i < V; i += 32) {
+    const float stat = fadd(fmul(s0, lu ? lu[i] : 0.0f), fmul(s1, lr ? lr[i] : 0.0f));
+    const float z = fadd(fmul(alpha, stat), fmul(wdyn, lm[i]));
+    pr[i] = z;
+    mx = fmaxf(mx, z);
+  }
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.0f;
+  for (int i0 = 0; i0 < V; i0 += 32) {
+    const int i = i0 + lane;
+    float e = 0.0f;
+    if (i < V) {
+      e = det_exp(fsub(pr[i], mx));
+      pr[i] = e;
+    }
+    const int cnt = min(32, V - i0);
+    for (int l = 0; l < cnt; ++l) sum = fadd(sum, __shfl_sync(0xffffffffu, e, l));
+  }
+  const float inv = fdiv(1.0f, sum);
+  // probabilities, positivity, double sum in reference order (coder.cpp:31-38)
+  double dsum = 0.0;
+  bool bad = false;
+  uint32_t assigned = 0;
+  for (int i0 = 0; i0 < V; i0 += 32) {
+    const int i = i0 + lane;
+    float pv = 0.0f;
+    if (i < V) {
+      pv = fmul(pr[i], inv);
+      pr[i] = pv;
+      if (!(pv > 0.0f)) bad = true;
+      uint32_t f;
+      rem_of(pv, f);
+      fq[i] = f;
+      assigned += f;
+    }
+    const int cnt = min(32, V - i0);
+    for (int l = 0; l < cnt; ++l) dsum = dsum + double(__shfl_sync(0xffffffffu, pv, l));
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if (bad || fabs(dsum - 1.0) > 1e-5) {
+    if (lane == 0) atomicExch(p.err, 1);  // InvalidDistribution
+    return;
+  }
+  assigned = warp_sum_u32(assigned);
+  const int64_t deficit = int64_t(kTotal) - int64_t(assigned);
+  __syncwarp();
+  if (deficit > 0) {
+    // stable_sort by (rem desc, idx asc), then +1 cyclically (coder.cpp:57-66)
+    const uint32_t full = uint32_t(deficit / V), part = uint32_t(deficit % V);
+    for (int i = lane; i < V; i += 32) {
+      uint32_t fi;
+      const double ri = rem_of(pr[i], fi);
+      uint32_t rank = 0;
+      for (int j = 0; j < V; ++j) {
+        uint32_t fj;
+        const double rj = rem_of(pr[j], fj);
+        rank += (rj > ri || (rj == ri && j < i)) ? 1u : 0u;
+      }
+      fq[i] = fi + full + (rank < part ? 1u : 0u);
+    }
+  } else if (deficit < 0) {
+    // stable_sort by (rem asc, idx asc), sweep -1 over entries with f > 1 until
+    // settled (coder.cpp:67-83) == P complete passes + a partial pass.
+    const int64_t S = -deficit;
+    // the cum row doubles as scratch for the pre-adjustment frequencies
+    for (int i = lane; i < V; i += 32) cm[i] = fq[i];
+    __syncwarp();
+    int64_t lo_p = 0, hi_p = kTotal;  // largest P with removed(P) <= S
+    while (lo_p < hi_p) {
+      const int64_t mid = (lo_p + hi_p + 1) / 2;
+      uint32_t rm = 0;
+      for (int i = lane; i < V; i += 32) rm += uint32_t(imin64(int64_t(cm[i]) - 1, mid));
+      rm = warp_sum_u32(rm);
+      if (int64_t(rm) <= S) lo_p = mid;
+      else hi_p = mid - 1;
+    }
+    const int64_t P = lo_p;
+    uint32_t rmP = 0, elig = 0;
+    for (int i = lane; i < V; i += 32) {
+      const int64_t fi = cm[i];
+      rmP += uint32_t(imin64(fi - 1, P));
+      elig += (fi - 1 > P) ? 1u : 0u;
+    }
+    rmP = warp_sum_u32(rmP);
+    elig = warp_sum_u32(elig);
+    const int64_t rpart = S - int64_t(rmP);
+    if (rpart > 0 && int64_t(elig) < rpart) {
+      if (lane == 0) atomicExch(p.err, 1);  // cannot settle surplus
+      return;
+    }
+    for (int i = lane; i < V; i += 32) {
+      uint32_t fi0;
+      const double ri = rem_of(pr[i], fi0);
+      const int64_t fi = cm[i];
+      int64_t dec = imin64(fi - 1, P);
+      if (rpart > 0 && fi - 1 > P) {
+        uint32_t rank = 0;
+        for (int j = 0; j < V; ++j) {
+          if (int64_t(cm[j]) - 1 <= P) continue;
+          uint32_t fj0;
+          const double rj = rem_of(pr[j], fj0);
+          rank += (rj < ri || (rj == ri && j < i)) ? 1u : 0u;
+        }
+        if (int64_t(rank) < rpart) dec += 1;
+      }
+      fq[i] = uint32_t(fi - dec);
+    }
+  }
+  __syncwarp();
+  // cum = exclusive prefix of freqs
+  uint32_t carry = 0;
+  for (int i0 = 0; i0 < V; i0 += 32) {
+    const int i = i0 + lane;
+    const uint32_t f = i < V ? fq[i] : 0u;
+    uint32_t inc = f;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (i < V) cm[i] = carry + inc - f;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  if (lane == 0) cm[V] = carry;
+}
+
+__global__ void k_bc_dlm(const float* __restrict__ probs, const uint32_t* __restrict__ tokens,
+                         ChunkGeo geo, int64_t tick, int t, const float* __restrict__ params,
+                         int64_t p_cs, int64_t off_alpha, float* dlm, int64_t cs_p, int R, int V,
+                         const int* __restrict__ active) {
+  const int c = active[blockIdx.y];
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= int64_t(R) * V) return;
+  const int r = int(idx / V), i = int(idx % V);
+  const uint64_t jstep = uint64_t(t) + uint64_t(tick - geo.offset[c]);
+  const uint32_t tgt = tokens[geo.start[c] + uint64_t(r) * geo.L[c] + jstep];
+  const float a = det_sigmoid(params[c * p_cs + off_alpha]);
+  float g = probs[c * cs_p + idx];
+  if (uint32_t(i) == tgt) g = fsub(g, 1.0f);
+  dlm[c * cs_p + idx] = fmul(g, fsub(1.0f, a));
+}
+
+// one warp per chunk; every lane runs the sequential chains redundantly
+__global__ void k_alpha_step(AlphaP p, const int* __restrict__ active, int n_active) {
+  const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wi >= n_active) return;
+  const int c = active[wi];
+  const int R = p.R, V = p.V;
+  const uint64_t mstep = uint64_t(p.tick - p.geo.offset[c]);
+  const uint64_t jstep = uint64_t(p.t) + mstep;
+  const int64_t aoff = c * p.p_cs + p.off_alpha;
+  const float a = det_sigmoid(p.w[aoff]);
+  const float s0 = (p.flags & 1) ? 1.0f : 0.0f, s1 = (p.flags & 2) ? 1.0f : 0.0f;
+  float loss = 0.0f, dalpha = 0.0f;
+  for (int r = 0; r < R; ++r) {
+    const uint32_t tgt = p.tokens[p.geo.start[c] + uint64_t(r) * p.geo.L[c] + jstep];
+    const int64_t ro = c * p.cs_p + int64_t(r) * V;
+    const float pt = p.probs[ro + tgt];
+    loss = fadd(loss, -det_log(pt < 1e-38f ? 1e-38f : pt));  // std::max(pt, 1e-38f)
+    for (int i0 = 0; i0 < V; i0 += 32) {
+      const int i = i0 + lane;
+      float term = 0.0f;
+      if (i < V) {
+        float g = p.probs[ro + i];
+        if (uint32_t(i) == tgt) g = fsub(g, 1.0f);
+        const float stat = fadd(fmul(s0, (p.flags & 1) ? p.lu[ro + i] : 0.0f),
+                                fmul(s1, (p.flags & 2) ? p.lr[ro + i] : 0.0f));
+        term = fmul(g, fsub(stat, p.lm[ro + i]));
+      }
+      const int cnt = min(32, V - i0);
+      for (int l = 0; l < cnt; ++l) dalpha = fadd(dalpha, __shfl_sync(0xffffffffu, term, l));
+    }
+  }
+  if (lane == 0) {
+    const float grad = fadd(0.0f, fmul(fmul(dalpha, a), fsub(1.0f, a)));
+    const float b1 = 0.9f, b2 = 0.999f;
+    const float mi = fadd(fmul(b1, p.m[aoff]), fmul(fsub(1.0f, b1), grad));
+    const float vi = fadd(fmul(b2, p.v[aoff]), fmul(fmul(fsub(1.0f, b2), grad), grad));
+    const float mhat = fdiv(mi, p.sc[c].bc1), vhat = fdiv(vi, p.sc[c].bc2);
+    p.w[aoff] = fsub(p.w[aoff], fdiv(fmul(5e-4f, mhat), fadd(__fsqrt_rn(vhat), 1e-8f)));
+    p.m[aoff] = mi;
+    p.v[aoff] = vi;
+    if (p.warm_loss && mstep < p.warm_steps[c]) p.warm_loss[c] += double(loss);
+  }
+}
+
+// ------------------------------------------------------------------ range coder
+__device__ __forceinline__ void enc_sym(uint64_t& low, uint64_t& range, uint8_t* out,
+                                        uint64_t& pos, uint32_t cum, uint32_t freq) {
+  const uint64_t rb = range >> 16;
+  const uint64_t old = low;
+  low += rb * cum;
+  if (low < old) {  // carry back-patch (coder.cpp:101-109)
+    uint64_t i = pos;
+    for (;;) {
+      out[i - 1] += 1;
+      if (out[i - 1] != 0) break;
+      --i;
+    }
+  }
+  range = rb * freq;
+  while (range < kRenorm) {
+    out[pos++] = uint8_t(low >> 56);
+    low <<= 8;
+    range <<= 8;
+  }
+}
+
+__device__ __forceinline__ uint8_t dec_byte(const uint8_t* in, uint64_t len, uint64_t& pos, int& err) {
+  if (pos >= len) {
+    err = 1;  // StreamExhausted
+    return 0;
+  }
+  return in[pos++];
+}
+
+// exact floor(code / rb) clamped to 65535 (coder.cpp:144-146)
+__device__ __forceinline__ uint32_t dec_target(uint64_t code, uint64_t rb) {
+  uint64_t q = uint64_t(double(code) / double(rb));
+  if (q > kTotal) q = kTotal;
+  while (q > 0 && (__umul64hi(q, rb) != 0 || q * rb > code)) --q;
+  while (code - q * rb >= rb) ++q;
+  return q >= kTotal ? kTotal - 1 : uint32_t(q);
+}
+
+__device__ __forceinline__ uint32_t dec_sym(uint64_t& code, uint64_t& range, const uint8_t* in,
+                                            uint64_t len, uint64_t& pos, const uint32_t* cum,
+                                            const uint32_t* freq, uint32_t V, int& err) {
+  const uint64_t rb = range >> 16;
+  const uint32_t tgt = dec_target(code, rb);
+  uint32_t lo = 0, hi = V;
+  while (hi - lo > 1) {
+    const uint32_t mid = lo + (hi - lo) / 2;
+    if (cum[mid] <= tgt) lo = mid;
+    else hi = mid;
+  }
+  code -= rb * cum[lo];
+  range = rb * freq[lo];
+  while (range < kRenorm) {
+    code = (code << 8) | dec_byte(in, len, pos, err);
+    range <<= 8;
+  }
+  return lo;
+}
+
+// Uniform warm-up symbols j < min(t, L) of every chunk (pipeline.cpp:121-123).
+__global__ void k_range_uniform(uint32_t* tokens, ChunkGeo geo, int t, int R, int V,
+                                uint8_t* payload, const uint64_t* pay_off, const uint64_t* pay_len,
+                                CoderState* cs, int n_chunks, bool decode) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_chunks) return;
+  const uint64_t L = geo.L[c], start = geo.start[c];
+  const uint64_t nj = L < uint64_t(t) ? L : uint64_t(t);
+  const uint32_t base = kTotal / uint32_t(V), extra = kTotal % uint32_t(V);
+  uint8_t* buf = payload + pay_off[c];
+  CoderState s;
+  s.low = 0;
+  s.range = ~0ull;
+  s.pos = 0;
+  s.code = 0;
+  s.err = 0;
+  s.pad = 0;
+  if (decode) {
+    for (int i = 0; i < 8; ++i) s.code = (s.code << 8) | dec_byte(buf, pay_len[c], s.pos, s.err);
+    // uniform dist: freq_i = base + (i < extra), cum_i = i*base + min(i, extra)
+    for (uint64_t j = 0; j < nj && !s.err; ++j)
+      for (int r = 0; r < R; ++r) {
+        const uint64_t rb = s.range >> 16;
+        const uint32_t tgt = dec_target(s.code, rb);
+        // symbol with cum_i <= tgt < cum_{i+1}
+        uint32_t lo = 0, hi = uint32_t(V);
+        while (hi - lo > 1) {
+          const uint32_t mid = lo + (hi - lo) / 2;
+          const uint32_t cmid = mid * base + (mid < extra ? mid : extra);
+          if (cmid <= tgt) lo = mid;
+          else hi = mid;
+        }
+        const uint32_t clo = lo * base + (lo < extra ? lo : extra);
+        s.code -= rb * clo;
+        s.range = rb * (base + (lo < extra ? 1u : 0u));
+        while (s.range < kRenorm) {
+          s.code = (s.code << 8) | dec_byte(buf, pay_len[c], s.pos, s.err);
+          s.range <<= 8;
+        }
+        tokens[start + uint64_t(r) * L + j] = lo;
+      }
+  } else {
+    for (uint64_t j = 0; j < nj; ++j)
+      for (int r = 0; r < R; ++r) {
+        const uint32_t sym = tokens[start + uint64_t(r) * L + j];
+        enc_sym(s.low, s.range, buf, s.pos, sym * base + (sym < extra ? sym : extra),
+                base + (sym < extra ? 1u : 0u));
+      }
+  }
+  cs[c] = s;
+}
+
+__global__ void k_range_step(uint32_t* tokens, ChunkGeo geo, int64_t tick, int t, int R, int V,
+                             const uint32_t* __restrict__ freq, const uint32_t* __restrict__ cum,
+                             int64_t cs_f, int64_t cs_c, uint8_t* payload,
+                             const uint64_t* pay_off, const uint64_t* pay_len, CoderState* cs,
+                             const int* __restrict__ active, int n_active, bool decode) {
+  const int wi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (wi >= n_active) return;
+  const int c = active[wi];
+  const uint64_t L = geo.L[c], start = geo.start[c];
+  const uint64_t jstep = uint64_t(t) + uint64_t(tick - geo.offset[c]);
+  uint8_t* buf = payload + pay_off[c];
+  CoderState s = cs[c];
+  if (s.err) return;
+  const uint32_t* fq = freq + c * cs_f;
+  const uint32_t* cm = cum + c * cs_c;
+  if (decode) {
+    for (int r = 0; r < R && !s.err; ++r) {
+      const uint32_t sym = dec_sym(s.code, s.range, buf, pay_len[c], s.pos, cm + int64_t(r) * (V + 1),
+                                   fq + int64_t(r) * V, uint32_t(V), s.err);
+      tokens[start + uint64_t(r) * L + jstep] = sym;
+    }
+  } else {
+    for (int r = 0; r < R; ++r) {
+      const uint32_t sym = tokens[start + uint64_t(r) * L + jstep];
+      enc_sym(s.low, s.range, buf, s.pos, cm[int64_t(r) * (V + 1) + sym], fq[int64_t(r) * V + sym]);
+    }
+  }
+  cs[c] = s;
+}
+
+__global__ void k_range_finish(uint8_t* payload, const uint64_t* pay_off, CoderState* cs, int n) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  CoderState s = cs[c];
+  uint8_t* buf = payload + pay_off[c];
+  for (int i = 0; i < 8; ++i) {
+    buf[s.pos++] = uint8_t(s.low >> 56);
+    s.low <<= 8;
+  }
+  cs[c] = s;
+}
+
+}  // namespace
+
+void launch_mix_quantize(const MixP& p, const int* active, int n_active, cudaStream_t st) {
+  if (n_active <= 0) return;
+  dim3 grid(unsigned((int64_t(p.R) * 32 + 255) / 256), n_active);
+  k_mix_quantize<<<grid, 256, 0, st>>>(p, active);
+}
+
+void launch_bc_dlm(const float* probs, const uint32_t* tokens, ChunkGeo geo, int64_t tick, int t,
+                   const float* params, int64_t p_cs, int64_t off_alpha, float* dlm, int64_t cs_p,
+                   int R, int V, const int* active, int n_active, cudaStream_t st) {
+  if (n_active <= 0) return;
+  dim3 grid(unsigned((int64_t(R) * V + 255) / 256), n_active);
+  k_bc_dlm<<<grid, 256, 0, st>>>(probs, tokens, geo, tick, t, params, p_cs, off_alpha, dlm, cs_p, R,
+                                 V, active);
+}
+
+void launch_alpha_step(const AlphaP& p, const int* active, int n_active, cudaStream_t st) {
+  if (n_active <= 0) return;
+  k_alpha_step<<<unsigned((n_active * 32 + 127) / 128), 128, 0, st>>>(p, active, n_active);
+}
+
+void launch_range_uniform(uint32_t* tokens, ChunkGeo geo, int t, int R, int V, uint8_t* payload,
+                          const uint64_t* pay_off, const uint64_t* pay_len, CoderState* cs,
+                          int n_chunks, bool decode, cudaStream_t st) {
+  if (n_chunks <= 0) return;
+  k_range_uniform<<<unsigned((n_chunks + 63) / 64), 64, 0, st>>>(tokens, geo, t, R, V, payload,
+                                                                 pay_off, pay_len, cs, n_chunks,
+                                                                 decode);
+}
+
+void launch_range_step(uint32_t* tokens, ChunkGeo geo, int64_t tick, int t, int R, int V,
+                       const uint32_t* freq, const uint32_t* cum, int64_t cs_f, int64_t cs_c,
+                       uint8_t* payload, const uint64_t* pay_off, const uint64_t* pay_len,
+                       CoderState* cs, const int* active, int n_active, bool decode,
+                       cudaStream_t st) {
+  if (n_active <= 0) return;
+  k_range_step<<<unsigned((n_active + 63) / 64), 64, 0, st>>>(tokens, geo, tick, t, R, V, freq, cum,
+                                                              cs_f, cs_c, payload, pay_off, pay_len,
+                                                              cs, active, n_active, decode);
+}
+
+void launch_range_finish(uint8_t* payload, const uint64_t* pay_off, CoderState* cs, int n_chunks,
+                         cudaStream_t st) {
+  if (n_chunks <= 0) return;
+  k_range_finish<<<unsigned((n_chunks + 63) / 64), 64, 0, st>>>(payload, pay_off, cs, n_chunks);
+}
+
+}  // namespace pmklc_b200

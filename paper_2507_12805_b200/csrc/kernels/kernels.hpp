@@ -1,0 +1,149 @@
+// Launch interface of the sm_100a kernels (host-callable launchers).
+//
+// Batching model: every per-chunk kernel takes `active` (device array of chunk
+// ids, length n_active) and indexes its chunk's data as base + chunk*stride.
+// One launch therefore advances every active data block ("chunk", the unit of
+// PMKLC-M block partitioning, pipeline.cpp:32-52) by one coded batch step.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace pmklc_b200 {
+
+// ---------------------------------------------------------------- tokenizer
+// tokens[j] = sum_i base[j*s+i] << 2(k-1-i)   (skmer.cpp:16-24)
+// Input: 2-bit packed bases, base i at bits 2*(i%4) of byte i/4.
+void launch_skmer_encode_packed(const uint8_t* packed, uint64_t n_bases, uint32_t s, uint32_t k,
+                                uint32_t* tokens, uint64_t m, cudaStream_t st);
+// Input: one byte per base, ASCII "ACGT" (pure input, no exception bytes).
+void launch_skmer_encode_ascii(const uint8_t* ascii, uint64_t n_bases, uint32_t s, uint32_t k,
+                               uint32_t* tokens, uint64_t m, cudaStream_t st);
+// Input: one byte per base, codes 0..3.
+void launch_skmer_encode_codes(const uint8_t* codes, uint64_t n_bases, uint32_t s, uint32_t k,
+                               uint32_t* tokens, uint64_t m, cudaStream_t st);
+
+// canonicalize (alphabet.cpp:22-35): per-block non-ACGT counts, then compaction.
+// block_counts has n_blocks(n) entries; after a host/device exclusive scan
+// block_offsets, scatter writes codes (compacted) and exception pos/byte.
+uint32_t canon_blocks(uint64_t n);
+void launch_canon_count(const uint8_t* raw, uint64_t n, uint32_t* block_counts, cudaStream_t st);
+void launch_canon_scatter(const uint8_t* raw, uint64_t n, const uint64_t* block_exc_offsets,
+                          uint8_t* codes, uint64_t* exc_pos, uint8_t* exc_byte, cudaStream_t st);
+// decode (skmer.cpp:63-83) + restore (alphabet.cpp:37-60) fused: writes the
+// original bytes. exc_pos sorted ascending (validated by the container reader).
+void launch_detokenize_restore(const uint32_t* tokens, uint64_t m, uint32_t s, uint32_t k,
+                               const uint8_t* residual, uint64_t n_res, const uint64_t* exc_pos,
+                               const uint8_t* exc_byte, uint64_t n_exc, uint8_t* out,
+                               uint64_t out_len, int* err, cudaStream_t st);
+
+// ---------------------------------------------------------------- chunk engine
+struct ChunkGeo {      // per-chunk constants, device arrays indexed by chunk id
+  const uint64_t* start;   // token offset of the chunk
+  const uint64_t* L;       // batch steps (substream length)
+  const int64_t* offset;   // tick of the chunk's first model step
+};
+
+struct Tape;  // device tape pointers, defined in engine
+
+// Exact-order GEMM: C[m][n] = init + sum_{k ascending} A(m,k) * B(k,n).
+struct GemmP {
+  const float* A; int64_t a_cs, lda;  // A(m,k) = AT ? A[k*lda+m] : A[m*lda+k]
+  const float* B; int64_t b_cs, ldb;  // B(k,n) = BT ? B[n*ldb+k] : B[k*ldb+n]
+  float* C; int64_t c_cs, ldc;
+  const float* bias; int64_t bias_cs;       // init==1
+  const float* mask; int64_t mask_cs, ldm;  // epilogue: C = (mask<=0) ? 0 : C   (Ffn::backward)
+  int M, N, K;
+  int ones_row;  // also compute row M with A(M,k)=1 (the bias grad stored right after W)
+  int init;      // 0 zero, 1 bias, 2 accumulate onto C
+  int relu_a;    // A(m,k) = A<0 ? 0 : A   (Ffn relu, layers.cpp:538-540)
+};
+void launch_gemm(const GemmP& p, bool at, bool bt, const int* active, int n_active,
+                 cudaStream_t st);
+
+struct DmDims { int R, T, E, H, F, V, NH; };
+
+// ctx gather (pipeline.cpp:180-182) + Embedding/PositionalEmbedding forward
+void launch_embed(const uint32_t* tokens, ChunkGeo geo, int64_t tick, const float* params,
+                  int64_t p_cs, int64_t off_emb, int64_t off_pos, uint32_t* ctx, int64_t ctx_cs,
+                  float* x, int64_t x_cs, DmDims d, const int* active, int n_active, cudaStream_t st);
+// Attention forward core: scores, det_softmax, context (layers.cpp:452-470)
+void launch_attn_fwd(const float* q, const float* k, const float* v, float* wts, float* cx,
+                     int64_t cs_q, int64_t cs_kv, int64_t cs_w, DmDims d, float inv,
+                     const int* active, int n_active, cudaStream_t st);
+// Attention backward core (layers.cpp:480-512)
+void launch_attn_bwd(const float* q, const float* k, const float* v, const float* wts,
+                     const float* dctx, float* dq, float* dk, float* dv, int64_t cs_q,
+                     int64_t cs_kv, int64_t cs_w, DmDims d, float inv, const int* active,
+                     int n_active, cudaStream_t st);
+// PositionalEmbedding + Embedding backward (layers.cpp:117-125,147-155)
+void launch_embed_bwd(const uint32_t* ctx, int64_t ctx_cs, const float* dx, int64_t dx_cs,
+                      const float* dxl, int64_t dxl_cs, float* grads, int64_t g_cs,
+                      int64_t off_emb, int64_t off_pos, DmDims d, const int* active, int n_active,
+                      cudaStream_t st);
+
+struct AdamScalars {   // per chunk
+  uint64_t step;
+  float b1p, b2p, bc1, bc2;
+  float pad[2];
+};
+// Adam over params [0, n) of each active chunk, then zero their grads (adam.cpp:21-43)
+void launch_adam(float* w, float* g, float* m, float* v, int64_t p_cs, int64_t n,
+                 const AdamScalars* sc, const int* active, int n_active, cudaStream_t st);
+// whole-state copy for Step-wise Model Passing: dst chunk <- src chunk
+void launch_state_copy(float* w, float* m, float* v, AdamScalars* sc, int64_t p_cs, int64_t n,
+                       const int2* pairs, int n_pairs, cudaStream_t st);
+
+// mix (mixer.cpp:14-42) + det_softmax + quantize (coder.cpp:28-88), one warp per row;
+// also advances the chunk's Adam step scalars (adam.cpp:23-27).
+struct MixP {
+  const float* lu; const float* lr; const float* lm; int64_t cs_l;
+  float* probs; uint32_t* freq; uint32_t* cum; int64_t cs_p, cs_c;
+  const float* params; int64_t p_cs; int64_t off_alpha;
+  AdamScalars* sc;
+  int flags, R, V;
+  int* err;
+};
+void launch_mix_quantize(const MixP& p, const int* active, int n_active, cudaStream_t st);
+
+// Backward-controller CE gradient: dlm = (probs - onehot(tgt)) * (1 - alpha)
+void launch_bc_dlm(const float* probs, const uint32_t* tokens, ChunkGeo geo, int64_t tick, int t,
+                   const float* params, int64_t p_cs, int64_t off_alpha, float* dlm, int64_t cs_p,
+                   int R, int V, const int* active, int n_active, cudaStream_t st);
+// d alpha (one sequential accumulator over rows then symbols, mixer.cpp:64-84),
+// alpha's Adam update, CE loss for early_loss_bits.
+struct AlphaP {
+  const float* probs; const float* lu; const float* lr; const float* lm; int64_t cs_p;
+  const uint32_t* tokens; ChunkGeo geo; int64_t tick; int t;
+  float* w; float* m; float* v; int64_t p_cs; int64_t off_alpha;
+  const AdamScalars* sc;
+  double* warm_loss; const uint64_t* warm_steps;
+  int flags, R, V;
+};
+void launch_alpha_step(const AlphaP& p, const int* active, int n_active, cudaStream_t st);
+
+// Range coder (coder.cpp:101-166): one thread per chunk, R symbols per step.
+struct CoderState { uint64_t low, range, pos, code; int err; int pad; };
+void launch_range_uniform(uint32_t* tokens, ChunkGeo geo, int t, int R, int V, uint8_t* payload,
+                          const uint64_t* pay_off, const uint64_t* pay_len, CoderState* cs,
+                          int n_chunks, bool decode, cudaStream_t st);
+void launch_range_step(uint32_t* tokens, ChunkGeo geo, int64_t tick, int t, int R, int V,
+                       const uint32_t* freq, const uint32_t* cum, int64_t cs_f, int64_t cs_c,
+                       uint8_t* payload, const uint64_t* pay_off, const uint64_t* pay_len,
+                       CoderState* cs, const int* active, int n_active, bool decode,
+                       cudaStream_t st);
+void launch_range_finish(uint8_t* payload, const uint64_t* pay_off, CoderState* cs, int n_chunks,
+                         cudaStream_t st);
+
+// Frozen BiGRU predictor forward (SPuM/SPrM, models.cpp:53-73, layers.cpp:213-260)
+struct BiGruP {
+  const float* w;       // flat PMKW parameter array on device
+  const int64_t* offs;  // device: param offsets in BiGru::ps order
+  int layers, V, T, Es, Hs, B, R;
+};
+void launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, float* work,
+                          int64_t work_cs, float* logits, int64_t lg_cs, const int* active,
+                          int n_active, cudaStream_t st);
+size_t bigru_work_floats(const BiGruP& p);
+
+}  // namespace pmklc_b200

@@ -1,0 +1,283 @@
+// (s,k)-mer tokenizer, canonicalization and detokenize/restore for sm_100a.
+//
+// skmer encode (reference: core/src/skmer.cpp:16-24, token j = base-4 number of
+// bases [j*s, j*s+k), most significant digit first) is HBM-bound: per base it
+// reads 2 bits (packed) or 1 byte (ASCII) and writes 4*m/n bytes of u32 tokens.
+// Each CTA stages the packed window covering its 2048 tokens in shared memory
+// with 128-bit coalesced loads (halo of k-1 bases included), then every thread
+// extracts 8 consecutive tokens with two 32-bit shared loads + a funnel shift +
+// a 2-bit digit reversal (__brev), and writes them as two 128-bit stores.
+#include <cstdint>
+
+#include "kernels.hpp"
+
+namespace pmklc_b200 {
+
+namespace {
+
+constexpr int kTokThreads = 256;
+constexpr int kTokPerThread = 8;
+constexpr int kTokPerBlock = kTokThreads * kTokPerThread;  // 2048
+// bases per block <= 2047*8 + 8 = 16384 -> 4096 packed bytes; +32 B slack
+constexpr int kStageBytes = (kTokPerBlock * 8 + 8) / 4 + 48;
+
+__device__ __forceinline__ uint32_t ascii_code(uint32_t c) { return ((c >> 1) ^ (c >> 2)) & 3u; }
+
+// Reverse the order of the 2-bit digits of a 2k-bit field whose digit i sits
+// at bits 2i (first base lowest) into the token's MSB-first order.
+__device__ __forceinline__ uint32_t digits_to_token(uint32_t f, uint32_t k) {
+  uint32_t x = __brev(f);
+  x = ((x >> 1) & 0x55555555u) | ((x & 0x55555555u) << 1);
+  return x >> (32u - 2u * k);
+}
+
+// Extract tokens [j0, j0+2048) from a packed shared-memory window whose first
+// byte holds base `sbase`.
+__device__ __forceinline__ void emit_tokens(const uint32_t* sw, uint64_t sbase, uint64_t j0,
+                                            uint32_t s, uint32_t k, uint32_t* tokens, uint64_t m) {
+  const uint64_t jt = j0 + uint64_t(threadIdx.x) * kTokPerThread;
+  if (jt >= m) return;
+  const uint32_t mask = (k == 16) ? 0xffffffffu : ((1u << (2u * k)) - 1u);
+  uint32_t out[kTokPerThread];
+#pragma unroll
+  for (int q = 0; q < kTokPerThread; ++q) {
+    const uint64_t bit = ((jt + q) * s - sbase) * 2;  // bit offset in window
+    const uint32_t wi = uint32_t(bit >> 5), sh = uint32_t(bit & 31);
+    const uint32_t lo = sw[wi], hi = sw[wi + 1];
+    const uint32_t f = __funnelshift_r(lo, hi, sh) & mask;
+    out[q] = digits_to_token(f, k);
+  }
+  if (jt + kTokPerThread <= m) {
+    uint4* dst = reinterpret_cast<uint4*>(tokens + jt);
+    dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
+    dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
+  } else {
+    for (int q = 0; q < kTokPerThread && jt + q < m; ++q) tokens[jt + q] = out[q];
+  }
+}
+
+__global__ void __launch_bounds__(kTokThreads) k_skmer_packed(const uint8_t* __restrict__ packed,
+                                                              uint64_t n, uint32_t s, uint32_t k,
+                                                              uint32_t* __restrict__ tokens,
+                                                              uint64_t m) {
+  __shared__ __align__(16) uint32_t sw[kStageBytes / 4];
+  const uint64_t j0 = uint64_t(blockIdx.x) * kTokPerBlock;
+  const uint64_t jlast = min(j0 + kTokPerBlock, m) - 1;
+  const uint64_t b_first = j0 * s, b_end = jlast * s + k;  // bases needed [b_first, b_end)
+  const uint64_t byte0 = (b_first / 4) & ~uint64_t(15);
+  const uint64_t byte_end = min((b_end + 3) / 4, (n + 3) / 4);
+  const uint64_t nbytes = byte_end - byte0;
+  const uint64_t nvec = nbytes / 16;
+  const uint4* src = reinterpret_cast<const uint4*>(packed + byte0);
+  uint4* dst = reinterpret_cast<uint4*>(sw);
+  for (uint64_t i = threadIdx.x; i < nvec; i += kTokThreads) dst[i] = __ldg(src + i);
+  uint8_t* sb = reinterpret_cast<uint8_t*>(sw);
+  for (uint64_t i = nvec * 16 + threadIdx.x; i < nbytes + 8; i += kTokThreads)
+    sb[i] = i < nbytes ? packed[byte0 + i] : 0;
+  __syncthreads();
+  emit_tokens(sw, byte0 * 4, j0, s, k, tokens, m);
+}
+
+// ASCII / code input: stage 16 bytes per step, pack to 2-bit on the way in.
+template <bool kAscii>
+__global__ void __launch_bounds__(kTokThreads) k_skmer_bytes(const uint8_t* __restrict__ in,
+                                                             uint64_t n, uint32_t s, uint32_t k,
+                                                             uint32_t* __restrict__ tokens,
+                                                             uint64_t m) {
+  __shared__ __align__(16) uint32_t sw[kStageBytes / 4];
+  const uint64_t j0 = uint64_t(blockIdx.x) * kTokPerBlock;
+  const uint64_t jlast = min(j0 + kTokPerBlock, m) - 1;
+  const uint64_t b_first = j0 * s, b_end = jlast * s + k;
+  const uint64_t base0 = b_first & ~uint64_t(15);  // 16-base (16-byte) aligned
+  const uint64_t nb = b_end - base0;
+  const uint64_t nwords = (nb + 15) / 16;  // one u32 of packed codes per 16 input bytes
+  for (uint64_t w = threadIdx.x; w < nwords; w += kTokThreads) {
+    const uint64_t b = base0 + w * 16;
+    uint32_t packed = 0;
+    if (b + 16 <= n && ((reinterpret_cast<uintptr_t>(in + b) & 15) == 0)) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(in + b));
+      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t byte = (wv[q] >> (8 * c)) & 0xffu;
+          packed |= (kAscii ? ascii_code(byte) : (byte & 3u)) << (2 * (q * 4 + c));
+        }
+    } else {
+      for (int c = 0; c < 16; ++c) {
+        const uint32_t byte = (b + c < n) ? in[b + c] : 0u;
+        packed |= (kAscii ? ascii_code(byte) : (byte & 3u)) << (2 * c);
+      }
+    }
+    sw[w] = packed;
+  }
+  if (threadIdx.x == 0) sw[nwords] = 0;
+  __syncthreads();
+  emit_tokens(sw, base0, j0, s, k, tokens, m);
+}
+
+// ------------------------------------------------------------ canonicalize
+constexpr int kCanonThreads = 256;
+constexpr int kCanonPerThread = 16;
+constexpr int kCanonPerBlock = kCanonThreads * kCanonPerThread;  // 4096 bytes
+
+__device__ __forceinline__ bool is_acgt(uint32_t c) {
+  return c == 'A' || c == 'C' || c == 'G' || c == 'T';
+}
+
+__global__ void k_canon_count(const uint8_t* __restrict__ raw, uint64_t n, uint32_t* counts) {
+  const uint64_t b0 = uint64_t(blockIdx.x) * kCanonPerBlock + threadIdx.x * kCanonPerThread;
+  uint32_t c = 0;
+  for (int i = 0; i < kCanonPerThread; ++i)
+    if (b0 + i < n && !is_acgt(raw[b0 + i])) ++c;
+  // block reduce
+  __shared__ uint32_t red[kCanonThreads / 32];
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < kCanonThreads / 32; ++w) t += red[w];
+    counts[blockIdx.x] = t;
+  }
+}
+
+// block_exc: exclusive prefix of exception counts per block (blocks+1 entries)
+__global__ void k_canon_scatter(const uint8_t* __restrict__ raw, uint64_t n,
+                                const uint64_t* __restrict__ block_exc, uint8_t* codes,
+                                uint64_t* exc_pos, uint8_t* exc_byte) {
+  const uint64_t b0 = uint64_t(blockIdx.x) * kCanonPerBlock + threadIdx.x * kCanonPerThread;
+  uint32_t c = 0;
+  uint8_t v[kCanonPerThread];
+  for (int i = 0; i < kCanonPerThread; ++i) {
+    v[i] = (b0 + i < n) ? raw[b0 + i] : 'A';
+    if (b0 + i < n && !is_acgt(v[i])) ++c;
+  }
+  // exclusive block scan of c
+  __shared__ uint32_t wsum[kCanonThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t inc = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  uint32_t before = 0;
+  for (int w = 0; w < wid; ++w) before += wsum[w];
+  uint64_t e = block_exc[blockIdx.x] + before + (inc - c);
+  for (int i = 0; i < kCanonPerThread; ++i) {
+    const uint64_t p = b0 + i;
+    if (p >= n) break;
+    if (is_acgt(v[i])) {
+      codes[p - e] = uint8_t(ascii_code(v[i]));
+    } else {
+      exc_pos[e] = p;
+      exc_byte[e] = v[i];
+      ++e;
+    }
+  }
+}
+
+// ------------------------------------------------------------ detokenize
+__global__ void k_detok_restore(const uint32_t* __restrict__ tokens, uint64_t m, uint32_t s,
+                                uint32_t k, const uint8_t* __restrict__ residual, uint64_t n_res,
+                                const uint64_t* __restrict__ exc_pos,
+                                const uint8_t* __restrict__ exc_byte, uint64_t n_exc,
+                                uint8_t* __restrict__ out, uint64_t out_len, int* err) {
+  constexpr int kPer = 16;
+  const uint64_t o0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * kPer;
+  if (o0 >= out_len) return;
+  const uint64_t covered = m ? (m - 1) * s + k : 0;
+  const uint32_t width_mask = (1u << (2 * k)) - 1u;
+  // exceptions before o0
+  uint64_t lo = 0, hi = n_exc;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) / 2;
+    if (exc_pos[mid] < o0) lo = mid + 1;
+    else hi = mid;
+  }
+  uint64_t e = lo;
+  uint8_t buf[kPer];
+  for (int i = 0; i < kPer; ++i) {
+    const uint64_t o = o0 + i;
+    if (o >= out_len) break;
+    if (e < n_exc && exc_pos[e] == o) {
+      buf[i] = exc_byte[e++];
+      continue;
+    }
+    const uint64_t b = o - e;  // base index
+    uint32_t code;
+    if (b < covered) {
+      uint64_t j = b / s;
+      if (j > m - 1) j = m - 1;
+      const uint32_t digit = uint32_t(b - j * s);
+      const uint32_t tok = tokens[j];
+      if (tok > width_mask) atomicExch(err, 1);
+      code = (tok >> (2 * (k - 1 - digit))) & 3u;
+    } else {
+      const uint64_t rb = b - covered;
+      if (rb >= n_res) {
+        atomicExch(err, 2);
+        code = 0;
+      } else {
+        code = residual[rb] & 3u;
+      }
+    }
+    buf[i] = "ACGT"[code];
+  }
+  if (o0 + kPer <= out_len && ((reinterpret_cast<uintptr_t>(out + o0) & 15) == 0)) {
+    uint4 v;
+    uint32_t* vw = reinterpret_cast<uint32_t*>(&v);
+    for (int q = 0; q < 4; ++q)
+      vw[q] = uint32_t(buf[4 * q]) | uint32_t(buf[4 * q + 1]) << 8 | uint32_t(buf[4 * q + 2]) << 16 |
+              uint32_t(buf[4 * q + 3]) << 24;
+    *reinterpret_cast<uint4*>(out + o0) = v;
+  } else {
+    for (int i = 0; i < kPer && o0 + i < out_len; ++i) out[o0 + i] = buf[i];
+  }
+}
+
+}  // namespace
+
+void launch_skmer_encode_packed(const uint8_t* packed, uint64_t n, uint32_t s, uint32_t k,
+                                uint32_t* tokens, uint64_t m, cudaStream_t st) {
+  if (!m) return;
+  const uint64_t blocks = (m + kTokPerBlock - 1) / kTokPerBlock;
+  k_skmer_packed<<<unsigned(blocks), kTokThreads, 0, st>>>(packed, n, s, k, tokens, m);
+}
+void launch_skmer_encode_ascii(const uint8_t* ascii, uint64_t n, uint32_t s, uint32_t k,
+                               uint32_t* tokens, uint64_t m, cudaStream_t st) {
+  if (!m) return;
+  const uint64_t blocks = (m + kTokPerBlock - 1) / kTokPerBlock;
+  k_skmer_bytes<true><<<unsigned(blocks), kTokThreads, 0, st>>>(ascii, n, s, k, tokens, m);
+}
+void launch_skmer_encode_codes(const uint8_t* codes, uint64_t n, uint32_t s, uint32_t k,
+                               uint32_t* tokens, uint64_t m, cudaStream_t st) {
+  if (!m) return;
+  const uint64_t blocks = (m + kTokPerBlock - 1) / kTokPerBlock;
+  k_skmer_bytes<false><<<unsigned(blocks), kTokThreads, 0, st>>>(codes, n, s, k, tokens, m);
+}
+uint32_t canon_blocks(uint64_t n) { return uint32_t((n + kCanonPerBlock - 1) / kCanonPerBlock); }
+void launch_canon_count(const uint8_t* raw, uint64_t n, uint32_t* counts, cudaStream_t st) {
+  if (!n) return;
+  k_canon_count<<<canon_blocks(n), kCanonThreads, 0, st>>>(raw, n, counts);
+}
+void launch_canon_scatter(const uint8_t* raw, uint64_t n, const uint64_t* block_exc,
+                          uint8_t* codes, uint64_t* exc_pos, uint8_t* exc_byte, cudaStream_t st) {
+  if (!n) return;
+  k_canon_scatter<<<canon_blocks(n), kCanonThreads, 0, st>>>(raw, n, block_exc, codes, exc_pos,
+                                                             exc_byte);
+}
+void launch_detokenize_restore(const uint32_t* tokens, uint64_t m, uint32_t s, uint32_t k,
+                               const uint8_t* residual, uint64_t n_res, const uint64_t* exc_pos,
+                               const uint8_t* exc_byte, uint64_t n_exc, uint8_t* out,
+                               uint64_t out_len, int* err, cudaStream_t st) {
+  if (!out_len) return;
+  const uint64_t threads = (out_len + 15) / 16;
+  k_detok_restore<<<unsigned((threads + 255) / 256), 256, 0, st>>>(
+      tokens, m, s, k, residual, n_res, exc_pos, exc_byte, n_exc, out, out_len, err);
+}
+
+}  // namespace pmklc_b200

@@ -59,10 +59,10 @@ class Checker:
             raise FileNotFoundError(f"{so} missing: run `make -C oracle` (build())")
         self.lib = C.CDLL(str(so))
         self.p = prefix
-        self.lib[prefix + "last_error"].restype = C.c_char_p
+        getattr(self.lib, prefix + "last_error").restype = C.c_char_p
 
     def _f(self, name):
-        return self.lib[self.p + name]
+        return getattr(self.lib, self.p + name)
 
     def _check(self, rc):
         if rc != 0:
