@@ -99,6 +99,11 @@ int pmklc_dump_chunk(const uint32_t* tokens, uint64_t n_tokens, uint32_t flags,
                      int32_t device, float* probs, uint64_t max_steps, uint8_t** payload,
                      size_t* payload_n);
 
+/* quantize (coder.cpp:28-88) of `rows` probability rows of `width` on the
+ * device, same kernel as the pipeline; freqs has rows*width entries */
+int pmklc_quantize(const float* probs, uint64_t rows, uint32_t width, int32_t device,
+                   uint32_t* freqs);
+
 /* (s,k)-mer tokenizer on host base codes 0..3 -> tokens (capacity m) */
 int pmklc_skmer_encode(const uint8_t* codes, uint64_t n, uint32_t s, uint32_t k, int32_t device,
                        uint32_t* tokens, uint64_t* m);

@@ -67,7 +67,7 @@ EXPORTS = [
     "pmklc_skmer_encode_packed_device", "pmklc_free", "pmklc_device_free", "pmklc_last_error",
     "pmklc_errc_name", "pmklc_version", "pmklc_synth_markov3", "pmklc_synth_uniform",
     "pmklc_synth_genome", "pmklc_synth_species", "pmklc_synth_packed_codes", "pmklc_plan_chunks",
-    "pmklc_schedule",
+    "pmklc_schedule", "pmklc_quantize",
 ]
 
 _lib = None
@@ -227,6 +227,16 @@ def dump_chunk(tokens, flags: int, k: int, t: int, bs: int, scale: int, dm_seed:
                                   device, probs.ctypes.data_as(C.c_void_p), C.c_uint64(max_steps),
                                   C.byref(out), C.byref(n)))
     return _take(out, n.value), probs[:max_steps]
+
+
+def quantize(probs, device: int = 0):
+    """pmklc::quantize on the device for a [rows, width] float32 array -> uint32 freqs."""
+    import numpy as np
+    p = np.ascontiguousarray(np.atleast_2d(probs), dtype=np.float32)
+    f = np.zeros(p.shape, dtype=np.uint32)
+    _check(lib().pmklc_quantize(p.ctypes.data_as(C.c_void_p), C.c_uint64(p.shape[0]),
+                                p.shape[1], device, f.ctypes.data_as(C.c_void_p)))
+    return f
 
 
 def skmer_encode(codes: bytes, s: int, k: int, device: int = 0):

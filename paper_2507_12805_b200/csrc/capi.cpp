@@ -194,6 +194,14 @@ int pmklc_dump_chunk(const uint32_t* tokens, uint64_t n_tokens, uint32_t flags,
   });
 }
 
+int pmklc_quantize(const float* probs, uint64_t rows, uint32_t width, int32_t device,
+                   uint32_t* freqs) {
+  return guard([&] {
+    std::vector<uint32_t> f = quantize_rows(probs, rows, width, device);
+    if (!f.empty()) std::memcpy(freqs, f.data(), f.size() * 4);
+  });
+}
+
 int pmklc_skmer_encode(const uint8_t* codes, uint64_t n, uint32_t s, uint32_t k, int32_t device,
                        uint32_t* tokens, uint64_t* m) {
   return guard([&] {

@@ -256,7 +256,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   DBuf<uint32_t> ctx(TW * s_ctx), freq(TW * s_rv), cum(TW * s_cum);
   DBuf<float> x(TW * s_x), kk(TW * s_kv), vv(TW * s_kv), q(TW * s_rh), wts(TW * s_w),
       cx(TW * s_rh), ao(TW * s_rh), pre(TW * s_rf), fo(TW * s_rh), lm(TW * s_rv),
-      probs(TW * s_rv), dlm(TW * s_rv), dffn(TW * s_rh), dact(TW * s_rf), datt(TW * s_rh),
+      probs(TW * s_rv), dlm(TW * s_rv), aterm(TW * s_rv), lterm(TW * R), dffn(TW * s_rh), dact(TW * s_rf), datt(TW * s_rh),
       dctx(TW * s_rh), dq(TW * s_rh), dk(TW * s_kv), dv(TW * s_kv), dx(TW * s_x), dxl(TW * s_re);
   DBuf<float> lu((run.flags & 1) ? TW * s_rv : 0), lr((run.flags & 2) ? TW * s_rv : 0);
   int64_t s_bw = 0;
@@ -422,13 +422,11 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
                       d_pay_off.p, d_pay_len.p, cstate.p, act, na, run.decode, st);
     ++run.launches;
     // ---------------- backward controller (OnlineTrainer::step, mixer.cpp:57-97)
-    launch_bc_dlm(probs.p, d_tokens, geo, tick, int(run.t), w.p, P, oA, dlm.p, s_rv, R, V, act, na,
-                  st);
-    ++run.launches;
-    AlphaP ap{probs.p, lu.p, lr.p, lm.p, s_rv, d_tokens, geo, tick, int(run.t), w.p, m.p, v.p, P, oA,
-              sc.p, warm_loss.p, d_warm.p, int(run.flags), R, V};
-    launch_alpha_step(ap, act, na, st);
-    ++run.launches;
+    BcP bp{probs.p, lu.p, lr.p, lm.p, s_rv, d_tokens, geo, tick, int(run.t), w.p, m.p, v.p, P, oA,
+           dlm.p, aterm.p, lterm.p, R, sc.p, warm_loss.p, d_warm.p, int(run.flags), R, V};
+    launch_bc_dlm(bp, act, na, st);
+    launch_alpha_step(bp, act, na, st);
+    run.launches += 2;
     // head, ffn, attention output projection (Linear::backward, layers.cpp:176-183)
     gemm(GemmP{fo.p, s_rh, H, dlm.p, s_rv, V, G_(DmLayout::HW), P, V, nullptr, 0, nullptr, 0, 0, H,
                V, R, 1, 2, 0},
@@ -947,6 +945,37 @@ std::vector<Bytes> encode_chunks(const std::vector<ChunkJob>& jobs, uint8_t flag
   if (W) run_chunks(run, d_tok.p, st);
   if (opt.stats) *opt.stats = run.stats;
   return run.payloads;
+}
+
+std::vector<uint32_t> quantize_rows(const float* probs, uint64_t rows, uint32_t width, int device) {
+  if (width == 0 || width > 65536) raise(errc::invalid_distribution, "unsupported width");
+  CK(cudaSetDevice(device));
+  Stream stream(device);
+  cudaStream_t st = stream.s;
+  const int64_t cs = int64_t(rows) * width;
+  DBuf<float> pr(cs + 1);
+  DBuf<uint32_t> fq(cs + 1), cm(rows * (width + 1) + 1);
+  DBuf<int> err(1), act(1);
+  err.zero(st);
+  act.zero(st);
+  pr.upload(probs, cs, st);
+  MixP mp{};
+  mp.probs = pr.p;
+  mp.freq = fq.p;
+  mp.cum = cm.p;
+  mp.R = int(rows);
+  mp.V = int(width);
+  mp.err = err.p;
+  mp.probs_given = 1;
+  launch_mix_quantize(mp, act.p, 1, st);
+  check_launch();
+  std::vector<uint32_t> out(cs);
+  int h_err = 0;
+  CK(cudaMemcpyAsync(out.data(), fq.p, cs * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&h_err, err.p, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h_err) raise(errc::invalid_distribution, "probabilities do not sum to 1");
+  return out;
 }
 
 std::vector<uint32_t> skmer_encode_codes(const uint8_t* codes, uint64_t n, uint32_t s, uint32_t k,

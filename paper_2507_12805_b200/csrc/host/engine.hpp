@@ -70,6 +70,10 @@ std::vector<Bytes> encode_chunks(const std::vector<ChunkJob>& jobs, uint8_t flag
                                  uint32_t bs, uint32_t scale, uint64_t dm_seed, int device,
                                  const CallOptions& opt = {});
 
+// quantize (coder.cpp:28-88) of `rows` probability rows on the device, with
+// the same kernel the pipeline uses (test hook for the closed-form quantizer)
+std::vector<uint32_t> quantize_rows(const float* probs, uint64_t rows, uint32_t width, int device);
+
 // Stand-alone tokenizer on host buffers of base codes 0..3 (for parity tests)
 std::vector<uint32_t> skmer_encode_codes(const uint8_t* codes, uint64_t n, uint32_t s, uint32_t k,
                                          int device);

@@ -39,7 +39,7 @@ __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t x) {
 __global__ void k_mix_quantize(MixP p, const int* __restrict__ active) {
   const int c = active[blockIdx.y];
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {  // Adam::step scalar prologue (adam.cpp:23-27)
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.sc) {  // Adam::step scalar prologue (adam.cpp:23-27)
     AdamScalars s = p.sc[c];
     s.step += 1;
     s.b1p = fmul(s.b1p, 0.9f);
@@ -58,31 +58,34 @@ __global__ void k_mix_quantize(MixP p, const int* __restrict__ active) {
   uint32_t* fq = p.freq + c * p.cs_p + int64_t(row) * V;
   uint32_t* cm = p.cum + c * p.cs_c + int64_t(row) * (V + 1);
 
-  const float alpha = det_sigmoid(p.params[c * p.p_cs + p.off_alpha]);
-  const float s0 = (p.flags & 1) ? 1.0f : 0.0f, s1 = (p.flags & 2) ? 1.0f : 0.0f;
-  const float s2 = (p.flags & 4) ? 1.0f : 0.0f;
-  const float wdyn = fmul(fsub(1.0f, alpha), s2);
-  // z = alpha*stat + ((1-alpha)*s2)*lm
-  float mx = -__int_as_float(0x7f800000);
-  for (int i = lane; i < V; i += 32) {
-    const float stat = fadd(fmul(s0, lu ? lu[i] : 0.0f), fmul(s1, lr ? lr[i] : 0.0f));
-    const float z = fadd(fmul(alpha, stat), fmul(wdyn, lm[i]));
-    pr[i] = z;
-    mx = fmaxf(mx, z);
-  }
-  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  float sum = 0.0f;
-  for (int i0 = 0; i0 < V; i0 += 32) {
-    const int i = i0 + lane;
-    float e = 0.0f;
-    if (i < V) {
-      e = det_exp(fsub(pr[i], mx));
-      pr[i] = e;
+  float inv = 1.0f;
+  if (!p.probs_given) {
+    const float alpha = det_sigmoid(p.params[c * p.p_cs + p.off_alpha]);
+    const float s0 = (p.flags & 1) ? 1.0f : 0.0f, s1 = (p.flags & 2) ? 1.0f : 0.0f;
+    const float s2 = (p.flags & 4) ? 1.0f : 0.0f;
+    const float wdyn = fmul(fsub(1.0f, alpha), s2);
+    // z = alpha*stat + ((1-alpha)*s2)*lm
+    float mx = -__int_as_float(0x7f800000);
+    for (int i = lane; i < V; i += 32) {
+      const float stat = fadd(fmul(s0, lu ? lu[i] : 0.0f), fmul(s1, lr ? lr[i] : 0.0f));
+      const float z = fadd(fmul(alpha, stat), fmul(wdyn, lm[i]));
+      pr[i] = z;
+      mx = fmaxf(mx, z);
     }
-    const int cnt = min(32, V - i0);
-    for (int l = 0; l < cnt; ++l) sum = fadd(sum, __shfl_sync(0xffffffffu, e, l));
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.0f;
+    for (int i0 = 0; i0 < V; i0 += 32) {
+      const int i = i0 + lane;
+      float e = 0.0f;
+      if (i < V) {
+        e = det_exp(fsub(pr[i], mx));
+        pr[i] = e;
+      }
+      const int cnt = min(32, V - i0);
+      for (int l = 0; l < cnt; ++l) sum = fadd(sum, __shfl_sync(0xffffffffu, e, l));
+    }
+    inv = fdiv(1.0f, sum);
   }
-  const float inv = fdiv(1.0f, sum);
   // probabilities, positivity, double sum in reference order (coder.cpp:31-38)
   double dsum = 0.0;
   bool bad = false;
@@ -91,7 +94,7 @@ __global__ void k_mix_quantize(MixP p, const int* __restrict__ active) {
     const int i = i0 + lane;
     float pv = 0.0f;
     if (i < V) {
-      pv = fmul(pr[i], inv);
+      pv = p.probs_given ? pr[i] : fmul(pr[i], inv);
       pr[i] = pv;
       if (!(pv > 0.0f)) bad = true;
       uint32_t f;
@@ -189,54 +192,73 @@ __global__ void k_mix_quantize(MixP p, const int* __restrict__ active) {
   if (lane == 0) cm[V] = carry;
 }
 
-__global__ void k_bc_dlm(const float* __restrict__ probs, const uint32_t* __restrict__ tokens,
-                         ChunkGeo geo, int64_t tick, int t, const float* __restrict__ params,
-                         int64_t p_cs, int64_t off_alpha, float* dlm, int64_t cs_p, int R, int V,
-                         const int* __restrict__ active) {
+__global__ void k_bc_dlm(BcP p, const int* __restrict__ active) {
   const int c = active[blockIdx.y];
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int R = p.R, V = p.V;
   if (idx >= int64_t(R) * V) return;
   const int r = int(idx / V), i = int(idx % V);
-  const uint64_t jstep = uint64_t(t) + uint64_t(tick - geo.offset[c]);
-  const uint32_t tgt = tokens[geo.start[c] + uint64_t(r) * geo.L[c] + jstep];
-  const float a = det_sigmoid(params[c * p_cs + off_alpha]);
-  float g = probs[c * cs_p + idx];
-  if (uint32_t(i) == tgt) g = fsub(g, 1.0f);
-  dlm[c * cs_p + idx] = fmul(g, fsub(1.0f, a));
+  const uint64_t jstep = uint64_t(p.t) + uint64_t(p.tick - p.geo.offset[c]);
+  const uint32_t tgt = p.tokens[p.geo.start[c] + uint64_t(r) * p.geo.L[c] + jstep];
+  const float a = det_sigmoid(p.w[c * p.p_cs + p.off_alpha]);
+  const int64_t o = c * p.cs_p + idx;
+  const float pv = p.probs[o];
+  float g = pv;
+  if (uint32_t(i) == tgt) {
+    g = fsub(g, 1.0f);
+    p.lterm[c * p.cs_l + r] = -det_log(pv < 1e-38f ? 1e-38f : pv);  // std::max(p, 1e-38f)
+  }
+  const float s0 = (p.flags & 1) ? 1.0f : 0.0f, s1 = (p.flags & 2) ? 1.0f : 0.0f;
+  const float stat = fadd(fmul(s0, (p.flags & 1) ? p.lu[o] : 0.0f),
+                          fmul(s1, (p.flags & 2) ? p.lr[o] : 0.0f));
+  p.aterm[o] = fmul(g, fsub(stat, p.lm[o]));
+  p.dlm[o] = fmul(g, fsub(1.0f, a));
 }
 
-// one warp per chunk; every lane runs the sequential chains redundantly
-__global__ void k_alpha_step(AlphaP p, const int* __restrict__ active, int n_active) {
-  const int wi = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wi >= n_active) return;
-  const int c = active[wi];
-  const int R = p.R, V = p.V;
-  const uint64_t mstep = uint64_t(p.tick - p.geo.offset[c]);
-  const uint64_t jstep = uint64_t(p.t) + mstep;
-  const int64_t aoff = c * p.p_cs + p.off_alpha;
-  const float a = det_sigmoid(p.w[aoff]);
-  const float s0 = (p.flags & 1) ? 1.0f : 0.0f, s1 = (p.flags & 2) ? 1.0f : 0.0f;
-  float loss = 0.0f, dalpha = 0.0f;
-  for (int r = 0; r < R; ++r) {
-    const uint32_t tgt = p.tokens[p.geo.start[c] + uint64_t(r) * p.geo.L[c] + jstep];
-    const int64_t ro = c * p.cs_p + int64_t(r) * V;
-    const float pt = p.probs[ro + tgt];
-    loss = fadd(loss, -det_log(pt < 1e-38f ? 1e-38f : pt));  // std::max(pt, 1e-38f)
-    for (int i0 = 0; i0 < V; i0 += 32) {
-      const int i = i0 + lane;
-      float term = 0.0f;
-      if (i < V) {
-        float g = p.probs[ro + i];
-        if (uint32_t(i) == tgt) g = fsub(g, 1.0f);
-        const float stat = fadd(fmul(s0, (p.flags & 1) ? p.lu[ro + i] : 0.0f),
-                                fmul(s1, (p.flags & 2) ? p.lr[ro + i] : 0.0f));
-        term = fmul(g, fsub(stat, p.lm[ro + i]));
-      }
-      const int cnt = min(32, V - i0);
-      for (int l = 0; l < cnt; ++l) dalpha = fadd(dalpha, __shfl_sync(0xffffffffu, term, l));
+// Block per chunk. Warp 0 lane 0 runs the d(alpha) chain over shared memory
+// while the other warps stage the next batch of terms (double buffer); warp
+// 1 lane 0 runs the (short) loss chain.
+constexpr int kAlphaBatch = 4096;
+__global__ void __launch_bounds__(256) k_alpha_step(BcP p, const int* __restrict__ active) {
+  __shared__ __align__(16) float buf[2][kAlphaBatch];
+  const int c = active[blockIdx.x];
+  const int64_t n = int64_t(p.R) * p.V;
+  const float* terms = p.aterm + c * p.cs_p;
+  const int nb = int((n + kAlphaBatch - 1) / kAlphaBatch);
+  const int tid = threadIdx.x;
+  float dalpha = 0.0f;
+  for (int i = tid; i < kAlphaBatch && i < n; i += 256) buf[0][i] = terms[i];
+  __syncthreads();
+  for (int b = 0; b < nb; ++b) {
+    if (b + 1 < nb && tid >= 32) {
+      const int64_t base = int64_t(b + 1) * kAlphaBatch;
+      for (int64_t i = tid - 32; i < kAlphaBatch && base + i < n; i += 224) buf[(b + 1) & 1][i] = terms[base + i];
     }
+    if (tid == 0) {
+      const int cnt = int(min(int64_t(kAlphaBatch), n - int64_t(b) * kAlphaBatch));
+      const float* q = buf[b & 1];
+      int i = 0;
+      for (; i + 4 <= cnt; i += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(q + i);
+        dalpha = fadd(dalpha, v.x);
+        dalpha = fadd(dalpha, v.y);
+        dalpha = fadd(dalpha, v.z);
+        dalpha = fadd(dalpha, v.w);
+      }
+      for (; i < cnt; ++i) dalpha = fadd(dalpha, q[i]);
+    }
+    __syncthreads();
   }
-  if (lane == 0) {
+  const uint64_t mstep = uint64_t(p.tick - p.geo.offset[c]);
+  if (tid == 32 && p.warm_loss && mstep < p.warm_steps[c]) {
+    const float* lt = p.lterm + c * p.cs_l;
+    float loss = 0.0f;
+    for (int r = 0; r < p.R; ++r) loss = fadd(loss, lt[r]);
+    p.warm_loss[c] += double(loss);
+  }
+  if (tid == 0) {
+    const int64_t aoff = c * p.p_cs + p.off_alpha;
+    const float a = det_sigmoid(p.w[aoff]);
     const float grad = fadd(0.0f, fmul(fmul(dalpha, a), fsub(1.0f, a)));
     const float b1 = 0.9f, b2 = 0.999f;
     const float mi = fadd(fmul(b1, p.m[aoff]), fmul(fsub(1.0f, b1), grad));
@@ -245,7 +267,6 @@ __global__ void k_alpha_step(AlphaP p, const int* __restrict__ active, int n_act
     p.w[aoff] = fsub(p.w[aoff], fdiv(fmul(5e-4f, mhat), fadd(__fsqrt_rn(vhat), 1e-8f)));
     p.m[aoff] = mi;
     p.v[aoff] = vi;
-    if (p.warm_loss && mstep < p.warm_steps[c]) p.warm_loss[c] += double(loss);
   }
 }
 
@@ -360,12 +381,21 @@ __global__ void k_range_uniform(uint32_t* tokens, ChunkGeo geo, int t, int R, in
   cs[c] = s;
 }
 
-__global__ void k_range_step(uint32_t* tokens, ChunkGeo geo, int64_t tick, int t, int R, int V,
-                             const uint32_t* __restrict__ freq, const uint32_t* __restrict__ cum,
-                             int64_t cs_f, int64_t cs_c, uint8_t* payload,
-                             const uint64_t* pay_off, const uint64_t* pay_len, CoderState* cs,
-                             const int* __restrict__ active, int n_active, bool decode) {
-  const int wi = blockIdx.x * blockDim.x + threadIdx.x;
+// One warp per chunk. Encode: the warp gathers 32 rows' (cum, freq) of the
+// coded symbols into shared memory, lane 0 runs the 64-bit coder over them.
+// Decode: every lane carries the same coder state; the symbol search is a
+// warp ballot over the cum row held in registers (prefetched one row ahead),
+// which equals the reference binary search (largest i with cum[i] <= target).
+constexpr int kCoderWarps = 4;
+constexpr int kMaxQ = 8;  // V <= 256 in registers; larger V uses the scalar search
+__global__ void __launch_bounds__(kCoderWarps * 32) k_range_step(
+    uint32_t* tokens, ChunkGeo geo, int64_t tick, int t, int R, int V,
+    const uint32_t* __restrict__ freq, const uint32_t* __restrict__ cum, int64_t cs_f,
+    int64_t cs_c, uint8_t* payload, const uint64_t* pay_off, const uint64_t* pay_len,
+    CoderState* cs, const int* __restrict__ active, int n_active, bool decode) {
+  __shared__ uint32_t sc_[kCoderWarps][32], sf_[kCoderWarps][32];
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wi = blockIdx.x * kCoderWarps + wl;
   if (wi >= n_active) return;
   const int c = active[wi];
   const uint64_t L = geo.L[c], start = geo.start[c];
@@ -375,19 +405,80 @@ __global__ void k_range_step(uint32_t* tokens, ChunkGeo geo, int64_t tick, int t
   if (s.err) return;
   const uint32_t* fq = freq + c * cs_f;
   const uint32_t* cm = cum + c * cs_c;
-  if (decode) {
-    for (int r = 0; r < R && !s.err; ++r) {
-      const uint32_t sym = dec_sym(s.code, s.range, buf, pay_len[c], s.pos, cm + int64_t(r) * (V + 1),
-                                   fq + int64_t(r) * V, uint32_t(V), s.err);
-      tokens[start + uint64_t(r) * L + jstep] = sym;
+  if (!decode) {
+    for (int r0 = 0; r0 < R; r0 += 32) {
+      const int r = r0 + lane;
+      if (r < R) {
+        const uint32_t sym = tokens[start + uint64_t(r) * L + jstep];
+        sc_[wl][lane] = cm[int64_t(r) * (V + 1) + sym];
+        sf_[wl][lane] = fq[int64_t(r) * V + sym];
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const int cnt = min(32, R - r0);
+        for (int q = 0; q < cnt; ++q) enc_sym(s.low, s.range, buf, s.pos, sc_[wl][q], sf_[wl][q]);
+      }
+      __syncwarp();
     }
-  } else {
-    for (int r = 0; r < R; ++r) {
-      const uint32_t sym = tokens[start + uint64_t(r) * L + jstep];
-      enc_sym(s.low, s.range, buf, s.pos, cm[int64_t(r) * (V + 1) + sym], fq[int64_t(r) * V + sym]);
-    }
+    if (lane == 0) cs[c] = s;
+    return;
   }
-  cs[c] = s;
+  const int nq = (V + 1 + 31) / 32;  // cum[0..V] (cum[V] = 2^16) in registers
+  if (nq > kMaxQ) {  // large alphabets: scalar path in lane 0
+    if (lane == 0) {
+      for (int r = 0; r < R && !s.err; ++r) {
+        const uint32_t sym = dec_sym(s.code, s.range, buf, pay_len[c], s.pos, cm + int64_t(r) * (V + 1),
+                                     fq + int64_t(r) * V, uint32_t(V), s.err);
+        tokens[start + uint64_t(r) * L + jstep] = sym;
+      }
+      cs[c] = s;
+    }
+    return;
+  }
+  const uint64_t plen = pay_len[c];
+  uint32_t cur[kMaxQ], nxt[kMaxQ];
+#pragma unroll
+  for (int q = 0; q < kMaxQ; ++q) {
+    const int i = lane + 32 * q;
+    cur[q] = (q < nq && i <= V) ? cm[i] : 0xffffffffu;
+  }
+  for (int r = 0; r < R; ++r) {
+    if (r + 1 < R) {
+#pragma unroll
+      for (int q = 0; q < kMaxQ; ++q) {
+        const int i = lane + 32 * q;
+        nxt[q] = (q < nq && i <= V) ? cm[int64_t(r + 1) * (V + 1) + i] : 0xffffffffu;
+      }
+    }
+    const uint64_t rb = s.range >> 16;
+    const uint32_t tgt = dec_target(s.code, rb);
+    int count = 0;
+#pragma unroll
+    for (int q = 0; q < kMaxQ; ++q)
+      if (q < nq) count += __popc(__ballot_sync(0xffffffffu, cur[q] <= tgt));
+    // tgt <= 65535 < cum[V]: the count covers i < V only, so sym = count-1 in [0, V)
+    const int sym = count - 1;
+    uint32_t csym = 0, cnext = 0;
+#pragma unroll
+    for (int q = 0; q < kMaxQ; ++q) {
+      const uint32_t v0 = __shfl_sync(0xffffffffu, cur[q], sym & 31);
+      const uint32_t v1 = __shfl_sync(0xffffffffu, cur[q], (sym + 1) & 31);
+      if (q == (sym >> 5)) csym = v0;
+      if (q == ((sym + 1) >> 5)) cnext = v1;
+    }
+    const uint32_t fsym = cnext - csym;  // freq = cum[s+1] - cum[s]
+    s.code -= rb * csym;
+    s.range = rb * fsym;
+    while (s.range < kRenorm) {
+      s.code = (s.code << 8) | dec_byte(buf, plen, s.pos, s.err);
+      s.range <<= 8;
+    }
+    if (lane == 0) tokens[start + uint64_t(r) * L + jstep] = uint32_t(sym);
+    if (s.err) break;
+#pragma unroll
+    for (int q = 0; q < kMaxQ; ++q) cur[q] = nxt[q];
+  }
+  if (lane == 0) cs[c] = s;
 }
 
 __global__ void k_range_finish(uint8_t* payload, const uint64_t* pay_off, CoderState* cs, int n) {
@@ -410,18 +501,15 @@ void launch_mix_quantize(const MixP& p, const int* active, int n_active, cudaStr
   k_mix_quantize<<<grid, 256, 0, st>>>(p, active);
 }
 
-void launch_bc_dlm(const float* probs, const uint32_t* tokens, ChunkGeo geo, int64_t tick, int t,
-                   const float* params, int64_t p_cs, int64_t off_alpha, float* dlm, int64_t cs_p,
-                   int R, int V, const int* active, int n_active, cudaStream_t st) {
+void launch_bc_dlm(const BcP& p, const int* active, int n_active, cudaStream_t st) {
   if (n_active <= 0) return;
-  dim3 grid(unsigned((int64_t(R) * V + 255) / 256), n_active);
-  k_bc_dlm<<<grid, 256, 0, st>>>(probs, tokens, geo, tick, t, params, p_cs, off_alpha, dlm, cs_p, R,
-                                 V, active);
+  dim3 grid(unsigned((int64_t(p.R) * p.V + 255) / 256), n_active);
+  k_bc_dlm<<<grid, 256, 0, st>>>(p, active);
 }
 
-void launch_alpha_step(const AlphaP& p, const int* active, int n_active, cudaStream_t st) {
+void launch_alpha_step(const BcP& p, const int* active, int n_active, cudaStream_t st) {
   if (n_active <= 0) return;
-  k_alpha_step<<<unsigned((n_active * 32 + 127) / 128), 128, 0, st>>>(p, active, n_active);
+  k_alpha_step<<<unsigned(n_active), 256, 0, st>>>(p, active);
 }
 
 void launch_range_uniform(uint32_t* tokens, ChunkGeo geo, int t, int R, int V, uint8_t* payload,
@@ -439,7 +527,7 @@ void launch_range_step(uint32_t* tokens, ChunkGeo geo, int64_t tick, int t, int 
                        CoderState* cs, const int* active, int n_active, bool decode,
                        cudaStream_t st) {
   if (n_active <= 0) return;
-  k_range_step<<<unsigned((n_active + 63) / 64), 64, 0, st>>>(tokens, geo, tick, t, R, V, freq, cum,
+  k_range_step<<<unsigned((n_active + kCoderWarps - 1) / kCoderWarps), kCoderWarps * 32, 0, st>>>(tokens, geo, tick, t, R, V, freq, cum,
                                                               cs_f, cs_c, payload, pay_off, pay_len,
                                                               cs, active, n_active, decode);
 }

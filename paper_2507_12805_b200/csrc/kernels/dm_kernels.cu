@@ -19,15 +19,28 @@ namespace pmklc_b200 {
 namespace {
 
 // ------------------------------------------------------------------ GEMM
-// Register-tiled SIMT GEMM: 16x16 threads, each owning TM x TN outputs laid
-// out with stride 16 so shared-memory reads are broadcast / conflict-free.
-// K is walked in ascending order tile by tile; the partial last tile is
-// bounded exactly (no zero padding: 0*x would change signed zeros / NaNs).
-template <bool AT, bool BT, int TM, int TN>
+// Shared-memory tiled SIMT GEMM: 16x16 threads, each owning TM x TN outputs
+// laid out with stride 16 (broadcast / conflict-free shared reads). K-tiles of
+// depth 32 are staged with cp.async (LDGSTS) into a double buffer so the next
+// tile's global loads overlap the current tile's math. K is walked in
+// ascending order tile by tile and the partial last tile is bounded exactly
+// (no zero padding: 0*x would change signed zeros / NaNs). The tile size is
+// picked per launch: big tiles when many chunks fill the chip (fewer shared
+// loads per MAC), 16x16 tiles when one chunk must finish fast (more SMs on
+// its short dependent chains).
+__device__ __forceinline__ void cp_async4(float* smem, const float* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <bool AT, bool BT, int TM, int TN, int BK, int STAGES>
 __global__ void __launch_bounds__(256) k_gemm_tiled(GemmP p, const int* __restrict__ active) {
-  constexpr int BM = 16 * TM, BN = 16 * TN, BK = 16;
-  __shared__ float As[BK][BM + 1];
-  __shared__ float Bs[BK][BN + 1];
+  constexpr int BM = 16 * TM, BN = 16 * TN;
+  __shared__ float As[STAGES][BK][BM + 4];
+  __shared__ float Bs[STAGES][BK][BN + 4];
   const int c = active[blockIdx.z];
   const float* A = p.A + c * p.a_cs;
   const float* B = p.B + c * p.b_cs;
@@ -35,6 +48,32 @@ __global__ void __launch_bounds__(256) k_gemm_tiled(GemmP p, const int* __restri
   const int Mx = p.M + (p.ones_row ? 1 : 0);
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int ntiles = (p.K + BK - 1) / BK;
+
+  auto load = [&](int tile) {
+    if (tile < ntiles) {
+      const int stage = tile % STAGES, k0 = tile * BK;
+      for (int idx = threadIdx.x; idx < BM * BK; idx += 256) {
+        int mm, kk;
+        if (AT) { mm = idx % BM; kk = idx / BM; }  // global contiguous in m
+        else    { kk = idx % BK; mm = idx / BK; }  // global contiguous in k
+        const int m = m0 + mm, k = k0 + kk;
+        if (k < p.K) {
+          if (m < p.M) cp_async4(&As[stage][kk][mm], AT ? A + int64_t(k) * p.lda + m : A + int64_t(m) * p.lda + k);
+          else if (m == p.M && p.ones_row) As[stage][kk][mm] = 1.0f;
+        }
+      }
+      for (int idx = threadIdx.x; idx < BN * BK; idx += 256) {
+        int nn, kk;
+        if (BT) { kk = idx % BK; nn = idx / BK; }
+        else    { nn = idx % BN; kk = idx / BN; }
+        const int n = n0 + nn, k = k0 + kk;
+        if (k < p.K && n < p.N)
+          cp_async4(&Bs[stage][kk][nn], BT ? B + int64_t(n) * p.ldb + k : B + int64_t(k) * p.ldb + n);
+      }
+    }
+    cp_async_commit();  // one group per tile slot, possibly empty
+  };
 
   float acc[TM][TN];
 #pragma unroll
@@ -50,62 +89,37 @@ __global__ void __launch_bounds__(256) k_gemm_tiled(GemmP p, const int* __restri
       acc[i][j] = v;
     }
 
-  for (int k0 = 0; k0 < p.K; k0 += BK) {
-    const int kmax = min(BK, p.K - k0);
-    for (int idx = threadIdx.x; idx < BM * BK; idx += 256) {
-      int mm, kk;
-      if (AT) { mm = idx % BM; kk = idx / BM; }  // contiguous in m
-      else    { kk = idx % BK; mm = idx / BK; }  // contiguous in k
-      const int m = m0 + mm, k = k0 + kk;
-      float v = 0.0f;
-      if (k < p.K) {
-        if (m < p.M) {
-          v = AT ? A[int64_t(k) * p.lda + m] : A[int64_t(m) * p.lda + k];
-          if (p.relu_a && v < 0.0f) v = 0.0f;
-        } else if (m == p.M && p.ones_row) {
-          v = 1.0f;
-        }
-      }
-      As[kk][mm] = v;
-    }
-    for (int idx = threadIdx.x; idx < BN * BK; idx += 256) {
-      int nn, kk;
-      if (BT) { kk = idx % BK; nn = idx / BK; }
-      else    { nn = idx % BN; kk = idx / BN; }
-      const int n = n0 + nn, k = k0 + kk;
-      float v = 0.0f;
-      if (k < p.K && n < p.N) v = BT ? B[int64_t(n) * p.ldb + k] : B[int64_t(k) * p.ldb + n];
-      Bs[kk][nn] = v;
-    }
+  const bool relu = p.relu_a != 0;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) load(s);
+  for (int tile = 0; tile < ntiles; ++tile) {
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
+    load(tile + STAGES - 1);  // refills the stage consumed in the previous iteration
+    const int stage = tile % STAGES;
+    const int kmax = min(BK, p.K - tile * BK);
+    auto body = [&](int kk) {
+      float a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        a[i] = As[stage][kk][ty + 16 * i];
+        if (relu && a[i] < 0.0f) a[i] = 0.0f;
+      }
+#pragma unroll
+      for (int j = 0; j < TN; ++j) b[j] = Bs[stage][kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = mac(acc[i][j], a[i], b[j]);
+    };
     if (kmax == BK) {
-#pragma unroll
-      for (int kk = 0; kk < BK; ++kk) {
-        float a[TM], b[TN];
-#pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = As[kk][ty + 16 * i];
-#pragma unroll
-        for (int j = 0; j < TN; ++j) b[j] = Bs[kk][tx + 16 * j];
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < TN; ++j) acc[i][j] = mac(acc[i][j], a[i], b[j]);
-      }
+#pragma unroll 8
+      for (int kk = 0; kk < BK; ++kk) body(kk);
     } else {
-      for (int kk = 0; kk < kmax; ++kk) {
-        float a[TM], b[TN];
-#pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = As[kk][ty + 16 * i];
-#pragma unroll
-        for (int j = 0; j < TN; ++j) b[j] = Bs[kk][tx + 16 * j];
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < TN; ++j) acc[i][j] = mac(acc[i][j], a[i], b[j]);
-      }
+      for (int kk = 0; kk < kmax; ++kk) body(kk);
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
 
 #pragma unroll
   for (int i = 0; i < TM; ++i)
@@ -120,60 +134,27 @@ __global__ void __launch_bounds__(256) k_gemm_tiled(GemmP p, const int* __restri
     }
 }
 
-// One output element per thread: the latency-optimal shape when a chunk has
-// few outputs and a long reduction (e.g. dWk: 17x64 outputs over R*T rows).
-template <bool AT, bool BT>
-__global__ void __launch_bounds__(256) k_gemm_rowdot(GemmP p, const int* __restrict__ active) {
-  const int c = active[blockIdx.z];
+template <bool AT, bool BT, int TM, int TN, int BK, int STAGES>
+void gemm_launch(const GemmP& p, const int* active, int n_active, cudaStream_t st) {
   const int Mx = p.M + (p.ones_row ? 1 : 0);
-  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= int64_t(Mx) * p.N) return;
-  const int m = int(idx / p.N), n = int(idx % p.N);
-  const float* A = p.A + c * p.a_cs;
-  const float* B = p.B + c * p.b_cs;
-  float* C = p.C + c * p.c_cs;
-  float acc = 0.0f;
-  if (p.init == 1) acc = p.bias[c * p.bias_cs + n];
-  else if (p.init == 2) acc = C[int64_t(m) * p.ldc + n];
-  const bool ones = (m == p.M);
-  const float* bp = BT ? B + int64_t(n) * p.ldb : B + n;
-  const int64_t bstep = BT ? 1 : p.ldb;
-  if (ones) {
-#pragma unroll 8
-    for (int k = 0; k < p.K; ++k) acc = fadd(acc, bp[k * bstep]);  // 1.0f*b == b exactly
-  } else {
-    const float* ap = AT ? A + m : A + int64_t(m) * p.lda;
-    const int64_t astep = AT ? p.lda : 1;
-    if (p.relu_a) {
-#pragma unroll 8
-      for (int k = 0; k < p.K; ++k) {
-        float a = ap[k * astep];
-        if (a < 0.0f) a = 0.0f;
-        acc = mac(acc, a, bp[k * bstep]);
-      }
-    } else {
-#pragma unroll 8
-      for (int k = 0; k < p.K; ++k) acc = mac(acc, ap[k * astep], bp[k * bstep]);
-    }
-  }
-  if (p.mask && p.mask[c * p.mask_cs + int64_t(m) * p.ldm + n] <= 0.0f) acc = 0.0f;
-  C[int64_t(m) * p.ldc + n] = acc;
+  dim3 grid((p.N + 16 * TN - 1) / (16 * TN), (Mx + 16 * TM - 1) / (16 * TM), n_active);
+  k_gemm_tiled<AT, BT, TM, TN, BK, STAGES><<<grid, 256, 0, st>>>(p, active);
 }
 
 template <bool AT, bool BT>
 void gemm_dispatch(const GemmP& p, const int* active, int n_active, cudaStream_t st) {
   const int Mx = p.M + (p.ones_row ? 1 : 0);
-  const int64_t outs = int64_t(Mx) * p.N;
-  // Tiled when the launch has enough 64x64 tiles to fill the chip twice;
-  // otherwise one output per thread (shortest dependent chain per SM).
-  const int64_t tiles = ((Mx + 63) / 64) * int64_t((p.N + 63) / 64) * n_active;
-  if (tiles >= 2 * 148 && p.N >= 32) {
-    dim3 grid((p.N + 63) / 64, (Mx + 63) / 64, n_active);
-    k_gemm_tiled<AT, BT, 4, 4><<<grid, 256, 0, st>>>(p, active);
-  } else {
-    dim3 grid(unsigned((outs + 255) / 256), 1, n_active);
-    k_gemm_rowdot<AT, BT><<<grid, 256, 0, st>>>(p, active);
-  }
+  auto blocks = [&](int tm, int tn) {
+    return int64_t((p.N + 16 * tn - 1) / (16 * tn)) * ((Mx + 16 * tm - 1) / (16 * tm)) * n_active;
+  };
+  // largest tile that still gives every SM at least two blocks
+  constexpr int64_t kFill = 2 * 148;
+  if (blocks(4, 4) >= kFill && p.N >= 48 && Mx >= 48)
+    gemm_launch<AT, BT, 4, 4, 32, 2>(p, active, n_active, st);
+  else if (blocks(2, 2) >= kFill && p.N >= 24 && Mx >= 24)
+    gemm_launch<AT, BT, 2, 2, 32, 3>(p, active, n_active, st);
+  else
+    gemm_launch<AT, BT, 1, 1, 64, 4>(p, active, n_active, st);
 }
 
 // ------------------------------------------------------------------ embed
@@ -302,8 +283,17 @@ __global__ void k_attn_bwd(const float* __restrict__ q, const float* __restrict_
 }
 
 // ------------------------------------------------------------------ embed bwd
-// pos grad: thread per (t, j), ascending rows. emb grad: warp per token value,
-// positions visited in (r,t) row-major order via 32-wide ballots, lanes = j.
+// pos grad: thread per (t, j), ascending rows, loads issued 16 rows ahead of
+// the dependent adds. emb grad: warp per token value, lanes = j; positions are
+// visited in (r,t) row-major order: a segment of ctx is staged in shared
+// memory, each warp ballots its hits into a shared list, then walks the list
+// with 16 independent dx loads in flight per batch.
+__device__ __forceinline__ float dx_at(const float* xp, const float* lp, int64_t pp, int j, int T, int E) {
+  float v = xp[pp * E + j];
+  if (int(pp % T) == T - 1) v = fadd(v, lp[(pp / T) * E + j]);  // dx[:,last,:] += dxl (layers.cpp:521)
+  return v;
+}
+
 __global__ void k_pos_bwd(const float* __restrict__ dx, int64_t dx_cs, const float* __restrict__ dxl,
                           int64_t dxl_cs, float* grads, int64_t g_cs, int64_t off_pos, DmDims d,
                           const int* __restrict__ active) {
@@ -316,56 +306,88 @@ __global__ void k_pos_bwd(const float* __restrict__ dx, int64_t dx_cs, const flo
   const float* xp = dx + c * dx_cs + int64_t(t) * d.E + j;
   const float* lp = dxl + c * dxl_cs + j;
   const int64_t rs = int64_t(d.T) * d.E;
-  for (int r = 0; r < d.R; ++r) {
-    float v = xp[r * rs];
-    if (t == d.T - 1) v = fadd(v, lp[int64_t(r) * d.E]);  // dx[:,last,:] += dxl (layers.cpp:521)
-    acc = fadd(acc, v);
+  const bool last = t == d.T - 1;
+  constexpr int kB = 16;
+  for (int r0 = 0; r0 < d.R; r0 += kB) {
+    float v[kB];
+    const int cnt = min(kB, d.R - r0);
+#pragma unroll
+    for (int q = 0; q < kB; ++q)
+      if (q < cnt) {
+        v[q] = xp[(r0 + q) * rs];
+        if (last) v[q] = fadd(v[q], lp[int64_t(r0 + q) * d.E]);
+      }
+#pragma unroll
+    for (int q = 0; q < kB; ++q)
+      if (q < cnt) acc = fadd(acc, v[q]);
   }
   *g = acc;
 }
 
-__global__ void k_emb_bwd(const uint32_t* __restrict__ ctx, int64_t ctx_cs,
-                          const float* __restrict__ dx, int64_t dx_cs, const float* __restrict__ dxl,
-                          int64_t dxl_cs, float* grads, int64_t g_cs, int64_t off_emb, DmDims d,
-                          const int* __restrict__ active) {
+constexpr int kEmbWarps = 8;
+constexpr int kEmbSeg = 2048;
+
+__global__ void __launch_bounds__(kEmbWarps * 32) k_emb_bwd(
+    const uint32_t* __restrict__ ctx, int64_t ctx_cs, const float* __restrict__ dx, int64_t dx_cs,
+    const float* __restrict__ dxl, int64_t dxl_cs, float* grads, int64_t g_cs, int64_t off_emb,
+    DmDims d, const int* __restrict__ active) {
+  __shared__ uint32_t sctx[kEmbSeg];
+  __shared__ uint16_t hits[kEmbWarps][kEmbSeg];
   const int c = active[blockIdx.y];
-  const int tokv = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (tokv >= d.V) return;
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tokv = blockIdx.x * kEmbWarps + wl;
   const uint32_t* cp = ctx + c * ctx_cs;
   const float* xp = dx + c * dx_cs;
   const float* lp = dxl + c * dxl_cs;
-  float* g = grads + c * g_cs + off_emb + int64_t(tokv) * d.E;
-  constexpr int kMaxJ = 8;  // E <= 256 (scale >= 1 gives E <= 64)
+  const bool active_warp = tokv < d.V;
+  float* g = grads + c * g_cs + off_emb + int64_t(active_warp ? tokv : 0) * d.E;
+  constexpr int kMaxJ = 2;  // E = 64/scale <= 64
   float acc[kMaxJ];
   const int nj = (d.E + 31) / 32;
-  for (int q = 0; q < nj; ++q) {
+#pragma unroll
+  for (int q = 0; q < kMaxJ; ++q) {
     const int j = lane + 32 * q;
-    acc[q] = j < d.E ? g[j] : 0.0f;
+    acc[q] = (active_warp && q < nj && j < d.E) ? g[j] : 0.0f;
   }
   const int64_t RT = int64_t(d.R) * d.T;
-  for (int64_t p0 = 0; p0 < RT; p0 += 32) {
-    const int64_t p = p0 + lane;
-    const bool hit = p < RT && cp[p] == uint32_t(tokv);
-    uint32_t bal = __ballot_sync(0xffffffffu, hit);
-    while (bal) {
-      const int b = __ffs(bal) - 1;
-      bal &= bal - 1;
-      const int64_t pp = p0 + b;
-      const bool last = int(pp % d.T) == d.T - 1;
-      const int64_t r = pp / d.T;
-      for (int q = 0; q < nj; ++q) {
+  for (int64_t s0 = 0; s0 < RT; s0 += kEmbSeg) {
+    const int seg = int(RT - s0 < kEmbSeg ? RT - s0 : kEmbSeg);
+    __syncthreads();
+    for (int i = threadIdx.x; i < seg; i += kEmbWarps * 32) sctx[i] = cp[s0 + i];
+    __syncthreads();
+    if (!active_warp) continue;
+    int nh = 0;
+    for (int p0 = 0; p0 < seg; p0 += 32) {
+      const int p = p0 + lane;
+      const bool hit = p < seg && sctx[p] == uint32_t(tokv);
+      const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+      if (hit) hits[wl][nh + __popc(bal & ((1u << lane) - 1u))] = uint16_t(p);
+      nh += __popc(bal);
+    }
+    __syncwarp();
+    constexpr int kB = 16;
+    for (int h0 = 0; h0 < nh; h0 += kB) {
+      const int cnt = min(kB, nh - h0);
+#pragma unroll
+      for (int q = 0; q < kMaxJ; ++q) {
         const int j = lane + 32 * q;
-        if (j < d.E) {
-          float v = xp[pp * d.E + j];
-          if (last) v = fadd(v, lp[r * d.E + j]);
-          acc[q] = fadd(acc[q], v);
-        }
+        if (q >= nj || j >= d.E) break;
+        float v[kB];
+#pragma unroll
+        for (int b = 0; b < kB; ++b)
+          if (b < cnt) v[b] = dx_at(xp, lp, s0 + hits[wl][h0 + b], j, d.T, d.E);
+#pragma unroll
+        for (int b = 0; b < kB; ++b)
+          if (b < cnt) acc[q] = fadd(acc[q], v[b]);
       }
     }
+    __syncwarp();
   }
-  for (int q = 0; q < nj; ++q) {
+  if (!active_warp) return;
+#pragma unroll
+  for (int q = 0; q < kMaxJ; ++q) {
     const int j = lane + 32 * q;
-    if (j < d.E) g[j] = acc[q];
+    if (q < nj && j < d.E) g[j] = acc[q];
   }
 }
 
@@ -455,8 +477,8 @@ void launch_embed_bwd(const uint32_t* ctx, int64_t ctx_cs, const float* dx, int6
   if (n_active <= 0) return;
   dim3 g1(unsigned((d.T * d.E + 255) / 256), n_active);
   k_pos_bwd<<<g1, 256, 0, st>>>(dx, dx_cs, dxl, dxl_cs, grads, g_cs, off_pos, d, active);
-  dim3 g2(unsigned((int64_t(d.V) * 32 + 255) / 256), n_active);
-  k_emb_bwd<<<g2, 256, 0, st>>>(ctx, ctx_cs, dx, dx_cs, dxl, dxl_cs, grads, g_cs, off_emb, d,
+  dim3 g2(unsigned((d.V + kEmbWarps - 1) / kEmbWarps), n_active);
+  k_emb_bwd<<<g2, kEmbWarps * 32, 0, st>>>(ctx, ctx_cs, dx, dx_cs, dxl, dxl_cs, grads, g_cs, off_emb, d,
                                 active);
 }
 

@@ -103,24 +103,28 @@ struct MixP {
   AdamScalars* sc;
   int flags, R, V;
   int* err;
+  int probs_given;  // test hook: rows of `probs` are already distributions (no mix/softmax)
 };
 void launch_mix_quantize(const MixP& p, const int* active, int n_active, cudaStream_t st);
 
-// Backward-controller CE gradient: dlm = (probs - onehot(tgt)) * (1 - alpha)
-void launch_bc_dlm(const float* probs, const uint32_t* tokens, ChunkGeo geo, int64_t tick, int t,
-                   const float* params, int64_t p_cs, int64_t off_alpha, float* dlm, int64_t cs_p,
-                   int R, int V, const int* active, int n_active, cudaStream_t st);
-// d alpha (one sequential accumulator over rows then symbols, mixer.cpp:64-84),
-// alpha's Adam update, CE loss for early_loss_bits.
-struct AlphaP {
+// Backward-controller step (OnlineTrainer::step, mixer.cpp:57-97), split so
+// that only one tiny serial chain remains:
+//  * launch_bc_dlm: dlm = (probs - onehot(tgt)) * (1 - alpha) and, per
+//    element, the d(alpha) term g*(stat - lm) and per row the CE loss term;
+//  * launch_alpha_step: the single sequential d(alpha) accumulator over rows
+//    then symbols (mixer.cpp:70-84) read back in order from shared memory,
+//    alpha's Adam update, and the early-loss sum.
+struct BcP {
   const float* probs; const float* lu; const float* lr; const float* lm; int64_t cs_p;
   const uint32_t* tokens; ChunkGeo geo; int64_t tick; int t;
   float* w; float* m; float* v; int64_t p_cs; int64_t off_alpha;
+  float* dlm; float* aterm; float* lterm; int64_t cs_l;  // lterm stride per chunk
   const AdamScalars* sc;
   double* warm_loss; const uint64_t* warm_steps;
   int flags, R, V;
 };
-void launch_alpha_step(const AlphaP& p, const int* active, int n_active, cudaStream_t st);
+void launch_bc_dlm(const BcP& p, const int* active, int n_active, cudaStream_t st);
+void launch_alpha_step(const BcP& p, const int* active, int n_active, cudaStream_t st);
 
 // Range coder (coder.cpp:101-166): one thread per chunk, R symbols per step.
 struct CoderState { uint64_t low, range, pos, code; int err; int pad; };

@@ -79,8 +79,8 @@ class Checker:
         cap = 4096
         st = (ChunkStats * cap)() if with_stats else None
         nch = C.c_size_t()
-        self._check(self._f("compress")(raw, len(raw), C.byref(cfg), C.byref(out), C.byref(n),
-                                        st, cap if with_stats else 0, C.byref(nch)))
+        self._check(self._f("compress")(raw, C.c_size_t(len(raw)), C.byref(cfg), C.byref(out), C.byref(n),
+                                        st, C.c_size_t(cap if with_stats else 0), C.byref(nch)))
         data = self._take(out, n.value)
         if with_stats:
             return data, [st[i] for i in range(nch.value)]
@@ -91,9 +91,9 @@ class Checker:
         n = C.c_size_t()
         cap = 4096
         st = (ChunkStats * cap)() if with_stats else None
-        self._check(self._f("decompress")(blob, len(blob), pub_path.encode() if pub_path else None,
+        self._check(self._f("decompress")(blob, C.c_size_t(len(blob)), pub_path.encode() if pub_path else None,
                                           workers, C.byref(out), C.byref(n), st,
-                                          cap if with_stats else 0))
+                                          C.c_size_t(cap if with_stats else 0)))
         data = self._take(out, n.value)
         if with_stats:
             return data, st
@@ -135,7 +135,7 @@ class Checker:
         n = C.c_size_t()
         self._check(self._f("range_encode")(freqs.ctypes.data_as(C.c_void_p), freqs.shape[1],
                                             dist_of.ctypes.data_as(C.c_void_p),
-                                            syms.ctypes.data_as(C.c_void_p), len(syms),
+                                            syms.ctypes.data_as(C.c_void_p), C.c_size_t(len(syms)),
                                             C.byref(out), C.byref(n)))
         return self._take(out, n.value)
 
@@ -144,7 +144,7 @@ class Checker:
         x = np.ascontiguousarray(x, dtype=np.float32)
         y = np.zeros_like(x)
         self._check(self._f("det")(which, x.ctypes.data_as(C.c_void_p),
-                                   y.ctypes.data_as(C.c_void_p), len(x)))
+                                   y.ctypes.data_as(C.c_void_p), C.c_size_t(len(x))))
         return y
 
     def softmax(self, x):
@@ -152,7 +152,7 @@ class Checker:
         x = np.ascontiguousarray(x, dtype=np.float32)
         y = np.zeros_like(x)
         self._check(self._f("softmax")(x.ctypes.data_as(C.c_void_p),
-                                       y.ctypes.data_as(C.c_void_p), len(x)))
+                                       y.ctypes.data_as(C.c_void_p), C.c_size_t(len(x))))
         return y
 
     def bigru_predict(self, path: str, ctx, vocab: int):
@@ -179,7 +179,7 @@ class Checker:
         self._check(self._f("dump_chunk")(
             tokens.ctypes.data_as(C.c_void_p), C.c_uint64(len(tokens)), flags,
             pub_path.encode() if pub_path else None, k, t, bs, scale, C.c_uint64(dm_seed),
-            inbound, len(inbound), probs.ctypes.data_as(C.c_void_p), C.c_uint64(max_steps),
+            inbound, C.c_size_t(len(inbound)), probs.ctypes.data_as(C.c_void_p), C.c_uint64(max_steps),
             C.byref(pay), C.byref(pn), C.byref(sn), C.byref(snn)))
         return self._take(pay, pn.value), self._take(sn, snn.value), probs[:max_steps]
 
