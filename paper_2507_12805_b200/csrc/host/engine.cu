@@ -247,6 +247,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   }
 
   // ---- tapes (one per chunk that ever steps)
+  const int64_t RT = int64_t(R) * T;
   const int64_t s_ctx = int64_t(R) * T, s_x = int64_t(R) * T * E, s_kv = int64_t(R) * T * H,
                 s_rh = int64_t(R) * H, s_w = int64_t(R) * NH * T, s_rf = int64_t(R) * F,
                 s_rv = int64_t(R) * V, s_cum = int64_t(R) * (V + 1), s_re = int64_t(R) * E;
@@ -257,7 +258,8 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   DBuf<float> x(TW * s_x), kk(TW * s_kv), vv(TW * s_kv), q(TW * s_rh), wts(TW * s_w),
       cx(TW * s_rh), ao(TW * s_rh), pre(TW * s_rf), fo(TW * s_rh), lm(TW * s_rv),
       probs(TW * s_rv), dlm(TW * s_rv), aterm(TW * s_rv), lterm(TW * R), dffn(TW * s_rh), dact(TW * s_rf), datt(TW * s_rh),
-      dctx(TW * s_rh), dq(TW * s_rh), dk(TW * s_kv), dv(TW * s_kv), dx(TW * s_x), dxl(TW * s_re);
+      dctx(TW * s_rh), dq(TW * s_rh), dk(TW * s_kv), dv(TW * s_kv), dx(TW * s_x), dxl(TW * s_re),
+      xl(TW * s_re);
   DBuf<float> lu((run.flags & 1) ? TW * s_rv : 0), lr((run.flags & 2) ? TW * s_rv : 0);
   int64_t s_bw = 0;
   DBuf<float> bwork;
@@ -293,12 +295,23 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   DBuf<double> warm_loss(W);
   warm_loss.zero(st);
 
-  // ---- schedule lists
+  // ---- schedule lists (CSR per tick) + the device tick descriptor
   DBuf<int> d_act(std::max<size_t>(sch.act.size(), 1));
   if (!sch.act.empty()) d_act.upload(reinterpret_cast<const int*>(sch.act.data()), sch.act.size(), st);
   DBuf<int2> d_hand(std::max<size_t>(sch.hand.size() / 2, 1));
   if (!sch.hand.empty())
     d_hand.upload(reinterpret_cast<const int2*>(sch.hand.data()), sch.hand.size() / 2, st);
+  DBuf<uint32_t> d_act_ptr(sch.act_ptr.size()), d_hand_ptr(sch.hand_ptr.size());
+  d_act_ptr.upload(sch.act_ptr.data(), sch.act_ptr.size(), st);
+  d_hand_ptr.upload(sch.hand_ptr.data(), sch.hand_ptr.size(), st);
+  uint32_t max_hand = 0;
+  for (size_t t = 0; t + 1 < sch.hand_ptr.size(); ++t)
+    max_hand = std::max(max_hand, sch.hand_ptr[t + 1] - sch.hand_ptr[t]);
+  DBuf<TickDesc> d_td(1);
+  {
+    const TickDesc td0{-1, nullptr, nullptr, 0, 0};
+    d_td.upload(&td0, 1, st);
+  }
 
   // snapshot hashes for stats: key (src, steps)
   std::map<std::pair<int64_t, uint64_t>, uint64_t> snap_hash;
@@ -350,35 +363,41 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   auto W_ = [&](DmLayout::Id i) { return w.p + lay.off(i); };
   auto G_ = [&](DmLayout::Id i) { return g.p + lay.off(i); };
 
-  for (int64_t tick = 0; tick < sch.ticks; ++tick) {
-    snapshots_for_tick(tick);
-    const uint32_t h0 = sch.hand_ptr[size_t(tick)], h1 = sch.hand_ptr[size_t(tick) + 1];
-    if (h1 > h0) {
-      launch_state_copy(w.p, m.p, v.p, sc.p, P, P, d_hand.p + h0, int(h1 - h0), st);
+  // One tick = one coded batch step of every active chunk. The sequence is
+  // fixed (grids sized for the schedule's max concurrency, surplus blocks
+  // exit), so it is captured once into a CUDA graph and replayed per tick.
+  const int na = int(std::max<uint32_t>(sch.max_active, 1));
+  const int nh = int(max_hand);
+  const TickDesc* act = d_td.p;
+  uint64_t tick_launches = 0;
+  auto enqueue_tick = [&](int64_t probe_tick) {
+    const uint64_t l0 = run.launches;
+    launch_tick_advance(d_td.p, d_act_ptr.p, d_act.p, d_hand_ptr.p, d_hand.p, sch.ticks, st);
+    ++run.launches;
+    if (nh > 0) {
+      launch_state_copy(w.p, m.p, v.p, sc.p, P, P, d_td.p, nh, st);
       ++run.launches;
     }
-    const uint32_t a0 = sch.act_ptr[size_t(tick)], a1 = sch.act_ptr[size_t(tick) + 1];
-    const int na = int(a1 - a0);
-    if (na == 0) continue;
-    const int* act = d_act.p + a0;
     auto gemm = [&](GemmP p, bool at, bool bt) {
       launch_gemm(p, at, bt, act, na, st);
       ++run.launches;
     };
     // ---------------- forward (AttentionModel::forward, models.cpp:122-136)
-    launch_embed(d_tokens, geo, tick, w.p, P, oE, oP, ctx.p, s_ctx, x.p, s_x, dd, act, na, st);
+    launch_embed(d_tokens, geo, w.p, P, oE, oP, ctx.p, s_ctx, x.p, s_x, xl.p, s_re, dd, act, na,
+                 st);
     ++run.launches;
     GemmP gp{};
     // K, V over all R*T rows, q over the last position (layers.cpp:437-445)
-    gp = GemmP{x.p, s_x, E, W_(DmLayout::KW), P, H, kk.p, s_kv, H, W_(DmLayout::KB), P,
+    // x is feature-major: A(row, e) = xT[e*RT + row]
+    gp = GemmP{x.p, s_x, RT, W_(DmLayout::KW), P, H, kk.p, s_kv, H, W_(DmLayout::KB), P,
                nullptr, 0, 0, R * T, H, E, 0, 1, 0};
-    gemm(gp, false, false);
+    gemm(gp, true, false);
     gp.B = W_(DmLayout::VW);
     gp.bias = W_(DmLayout::VB);
     gp.C = vv.p;
-    gemm(gp, false, false);
-    gp = GemmP{x.p + int64_t(T - 1) * E, s_x, int64_t(T) * E, W_(DmLayout::QW), P, H, q.p, s_rh, H,
-               W_(DmLayout::QB), P, nullptr, 0, 0, R, H, E, 0, 1, 0};
+    gemm(gp, true, false);
+    gp = GemmP{xl.p, s_re, E, W_(DmLayout::QW), P, H, q.p, s_rh, H, W_(DmLayout::QB), P, nullptr, 0,
+               0, R, H, E, 0, 1, 0};
     gemm(gp, false, false);
     launch_attn_fwd(q.p, kk.p, vv.p, wts.p, cx.p, s_rh, s_kv, s_w, dd, inv_hd, act, na, st);
     ++run.launches;
@@ -408,9 +427,9 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
             int(run.flags), R, V, err.p};
     launch_mix_quantize(mp, act, na, st);
     ++run.launches;
-    if (run.opt && run.opt->probe && run.opt->probe_chunk >= 0) {
+    if (probe_tick >= 0) {
       const int64_t pc = run.opt->probe_chunk;
-      const int64_t ms = tick - sch.offset[size_t(pc)];
+      const int64_t ms = probe_tick - sch.offset[size_t(pc)];
       if (sch.M[size_t(pc)] && ms >= 0 && uint64_t(ms) < sch.M[size_t(pc)] &&
           uint64_t(ms) < run.opt->probe_steps) {
         std::vector<float>& pr = *run.opt->probe;
@@ -418,11 +437,11 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
                            cudaMemcpyDeviceToHost, st));
       }
     }
-    launch_range_step(d_tokens, geo, tick, int(run.t), R, V, freq.p, cum.p, s_rv, s_cum, payload.p,
+    launch_range_step(d_tokens, geo, int(run.t), R, V, freq.p, cum.p, s_rv, s_cum, payload.p,
                       d_pay_off.p, d_pay_len.p, cstate.p, act, na, run.decode, st);
     ++run.launches;
     // ---------------- backward controller (OnlineTrainer::step, mixer.cpp:57-97)
-    BcP bp{probs.p, lu.p, lr.p, lm.p, s_rv, d_tokens, geo, tick, int(run.t), w.p, m.p, v.p, P, oA,
+    BcP bp{probs.p, lu.p, lr.p, lm.p, s_rv, d_tokens, geo, d_td.p, int(run.t), w.p, m.p, v.p, P, oA,
            dlm.p, aterm.p, lterm.p, R, sc.p, warm_loss.p, d_warm.p, int(run.flags), R, V};
     launch_bc_dlm(bp, act, na, st);
     launch_alpha_step(bp, act, na, st);
@@ -456,21 +475,25 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
                     act, na, st);
     ++run.launches;
     // q/k/v projections: weight+bias grads, then dx = dk Wk^T + dv Wv^T, dxl = dq Wq^T
-    gemm(GemmP{x.p, s_x, E, dk.p, s_kv, H, G_(DmLayout::KW), P, H, nullptr, 0, nullptr, 0, 0, E, H,
-               R * T, 1, 2, 0},
+    // dWk|dbk and dWv|dbv: reductions over all R*T rows of feature-major x, dk, dv
+    {
+      const NtP pk{x.p, dk.p, G_(DmLayout::KW), s_x, s_kv, P, RT, RT, H, E, H, int(RT)};
+      NtP pv = pk;
+      pv.B = dv.p;
+      pv.C = G_(DmLayout::VW);
+      launch_gemm_nt(pk, &pv, act, na, st);
+      ++run.launches;
+    }
+    gemm(GemmP{xl.p, s_re, E, dq.p, s_rh, H, G_(DmLayout::QW), P, H, nullptr, 0, nullptr, 0, 0, E,
+               H, R, 1, 2, 0},
          true, false);
-    gemm(GemmP{x.p, s_x, E, dv.p, s_kv, H, G_(DmLayout::VW), P, H, nullptr, 0, nullptr, 0, 0, E, H,
-               R * T, 1, 2, 0},
-         true, false);
-    gemm(GemmP{x.p + int64_t(T - 1) * E, s_x, int64_t(T) * E, dq.p, s_rh, H, G_(DmLayout::QW), P, H,
-               nullptr, 0, nullptr, 0, 0, E, H, R, 1, 2, 0},
-         true, false);
-    gemm(GemmP{dk.p, s_kv, H, W_(DmLayout::KW), P, H, dx.p, s_x, E, nullptr, 0, nullptr, 0, 0,
+    // dx = dk Wk^T + dv Wv^T (k terms then v terms), dk/dv feature-major
+    gemm(GemmP{dk.p, s_kv, RT, W_(DmLayout::KW), P, H, dx.p, s_x, E, nullptr, 0, nullptr, 0, 0,
                R * T, E, H, 0, 0, 0},
-         false, true);
-    gemm(GemmP{dv.p, s_kv, H, W_(DmLayout::VW), P, H, dx.p, s_x, E, nullptr, 0, nullptr, 0, 0,
+         true, true);
+    gemm(GemmP{dv.p, s_kv, RT, W_(DmLayout::VW), P, H, dx.p, s_x, E, nullptr, 0, nullptr, 0, 0,
                R * T, E, H, 0, 2, 0},
-         false, true);
+         true, true);
     gemm(GemmP{dq.p, s_rh, H, W_(DmLayout::QW), P, H, dxl.p, s_re, E, nullptr, 0, nullptr, 0, 0, R,
                E, H, 0, 0, 0},
          false, true);
@@ -480,6 +503,28 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     launch_adam(w.p, g.p, m.p, v.p, P, P - 1, sc.p, act, na, st);
     ++run.launches;
     check_launch();
+    tick_launches = run.launches - l0;
+  };
+
+  const bool probing = run.opt && run.opt->probe && run.opt->probe_chunk >= 0;
+  const bool host_sync = probing || want_stats;
+  if (sch.ticks > 0 && !host_sync) {
+    // capture one tick, replay it sch.ticks times
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    enqueue_tick(-1);
+    CK(cudaStreamEndCapture(st, &graph));
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    for (int64_t tick = 0; tick < sch.ticks; ++tick) CK(cudaGraphLaunch(exec, st));
+    run.launches += tick_launches * uint64_t(sch.ticks - 1);
+    CK(cudaGraphExecDestroy(exec));
+    CK(cudaGraphDestroy(graph));
+  } else {
+    for (int64_t tick = 0; tick < sch.ticks; ++tick) {
+      snapshots_for_tick(tick);
+      enqueue_tick(probing ? tick : -1);
+    }
   }
   snapshots_for_tick(sch.ticks);
   if (!run.decode) {
@@ -956,8 +1001,13 @@ std::vector<uint32_t> quantize_rows(const float* probs, uint64_t rows, uint32_t 
   DBuf<float> pr(cs + 1);
   DBuf<uint32_t> fq(cs + 1), cm(rows * (width + 1) + 1);
   DBuf<int> err(1), act(1);
+  DBuf<TickDesc> td(1);
   err.zero(st);
   act.zero(st);
+  {
+    const TickDesc t0{0, act.p, nullptr, 1, 0};
+    td.upload(&t0, 1, st);
+  }
   pr.upload(probs, cs, st);
   MixP mp{};
   mp.probs = pr.p;
@@ -967,7 +1017,7 @@ std::vector<uint32_t> quantize_rows(const float* probs, uint64_t rows, uint32_t 
   mp.V = int(width);
   mp.err = err.p;
   mp.probs_given = 1;
-  launch_mix_quantize(mp, act.p, 1, st);
+  launch_mix_quantize(mp, td.p, 1, st);
   check_launch();
   std::vector<uint32_t> out(cs);
   int h_err = 0;

@@ -31,10 +31,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_bigru_layer(BiGruP p, int l, co
                                                              int64_t ctx_cs, const float* in_buf,
                                                              float* out_buf, float* fin,
                                                              int64_t work_cs,
-                                                             const int* __restrict__ active) {
+                                                             const TickDesc* __restrict__ td) {
   __shared__ float sx[kWarps][kMaxIn];
   __shared__ float sh[kWarps][kMaxH];
-  const int c = active[blockIdx.y];
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wg = blockIdx.x * kWarps + wl;
   if (wg >= p.R * 2) return;
@@ -91,8 +92,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_bigru_layer(BiGruP p, int l, co
 
 // bott = tanh(bott.b + fin . bott.w); one thread per (row, unit)
 __global__ void k_bigru_bott(BiGruP p, const float* fin, float* bact, int64_t work_cs,
-                             const int* __restrict__ active) {
-  const int c = active[blockIdx.y];
+                             const TickDesc* __restrict__ td) {
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= p.R * p.B) return;
   const int r = idx / p.B, j = idx % p.B, K = 2 * p.Hs;
@@ -106,8 +108,9 @@ __global__ void k_bigru_bott(BiGruP p, const float* fin, float* bact, int64_t wo
 
 // logits = out.b + bott . out.w
 __global__ void k_bigru_out(BiGruP p, const float* bact, int64_t work_cs, float* logits,
-                            int64_t lg_cs, const int* __restrict__ active) {
-  const int c = active[blockIdx.y];
+                            int64_t lg_cs, const TickDesc* __restrict__ td) {
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= p.R * p.V) return;
   const int r = idx / p.V, v = idx % p.V;
@@ -127,23 +130,23 @@ size_t bigru_work_floats(const BiGruP& p) {
 }
 
 void launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, float* work,
-                          int64_t work_cs, float* logits, int64_t lg_cs, const int* active,
-                          int n_active, cudaStream_t st) {
-  if (n_active <= 0) return;
+                          int64_t work_cs, float* logits, int64_t lg_cs, const TickDesc* td,
+                          int max_active, cudaStream_t st) {
+  if (max_active <= 0) return;
   const int64_t layer_sz = int64_t(p.R) * p.T * 2 * p.Hs;
   float* buf[2] = {work, work + layer_sz};
   float* fin = work + 2 * layer_sz;
   float* bact = fin + int64_t(p.R) * 2 * p.Hs;
-  dim3 grid(unsigned((p.R * 2 + kWarps - 1) / kWarps), n_active);
+  dim3 grid(unsigned((p.R * 2 + kWarps - 1) / kWarps), max_active);
   for (int l = 0; l < p.layers; ++l) {
     const float* in = l == 0 ? nullptr : buf[(l - 1) & 1];
     k_bigru_layer<<<grid, kWarps * 32, 0, st>>>(p, l, ctx, ctx_cs, in, buf[l & 1],
-                                                l == p.layers - 1 ? fin : nullptr, work_cs, active);
+                                                l == p.layers - 1 ? fin : nullptr, work_cs, td);
   }
-  dim3 g2(unsigned((p.R * p.B + 255) / 256), n_active);
-  k_bigru_bott<<<g2, 256, 0, st>>>(p, fin, bact, work_cs, active);
-  dim3 g3(unsigned((p.R * p.V + 255) / 256), n_active);
-  k_bigru_out<<<g3, 256, 0, st>>>(p, bact, work_cs, logits, lg_cs, active);
+  dim3 g2(unsigned((p.R * p.B + 255) / 256), max_active);
+  k_bigru_bott<<<g2, 256, 0, st>>>(p, fin, bact, work_cs, td);
+  dim3 g3(unsigned((p.R * p.V + 255) / 256), max_active);
+  k_bigru_out<<<g3, 256, 0, st>>>(p, bact, work_cs, logits, lg_cs, td);
 }
 
 }  // namespace pmklc_b200

@@ -36,8 +36,9 @@ __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t x) {
   return x;
 }
 
-__global__ void k_mix_quantize(MixP p, const int* __restrict__ active) {
-  const int c = active[blockIdx.y];
+__global__ void k_mix_quantize(MixP p, const TickDesc* __restrict__ td) {
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (blockIdx.x == 0 && threadIdx.x == 0 && p.sc) {  // Adam::step scalar prologue (adam.cpp:23-27)
     AdamScalars s = p.sc[c];
@@ -192,13 +193,14 @@ __global__ void k_mix_quantize(MixP p, const int* __restrict__ active) {
   if (lane == 0) cm[V] = carry;
 }
 
-__global__ void k_bc_dlm(BcP p, const int* __restrict__ active) {
-  const int c = active[blockIdx.y];
+__global__ void k_bc_dlm(BcP p, const TickDesc* __restrict__ td) {
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int R = p.R, V = p.V;
   if (idx >= int64_t(R) * V) return;
   const int r = int(idx / V), i = int(idx % V);
-  const uint64_t jstep = uint64_t(p.t) + uint64_t(p.tick - p.geo.offset[c]);
+  const uint64_t jstep = uint64_t(p.t) + uint64_t(p.td->tick - p.geo.offset[c]);
   const uint32_t tgt = p.tokens[p.geo.start[c] + uint64_t(r) * p.geo.L[c] + jstep];
   const float a = det_sigmoid(p.w[c * p.p_cs + p.off_alpha]);
   const int64_t o = c * p.cs_p + idx;
@@ -219,9 +221,10 @@ __global__ void k_bc_dlm(BcP p, const int* __restrict__ active) {
 // while the other warps stage the next batch of terms (double buffer); warp
 // 1 lane 0 runs the (short) loss chain.
 constexpr int kAlphaBatch = 4096;
-__global__ void __launch_bounds__(256) k_alpha_step(BcP p, const int* __restrict__ active) {
+__global__ void __launch_bounds__(256) k_alpha_step(BcP p, const TickDesc* __restrict__ td) {
   __shared__ __align__(16) float buf[2][kAlphaBatch];
-  const int c = active[blockIdx.x];
+  if (blockIdx.x >= unsigned(p.td->n_act)) return;
+  const int c = p.td->act[blockIdx.x];
   const int64_t n = int64_t(p.R) * p.V;
   const float* terms = p.aterm + c * p.cs_p;
   const int nb = int((n + kAlphaBatch - 1) / kAlphaBatch);
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(256) k_alpha_step(BcP p, const int* __restrict
     }
     __syncthreads();
   }
-  const uint64_t mstep = uint64_t(p.tick - p.geo.offset[c]);
+  const uint64_t mstep = uint64_t(p.td->tick - p.geo.offset[c]);
   if (tid == 32 && p.warm_loss && mstep < p.warm_steps[c]) {
     const float* lt = p.lterm + c * p.cs_l;
     float loss = 0.0f;
@@ -389,17 +392,17 @@ __global__ void k_range_uniform(uint32_t* tokens, ChunkGeo geo, int t, int R, in
 constexpr int kCoderWarps = 4;
 constexpr int kMaxQ = 8;  // V <= 256 in registers; larger V uses the scalar search
 __global__ void __launch_bounds__(kCoderWarps * 32) k_range_step(
-    uint32_t* tokens, ChunkGeo geo, int64_t tick, int t, int R, int V,
+    uint32_t* tokens, ChunkGeo geo, int t, int R, int V,
     const uint32_t* __restrict__ freq, const uint32_t* __restrict__ cum, int64_t cs_f,
     int64_t cs_c, uint8_t* payload, const uint64_t* pay_off, const uint64_t* pay_len,
-    CoderState* cs, const int* __restrict__ active, int n_active, bool decode) {
+    CoderState* cs, const TickDesc* __restrict__ td, bool decode) {
   __shared__ uint32_t sc_[kCoderWarps][32], sf_[kCoderWarps][32];
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wi = blockIdx.x * kCoderWarps + wl;
-  if (wi >= n_active) return;
-  const int c = active[wi];
+  if (wi >= td->n_act) return;
+  const int c = td->act[wi];
   const uint64_t L = geo.L[c], start = geo.start[c];
-  const uint64_t jstep = uint64_t(t) + uint64_t(tick - geo.offset[c]);
+  const uint64_t jstep = uint64_t(t) + uint64_t(td->tick - geo.offset[c]);
   uint8_t* buf = payload + pay_off[c];
   CoderState s = cs[c];
   if (s.err) return;
@@ -495,21 +498,21 @@ __global__ void k_range_finish(uint8_t* payload, const uint64_t* pay_off, CoderS
 
 }  // namespace
 
-void launch_mix_quantize(const MixP& p, const int* active, int n_active, cudaStream_t st) {
-  if (n_active <= 0) return;
-  dim3 grid(unsigned((int64_t(p.R) * 32 + 255) / 256), n_active);
-  k_mix_quantize<<<grid, 256, 0, st>>>(p, active);
+void launch_mix_quantize(const MixP& p, const TickDesc* td, int max_active, cudaStream_t st) {
+  if (max_active <= 0) return;
+  dim3 grid(unsigned((int64_t(p.R) * 32 + 255) / 256), max_active);
+  k_mix_quantize<<<grid, 256, 0, st>>>(p, td);
 }
 
-void launch_bc_dlm(const BcP& p, const int* active, int n_active, cudaStream_t st) {
-  if (n_active <= 0) return;
-  dim3 grid(unsigned((int64_t(p.R) * p.V + 255) / 256), n_active);
-  k_bc_dlm<<<grid, 256, 0, st>>>(p, active);
+void launch_bc_dlm(const BcP& p, const TickDesc* td, int max_active, cudaStream_t st) {
+  if (max_active <= 0) return;
+  dim3 grid(unsigned((int64_t(p.R) * p.V + 255) / 256), max_active);
+  k_bc_dlm<<<grid, 256, 0, st>>>(p, td);
 }
 
-void launch_alpha_step(const BcP& p, const int* active, int n_active, cudaStream_t st) {
-  if (n_active <= 0) return;
-  k_alpha_step<<<unsigned(n_active), 256, 0, st>>>(p, active);
+void launch_alpha_step(const BcP& p, const TickDesc* td, int max_active, cudaStream_t st) {
+  if (max_active <= 0) return;
+  k_alpha_step<<<unsigned(max_active), 256, 0, st>>>(p, td);
 }
 
 void launch_range_uniform(uint32_t* tokens, ChunkGeo geo, int t, int R, int V, uint8_t* payload,
@@ -521,15 +524,15 @@ void launch_range_uniform(uint32_t* tokens, ChunkGeo geo, int t, int R, int V, u
                                                                  decode);
 }
 
-void launch_range_step(uint32_t* tokens, ChunkGeo geo, int64_t tick, int t, int R, int V,
+void launch_range_step(uint32_t* tokens, ChunkGeo geo, int t, int R, int V,
                        const uint32_t* freq, const uint32_t* cum, int64_t cs_f, int64_t cs_c,
                        uint8_t* payload, const uint64_t* pay_off, const uint64_t* pay_len,
-                       CoderState* cs, const int* active, int n_active, bool decode,
+                       CoderState* cs, const TickDesc* td, int max_active, bool decode,
                        cudaStream_t st) {
-  if (n_active <= 0) return;
-  k_range_step<<<unsigned((n_active + kCoderWarps - 1) / kCoderWarps), kCoderWarps * 32, 0, st>>>(tokens, geo, tick, t, R, V, freq, cum,
+  if (max_active <= 0) return;
+  k_range_step<<<unsigned((max_active + kCoderWarps - 1) / kCoderWarps), kCoderWarps * 32, 0, st>>>(tokens, geo, t, R, V, freq, cum,
                                                               cs_f, cs_c, payload, pay_off, pay_len,
-                                                              cs, active, n_active, decode);
+                                                              cs, td, decode);
 }
 
 void launch_range_finish(uint8_t* payload, const uint64_t* pay_off, CoderState* cs, int n_chunks,

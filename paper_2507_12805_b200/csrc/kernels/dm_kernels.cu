@@ -9,6 +9,7 @@
 // FP32 SIMT pipe rather than tcgen05: tensor-core accumulation order is
 // unspecified, and the decoder must replay the encoder's online training bit
 // for bit.
+#include <algorithm>
 #include <cstdint>
 
 #include "detmath.cuh"
@@ -36,24 +37,25 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <bool AT, bool BT, int TM, int TN, int BK, int STAGES>
-__global__ void __launch_bounds__(256) k_gemm_tiled(GemmP p, const int* __restrict__ active) {
-  constexpr int BM = 16 * TM, BN = 16 * TN;
-  __shared__ float As[STAGES][BK][BM + 4];
-  __shared__ float Bs[STAGES][BK][BN + 4];
-  const int c = active[blockIdx.z];
+template <bool AT, bool BT, int TM, int TN, int BK, int STAGES, int TX, int TY>
+__global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc* __restrict__ td) {
+  constexpr int NT = TX * TY, BM = TY * TM, BN = TX * TN;
+  __shared__ __align__(16) float As[STAGES][BK][BM + 4];
+  __shared__ __align__(16) float Bs[STAGES][BK][BN + 4];
+  if (blockIdx.z >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.z];
   const float* A = p.A + c * p.a_cs;
   const float* B = p.B + c * p.b_cs;
   float* C = p.C + c * p.c_cs;
   const int Mx = p.M + (p.ones_row ? 1 : 0);
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int ntiles = (p.K + BK - 1) / BK;
 
   auto load = [&](int tile) {
     if (tile < ntiles) {
       const int stage = tile % STAGES, k0 = tile * BK;
-      for (int idx = threadIdx.x; idx < BM * BK; idx += 256) {
+      for (int idx = threadIdx.x; idx < BM * BK; idx += NT) {
         int mm, kk;
         if (AT) { mm = idx % BM; kk = idx / BM; }  // global contiguous in m
         else    { kk = idx % BK; mm = idx / BK; }  // global contiguous in k
@@ -63,7 +65,7 @@ __global__ void __launch_bounds__(256) k_gemm_tiled(GemmP p, const int* __restri
           else if (m == p.M && p.ones_row) As[stage][kk][mm] = 1.0f;
         }
       }
-      for (int idx = threadIdx.x; idx < BN * BK; idx += 256) {
+      for (int idx = threadIdx.x; idx < BN * BK; idx += NT) {
         int nn, kk;
         if (BT) { kk = idx % BK; nn = idx / BK; }
         else    { nn = idx % BN; kk = idx / BN; }
@@ -80,7 +82,7 @@ __global__ void __launch_bounds__(256) k_gemm_tiled(GemmP p, const int* __restri
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
-      const int m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
+      const int m = m0 + ty * TM + i, n = n0 + tx * TN + j;
       float v = 0.0f;
       if (m < Mx && n < p.N) {
         if (p.init == 1) v = p.bias[c * p.bias_cs + n];
@@ -99,14 +101,34 @@ __global__ void __launch_bounds__(256) k_gemm_tiled(GemmP p, const int* __restri
     const int stage = tile % STAGES;
     const int kmax = min(BK, p.K - tile * BK);
     auto body = [&](int kk) {
+      // each thread's TM (TN) operands are contiguous: one vector shared load each
       float a[TM], b[TN];
+      const float* ap = &As[stage][kk][ty * TM];
+      const float* bp = &Bs[stage][kk][tx * TN];
+      if constexpr (TM == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(ap);
+        a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
+      } else if constexpr (TM == 2) {
+        const float2 v = *reinterpret_cast<const float2*>(ap);
+        a[0] = v.x; a[1] = v.y;
+      } else {
 #pragma unroll
-      for (int i = 0; i < TM; ++i) {
-        a[i] = As[stage][kk][ty + 16 * i];
-        if (relu && a[i] < 0.0f) a[i] = 0.0f;
+        for (int i = 0; i < TM; ++i) a[i] = ap[i];
       }
+      if constexpr (TN == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(bp);
+        b[0] = v.x; b[1] = v.y; b[2] = v.z; b[3] = v.w;
+      } else if constexpr (TN == 2) {
+        const float2 v = *reinterpret_cast<const float2*>(bp);
+        b[0] = v.x; b[1] = v.y;
+      } else {
 #pragma unroll
-      for (int j = 0; j < TN; ++j) b[j] = Bs[stage][kk][tx + 16 * j];
+        for (int j = 0; j < TN; ++j) b[j] = bp[j];
+      }
+      if (relu) {
+#pragma unroll
+        for (int i = 0; i < TM; ++i) a[i] = a[i] < 0.0f ? 0.0f : a[i];
+      }
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -125,7 +147,7 @@ __global__ void __launch_bounds__(256) k_gemm_tiled(GemmP p, const int* __restri
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
-      const int m = m0 + ty + 16 * i, n = n0 + tx + 16 * j;
+      const int m = m0 + ty * TM + i, n = n0 + tx * TN + j;
       if (m < Mx && n < p.N) {
         float v = acc[i][j];
         if (p.mask && p.mask[c * p.mask_cs + int64_t(m) * p.ldm + n] <= 0.0f) v = 0.0f;
@@ -134,47 +156,208 @@ __global__ void __launch_bounds__(256) k_gemm_tiled(GemmP p, const int* __restri
     }
 }
 
-template <bool AT, bool BT, int TM, int TN, int BK, int STAGES>
-void gemm_launch(const GemmP& p, const int* active, int n_active, cudaStream_t st) {
+template <bool AT, bool BT, int TM, int TN, int BK, int STAGES, int TX = 16, int TY = 16>
+void gemm_launch(const GemmP& p, const TickDesc* td, int max_active, cudaStream_t st) {
   const int Mx = p.M + (p.ones_row ? 1 : 0);
-  dim3 grid((p.N + 16 * TN - 1) / (16 * TN), (Mx + 16 * TM - 1) / (16 * TM), n_active);
-  k_gemm_tiled<AT, BT, TM, TN, BK, STAGES><<<grid, 256, 0, st>>>(p, active);
+  dim3 grid((p.N + TX * TN - 1) / (TX * TN), (Mx + TY * TM - 1) / (TY * TM), max_active);
+  k_gemm_tiled<AT, BT, TM, TN, BK, STAGES, TX, TY><<<grid, TX * TY, 0, st>>>(p, td);
 }
 
 template <bool AT, bool BT>
-void gemm_dispatch(const GemmP& p, const int* active, int n_active, cudaStream_t st) {
+void gemm_dispatch(const GemmP& p, const TickDesc* td, int max_active, cudaStream_t st) {
   const int Mx = p.M + (p.ones_row ? 1 : 0);
-  auto blocks = [&](int tm, int tn) {
-    return int64_t((p.N + 16 * tn - 1) / (16 * tn)) * ((Mx + 16 * tm - 1) / (16 * tm)) * n_active;
+  auto blocks = [&](int bm, int bn) {
+    return int64_t((p.N + bn - 1) / bn) * ((Mx + bm - 1) / bm) * max_active;
   };
-  // largest tile that still gives every SM at least two blocks
+  // Largest tile that still gives every SM two blocks (throughput); for a
+  // launch too small to fill the chip, one output per thread, and for long
+  // reductions over few outputs, one-warp blocks (4x8 outputs) so the
+  // dependent chains spread over as many SMs as possible.
   constexpr int64_t kFill = 2 * 148;
-  if (blocks(4, 4) >= kFill && p.N >= 48 && Mx >= 48)
-    gemm_launch<AT, BT, 4, 4, 32, 2>(p, active, n_active, st);
-  else if (blocks(2, 2) >= kFill && p.N >= 24 && Mx >= 24)
-    gemm_launch<AT, BT, 2, 2, 32, 3>(p, active, n_active, st);
+  if (blocks(64, 64) >= kFill && p.N >= 48 && Mx >= 48)
+    gemm_launch<AT, BT, 4, 4, 32, 2>(p, td, max_active, st);
+  else if (blocks(64, 16) >= kFill && p.N <= 16 && Mx >= 48)
+    gemm_launch<AT, BT, 4, 1, 32, 2>(p, td, max_active, st);
+  else if (blocks(32, 32) >= kFill && p.N >= 24 && Mx >= 24)
+    gemm_launch<AT, BT, 2, 2, 32, 3>(p, td, max_active, st);
+  else if (blocks(16, 16) >= 148 || p.K <= 256)
+    gemm_launch<AT, BT, 1, 1, 64, 4>(p, td, max_active, st);
   else
-    gemm_launch<AT, BT, 1, 1, 64, 4>(p, active, n_active, st);
+    gemm_launch<AT, BT, 1, 1, 128, 4, 8, 4>(p, td, max_active, st);
+}
+
+// ------------------------------------------------------------------ NT reduction
+
+// TMA bulk-copy ring (cp.async.bulk + mbarrier complete_tx): one elected
+// thread streams each stage's operand rows (1 A row + up to 64 B rows of BK
+// floats) into shared memory; consumers wait on the stage's mbarrier phase.
+constexpr int kNtThreads = 64, kNtBK = 64, kNtStages = 4;
+constexpr int kNtSB = kNtBK + 4;  // padded B row: LDS.128 of 32 rows = 4 wavefronts
+constexpr size_t kNtSmem =
+    size_t(kNtStages) * (kNtBK + kNtThreads * kNtSB) * sizeof(float) + kNtStages * sizeof(uint64_t);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(phase));
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// VEC: every row segment is 16-byte aligned and a multiple of 16 bytes
+// (host-checked), so TMA bulk copies stream them; otherwise 4-byte cp.async.
+template <bool VEC>
+__global__ void __launch_bounds__(kNtThreads) k_gemm_nt(NtP p0, NtP p1, const TickDesc* __restrict__ td) {
+  extern __shared__ __align__(128) float sm[];
+  if (blockIdx.z >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.z];
+  int m = blockIdx.y;
+  const bool second = m >= p0.M + 1;
+  if (second) m -= p0.M + 1;
+  const float* Ab = second ? p1.A : p0.A;
+  const float* Bb = second ? p1.B : p0.B;
+  float* Cb = second ? p1.C : p0.C;
+  const int64_t a_cs = second ? p1.a_cs : p0.a_cs, b_cs = second ? p1.b_cs : p0.b_cs,
+                c_cs = second ? p1.c_cs : p0.c_cs, lda = second ? p1.lda : p0.lda,
+                ldb = second ? p1.ldb : p0.ldb, ldc = second ? p1.ldc : p0.ldc;
+  const int M = second ? p1.M : p0.M, N = second ? p1.N : p0.N, K = second ? p1.K : p0.K;
+  if (m > M) return;
+  const int n0 = blockIdx.x * kNtThreads;
+  if (n0 >= N) return;
+  const int tid = threadIdx.x, n = n0 + tid;
+  const bool ones = m == M;  // bias row: plain sum of the gradient rows
+  const float* A = Ab + c * a_cs + int64_t(m) * lda;
+  const float* B = Bb + c * b_cs + int64_t(n0) * ldb;
+  float* C = Cb + c * c_cs;
+  float* As = sm;
+  float* Bs = sm + kNtStages * kNtBK;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(Bs + kNtStages * kNtThreads * kNtSB);
+  const int ntiles = (K + kNtBK - 1) / kNtBK;
+  const int nrows = min(kNtThreads, N - n0);
+
+  if (VEC && tid == 0) {
+    for (int s = 0; s < kNtStages; ++s) mbar_init(&bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  __syncthreads();
+
+  // stage `tile`: thread 0 arms the stage barrier with the byte count before
+  // the block barrier; afterwards every thread issues (at most) one row copy.
+  auto arm = [&](int tile) {
+    if (VEC && tid == 0 && tile < ntiles) {
+      const uint32_t rb = uint32_t(min(kNtBK, K - tile * kNtBK)) * 4u;
+      mbar_expect_tx(&bar[tile % kNtStages], rb * uint32_t(nrows + (ones ? 0 : 1)));
+    }
+  };
+  auto load = [&](int tile) {
+    if (tile >= ntiles) {
+      if (!VEC) cp_async_commit();
+      return;
+    }
+    const int st = tile % kNtStages, k0 = tile * kNtBK, kc = min(kNtBK, K - k0);
+    float* as = As + st * kNtBK;
+    float* bs = Bs + st * kNtThreads * kNtSB;
+    if (VEC) {
+      const uint32_t rb = uint32_t(kc) * 4u;
+      if (tid < nrows) tma_bulk_g2s(bs + tid * kNtSB, B + int64_t(tid) * ldb + k0, rb, &bar[st]);
+      if (!ones && tid == kNtThreads - 1) tma_bulk_g2s(as, A + k0, rb, &bar[st]);
+    } else {
+      if (!ones)
+        for (int i = tid; i < kc; i += kNtThreads) cp_async4(as + i, A + k0 + i);
+      for (int rr = 0; rr < nrows; ++rr)
+        for (int i = tid; i < kc; i += kNtThreads) cp_async4(bs + rr * kNtSB + i, B + int64_t(rr) * ldb + k0 + i);
+      cp_async_commit();
+    }
+  };
+
+  float acc = (n < N) ? C[int64_t(m) * ldc + n] : 0.0f;
+#pragma unroll
+  for (int s = 0; s < kNtStages - 1; ++s) arm(s);
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < kNtStages - 1; ++s) load(s);
+  for (int tile = 0; tile < ntiles; ++tile) {
+    const int st = tile % kNtStages;
+    if (VEC) mbar_wait(&bar[st], uint32_t(tile / kNtStages) & 1u);
+    else cp_async_wait<kNtStages - 2>();
+    arm(tile + kNtStages - 1);
+    __syncthreads();  // everyone is past tile-1: its stage may be refilled
+    load(tile + kNtStages - 1);
+    const int kc = min(kNtBK, K - tile * kNtBK);
+    const float* as = As + st * kNtBK;
+    const float* bs = Bs + (st * kNtThreads + tid) * kNtSB;
+    if (tid < nrows) {
+      if (kc == kNtBK) {
+        if (ones) {
+#pragma unroll
+          for (int kk = 0; kk < kNtBK; kk += 4) {
+            const float4 b = *reinterpret_cast<const float4*>(bs + kk);
+            acc = fadd(acc, b.x);  // 1.0f * b == b exactly
+            acc = fadd(acc, b.y);
+            acc = fadd(acc, b.z);
+            acc = fadd(acc, b.w);
+          }
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < kNtBK; kk += 4) {
+            const float4 a = *reinterpret_cast<const float4*>(as + kk);
+            const float4 b = *reinterpret_cast<const float4*>(bs + kk);
+            acc = mac(acc, a.x, b.x);
+            acc = mac(acc, a.y, b.y);
+            acc = mac(acc, a.z, b.z);
+            acc = mac(acc, a.w, b.w);
+          }
+        }
+      } else {
+        for (int kk = 0; kk < kc; ++kk) acc = ones ? fadd(acc, bs[kk]) : mac(acc, as[kk], bs[kk]);
+      }
+    }
+  }
+  if (!VEC) cp_async_wait<0>();
+  if (n < N) C[int64_t(m) * ldc + n] = acc;
 }
 
 // ------------------------------------------------------------------ embed
-__global__ void k_embed(const uint32_t* __restrict__ tokens, ChunkGeo geo, int64_t tick,
+// x = emb[tok] + pos written feature-major xT[E][R*T] (the K/V projections and
+// their weight gradients read it by feature), plus the last-position rows
+// xl[R][E] for the query projection.
+__global__ void k_embed(const uint32_t* __restrict__ tokens, ChunkGeo geo,
                         const float* __restrict__ params, int64_t p_cs, int64_t off_emb,
-                        int64_t off_pos, uint32_t* ctx, int64_t ctx_cs, float* x, int64_t x_cs,
-                        DmDims d, const int* __restrict__ active) {
-  const int c = active[blockIdx.y];
-  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t total = int64_t(d.R) * d.T * d.E;
-  if (idx >= total) return;
-  const int j = int(idx % d.E);
-  const int64_t rt = idx / d.E;
+                        int64_t off_pos, uint32_t* ctx, int64_t ctx_cs, float* xT, int64_t x_cs,
+                        float* xl, int64_t xl_cs, DmDims d, const TickDesc* __restrict__ td) {
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
+  const int64_t RT = int64_t(d.R) * d.T;
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // = j*RT + rt
+  if (idx >= RT * d.E) return;
+  const int64_t rt = idx % RT;
+  const int j = int(idx / RT);
   const int t = int(rt % d.T), r = int(rt / d.T);
   const uint64_t L = geo.L[c];
-  const uint64_t jstep = uint64_t(d.T) + uint64_t(tick - geo.offset[c]);  // coded position
+  const uint64_t jstep = uint64_t(d.T) + uint64_t(td->tick - geo.offset[c]);  // coded position
   const uint32_t tok = tokens[geo.start[c] + uint64_t(r) * L + (jstep - d.T) + t];
   if (j == 0) ctx[c * ctx_cs + rt] = tok;
   const float* P = params + c * p_cs;
-  x[c * x_cs + idx] = fadd(P[off_emb + int64_t(tok) * d.E + j], P[off_pos + int64_t(t) * d.E + j]);
+  const float xv = fadd(P[off_emb + int64_t(tok) * d.E + j], P[off_pos + int64_t(t) * d.E + j]);
+  xT[c * x_cs + idx] = xv;
+  if (t == d.T - 1) xl[c * xl_cs + int64_t(r) * d.E + j] = xv;
 }
 
 // ------------------------------------------------------------------ attention
@@ -184,8 +367,9 @@ __global__ void k_embed(const uint32_t* __restrict__ tokens, ChunkGeo geo, int64
 __global__ void k_attn_fwd(const float* __restrict__ q, const float* __restrict__ k,
                            const float* __restrict__ v, float* wts, float* cx, int64_t cs_q,
                            int64_t cs_kv, int64_t cs_w, DmDims d, float inv,
-                           const int* __restrict__ active) {
-  const int c = active[blockIdx.y];
+                           const TickDesc* __restrict__ td) {
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= d.R * d.NH) return;
   const int r = warp / d.NH, h = warp % d.NH, HD = d.H / d.NH, T = d.T;
@@ -227,58 +411,217 @@ __global__ void k_attn_fwd(const float* __restrict__ q, const float* __restrict_
   }
 }
 
-__global__ void k_attn_bwd(const float* __restrict__ q, const float* __restrict__ k,
+// dk, dv are written feature-major ([H][R*T]: element (h*HD+d, r*T+t)) so the
+// K/V weight-gradient reductions over R*T rows read contiguous rows.
+constexpr int kAttnMaxT = 256;  // ds_t kept in shared memory up to this context length
+__global__ void __launch_bounds__(256) k_attn_bwd(const float* __restrict__ q, const float* __restrict__ k,
                            const float* __restrict__ v, const float* __restrict__ wts,
-                           const float* __restrict__ dctx, float* dq, float* dk, float* dv,
+                           const float* __restrict__ dctx, float* dq, float* dkT, float* dvT,
                            int64_t cs_q, int64_t cs_kv, int64_t cs_w, DmDims d, float inv,
-                           const int* __restrict__ active) {
-  const int c = active[blockIdx.y];
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+                           const TickDesc* __restrict__ td) {
+  __shared__ float sds[8][kAttnMaxT];
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (warp >= d.R * d.NH) return;
   const int r = warp / d.NH, h = warp % d.NH, HD = d.H / d.NH, T = d.T;
+  const int64_t RT = int64_t(d.R) * T;
   const int64_t qo = c * cs_q + int64_t(r) * d.H + h * HD;
-  const int64_t ko = c * cs_kv + int64_t(r) * T * d.H + h * HD;
+  const int64_t ko = c * cs_kv + int64_t(r) * T * d.H + h * HD;       // row-major K, V
+  const int64_t to = c * cs_kv + int64_t(h) * HD * RT + int64_t(r) * T;  // feature-major dk, dv
   const float* w = wts + c * cs_w + (int64_t(r) * d.NH + h) * T;
   const float* dc = dctx + qo;
-  // dv_t[d] = 0 + w_t*dc[d];  dwt_t = sum_d dc[d]*v_t[d]
-  // dot = sum_t w_t*dwt_t (sequential, all lanes redundantly)
+  // dv_t[d] = 0 + w_t*dc[d];  dwt_t = sum_d dc[d]*v_t[d];  dot = sum_t w_t*dwt_t
   float dot = 0.0f;
-  for (int t0 = 0; t0 < T; t0 += 32) {
+  float dwt_reg[kAttnMaxT / 32];
+  for (int t0 = 0, q8 = 0; t0 < T; t0 += 32, ++q8) {
     const int t = t0 + lane;
     float prod = 0.0f;
     if (t < T) {
       const float wt = w[t];
       float acc = 0.0f;
       for (int dd = 0; dd < HD; ++dd) {
-        dv[ko + int64_t(t) * d.H + dd] = fadd(0.0f, fmul(wt, dc[dd]));
+        dvT[to + int64_t(dd) * RT + t] = fadd(0.0f, fmul(wt, dc[dd]));
         acc = mac(acc, dc[dd], v[ko + int64_t(t) * d.H + dd]);
       }
       prod = fmul(wt, acc);
-      dk[ko + int64_t(t) * d.H] = acc;  // stash dwt_t in dk's first slot until ds is known
+      if (q8 < kAttnMaxT / 32) dwt_reg[q8] = acc;
     }
     const int cnt = min(32, T - t0);
     for (int i = 0; i < cnt; ++i) dot = fadd(dot, __shfl_sync(0xffffffffu, prod, i));
   }
-  __syncwarp();
-  // ds_t = (w_t*(dwt_t - dot))*inv;  dk_t[d] = 0 + ds_t*q[d]; stash ds_t in dwt slot first
-  for (int t = lane; t < T; t += 32) {
-    const float dwt = dk[ko + int64_t(t) * d.H];
+  // ds_t = (w_t*(dwt_t - dot))*inv;  dk_t[d] = 0 + ds_t*q[d]
+  const bool keep = T <= kAttnMaxT;
+  for (int t0 = 0, q8 = 0; t0 < T; t0 += 32, ++q8) {
+    const int t = t0 + lane;
+    if (t >= T) break;
+    float dwt;
+    if (keep) {
+      dwt = dwt_reg[q8];
+    } else {
+      dwt = 0.0f;
+      for (int dd = 0; dd < HD; ++dd) dwt = mac(dwt, dc[dd], v[ko + int64_t(t) * d.H + dd]);
+    }
     const float ds = fmul(fmul(w[t], fsub(dwt, dot)), inv);
-    for (int dd = HD - 1; dd >= 0; --dd)  // slot 0 (dwt) overwritten last
-      dk[ko + int64_t(t) * d.H + dd] = fadd(0.0f, fmul(ds, q[qo + dd]));
-    // keep ds for the dq pass: recover as dk_t[0]/q[0] is not exact; store separately
+    if (keep) sds[wl][t] = ds;
+    for (int dd = 0; dd < HD; ++dd) dkT[to + int64_t(dd) * RT + t] = fadd(0.0f, fmul(ds, q[qo + dd]));
   }
   __syncwarp();
-  // dq[d] = sum_t ds_t*k_t[d]: recompute ds_t in registers per t (cheap, exact same ops)
+  // dq[d] = 0 + sum_t ds_t*k_t[d], ascending t
   if (lane < HD) {
     float acc = 0.0f;
     for (int t = 0; t < T; ++t) {
-      float dwt = 0.0f;
-      for (int dd = 0; dd < HD; ++dd) dwt = mac(dwt, dc[dd], v[ko + int64_t(t) * d.H + dd]);
-      const float ds = fmul(fmul(w[t], fsub(dwt, dot)), inv);
+      float ds;
+      if (keep) {
+        ds = sds[wl][t];
+      } else {
+        float dwt = 0.0f;
+        for (int dd = 0; dd < HD; ++dd) dwt = mac(dwt, dc[dd], v[ko + int64_t(t) * d.H + dd]);
+        ds = fmul(fmul(w[t], fsub(dwt, dot)), inv);
+      }
       acc = mac(acc, ds, k[ko + int64_t(t) * d.H + lane]);
     }
     dq[qo + lane] = acc;
+  }
+}
+
+// Row-blocked attention (the default path whenever a row's K and V fit in
+// shared memory): one block per (chunk, coded row), K[r] and V[r] ([T][H]) are
+// staged once with coalesced 16-byte loads into rows padded to H+4 floats, one
+// warp per head. Same operation order as the warp-per-(row,head) kernels.
+constexpr int kRowThreads = 256;  // 8 warps = the model's 8 heads
+__host__ __device__ inline size_t attn_row_smem(const DmDims& d) {
+  return (size_t(2) * d.T * (d.H + 4) + size_t(d.NH) * d.T + 2 * d.H) * sizeof(float);
+}
+
+__device__ __forceinline__ void stage_rows(float* dst, const float* src, int T, int H) {
+  // src [T][H] contiguous (H multiple of 4) -> dst rows of H+4
+  const int nv = T * (H / 4);
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    const int t = i / (H / 4), v4 = i % (H / 4);
+    *reinterpret_cast<float4*>(dst + t * (H + 4) + 4 * v4) =
+        __ldg(reinterpret_cast<const float4*>(src + int64_t(t) * H + 4 * v4));
+  }
+}
+
+__global__ void __launch_bounds__(kRowThreads) k_attn_fwd_row(
+    const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
+    float* wts, float* cx, int64_t cs_q, int64_t cs_kv, int64_t cs_w, DmDims d, float inv,
+    const TickDesc* __restrict__ td) {
+  extern __shared__ __align__(128) float sm[];
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
+  const int r = blockIdx.x, T = d.T, H = d.H, HD = H / d.NH, HP = H + 4;
+  const int h = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* Ks = sm;
+  float* Vs = Ks + T * HP;
+  float* Ws = Vs + T * HP;   // [NH][T]
+  float* Qs = Ws + d.NH * T; // [H]
+  const int64_t ko = c * cs_kv + int64_t(r) * T * H;
+  stage_rows(Ks, k + ko, T, H);
+  stage_rows(Vs, v + ko, T, H);
+  for (int i = threadIdx.x; i < H; i += blockDim.x) Qs[i] = q[c * cs_q + int64_t(r) * H + i];
+  __syncthreads();
+  if (h >= d.NH) return;
+  const float* qh = Qs + h * HD;
+  float* wrow = Ws + h * T;
+  float mx = -__int_as_float(0x7f800000);
+  for (int t = lane; t < T; t += 32) {
+    const float* kr = Ks + t * HP + h * HD;
+    float s = 0.0f;
+    for (int dd = 0; dd < HD; ++dd) s = mac(s, qh[dd], kr[dd]);
+    s = fmul(s, inv);
+    wrow[t] = s;
+    mx = fmaxf(mx, s);
+  }
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.0f;
+  for (int t0 = 0; t0 < T; t0 += 32) {
+    const int t = t0 + lane;
+    float e = 0.0f;
+    if (t < T) {
+      e = det_exp(fsub(wrow[t], mx));
+      wrow[t] = e;
+    }
+    const int cnt = min(32, T - t0);
+    for (int i = 0; i < cnt; ++i) sum = fadd(sum, __shfl_sync(0xffffffffu, e, i));
+  }
+  const float invs = fdiv(1.0f, sum);
+  float* wg = wts + c * cs_w + (int64_t(r) * d.NH + h) * T;
+  for (int t = lane; t < T; t += 32) {
+    const float wv = fmul(wrow[t], invs);
+    wrow[t] = wv;
+    wg[t] = wv;
+  }
+  __syncwarp();
+  if (lane < HD) {
+    float acc = 0.0f;
+    for (int t = 0; t < T; ++t) acc = mac(acc, wrow[t], Vs[t * HP + h * HD + lane]);
+    cx[c * cs_q + int64_t(r) * H + h * HD + lane] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
+    const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
+    const float* __restrict__ wts, const float* __restrict__ dctx, float* dq, float* dkT,
+    float* dvT, int64_t cs_q, int64_t cs_kv, int64_t cs_w, DmDims d, float inv,
+    const TickDesc* __restrict__ td) {
+  extern __shared__ __align__(128) float sm[];
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
+  const int r = blockIdx.x, T = d.T, H = d.H, HD = H / d.NH, HP = H + 4;
+  const int h = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t RT = int64_t(d.R) * T;
+  float* Ks = sm;
+  float* Vs = Ks + T * HP;
+  float* Ds = Vs + T * HP;    // [NH][T]: ds_t per head
+  float* Qs = Ds + d.NH * T;  // [H]
+  float* Cs = Qs + H;         // dctx row [H]
+  const int64_t ko = c * cs_kv + int64_t(r) * T * H;
+  stage_rows(Ks, k + ko, T, H);
+  stage_rows(Vs, v + ko, T, H);
+  for (int i = threadIdx.x; i < H; i += blockDim.x) {
+    Qs[i] = q[c * cs_q + int64_t(r) * H + i];
+    Cs[i] = dctx[c * cs_q + int64_t(r) * H + i];
+  }
+  __syncthreads();
+  if (h >= d.NH) return;
+  const float* w = wts + c * cs_w + (int64_t(r) * d.NH + h) * T;
+  const float* dc = Cs + h * HD;
+  const int64_t to = c * cs_kv + int64_t(h) * HD * RT + int64_t(r) * T;  // feature-major dk, dv
+  float* dsw = Ds + h * T;
+  // dv_t[d] = 0 + w_t*dc[d]; dwt_t = sum_d dc[d]*v_t[d]; dot = sum_t w_t*dwt_t
+  float dot = 0.0f;
+  for (int t0 = 0; t0 < T; t0 += 32) {
+    const int t = t0 + lane;
+    float prod = 0.0f;
+    if (t < T) {
+      const float wt = w[t];
+      const float* vr = Vs + t * HP + h * HD;
+      float acc = 0.0f;
+      for (int dd = 0; dd < HD; ++dd) {
+        dvT[to + int64_t(dd) * RT + t] = fadd(0.0f, fmul(wt, dc[dd]));
+        acc = mac(acc, dc[dd], vr[dd]);
+      }
+      dsw[t] = acc;  // dwt_t, turned into ds_t below
+      prod = fmul(wt, acc);
+    }
+    const int cnt = min(32, T - t0);
+    for (int i = 0; i < cnt; ++i) dot = fadd(dot, __shfl_sync(0xffffffffu, prod, i));
+  }
+  // ds_t = (w_t*(dwt_t - dot))*inv;  dk_t[d] = 0 + ds_t*q[d]
+  for (int t = lane; t < T; t += 32) {
+    const float ds = fmul(fmul(w[t], fsub(dsw[t], dot)), inv);
+    dsw[t] = ds;
+    for (int dd = 0; dd < HD; ++dd) dkT[to + int64_t(dd) * RT + t] = fadd(0.0f, fmul(ds, Qs[h * HD + dd]));
+  }
+  __syncwarp();
+  // dq[d] = 0 + sum_t ds_t*k_t[d]
+  if (lane < HD) {
+    float acc = 0.0f;
+    for (int t = 0; t < T; ++t) acc = mac(acc, dsw[t], Ks[t * HP + h * HD + lane]);
+    dq[c * cs_q + int64_t(r) * H + h * HD + lane] = acc;
   }
 }
 
@@ -288,16 +631,11 @@ __global__ void k_attn_bwd(const float* __restrict__ q, const float* __restrict_
 // visited in (r,t) row-major order: a segment of ctx is staged in shared
 // memory, each warp ballots its hits into a shared list, then walks the list
 // with 16 independent dx loads in flight per batch.
-__device__ __forceinline__ float dx_at(const float* xp, const float* lp, int64_t pp, int j, int T, int E) {
-  float v = xp[pp * E + j];
-  if (int(pp % T) == T - 1) v = fadd(v, lp[(pp / T) * E + j]);  // dx[:,last,:] += dxl (layers.cpp:521)
-  return v;
-}
-
 __global__ void k_pos_bwd(const float* __restrict__ dx, int64_t dx_cs, const float* __restrict__ dxl,
                           int64_t dxl_cs, float* grads, int64_t g_cs, int64_t off_pos, DmDims d,
-                          const int* __restrict__ active) {
-  const int c = active[blockIdx.y];
+                          const TickDesc* __restrict__ td) {
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= d.T * d.E) return;
   const int t = idx / d.E, j = idx % d.E;
@@ -308,18 +646,24 @@ __global__ void k_pos_bwd(const float* __restrict__ dx, int64_t dx_cs, const flo
   const int64_t rs = int64_t(d.T) * d.E;
   const bool last = t == d.T - 1;
   constexpr int kB = 16;
-  for (int r0 = 0; r0 < d.R; r0 += kB) {
-    float v[kB];
-    const int cnt = min(kB, d.R - r0);
+  int r0 = 0;
+  for (; r0 + kB <= d.R; r0 += kB) {  // full batches: 16 loads in flight, then the chain
+    float v[kB], l[kB];
 #pragma unroll
-    for (int q = 0; q < kB; ++q)
-      if (q < cnt) {
-        v[q] = xp[(r0 + q) * rs];
-        if (last) v[q] = fadd(v[q], lp[int64_t(r0 + q) * d.E]);
-      }
+    for (int q = 0; q < kB; ++q) v[q] = __ldg(xp + (r0 + q) * rs);
+    if (last) {
 #pragma unroll
-    for (int q = 0; q < kB; ++q)
-      if (q < cnt) acc = fadd(acc, v[q]);
+      for (int q = 0; q < kB; ++q) l[q] = __ldg(lp + int64_t(r0 + q) * d.E);
+#pragma unroll
+      for (int q = 0; q < kB; ++q) v[q] = fadd(v[q], l[q]);  // dx[:,last,:] += dxl (layers.cpp:521)
+    }
+#pragma unroll
+    for (int q = 0; q < kB; ++q) acc = fadd(acc, v[q]);
+  }
+  for (; r0 < d.R; ++r0) {
+    float v = xp[r0 * rs];
+    if (last) v = fadd(v, lp[int64_t(r0) * d.E]);
+    acc = fadd(acc, v);
   }
   *g = acc;
 }
@@ -330,10 +674,11 @@ constexpr int kEmbSeg = 2048;
 __global__ void __launch_bounds__(kEmbWarps * 32) k_emb_bwd(
     const uint32_t* __restrict__ ctx, int64_t ctx_cs, const float* __restrict__ dx, int64_t dx_cs,
     const float* __restrict__ dxl, int64_t dxl_cs, float* grads, int64_t g_cs, int64_t off_emb,
-    DmDims d, const int* __restrict__ active) {
+    DmDims d, const TickDesc* __restrict__ td) {
   __shared__ uint32_t sctx[kEmbSeg];
   __shared__ uint16_t hits[kEmbWarps][kEmbSeg];
-  const int c = active[blockIdx.y];
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tokv = blockIdx.x * kEmbWarps + wl;
   const uint32_t* cp = ctx + c * ctx_cs;
@@ -371,14 +716,23 @@ __global__ void __launch_bounds__(kEmbWarps * 32) k_emb_bwd(
 #pragma unroll
       for (int q = 0; q < kMaxJ; ++q) {
         const int j = lane + 32 * q;
-        if (q >= nj || j >= d.E) break;
-        float v[kB];
+        if (q >= nj) break;
+        const bool jv = j < d.E;
+        const int jj = jv ? j : 0;
+        float v[kB], l[kB];
+        bool lastp[kB];
 #pragma unroll
-        for (int b = 0; b < kB; ++b)
-          if (b < cnt) v[b] = dx_at(xp, lp, s0 + hits[wl][h0 + b], j, d.T, d.E);
+        for (int b = 0; b < kB; ++b) {  // all loads first (clamped index past the end)
+          const int64_t pp = s0 + hits[wl][h0 + (b < cnt ? b : 0)];
+          lastp[b] = int(pp % d.T) == d.T - 1;
+          v[b] = __ldg(xp + pp * d.E + jj);
+          l[b] = __ldg(lp + (pp / d.T) * d.E + jj);
+        }
 #pragma unroll
-        for (int b = 0; b < kB; ++b)
-          if (b < cnt) acc[q] = fadd(acc[q], v[b]);
+        for (int b = 0; b < kB; ++b) {
+          const float x = lastp[b] ? fadd(v[b], l[b]) : v[b];  // dx[:,last,:] += dxl
+          if (b < cnt && jv) acc[q] = fadd(acc[q], x);
+        }
       }
     }
     __syncwarp();
@@ -394,8 +748,9 @@ __global__ void __launch_bounds__(kEmbWarps * 32) k_emb_bwd(
 // ------------------------------------------------------------------ Adam
 __global__ void k_adam(float* __restrict__ w, float* __restrict__ g, float* __restrict__ m,
                        float* __restrict__ v, int64_t p_cs, int64_t n,
-                       const AdamScalars* __restrict__ sc, const int* __restrict__ active) {
-  const int c = active[blockIdx.y];
+                       const AdamScalars* __restrict__ sc, const TickDesc* __restrict__ td) {
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
   const float bc1 = sc[c].bc1, bc2 = sc[c].bc2;
   const float b1 = 0.9f, b2 = 0.999f, lr = 5e-4f, eps = 1e-8f;
   const float omb1 = fsub(1.0f, b1), omb2 = fsub(1.0f, b2);
@@ -416,8 +771,9 @@ __global__ void k_adam(float* __restrict__ w, float* __restrict__ g, float* __re
 }
 
 __global__ void k_state_copy(float* w, float* m, float* v, AdamScalars* sc, int64_t p_cs, int64_t n,
-                             const int2* __restrict__ pairs) {
-  const int2 pr = pairs[blockIdx.y];  // x = src, y = dst
+                             const TickDesc* __restrict__ td) {
+  if (blockIdx.y >= unsigned(td->n_hand)) return;
+  const int2 pr = td->hand[blockIdx.y];  // x = src, y = dst
   const int64_t so = pr.x * p_cs, dof = pr.y * p_cs;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -428,74 +784,141 @@ __global__ void k_state_copy(float* w, float* m, float* v, AdamScalars* sc, int6
   if (blockIdx.x == 0 && threadIdx.x == 0) sc[pr.y] = sc[pr.x];
 }
 
-}  // namespace
-
-void launch_gemm(const GemmP& p, bool at, bool bt, const int* active, int n_active,
-                 cudaStream_t st) {
-  if (n_active <= 0 || p.N <= 0 || p.M + p.ones_row <= 0) return;
-  if (at && bt) gemm_dispatch<true, true>(p, active, n_active, st);
-  else if (at) gemm_dispatch<true, false>(p, active, n_active, st);
-  else if (bt) gemm_dispatch<false, true>(p, active, n_active, st);
-  else gemm_dispatch<false, false>(p, active, n_active, st);
+__global__ void k_tick_advance(TickDesc* td, const uint32_t* __restrict__ act_ptr,
+                               const int* __restrict__ act_all, const uint32_t* __restrict__ hand_ptr,
+                               const int2* __restrict__ hand_all, int64_t ticks) {
+  const int64_t t = td->tick + 1;
+  td->tick = t;
+  if (t < ticks) {
+    td->act = act_all + act_ptr[t];
+    td->n_act = int(act_ptr[t + 1] - act_ptr[t]);
+    td->hand = hand_all + hand_ptr[t];
+    td->n_hand = int(hand_ptr[t + 1] - hand_ptr[t]);
+  } else {
+    td->n_act = 0;
+    td->n_hand = 0;
+  }
 }
 
-void launch_embed(const uint32_t* tokens, ChunkGeo geo, int64_t tick, const float* params,
+}  // namespace
+
+void launch_gemm(const GemmP& p, bool at, bool bt, const TickDesc* td, int max_active,
+                 cudaStream_t st) {
+  if (max_active <= 0 || p.N <= 0 || p.M + p.ones_row <= 0) return;
+  if (at && bt) gemm_dispatch<true, true>(p, td, max_active, st);
+  else if (at) gemm_dispatch<true, false>(p, td, max_active, st);
+  else if (bt) gemm_dispatch<false, true>(p, td, max_active, st);
+  else gemm_dispatch<false, false>(p, td, max_active, st);
+}
+
+void launch_gemm_nt(const NtP& p0, const NtP* p1, const TickDesc* td, int max_active,
+                    cudaStream_t st) {
+  if (max_active <= 0 || p0.N <= 0) return;
+  const NtP q1 = p1 ? *p1 : p0;
+  auto al = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+  auto vec_ok = [&](const NtP& p) {  // TMA bulk: 16-byte aligned rows, sizes multiple of 16 B
+    return p.K % 4 == 0 && p.lda % 4 == 0 && p.ldb % 4 == 0 && p.a_cs % 4 == 0 &&
+           p.b_cs % 4 == 0 && al(p.A) && al(p.B);
+  };
+  const bool vec = vec_ok(p0) && vec_ok(q1);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_gemm_nt<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNtSmem));
+    cudaFuncSetAttribute(k_gemm_nt<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNtSmem));
+    attr_set = true;
+  }
+  const int nx = (std::max(p0.N, q1.N) + kNtThreads - 1) / kNtThreads;
+  const int ny = (p0.M + 1) + (p1 ? p1->M + 1 : 0);
+  dim3 grid(nx, ny, max_active);
+  if (vec) k_gemm_nt<true><<<grid, kNtThreads, kNtSmem, st>>>(p0, q1, td);
+  else k_gemm_nt<false><<<grid, kNtThreads, kNtSmem, st>>>(p0, q1, td);
+}
+
+void launch_embed(const uint32_t* tokens, ChunkGeo geo, const float* params,
                   int64_t p_cs, int64_t off_emb, int64_t off_pos, uint32_t* ctx, int64_t ctx_cs,
-                  float* x, int64_t x_cs, DmDims d, const int* active, int n_active,
-                  cudaStream_t st) {
-  if (n_active <= 0) return;
+                  float* x, int64_t x_cs, float* xl, int64_t xl_cs, DmDims d, const TickDesc* td,
+                  int max_active, cudaStream_t st) {
+  if (max_active <= 0) return;
   const int64_t total = int64_t(d.R) * d.T * d.E;
-  dim3 grid(unsigned((total + 255) / 256), n_active);
-  k_embed<<<grid, 256, 0, st>>>(tokens, geo, tick, params, p_cs, off_emb, off_pos, ctx, ctx_cs, x,
-                                x_cs, d, active);
+  dim3 grid(unsigned((total + 255) / 256), max_active);
+  k_embed<<<grid, 256, 0, st>>>(tokens, geo, params, p_cs, off_emb, off_pos, ctx, ctx_cs, x,
+                                x_cs, xl, xl_cs, d, td);
 }
 
 void launch_attn_fwd(const float* q, const float* k, const float* v, float* wts, float* cx,
                      int64_t cs_q, int64_t cs_kv, int64_t cs_w, DmDims d, float inv,
-                     const int* active, int n_active, cudaStream_t st) {
-  if (n_active <= 0) return;
+                     const TickDesc* td, int max_active, cudaStream_t st) {
+  if (max_active <= 0) return;
+  const size_t smem = attn_row_smem(d);
+  if (d.NH <= 8 && d.H % 4 == 0 && smem <= 200 * 1024) {
+    static size_t attr = 0;
+    if (smem > attr) {
+      cudaFuncSetAttribute(k_attn_fwd_row, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      attr = smem;
+    }
+    k_attn_fwd_row<<<dim3(d.R, max_active), kRowThreads, smem, st>>>(q, k, v, wts, cx, cs_q, cs_kv,
+                                                                      cs_w, d, inv, td);
+    return;
+  }
   const int64_t warps = int64_t(d.R) * d.NH;
-  dim3 grid(unsigned((warps * 32 + 255) / 256), n_active);
-  k_attn_fwd<<<grid, 256, 0, st>>>(q, k, v, wts, cx, cs_q, cs_kv, cs_w, d, inv, active);
+  dim3 grid(unsigned((warps * 32 + 255) / 256), max_active);
+  k_attn_fwd<<<grid, 256, 0, st>>>(q, k, v, wts, cx, cs_q, cs_kv, cs_w, d, inv, td);
 }
 
 void launch_attn_bwd(const float* q, const float* k, const float* v, const float* wts,
                      const float* dctx, float* dq, float* dk, float* dv, int64_t cs_q,
-                     int64_t cs_kv, int64_t cs_w, DmDims d, float inv, const int* active,
-                     int n_active, cudaStream_t st) {
-  if (n_active <= 0) return;
+                     int64_t cs_kv, int64_t cs_w, DmDims d, float inv, const TickDesc* td,
+                     int max_active, cudaStream_t st) {
+  if (max_active <= 0) return;
+  const size_t smem = attn_row_smem(d) + d.H * sizeof(float);
+  if (d.NH <= 8 && d.H % 4 == 0 && smem <= 200 * 1024) {
+    static size_t attr = 0;
+    if (smem > attr) {
+      cudaFuncSetAttribute(k_attn_bwd_row, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      attr = smem;
+    }
+    k_attn_bwd_row<<<dim3(d.R, max_active), kRowThreads, smem, st>>>(
+        q, k, v, wts, dctx, dq, dk, dv, cs_q, cs_kv, cs_w, d, inv, td);
+    return;
+  }
   const int64_t warps = int64_t(d.R) * d.NH;
-  dim3 grid(unsigned((warps * 32 + 255) / 256), n_active);
+  dim3 grid(unsigned((warps * 32 + 255) / 256), max_active);
   k_attn_bwd<<<grid, 256, 0, st>>>(q, k, v, wts, dctx, dq, dk, dv, cs_q, cs_kv, cs_w, d, inv,
-                                   active);
+                                   td);
 }
 
 void launch_embed_bwd(const uint32_t* ctx, int64_t ctx_cs, const float* dx, int64_t dx_cs,
                       const float* dxl, int64_t dxl_cs, float* grads, int64_t g_cs,
-                      int64_t off_emb, int64_t off_pos, DmDims d, const int* active, int n_active,
+                      int64_t off_emb, int64_t off_pos, DmDims d, const TickDesc* td, int max_active,
                       cudaStream_t st) {
-  if (n_active <= 0) return;
-  dim3 g1(unsigned((d.T * d.E + 255) / 256), n_active);
-  k_pos_bwd<<<g1, 256, 0, st>>>(dx, dx_cs, dxl, dxl_cs, grads, g_cs, off_pos, d, active);
-  dim3 g2(unsigned((d.V + kEmbWarps - 1) / kEmbWarps), n_active);
+  if (max_active <= 0) return;
+  dim3 g1(unsigned((d.T * d.E + 255) / 256), max_active);
+  k_pos_bwd<<<g1, 256, 0, st>>>(dx, dx_cs, dxl, dxl_cs, grads, g_cs, off_pos, d, td);
+  dim3 g2(unsigned((d.V + kEmbWarps - 1) / kEmbWarps), max_active);
   k_emb_bwd<<<g2, kEmbWarps * 32, 0, st>>>(ctx, ctx_cs, dx, dx_cs, dxl, dxl_cs, grads, g_cs, off_emb, d,
-                                active);
+                                td);
 }
 
 void launch_adam(float* w, float* g, float* m, float* v, int64_t p_cs, int64_t n,
-                 const AdamScalars* sc, const int* active, int n_active, cudaStream_t st) {
-  if (n_active <= 0 || n <= 0) return;
+                 const AdamScalars* sc, const TickDesc* td, int max_active, cudaStream_t st) {
+  if (max_active <= 0 || n <= 0) return;
   const int64_t per = (n + 255) / 256;
-  dim3 grid(unsigned(per < 64 ? per : 64), n_active);
-  k_adam<<<grid, 256, 0, st>>>(w, g, m, v, p_cs, n, sc, active);
+  dim3 grid(unsigned(per < 64 ? per : 64), max_active);
+  k_adam<<<grid, 256, 0, st>>>(w, g, m, v, p_cs, n, sc, td);
 }
 
 void launch_state_copy(float* w, float* m, float* v, AdamScalars* sc, int64_t p_cs, int64_t n,
-                       const int2* pairs, int n_pairs, cudaStream_t st) {
-  if (n_pairs <= 0) return;
+                       const TickDesc* td, int max_pairs, cudaStream_t st) {
+  if (max_pairs <= 0) return;
   const int64_t per = (n + 255) / 256;
-  dim3 grid(unsigned(per < 64 ? per : 64), n_pairs);
-  k_state_copy<<<grid, 256, 0, st>>>(w, m, v, sc, p_cs, n, pairs);
+  dim3 grid(unsigned(per < 64 ? per : 64), max_pairs);
+  k_state_copy<<<grid, 256, 0, st>>>(w, m, v, sc, p_cs, n, td);
+}
+
+void launch_tick_advance(TickDesc* td, const uint32_t* act_ptr, const int* act_all,
+                         const uint32_t* hand_ptr, const int2* hand_all, int64_t ticks,
+                         cudaStream_t st) {
+  k_tick_advance<<<1, 1, 0, st>>>(td, act_ptr, act_all, hand_ptr, hand_all, ticks);
 }
 
 }  // namespace pmklc_b200

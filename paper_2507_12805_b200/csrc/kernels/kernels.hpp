@@ -1,9 +1,12 @@
 // Launch interface of the sm_100a kernels (host-callable launchers).
 //
-// Batching model: every per-chunk kernel takes `active` (device array of chunk
-// ids, length n_active) and indexes its chunk's data as base + chunk*stride.
-// One launch therefore advances every active data block ("chunk", the unit of
-// PMKLC-M block partitioning, pipeline.cpp:32-52) by one coded batch step.
+// Batching model: every per-chunk kernel reads a device-resident TickDesc
+// (current tick, the chunk ids stepping this tick, the SMP handoffs due now)
+// and indexes its chunk's data as base + chunk*stride. One launch therefore
+// advances every active data block ("chunk", the unit of PMKLC-M block
+// partitioning, pipeline.cpp:32-52) by one coded batch step. Grids are sized
+// for the schedule's maximum concurrency and surplus blocks exit, so the
+// whole per-tick kernel sequence is a fixed CUDA graph replayed every tick.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -44,7 +47,16 @@ struct ChunkGeo {      // per-chunk constants, device arrays indexed by chunk id
   const int64_t* offset;   // tick of the chunk's first model step
 };
 
-struct Tape;  // device tape pointers, defined in engine
+struct TickDesc {
+  int64_t tick;       // -1 before the first advance
+  const int* act;     // chunk ids doing a model step at this tick
+  const int2* hand;   // (src, dst) state handoffs due before this tick's step
+  int n_act, n_hand;
+};
+// tick += 1 and point act/hand at that tick's CSR slices (n = 0 past the end)
+void launch_tick_advance(TickDesc* td, const uint32_t* act_ptr, const int* act_all,
+                         const uint32_t* hand_ptr, const int2* hand_all, int64_t ticks,
+                         cudaStream_t st);
 
 // Exact-order GEMM: C[m][n] = init + sum_{k ascending} A(m,k) * B(k,n).
 struct GemmP {
@@ -58,28 +70,42 @@ struct GemmP {
   int init;      // 0 zero, 1 bias, 2 accumulate onto C
   int relu_a;    // A(m,k) = A<0 ? 0 : A   (Ffn relu, layers.cpp:538-540)
 };
-void launch_gemm(const GemmP& p, bool at, bool bt, const int* active, int n_active,
+void launch_gemm(const GemmP& p, bool at, bool bt, const TickDesc* td, int max_active,
                  cudaStream_t st);
+// Long-reduction "NT" product for weight gradients over many rows:
+// C[m][n] += sum_{k ascending} A[m][k] * B[n][k] (+ row M: sum_k B[n][k]),
+// A, B feature-major (contiguous in k). One thread per output; both operand
+// rows are staged with 16-byte cp.async into a 3-stage shared ring and read as
+// LDS.128, so the only serial cost left is the K-long FADD chain itself.
+// Two independent problems (e.g. dWk and dWv) can share one launch.
+struct NtP {
+  const float* A; const float* B; float* C;
+  int64_t a_cs, b_cs, c_cs, lda, ldb, ldc;
+  int M, N, K;
+};
+void launch_gemm_nt(const NtP& p0, const NtP* p1, const TickDesc* td, int max_active,
+                    cudaStream_t st);
 
 struct DmDims { int R, T, E, H, F, V, NH; };
 
 // ctx gather (pipeline.cpp:180-182) + Embedding/PositionalEmbedding forward
-void launch_embed(const uint32_t* tokens, ChunkGeo geo, int64_t tick, const float* params,
+void launch_embed(const uint32_t* tokens, ChunkGeo geo, const float* params,
                   int64_t p_cs, int64_t off_emb, int64_t off_pos, uint32_t* ctx, int64_t ctx_cs,
-                  float* x, int64_t x_cs, DmDims d, const int* active, int n_active, cudaStream_t st);
+                  float* xT, int64_t x_cs, float* xl, int64_t xl_cs, DmDims d, const TickDesc* td,
+                  int max_active, cudaStream_t st);
 // Attention forward core: scores, det_softmax, context (layers.cpp:452-470)
 void launch_attn_fwd(const float* q, const float* k, const float* v, float* wts, float* cx,
                      int64_t cs_q, int64_t cs_kv, int64_t cs_w, DmDims d, float inv,
-                     const int* active, int n_active, cudaStream_t st);
+                     const TickDesc* td, int max_active, cudaStream_t st);
 // Attention backward core (layers.cpp:480-512)
 void launch_attn_bwd(const float* q, const float* k, const float* v, const float* wts,
                      const float* dctx, float* dq, float* dk, float* dv, int64_t cs_q,
-                     int64_t cs_kv, int64_t cs_w, DmDims d, float inv, const int* active,
-                     int n_active, cudaStream_t st);
+                     int64_t cs_kv, int64_t cs_w, DmDims d, float inv, const TickDesc* td,
+                     int max_active, cudaStream_t st);
 // PositionalEmbedding + Embedding backward (layers.cpp:117-125,147-155)
 void launch_embed_bwd(const uint32_t* ctx, int64_t ctx_cs, const float* dx, int64_t dx_cs,
                       const float* dxl, int64_t dxl_cs, float* grads, int64_t g_cs,
-                      int64_t off_emb, int64_t off_pos, DmDims d, const int* active, int n_active,
+                      int64_t off_emb, int64_t off_pos, DmDims d, const TickDesc* td, int max_active,
                       cudaStream_t st);
 
 struct AdamScalars {   // per chunk
@@ -89,10 +115,10 @@ struct AdamScalars {   // per chunk
 };
 // Adam over params [0, n) of each active chunk, then zero their grads (adam.cpp:21-43)
 void launch_adam(float* w, float* g, float* m, float* v, int64_t p_cs, int64_t n,
-                 const AdamScalars* sc, const int* active, int n_active, cudaStream_t st);
+                 const AdamScalars* sc, const TickDesc* td, int max_active, cudaStream_t st);
 // whole-state copy for Step-wise Model Passing: dst chunk <- src chunk
 void launch_state_copy(float* w, float* m, float* v, AdamScalars* sc, int64_t p_cs, int64_t n,
-                       const int2* pairs, int n_pairs, cudaStream_t st);
+                       const TickDesc* td, int max_pairs, cudaStream_t st);
 
 // mix (mixer.cpp:14-42) + det_softmax + quantize (coder.cpp:28-88), one warp per row;
 // also advances the chunk's Adam step scalars (adam.cpp:23-27).
@@ -105,7 +131,7 @@ struct MixP {
   int* err;
   int probs_given;  // test hook: rows of `probs` are already distributions (no mix/softmax)
 };
-void launch_mix_quantize(const MixP& p, const int* active, int n_active, cudaStream_t st);
+void launch_mix_quantize(const MixP& p, const TickDesc* td, int max_active, cudaStream_t st);
 
 // Backward-controller step (OnlineTrainer::step, mixer.cpp:57-97), split so
 // that only one tiny serial chain remains:
@@ -116,25 +142,25 @@ void launch_mix_quantize(const MixP& p, const int* active, int n_active, cudaStr
 //    alpha's Adam update, and the early-loss sum.
 struct BcP {
   const float* probs; const float* lu; const float* lr; const float* lm; int64_t cs_p;
-  const uint32_t* tokens; ChunkGeo geo; int64_t tick; int t;
+  const uint32_t* tokens; ChunkGeo geo; const TickDesc* td; int t;
   float* w; float* m; float* v; int64_t p_cs; int64_t off_alpha;
   float* dlm; float* aterm; float* lterm; int64_t cs_l;  // lterm stride per chunk
   const AdamScalars* sc;
   double* warm_loss; const uint64_t* warm_steps;
   int flags, R, V;
 };
-void launch_bc_dlm(const BcP& p, const int* active, int n_active, cudaStream_t st);
-void launch_alpha_step(const BcP& p, const int* active, int n_active, cudaStream_t st);
+void launch_bc_dlm(const BcP& p, const TickDesc* td, int max_active, cudaStream_t st);
+void launch_alpha_step(const BcP& p, const TickDesc* td, int max_active, cudaStream_t st);
 
 // Range coder (coder.cpp:101-166): one thread per chunk, R symbols per step.
 struct CoderState { uint64_t low, range, pos, code; int err; int pad; };
 void launch_range_uniform(uint32_t* tokens, ChunkGeo geo, int t, int R, int V, uint8_t* payload,
                           const uint64_t* pay_off, const uint64_t* pay_len, CoderState* cs,
                           int n_chunks, bool decode, cudaStream_t st);
-void launch_range_step(uint32_t* tokens, ChunkGeo geo, int64_t tick, int t, int R, int V,
+void launch_range_step(uint32_t* tokens, ChunkGeo geo, int t, int R, int V,
                        const uint32_t* freq, const uint32_t* cum, int64_t cs_f, int64_t cs_c,
                        uint8_t* payload, const uint64_t* pay_off, const uint64_t* pay_len,
-                       CoderState* cs, const int* active, int n_active, bool decode,
+                       CoderState* cs, const TickDesc* td, int max_active, bool decode,
                        cudaStream_t st);
 void launch_range_finish(uint8_t* payload, const uint64_t* pay_off, CoderState* cs, int n_chunks,
                          cudaStream_t st);
@@ -146,8 +172,8 @@ struct BiGruP {
   int layers, V, T, Es, Hs, B, R;
 };
 void launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, float* work,
-                          int64_t work_cs, float* logits, int64_t lg_cs, const int* active,
-                          int n_active, cudaStream_t st);
+                          int64_t work_cs, float* logits, int64_t lg_cs, const TickDesc* td,
+                          int max_active, cudaStream_t st);
 size_t bigru_work_floats(const BiGruP& p);
 
 }  // namespace pmklc_b200
