@@ -1,0 +1,301 @@
+"""PMKLC B200 benchmark (driver contract in the task statement).
+
+One step = compress + decompress of the whole workload (the paper's Eq. 4
+throughput THP = size / (CT + DT)), device-resident input for
+`value`, host buffers through the public API for `e2e`.
+
+Default workload (N=1): BASELINE config 3 — a 100 MB synthetic genome (10
+order-k Markov segments, k in 2..5, GC bias varied, 1 % copy-repeats),
+PMKLC-S block-partitioned into W=128 data blocks, public (seeded, untrained
+SPuM) + dynamic models (the selector never enables private and public
+together below the 500 MB threshold, mixer.cpp:9-12), reference defaults
+s=k=3, t=32, bs=320, scale 4, SMP 0.05.
+
+--impl reference times the reference C++ library itself (oracle/_ref, built
+from /root/reference sources) on the host cores over a bounded sample of the
+same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Compress/decompress MB/s at 1/2/4/8 B200; bits/base vs CPU reference"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--mb", type=float, default=100.0, help="workload size in 10^6 bytes")
+    ap.add_argument("--workers", type=int, default=128, help="data blocks W")
+    ap.add_argument("--no-spum", action="store_true", help="dynamic model only (flags 4)")
+    ap.add_argument("--skip-cpu", action="store_true", help="skip the cpu_baseline leg")
+    return ap.parse_args()
+
+
+def workload(args, tmpdir):
+    import paper_2507_12805_b200 as P
+    n = int(args.mb * 1e6)
+    raw = P.synth("genome", n, 2025, 10)
+    cfg = P.CompressConfig(workers=args.workers)
+    spum = ""
+    if not args.no_spum:
+        spum = str(Path(tmpdir) / "spum_k3_t32_s4.bin")
+        P.write_bigru(spum, 3, 32, 4, 0xACE3, layers=2)
+        cfg.pub_model_path = spum
+    desc = (f"config3: {n/1e6:g} MB synthetic genome (10 order-k Markov segments k=2..5 + 1% "
+            f"repeats), PMKLC-S W={args.workers} blocks, "
+            f"{'DM only (flags 4)' if args.no_spum else 'SPuM(seeded)+DM (flags 5)'}, "
+            f"s=k=3 t=32 bs=320 scale=4 smp=0.05")
+    return raw, cfg, spum, desc
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, idx):
+        self.idx = idx
+        self.p = None
+        self.f = None
+
+    def __enter__(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        try:
+            lines = [l.split(",") for l in open(self.f.name).read().strip().splitlines() if l.strip()]
+        except Exception:
+            return None
+        if not lines:
+            return None
+        sm = [float(l[1]) for l in lines if l[1].strip().replace(".", "").isdigit()]
+        mx = [float(l[2]) for l in lines if l[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for l in lines for i in range(4)
+                          if len(l) > 5 + i and l[5 + i].strip() == "Active"})
+        loaded = [s for s in sm if s > 0.5 * max(sm)] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(lines)}
+
+
+def flush_l2(torch, buf):
+    buf.add_(1)  # 256 MiB write > 126 MB L2, between timed steps (not timed)
+
+
+def cpu_reference(raw, cfg, spum, threads, reps, warm):
+    """The reference library (oracle/_ref) on host cores over a bounded sample."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracles as O
+    R = O.ref() if O.REF_SO.exists() else O.port()
+    kind = "reference" if O.REF_SO.exists() else "port"
+    # sample: `threads` chunks of 64 batch steps each (same per-step cost as
+    # the full run: 32 warm-up + 32 model steps per chunk)
+    per_chunk = 320 * 3 * 64
+    n = min(len(raw), threads * per_chunk)
+    sample = raw[:n]
+    c = O.make_cfg(workers=threads, pub_path=spum or None)
+    times = []
+    blob = b""
+    for i in range(warm + reps):
+        t0 = time.perf_counter()
+        blob = R.compress(sample, c)
+        t1 = time.perf_counter()
+        out = R.decompress(blob, pub_path=spum or None, workers=threads)
+        t2 = time.perf_counter()
+        assert out == sample
+        if i >= warm:
+            times.append((t1 - t0, t2 - t1))
+    ct = sum(t[0] for t in times) / len(times)
+    dt = sum(t[1] for t in times) / len(times)
+    return {"value": n / 1e6 / (ct + dt), "unit": "MB/s", "cores": threads, "kind": kind,
+            "sample": f"first {n} B of the workload, W={threads} blocks x 64 batch steps, "
+                      f"{'SPuM+DM' if spum else 'DM'}; compress {ct:.2f} s + decompress {dt:.2f} s",
+            "compress_MBps": n / 1e6 / ct, "decompress_MBps": n / 1e6 / dt,
+            "bits_per_base": 8.0 * len(blob) / n}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    tmp = tempfile.mkdtemp(prefix="pmklc_bench_")
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        raw, cfg, spum, desc = workload(args, tmp)
+        threads = min(os.cpu_count() or 1, 256, args.workers)
+        r = cpu_reference(raw, cfg, spum, threads, args.steps, args.warmup)
+        line = {"metric": METRIC, "value": r["value"], "unit": "MB/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1000.0 * (r["value"] and (len(raw[:threads * 320 * 3 * 64]) / 1e6 / r["value"])),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "impl": "reference",
+                "config": {"workload": desc, "parallelism": f"{threads} host threads"},
+                "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": r["value"], "unit": "MB/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0},
+                "compress_MBps": r["compress_MBps"], "decompress_MBps": r["decompress_MBps"],
+                "bits_per_base_sample": r["bits_per_base"]}
+        print(json.dumps(line))
+        return
+
+    import torch
+    import paper_2507_12805_b200 as P
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = local
+    raw, cfg, spum, desc = workload(args, tmp)
+    cfg.device = dev
+    n = len(raw)
+    d_raw = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(f"cuda:{dev}")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+
+    def step_device():
+        tm_c, tm_d = P.Timing(), P.Timing()
+        blob = P.compress_device(d_raw.data_ptr(), n, cfg, tm_c)
+        dptr, dlen = P.decompress_to_device(blob, spum, dev, tm_d)
+        P.device_free(dptr)
+        return blob, tm_c, tm_d
+
+    # correctness of the measured path: lossless round trip
+    blob, _, _ = step_device()
+    assert P.decompress(blob, spum, device=dev) == raw, "round trip mismatch"
+
+    for _ in range(max(args.warmup - 1, 0)):
+        step_device()
+
+    ct = dt = 0.0
+    launches = 0
+    clk = Clocks(dev)
+    times = []
+    with clk:
+        for _ in range(args.steps):
+            flush_l2(torch, flush)
+            if world > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record()
+            tm_c, tm_d = P.Timing(), P.Timing()
+            blob = P.compress_device(d_raw.data_ptr(), n, cfg, tm_c)
+            e1.record()
+            dptr, dlen = P.decompress_to_device(blob, spum, dev, tm_d)
+            e2.record()
+            torch.cuda.synchronize()
+            P.device_free(dptr)
+            c_ms, d_ms = e0.elapsed_time(e1), e1.elapsed_time(e2)
+            times.append(c_ms + d_ms)
+            ct += c_ms
+            dt += d_ms
+            launches += tm_c.kernel_launches + tm_d.kernel_launches
+    step_ms = max(times) if world == 1 else None
+    tot_ms = ct + dt
+    if world > 1:
+        t = torch.tensor([tot_ms], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = world * n * args.steps / 1e6 / (tot_ms / 1000.0)
+
+    # e2e through the public host API (host buffers, H2D/D2H inside)
+    e_times = []
+    for _ in range(max(1, args.steps // 2)):
+        flush_l2(torch, flush)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        b2 = P.compress(raw, cfg)
+        back = P.decompress(b2, spum, device=dev)
+        torch.cuda.synchronize()
+        e_times.append(time.perf_counter() - t0)
+        assert back == raw
+    e2e_val = world * n / 1e6 / (sum(e_times) / len(e_times))
+
+    line = None
+    if rank == 0:
+        # roofline: top kernel of the launch list (k_gemm_nt, dWk|dWv over R*t rows),
+        # live CUDA-event timing at the workload's concurrency, against the
+        # measured non-FMA FP32 issue peak (MEASURED_PEAKS.json has no FP32 figure)
+        chunks = min(args.workers, 64)
+        k_ms, k_fl, k_by = P.bench_kernel("gemm_nt", chunks, iters=10, device=dev)
+        p_ms, p_fl, _ = P.bench_kernel("fp32_peak", 1, iters=10, device=dev)
+        peak_tf = p_fl / (p_ms / 1000.0) / 1e12
+        ach_tf = k_fl / (k_ms / 1000.0) / 1e12
+        traffic = None
+        tf = ROOT / "profiles" / "roofline_traffic.json"
+        if tf.exists():
+            try:
+                traffic = json.loads(tf.read_text()).get("gemm_nt_dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        cpu = None
+        if not args.skip_cpu and world == 1:
+            threads = min(os.cpu_count() or 1, 256, args.workers)
+            try:
+                cpu_full = cpu_reference(raw, cfg, spum, threads, 1, 0)
+                cpu = {k: cpu_full[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            except Exception as e:  # report, do not hide
+                cpu = {"value": None, "unit": "MB/s", "cores": threads, "kind": "reference",
+                       "sample": f"failed: {e}"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "MB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": desc, "bytes": n, "parallelism": f"{world} GPU replica(s)",
+                       "l2": "256 MiB flush write between timed steps"},
+            "compress_MBps": world * n * args.steps / 1e6 / (ct / 1000.0),
+            "decompress_MBps": world * n * args.steps / 1e6 / (dt / 1000.0),
+            "bits_per_base": 8.0 * len(blob) / n,
+            "container_bytes": len(blob),
+            "roofline": {"kernel": "k_gemm_nt (dWk|dbk + dWv|dbv over R*t=10240 rows, "
+                                   f"{chunks} chunks)",
+                         "bound": "fp32", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                         "frac": ach_tf / peak_tf, "traffic": traffic,
+                         "peak_source": "live non-FMA FP32 microbenchmark (MEASURED_PEAKS.json "
+                                        "has no FP32 figure); EXACT mode cannot use tensor cores",
+                         "avg_launch_ms": k_ms, "flops_per_launch": k_fl},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": "MB/s", "h2d_bytes_per_step": n + len(blob),
+                    "d2h_bytes_per_step": len(blob) + n},
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -125,6 +125,19 @@ int pmklc_schedule(const uint64_t* lens, size_t n_chunks, uint32_t bs, uint32_t 
                    uint16_t smp_per_myriad, int64_t* offset, int64_t* src, uint64_t* src_steps,
                    uint64_t* model_steps, int64_t* ticks);
 
+/* seeded (untrained) BiGRU predictor file in the reference's PMKW format
+ * (BiGruModel + serialize_model, models.cpp:38-51,159-173); layers = 2 is a
+ * SPuM as the reference tests write it (acceptance.cpp:58-69). Host-only. */
+int pmklc_write_bigru(const char* path, uint32_t k, uint32_t t, uint32_t scale, int32_t layers,
+                      uint64_t seed, uint64_t* fingerprint);
+
+/* live microbenchmark of a hot kernel at the engine's shapes over `chunks`
+ * chunks ("gemm_nt", "gemm_ffn", "fp32_peak"): average ms per launch and the
+ * algorithmic flops / bytes of one launch (bench.py roofline) */
+int pmklc_bench_kernel(const char* name, int32_t device, uint32_t chunks, uint32_t scale,
+                       uint32_t rows, uint32_t t, int32_t iters, double* avg_ms, double* flops,
+                       double* bytes);
+
 void pmklc_free(void* p);
 void pmklc_device_free(void* d_p);
 const char* pmklc_last_error(void);

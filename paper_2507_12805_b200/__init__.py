@@ -67,7 +67,7 @@ EXPORTS = [
     "pmklc_skmer_encode_packed_device", "pmklc_free", "pmklc_device_free", "pmklc_last_error",
     "pmklc_errc_name", "pmklc_version", "pmklc_synth_markov3", "pmklc_synth_uniform",
     "pmklc_synth_genome", "pmklc_synth_species", "pmklc_synth_packed_codes", "pmklc_plan_chunks",
-    "pmklc_schedule", "pmklc_quantize",
+    "pmklc_schedule", "pmklc_quantize", "pmklc_write_bigru", "pmklc_bench_kernel",
 ]
 
 _lib = None
@@ -303,6 +303,22 @@ def synth(kind: str, n: int, seed: int, extra: int = 0) -> bytes:
     else:
         raise ValueError(kind)
     return bytes(buf)[:n]
+
+
+def write_bigru(path: str, k: int, t: int, scale: int, seed: int, layers: int = 2) -> int:
+    """Write a seeded (untrained) BiGRU model file (PMKW); returns its FNV-1a fingerprint."""
+    fp = C.c_uint64()
+    _check(lib().pmklc_write_bigru(path.encode(), k, t, scale, layers, C.c_uint64(seed), C.byref(fp)))
+    return fp.value
+
+
+def bench_kernel(name: str, chunks: int, scale: int = 4, rows: int = 320, t: int = 32,
+                 iters: int = 20, device: int = 0):
+    """Live microbenchmark: (avg_ms per launch, flops per launch, bytes per launch)."""
+    ms, fl, by = C.c_double(), C.c_double(), C.c_double()
+    _check(lib().pmklc_bench_kernel(name.encode(), device, chunks, scale, rows, t, iters,
+                                    C.byref(ms), C.byref(fl), C.byref(by)))
+    return ms.value, fl.value, by.value
 
 
 def version() -> str:

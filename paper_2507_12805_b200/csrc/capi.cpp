@@ -1,6 +1,7 @@
 // extern "C" boundary (include/pmklc_b200.h) over the B200 engine.
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -253,6 +254,30 @@ int pmklc_schedule(const uint64_t* lens, size_t n, uint32_t bs, uint32_t t, uint
       model_steps[i] = sc.M[i];
     }
     *ticks = sc.ticks;
+  });
+}
+
+int pmklc_write_bigru(const char* path, uint32_t k, uint32_t t, uint32_t scale, int32_t layers,
+                      uint64_t seed, uint64_t* fingerprint) {
+  return guard([&] {
+    const Bytes b = seeded_bigru_file(k, t, scale, layers, seed);
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) raise(errc::io_error, std::string("cannot create ") + path);
+    const size_t put = std::fwrite(b.data(), 1, b.size(), f);
+    const bool ok = put == b.size() && std::fclose(f) == 0;
+    if (!ok) raise(errc::io_error, std::string("short write on ") + path);
+    if (fingerprint) *fingerprint = fnv1a64(b);
+  });
+}
+
+int pmklc_bench_kernel(const char* name, int32_t device, uint32_t chunks, uint32_t scale,
+                       uint32_t rows, uint32_t t, int32_t iters, double* avg_ms, double* flops,
+                       double* bytes) {
+  return guard([&] {
+    const KernelBench kb = bench_kernel(name, device, chunks, scale, rows, t, iters);
+    *avg_ms = kb.avg_ms;
+    if (flops) *flops = kb.flops;
+    if (bytes) *bytes = kb.bytes;
   });
 }
 

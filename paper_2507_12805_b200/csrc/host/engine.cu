@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 
@@ -26,41 +27,67 @@ namespace {
       raise(errc::cuda_error, std::string(#x) + ": " + cudaGetErrorString(e_));    \
   } while (0)
 
+// Device buffers come from the device's default memory pool through the
+// stream-ordered allocator; the pool keeps freed memory (release threshold =
+// max), so repeated calls reuse HBM instead of paying cudaMalloc/cudaFree.
+void configure_pool(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = ~uint64_t(0);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
+
+thread_local cudaStream_t g_alloc_stream = nullptr;  // the calling engine's stream
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  cudaStream_t st = nullptr;
   DBuf() = default;
   explicit DBuf(size_t count) { alloc(count); }
   void alloc(size_t count) {
     free();
     n = count;
-    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+    st = g_alloc_stream;
+    if (count) CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), st));
   }
   void free() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, st);
     p = nullptr;
     n = 0;
   }
   ~DBuf() { free(); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  void upload(const T* h, size_t count, cudaStream_t st, size_t at = 0) {
-    if (count) CK(cudaMemcpyAsync(p + at, h, count * sizeof(T), cudaMemcpyHostToDevice, st));
+  void upload(const T* h, size_t count, cudaStream_t s, size_t at = 0) {
+    if (count) CK(cudaMemcpyAsync(p + at, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
   }
-  void zero(cudaStream_t st) {
-    if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), st));
+  void zero(cudaStream_t s) {
+    if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
   }
 };
 
 struct Stream {
   cudaStream_t s = nullptr;
+  cudaStream_t prev = nullptr;
   explicit Stream(int device) {
     CK(cudaSetDevice(device));
+    configure_pool(device);
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    prev = g_alloc_stream;
+    g_alloc_stream = s;
   }
   ~Stream() {
-    if (s) cudaStreamDestroy(s);
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+    g_alloc_stream = prev;
   }
 };
 
@@ -1051,6 +1078,102 @@ void skmer_encode_packed_device(const uint8_t* d_packed, uint64_t n_bases, uint3
   const uint64_t m = token_count(n_bases, s, k);
   launch_skmer_encode_packed(d_packed, n_bases, s, k, d_tokens, m, static_cast<cudaStream_t>(stream));
   check_launch();
+}
+
+Bytes seeded_bigru_file(uint32_t k, uint32_t t, uint32_t scale, int layers, uint64_t seed) {
+  if (k < 1 || k > 8) raise(errc::config_invalid, "k out of range");
+  const Dims d = Dims::make(uint32_t(1) << (2 * k), t, scale);
+  return BiGru::seeded(d, layers, seed).serialize();
+}
+
+namespace {
+// Long independent FMUL+FADD chains: 8 per thread, the non-FMA FP32 issue ceiling.
+__global__ void k_fp32_peak(float* out, int iters, float a, float b) {
+  float x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = float(threadIdx.x + i);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = __fadd_rn(__fmul_rn(x[i], a), b);
+  }
+  float s = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 1234.5f) out[0] = s;
+}
+}  // namespace
+
+KernelBench bench_kernel(const std::string& name, int device, uint32_t chunks, uint32_t scale,
+                         uint32_t R, uint32_t t, int iters) {
+  CK(cudaSetDevice(device));
+  Stream stream(device);
+  cudaStream_t st = stream.s;
+  KernelBench kb;
+  Event e0, e1;
+  if (name == "fp32_peak") {
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    DBuf<float> out(1);
+    const int blocks = sms * 8, threads = 256, inner = 4096;
+    k_fp32_peak<<<blocks, threads, 0, st>>>(out.p, inner, 0.999f, 0.001f);  // warm-up
+    e0.record(st);
+    for (int i = 0; i < iters; ++i) k_fp32_peak<<<blocks, threads, 0, st>>>(out.p, inner, 0.999f, 0.001f);
+    e1.record(st);
+    check_launch();
+    CK(cudaStreamSynchronize(st));
+    kb.avg_ms = Event::ms(e0, e1) / iters;
+    kb.flops = 2.0 * 8.0 * double(inner) * blocks * threads;
+    return kb;
+  }
+  const Dims d = Dims::make(64, t, scale);
+  const DmLayout lay(d);
+  const int64_t P = int64_t(lay.total);
+  const int H = int(d.dh), F = int(d.df), E = int(d.de);
+  const int64_t RT = int64_t(R) * t;
+  DBuf<int> act(chunks);
+  std::vector<int> ids(chunks);
+  for (uint32_t i = 0; i < chunks; ++i) ids[i] = int(i);
+  act.upload(ids.data(), chunks, st);
+  DBuf<TickDesc> td(1);
+  const TickDesc t0{0, act.p, nullptr, int(chunks), 0};
+  td.upload(&t0, 1, st);
+  DBuf<float> w(size_t(chunks) * P), g(size_t(chunks) * P);
+  w.zero(st);
+  g.zero(st);
+  std::function<void()> launch;
+  DBuf<float> a, b, c;
+  const TickDesc* tdp = td.p;
+  if (name == "gemm_nt") {
+    a.alloc(size_t(chunks) * RT * E);
+    b.alloc(size_t(chunks) * RT * H);
+    CK(cudaMemsetAsync(a.p, 0, a.n * 4, st));
+    CK(cudaMemsetAsync(b.p, 0, b.n * 4, st));
+    const NtP pk{a.p, b.p, g.p + lay.off(DmLayout::KW), RT * E, RT * H, P, RT, RT, H, E, H, int(RT)};
+    NtP pv = pk;
+    pv.C = g.p + lay.off(DmLayout::VW);
+    launch = [=]() { launch_gemm_nt(pk, &pv, tdp, int(chunks), st); };
+    kb.flops = 2.0 * 2.0 * double(E + 1) * H * double(RT) * chunks;
+    kb.bytes = 2.0 * (double(RT) * (E + H)) * 4.0 * chunks;  // each operand row read once
+  } else if (name == "gemm_ffn") {
+    a.alloc(size_t(chunks) * R * F);
+    c.alloc(size_t(chunks) * R * H);
+    CK(cudaMemsetAsync(a.p, 0, a.n * 4, st));
+    const GemmP gp{a.p, int64_t(R) * F, F, w.p + lay.off(DmLayout::UW), P, H, c.p, int64_t(R) * H, H,
+                   w.p + lay.off(DmLayout::UB), P, nullptr, 0, 0, int(R), H, F, 0, 1, 1};
+    launch = [=]() { launch_gemm(gp, false, false, tdp, int(chunks), st); };
+    kb.flops = 2.0 * double(R) * H * F * chunks;
+    kb.bytes = (double(R) * F + double(F) * H + double(R) * H) * 4.0 * chunks;
+  } else {
+    raise(errc::config_invalid, "unknown kernel " + name);
+  }
+  launch();
+  e0.record(st);
+  for (int i = 0; i < iters; ++i) launch();
+  e1.record(st);
+  check_launch();
+  CK(cudaStreamSynchronize(st));
+  kb.avg_ms = Event::ms(e0, e1) / iters;
+  return kb;
 }
 
 }  // namespace pmklc_b200

@@ -81,4 +81,18 @@ std::vector<uint32_t> skmer_encode_codes(const uint8_t* codes, uint64_t n, uint3
 void skmer_encode_packed_device(const uint8_t* d_packed, uint64_t n_bases, uint32_t s, uint32_t k,
                                 uint32_t* d_tokens, void* stream);
 
+// PMKW bytes of a seeded (untrained) BiGRU predictor (BiGruModel ctor +
+// serialize_model, models.cpp:38-51,159-173): the SPuM file the reference
+// tests and benchmarks use (acceptance.cpp:58-69). Host-only.
+Bytes seeded_bigru_file(uint32_t k, uint32_t t, uint32_t scale, int layers, uint64_t seed);
+
+// Live microbenchmarks for bench.py's roofline: average device time of one
+// launch of a hot kernel at the engine's real shapes over `chunks` chunks.
+//   "gemm_nt"  : dWk|dbk + dWv|dbv reduction over R*t rows (k_gemm_nt)
+//   "gemm_ffn" : ffn.outer forward, relu(pre)[R,F] x W2[F,H] (tiled exact GEMM)
+//   "fp32_peak": FMUL+FADD issue-rate kernel (no FMA), flops = 2 per MAC
+struct KernelBench { double avg_ms = 0, flops = 0, bytes = 0; };
+KernelBench bench_kernel(const std::string& name, int device, uint32_t chunks, uint32_t scale,
+                         uint32_t R, uint32_t t, int iters);
+
 }  // namespace pmklc_b200

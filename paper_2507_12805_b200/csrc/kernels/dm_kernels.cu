@@ -188,41 +188,21 @@ void gemm_dispatch(const GemmP& p, const TickDesc* td, int max_active, cudaStrea
 
 // ------------------------------------------------------------------ NT reduction
 
-// TMA bulk-copy ring (cp.async.bulk + mbarrier complete_tx): one elected
-// thread streams each stage's operand rows (1 A row + up to 64 B rows of BK
-// floats) into shared memory; consumers wait on the stage's mbarrier phase.
-constexpr int kNtThreads = 64, kNtBK = 64, kNtStages = 4;
-constexpr int kNtSB = kNtBK + 4;  // padded B row: LDS.128 of 32 rows = 4 wavefronts
-constexpr size_t kNtSmem =
-    size_t(kNtStages) * (kNtBK + kNtThreads * kNtSB) * sizeof(float) + kNtStages * sizeof(uint64_t);
-
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes));
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n.reg .pred P1;\nWAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(phase));
-}
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
+__device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem));
 }
 
-// VEC: every row segment is 16-byte aligned and a multiple of 16 bytes
-// (host-checked), so TMA bulk copies stream them; otherwise 4-byte cp.async.
+// 64 threads = 64 outputs (one m, 64 n); K-tiles of 64 staged by 16-byte
+// cp.async (every thread streams 16 B-row chunks + a quarter of the A row per
+// tile with pointer-increment addressing) into a 4-deep ring.
+constexpr int kNtThreads = 64, kNtBK = 64, kNtStages = 4;
+constexpr int kNtSB = kNtBK + 4;  // padded B row: LDS.128 of 32 rows = 4 wavefronts
+constexpr size_t kNtSmem = size_t(kNtStages) * (kNtBK + kNtThreads * kNtSB) * sizeof(float);
+
+// VEC: rows 16-byte aligned, K multiple of 4 (host-checked); else 4-byte copies.
 template <bool VEC>
 __global__ void __launch_bounds__(kNtThreads) k_gemm_nt(NtP p0, NtP p1, const TickDesc* __restrict__ td) {
   extern __shared__ __align__(128) float sm[];
@@ -248,59 +228,41 @@ __global__ void __launch_bounds__(kNtThreads) k_gemm_nt(NtP p0, NtP p1, const Ti
   float* C = Cb + c * c_cs;
   float* As = sm;
   float* Bs = sm + kNtStages * kNtBK;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(Bs + kNtStages * kNtThreads * kNtSB);
   const int ntiles = (K + kNtBK - 1) / kNtBK;
   const int nrows = min(kNtThreads, N - n0);
+  // this thread's copy slots: rows r0 + 4q (q < 16), 16-byte chunk v (VEC path)
+  const int v = tid & 15, r0 = tid >> 4;
 
-  if (VEC && tid == 0) {
-    for (int s = 0; s < kNtStages; ++s) mbar_init(&bar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
-  }
-  __syncthreads();
-
-  // stage `tile`: thread 0 arms the stage barrier with the byte count before
-  // the block barrier; afterwards every thread issues (at most) one row copy.
-  auto arm = [&](int tile) {
-    if (VEC && tid == 0 && tile < ntiles) {
-      const uint32_t rb = uint32_t(min(kNtBK, K - tile * kNtBK)) * 4u;
-      mbar_expect_tx(&bar[tile % kNtStages], rb * uint32_t(nrows + (ones ? 0 : 1)));
-    }
-  };
   auto load = [&](int tile) {
-    if (tile >= ntiles) {
-      if (!VEC) cp_async_commit();
-      return;
+    if (tile < ntiles) {
+      const int st = tile % kNtStages, k0 = tile * kNtBK, kc = min(kNtBK, K - k0);
+      float* as = As + st * kNtBK;
+      float* bs = Bs + st * kNtThreads * kNtSB;
+      if (VEC && kc == kNtBK) {
+        if (!ones && tid < 16) cp_async16(as + 4 * v, A + k0 + 4 * v);
+        const float* src = B + int64_t(r0) * ldb + k0 + 4 * v;
+        float* dst = bs + r0 * kNtSB + 4 * v;
+#pragma unroll
+        for (int q = 0; q < kNtThreads / 4; ++q)
+          if (r0 + 4 * q < nrows) cp_async16(dst + q * 4 * kNtSB, src + int64_t(q) * 4 * ldb);
+      } else {
+        if (!ones)
+          for (int i = tid; i < kc; i += kNtThreads) cp_async4(as + i, A + k0 + i);
+        for (int rr = 0; rr < nrows; ++rr)
+          for (int i = tid; i < kc; i += kNtThreads) cp_async4(bs + rr * kNtSB + i, B + int64_t(rr) * ldb + k0 + i);
+      }
     }
-    const int st = tile % kNtStages, k0 = tile * kNtBK, kc = min(kNtBK, K - k0);
-    float* as = As + st * kNtBK;
-    float* bs = Bs + st * kNtThreads * kNtSB;
-    if (VEC) {
-      const uint32_t rb = uint32_t(kc) * 4u;
-      if (tid < nrows) tma_bulk_g2s(bs + tid * kNtSB, B + int64_t(tid) * ldb + k0, rb, &bar[st]);
-      if (!ones && tid == kNtThreads - 1) tma_bulk_g2s(as, A + k0, rb, &bar[st]);
-    } else {
-      if (!ones)
-        for (int i = tid; i < kc; i += kNtThreads) cp_async4(as + i, A + k0 + i);
-      for (int rr = 0; rr < nrows; ++rr)
-        for (int i = tid; i < kc; i += kNtThreads) cp_async4(bs + rr * kNtSB + i, B + int64_t(rr) * ldb + k0 + i);
-      cp_async_commit();
-    }
+    cp_async_commit();  // one group per tile slot, possibly empty
   };
 
   float acc = (n < N) ? C[int64_t(m) * ldc + n] : 0.0f;
 #pragma unroll
-  for (int s = 0; s < kNtStages - 1; ++s) arm(s);
-  __syncthreads();
-#pragma unroll
   for (int s = 0; s < kNtStages - 1; ++s) load(s);
   for (int tile = 0; tile < ntiles; ++tile) {
-    const int st = tile % kNtStages;
-    if (VEC) mbar_wait(&bar[st], uint32_t(tile / kNtStages) & 1u);
-    else cp_async_wait<kNtStages - 2>();
-    arm(tile + kNtStages - 1);
-    __syncthreads();  // everyone is past tile-1: its stage may be refilled
+    cp_async_wait<kNtStages - 2>();
+    __syncthreads();  // tile landed for everyone; everyone is past tile-1
     load(tile + kNtStages - 1);
-    const int kc = min(kNtBK, K - tile * kNtBK);
+    const int st = tile % kNtStages, kc = min(kNtBK, K - tile * kNtBK);
     const float* as = As + st * kNtBK;
     const float* bs = Bs + (st * kNtThreads + tid) * kNtSB;
     if (tid < nrows) {
@@ -330,7 +292,7 @@ __global__ void __launch_bounds__(kNtThreads) k_gemm_nt(NtP p0, NtP p1, const Ti
       }
     }
   }
-  if (!VEC) cp_async_wait<0>();
+  cp_async_wait<0>();
   if (n < N) C[int64_t(m) * ldc + n] = acc;
 }
 
