@@ -149,25 +149,49 @@ void unpack_tokens(const uint8_t* b, size_t bn, uint32_t k, uint32_t* out, uint6
   }
 }
 
-// A frozen BiGRU predictor resident on the device.
+// A frozen BiGRU predictor resident on the device, plus its layer-0
+// input-projection table xi0[dir][gate][tok][j] = b_i{gate}[j] +
+// sum_p emb[tok][p]*W_i{gate}[p][j] (ascending p; Linear forward order,
+// layers.cpp:170-174 / tensor.cpp:29-36), computed once on the host with the
+// same IEEE single operations (host code is built with -ffp-contract=off).
 struct DevBiGru {
   BiGru host;
-  DBuf<float> w;
+  DBuf<float> w, xi0;
   DBuf<int64_t> offs;
+  std::vector<int64_t> hoffs;
   void upload(BiGru m, cudaStream_t st) {
     host = std::move(m);
     w.alloc(host.total);
     w.upload(host.w.data(), host.total, st);
-    std::vector<int64_t> o;
-    for (const ParamDesc& p : host.ps) o.push_back(int64_t(p.off));
-    offs.alloc(o.size());
-    offs.upload(o.data(), o.size(), st);
+    hoffs.clear();
+    for (const ParamDesc& p : host.ps) hoffs.push_back(int64_t(p.off));
+    offs.alloc(hoffs.size());
+    offs.upload(hoffs.data(), hoffs.size(), st);
+    const int64_t V = host.d.V, Es = host.d.se, H = host.d.sh;
+    std::vector<float> tab(size_t(2 * 3 * V * H));
+    const float* emb = host.w.data() + host.ps[0].off;
+    for (int dir = 0; dir < 2; ++dir)
+      for (int g = 0; g < 3; ++g) {
+        const float* W = host.w.data() + host.ps[size_t(host.idx(0, dir, BiGru::WIR + g))].off;
+        const float* b = host.w.data() + host.ps[size_t(host.idx(0, dir, BiGru::BIR + g))].off;
+        float* out = tab.data() + size_t((dir * 3 + g) * V * H);
+        for (int64_t tok = 0; tok < V; ++tok)
+          for (int64_t j = 0; j < H; ++j) {
+            float acc = b[j];
+            for (int64_t p = 0; p < Es; ++p) acc = acc + emb[tok * Es + p] * W[p * H + j];
+            out[tok * H + j] = acc;
+          }
+      }
+    xi0.alloc(tab.size());
+    xi0.upload(tab.data(), tab.size(), st);
     CK(cudaStreamSynchronize(st));
   }
   BiGruP params(int R) const {
     BiGruP p;
     p.w = w.p;
     p.offs = offs.p;
+    p.hoffs = hoffs.data();
+    p.xi0 = xi0.p;
     p.layers = host.layers;
     p.V = int(host.d.V);
     p.T = int(host.d.T);
@@ -443,11 +467,11 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     // ---------------- static predictors
     if (run.flags & 1) {
       launch_bigru_predict(run.pub->params(R), ctx.p, s_ctx, bwork.p, s_bw, lu.p, s_rv, act, na, st);
-      run.launches += run.pub->host.layers + 2;
+      run.launches += 3 * run.pub->host.layers + 1;
     }
     if (run.flags & 2) {
       launch_bigru_predict(run.priv->params(R), ctx.p, s_ctx, bwork.p, s_bw, lr.p, s_rv, act, na, st);
-      run.launches += run.priv->host.layers + 2;
+      run.launches += 3 * run.priv->host.layers + 1;
     }
     // ---------------- mix + quantize + code
     MixP mp{lu.p, lr.p, lm.p, s_rv, probs.p, freq.p, cum.p, s_rv, s_cum, w.p, P, oA, sc.p,
@@ -846,6 +870,7 @@ void decompress_impl(const uint8_t* blob, size_t n, const std::string& pub_path,
     raise(errc::corrupt_stream, "token count does not match the original length");
 
   DBuf<uint32_t> d_tok(total + 8);
+  d_tok.zero(st);
   Plan plan;
   plan.bs = c.bs;
   plan.t = c.t;

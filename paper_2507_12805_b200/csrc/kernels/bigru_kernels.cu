@@ -2,12 +2,15 @@
 // Reference: BiGruModel::forward (core/src/models.cpp:53-73), Gru::forward
 // (core/src/layers.cpp:213-260), BiGru::forward/final_state (344-399).
 //
-// The recurrence is serial in time, so parallelism is rows x directions: one
-// warp runs one (row, direction) sequence, lane j owning hidden units j,
-// j+32, ...; the previous hidden state and the current input are staged in
-// shared memory so every lane reads them as broadcasts. Each gate pre-activation
-// is accumulated exactly as the reference does: bias, then ascending input
-// terms, then (r,z gates) the recurrent bias and ascending hidden terms.
+// Per GRU step and unit j the reference evaluates (layers.cpp:229-258)
+//   ar = b_ir + x.W_ir ; ar += b_hr ; ar += h.W_hr        (ascending indices)
+//   az = b_iz + x.W_iz ; az += b_hz ; az += h.W_hz
+//   hh = b_hn + h.W_hn ; an = b_in + x.W_in
+//   r = sig(ar), z = sig(az), n = tanh(an + r*hh), h' = (1-z)*n + z*h
+// The x-terms never depend on h: layer 0's are a per-token table (xi0),
+// deeper layers' are one batched exact GEMM over all R*t positions. The
+// recurrent part runs one warp per (row, direction), lane j = unit j, with
+// its three W_h* columns in registers and h broadcast from shared memory.
 #include <cstdint>
 
 #include "detmath.cuh"
@@ -18,135 +21,286 @@ namespace pmklc_b200 {
 namespace {
 
 enum { WIR, WIZ, WIN, WHR, WHZ, WHN, BIR, BIZ, BIN, BHR, BHZ, BHN, NG };
-constexpr int kWarps = 4;
-constexpr int kMaxH = 128;   // sp_hidden at scale 1
-constexpr int kMaxIn = 256;  // 2*sp_hidden at scale 1
+constexpr int kRecWarps = 8;
 
 __device__ __forceinline__ int64_t poff(const int64_t* offs, int l, int dir, int t) {
   return offs[1 + (l * 2 + dir) * NG + t];
 }
 
-// in_buf: layer input [R,T,in] (nullptr for layer 0: gathered from the embedding)
-__global__ void __launch_bounds__(kWarps * 32) k_bigru_layer(BiGruP p, int l, const uint32_t* ctx,
-                                                             int64_t ctx_cs, const float* in_buf,
-                                                             float* out_buf, float* fin,
-                                                             int64_t work_cs,
-                                                             const TickDesc* __restrict__ td) {
-  __shared__ float sx[kWarps][kMaxIn];
-  __shared__ float sh[kWarps][kMaxH];
+// xi: layer >= 1 input projections of this chunk, [2 dirs][3 gates][R*T][Hs]
+// out: layer output [R][T][2Hs]; fin (last layer): [R][2Hs]
+// One warp runs kRPW rows of one direction: the W_h* columns held in
+// registers serve every row, and the rows' chains interleave (ILP).
+constexpr int kRPW = 2;
+template <int HS>
+__global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
+    BiGruP p, int l, const uint32_t* __restrict__ ctx, int64_t ctx_cs, const float* __restrict__ xi,
+    float* out, float* fin, int64_t work_cs, const TickDesc* __restrict__ td) {
+  __shared__ __align__(16) float sh[kRecWarps][kRPW][2][32];
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wg = blockIdx.x * kWarps + wl;
-  if (wg >= p.R * 2) return;
-  const int r = wg >> 1, dir = wg & 1;
-  const int H = p.Hs, T = p.T, in = (l == 0) ? p.Es : 2 * p.Hs;
+  const int g = blockIdx.x * kRecWarps + wl;  // = (row group, dir)
+  const int ngroups = (p.R + kRPW - 1) / kRPW;
+  if (g >= ngroups * 2) return;
+  const int r0 = (g >> 1) * kRPW, dir = g & 1, T = p.T, H = HS;
+  const int64_t RT = int64_t(p.R) * T;
   const float* W = p.w;
-  const float *wir = W + poff(p.offs, l, dir, WIR), *wiz = W + poff(p.offs, l, dir, WIZ),
-              *win = W + poff(p.offs, l, dir, WIN), *whr = W + poff(p.offs, l, dir, WHR),
-              *whz = W + poff(p.offs, l, dir, WHZ), *whn = W + poff(p.offs, l, dir, WHN);
-  const float *bir = W + poff(p.offs, l, dir, BIR), *biz = W + poff(p.offs, l, dir, BIZ),
-              *bin = W + poff(p.offs, l, dir, BIN), *bhr = W + poff(p.offs, l, dir, BHR),
-              *bhz = W + poff(p.offs, l, dir, BHZ), *bhn = W + poff(p.offs, l, dir, BHN);
-  const float* emb = W + p.offs[0];
-  const uint32_t* cr = ctx + c * ctx_cs + int64_t(r) * T;
-  const float* inr = in_buf ? in_buf + c * work_cs + int64_t(r) * T * in : nullptr;
-  float* outr = out_buf + c * work_cs + int64_t(r) * T * 2 * H;
-  for (int j = lane; j < H; j += 32) sh[wl][j] = 0.0f;  // h0 = 0
+  const float* whr = W + poff(p.offs, l, dir, WHR);
+  const float* whz = W + poff(p.offs, l, dir, WHZ);
+  const float* whn = W + poff(p.offs, l, dir, WHN);
+  const int j = lane;
+  const bool act = j < H;
+  float wr[HS], wz[HS], wn[HS];
+#pragma unroll
+  for (int q = 0; q < HS; ++q) {
+    wr[q] = act ? whr[q * H + j] : 0.f;
+    wz[q] = act ? whz[q * H + j] : 0.f;
+    wn[q] = act ? whn[q * H + j] : 0.f;
+  }
+  float bhr = 0.f, bhz = 0.f, bhn = 0.f;
+  if (act) {
+    bhr = W[poff(p.offs, l, dir, BHR) + j];
+    bhz = W[poff(p.offs, l, dir, BHZ) + j];
+    bhn = W[poff(p.offs, l, dir, BHN) + j];
+  }
+  bool rv_ok[kRPW];
+#pragma unroll
+  for (int u = 0; u < kRPW; ++u) {
+    rv_ok[u] = r0 + u < p.R;
+    if (act) sh[wl][u][0][j] = 0.0f;  // h0 = 0
+  }
+  const float* xr = xi ? xi + c * work_cs + int64_t(dir) * 3 * RT * H : nullptr;
+  const float* t0 = p.xi0 + int64_t(dir) * 3 * p.V * H;  // layer-0 tables [3][V][H]
   __syncwarp();
+  int cur = 0;
   for (int step = 0; step < T; ++step) {
-    const int tt = dir ? (T - 1 - step) : step;  // bwd direction reads time-reversed input
-    for (int q = lane; q < in; q += 32)
-      sx[wl][q] = inr ? inr[int64_t(tt) * in + q] : emb[int64_t(cr[tt]) * p.Es + q];
+    const int tt = dir ? (T - 1 - step) : step;  // bwd direction consumes time-reversed input
+    float ar[kRPW], az[kRPW], an[kRPW], hh[kRPW];
+#pragma unroll
+    for (int u = 0; u < kRPW; ++u) {
+      const int r = rv_ok[u] ? r0 + u : r0;
+      if (l == 0) {
+        const int64_t tok = ctx[c * ctx_cs + int64_t(r) * T + tt];
+        ar[u] = act ? t0[tok * H + j] : 0.f;
+        az[u] = act ? t0[int64_t(p.V) * H + tok * H + j] : 0.f;
+        an[u] = act ? t0[2 * int64_t(p.V) * H + tok * H + j] : 0.f;
+      } else {
+        const int64_t pos = (int64_t(r) * T + tt) * H + j;
+        ar[u] = act ? xr[pos] : 0.f;
+        az[u] = act ? xr[RT * H + pos] : 0.f;
+        an[u] = act ? xr[2 * RT * H + pos] : 0.f;
+      }
+      ar[u] = fadd(ar[u], bhr);
+      az[u] = fadd(az[u], bhz);
+      hh[u] = bhn;
+    }
+#pragma unroll
+    for (int q = 0; q < HS; q += 4) {
+#pragma unroll
+      for (int u = 0; u < kRPW; ++u) {
+        const float4 hv = *reinterpret_cast<const float4*>(&sh[wl][u][cur][q]);
+        ar[u] = mac(ar[u], hv.x, wr[q]);
+        az[u] = mac(az[u], hv.x, wz[q]);
+        hh[u] = mac(hh[u], hv.x, wn[q]);
+        ar[u] = mac(ar[u], hv.y, wr[q + 1]);
+        az[u] = mac(az[u], hv.y, wz[q + 1]);
+        hh[u] = mac(hh[u], hv.y, wn[q + 1]);
+        ar[u] = mac(ar[u], hv.z, wr[q + 2]);
+        az[u] = mac(az[u], hv.z, wz[q + 2]);
+        hh[u] = mac(hh[u], hv.z, wn[q + 2]);
+        ar[u] = mac(ar[u], hv.w, wr[q + 3]);
+        az[u] = mac(az[u], hv.w, wz[q + 3]);
+        hh[u] = mac(hh[u], hv.w, wn[q + 3]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kRPW; ++u) {
+      if (!act) continue;
+      const float rv = det_sigmoid(ar[u]), zv = det_sigmoid(az[u]);
+      const float nv = det_tanh(fadd(an[u], fmul(rv, hh[u])));
+      const float hn = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, sh[wl][u][cur][j]));
+      sh[wl][u][cur ^ 1][j] = hn;
+      if (rv_ok[u]) out[c * work_cs + (int64_t(r0 + u) * T + tt) * 2 * H + dir * H + j] = hn;
+    }
     __syncwarp();
-    float hnew[kMaxH / 32];
-    int u = 0;
-    for (int j = lane; j < H; j += 32, ++u) {
-      float ar = bir[j], az = biz[j], an = bin[j], hh = bhn[j];
-      for (int q = 0; q < in; ++q) {
-        const float xv = sx[wl][q];
-        ar = mac(ar, xv, wir[int64_t(q) * H + j]);
+    cur ^= 1;
+  }
+  if (fin && act) {
+#pragma unroll
+    for (int u = 0; u < kRPW; ++u)
+      if (rv_ok[u]) fin[c * work_cs + int64_t(r0 + u) * 2 * H + dir * H + j] = sh[wl][u][cur][j];
+  }
+}
+
+// Generic recurrence (any Hs; lane owns units j, j+32, ...; weights via L1).
+__global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec_generic(
+    BiGruP p, int l, const uint32_t* __restrict__ ctx, int64_t ctx_cs, const float* __restrict__ xi,
+    float* out, float* fin, int64_t work_cs, const TickDesc* __restrict__ td) {
+  extern __shared__ __align__(16) float shd[];  // [kRecWarps][2][Hs]
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * kRecWarps + wl;
+  if (g >= p.R * 2) return;
+  const int r = g >> 1, dir = g & 1, T = p.T, H = p.Hs;
+  const int64_t RT = int64_t(p.R) * T;
+  const float* W = p.w;
+  const float* whr = W + poff(p.offs, l, dir, WHR);
+  const float* whz = W + poff(p.offs, l, dir, WHZ);
+  const float* whn = W + poff(p.offs, l, dir, WHN);
+  const float* bhr = W + poff(p.offs, l, dir, BHR);
+  const float* bhz = W + poff(p.offs, l, dir, BHZ);
+  const float* bhn = W + poff(p.offs, l, dir, BHN);
+  const uint32_t* cr = ctx + c * ctx_cs + int64_t(r) * T;
+  const float* xr = xi ? xi + c * work_cs + int64_t(dir) * 3 * RT * H : nullptr;
+  const float* t0 = p.xi0 + int64_t(dir) * 3 * p.V * H;
+  float* outr = out + c * work_cs + int64_t(r) * T * 2 * H;
+  float* buf0 = shd + (wl * 2 + 0) * H;
+  float* buf1 = shd + (wl * 2 + 1) * H;
+  for (int j = lane; j < H; j += 32) buf0[j] = 0.0f;
+  __syncwarp();
+  int cur = 0;
+  for (int step = 0; step < T; ++step) {
+    const int tt = dir ? (T - 1 - step) : step;
+    const float* h = cur ? buf1 : buf0;
+    float* hnx = cur ? buf0 : buf1;
+    for (int j = lane; j < H; j += 32) {
+      float ar, az, an;
+      if (l == 0) {
+        const int64_t tok = cr[tt];
+        ar = t0[tok * H + j];
+        az = t0[int64_t(p.V) * H + tok * H + j];
+        an = t0[2 * int64_t(p.V) * H + tok * H + j];
+      } else {
+        const int64_t pos = (int64_t(r) * T + tt) * H + j;
+        ar = xr[pos];
+        az = xr[RT * H + pos];
+        an = xr[2 * RT * H + pos];
       }
       ar = fadd(ar, bhr[j]);
-      for (int q = 0; q < H; ++q) ar = mac(ar, sh[wl][q], whr[int64_t(q) * H + j]);
-      for (int q = 0; q < in; ++q) az = mac(az, sx[wl][q], wiz[int64_t(q) * H + j]);
+      for (int q = 0; q < H; ++q) ar = mac(ar, h[q], whr[int64_t(q) * H + j]);
       az = fadd(az, bhz[j]);
-      for (int q = 0; q < H; ++q) az = mac(az, sh[wl][q], whz[int64_t(q) * H + j]);
-      for (int q = 0; q < H; ++q) hh = mac(hh, sh[wl][q], whn[int64_t(q) * H + j]);
-      for (int q = 0; q < in; ++q) an = mac(an, sx[wl][q], win[int64_t(q) * H + j]);
+      for (int q = 0; q < H; ++q) az = mac(az, h[q], whz[int64_t(q) * H + j]);
+      float hh = bhn[j];
+      for (int q = 0; q < H; ++q) hh = mac(hh, h[q], whn[int64_t(q) * H + j]);
       const float rv = det_sigmoid(ar), zv = det_sigmoid(az);
       const float nv = det_tanh(fadd(an, fmul(rv, hh)));
-      hnew[u] = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, sh[wl][j]));
+      const float hv = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, h[j]));
+      hnx[j] = hv;
+      outr[int64_t(tt) * 2 * H + dir * H + j] = hv;
     }
     __syncwarp();
-    u = 0;
-    for (int j = lane; j < H; j += 32, ++u) {
-      sh[wl][j] = hnew[u];
-      outr[int64_t(tt) * 2 * H + dir * H + j] = hnew[u];
-    }
-    __syncwarp();
+    cur ^= 1;
   }
+  const float* hl = cur ? buf1 : buf0;
   if (fin)
-    for (int j = lane; j < H; j += 32) fin[c * work_cs + int64_t(r) * 2 * H + dir * H + j] = sh[wl][j];
+    for (int j = lane; j < H; j += 32) fin[c * work_cs + int64_t(r) * 2 * H + dir * H + j] = hl[j];
 }
 
-// bott = tanh(bott.b + fin . bott.w); one thread per (row, unit)
-__global__ void k_bigru_bott(BiGruP p, const float* fin, float* bact, int64_t work_cs,
-                             const TickDesc* __restrict__ td) {
+__global__ void k_tanh_inplace(float* x, int64_t n, int64_t cs, const TickDesc* __restrict__ td) {
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= p.R * p.B) return;
-  const int r = idx / p.B, j = idx % p.B, K = 2 * p.Hs;
-  const int b0 = 1 + p.layers * 2 * NG;
-  const float* w = p.w + p.offs[b0];
-  float acc = p.w[p.offs[b0 + 1] + j];
-  const float* f = fin + c * work_cs + int64_t(r) * K;
-  for (int q = 0; q < K; ++q) acc = mac(acc, f[q], w[int64_t(q) * p.B + j]);
-  bact[c * work_cs + idx] = det_tanh(acc);
-}
-
-// logits = out.b + bott . out.w
-__global__ void k_bigru_out(BiGruP p, const float* bact, int64_t work_cs, float* logits,
-                            int64_t lg_cs, const TickDesc* __restrict__ td) {
-  if (blockIdx.y >= unsigned(td->n_act)) return;
-  const int c = td->act[blockIdx.y];
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= p.R * p.V) return;
-  const int r = idx / p.V, v = idx % p.V;
-  const int b0 = 1 + p.layers * 2 * NG;
-  const float* w = p.w + p.offs[b0 + 2];
-  float acc = p.w[p.offs[b0 + 3] + v];
-  const float* b = bact + c * work_cs + int64_t(r) * p.B;
-  for (int q = 0; q < p.B; ++q) acc = mac(acc, b[q], w[int64_t(q) * p.V + v]);
-  logits[c * lg_cs + idx] = acc;
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[c * cs + i] = det_tanh(x[c * cs + i]);
 }
 
 }  // namespace
 
+// work layout per chunk: xi [2][3][R*T][Hs] | out0 [R][T][2Hs] | out1 [R][T][2Hs] |
+//                        fin [R][2Hs] | bott [R][B]
 size_t bigru_work_floats(const BiGruP& p) {
-  // two layer-output buffers [R,T,2H] + fin [R,2H] + bact [R,B]
-  return size_t(p.R) * (2 * size_t(p.T) * 2 * p.Hs + 2 * p.Hs + p.B);
+  const size_t RT = size_t(p.R) * p.T;
+  return 6 * RT * p.Hs + 2 * RT * 2 * p.Hs + size_t(p.R) * 2 * p.Hs + size_t(p.R) * p.B;
 }
 
 void launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, float* work,
                           int64_t work_cs, float* logits, int64_t lg_cs, const TickDesc* td,
                           int max_active, cudaStream_t st) {
   if (max_active <= 0) return;
-  const int64_t layer_sz = int64_t(p.R) * p.T * 2 * p.Hs;
-  float* buf[2] = {work, work + layer_sz};
-  float* fin = work + 2 * layer_sz;
-  float* bact = fin + int64_t(p.R) * 2 * p.Hs;
-  dim3 grid(unsigned((p.R * 2 + kWarps - 1) / kWarps), max_active);
+  const int64_t RT = int64_t(p.R) * p.T, H = p.Hs;
+  float* xi = work;
+  float* outs[2] = {xi + 6 * RT * H, xi + 6 * RT * H + RT * 2 * H};
+  float* fin = outs[1] + RT * 2 * H;
+  float* bott = fin + int64_t(p.R) * 2 * H;
+  const dim3 rgrid(unsigned((p.R * 2 + kRecWarps - 1) / kRecWarps), max_active);
+  const int ngroups = (p.R + kRPW - 1) / kRPW;
+  const dim3 rgrid2(unsigned((ngroups * 2 + kRecWarps - 1) / kRecWarps), max_active);
   for (int l = 0; l < p.layers; ++l) {
-    const float* in = l == 0 ? nullptr : buf[(l - 1) & 1];
-    k_bigru_layer<<<grid, kWarps * 32, 0, st>>>(p, l, ctx, ctx_cs, in, buf[l & 1],
-                                                l == p.layers - 1 ? fin : nullptr, work_cs, td);
+    float* out = outs[l & 1];
+    if (l > 0) {
+      // x-projections of layer l for every position: 3 gates per direction,
+      // C[gate][RT][H] = b_i{gate} + in . W_i{gate}
+      const float* in = outs[(l - 1) & 1];
+      const int in_w = int(2 * H);
+      for (int dir = 0; dir < 2; ++dir) {
+        GemmP gp{};
+        gp.A = in;
+        gp.a_cs = work_cs;
+        gp.lda = in_w;
+        gp.B = p.w + p.hoffs[1 + (l * 2 + dir) * NG + WIR];
+        gp.ldb = H;
+        gp.C = xi + int64_t(dir) * 3 * RT * H;
+        gp.c_cs = work_cs;
+        gp.ldc = H;
+        gp.bias = p.w + p.hoffs[1 + (l * 2 + dir) * NG + BIR];
+        gp.M = int(RT);
+        gp.N = int(H);
+        gp.K = in_w;
+        gp.init = 1;
+        gp.nprob = 3;
+        gp.b_ps = int64_t(in_w) * H;  // w_ir, w_iz, w_in consecutive
+        gp.c_ps = RT * H;
+        gp.bias_ps = H;               // b_ir, b_iz, b_in consecutive
+        launch_gemm(gp, false, false, td, max_active, st);
+      }
+    }
+    float* f = (l == p.layers - 1) ? fin : nullptr;
+    const float* xl = l == 0 ? nullptr : xi;
+    if (p.Hs == 32)
+      k_bigru_rec<32><<<rgrid2, kRecWarps * 32, 0, st>>>(p, l, ctx, ctx_cs, xl, out, f, work_cs, td);
+    else if (p.Hs == 16)
+      k_bigru_rec<16><<<rgrid2, kRecWarps * 32, 0, st>>>(p, l, ctx, ctx_cs, xl, out, f, work_cs, td);
+    else if (p.Hs == 8)
+      k_bigru_rec<8><<<rgrid2, kRecWarps * 32, 0, st>>>(p, l, ctx, ctx_cs, xl, out, f, work_cs, td);
+    else
+      k_bigru_rec_generic<<<rgrid, kRecWarps * 32, kRecWarps * 2 * p.Hs * sizeof(float), st>>>(
+          p, l, ctx, ctx_cs, xl, out, f, work_cs, td);
   }
-  dim3 g2(unsigned((p.R * p.B + 255) / 256), max_active);
-  k_bigru_bott<<<g2, 256, 0, st>>>(p, fin, bact, work_cs, td);
-  dim3 g3(unsigned((p.R * p.V + 255) / 256), max_active);
-  k_bigru_out<<<g3, 256, 0, st>>>(p, bact, work_cs, logits, lg_cs, td);
+  // bott = tanh(bott.b + fin . bott.w);  logits = out.b + bott . out.w
+  const int b0 = 1 + p.layers * 2 * NG;
+  GemmP g1{};
+  g1.A = fin;
+  g1.a_cs = work_cs;
+  g1.lda = 2 * H;
+  g1.B = p.w + p.hoffs[b0];
+  g1.ldb = p.B;
+  g1.C = bott;
+  g1.c_cs = work_cs;
+  g1.ldc = p.B;
+  g1.bias = p.w + p.hoffs[b0 + 1];
+  g1.M = p.R;
+  g1.N = p.B;
+  g1.K = int(2 * H);
+  g1.init = 1;
+  launch_gemm(g1, false, false, td, max_active, st);
+  const int64_t nb = int64_t(p.R) * p.B;
+  k_tanh_inplace<<<dim3(unsigned((nb + 255) / 256), max_active), 256, 0, st>>>(bott, nb, work_cs, td);
+  GemmP g2{};
+  g2.A = bott;
+  g2.a_cs = work_cs;
+  g2.lda = p.B;
+  g2.B = p.w + p.hoffs[b0 + 2];
+  g2.ldb = p.V;
+  g2.C = logits;
+  g2.c_cs = lg_cs;
+  g2.ldc = p.V;
+  g2.bias = p.w + p.hoffs[b0 + 3];
+  g2.M = p.R;
+  g2.N = p.V;
+  g2.K = p.B;
+  g2.init = 1;
+  launch_gemm(g2, false, false, td, max_active, st);
 }
 
 }  // namespace pmklc_b200

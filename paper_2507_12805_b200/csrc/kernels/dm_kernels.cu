@@ -42,11 +42,14 @@ __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc*
   constexpr int NT = TX * TY, BM = TY * TM, BN = TX * TN;
   __shared__ __align__(16) float As[STAGES][BK][BM + 4];
   __shared__ __align__(16) float Bs[STAGES][BK][BN + 4];
-  if (blockIdx.z >= unsigned(td->n_act)) return;
-  const int c = td->act[blockIdx.z];
-  const float* A = p.A + c * p.a_cs;
-  const float* B = p.B + c * p.b_cs;
-  float* C = p.C + c * p.c_cs;
+  const int np = p.nprob > 1 ? p.nprob : 1;
+  const int slot = blockIdx.z / np, prob = blockIdx.z % np;
+  if (slot >= td->n_act) return;
+  const int c = td->act[slot];
+  const float* A = p.A + c * p.a_cs + prob * p.a_ps;
+  const float* B = p.B + c * p.b_cs + prob * p.b_ps;
+  float* C = p.C + c * p.c_cs + prob * p.c_ps;
+  const float* bias = p.bias ? p.bias + c * p.bias_cs + prob * p.bias_ps : nullptr;
   const int Mx = p.M + (p.ones_row ? 1 : 0);
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
@@ -85,7 +88,7 @@ __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc*
       const int m = m0 + ty * TM + i, n = n0 + tx * TN + j;
       float v = 0.0f;
       if (m < Mx && n < p.N) {
-        if (p.init == 1) v = p.bias[c * p.bias_cs + n];
+        if (p.init == 1) v = bias[n];
         else if (p.init == 2) v = C[int64_t(m) * p.ldc + n];
       }
       acc[i][j] = v;
@@ -159,7 +162,8 @@ __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc*
 template <bool AT, bool BT, int TM, int TN, int BK, int STAGES, int TX = 16, int TY = 16>
 void gemm_launch(const GemmP& p, const TickDesc* td, int max_active, cudaStream_t st) {
   const int Mx = p.M + (p.ones_row ? 1 : 0);
-  dim3 grid((p.N + TX * TN - 1) / (TX * TN), (Mx + TY * TM - 1) / (TY * TM), max_active);
+  const int np = p.nprob > 1 ? p.nprob : 1;
+  dim3 grid((p.N + TX * TN - 1) / (TX * TN), (Mx + TY * TM - 1) / (TY * TM), max_active * np);
   k_gemm_tiled<AT, BT, TM, TN, BK, STAGES, TX, TY><<<grid, TX * TY, 0, st>>>(p, td);
 }
 
@@ -167,7 +171,7 @@ template <bool AT, bool BT>
 void gemm_dispatch(const GemmP& p, const TickDesc* td, int max_active, cudaStream_t st) {
   const int Mx = p.M + (p.ones_row ? 1 : 0);
   auto blocks = [&](int bm, int bn) {
-    return int64_t((p.N + bn - 1) / bn) * ((Mx + bm - 1) / bm) * max_active;
+    return int64_t((p.N + bn - 1) / bn) * ((Mx + bm - 1) / bm) * max_active * (p.nprob > 1 ? p.nprob : 1);
   };
   // Largest tile that still gives every SM two blocks (throughput); for a
   // launch too small to fill the chip, one output per thread, and for long
@@ -178,6 +182,8 @@ void gemm_dispatch(const GemmP& p, const TickDesc* td, int max_active, cudaStrea
     gemm_launch<AT, BT, 4, 4, 32, 2>(p, td, max_active, st);
   else if (blocks(64, 16) >= kFill && p.N <= 16 && Mx >= 48)
     gemm_launch<AT, BT, 4, 1, 32, 2>(p, td, max_active, st);
+  else if (blocks(64, 32) >= kFill && p.N <= 32 && Mx >= 48)
+    gemm_launch<AT, BT, 4, 2, 32, 2>(p, td, max_active, st);
   else if (blocks(32, 32) >= kFill && p.N >= 24 && Mx >= 24)
     gemm_launch<AT, BT, 2, 2, 32, 3>(p, td, max_active, st);
   else if (blocks(16, 16) >= 148 || p.K <= 256)
@@ -314,7 +320,9 @@ __global__ void k_embed(const uint32_t* __restrict__ tokens, ChunkGeo geo,
   const int t = int(rt % d.T), r = int(rt / d.T);
   const uint64_t L = geo.L[c];
   const uint64_t jstep = uint64_t(d.T) + uint64_t(td->tick - geo.offset[c]);  // coded position
-  const uint32_t tok = tokens[geo.start[c] + uint64_t(r) * L + (jstep - d.T) + t];
+  // tokens are < V = 4^k by construction; the mask only guards memory after a
+  // decode error (slots past a truncated codestream are never written)
+  const uint32_t tok = tokens[geo.start[c] + uint64_t(r) * L + (jstep - d.T) + t] & uint32_t(d.V - 1);
   if (j == 0) ctx[c * ctx_cs + rt] = tok;
   const float* P = params + c * p_cs;
   const float xv = fadd(P[off_emb + int64_t(tok) * d.E + j], P[off_pos + int64_t(t) * d.E + j]);

@@ -69,6 +69,10 @@ struct GemmP {
   int ones_row;  // also compute row M with A(M,k)=1 (the bias grad stored right after W)
   int init;      // 0 zero, 1 bias, 2 accumulate onto C
   int relu_a;    // A(m,k) = A<0 ? 0 : A   (Ffn relu, layers.cpp:538-540)
+  // optional batch of `nprob` same-shape problems per chunk (0 or 1 = single):
+  // problem q uses A + q*a_ps, B + q*b_ps, C + q*c_ps, bias + q*bias_ps
+  int nprob;
+  int64_t a_ps, b_ps, c_ps, bias_ps;
 };
 void launch_gemm(const GemmP& p, bool at, bool bt, const TickDesc* td, int max_active,
                  cudaStream_t st);
@@ -165,10 +169,17 @@ void launch_range_step(uint32_t* tokens, ChunkGeo geo, int t, int R, int V,
 void launch_range_finish(uint8_t* payload, const uint64_t* pay_off, CoderState* cs, int n_chunks,
                          cudaStream_t st);
 
-// Frozen BiGRU predictor forward (SPuM/SPrM, models.cpp:53-73, layers.cpp:213-260)
+// Frozen BiGRU predictor forward (SPuM/SPrM, models.cpp:53-73, layers.cpp:213-260).
+// Layer 0's input projections b_i* + emb[tok].W_i* depend on the token only,
+// so they are a per-model table xi0 [2 dirs][3 gates][V][Hs] computed once
+// on the host in the reference's operation order. Deeper layers' input
+// projections run as batched exact GEMMs over all R*t positions; only the
+// recurrent part is serial in time (one warp per row and direction).
 struct BiGruP {
   const float* w;       // flat PMKW parameter array on device
   const int64_t* offs;  // device: param offsets in BiGru::ps order
+  const int64_t* hoffs; // host copy of the same offsets
+  const float* xi0;     // device table [2][3][V][Hs]
   int layers, V, T, Es, Hs, B, R;
 };
 void launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, float* work,
