@@ -71,7 +71,23 @@ class Clocks:
         self.p = None
         self.f = None
 
+    def start(self):
+        """Start sampling and wait for the first sample: NVML initialisation
+        can stall the driver for seconds, so it must happen before warm-up."""
+        self.__enter__()
+        t0 = time.time()
+        while self.p and time.time() - t0 < 15:
+            try:
+                if open(self.f.name).read().strip():
+                    break
+            except Exception:
+                pass
+            time.sleep(0.2)
+        return self
+
     def __enter__(self):
+        if self.p:
+            return self
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -190,6 +206,7 @@ def main():
         P.device_free(dptr)
         return blob, tm_c, tm_d
 
+    clk = Clocks(dev).start()
     # correctness of the measured path: lossless round trip
     blob, _, _ = step_device()
     assert P.decompress(blob, spum, device=dev) == raw, "round trip mismatch"
@@ -199,7 +216,6 @@ def main():
 
     ct = dt = 0.0
     launches = 0
-    clk = Clocks(dev)
     times = []
     with clk:
         for _ in range(args.steps):
