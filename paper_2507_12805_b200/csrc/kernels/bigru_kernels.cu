@@ -29,35 +29,33 @@ __device__ __forceinline__ int64_t poff(const int64_t* offs, int l, int dir, int
 
 // xi: layer >= 1 input projections of this chunk, [2 dirs][3 gates][R*T][Hs]
 // out: layer output [R][T][2Hs]; fin (last layer): [R][2Hs]
-// One warp runs kRPW rows of one direction: the W_h* columns held in
-// registers serve every row, and the rows' chains interleave (ILP).
-constexpr int kRPW = 2;
+// Blocks are single-direction; the direction's W_h* (3 x Hs x Hs) sit in
+// shared memory, each warp runs kRPW rows so one weight read feeds kRPW
+// independent chains (and the register budget leaves room for 4+ blocks/SM).
+constexpr int kRPW = 4;
 template <int HS>
 __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
     BiGruP p, int l, const uint32_t* __restrict__ ctx, int64_t ctx_cs, const float* __restrict__ xi,
     float* out, float* fin, int64_t work_cs, const TickDesc* __restrict__ td) {
+  __shared__ __align__(16) float sw[3][HS][HS];
   __shared__ __align__(16) float sh[kRecWarps][kRPW][2][32];
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.x * kRecWarps + wl;  // = (row group, dir)
-  const int ngroups = (p.R + kRPW - 1) / kRPW;
-  if (g >= ngroups * 2) return;
-  const int r0 = (g >> 1) * kRPW, dir = g & 1, T = p.T, H = HS;
+  const int dir = blockIdx.x & 1;
+  const int grp = (blockIdx.x >> 1) * kRecWarps + wl;  // row group of this warp
+  const int T = p.T, H = HS;
   const int64_t RT = int64_t(p.R) * T;
   const float* W = p.w;
-  const float* whr = W + poff(p.offs, l, dir, WHR);
-  const float* whz = W + poff(p.offs, l, dir, WHZ);
-  const float* whn = W + poff(p.offs, l, dir, WHN);
+  for (int i = threadIdx.x; i < 3 * HS * HS; i += blockDim.x) {
+    const int gate = i / (HS * HS), rem = i % (HS * HS);
+    sw[gate][rem / HS][rem % HS] = W[poff(p.offs, l, dir, WHR + gate) + rem];
+  }
+  __syncthreads();
+  const int r0 = grp * kRPW;
+  if (r0 >= p.R) return;
   const int j = lane;
   const bool act = j < H;
-  float wr[HS], wz[HS], wn[HS];
-#pragma unroll
-  for (int q = 0; q < HS; ++q) {
-    wr[q] = act ? whr[q * H + j] : 0.f;
-    wz[q] = act ? whz[q * H + j] : 0.f;
-    wn[q] = act ? whn[q * H + j] : 0.f;
-  }
   float bhr = 0.f, bhz = 0.f, bhn = 0.f;
   if (act) {
     bhr = W[poff(p.offs, l, dir, BHR) + j];
@@ -72,6 +70,7 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
   }
   const float* xr = xi ? xi + c * work_cs + int64_t(dir) * 3 * RT * H : nullptr;
   const float* t0 = p.xi0 + int64_t(dir) * 3 * p.V * H;  // layer-0 tables [3][V][H]
+  const int jj = act ? j : 0;
   __syncwarp();
   int cur = 0;
   for (int step = 0; step < T; ++step) {
@@ -82,36 +81,34 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
       const int r = rv_ok[u] ? r0 + u : r0;
       if (l == 0) {
         const int64_t tok = ctx[c * ctx_cs + int64_t(r) * T + tt];
-        ar[u] = act ? t0[tok * H + j] : 0.f;
-        az[u] = act ? t0[int64_t(p.V) * H + tok * H + j] : 0.f;
-        an[u] = act ? t0[2 * int64_t(p.V) * H + tok * H + j] : 0.f;
+        ar[u] = t0[tok * H + jj];
+        az[u] = t0[int64_t(p.V) * H + tok * H + jj];
+        an[u] = t0[2 * int64_t(p.V) * H + tok * H + jj];
       } else {
-        const int64_t pos = (int64_t(r) * T + tt) * H + j;
-        ar[u] = act ? xr[pos] : 0.f;
-        az[u] = act ? xr[RT * H + pos] : 0.f;
-        an[u] = act ? xr[2 * RT * H + pos] : 0.f;
+        const int64_t pos = (int64_t(r) * T + tt) * H + jj;
+        ar[u] = xr[pos];
+        az[u] = xr[RT * H + pos];
+        an[u] = xr[2 * RT * H + pos];
       }
       ar[u] = fadd(ar[u], bhr);
       az[u] = fadd(az[u], bhz);
       hh[u] = bhn;
     }
-#pragma unroll
+#pragma unroll 2
     for (int q = 0; q < HS; q += 4) {
+      float4 hv[kRPW];
 #pragma unroll
-      for (int u = 0; u < kRPW; ++u) {
-        const float4 hv = *reinterpret_cast<const float4*>(&sh[wl][u][cur][q]);
-        ar[u] = mac(ar[u], hv.x, wr[q]);
-        az[u] = mac(az[u], hv.x, wz[q]);
-        hh[u] = mac(hh[u], hv.x, wn[q]);
-        ar[u] = mac(ar[u], hv.y, wr[q + 1]);
-        az[u] = mac(az[u], hv.y, wz[q + 1]);
-        hh[u] = mac(hh[u], hv.y, wn[q + 1]);
-        ar[u] = mac(ar[u], hv.z, wr[q + 2]);
-        az[u] = mac(az[u], hv.z, wz[q + 2]);
-        hh[u] = mac(hh[u], hv.z, wn[q + 2]);
-        ar[u] = mac(ar[u], hv.w, wr[q + 3]);
-        az[u] = mac(az[u], hv.w, wz[q + 3]);
-        hh[u] = mac(hh[u], hv.w, wn[q + 3]);
+      for (int u = 0; u < kRPW; ++u) hv[u] = *reinterpret_cast<const float4*>(&sh[wl][u][cur][q]);
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        const float wr = sw[0][q + qq][jj], wz = sw[1][q + qq][jj], wn = sw[2][q + qq][jj];
+#pragma unroll
+        for (int u = 0; u < kRPW; ++u) {
+          const float hq = qq == 0 ? hv[u].x : qq == 1 ? hv[u].y : qq == 2 ? hv[u].z : hv[u].w;
+          ar[u] = mac(ar[u], hq, wr);
+          az[u] = mac(az[u], hq, wz);
+          hh[u] = mac(hh[u], hq, wn);
+        }
       }
     }
 #pragma unroll
@@ -225,7 +222,7 @@ void launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, 
   float* bott = fin + int64_t(p.R) * 2 * H;
   const dim3 rgrid(unsigned((p.R * 2 + kRecWarps - 1) / kRecWarps), max_active);
   const int ngroups = (p.R + kRPW - 1) / kRPW;
-  const dim3 rgrid2(unsigned((ngroups * 2 + kRecWarps - 1) / kRecWarps), max_active);
+  const dim3 rgrid2(unsigned(2 * ((ngroups + kRecWarps - 1) / kRecWarps)), max_active);
   for (int l = 0; l < p.layers; ++l) {
     float* out = outs[l & 1];
     if (l > 0) {

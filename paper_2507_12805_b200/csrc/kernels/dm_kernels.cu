@@ -201,22 +201,28 @@ __device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem));
 }
 
-// 64 threads = 64 outputs (one m, 64 n); K-tiles of 64 staged by 16-byte
-// cp.async (every thread streams 16 B-row chunks + a quarter of the A row per
-// tile with pointer-increment addressing) into a 4-deep ring.
-constexpr int kNtThreads = 64, kNtBK = 64, kNtStages = 4;
+// Block = MR output rows x 64 columns (64*MR threads, one output each).
+// K-tiles of 64 are staged by 16-byte cp.async into a 4-deep ring; one staged
+// B tile serves all MR rows. MR=1 spreads a single chunk's few outputs over
+// the most SMs (latency regime); MR=4 amortizes the B tile when many chunks
+// are in flight (throughput regime).
+constexpr int kNtCols = 64, kNtBK = 64, kNtStages = 4;
 constexpr int kNtSB = kNtBK + 4;  // padded B row: LDS.128 of 32 rows = 4 wavefronts
-constexpr size_t kNtSmem = size_t(kNtStages) * (kNtBK + kNtThreads * kNtSB) * sizeof(float);
+__host__ __device__ constexpr size_t nt_smem(int mr) {
+  return size_t(kNtStages) * (size_t(mr) * kNtBK + size_t(kNtCols) * kNtSB) * sizeof(float);
+}
 
 // VEC: rows 16-byte aligned, K multiple of 4 (host-checked); else 4-byte copies.
-template <bool VEC>
-__global__ void __launch_bounds__(kNtThreads) k_gemm_nt(NtP p0, NtP p1, const TickDesc* __restrict__ td) {
+template <bool VEC, int MR>
+__global__ void __launch_bounds__(kNtCols * MR) k_gemm_nt(NtP p0, NtP p1, const TickDesc* __restrict__ td) {
   extern __shared__ __align__(128) float sm[];
+  constexpr int NT = kNtCols * MR;
   if (blockIdx.z >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.z];
-  int m = blockIdx.y;
-  const bool second = m >= p0.M + 1;
-  if (second) m -= p0.M + 1;
+  const int nb0 = (p0.M + 1 + MR - 1) / MR;  // row blocks of problem 0 (incl. bias row)
+  int mb = blockIdx.y;
+  const bool second = mb >= nb0;
+  if (second) mb -= nb0;
   const float* Ab = second ? p1.A : p0.A;
   const float* Bb = second ? p1.B : p0.B;
   float* Cb = second ? p1.C : p0.C;
@@ -224,44 +230,44 @@ __global__ void __launch_bounds__(kNtThreads) k_gemm_nt(NtP p0, NtP p1, const Ti
                 c_cs = second ? p1.c_cs : p0.c_cs, lda = second ? p1.lda : p0.lda,
                 ldb = second ? p1.ldb : p0.ldb, ldc = second ? p1.ldc : p0.ldc;
   const int M = second ? p1.M : p0.M, N = second ? p1.N : p0.N, K = second ? p1.K : p0.K;
-  if (m > M) return;
-  const int n0 = blockIdx.x * kNtThreads;
+  const int m0 = mb * MR;
+  if (m0 > M) return;
+  const int n0 = blockIdx.x * kNtCols;
   if (n0 >= N) return;
-  const int tid = threadIdx.x, n = n0 + tid;
-  const bool ones = m == M;  // bias row: plain sum of the gradient rows
-  const float* A = Ab + c * a_cs + int64_t(m) * lda;
+  const int tid = threadIdx.x, col = tid % kNtCols, mr = tid / kNtCols;
+  const int m = m0 + mr, n = n0 + col;
+  const bool ones = m == M;      // bias row: plain sum of the gradient rows
+  const bool live = m <= M && n < N;
+  const int nrows = min(kNtCols, N - n0);
+  const int arows = min(MR, M - m0);  // real A rows in this block (bias row has none)
+  const float* A = Ab + c * a_cs + int64_t(m0) * lda;
   const float* B = Bb + c * b_cs + int64_t(n0) * ldb;
   float* C = Cb + c * c_cs;
-  float* As = sm;
-  float* Bs = sm + kNtStages * kNtBK;
+  float* As = sm;                                  // [stage][MR][BK]
+  float* Bs = sm + kNtStages * MR * kNtBK;         // [stage][64][SB]
   const int ntiles = (K + kNtBK - 1) / kNtBK;
-  const int nrows = min(kNtThreads, N - n0);
-  // this thread's copy slots: rows r0 + 4q (q < 16), 16-byte chunk v (VEC path)
-  const int v = tid & 15, r0 = tid >> 4;
 
   auto load = [&](int tile) {
     if (tile < ntiles) {
       const int st = tile % kNtStages, k0 = tile * kNtBK, kc = min(kNtBK, K - k0);
-      float* as = As + st * kNtBK;
-      float* bs = Bs + st * kNtThreads * kNtSB;
+      float* as = As + st * MR * kNtBK;
+      float* bs = Bs + st * kNtCols * kNtSB;
       if (VEC && kc == kNtBK) {
-        if (!ones && tid < 16) cp_async16(as + 4 * v, A + k0 + 4 * v);
-        const float* src = B + int64_t(r0) * ldb + k0 + 4 * v;
-        float* dst = bs + r0 * kNtSB + 4 * v;
-#pragma unroll
-        for (int q = 0; q < kNtThreads / 4; ++q)
-          if (r0 + 4 * q < nrows) cp_async16(dst + q * 4 * kNtSB, src + int64_t(q) * 4 * ldb);
+        for (int i = tid; i < arows * 16; i += NT)
+          cp_async16(as + (i >> 4) * kNtBK + 4 * (i & 15), A + int64_t(i >> 4) * lda + k0 + 4 * (i & 15));
+        for (int i = tid; i < nrows * 16; i += NT)
+          cp_async16(bs + (i >> 4) * kNtSB + 4 * (i & 15), B + int64_t(i >> 4) * ldb + k0 + 4 * (i & 15));
       } else {
-        if (!ones)
-          for (int i = tid; i < kc; i += kNtThreads) cp_async4(as + i, A + k0 + i);
-        for (int rr = 0; rr < nrows; ++rr)
-          for (int i = tid; i < kc; i += kNtThreads) cp_async4(bs + rr * kNtSB + i, B + int64_t(rr) * ldb + k0 + i);
+        for (int i = tid; i < arows * kc; i += NT)
+          cp_async4(as + (i / kc) * kNtBK + i % kc, A + int64_t(i / kc) * lda + k0 + i % kc);
+        for (int i = tid; i < nrows * kc; i += NT)
+          cp_async4(bs + (i / kc) * kNtSB + i % kc, B + int64_t(i / kc) * ldb + k0 + i % kc);
       }
     }
     cp_async_commit();  // one group per tile slot, possibly empty
   };
 
-  float acc = (n < N) ? C[int64_t(m) * ldc + n] : 0.0f;
+  float acc = live ? C[int64_t(m) * ldc + n] : 0.0f;
 #pragma unroll
   for (int s = 0; s < kNtStages - 1; ++s) load(s);
   for (int tile = 0; tile < ntiles; ++tile) {
@@ -269,9 +275,9 @@ __global__ void __launch_bounds__(kNtThreads) k_gemm_nt(NtP p0, NtP p1, const Ti
     __syncthreads();  // tile landed for everyone; everyone is past tile-1
     load(tile + kNtStages - 1);
     const int st = tile % kNtStages, kc = min(kNtBK, K - tile * kNtBK);
-    const float* as = As + st * kNtBK;
-    const float* bs = Bs + (st * kNtThreads + tid) * kNtSB;
-    if (tid < nrows) {
+    const float* as = As + (st * MR + mr) * kNtBK;
+    const float* bs = Bs + (st * kNtCols + col) * kNtSB;
+    if (live) {
       if (kc == kNtBK) {
         if (ones) {
 #pragma unroll
@@ -299,7 +305,7 @@ __global__ void __launch_bounds__(kNtThreads) k_gemm_nt(NtP p0, NtP p1, const Ti
     }
   }
   cp_async_wait<0>();
-  if (n < N) C[int64_t(m) * ldc + n] = acc;
+  if (live) C[int64_t(m) * ldc + n] = acc;
 }
 
 // ------------------------------------------------------------------ embed
@@ -786,22 +792,31 @@ void launch_gemm_nt(const NtP& p0, const NtP* p1, const TickDesc* td, int max_ac
   if (max_active <= 0 || p0.N <= 0) return;
   const NtP q1 = p1 ? *p1 : p0;
   auto al = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
-  auto vec_ok = [&](const NtP& p) {  // TMA bulk: 16-byte aligned rows, sizes multiple of 16 B
+  auto vec_ok = [&](const NtP& p) {  // 16-byte rows for cp.async.cg 16
     return p.K % 4 == 0 && p.lda % 4 == 0 && p.ldb % 4 == 0 && p.a_cs % 4 == 0 &&
            p.b_cs % 4 == 0 && al(p.A) && al(p.B);
   };
   const bool vec = vec_ok(p0) && vec_ok(q1);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_gemm_nt<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNtSmem));
-    cudaFuncSetAttribute(k_gemm_nt<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNtSmem));
+    cudaFuncSetAttribute(k_gemm_nt<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(nt_smem(1)));
+    cudaFuncSetAttribute(k_gemm_nt<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(nt_smem(1)));
+    cudaFuncSetAttribute(k_gemm_nt<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(nt_smem(4)));
+    cudaFuncSetAttribute(k_gemm_nt<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(nt_smem(4)));
     attr_set = true;
   }
-  const int nx = (std::max(p0.N, q1.N) + kNtThreads - 1) / kNtThreads;
-  const int ny = (p0.M + 1) + (p1 ? p1->M + 1 : 0);
-  dim3 grid(nx, ny, max_active);
-  if (vec) k_gemm_nt<true><<<grid, kNtThreads, kNtSmem, st>>>(p0, q1, td);
-  else k_gemm_nt<false><<<grid, kNtThreads, kNtSmem, st>>>(p0, q1, td);
+  const int nx = (std::max(p0.N, q1.N) + kNtCols - 1) / kNtCols;
+  auto rows = [&](int mr) { return (p0.M + 1 + mr - 1) / mr + (p1 ? (p1->M + 1 + mr - 1) / mr : 0); };
+  // one-row blocks while the launch cannot fill the chip, else 4-row blocks
+  if (int64_t(nx) * rows(1) * max_active < 2 * 148) {
+    dim3 grid(nx, rows(1), max_active);
+    if (vec) k_gemm_nt<true, 1><<<grid, kNtCols, nt_smem(1), st>>>(p0, q1, td);
+    else k_gemm_nt<false, 1><<<grid, kNtCols, nt_smem(1), st>>>(p0, q1, td);
+  } else {
+    dim3 grid(nx, rows(4), max_active);
+    if (vec) k_gemm_nt<true, 4><<<grid, kNtCols * 4, nt_smem(4), st>>>(p0, q1, td);
+    else k_gemm_nt<false, 4><<<grid, kNtCols * 4, nt_smem(4), st>>>(p0, q1, td);
+  }
 }
 
 void launch_embed(const uint32_t* tokens, ChunkGeo geo, const float* params,
