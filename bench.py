@@ -174,7 +174,7 @@ def main():
         line = {"metric": METRIC, "value": r["value"], "unit": "MB/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": 1000.0 * (r["value"] and (len(raw[:threads * 320 * 3 * 64]) / 1e6 / r["value"])),
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "impl": "reference",
                 "config": {"workload": desc, "parallelism": f"{threads} host threads"},
                 "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -190,7 +190,7 @@ def main():
 
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group("gloo", init_method="env://")  # host control plane only
     torch.cuda.set_device(local)
     dev = local
     raw, cfg, spum, desc = workload(args, tmp)
@@ -198,65 +198,102 @@ def main():
     n = len(raw)
     d_raw = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(f"cuda:{dev}")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+    ctx = P.DistContext(rank, world, dev) if world > 1 else None
 
-    def step_device():
+    def bcast(blob):
+        if world == 1:
+            return blob
+        obj = [blob]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def run_step(timed):
+        """compress (device-resident input) + decompress; PMKLC-M over all ranks."""
         tm_c, tm_d = P.Timing(), P.Timing()
-        blob = P.compress_device(d_raw.data_ptr(), n, cfg, tm_c)
-        dptr, dlen = P.decompress_to_device(blob, spum, dev, tm_d)
-        P.device_free(dptr)
-        return blob, tm_c, tm_d
-
-    clk = Clocks(dev).start()
-    # correctness of the measured path: lossless round trip
-    blob, _, _ = step_device()
-    assert P.decompress(blob, spum, device=dev) == raw, "round trip mismatch"
-
-    for _ in range(max(args.warmup - 1, 0)):
-        step_device()
-
-    ct = dt = 0.0
-    launches = 0
-    times = []
-    with clk:
-        for _ in range(args.steps):
-            flush_l2(torch, flush)
-            if world > 1:
-                torch.distributed.barrier()
-            torch.cuda.synchronize()
-            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-            e0.record()
-            tm_c, tm_d = P.Timing(), P.Timing()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        if ctx is None:
             blob = P.compress_device(d_raw.data_ptr(), n, cfg, tm_c)
-            e1.record()
+        else:
+            blob = ctx.compress_device(d_raw.data_ptr(), n, cfg, tm_c)
+        e1.record()
+        torch.cuda.synchronize()
+        blob = bcast(blob)  # container to every rank (not timed)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e1b = torch.cuda.Event(enable_timing=True)
+        e1b.record()
+        if ctx is None:
             dptr, dlen = P.decompress_to_device(blob, spum, dev, tm_d)
             e2.record()
             torch.cuda.synchronize()
             P.device_free(dptr)
-            c_ms, d_ms = e0.elapsed_time(e1), e1.elapsed_time(e2)
-            times.append(c_ms + d_ms)
+        else:
+            out = ctx.decompress(blob, spum, tm_d)
+            e2.record()
+            torch.cuda.synchronize()
+            if rank == 0:
+                assert len(out) == n
+        c_ms, d_ms = e0.elapsed_time(e1), e1b.elapsed_time(e2)
+        return blob, c_ms, d_ms, tm_c.kernel_launches + tm_d.kernel_launches
+
+    clk = Clocks(dev).start()
+    # correctness of the measured path: lossless round trip
+    blob, _, _, _ = run_step(False)
+    if ctx is None:
+        assert P.decompress(blob, spum, device=dev) == raw, "round trip mismatch"
+    else:
+        out = ctx.decompress(blob, spum)
+        if rank == 0:
+            assert out == raw, "round trip mismatch"
+
+    for _ in range(max(args.warmup - 1, 0)):
+        run_step(False)
+
+    ct = dt = 0.0
+    launches = 0
+    with clk:
+        for _ in range(args.steps):
+            flush_l2(torch, flush)
+            blob, c_ms, d_ms, l = run_step(True)
+            if world > 1:  # max over ranks, per phase
+                tt = torch.tensor([c_ms, d_ms], dtype=torch.float64)
+                torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+                c_ms, d_ms = float(tt[0]), float(tt[1])
             ct += c_ms
             dt += d_ms
-            launches += tm_c.kernel_launches + tm_d.kernel_launches
-    step_ms = max(times) if world == 1 else None
+            launches += l
     tot_ms = ct + dt
-    if world > 1:
-        t = torch.tensor([tot_ms], device=f"cuda:{dev}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        tot_ms = float(t.item())
-    value = world * n * args.steps / 1e6 / (tot_ms / 1000.0)
+    value = n * args.steps / 1e6 / (tot_ms / 1000.0)
 
     # e2e through the public host API (host buffers, H2D/D2H inside)
     e_times = []
     for _ in range(max(1, args.steps // 2)):
         flush_l2(torch, flush)
+        if world > 1:
+            torch.distributed.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        b2 = P.compress(raw, cfg)
-        back = P.decompress(b2, spum, device=dev)
+        if ctx is None:
+            b2 = P.compress(raw, cfg)
+            back = P.decompress(b2, spum, device=dev)
+        else:
+            b2 = bcast(ctx.compress(raw, cfg))
+            back = ctx.decompress(b2, spum)
         torch.cuda.synchronize()
-        e_times.append(time.perf_counter() - t0)
-        assert back == raw
-    e2e_val = world * n / 1e6 / (sum(e_times) / len(e_times))
+        el = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([el], dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            el = float(tt[0])
+        e_times.append(el)
+        if rank == 0:
+            assert back == raw
+    e2e_val = n / 1e6 / (sum(e_times) / len(e_times))
 
     line = None
     if rank == 0:
@@ -287,11 +324,13 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "MB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": desc, "bytes": n, "parallelism": f"{world} GPU replica(s)",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": desc, "bytes": n,
+                       "parallelism": (f"PMKLC-M over {world} GPUs: chunk c on GPU c%{world}, "
+                                       "SMP handoffs as NCCL send/recv") if world > 1 else "1 GPU",
                        "l2": "256 MiB flush write between timed steps"},
-            "compress_MBps": world * n * args.steps / 1e6 / (ct / 1000.0),
-            "decompress_MBps": world * n * args.steps / 1e6 / (dt / 1000.0),
+            "compress_MBps": n * args.steps / 1e6 / (ct / 1000.0),
+            "decompress_MBps": n * args.steps / 1e6 / (dt / 1000.0),
             "bits_per_base": 8.0 * len(blob) / n,
             "container_bytes": len(blob),
             "roofline": {"kernel": "k_gemm_nt (dWk|dbk + dWv|dbv over R*t=10240 rows, "
@@ -310,6 +349,7 @@ def main():
         print(json.dumps(line))
     if world > 1:
         torch.distributed.barrier()
+        ctx.close()
         torch.distributed.destroy_process_group()
 
 

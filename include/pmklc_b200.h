@@ -125,6 +125,30 @@ int pmklc_schedule(const uint64_t* lens, size_t n_chunks, uint32_t bs, uint32_t 
                    uint16_t smp_per_myriad, int64_t* offset, int64_t* src, uint64_t* src_steps,
                    uint64_t* model_steps, int64_t* ticks);
 
+/* ---- PMKLC-M across GPUs (one process per GPU) -------------------------
+ * Chunk c runs on rank c % world; an SMP handoff between chunks on different
+ * ranks is an NCCL send/recv of the state slot at the handoff tick (replaces
+ * the in-process promise chain of run_chunks, pipeline.cpp:253-294). Rank 0
+ * obtains the id (pmklc_nccl_id), the caller broadcasts its 128 bytes. */
+int pmklc_nccl_id(uint8_t* out128);
+int pmklc_dist_create(const uint8_t* id128, int32_t rank, int32_t world, int32_t device,
+                      void** handle);
+void pmklc_dist_destroy(void* handle);
+/* every rank passes the whole input (host `in` or device `d_in`); rank 0
+ * receives the container, other ranks an empty buffer */
+int pmklc_compress_dist(void* handle, const uint8_t* in, const uint8_t* d_in, size_t n,
+                        const pmklc_cfg* cfg, uint8_t** out, size_t* out_n, pmklc_timing* timing);
+/* every rank passes the container; rank 0 receives the original bytes */
+int pmklc_decompress_dist(void* handle, const uint8_t* in, size_t n, const char* pub_model_path,
+                          uint8_t** out, size_t* out_n, pmklc_timing* timing);
+/* host logic of the above (CPU-testable): this rank's cross-rank handoff ops
+ * in tick order (send = 1: this rank sends chunk src's state to `peer`) and
+ * the number of (tick, chunk) model steps it runs */
+int pmklc_dist_plan(const uint64_t* lens, size_t n_chunks, uint32_t bs, uint32_t t,
+                    uint16_t smp_per_myriad, int32_t rank, int32_t world, int64_t* op_tick,
+                    int32_t* op_src, int32_t* op_dst, int32_t* op_peer, uint8_t* op_send,
+                    size_t cap, size_t* n_ops, uint64_t* local_steps);
+
 /* seeded (untrained) BiGRU predictor file in the reference's PMKW format
  * (BiGruModel + serialize_model, models.cpp:38-51,159-173); layers = 2 is a
  * SPuM as the reference tests write it (acceptance.cpp:58-69). Host-only. */

@@ -1633,6 +1633,38 @@ int orc_dump_chunk(const uint32_t* tokens, uint64_t n_tokens, uint32_t flags_bit
   *snap_n = s.n;
   LEAVE;
 }
+/* one chunk from an inbound snapshot; also returns the trainer snapshot taken
+ * when steps_done == snap_at (ChunkWorker::maybe_snapshot, pipeline.cpp:207-213),
+ * empty when never reached */
+int orc_encode_chunk_snap(const uint32_t* tokens, uint64_t n_tokens, uint32_t flags_bits,
+                          const char* pub_path, uint32_t k, uint32_t t, uint32_t bs,
+                          uint32_t scale, uint64_t dm_seed, const uint8_t* inbound,
+                          size_t inbound_n, uint64_t snap_at, uint8_t** payload,
+                          size_t* payload_n, uint8_t** snap, size_t* snap_n) {
+  ENTRY;
+  const dims_t dims = make_dims(1u << (2 * k), t, scale);
+  bigru_t pub;
+  if (flags_bits & 1) {
+    buf_t f = read_whole(pub_path);
+    bigru_deserialize(&pub, f.p, f.n);
+    free(f.p);
+  }
+  buf_t sb = {0};
+  chunk_spec sp = {(int)flags_bits, (flags_bits & 1) ? &pub : NULL, NULL, dims, t, bs, dm_seed,
+                   inbound, inbound_n, snap_at, snap_at ? &sb : NULL, NULL, NULL, 0};
+  worker_t w;
+  worker_init(&w, &sp, n_tokens);
+  buf_t o = {0};
+  worker_encode(&w, tokens, &o);
+  worker_free(&w);
+  if (flags_bits & 1) bigru_free(&pub);
+  *payload = o.p;
+  *payload_n = o.n;
+  *snap = sb.p;
+  *snap_n = sb.n;
+  LEAVE;
+}
+
 int orc_pretrain_private(const uint32_t* tokens, uint64_t m, const char* pub_path, uint32_t k,
                          uint32_t t, uint32_t batch, uint32_t scale, uint64_t seed,
                          uint8_t** out, size_t* out_n) {

@@ -55,6 +55,11 @@ int orc_dump_chunk(const uint32_t* tokens, uint64_t n_tokens, uint32_t flags_bit
                    uint64_t dm_seed, const uint8_t* inbound, size_t inbound_n, float* probs,
                    uint64_t max_steps, uint8_t** payload, size_t* payload_n, uint8_t** snap,
                    size_t* snap_n);
+int orc_encode_chunk_snap(const uint32_t* tokens, uint64_t n_tokens, uint32_t flags_bits,
+                          const char* pub_path, uint32_t k, uint32_t t, uint32_t bs,
+                          uint32_t scale, uint64_t dm_seed, const uint8_t* inbound,
+                          size_t inbound_n, uint64_t snap_at, uint8_t** payload,
+                          size_t* payload_n, uint8_t** snap, size_t* snap_n);
 int orc_pretrain_private(const uint32_t* tokens, uint64_t m, const char* pub_path, uint32_t k,
                          uint32_t t, uint32_t batch, uint32_t scale, uint64_t seed,
                          uint8_t** out, size_t* out_n);

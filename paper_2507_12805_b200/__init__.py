@@ -68,6 +68,8 @@ EXPORTS = [
     "pmklc_errc_name", "pmklc_version", "pmklc_synth_markov3", "pmklc_synth_uniform",
     "pmklc_synth_genome", "pmklc_synth_species", "pmklc_synth_packed_codes", "pmklc_plan_chunks",
     "pmklc_schedule", "pmklc_quantize", "pmklc_write_bigru", "pmklc_bench_kernel",
+    "pmklc_nccl_id", "pmklc_dist_create", "pmklc_dist_destroy", "pmklc_compress_dist",
+    "pmklc_decompress_dist", "pmklc_dist_plan",
 ]
 
 _lib = None
@@ -319,6 +321,72 @@ def bench_kernel(name: str, chunks: int, scale: int = 4, rows: int = 320, t: int
     _check(lib().pmklc_bench_kernel(name.encode(), device, chunks, scale, rows, t, iters,
                                     C.byref(ms), C.byref(fl), C.byref(by)))
     return ms.value, fl.value, by.value
+
+
+def dist_plan(lens: Sequence[int], bs: int, t: int, smp_per_myriad: int, rank: int, world: int):
+    """This rank's cross-rank SMP handoffs [(tick, src, dst, peer, send)] and its
+    number of model steps (host logic of PMKLC-M, no GPU needed)."""
+    nc = len(lens)
+    L = (C.c_uint64 * nc)(*lens)
+    cap = 4 * nc + 4
+    tk = (C.c_int64 * cap)()
+    sr, ds, pe = (C.c_int32 * cap)(), (C.c_int32 * cap)(), (C.c_int32 * cap)()
+    se = (C.c_uint8 * cap)()
+    nops, steps = C.c_size_t(), C.c_uint64()
+    _check(lib().pmklc_dist_plan(L, C.c_size_t(nc), bs, t, C.c_uint16(smp_per_myriad), rank, world,
+                                 tk, sr, ds, pe, se, C.c_size_t(cap), C.byref(nops), C.byref(steps)))
+    return [(tk[i], sr[i], ds[i], pe[i], bool(se[i])) for i in range(nops.value)], steps.value
+
+
+class DistContext:
+    """PMKLC-M communicator for this process's GPU. Uses torch.distributed
+    (any backend) only to broadcast the 128-byte NCCL id from rank 0."""
+
+    def __init__(self, rank: int, world: int, device: int):
+        import torch.distributed as dist
+        buf = (C.c_uint8 * 128)()
+        if rank == 0:
+            _check(lib().pmklc_nccl_id(buf))
+        obj = [bytes(buf)]
+        dist.broadcast_object_list(obj, src=0)
+        idb = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        _check(lib().pmklc_dist_create(idb, rank, world, device, C.byref(h)))
+        self.h, self.rank, self.world, self.device = h, rank, world, device
+
+    def compress(self, raw: bytes, cfg: CompressConfig, timing: Optional[Timing] = None) -> bytes:
+        c = cfg._c()
+        out = C.POINTER(C.c_uint8)()
+        n = C.c_size_t()
+        tm = timing if timing is not None else Timing()
+        _check(lib().pmklc_compress_dist(self.h, raw, None, C.c_size_t(len(raw)), C.byref(c),
+                                         C.byref(out), C.byref(n), C.byref(tm)))
+        return _take(out, n.value)
+
+    def compress_device(self, d_ptr: int, n: int, cfg: CompressConfig,
+                        timing: Optional[Timing] = None) -> bytes:
+        c = cfg._c()
+        out = C.POINTER(C.c_uint8)()
+        on = C.c_size_t()
+        tm = timing if timing is not None else Timing()
+        _check(lib().pmklc_compress_dist(self.h, None, C.c_void_p(d_ptr), C.c_size_t(n), C.byref(c),
+                                         C.byref(out), C.byref(on), C.byref(tm)))
+        return _take(out, on.value)
+
+    def decompress(self, blob: bytes, pub_model_path: str = "",
+                   timing: Optional[Timing] = None) -> bytes:
+        out = C.POINTER(C.c_uint8)()
+        n = C.c_size_t()
+        tm = timing if timing is not None else Timing()
+        _check(lib().pmklc_decompress_dist(self.h, blob, C.c_size_t(len(blob)),
+                                           pub_model_path.encode() if pub_model_path else None,
+                                           C.byref(out), C.byref(n), C.byref(tm)))
+        return _take(out, n.value)
+
+    def close(self):
+        if self.h:
+            lib().pmklc_dist_destroy(self.h)
+            self.h = None
 
 
 def version() -> str:

@@ -281,6 +281,71 @@ int pmklc_bench_kernel(const char* name, int32_t device, uint32_t chunks, uint32
   });
 }
 
+int pmklc_nccl_id(uint8_t* out128) {
+  return guard([&] { nccl_unique_id(out128); });
+}
+
+int pmklc_dist_create(const uint8_t* id128, int32_t rank, int32_t world, int32_t device, void** handle) {
+  return guard([&] { *handle = dist_create(id128, rank, world, device); });
+}
+
+void pmklc_dist_destroy(void* handle) { dist_destroy(static_cast<Dist*>(handle)); }
+
+int pmklc_compress_dist(void* handle, const uint8_t* in, const uint8_t* d_in, size_t n,
+                        const pmklc_cfg* cfg, uint8_t** out, size_t* out_n, pmklc_timing* timing) {
+  return guard([&] {
+    Timing t;
+    CallOptions opt;
+    opt.timing = &t;
+    Bytes v = compress_dist(*static_cast<Dist*>(handle), in, d_in, n, to_cfg(cfg), opt);
+    copy_timing(t, timing);
+    *out = dup(v);
+    *out_n = v.size();
+  });
+}
+
+int pmklc_decompress_dist(void* handle, const uint8_t* in, size_t n, const char* pub_model_path,
+                          uint8_t** out, size_t* out_n, pmklc_timing* timing) {
+  return guard([&] {
+    Timing t;
+    CallOptions opt;
+    opt.timing = &t;
+    Bytes v = decompress_dist(*static_cast<Dist*>(handle), in, n, pub_model_path ? pub_model_path : "", opt);
+    copy_timing(t, timing);
+    *out = dup(v);
+    *out_n = v.size();
+  });
+}
+
+int pmklc_dist_plan(const uint64_t* lens, size_t n_chunks, uint32_t bs, uint32_t t, uint16_t myriad,
+                    int32_t rank, int32_t world, int64_t* op_tick, int32_t* op_src, int32_t* op_dst,
+                    int32_t* op_peer, uint8_t* op_send, size_t cap, size_t* n_ops,
+                    uint64_t* local_steps) {
+  return guard([&] {
+    if (world < 1 || rank < 0 || rank >= world) raise(errc::config_invalid, "rank/world");
+    Plan p;
+    p.bs = bs;
+    p.t = t;
+    p.myriad = myriad;
+    uint64_t s = 0;
+    for (size_t i = 0; i < n_chunks; ++i) {
+      p.start.push_back(s);
+      p.len.push_back(lens[i]);
+      s += lens[i];
+    }
+    const RankPlan rp = plan_rank(make_schedule(p, myriad > 0), rank, world);
+    *n_ops = rp.ops.size();
+    for (size_t i = 0; i < rp.ops.size() && i < cap; ++i) {
+      op_tick[i] = rp.ops[i].tick;
+      op_src[i] = rp.ops[i].src;
+      op_dst[i] = rp.ops[i].dst;
+      op_peer[i] = rp.ops[i].peer;
+      op_send[i] = rp.ops[i].send ? 1 : 0;
+    }
+    if (local_steps) *local_steps = rp.local.act.size();
+  });
+}
+
 void pmklc_free(void* p) { std::free(p); }
 void pmklc_device_free(void* d_p) {
   if (d_p) cudaFree(d_p);

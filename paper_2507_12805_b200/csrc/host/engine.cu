@@ -13,6 +13,7 @@
 
 #include "../kernels/kernels.hpp"
 #include "container.hpp"
+#include "nccl_loader.hpp"
 #include "plan.hpp"
 #include "rng.hpp"
 
@@ -221,6 +222,9 @@ struct ChunkRun {
   std::vector<const uint8_t*> pay_in;
   std::vector<uint64_t> pay_in_len;
   const CallOptions* opt = nullptr;
+  // PMKLC-M across ranks (nullptr: single GPU)
+  const RankPlan* rplan = nullptr;
+  ncclComm_t comm = nullptr;
   // outputs
   std::vector<Bytes> payloads;  // encode
   std::vector<ChunkStats> stats;
@@ -346,18 +350,20 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   DBuf<double> warm_loss(W);
   warm_loss.zero(st);
 
-  // ---- schedule lists (CSR per tick) + the device tick descriptor
-  DBuf<int> d_act(std::max<size_t>(sch.act.size(), 1));
-  if (!sch.act.empty()) d_act.upload(reinterpret_cast<const int*>(sch.act.data()), sch.act.size(), st);
-  DBuf<int2> d_hand(std::max<size_t>(sch.hand.size() / 2, 1));
-  if (!sch.hand.empty())
-    d_hand.upload(reinterpret_cast<const int2*>(sch.hand.data()), sch.hand.size() / 2, st);
-  DBuf<uint32_t> d_act_ptr(sch.act_ptr.size()), d_hand_ptr(sch.hand_ptr.size());
-  d_act_ptr.upload(sch.act_ptr.data(), sch.act_ptr.size(), st);
-  d_hand_ptr.upload(sch.hand_ptr.data(), sch.hand_ptr.size(), st);
+  // ---- schedule lists (CSR per tick) + the device tick descriptor; with
+  // several ranks the lists are this rank's (its chunks, local handoffs)
+  const Schedule& lsch = run.rplan ? run.rplan->local : sch;
+  DBuf<int> d_act(std::max<size_t>(lsch.act.size(), 1));
+  if (!lsch.act.empty()) d_act.upload(reinterpret_cast<const int*>(lsch.act.data()), lsch.act.size(), st);
+  DBuf<int2> d_hand(std::max<size_t>(lsch.hand.size() / 2, 1));
+  if (!lsch.hand.empty())
+    d_hand.upload(reinterpret_cast<const int2*>(lsch.hand.data()), lsch.hand.size() / 2, st);
+  DBuf<uint32_t> d_act_ptr(lsch.act_ptr.size()), d_hand_ptr(lsch.hand_ptr.size());
+  d_act_ptr.upload(lsch.act_ptr.data(), lsch.act_ptr.size(), st);
+  d_hand_ptr.upload(lsch.hand_ptr.data(), lsch.hand_ptr.size(), st);
   uint32_t max_hand = 0;
-  for (size_t t = 0; t + 1 < sch.hand_ptr.size(); ++t)
-    max_hand = std::max(max_hand, sch.hand_ptr[t + 1] - sch.hand_ptr[t]);
+  for (size_t t = 0; t + 1 < lsch.hand_ptr.size(); ++t)
+    max_hand = std::max(max_hand, lsch.hand_ptr[t + 1] - lsch.hand_ptr[t]);
   DBuf<TickDesc> d_td(1);
   {
     const TickDesc td0{-1, nullptr, nullptr, 0, 0};
@@ -417,7 +423,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   // One tick = one coded batch step of every active chunk. The sequence is
   // fixed (grids sized for the schedule's max concurrency, surplus blocks
   // exit), so it is captured once into a CUDA graph and replayed per tick.
-  const int na = int(std::max<uint32_t>(sch.max_active, 1));
+  const int na = int(std::max<uint32_t>(lsch.max_active, 1));
   const int nh = int(max_hand);
   const TickDesc* act = d_td.p;
   uint64_t tick_launches = 0;
@@ -557,6 +563,31 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     tick_launches = run.launches - l0;
   };
 
+  // cross-rank SMP handoffs due at a tick: grouped point-to-point transfers
+  // of the whole state slot (w, m, v, Adam scalars) on the engine stream,
+  // between the previous tick's graph and this tick's
+  size_t op_i = 0;
+  auto comm_ops = [&](int64_t tick) {
+    if (!run.rplan) return;
+    const std::vector<CommOp>& ops = run.rplan->ops;
+    if (op_i >= ops.size() || ops[op_i].tick != tick) return;
+    auto nck = [](ncclResult_t r) {
+      if (r != ncclSuccess) raise(errc::cuda_error, std::string("NCCL: ") + nccl().GetErrorString(r));
+    };
+    nck(nccl().GroupStart());
+    for (; op_i < ops.size() && ops[op_i].tick == tick; ++op_i) {
+      const CommOp& o = ops[op_i];
+      const int64_t c = o.send ? o.src : o.dst;
+      float* bufs[3] = {w.p + c * P, m.p + c * P, v.p + c * P};
+      for (float* b : bufs) {
+        if (o.send) nck(nccl().Send(b, size_t(P), ncclFloat32, o.peer, run.comm, st));
+        else nck(nccl().Recv(b, size_t(P), ncclFloat32, o.peer, run.comm, st));
+      }
+      if (o.send) nck(nccl().Send(sc.p + c, sizeof(AdamScalars), ncclUint8, o.peer, run.comm, st));
+      else nck(nccl().Recv(sc.p + c, sizeof(AdamScalars), ncclUint8, o.peer, run.comm, st));
+    }
+    nck(nccl().GroupEnd());
+  };
   const bool probing = run.opt && run.opt->probe && run.opt->probe_chunk >= 0;
   const bool host_sync = probing || want_stats;
   if (sch.ticks > 0 && !host_sync) {
@@ -567,13 +598,17 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     enqueue_tick(-1);
     CK(cudaStreamEndCapture(st, &graph));
     CK(cudaGraphInstantiate(&exec, graph, 0));
-    for (int64_t tick = 0; tick < sch.ticks; ++tick) CK(cudaGraphLaunch(exec, st));
+    for (int64_t tick = 0; tick < sch.ticks; ++tick) {
+      comm_ops(tick);
+      CK(cudaGraphLaunch(exec, st));
+    }
     run.launches += tick_launches * uint64_t(sch.ticks - 1);
     CK(cudaGraphExecDestroy(exec));
     CK(cudaGraphDestroy(graph));
   } else {
     for (int64_t tick = 0; tick < sch.ticks; ++tick) {
       snapshots_for_tick(tick);
+      comm_ops(tick);
       enqueue_tick(probing ? tick : -1);
     }
   }
@@ -683,8 +718,12 @@ void canonicalize_device(const uint8_t* d_raw, uint64_t n, Canon& out, cudaStrea
   CK(cudaStreamSynchronize(st));
 }
 
+void nck(ncclResult_t r) {
+  if (r != ncclSuccess) raise(errc::cuda_error, std::string("NCCL: ") + nccl().GetErrorString(r));
+}
+
 Bytes compress_impl(const uint8_t* h_raw, const uint8_t* d_raw_in, size_t n, const Config& cfg,
-                    const CallOptions& opt) {
+                    const CallOptions& opt, const Dist* dist = nullptr) {
   cfg.validate();
   CK(cudaSetDevice(cfg.device));
   Stream stream(cfg.device);
@@ -765,7 +804,63 @@ Bytes compress_impl(const uint8_t* h_raw, const uint8_t* d_raw_in, size_t n, con
   run.start = plan.start;
   run.sch = make_schedule(plan, myriad > 0);
   run.opt = &opt;
+  RankPlan rplan;
+  const bool multi = dist && dist->world > 1;
+  if (multi) {
+    rplan = plan_rank(run.sch, dist->rank, dist->world);
+    run.rplan = &rplan;
+    run.comm = static_cast<ncclComm_t>(dist->comm);
+  }
   if (W) run_chunks(run, d_tok.p, st);
+  if (multi && W) {
+    // gather every chunk's codestream on rank 0: sizes by all-reduce, then
+    // each rank's own payloads (chunk order, concatenated) by send/recv
+    const ncclComm_t comm = static_cast<ncclComm_t>(dist->comm);
+    std::vector<uint64_t> sz(W, 0);
+    for (size_t c = 0; c < W; ++c)
+      if (rplan.mine[c]) sz[c] = run.payloads[c].size();
+    DBuf<uint64_t> dsz(W);
+    dsz.upload(sz.data(), W, st);
+    nck(nccl().AllReduce(dsz.p, dsz.p, W, ncclUint64, ncclSum, comm, st));
+    CK(cudaMemcpyAsync(sz.data(), dsz.p, W * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<uint64_t> per_rank(size_t(dist->world), 0);
+    for (size_t c = 0; c < W; ++c) per_rank[size_t(owner_of(c, dist->world))] += sz[c];
+    if (dist->rank != 0) {
+      Bytes cat;
+      for (size_t c = 0; c < W; ++c)
+        if (rplan.mine[c]) cat.insert(cat.end(), run.payloads[c].begin(), run.payloads[c].end());
+      DBuf<uint8_t> buf(cat.size() + 1);
+      buf.upload(cat.data(), cat.size(), st);
+      nck(nccl().Send(buf.p, cat.size(), ncclUint8, 0, comm, st));
+      CK(cudaStreamSynchronize(st));
+      if (opt.stats) *opt.stats = run.stats;
+      return Bytes{};
+    }
+    std::vector<DBuf<uint8_t>> bufs(size_t(dist->world));
+    nck(nccl().GroupStart());
+    for (int r = 1; r < dist->world; ++r) {
+      bufs[size_t(r)].alloc(per_rank[size_t(r)] + 1);
+      nck(nccl().Recv(bufs[size_t(r)].p, per_rank[size_t(r)], ncclUint8, r, comm, st));
+    }
+    nck(nccl().GroupEnd());
+    std::vector<uint64_t> at(size_t(dist->world), 0);
+    std::vector<Bytes> host(size_t(dist->world));
+    for (int r = 1; r < dist->world; ++r) {
+      host[size_t(r)].resize(per_rank[size_t(r)]);
+      if (per_rank[size_t(r)])
+        CK(cudaMemcpyAsync(host[size_t(r)].data(), bufs[size_t(r)].p, per_rank[size_t(r)],
+                           cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    for (size_t c = 0; c < W; ++c) {
+      const int r = owner_of(c, dist->world);
+      if (r == 0) continue;
+      const uint8_t* src = host[size_t(r)].data() + at[size_t(r)];
+      run.payloads[c].assign(src, src + sz[c]);
+      at[size_t(r)] += sz[c];
+    }
+  }
 
   // trailers: leftover tokens of each chunk (len - bs*L)
   Container c;
@@ -826,7 +921,8 @@ struct DecodeResult {
 };
 
 void decompress_impl(const uint8_t* blob, size_t n, const std::string& pub_path, int device,
-                     const CallOptions& opt, DecodeResult& res, cudaStream_t st) {
+                     const CallOptions& opt, DecodeResult& res, cudaStream_t st,
+                     const Dist* dist = nullptr) {
   Event t0, t1, t2, t3;
   t0.record(st);
   const Container c = read_container(blob, n);
@@ -897,7 +993,34 @@ void decompress_impl(const uint8_t* blob, size_t n, const std::string& pub_path,
     run.pay_in_len.push_back(c.chunks[i].payload_len);
   }
   t1.record(st);
+  RankPlan rplan;
+  const bool multi = dist && dist->world > 1;
+  if (multi) {
+    rplan = plan_rank(run.sch, dist->rank, dist->world);
+    run.rplan = &rplan;
+    run.comm = static_cast<ncclComm_t>(dist->comm);
+  }
   if (W) run_chunks(run, d_tok.p, st);
+  if (multi && W) {
+    // decoded tokens of every chunk to rank 0 (device to device)
+    const ncclComm_t comm = static_cast<ncclComm_t>(dist->comm);
+    nck(nccl().GroupStart());
+    for (size_t i = 0; i < W; ++i) {
+      const int r = owner_of(i, dist->world);
+      const uint64_t used = uint64_t(c.bs) * run.sch.L[i];
+      if (r == 0 || used == 0) continue;
+      if (dist->rank == r) nck(nccl().Send(d_tok.p + c.chunks[i].token_start, used, ncclUint32, 0, comm, st));
+      else if (dist->rank == 0)
+        nck(nccl().Recv(d_tok.p + c.chunks[i].token_start, used, ncclUint32, r, comm, st));
+    }
+    nck(nccl().GroupEnd());
+    if (dist->rank != 0) {
+      CK(cudaStreamSynchronize(st));
+      if (opt.stats) *opt.stats = run.stats;
+      res.len = 0;
+      return;
+    }
+  }
   // trailers (pipeline.cpp:431-436)
   for (size_t i = 0; i < W; ++i) {
     const ChunkEntry& e = c.chunks[i];
@@ -957,11 +1080,11 @@ void decompress_impl(const uint8_t* blob, size_t n, const std::string& pub_path,
 }  // namespace
 
 Bytes compress(const uint8_t* raw, size_t n, const Config& cfg, const CallOptions& opt) {
-  return compress_impl(raw, nullptr, n, cfg, opt);
+  return compress_impl(raw, nullptr, n, cfg, opt, nullptr);
 }
 
 Bytes compress_device(const uint8_t* d_raw, size_t n, const Config& cfg, const CallOptions& opt) {
-  return compress_impl(nullptr, d_raw, n, cfg, opt);
+  return compress_impl(nullptr, d_raw, n, cfg, opt, nullptr);
 }
 
 Bytes decompress(const uint8_t* blob, size_t n, const std::string& pub_model_path, uint32_t workers,
@@ -1199,6 +1322,51 @@ KernelBench bench_kernel(const std::string& name, int device, uint32_t chunks, u
   CK(cudaStreamSynchronize(st));
   kb.avg_ms = Event::ms(e0, e1) / iters;
   return kb;
+}
+
+void nccl_unique_id(uint8_t out[128]) {
+  ncclUniqueId id;
+  nck(nccl().GetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  std::memcpy(out, &id, 128);
+}
+
+Dist* dist_create(const uint8_t id[128], int rank, int world, int device) {
+  CK(cudaSetDevice(device));
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, 128);
+  ncclComm_t comm = nullptr;
+  nck(nccl().CommInitRank(&comm, world, uid, rank));
+  Dist* d = new Dist;
+  d->comm = comm;
+  d->rank = rank;
+  d->world = world;
+  d->device = device;
+  return d;
+}
+
+void dist_destroy(Dist* d) {
+  if (!d) return;
+  if (d->comm) nccl().CommDestroy(static_cast<ncclComm_t>(d->comm));
+  delete d;
+}
+
+Bytes compress_dist(const Dist& d, const uint8_t* h_raw, const uint8_t* d_raw, size_t n,
+                    const Config& cfg_in, const CallOptions& opt) {
+  Config cfg = cfg_in;
+  cfg.device = d.device;
+  return compress_impl(h_raw, d_raw, n, cfg, opt, &d);
+}
+
+Bytes decompress_dist(const Dist& d, const uint8_t* blob, size_t n, const std::string& pub_model_path,
+                      const CallOptions& opt) {
+  CK(cudaSetDevice(d.device));
+  Stream stream(d.device);
+  DecodeResult res;
+  decompress_impl(blob, n, pub_model_path, d.device, opt, res, stream.s, &d);
+  Bytes out(res.len);
+  if (res.len) CK(cudaMemcpy(out.data(), res.out.p, res.len, cudaMemcpyDeviceToHost));
+  return out;
 }
 
 }  // namespace pmklc_b200

@@ -48,6 +48,22 @@ struct CallOptions {
   std::vector<float>* probe = nullptr;
 };
 
+// PMKLC-M: one process per GPU, NCCL communicator between them.
+struct Dist {
+  void* comm = nullptr;  // ncclComm_t
+  int rank = 0, world = 1, device = 0;
+};
+void nccl_unique_id(uint8_t out[128]);
+Dist* dist_create(const uint8_t id[128], int rank, int world, int device);
+void dist_destroy(Dist* d);
+// Every rank passes the whole input; rank 0 receives the container (others
+// return an empty vector). Chunks run on rank c % world (plan_rank).
+Bytes compress_dist(const Dist& d, const uint8_t* h_raw, const uint8_t* d_raw, size_t n,
+                    const Config& cfg, const CallOptions& opt = {});
+// Every rank passes the container; rank 0 receives the decompressed bytes.
+Bytes decompress_dist(const Dist& d, const uint8_t* blob, size_t n, const std::string& pub_model_path,
+                      const CallOptions& opt = {});
+
 // host buffers in / out
 Bytes compress(const uint8_t* raw, size_t n, const Config& cfg, const CallOptions& opt = {});
 Bytes decompress(const uint8_t* blob, size_t n, const std::string& pub_model_path, uint32_t workers,

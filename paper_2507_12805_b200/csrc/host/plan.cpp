@@ -94,4 +94,44 @@ Schedule make_schedule(const Plan& p, bool smp_on) {
   return s;
 }
 
+RankPlan plan_rank(const Schedule& s, int rank, int world) {
+  RankPlan rp;
+  rp.rank = rank;
+  rp.world = world;
+  rp.local = s;
+  const size_t W = s.L.size();
+  rp.mine.resize(W);
+  for (size_t c = 0; c < W; ++c) rp.mine[c] = owner_of(c, world) == rank;
+  Schedule& l = rp.local;
+  l.act.clear();
+  l.hand.clear();
+  l.act_ptr.assign(1, 0);
+  l.hand_ptr.assign(1, 0);
+  l.max_active = 0;
+  for (int64_t t = 0; t < s.ticks; ++t) {
+    uint32_t n = 0;
+    for (uint32_t i = s.act_ptr[size_t(t)]; i < s.act_ptr[size_t(t) + 1]; ++i)
+      if (rp.mine[s.act[i]]) {
+        l.act.push_back(s.act[i]);
+        ++n;
+      }
+    l.act_ptr.push_back(uint32_t(l.act.size()));
+    l.max_active = std::max(l.max_active, n);
+    for (uint32_t i = s.hand_ptr[size_t(t)]; i < s.hand_ptr[size_t(t) + 1]; ++i) {
+      const int32_t src = s.hand[2 * i], dst = s.hand[2 * i + 1];
+      const bool ms = rp.mine[size_t(src)], md = rp.mine[size_t(dst)];
+      if (ms && md) {
+        l.hand.push_back(src);
+        l.hand.push_back(dst);
+      } else if (ms) {
+        rp.ops.push_back(CommOp{t, src, dst, owner_of(size_t(dst), world), true});
+      } else if (md) {
+        rp.ops.push_back(CommOp{t, src, dst, owner_of(size_t(src), world), false});
+      }
+    }
+    l.hand_ptr.push_back(uint32_t(l.hand.size() / 2));
+  }
+  return rp;
+}
+
 }  // namespace pmklc_b200

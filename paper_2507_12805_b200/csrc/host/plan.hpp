@@ -43,4 +43,26 @@ struct Schedule {
 // smp_on: myriad > 0 (the container's smp_per_myriad field)
 Schedule make_schedule(const Plan& p, bool smp_on);
 
+// PMKLC-M across ranks (one GPU each): chunk c is owned by rank c % world
+// (round robin, so the SMP wavefront of consecutive chunks spreads over all
+// GPUs). A rank steps only its own chunks; an SMP handoff between chunks on
+// different ranks becomes a point-to-point transfer of the state slot at the
+// handoff tick (sender: state after src_steps model steps; receiver: the
+// destination slot, before its first model step). Both sides derive the same
+// op list from the same schedule, in the same order, so sends and receives
+// match without negotiation.
+struct CommOp {
+  int64_t tick;
+  int32_t src, dst, peer;
+  bool send;
+};
+struct RankPlan {
+  int rank = 0, world = 1;
+  Schedule local;            // act / hand filtered to this rank (hand: local->local only)
+  std::vector<CommOp> ops;   // cross-rank handoffs touching this rank, tick order
+  std::vector<uint8_t> mine; // per chunk: owned by this rank
+};
+inline int owner_of(size_t chunk, int world) { return int(chunk % size_t(world)); }
+RankPlan plan_rank(const Schedule& s, int rank, int world);
+
 }  // namespace pmklc_b200

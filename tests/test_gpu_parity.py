@@ -251,3 +251,23 @@ def test_truncated_payload_stream_exhausted(P):
     with pytest.raises(P.PmklcError) as e:
         P.decompress(bytes(b))
     assert e.value.errc in ("StreamExhausted", "CorruptStream")
+
+
+def test_dist_context_single_rank(P, checker):
+    # the PMKLC-M entry points with a 1-rank NCCL communicator: same container
+    import torch.distributed as dist
+    import os
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29541")
+    if not dist.is_initialized():
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    ctx = P.DistContext(0, 1, 0)
+    try:
+        raw = P.synth("markov3", 60000, 77)
+        kw = dict(t=8, bs=32, scale=16, workers=4, smp=0.2)
+        blob = ctx.compress(raw, P.CompressConfig(**_cfgs(kw)))
+        assert blob == checker.compress(raw, O.make_cfg(**kw))
+        assert ctx.decompress(blob) == raw
+    finally:
+        ctx.close()
+        dist.destroy_process_group()
