@@ -718,6 +718,143 @@ void canonicalize_device(const uint8_t* d_raw, uint64_t n, Canon& out, cudaStrea
   CK(cudaStreamSynchronize(st));
 }
 
+// pretrain_private (training.cpp:62-83) on the device: derive_private_init
+// when the public model fits (models.cpp:200-215), else a seeded 1-layer
+// BiGRU; then train_pass (training.cpp:8-41): one Adam step per batch of
+// `batch` consecutive positions, strictly in order. Full batches replay one
+// captured CUDA graph (the position lives in device memory); the final
+// partial batch runs eagerly.
+BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, const Dims& dims,
+                           uint32_t t, uint32_t batch, uint64_t seed, cudaStream_t st,
+                           uint64_t* launches) {
+  if (m < uint64_t(t) + 1) raise(errc::target_too_short, "target shorter than t+1 tokens");
+  BiGru model = BiGru::seeded(dims, 1, seed);
+  if (pub && pub->fits(dims)) {
+    for (const ParamDesc& d : model.ps) {
+      if (d.name != "emb.table" && d.name.rfind("gru0.", 0) != 0) continue;
+      for (const ParamDesc& q : pub->ps)
+        if (q.name == d.name) {
+          if (q.count != d.count) raise(errc::architecture_mismatch, d.name);
+          std::memcpy(model.w.data() + d.off, pub->w.data() + q.off, d.count * 4);
+          break;
+        }
+    }
+  }
+  const int Es = int(dims.se), H = int(dims.sh), B = int(dims.sb), V = int(dims.V), T = int(t);
+  if (H > 32) raise(errc::config_invalid, "SPrM pre-pass on the GPU supports sp_hidden <= 32 (scale >= 4)");
+  const int64_t P = int64_t(model.total);
+  DBuf<float> w(P), g(P), mo(P), vo(P);
+  w.upload(model.w.data(), P, st);
+  g.zero(st);
+  mo.zero(st);
+  vo.zero(st);
+  std::vector<int64_t> hoffs;
+  for (const ParamDesc& d : model.ps) hoffs.push_back(int64_t(d.off));
+  DBuf<int64_t> offs(hoffs.size());
+  offs.upload(hoffs.data(), hoffs.size(), st);
+  DBuf<AdamScalars> sc(1);
+  const AdamScalars s0{0, 1.0f, 1.0f, 0.0f, 0.0f, {0, 0}};
+  sc.upload(&s0, 1, st);
+  const int64_t R = batch, RT = R * T;
+  DBuf<uint32_t> ctx(RT);
+  DBuf<float> X(2 * Es * RT), tab(6 * int64_t(V) * H), tape(10 * RT * H), fin(R * 2 * H),
+      bact(R * B), logits(R * V), gg(R * V), dbact(R * B), dfin(R * 2 * H), G(8 * H * RT),
+      HP(2 * H * RT), dx(RT * Es);
+  DBuf<int64_t> pos(1);
+  const int64_t p0 = t;
+  pos.upload(&p0, 1, st);
+  DBuf<int> act(1);
+  act.zero(st);
+  DBuf<TickDesc> td(1);
+  const TickDesc tdh{0, act.p, nullptr, 1, 0};
+  td.upload(&tdh, 1, st);
+  auto W_ = [&](int i) { return w.p + hoffs[size_t(i)]; };
+  auto G_ = [&](int i) { return g.p + hoffs[size_t(i)]; };
+  const int b0 = model.bott();
+  uint64_t nl = 0;
+  auto step = [&](int rows) {
+    SprmP sp{w.p, offs.p, rows, T, Es, H, V, B};
+    const int64_t rt = int64_t(rows) * T;
+    launch_sprm_prep(d_tok, pos.p, sp, ctx.p, X.p, tab.p, st);
+    launch_sprm_fwd(sp, ctx.p, tab.p, tape.p, fin.p, st);
+    // head: bact = tanh(bott.b + fin.bott.w); logits = out.b + bact.out.w
+    GemmP g1{};
+    g1.A = fin.p; g1.lda = 2 * H; g1.B = W_(b0); g1.ldb = B; g1.C = bact.p; g1.ldc = B;
+    g1.bias = W_(b0 + 1); g1.M = rows; g1.N = B; g1.K = 2 * H; g1.init = 1;
+    launch_gemm(g1, false, false, td.p, 1, st);
+    launch_tanh_vec(bact.p, int64_t(rows) * B, st);
+    GemmP g2{};
+    g2.A = bact.p; g2.lda = B; g2.B = W_(b0 + 2); g2.ldb = V; g2.C = logits.p; g2.ldc = V;
+    g2.bias = W_(b0 + 3); g2.M = rows; g2.N = V; g2.K = B; g2.init = 1;
+    launch_gemm(g2, false, false, td.p, 1, st);
+    launch_sprm_ce(sp, d_tok, pos.p, logits.p, gg.p, st);
+    // out.backward, tanh', bott.backward (models.cpp:75-86)
+    GemmP g3{};
+    g3.A = bact.p; g3.lda = B; g3.B = gg.p; g3.ldb = V; g3.C = G_(b0 + 2); g3.ldc = V;
+    g3.M = B; g3.N = V; g3.K = rows; g3.ones_row = 1; g3.init = 2;
+    launch_gemm(g3, true, false, td.p, 1, st);
+    GemmP g4{};
+    g4.A = gg.p; g4.lda = V; g4.B = W_(b0 + 2); g4.ldb = V; g4.C = dbact.p; g4.ldc = B;
+    g4.M = rows; g4.N = B; g4.K = V; g4.init = 0;
+    launch_gemm(g4, false, true, td.p, 1, st);
+    launch_sprm_tanh_grad(dbact.p, bact.p, int64_t(rows) * B, st);
+    GemmP g5{};
+    g5.A = fin.p; g5.lda = 2 * H; g5.B = dbact.p; g5.ldb = B; g5.C = G_(b0); g5.ldc = B;
+    g5.M = 2 * H; g5.N = B; g5.K = rows; g5.ones_row = 1; g5.init = 2;
+    launch_gemm(g5, true, false, td.p, 1, st);
+    GemmP g6{};
+    g6.A = dbact.p; g6.lda = B; g6.B = W_(b0); g6.ldb = B; g6.C = dfin.p; g6.ldc = 2 * H;
+    g6.M = rows; g6.N = 2 * H; g6.K = B; g6.init = 0;
+    launch_gemm(g6, false, true, td.p, 1, st);
+    // backward through time, then the weight-gradient reductions over (t desc, rows asc)
+    launch_sprm_bptt(sp, tape.p, dfin.p, G.p, HP.p, st);
+    for (int d = 0; d < 2; ++d) {
+      const float* Gan = G.p + (int64_t(0 * 2 + d) * H) * rt;
+      const float* Gar = G.p + (int64_t(1 * 2 + d) * H) * rt;
+      const float* Gaz = G.p + (int64_t(2 * 2 + d) * H) * rt;
+      const float* Ghh = G.p + (int64_t(3 * 2 + d) * H) * rt;
+      const float* Xd = X.p + int64_t(d) * Es * rt;
+      const float* Hd = HP.p + int64_t(d) * H * rt;
+      auto idx = [&](int gt) { return model.idx(0, d, gt); };
+      auto nt = [&](const float* A, int M, const float* Bm, int wg, int bg) {
+        return NtP{A, Bm, G_(idx(wg)), 0, 0, 0, rt, rt, H, M, H, int(rt), G_(idx(bg))};
+      };
+      const NtP a1 = nt(Xd, Es, Gan, BiGru::WIN, BiGru::BIN), a2 = nt(Xd, Es, Gar, BiGru::WIR, BiGru::BIR);
+      const NtP a3 = nt(Xd, Es, Gaz, BiGru::WIZ, BiGru::BIZ), a4 = nt(Hd, H, Ghh, BiGru::WHN, BiGru::BHN);
+      const NtP a5 = nt(Hd, H, Gar, BiGru::WHR, BiGru::BHR), a6 = nt(Hd, H, Gaz, BiGru::WHZ, BiGru::BHZ);
+      launch_gemm_nt(a1, &a2, td.p, 1, st);
+      launch_gemm_nt(a3, &a4, td.p, 1, st);
+      launch_gemm_nt(a5, &a6, td.p, 1, st);
+    }
+    launch_sprm_dx(sp, G.p, dx.p, st);
+    launch_sprm_emb_grad(sp, ctx.p, dx.p, g.p + hoffs[0], st);
+    launch_adam_scalars(sc.p, st);
+    launch_adam(w.p, g.p, mo.p, vo.p, 0, P, sc.p, td.p, 1, st);
+    launch_pos_advance(pos.p, batch, st);
+    nl += 22;
+  };
+  const uint64_t nsteps = (m - t + batch - 1) / batch;
+  const uint64_t full = (m - t) / batch;
+  if (full > 0) {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    step(int(batch));
+    CK(cudaStreamEndCapture(st, &graph));
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    for (uint64_t i = 0; i < full; ++i) CK(cudaGraphLaunch(exec, st));
+    nl += 22 * (full - 1);
+    CK(cudaGraphExecDestroy(exec));
+    CK(cudaGraphDestroy(graph));
+  }
+  if (nsteps > full) step(int((m - t) - full * batch));
+  check_launch();
+  CK(cudaMemcpyAsync(model.w.data(), w.p, P * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (launches) *launches += nl;
+  return model;
+}
+
 void nck(ncclResult_t r) {
   if (r != ncclSuccess) raise(errc::cuda_error, std::string("NCCL: ") + nccl().GetErrorString(r));
 }
@@ -786,9 +923,14 @@ Bytes compress_impl(const uint8_t* h_raw, const uint8_t* d_raw_in, size_t n, con
   }
   if ((flags & 1) && !models.has_pub) flags = 4;
   if ((flags & 2) && m < uint64_t(cfg.t) + 1) flags = 4;
-  if (flags & 2)
-    raise(errc::config_invalid,
-          "private-model pre-pass (pretrain_private) is not implemented on the B200 path yet");
+  BiGru priv_model;
+  uint64_t sprm_launches = 0;
+  if (flags & 2) {
+    priv_model = pretrain_private_gpu(d_tok.p, m, models.has_pub ? &models.pub.host : nullptr, dims,
+                                      cfg.t, cfg.bs, sprm_seed, st, &sprm_launches);
+    models.priv.upload(priv_model, st);
+    models.has_priv = true;
+  }
 
   const uint16_t myriad = uint16_t(std::lround(double(cfg.smp_fraction) * 10000.0));
   const Plan plan = plan_chunks(m, cfg.workers, cfg.bs, cfg.t, myriad);
@@ -800,6 +942,7 @@ Bytes compress_impl(const uint8_t* h_raw, const uint8_t* d_raw_in, size_t n, con
   run.flags = flags;
   run.decode = false;
   run.pub = models.has_pub ? &models.pub : nullptr;
+  run.priv = models.has_priv ? &models.priv : nullptr;
   run.dm_seed = dm_seed;
   run.start = plan.start;
   run.sch = make_schedule(plan, myriad > 0);
@@ -892,6 +1035,7 @@ Bytes compress_impl(const uint8_t* h_raw, const uint8_t* d_raw_in, size_t n, con
     c.payload_ptr.push_back(run.payloads[i].data());
     c.trailer_ptr.push_back(trailers[i].data());
   }
+  if (flags & 2) c.private_model = priv_model.serialize();
   c.exc_pos = std::move(canon.exc_pos);
   c.exc_byte = std::move(canon.exc_byte);
   c.residual = std::move(residual);
@@ -907,7 +1051,7 @@ Bytes compress_impl(const uint8_t* h_raw, const uint8_t* d_raw_in, size_t n, con
     tm.warmup_ms = run.warm_ms;
     tm.model_ms = run.model_ms;
     tm.ticks = uint64_t(run.sch.ticks);
-    tm.kernel_launches = run.launches + 3;
+    tm.kernel_launches = run.launches + sprm_launches + 3;
     tm.chunks = W;
     tm.h2d_bytes = h2d;
     tm.d2h_bytes = out.size();

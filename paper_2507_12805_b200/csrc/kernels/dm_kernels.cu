@@ -226,6 +226,7 @@ __global__ void __launch_bounds__(kNtCols * MR) k_gemm_nt(NtP p0, NtP p1, const 
   const float* Ab = second ? p1.A : p0.A;
   const float* Bb = second ? p1.B : p0.B;
   float* Cb = second ? p1.C : p0.C;
+  float* CBb = second ? p1.cb : p0.cb;
   const int64_t a_cs = second ? p1.a_cs : p0.a_cs, b_cs = second ? p1.b_cs : p0.b_cs,
                 c_cs = second ? p1.c_cs : p0.c_cs, lda = second ? p1.lda : p0.lda,
                 ldb = second ? p1.ldb : p0.ldb, ldc = second ? p1.ldc : p0.ldc;
@@ -267,7 +268,8 @@ __global__ void __launch_bounds__(kNtCols * MR) k_gemm_nt(NtP p0, NtP p1, const 
     cp_async_commit();  // one group per tile slot, possibly empty
   };
 
-  float acc = live ? C[int64_t(m) * ldc + n] : 0.0f;
+  float* out = live ? ((ones && CBb) ? CBb + c * c_cs + n : C + int64_t(m) * ldc + n) : nullptr;
+  float acc = live ? *out : 0.0f;
 #pragma unroll
   for (int s = 0; s < kNtStages - 1; ++s) load(s);
   for (int tile = 0; tile < ntiles; ++tile) {
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__(kNtCols * MR) k_gemm_nt(NtP p0, NtP p1, const 
     }
   }
   cp_async_wait<0>();
-  if (live) C[int64_t(m) * ldc + n] = acc;
+  if (live) *out = acc;
 }
 
 // ------------------------------------------------------------------ embed

@@ -86,6 +86,7 @@ struct NtP {
   const float* A; const float* B; float* C;
   int64_t a_cs, b_cs, c_cs, lda, ldb, ldc;
   int M, N, K;
+  float* cb;  // bias-row output (row M); nullptr: C + M*ldc (bias stored right after W)
 };
 void launch_gemm_nt(const NtP& p0, const NtP* p1, const TickDesc* td, int max_active,
                     cudaStream_t st);
@@ -186,5 +187,28 @@ void launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, 
                           int64_t work_cs, float* logits, int64_t lg_cs, const TickDesc* td,
                           int max_active, cudaStream_t st);
 size_t bigru_work_floats(const BiGruP& p);
+
+// SPrM pre-pass (pretrain_private / train_pass, training.cpp:8-83): one-layer
+// BiGRU trained with Adam over the whole token stream, bs rows per step.
+struct SprmP {
+  const float* w;       // flat parameter array (BiGru layout, 1 layer)
+  const int64_t* offs;  // device param offsets
+  int R, T, Es, H, V, B;
+};
+void launch_sprm_prep(const uint32_t* tokens, const int64_t* pos, const SprmP& s, uint32_t* ctx,
+                      float* X, float* tab, cudaStream_t st);
+void launch_sprm_fwd(const SprmP& s, const uint32_t* ctx, const float* tab, float* tape, float* fin,
+                     cudaStream_t st);
+void launch_sprm_ce(const SprmP& s, const uint32_t* tokens, const int64_t* pos, const float* logits,
+                    float* g, cudaStream_t st);
+void launch_sprm_tanh_grad(float* dbact, const float* bact, int64_t n, cudaStream_t st);
+void launch_sprm_bptt(const SprmP& s, const float* tape, const float* dfin, float* G, float* HP,
+                      cudaStream_t st);
+void launch_sprm_dx(const SprmP& s, const float* G, float* dx, cudaStream_t st);
+void launch_sprm_emb_grad(const SprmP& s, const uint32_t* ctx, const float* dx, float* grad_emb,
+                          cudaStream_t st);
+void launch_tanh_vec(float* x, int64_t n, cudaStream_t st);
+void launch_adam_scalars(AdamScalars* sc, cudaStream_t st);
+void launch_pos_advance(int64_t* pos, int64_t by, cudaStream_t st);
 
 }  // namespace pmklc_b200

@@ -1,0 +1,330 @@
+// SPrM pre-pass on sm_100a: one-layer BiGRU training pass (train_pass,
+// core/src/training.cpp:8-41) — forward with tape, det_softmax + CE grad,
+// backward through time (Gru::backward, layers.cpp:262-327; BiGru::backward,
+// 369-387; BiGruModel::backward, models.cpp:75-96) and Adam, one launch
+// sequence per batch of `bs` rows, strictly sequential across batches.
+//
+// Layouts (d = direction, t = the GRU's own time, r = row, j/q = unit):
+//   tape r,z,n,hh,out : [2][T][R][H]
+//   feature-major reduction operands, k = (T-1-t)*R + r so that ascending k
+//   is the reference's accumulation order (t descending, rows ascending):
+//   G{an,ar,az,hh}[d][j][k], HP[d][q][k] (h_{t-1}), X[d][i][k] (GRU input)
+#include <algorithm>
+#include <cstdint>
+
+#include "detmath.cuh"
+#include "kernels.hpp"
+
+namespace pmklc_b200 {
+
+namespace {
+
+enum { WIR, WIZ, WIN, WHR, WHZ, WHN, BIR, BIZ, BIN, BHR, BHZ, BHN, NG };
+__device__ __forceinline__ int64_t goff(const int64_t* offs, int dir, int t) {
+  return offs[1 + dir * NG + t];
+}
+
+// contexts of the batch at position p: ctx[r][i] = tok[p + r - T + i]; also
+// the GRU inputs X[d][i][k] and the per-token layer-0 projection table.
+__global__ void k_sprm_prep(const uint32_t* __restrict__ tokens, const int64_t* __restrict__ pos,
+                            SprmP s, uint32_t* ctx, float* X, float* tab) {
+  const int64_t p = *pos;
+  const int R = s.R, T = s.T, Es = s.Es, H = s.H, V = s.V;
+  const int64_t RT = int64_t(R) * T;
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const float* W = s.w;
+  if (tid < RT) {
+    const int r = int(tid / T), i = int(tid % T);
+    ctx[tid] = tokens[p + r - T + i];
+  }
+  // table[d][g][tok][j] = b_ig[j] + sum_p emb[tok][p] W_ig[p][j]
+  const int64_t ntab = int64_t(2) * 3 * V * H;
+  if (tid < ntab) {
+    const int j = int(tid % H);
+    const int64_t rest = tid / H;
+    const int tok = int(rest % V), dg = int(rest / V), d = dg / 3, g = dg % 3;
+    const float* Wg = W + goff(s.offs, d, WIR + g);
+    float acc = W[goff(s.offs, d, BIR + g) + j];
+    const float* e = W + s.offs[0] + int64_t(tok) * Es;
+    for (int q = 0; q < Es; ++q) acc = mac(acc, e[q], Wg[int64_t(q) * H + j]);
+    tab[tid] = acc;
+  }
+  // X[d][i][k]: fwd input at its time t is x[r][t]; bwd's is x[r][T-1-t]
+  const int64_t nx = int64_t(2) * Es * RT;
+  if (tid < nx) {
+    const int64_t k = tid % RT;
+    const int64_t rest = tid / RT;
+    const int i = int(rest % Es), d = int(rest / Es);
+    const int tt = int(T - 1 - k / R), r = int(k % R);  // own time t = T-1-k/R
+    const int src_t = d ? (T - 1 - tt) : tt;
+    const uint32_t tok = tokens[p + r - T + src_t];
+    X[tid] = W[s.offs[0] + int64_t(tok) * Es + i];
+  }
+}
+
+// forward recurrence with tape; warp per (row, dir), lane = unit (H <= 32)
+__global__ void __launch_bounds__(256) k_sprm_fwd(SprmP s, const uint32_t* __restrict__ ctx,
+                                                  const float* __restrict__ tab, float* tape,
+                                                  float* fin) {
+  __shared__ __align__(16) float sh[8][2][32];
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * 8 + wl;
+  if (g >= s.R * 2) return;
+  const int r = g >> 1, d = g & 1, T = s.T, H = s.H, R = s.R, V = s.V;
+  const float* W = s.w;
+  const bool act = lane < H;
+  const int j = act ? lane : 0;
+  const float* whr = W + goff(s.offs, d, WHR);
+  const float* whz = W + goff(s.offs, d, WHZ);
+  const float* whn = W + goff(s.offs, d, WHN);
+  const float bhr = W[goff(s.offs, d, BHR) + j], bhz = W[goff(s.offs, d, BHZ) + j],
+              bhn = W[goff(s.offs, d, BHN) + j];
+  const float* t0 = tab + int64_t(d) * 3 * V * H;
+  const int64_t TRH = int64_t(T) * R * H;
+  float* tr = tape + (int64_t(0 * 2 + d) * TRH);
+  float* tz = tape + (int64_t(1 * 2 + d) * TRH);
+  float* tn = tape + (int64_t(2 * 2 + d) * TRH);
+  float* th = tape + (int64_t(3 * 2 + d) * TRH);
+  float* to = tape + (int64_t(4 * 2 + d) * TRH);
+  if (act) sh[wl][0][j] = 0.0f;
+  __syncwarp();
+  int cur = 0;
+  for (int t = 0; t < T; ++t) {
+    const int src_t = d ? (T - 1 - t) : t;
+    const int64_t tok = ctx[int64_t(r) * T + src_t];
+    const float* h = sh[wl][cur];
+    float ar = fadd(t0[tok * H + j], bhr);
+    for (int q = 0; q < H; ++q) ar = mac(ar, h[q], whr[int64_t(q) * H + j]);
+    float az = fadd(t0[int64_t(V) * H + tok * H + j], bhz);
+    for (int q = 0; q < H; ++q) az = mac(az, h[q], whz[int64_t(q) * H + j]);
+    float hh = bhn;
+    for (int q = 0; q < H; ++q) hh = mac(hh, h[q], whn[int64_t(q) * H + j]);
+    const float an = t0[2 * int64_t(V) * H + tok * H + j];
+    const float rv = det_sigmoid(ar), zv = det_sigmoid(az);
+    const float nv = det_tanh(fadd(an, fmul(rv, hh)));
+    const float hv = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, h[j]));
+    if (act) {
+      const int64_t o = (int64_t(t) * R + r) * H + j;
+      tr[o] = rv;
+      tz[o] = zv;
+      tn[o] = nv;
+      th[o] = hh;
+      to[o] = hv;
+      sh[wl][cur ^ 1][j] = hv;
+    }
+    __syncwarp();
+    cur ^= 1;
+  }
+  if (act) fin[int64_t(r) * 2 * H + d * H + j] = sh[wl][cur][j];  // final_state (layers.cpp:389-399)
+}
+
+// g = det_softmax(logits) ; loss term ; g[tgt] -= 1   (training.cpp:28-34)
+__global__ void k_sprm_ce(SprmP s, const uint32_t* __restrict__ tokens,
+                          const int64_t* __restrict__ pos, const float* __restrict__ logits,
+                          float* g) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= s.R) return;
+  const int V = s.V;
+  const float* lr = logits + int64_t(row) * V;
+  float* gr = g + int64_t(row) * V;
+  float mx = -__int_as_float(0x7f800000);
+  for (int i = lane; i < V; i += 32) mx = fmaxf(mx, lr[i]);
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float sum = 0.0f;
+  for (int i0 = 0; i0 < V; i0 += 32) {
+    const int i = i0 + lane;
+    float e = 0.0f;
+    if (i < V) {
+      e = det_exp(fsub(lr[i], mx));
+      gr[i] = e;
+    }
+    const int cnt = min(32, V - i0);
+    for (int l = 0; l < cnt; ++l) sum = fadd(sum, __shfl_sync(0xffffffffu, e, l));
+  }
+  const float inv = fdiv(1.0f, sum);
+  const uint32_t tgt = tokens[*pos + row] & uint32_t(V - 1);
+  __syncwarp();
+  for (int i = lane; i < V; i += 32) {
+    float v = fmul(gr[i], inv);
+    if (uint32_t(i) == tgt) v = fsub(v, 1.0f);
+    gr[i] = v;
+  }
+}
+
+// dbact *= (1 - a*a)   (models.cpp:81-84)
+__global__ void k_sprm_tanh_grad(float* dbact, const float* __restrict__ bact, int64_t n) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const float a = bact[i];
+    dbact[i] = fmul(dbact[i], fsub(1.0f, fmul(a, a)));
+  }
+}
+
+// Backward through time, warp per (row, dir), lane = unit. Serial part only:
+// the gate gradients and the dh recurrence; the weight gradients and dx are
+// reductions over the stored per-step values afterwards.
+__global__ void __launch_bounds__(256) k_sprm_bptt(SprmP s, const float* __restrict__ tape,
+                                                   const float* __restrict__ dfin, float* Gr,
+                                                   float* HP) {
+  __shared__ __align__(16) float sg[8][3][32];  // dhh, dar, daz of this step
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = blockIdx.x * 8 + wl;
+  if (g >= s.R * 2) return;
+  const int r = g >> 1, d = g & 1, T = s.T, H = s.H, R = s.R;
+  const int64_t RT = int64_t(R) * T;
+  const float* W = s.w;
+  const bool act = lane < H;
+  const int j = act ? lane : 0;
+  const float* whr = W + goff(s.offs, d, WHR);
+  const float* whz = W + goff(s.offs, d, WHZ);
+  const float* whn = W + goff(s.offs, d, WHN);
+  const int64_t TRH = int64_t(T) * R * H;
+  const float* tr = tape + (int64_t(0 * 2 + d) * TRH);
+  const float* tz = tape + (int64_t(1 * 2 + d) * TRH);
+  const float* tn = tape + (int64_t(2 * 2 + d) * TRH);
+  const float* th = tape + (int64_t(3 * 2 + d) * TRH);
+  const float* to = tape + (int64_t(4 * 2 + d) * TRH);
+  // G[gate][d][j][k] (gate: 0 an, 1 ar, 2 az, 3 hh), HP[d][q][k]
+  float* gan = Gr + (int64_t(0 * 2 + d) * H) * RT;
+  float* gar = Gr + (int64_t(1 * 2 + d) * H) * RT;
+  float* gaz = Gr + (int64_t(2 * 2 + d) * H) * RT;
+  float* ghh = Gr + (int64_t(3 * 2 + d) * H) * RT;
+  float* hp = HP + int64_t(d) * H * RT;
+  // dcur: only the GRU's last own step receives the final-state gradient
+  // (final_state_backward, layers.cpp:401-413), through 0 + dfin
+  const float dlast = fadd(0.0f, dfin[int64_t(r) * 2 * H + d * H + j]);
+  float dh = 0.0f;
+  for (int t = T - 1; t >= 0; --t) {
+    dh = fadd(dh, t == T - 1 ? dlast : 0.0f);  // gather_add_step(dout, t, dh)
+    const int64_t o = (int64_t(t) * R + r) * H + j;
+    const float rv = tr[o], zv = tz[o], nv = tn[o], hhv = th[o];
+    const float hprev = t == 0 ? 0.0f : to[o - int64_t(R) * H];
+    const float dzv = fmul(dh, fsub(hprev, nv));
+    const float danv = fmul(fmul(dh, fsub(1.0f, zv)), fsub(1.0f, fmul(nv, nv)));
+    const float dar = fmul(fmul(fmul(danv, hhv), rv), fsub(1.0f, rv));
+    const float daz = fmul(fmul(dzv, zv), fsub(1.0f, zv));
+    const float dhh = fmul(danv, rv);
+    float dn = fmul(dh, zv);
+    const int64_t k = int64_t(T - 1 - t) * R + r;
+    if (act) {
+      gan[int64_t(j) * RT + k] = danv;
+      gar[int64_t(j) * RT + k] = dar;
+      gaz[int64_t(j) * RT + k] = daz;
+      ghh[int64_t(j) * RT + k] = dhh;
+      hp[int64_t(j) * RT + k] = hprev;
+      sg[wl][0][j] = dhh;
+      sg[wl][1][j] = dar;
+      sg[wl][2][j] = daz;
+    }
+    __syncwarp();
+    // dh_next = dh*z + dhh.W_hn^T + dar.W_hr^T + daz.W_hz^T  (layers.cpp:306-308)
+    const float* rn = whn + int64_t(j) * H;
+    const float* rr = whr + int64_t(j) * H;
+    const float* rz = whz + int64_t(j) * H;
+    for (int q = 0; q < H; ++q) dn = mac(dn, sg[wl][0][q], rn[q]);
+    for (int q = 0; q < H; ++q) dn = mac(dn, sg[wl][1][q], rr[q]);
+    for (int q = 0; q < H; ++q) dn = mac(dn, sg[wl][2][q], rz[q]);
+    __syncwarp();
+    dh = dn;
+  }
+}
+
+// dx[r][t][i] = (0 + dxt_fwd(t)) + (0 + dxt_bwd(T-1-t)),
+// dxt(t) = 0 + dan.W_in^T + dar.W_ir^T + daz.W_iz^T   (layers.cpp:300-304, 384-386)
+__global__ void k_sprm_dx(SprmP s, const float* __restrict__ Gr, float* dx) {
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int R = s.R, T = s.T, Es = s.Es, H = s.H;
+  const int64_t RT = int64_t(R) * T;
+  if (idx >= RT * Es) return;
+  const int i = int(idx % Es);
+  const int64_t rt = idx / Es;
+  const int r = int(rt / T), t = int(rt % T);
+  const float* W = s.w;
+  float part[2];
+  for (int d = 0; d < 2; ++d) {
+    const int own_t = d ? (T - 1 - t) : t;
+    const int64_t k = int64_t(T - 1 - own_t) * R + r;
+    float acc = 0.0f;
+    const int gates[3] = {WIN, WIR, WIZ};
+    const int gsel[3] = {0, 1, 2};
+    for (int u = 0; u < 3; ++u) {
+      const float* gg = Gr + (int64_t(gsel[u] * 2 + d) * H) * RT;
+      const float* Wg = W + goff(s.offs, d, gates[u]) + int64_t(i) * H;
+      for (int q = 0; q < H; ++q) acc = mac(acc, gg[int64_t(q) * RT + k], Wg[q]);
+    }
+    part[d] = acc;
+  }
+  dx[idx] = fadd(fadd(0.0f, part[0]), fadd(0.0f, part[1]));  // dx += dx_rev (both from zero)
+}
+
+// emb grad: grad[tok][j] += dx[r][t][j], (r,t) row-major order (layers.cpp:117-125)
+__global__ void k_sprm_emb_grad(SprmP s, const uint32_t* __restrict__ ctx,
+                                const float* __restrict__ dx, float* grad_emb) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= s.V * s.Es) return;
+  const uint32_t tok = uint32_t(idx / s.Es);
+  const int j = idx % s.Es;
+  float acc = grad_emb[idx];
+  const int64_t RT = int64_t(s.R) * s.T;
+  for (int64_t p = 0; p < RT; ++p)
+    if (ctx[p] == tok) acc = fadd(acc, dx[p * s.Es + j]);
+  grad_emb[idx] = acc;
+}
+
+__global__ void k_tanh_vec(float* x, int64_t n) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = det_tanh(x[i]);
+}
+
+__global__ void k_adam_scalars(AdamScalars* sc) {
+  AdamScalars a = *sc;
+  a.step += 1;
+  a.b1p = fmul(a.b1p, 0.9f);
+  a.b2p = fmul(a.b2p, 0.999f);
+  a.bc1 = fsub(1.0f, a.b1p);
+  a.bc2 = fsub(1.0f, a.b2p);
+  *sc = a;
+}
+
+__global__ void k_pos_advance(int64_t* pos, int64_t by) { *pos += by; }
+
+}  // namespace
+
+void launch_sprm_prep(const uint32_t* tokens, const int64_t* pos, const SprmP& s, uint32_t* ctx,
+                      float* X, float* tab, cudaStream_t st) {
+  const int64_t n = std::max<int64_t>(std::max<int64_t>(int64_t(s.R) * s.T, 6ll * s.V * s.H),
+                                      2ll * s.Es * s.R * s.T);
+  k_sprm_prep<<<unsigned((n + 255) / 256), 256, 0, st>>>(tokens, pos, s, ctx, X, tab);
+}
+void launch_sprm_fwd(const SprmP& s, const uint32_t* ctx, const float* tab, float* tape, float* fin,
+                     cudaStream_t st) {
+  k_sprm_fwd<<<unsigned((s.R * 2 + 7) / 8), 256, 0, st>>>(s, ctx, tab, tape, fin);
+}
+void launch_sprm_ce(const SprmP& s, const uint32_t* tokens, const int64_t* pos, const float* logits,
+                    float* g, cudaStream_t st) {
+  k_sprm_ce<<<unsigned((s.R * 32 + 255) / 256), 256, 0, st>>>(s, tokens, pos, logits, g);
+}
+void launch_sprm_tanh_grad(float* dbact, const float* bact, int64_t n, cudaStream_t st) {
+  k_sprm_tanh_grad<<<unsigned((n + 255) / 256), 256, 0, st>>>(dbact, bact, n);
+}
+void launch_sprm_bptt(const SprmP& s, const float* tape, const float* dfin, float* G, float* HP,
+                      cudaStream_t st) {
+  k_sprm_bptt<<<unsigned((s.R * 2 + 7) / 8), 256, 0, st>>>(s, tape, dfin, G, HP);
+}
+void launch_sprm_dx(const SprmP& s, const float* G, float* dx, cudaStream_t st) {
+  const int64_t n = int64_t(s.R) * s.T * s.Es;
+  k_sprm_dx<<<unsigned((n + 255) / 256), 256, 0, st>>>(s, G, dx);
+}
+void launch_sprm_emb_grad(const SprmP& s, const uint32_t* ctx, const float* dx, float* grad_emb,
+                          cudaStream_t st) {
+  k_sprm_emb_grad<<<unsigned((s.V * s.Es + 127) / 128), 128, 0, st>>>(s, ctx, dx, grad_emb);
+}
+void launch_tanh_vec(float* x, int64_t n, cudaStream_t st) {
+  k_tanh_vec<<<unsigned((n + 255) / 256), 256, 0, st>>>(x, n);
+}
+void launch_adam_scalars(AdamScalars* sc, cudaStream_t st) { k_adam_scalars<<<1, 1, 0, st>>>(sc); }
+void launch_pos_advance(int64_t* pos, int64_t by, cudaStream_t st) {
+  k_pos_advance<<<1, 1, 0, st>>>(pos, by);
+}
+
+}  // namespace pmklc_b200

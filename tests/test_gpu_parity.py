@@ -271,3 +271,33 @@ def test_dist_context_single_rank(P, checker):
     finally:
         ctx.close()
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("with_pub", [False, True])
+def test_sprm_prepass_branch(P, checker, spum_k3, with_pub):
+    # input above the selector threshold -> private model trained inside compress
+    # (pretrain_private, training.cpp:62-83); the container carries its PMKW bytes,
+    # so byte identity pins the whole training pass
+    raw = P.synth("markov3", 40000, 61) + b"NNacgt>\n"
+    kw = dict(t=8, bs=64, scale=16, workers=2, threshold=0)
+    if with_pub:
+        kw["pub_path"] = spum_k3  # derive_private_init: emb + gru0 copied from the SPuM
+    ckw = dict(kw)
+    thr = ckw.pop("threshold")
+    cfg = P.CompressConfig(**_cfgs(ckw), selector_threshold=thr)
+    blob = P.compress(raw, cfg)
+    want = checker.compress(raw, O.make_cfg(**kw))
+    assert blob[5] == 6 and want[5] == 6
+    assert blob == want
+    assert P.decompress(blob, spum_k3 if with_pub else "") == raw
+    assert checker.decompress(blob, pub_path=spum_k3 if with_pub else None) == raw
+
+
+def test_sprm_prepass_default_widths(P, checker):
+    # scale 4, t = 32, bs = 320: the widths of BASELINE configs 4/5
+    raw = P.synth("markov3", 150000, 62)
+    kw = dict(workers=2, threshold=0)
+    cfg = P.CompressConfig(workers=2, selector_threshold=0)
+    blob = P.compress(raw, cfg)
+    assert blob == checker.compress(raw, O.make_cfg(**kw))
+    assert P.decompress(blob) == raw
