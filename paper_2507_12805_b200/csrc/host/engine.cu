@@ -758,8 +758,8 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
   const int64_t R = batch, RT = R * T;
   DBuf<uint32_t> ctx(RT);
   DBuf<float> X(2 * Es * RT), tab(6 * int64_t(V) * H), tape(10 * RT * H), fin(R * 2 * H),
-      bact(R * B), logits(R * V), gg(R * V), dbact(R * B), dfin(R * 2 * H), G(8 * H * RT),
-      HP(2 * H * RT), dx(RT * Es);
+      bact(R * B), logits(R * V), gg(R * V), dbact(R * B), dfin(R * 2 * H), G(10 * H * RT),
+      Gt(10 * H * RT), dx(RT * Es);
   DBuf<int64_t> pos(1);
   const int64_t p0 = t;
   pos.upload(&p0, 1, st);
@@ -807,14 +807,15 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
     g6.M = rows; g6.N = 2 * H; g6.K = B; g6.init = 0;
     launch_gemm(g6, false, true, td.p, 1, st);
     // backward through time, then the weight-gradient reductions over (t desc, rows asc)
-    launch_sprm_bptt(sp, tape.p, dfin.p, G.p, HP.p, st);
+    launch_sprm_bptt(sp, tape.p, dfin.p, Gt.p, G.p, st);
+    NtP probs[12];
     for (int d = 0; d < 2; ++d) {
       const float* Gan = G.p + (int64_t(0 * 2 + d) * H) * rt;
       const float* Gar = G.p + (int64_t(1 * 2 + d) * H) * rt;
       const float* Gaz = G.p + (int64_t(2 * 2 + d) * H) * rt;
       const float* Ghh = G.p + (int64_t(3 * 2 + d) * H) * rt;
       const float* Xd = X.p + int64_t(d) * Es * rt;
-      const float* Hd = HP.p + int64_t(d) * H * rt;
+      const float* Hd = G.p + (int64_t(4 * 2 + d) * H) * rt;
       auto idx = [&](int gt) { return model.idx(0, d, gt); };
       auto nt = [&](const float* A, int M, const float* Bm, int wg, int bg) {
         return NtP{A, Bm, G_(idx(wg)), 0, 0, 0, rt, rt, H, M, H, int(rt), G_(idx(bg))};
@@ -822,16 +823,17 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
       const NtP a1 = nt(Xd, Es, Gan, BiGru::WIN, BiGru::BIN), a2 = nt(Xd, Es, Gar, BiGru::WIR, BiGru::BIR);
       const NtP a3 = nt(Xd, Es, Gaz, BiGru::WIZ, BiGru::BIZ), a4 = nt(Hd, H, Ghh, BiGru::WHN, BiGru::BHN);
       const NtP a5 = nt(Hd, H, Gar, BiGru::WHR, BiGru::BHR), a6 = nt(Hd, H, Gaz, BiGru::WHZ, BiGru::BHZ);
-      launch_gemm_nt(a1, &a2, td.p, 1, st);
-      launch_gemm_nt(a3, &a4, td.p, 1, st);
-      launch_gemm_nt(a5, &a6, td.p, 1, st);
+      const NtP six[6] = {a1, a2, a3, a4, a5, a6};
+      for (int u = 0; u < 6; ++u) probs[d * 6 + u] = six[u];
     }
+    launch_gemm_nt_batch(probs, 12, td.p, 1, st);
     launch_sprm_dx(sp, G.p, dx.p, st);
-    launch_sprm_emb_grad(sp, ctx.p, dx.p, g.p + hoffs[0], st);
+    const DmDims ed{rows, T, Es, H, 0, V, 0};
+    launch_emb_grad(ctx.p, 0, dx.p, 0, g.p, 0, int64_t(hoffs[0]), ed, td.p, 1, st);
     launch_adam_scalars(sc.p, st);
     launch_adam(w.p, g.p, mo.p, vo.p, 0, P, sc.p, td.p, 1, st);
     launch_pos_advance(pos.p, batch, st);
-    nl += 22;
+    nl += 19;
   };
   const uint64_t nsteps = (m - t + batch - 1) / batch;
   const uint64_t full = (m - t) / batch;
@@ -843,7 +845,7 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
     CK(cudaStreamEndCapture(st, &graph));
     CK(cudaGraphInstantiate(&exec, graph, 0));
     for (uint64_t i = 0; i < full; ++i) CK(cudaGraphLaunch(exec, st));
-    nl += 22 * (full - 1);
+    nl += 19 * (full - 1);
     CK(cudaGraphExecDestroy(exec));
     CK(cudaGraphDestroy(graph));
   }

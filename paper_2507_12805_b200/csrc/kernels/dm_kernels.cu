@@ -212,25 +212,30 @@ __host__ __device__ constexpr size_t nt_smem(int mr) {
   return size_t(kNtStages) * (size_t(mr) * kNtBK + size_t(kNtCols) * kNtSB) * sizeof(float);
 }
 
+struct NtBatch {
+  NtP p[kNtMaxProb];
+  int first_block[kNtMaxProb + 1];  // prefix of row blocks per problem
+  int n;
+};
+
 // VEC: rows 16-byte aligned, K multiple of 4 (host-checked); else 4-byte copies.
 template <bool VEC, int MR>
-__global__ void __launch_bounds__(kNtCols * MR) k_gemm_nt(NtP p0, NtP p1, const TickDesc* __restrict__ td) {
+__global__ void __launch_bounds__(kNtCols * MR) k_gemm_nt(NtBatch nb, const TickDesc* __restrict__ td) {
   extern __shared__ __align__(128) float sm[];
   constexpr int NT = kNtCols * MR;
   if (blockIdx.z >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.z];
-  const int nb0 = (p0.M + 1 + MR - 1) / MR;  // row blocks of problem 0 (incl. bias row)
-  int mb = blockIdx.y;
-  const bool second = mb >= nb0;
-  if (second) mb -= nb0;
-  const float* Ab = second ? p1.A : p0.A;
-  const float* Bb = second ? p1.B : p0.B;
-  float* Cb = second ? p1.C : p0.C;
-  float* CBb = second ? p1.cb : p0.cb;
-  const int64_t a_cs = second ? p1.a_cs : p0.a_cs, b_cs = second ? p1.b_cs : p0.b_cs,
-                c_cs = second ? p1.c_cs : p0.c_cs, lda = second ? p1.lda : p0.lda,
-                ldb = second ? p1.ldb : p0.ldb, ldc = second ? p1.ldc : p0.ldc;
-  const int M = second ? p1.M : p0.M, N = second ? p1.N : p0.N, K = second ? p1.K : p0.K;
+  int prob = 0;
+  while (prob + 1 < nb.n && int(blockIdx.y) >= nb.first_block[prob + 1]) ++prob;
+  const NtP& pp = nb.p[prob];
+  const int mb = int(blockIdx.y) - nb.first_block[prob];
+  const float* Ab = pp.A;
+  const float* Bb = pp.B;
+  float* Cb = pp.C;
+  float* CBb = pp.cb;
+  const int64_t a_cs = pp.a_cs, b_cs = pp.b_cs, c_cs = pp.c_cs, lda = pp.lda, ldb = pp.ldb,
+                ldc = pp.ldc;
+  const int M = pp.M, N = pp.N, K = pp.K;
   const int m0 = mb * MR;
   if (m0 > M) return;
   const int n0 = blockIdx.x * kNtCols;
@@ -661,7 +666,7 @@ __global__ void __launch_bounds__(kEmbWarps * 32) k_emb_bwd(
   const int tokv = blockIdx.x * kEmbWarps + wl;
   const uint32_t* cp = ctx + c * ctx_cs;
   const float* xp = dx + c * dx_cs;
-  const float* lp = dxl + c * dxl_cs;
+  const float* lp = dxl ? dxl + c * dxl_cs : nullptr;
   const bool active_warp = tokv < d.V;
   float* g = grads + c * g_cs + off_emb + int64_t(active_warp ? tokv : 0) * d.E;
   constexpr int kMaxJ = 2;  // E = 64/scale <= 64
@@ -704,11 +709,11 @@ __global__ void __launch_bounds__(kEmbWarps * 32) k_emb_bwd(
           const int64_t pp = s0 + hits[wl][h0 + (b < cnt ? b : 0)];
           lastp[b] = int(pp % d.T) == d.T - 1;
           v[b] = __ldg(xp + pp * d.E + jj);
-          l[b] = __ldg(lp + (pp / d.T) * d.E + jj);
+          l[b] = dxl ? __ldg(lp + (pp / d.T) * d.E + jj) : 0.0f;
         }
 #pragma unroll
         for (int b = 0; b < kB; ++b) {
-          const float x = lastp[b] ? fadd(v[b], l[b]) : v[b];  // dx[:,last,:] += dxl
+          const float x = (dxl && lastp[b]) ? fadd(v[b], l[b]) : v[b];  // dx[:,last,:] += dxl
           if (b < cnt && jv) acc[q] = fadd(acc[q], x);
         }
       }
@@ -720,6 +725,91 @@ __global__ void __launch_bounds__(kEmbWarps * 32) k_emb_bwd(
   for (int q = 0; q < kMaxJ; ++q) {
     const int j = lane + 32 * q;
     if (q < nj && j < d.E) g[j] = acc[q];
+  }
+}
+
+// Sort-based embedding gradient (the default when a chunk's R*t positions and
+// the vocabulary fit in shared memory): stable counting sort of the positions
+// by token (histogram, scan, warp match-any ranks keep (r,t) order), then one
+// thread per (token, column) walks its contiguous list in order with 16 loads
+// in flight. Same per-element order as Embedding::backward (layers.cpp:117-125).
+constexpr int kSortThreads = 1024;
+constexpr int kSortMaxPos = 10240;
+constexpr int kSortMaxV = 256;
+__global__ void __launch_bounds__(kSortThreads) k_emb_bwd_sorted(
+    const uint32_t* __restrict__ ctx, int64_t ctx_cs, const float* __restrict__ dx, int64_t dx_cs,
+    const float* __restrict__ dxl, int64_t dxl_cs, float* grads, int64_t g_cs, int64_t off_emb,
+    DmDims d, const TickDesc* __restrict__ td) {
+  __shared__ uint16_t sorted[kSortMaxPos];
+  __shared__ int cnt[kSortMaxV], off[kSortMaxV + 1], run[kSortMaxV];
+  __shared__ uint16_t wc[32][kSortMaxV];  // per-warp counts of each token in the current slab
+  if (blockIdx.x >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.x];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int V = d.V, RT = d.R * d.T;
+  const uint32_t* cp = ctx + c * ctx_cs;
+  for (int v = tid; v < V; v += kSortThreads) {
+    cnt[v] = 0;
+    run[v] = 0;
+  }
+  __syncthreads();
+  for (int p = tid; p < RT; p += kSortThreads) atomicAdd(&cnt[cp[p]], 1);
+  __syncthreads();
+  if (tid == 0) {
+    int a = 0;
+    for (int v = 0; v < V; ++v) {
+      off[v] = a;
+      a += cnt[v];
+    }
+    off[V] = a;
+  }
+  __syncthreads();
+  for (int base = 0; base < RT; base += kSortThreads) {
+    for (int i = tid; i < 32 * V; i += kSortThreads) wc[i / V][i % V] = 0;
+    __syncthreads();
+    const int p = base + tid;
+    const bool ok = p < RT;
+    const uint32_t v = ok ? cp[p] : 0xffffffffu;
+    const unsigned mask = __match_any_sync(0xffffffffu, v);
+    const int rank_w = __popc(mask & ((1u << lane) - 1u));
+    if (ok && rank_w == 0) wc[w][v] = uint16_t(__popc(mask));
+    __syncthreads();
+    if (ok) {
+      int before = 0;
+      for (int ww = 0; ww < w; ++ww) before += wc[ww][v];
+      sorted[off[v] + run[v] + before + rank_w] = uint16_t(p);
+    }
+    __syncthreads();
+    for (int vv = tid; vv < V; vv += kSortThreads) {
+      int tot = 0;
+      for (int ww = 0; ww < 32; ++ww) tot += wc[ww][vv];
+      run[vv] += tot;
+    }
+    __syncthreads();
+  }
+  const float* xp = dx + c * dx_cs;
+  const float* lp = dxl ? dxl + c * dxl_cs : nullptr;
+  for (int o = tid; o < V * d.E; o += kSortThreads) {
+    const int v = o / d.E, j = o % d.E;
+    float* g = grads + c * g_cs + off_emb + o;
+    float acc = *g;
+    const int b0 = off[v], b1 = off[v + 1];
+    constexpr int kB = 16;
+    for (int h0 = b0; h0 < b1; h0 += kB) {
+      float x[kB];
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        const int h = h0 + b < b1 ? h0 + b : b0;
+        const int pp = sorted[h];
+        float val = __ldg(xp + int64_t(pp) * d.E + j);
+        if (lp && pp % d.T == d.T - 1) val = fadd(val, __ldg(lp + int64_t(pp / d.T) * d.E + j));
+        x[b] = val;
+      }
+#pragma unroll
+      for (int b = 0; b < kB; ++b)
+        if (h0 + b < b1) acc = fadd(acc, x[b]);
+    }
+    *g = acc;
   }
 }
 
@@ -789,16 +879,18 @@ void launch_gemm(const GemmP& p, bool at, bool bt, const TickDesc* td, int max_a
   else gemm_dispatch<false, false>(p, td, max_active, st);
 }
 
-void launch_gemm_nt(const NtP& p0, const NtP* p1, const TickDesc* td, int max_active,
-                    cudaStream_t st) {
-  if (max_active <= 0 || p0.N <= 0) return;
-  const NtP q1 = p1 ? *p1 : p0;
+void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int max_active,
+                          cudaStream_t st) {
+  if (max_active <= 0 || nprob <= 0) return;
   auto al = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
-  auto vec_ok = [&](const NtP& p) {  // 16-byte rows for cp.async.cg 16
-    return p.K % 4 == 0 && p.lda % 4 == 0 && p.ldb % 4 == 0 && p.a_cs % 4 == 0 &&
-           p.b_cs % 4 == 0 && al(p.A) && al(p.B);
-  };
-  const bool vec = vec_ok(p0) && vec_ok(q1);
+  bool vec = true;
+  int maxn = 0;
+  for (int i = 0; i < nprob; ++i) {
+    const NtP& p = probs[i];
+    vec = vec && p.K % 4 == 0 && p.lda % 4 == 0 && p.ldb % 4 == 0 && p.a_cs % 4 == 0 &&
+          p.b_cs % 4 == 0 && al(p.A) && al(p.B);
+    maxn = std::max(maxn, p.N);
+  }
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k_gemm_nt<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(nt_smem(1)));
@@ -807,18 +899,35 @@ void launch_gemm_nt(const NtP& p0, const NtP* p1, const TickDesc* td, int max_ac
     cudaFuncSetAttribute(k_gemm_nt<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(nt_smem(4)));
     attr_set = true;
   }
-  const int nx = (std::max(p0.N, q1.N) + kNtCols - 1) / kNtCols;
-  auto rows = [&](int mr) { return (p0.M + 1 + mr - 1) / mr + (p1 ? (p1->M + 1 + mr - 1) / mr : 0); };
+  const int nx = (maxn + kNtCols - 1) / kNtCols;
+  auto build = [&](int mr, NtBatch& nb) {
+    nb.n = nprob;
+    nb.first_block[0] = 0;
+    for (int i = 0; i < nprob; ++i) {
+      nb.p[i] = probs[i];
+      nb.first_block[i + 1] = nb.first_block[i] + (probs[i].M + 1 + mr - 1) / mr;
+    }
+    return nb.first_block[nprob];
+  };
+  NtBatch nb;
+  const int rows1 = build(1, nb);
   // one-row blocks while the launch cannot fill the chip, else 4-row blocks
-  if (int64_t(nx) * rows(1) * max_active < 2 * 148) {
-    dim3 grid(nx, rows(1), max_active);
-    if (vec) k_gemm_nt<true, 1><<<grid, kNtCols, nt_smem(1), st>>>(p0, q1, td);
-    else k_gemm_nt<false, 1><<<grid, kNtCols, nt_smem(1), st>>>(p0, q1, td);
+  if (int64_t(nx) * rows1 * max_active < 2 * 148) {
+    dim3 grid(nx, rows1, max_active);
+    if (vec) k_gemm_nt<true, 1><<<grid, kNtCols, nt_smem(1), st>>>(nb, td);
+    else k_gemm_nt<false, 1><<<grid, kNtCols, nt_smem(1), st>>>(nb, td);
   } else {
-    dim3 grid(nx, rows(4), max_active);
-    if (vec) k_gemm_nt<true, 4><<<grid, kNtCols * 4, nt_smem(4), st>>>(p0, q1, td);
-    else k_gemm_nt<false, 4><<<grid, kNtCols * 4, nt_smem(4), st>>>(p0, q1, td);
+    const int rows4 = build(4, nb);
+    dim3 grid(nx, rows4, max_active);
+    if (vec) k_gemm_nt<true, 4><<<grid, kNtCols * 4, nt_smem(4), st>>>(nb, td);
+    else k_gemm_nt<false, 4><<<grid, kNtCols * 4, nt_smem(4), st>>>(nb, td);
   }
+}
+
+void launch_gemm_nt(const NtP& p0, const NtP* p1, const TickDesc* td, int max_active,
+                    cudaStream_t st) {
+  NtP ps[2] = {p0, p1 ? *p1 : p0};
+  launch_gemm_nt_batch(ps, p1 ? 2 : 1, td, max_active, st);
 }
 
 void launch_embed(const uint32_t* tokens, ChunkGeo geo, const float* params,
@@ -872,6 +981,20 @@ void launch_attn_bwd(const float* q, const float* k, const float* v, const float
   dim3 grid(unsigned((warps * 32 + 255) / 256), max_active);
   k_attn_bwd<<<grid, 256, 0, st>>>(q, k, v, wts, dctx, dq, dk, dv, cs_q, cs_kv, cs_w, d, inv,
                                    td);
+}
+
+void launch_emb_grad(const uint32_t* ctx, int64_t ctx_cs, const float* dx, int64_t dx_cs,
+                     float* grads, int64_t g_cs, int64_t off_emb, DmDims d, const TickDesc* td,
+                     int max_active, cudaStream_t st) {
+  if (max_active <= 0) return;
+  if (d.R * d.T <= kSortMaxPos && d.V <= kSortMaxV) {
+    k_emb_bwd_sorted<<<max_active, kSortThreads, 0, st>>>(ctx, ctx_cs, dx, dx_cs, nullptr, 0, grads,
+                                                         g_cs, off_emb, d, td);
+    return;
+  }
+  dim3 g2(unsigned((d.V + kEmbWarps - 1) / kEmbWarps), max_active);
+  k_emb_bwd<<<g2, kEmbWarps * 32, 0, st>>>(ctx, ctx_cs, dx, dx_cs, nullptr, 0, grads, g_cs, off_emb,
+                                           d, td);
 }
 
 void launch_embed_bwd(const uint32_t* ctx, int64_t ctx_cs, const float* dx, int64_t dx_cs,

@@ -90,6 +90,10 @@ struct NtP {
 };
 void launch_gemm_nt(const NtP& p0, const NtP* p1, const TickDesc* td, int max_active,
                     cudaStream_t st);
+// up to kNtMaxProb independent problems in one launch (all run concurrently)
+constexpr int kNtMaxProb = 12;
+void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int max_active,
+                          cudaStream_t st);
 
 struct DmDims { int R, T, E, H, F, V, NH; };
 
@@ -112,6 +116,11 @@ void launch_embed_bwd(const uint32_t* ctx, int64_t ctx_cs, const float* dx, int6
                       const float* dxl, int64_t dxl_cs, float* grads, int64_t g_cs,
                       int64_t off_emb, int64_t off_pos, DmDims d, const TickDesc* td, int max_active,
                       cudaStream_t st);
+
+// Embedding::backward alone (no positional / last-position term), any model
+void launch_emb_grad(const uint32_t* ctx, int64_t ctx_cs, const float* dx, int64_t dx_cs,
+                     float* grads, int64_t g_cs, int64_t off_emb, DmDims d, const TickDesc* td,
+                     int max_active, cudaStream_t st);
 
 struct AdamScalars {   // per chunk
   uint64_t step;
@@ -202,7 +211,8 @@ void launch_sprm_fwd(const SprmP& s, const uint32_t* ctx, const float* tab, floa
 void launch_sprm_ce(const SprmP& s, const uint32_t* tokens, const int64_t* pos, const float* logits,
                     float* g, cudaStream_t st);
 void launch_sprm_tanh_grad(float* dbact, const float* bact, int64_t n, cudaStream_t st);
-void launch_sprm_bptt(const SprmP& s, const float* tape, const float* dfin, float* G, float* HP,
+// BPTT + transpose: G = [5 (an, ar, az, hh, hprev)][2][Hs][R*T] feature-major
+void launch_sprm_bptt(const SprmP& s, const float* tape, const float* dfin, float* Gt, float* G,
                       cudaStream_t st);
 void launch_sprm_dx(const SprmP& s, const float* G, float* dx, cudaStream_t st);
 void launch_sprm_emb_grad(const SprmP& s, const uint32_t* ctx, const float* dx, float* grad_emb,

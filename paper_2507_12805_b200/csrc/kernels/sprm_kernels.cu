@@ -67,16 +67,20 @@ __global__ void __launch_bounds__(256) k_sprm_fwd(SprmP s, const uint32_t* __res
                                                   const float* __restrict__ tab, float* tape,
                                                   float* fin) {
   __shared__ __align__(16) float sh[8][2][32];
+  __shared__ float sw[3][32][32];  // [gate][q][j] = W_h{r,z,n}[q][j]
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.x * 8 + wl;
-  if (g >= s.R * 2) return;
-  const int r = g >> 1, d = g & 1, T = s.T, H = s.H, R = s.R, V = s.V;
+  const int d = blockIdx.x & 1;
+  const int r = (blockIdx.x >> 1) * 8 + wl;
+  const int T = s.T, H = s.H, R = s.R, V = s.V;
   const float* W = s.w;
+  for (int i = threadIdx.x; i < 3 * H * H; i += blockDim.x) {
+    const int gate = i / (H * H), rem = i % (H * H);
+    sw[gate][rem / H][rem % H] = W[goff(s.offs, d, WHR + gate) + rem];
+  }
+  __syncthreads();
+  if (r >= R) return;
   const bool act = lane < H;
   const int j = act ? lane : 0;
-  const float* whr = W + goff(s.offs, d, WHR);
-  const float* whz = W + goff(s.offs, d, WHZ);
-  const float* whn = W + goff(s.offs, d, WHN);
   const float bhr = W[goff(s.offs, d, BHR) + j], bhz = W[goff(s.offs, d, BHZ) + j],
               bhn = W[goff(s.offs, d, BHN) + j];
   const float* t0 = tab + int64_t(d) * 3 * V * H;
@@ -94,11 +98,11 @@ __global__ void __launch_bounds__(256) k_sprm_fwd(SprmP s, const uint32_t* __res
     const int64_t tok = ctx[int64_t(r) * T + src_t];
     const float* h = sh[wl][cur];
     float ar = fadd(t0[tok * H + j], bhr);
-    for (int q = 0; q < H; ++q) ar = mac(ar, h[q], whr[int64_t(q) * H + j]);
+    for (int q = 0; q < H; ++q) ar = mac(ar, h[q], sw[0][q][j]);
     float az = fadd(t0[int64_t(V) * H + tok * H + j], bhz);
-    for (int q = 0; q < H; ++q) az = mac(az, h[q], whz[int64_t(q) * H + j]);
+    for (int q = 0; q < H; ++q) az = mac(az, h[q], sw[1][q][j]);
     float hh = bhn;
-    for (int q = 0; q < H; ++q) hh = mac(hh, h[q], whn[int64_t(q) * H + j]);
+    for (int q = 0; q < H; ++q) hh = mac(hh, h[q], sw[2][q][j]);
     const float an = t0[2 * int64_t(V) * H + tok * H + j];
     const float rv = det_sigmoid(ar), zv = det_sigmoid(az);
     const float nv = det_tanh(fadd(an, fmul(rv, hh)));
@@ -160,38 +164,42 @@ __global__ void k_sprm_tanh_grad(float* dbact, const float* __restrict__ bact, i
   }
 }
 
-// Backward through time, warp per (row, dir), lane = unit. Serial part only:
-// the gate gradients and the dh recurrence; the weight gradients and dx are
-// reductions over the stored per-step values afterwards.
+// Backward through time. Blocks are single-direction (8 warps = 8 rows, lane =
+// unit); the direction's W_h* are staged transposed in shared memory so the
+// dh recurrence reads conflict-free. Serial part only: the gate gradients and
+// h_{t-1} are stored row-major Gt[5][2][T][R][H] (an, ar, az, hh, hprev) and
+// transposed afterwards into the feature-major reduction operands.
 __global__ void __launch_bounds__(256) k_sprm_bptt(SprmP s, const float* __restrict__ tape,
-                                                   const float* __restrict__ dfin, float* Gr,
-                                                   float* HP) {
+                                                   const float* __restrict__ dfin, float* Gt) {
+  __shared__ float swt[3][32][33];              // [gate][q][j] = W_h{gate}[j][q]
   __shared__ __align__(16) float sg[8][3][32];  // dhh, dar, daz of this step
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = blockIdx.x * 8 + wl;
-  if (g >= s.R * 2) return;
-  const int r = g >> 1, d = g & 1, T = s.T, H = s.H, R = s.R;
-  const int64_t RT = int64_t(R) * T;
+  const int d = blockIdx.x & 1;
+  const int r = (blockIdx.x >> 1) * 8 + wl;
+  const int T = s.T, H = s.H, R = s.R;
   const float* W = s.w;
+  for (int i = threadIdx.x; i < 3 * H * H; i += blockDim.x) {
+    const int gate = i / (H * H), rem = i % (H * H), jj = rem / H, q = rem % H;
+    const float* Wg = W + goff(s.offs, d, gate == 0 ? WHN : gate == 1 ? WHR : WHZ);
+    swt[gate][q][jj] = Wg[int64_t(jj) * H + q];
+  }
+  __syncthreads();
+  if (r >= R) return;
   const bool act = lane < H;
   const int j = act ? lane : 0;
-  const float* whr = W + goff(s.offs, d, WHR);
-  const float* whz = W + goff(s.offs, d, WHZ);
-  const float* whn = W + goff(s.offs, d, WHN);
   const int64_t TRH = int64_t(T) * R * H;
   const float* tr = tape + (int64_t(0 * 2 + d) * TRH);
   const float* tz = tape + (int64_t(1 * 2 + d) * TRH);
   const float* tn = tape + (int64_t(2 * 2 + d) * TRH);
   const float* th = tape + (int64_t(3 * 2 + d) * TRH);
   const float* to = tape + (int64_t(4 * 2 + d) * TRH);
-  // G[gate][d][j][k] (gate: 0 an, 1 ar, 2 az, 3 hh), HP[d][q][k]
-  float* gan = Gr + (int64_t(0 * 2 + d) * H) * RT;
-  float* gar = Gr + (int64_t(1 * 2 + d) * H) * RT;
-  float* gaz = Gr + (int64_t(2 * 2 + d) * H) * RT;
-  float* ghh = Gr + (int64_t(3 * 2 + d) * H) * RT;
-  float* hp = HP + int64_t(d) * H * RT;
-  // dcur: only the GRU's last own step receives the final-state gradient
-  // (final_state_backward, layers.cpp:401-413), through 0 + dfin
+  float* gan = Gt + int64_t(0 * 2 + d) * TRH;
+  float* gar = Gt + int64_t(1 * 2 + d) * TRH;
+  float* gaz = Gt + int64_t(2 * 2 + d) * TRH;
+  float* ghh = Gt + int64_t(3 * 2 + d) * TRH;
+  float* ghp = Gt + int64_t(4 * 2 + d) * TRH;
+  // only the GRU's last own step receives the final-state gradient
+  // (final_state_backward, layers.cpp:401-413), as 0 + dfin
   const float dlast = fadd(0.0f, dfin[int64_t(r) * 2 * H + d * H + j]);
   float dh = 0.0f;
   for (int t = T - 1; t >= 0; --t) {
@@ -205,27 +213,49 @@ __global__ void __launch_bounds__(256) k_sprm_bptt(SprmP s, const float* __restr
     const float daz = fmul(fmul(dzv, zv), fsub(1.0f, zv));
     const float dhh = fmul(danv, rv);
     float dn = fmul(dh, zv);
-    const int64_t k = int64_t(T - 1 - t) * R + r;
     if (act) {
-      gan[int64_t(j) * RT + k] = danv;
-      gar[int64_t(j) * RT + k] = dar;
-      gaz[int64_t(j) * RT + k] = daz;
-      ghh[int64_t(j) * RT + k] = dhh;
-      hp[int64_t(j) * RT + k] = hprev;
+      gan[o] = danv;
+      gar[o] = dar;
+      gaz[o] = daz;
+      ghh[o] = dhh;
+      ghp[o] = hprev;
       sg[wl][0][j] = dhh;
       sg[wl][1][j] = dar;
       sg[wl][2][j] = daz;
     }
     __syncwarp();
     // dh_next = dh*z + dhh.W_hn^T + dar.W_hr^T + daz.W_hz^T  (layers.cpp:306-308)
-    const float* rn = whn + int64_t(j) * H;
-    const float* rr = whr + int64_t(j) * H;
-    const float* rz = whz + int64_t(j) * H;
-    for (int q = 0; q < H; ++q) dn = mac(dn, sg[wl][0][q], rn[q]);
-    for (int q = 0; q < H; ++q) dn = mac(dn, sg[wl][1][q], rr[q]);
-    for (int q = 0; q < H; ++q) dn = mac(dn, sg[wl][2][q], rz[q]);
+    for (int q = 0; q < H; ++q) dn = mac(dn, sg[wl][0][q], swt[0][q][j]);
+    for (int q = 0; q < H; ++q) dn = mac(dn, sg[wl][1][q], swt[1][q][j]);
+    for (int q = 0; q < H; ++q) dn = mac(dn, sg[wl][2][q], swt[2][q][j]);
     __syncwarp();
     dh = dn;
+  }
+}
+
+// Gt[g][d][t][r][j] -> G[g][d][j][k], k = (T-1-t)*R + r (32x32 smem tiles)
+__global__ void k_sprm_transpose(SprmP s, const float* __restrict__ Gt, float* G) {
+  __shared__ float tile[32][33];
+  const int T = s.T, H = s.H, R = s.R;
+  const int64_t RT = int64_t(R) * T;
+  const int gd = blockIdx.z;  // gate*2 + d
+  const int64_t k0 = int64_t(blockIdx.x) * 32;
+  const int j0 = blockIdx.y * 32;
+  const float* src = Gt + int64_t(gd) * RT * H;
+  float* dst = G + int64_t(gd) * H * RT;
+  for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
+    const int64_t k = k0 + yy;
+    const int j = j0 + threadIdx.x;
+    if (k < RT && j < H) {
+      const int t = int(T - 1 - k / R), r = int(k % R);
+      tile[yy][threadIdx.x] = src[(int64_t(t) * R + r) * H + j];
+    }
+  }
+  __syncthreads();
+  for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
+    const int j = j0 + yy;
+    const int64_t k = k0 + threadIdx.x;
+    if (k < RT && j < H) dst[int64_t(j) * RT + k] = tile[threadIdx.x][yy];
   }
 }
 
@@ -298,7 +328,7 @@ void launch_sprm_prep(const uint32_t* tokens, const int64_t* pos, const SprmP& s
 }
 void launch_sprm_fwd(const SprmP& s, const uint32_t* ctx, const float* tab, float* tape, float* fin,
                      cudaStream_t st) {
-  k_sprm_fwd<<<unsigned((s.R * 2 + 7) / 8), 256, 0, st>>>(s, ctx, tab, tape, fin);
+  k_sprm_fwd<<<unsigned(2 * ((s.R + 7) / 8)), 256, 0, st>>>(s, ctx, tab, tape, fin);
 }
 void launch_sprm_ce(const SprmP& s, const uint32_t* tokens, const int64_t* pos, const float* logits,
                     float* g, cudaStream_t st) {
@@ -307,9 +337,12 @@ void launch_sprm_ce(const SprmP& s, const uint32_t* tokens, const int64_t* pos, 
 void launch_sprm_tanh_grad(float* dbact, const float* bact, int64_t n, cudaStream_t st) {
   k_sprm_tanh_grad<<<unsigned((n + 255) / 256), 256, 0, st>>>(dbact, bact, n);
 }
-void launch_sprm_bptt(const SprmP& s, const float* tape, const float* dfin, float* G, float* HP,
+void launch_sprm_bptt(const SprmP& s, const float* tape, const float* dfin, float* Gt, float* G,
                       cudaStream_t st) {
-  k_sprm_bptt<<<unsigned((s.R * 2 + 7) / 8), 256, 0, st>>>(s, tape, dfin, G, HP);
+  k_sprm_bptt<<<unsigned(2 * ((s.R + 7) / 8)), 256, 0, st>>>(s, tape, dfin, Gt);
+  const int64_t RT = int64_t(s.R) * s.T;
+  dim3 grid(unsigned((RT + 31) / 32), unsigned((s.H + 31) / 32), 10);
+  k_sprm_transpose<<<grid, dim3(32, 8), 0, st>>>(s, Gt, G);
 }
 void launch_sprm_dx(const SprmP& s, const float* G, float* dx, cudaStream_t st) {
   const int64_t n = int64_t(s.R) * s.T * s.Es;
