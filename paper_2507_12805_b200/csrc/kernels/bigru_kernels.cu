@@ -37,8 +37,9 @@ template <int HS>
 __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
     BiGruP p, int l, const uint32_t* __restrict__ ctx, int64_t ctx_cs, const float* __restrict__ xi,
     float* out, float* fin, int64_t work_cs, const TickDesc* __restrict__ td) {
+  static_assert(kRPW == 4, "rows are paired (0,1),(2,3)");
   __shared__ __align__(16) float sw[3][HS][HS];
-  __shared__ __align__(16) float sh[kRecWarps][kRPW][2][32];
+  __shared__ __align__(16) float sh[kRecWarps][2][32][kRPW];  // h[q][row] per warp
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -64,10 +65,8 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
   }
   bool rv_ok[kRPW];
 #pragma unroll
-  for (int u = 0; u < kRPW; ++u) {
-    rv_ok[u] = r0 + u < p.R;
-    if (act) sh[wl][u][0][j] = 0.0f;  // h0 = 0
-  }
+  for (int u = 0; u < kRPW; ++u) rv_ok[u] = r0 + u < p.R;
+  *reinterpret_cast<float4*>(&sh[wl][0][j][0]) = make_float4(0.f, 0.f, 0.f, 0.f);  // h0 = 0
   const float* xr = xi ? xi + c * work_cs + int64_t(dir) * 3 * RT * H : nullptr;
   const float* t0 = p.xi0 + int64_t(dir) * 3 * p.V * H;  // layer-0 tables [3][V][H]
   const int jj = act ? j : 0;
@@ -75,7 +74,7 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
   int cur = 0;
   for (int step = 0; step < T; ++step) {
     const int tt = dir ? (T - 1 - step) : step;  // bwd direction consumes time-reversed input
-    float ar[kRPW], az[kRPW], an[kRPW], hh[kRPW];
+    float ar[kRPW], az[kRPW], an[kRPW];
 #pragma unroll
     for (int u = 0; u < kRPW; ++u) {
       const int r = rv_ok[u] ? r0 + u : r0;
@@ -92,41 +91,45 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
       }
       ar[u] = fadd(ar[u], bhr);
       az[u] = fadd(az[u], bhz);
-      hh[u] = bhn;
     }
-#pragma unroll 2
-    for (int q = 0; q < HS; q += 4) {
-      float4 hv[kRPW];
-#pragma unroll
-      for (int u = 0; u < kRPW; ++u) hv[u] = *reinterpret_cast<const float4*>(&sh[wl][u][cur][q]);
-#pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        const float wr = sw[0][q + qq][jj], wz = sw[1][q + qq][jj], wn = sw[2][q + qq][jj];
-#pragma unroll
-        for (int u = 0; u < kRPW; ++u) {
-          const float hq = qq == 0 ? hv[u].x : qq == 1 ? hv[u].y : qq == 2 ? hv[u].z : hv[u].w;
-          ar[u] = mac(ar[u], hq, wr);
-          az[u] = mac(az[u], hq, wz);
-          hh[u] = mac(hh[u], hq, wn);
-        }
-      }
+    // gate pre-activations for rows (0,1) and (2,3) as paired chains, k ascending
+    f2_t ar01 = f2_pack(ar[0], ar[1]), ar23 = f2_pack(ar[2], ar[3]);
+    f2_t az01 = f2_pack(az[0], az[1]), az23 = f2_pack(az[2], az[3]);
+    f2_t hh01 = f2_bcast(bhn), hh23 = f2_bcast(bhn);
+#pragma unroll 8
+    for (int q = 0; q < HS; ++q) {
+      const float4 hv = *reinterpret_cast<const float4*>(&sh[wl][cur][q][0]);
+      const f2_t h01 = f2_pack(hv.x, hv.y), h23 = f2_pack(hv.z, hv.w);
+      const f2_t wr = f2_bcast(sw[0][q][jj]), wz = f2_bcast(sw[1][q][jj]);
+      const f2_t wn = f2_bcast(sw[2][q][jj]);
+      ar01 = f2_mac(ar01, h01, wr);
+      ar23 = f2_mac(ar23, h23, wr);
+      az01 = f2_mac(az01, h01, wz);
+      az23 = f2_mac(az23, h23, wz);
+      hh01 = f2_mac(hh01, h01, wn);
+      hh23 = f2_mac(hh23, h23, wn);
     }
+    const float arv[kRPW] = {f2_lo(ar01), f2_hi(ar01), f2_lo(ar23), f2_hi(ar23)};
+    const float azv[kRPW] = {f2_lo(az01), f2_hi(az01), f2_lo(az23), f2_hi(az23)};
+    const float hhv[kRPW] = {f2_lo(hh01), f2_hi(hh01), f2_lo(hh23), f2_hi(hh23)};
+    const float4 hp = *reinterpret_cast<const float4*>(&sh[wl][cur][jj][0]);
+    const float hprev[kRPW] = {hp.x, hp.y, hp.z, hp.w};
+    float hn[kRPW];
 #pragma unroll
     for (int u = 0; u < kRPW; ++u) {
-      if (!act) continue;
-      const float rv = det_sigmoid(ar[u]), zv = det_sigmoid(az[u]);
-      const float nv = det_tanh(fadd(an[u], fmul(rv, hh[u])));
-      const float hn = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, sh[wl][u][cur][j]));
-      sh[wl][u][cur ^ 1][j] = hn;
-      if (rv_ok[u]) out[c * work_cs + (int64_t(r0 + u) * T + tt) * 2 * H + dir * H + j] = hn;
+      const float rv = det_sigmoid(arv[u]), zv = det_sigmoid(azv[u]);
+      const float nv = det_tanh(fadd(an[u], fmul(rv, hhv[u])));
+      hn[u] = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, hprev[u]));
+      if (act && rv_ok[u]) out[c * work_cs + (int64_t(r0 + u) * T + tt) * 2 * H + dir * H + j] = hn[u];
     }
+    if (act) *reinterpret_cast<float4*>(&sh[wl][cur ^ 1][j][0]) = make_float4(hn[0], hn[1], hn[2], hn[3]);
     __syncwarp();
     cur ^= 1;
   }
   if (fin && act) {
 #pragma unroll
     for (int u = 0; u < kRPW; ++u)
-      if (rv_ok[u]) fin[c * work_cs + int64_t(r0 + u) * 2 * H + dir * H + j] = sh[wl][u][cur][j];
+      if (rv_ok[u]) fin[c * work_cs + int64_t(r0 + u) * 2 * H + dir * H + j] = sh[wl][cur][j][u];
   }
 }
 

@@ -15,6 +15,36 @@ __device__ __forceinline__ float fdiv(float a, float b) { return __fdiv_rn(a, b)
 // acc + a*b with the product rounded first (no FMA)
 __device__ __forceinline__ float mac(float acc, float a, float b) { return __fadd_rn(acc, __fmul_rn(a, b)); }
 
+// Paired FP32 (Blackwell FMUL2/FADD2-class issue): two independent lanes of
+// the same exact operations in one instruction, each IEEE round-to-nearest,
+// bit-identical to the scalar pair (checked on B200: tools/x2/x2bench.cu).
+// ptxas contracts a single-use mul.rn.f32x2 into the following add.rn.f32x2
+// (even with -fmad=false), so the product is formed as fma.rn.f32x2(a, b, z)
+// with z = (-0, -0) read from __constant__ memory: a*b + (-0) is exactly
+// round(a*b) for every input, and an fma followed by an add cannot be fused.
+typedef unsigned long long f2_t;
+static __constant__ f2_t c_negzero2 = 0x8000000080000000ull;
+__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ f2_t f2_bcast(float x) { return f2_pack(x, x); }
+__device__ __forceinline__ float f2_lo(f2_t v) { return __uint_as_float(uint32_t(v)); }
+__device__ __forceinline__ float f2_hi(f2_t v) { return __uint_as_float(uint32_t(v >> 32)); }
+__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
+  f2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c_negzero2));
+  return r;
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// (acc.lo + a.lo*b.lo, acc.hi + a.hi*b.hi), products rounded first
+__device__ __forceinline__ f2_t f2_mac(f2_t acc, f2_t a, f2_t b) { return f2_add(acc, f2_mul(a, b)); }
+
 // det_exp: range reduction + degree-6 Taylor (detmath.cpp:24-43)
 __device__ __forceinline__ float det_exp(float x) {
   if (x > 87.0f) x = 87.0f;

@@ -9,6 +9,7 @@
 // FP32 SIMT pipe rather than tcgen05: tensor-core accumulation order is
 // unspecified, and the decoder must replay the encoder's online training bit
 // for bit.
+#include <type_traits>
 #include <algorithm>
 #include <cstdint>
 
@@ -80,7 +81,12 @@ __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc*
     cp_async_commit();  // one group per tile slot, possibly empty
   };
 
+  // Accumulators: column pairs (j, j+1) run as one paired chain when TN is even
+  // (same per-element operations, half the issue slots).
+  constexpr bool kPair = TN % 2 == 0;
+  constexpr int TNP = kPair ? TN / 2 : 1;
   float acc[TM][TN];
+  f2_t acc2[TM][TNP];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -93,6 +99,12 @@ __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc*
       }
       acc[i][j] = v;
     }
+  if constexpr (kPair) {
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TNP; ++j) acc2[i][j] = f2_pack(acc[i][2 * j], acc[i][2 * j + 1]);
+  }
 
   const bool relu = p.relu_a != 0;
 #pragma unroll
@@ -103,7 +115,7 @@ __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc*
     load(tile + STAGES - 1);  // refills the stage consumed in the previous iteration
     const int stage = tile % STAGES;
     const int kmax = min(BK, p.K - tile * BK);
-    auto body = [&](int kk) {
+    auto body = [&](int kk, auto relu_c) {
       // each thread's TM (TN) operands are contiguous: one vector shared load each
       float a[TM], b[TN];
       const float* ap = &As[stage][kk][ty * TM];
@@ -128,23 +140,45 @@ __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc*
 #pragma unroll
         for (int j = 0; j < TN; ++j) b[j] = bp[j];
       }
-      if (relu) {
+      if constexpr (decltype(relu_c)::value) {
 #pragma unroll
         for (int i = 0; i < TM; ++i) a[i] = a[i] < 0.0f ? 0.0f : a[i];
       }
+      if constexpr (kPair) {
 #pragma unroll
-      for (int i = 0; i < TM; ++i)
+        for (int i = 0; i < TM; ++i) {
+          const f2_t ai = f2_bcast(a[i]);
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = mac(acc[i][j], a[i], b[j]);
+          for (int j = 0; j < TNP; ++j) acc2[i][j] = f2_mac(acc2[i][j], ai, f2_pack(b[2 * j], b[2 * j + 1]));
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = mac(acc[i][j], a[i], b[j]);
+      }
     };
-    if (kmax == BK) {
+    auto run = [&](auto relu_c) {
+      if (kmax == BK) {
 #pragma unroll 8
-      for (int kk = 0; kk < BK; ++kk) body(kk);
-    } else {
-      for (int kk = 0; kk < kmax; ++kk) body(kk);
-    }
+        for (int kk = 0; kk < BK; ++kk) body(kk, relu_c);
+      } else {
+        for (int kk = 0; kk < kmax; ++kk) body(kk, relu_c);
+      }
+    };
+    if (relu) run(std::true_type{});
+    else run(std::false_type{});
   }
   cp_async_wait<0>();
+  if constexpr (kPair) {
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TNP; ++j) {
+        acc[i][2 * j] = f2_lo(acc2[i][j]);
+        acc[i][2 * j + 1] = f2_hi(acc2[i][j]);
+      }
+  }
 
 #pragma unroll
   for (int i = 0; i < TM; ++i)
@@ -206,113 +240,159 @@ __device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
 // B tile serves all MR rows. MR=1 spreads a single chunk's few outputs over
 // the most SMs (latency regime); MR=4 amortizes the B tile when many chunks
 // are in flight (throughput regime).
-constexpr int kNtCols = 64, kNtBK = 64, kNtStages = 4;
-constexpr int kNtSB = kNtBK + 4;  // padded B row: LDS.128 of 32 rows = 4 wavefronts
-__host__ __device__ constexpr size_t nt_smem(int mr) {
-  return size_t(kNtStages) * (size_t(mr) * kNtBK + size_t(kNtCols) * kNtSB) * sizeof(float);
+// Long-K "NT" reduction C[m][n] (+)= sum_k A[m][k] * B[n][k] (weight gradients:
+// feature-major activations x feature-major output gradients, k = the R*t
+// position index in the reference's accumulation order). Every output is one
+// sequential chain over k, so parallelism is across outputs only.
+//
+// Warp-autonomous design: a warp owns a task of RPT rows x 32 columns of one
+// problem and streams its own operands through a private 3-stage cp.async ring
+// (no block barriers, only __syncwarp). Each lane keeps RPT chains for its
+// column; A is staged interleaved [k][row] so one broadcast LDS.128 yields row
+// pairs for the paired FP32 chains; B is read once per RPT rows. Row M of a
+// problem is the bias row (A == 1, so 1*b == b exactly: the plain sum).
+constexpr int kNwBK = 32, kNwWarps = 2;
+constexpr int kNwSB = kNwBK + 4;  // padded B row: LDS.128 of 32 rows is conflict-free
+__host__ __device__ constexpr int nw_warp_floats(int rpt, int stages) {
+  return stages * (rpt * kNwBK + 32 * kNwSB);
 }
 
 struct NtBatch {
   NtP p[kNtMaxProb];
-  int first_block[kNtMaxProb + 1];  // prefix of row blocks per problem
+  int first_task[kNtMaxProb + 1];  // prefix of warp tasks per problem
+  int colgroups[kNtMaxProb];
   int n;
 };
 
-// VEC: rows 16-byte aligned, K multiple of 4 (host-checked); else 4-byte copies.
-template <bool VEC, int MR>
-__global__ void __launch_bounds__(kNtCols * MR) k_gemm_nt(NtBatch nb, const TickDesc* __restrict__ td) {
+// VEC: B rows 16-byte aligned and K a multiple of 4 (host-checked).
+// STAGES: ring depth; 3 when the chip is full of warps, 8 when a few warps must
+// cover the L2 latency alone.
+template <bool VEC, int RPT, int STAGES>
+__global__ void __launch_bounds__(kNwWarps * 32) k_gemm_nt(NtBatch nb, const TickDesc* __restrict__ td) {
+  constexpr int kNwStages = STAGES;
   extern __shared__ __align__(128) float sm[];
-  constexpr int NT = kNtCols * MR;
-  if (blockIdx.z >= unsigned(td->n_act)) return;
-  const int c = td->act[blockIdx.z];
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int task = int(blockIdx.x) * kNwWarps + w;
+  if (task >= nb.first_task[nb.n]) return;  // warp-uniform; no block barriers below
   int prob = 0;
-  while (prob + 1 < nb.n && int(blockIdx.y) >= nb.first_block[prob + 1]) ++prob;
+  while (prob + 1 < nb.n && task >= nb.first_task[prob + 1]) ++prob;
   const NtP& pp = nb.p[prob];
-  const int mb = int(blockIdx.y) - nb.first_block[prob];
-  const float* Ab = pp.A;
-  const float* Bb = pp.B;
-  float* Cb = pp.C;
-  float* CBb = pp.cb;
-  const int64_t a_cs = pp.a_cs, b_cs = pp.b_cs, c_cs = pp.c_cs, lda = pp.lda, ldb = pp.ldb,
-                ldc = pp.ldc;
+  const int lt = task - nb.first_task[prob];
+  const int cg = lt % nb.colgroups[prob], rg = lt / nb.colgroups[prob];
   const int M = pp.M, N = pp.N, K = pp.K;
-  const int m0 = mb * MR;
-  if (m0 > M) return;
-  const int n0 = blockIdx.x * kNtCols;
-  if (n0 >= N) return;
-  const int tid = threadIdx.x, col = tid % kNtCols, mr = tid / kNtCols;
-  const int m = m0 + mr, n = n0 + col;
-  const bool ones = m == M;      // bias row: plain sum of the gradient rows
-  const bool live = m <= M && n < N;
-  const int nrows = min(kNtCols, N - n0);
-  const int arows = min(MR, M - m0);  // real A rows in this block (bias row has none)
-  const float* A = Ab + c * a_cs + int64_t(m0) * lda;
-  const float* B = Bb + c * b_cs + int64_t(n0) * ldb;
-  float* C = Cb + c * c_cs;
-  float* As = sm;                                  // [stage][MR][BK]
-  float* Bs = sm + kNtStages * MR * kNtBK;         // [stage][64][SB]
-  const int ntiles = (K + kNtBK - 1) / kNtBK;
-
+  const int64_t lda = pp.lda, ldb = pp.ldb, ldc = pp.ldc;
+  const int m0 = rg * RPT, n0 = cg * 32, n = n0 + lane;
+  const int arows = max(0, min(RPT, M - m0));  // rows with A data; the rest are 1 (bias) or 0
+  const int nrows = min(32, N - n0);
+  float* As = sm + w * nw_warp_floats(RPT, STAGES);  // [stage][BK][RPT]
+  float* Bs = As + kNwStages * RPT * kNwBK;  // [stage][32][SB]
+  const float* A = pp.A + c * pp.a_cs + int64_t(m0) * lda;
+  const float* B = pp.B + c * pp.b_cs + int64_t(n0) * ldb;
+  for (int r = arows; r < RPT; ++r) {
+    const float v = m0 + r == M ? 1.0f : 0.0f;
+    for (int i = lane; i < kNwStages * kNwBK; i += 32) As[i * RPT + r] = v;
+  }
+  const int ntiles = (K + kNwBK - 1) / kNwBK;
+  // full tiles: lane copies A[r][k0 + lane] for each row (BK == 32) and the
+  // 16-byte chunk (lane & 7) of B rows (lane >> 3) + 4j, j < 8
+  static_assert(kNwBK == 32, "one A element and one B chunk column per lane");
+  const float* bl = B + int64_t(lane >> 3) * ldb + 4 * (lane & 7);
+  const int bsl = (lane >> 3) * kNwSB + 4 * (lane & 7);
   auto load = [&](int tile) {
     if (tile < ntiles) {
-      const int st = tile % kNtStages, k0 = tile * kNtBK, kc = min(kNtBK, K - k0);
-      float* as = As + st * MR * kNtBK;
-      float* bs = Bs + st * kNtCols * kNtSB;
-      if (VEC && kc == kNtBK) {
-        for (int i = tid; i < arows * 16; i += NT)
-          cp_async16(as + (i >> 4) * kNtBK + 4 * (i & 15), A + int64_t(i >> 4) * lda + k0 + 4 * (i & 15));
-        for (int i = tid; i < nrows * 16; i += NT)
-          cp_async16(bs + (i >> 4) * kNtSB + 4 * (i & 15), B + int64_t(i >> 4) * ldb + k0 + 4 * (i & 15));
+      const int st = tile % kNwStages, k0 = tile * kNwBK, kc = min(kNwBK, K - k0);
+      float* as = As + st * kNwBK * RPT;
+      float* bs = Bs + st * 32 * kNwSB;
+      if (kc == kNwBK) {
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+          if (r < arows) cp_async4(as + lane * RPT + r, A + int64_t(r) * lda + k0 + lane);
+        if (VEC && nrows == 32) {
+          const float* src = bl + k0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j, src += 4 * ldb) cp_async16(bs + bsl + j * 4 * kNwSB, src);
+        } else {
+          for (int i = lane; i < nrows * kNwBK; i += 32)
+            cp_async4(bs + (i / kNwBK) * kNwSB + i % kNwBK, B + int64_t(i / kNwBK) * ldb + k0 + i % kNwBK);
+        }
       } else {
-        for (int i = tid; i < arows * kc; i += NT)
-          cp_async4(as + (i / kc) * kNtBK + i % kc, A + int64_t(i / kc) * lda + k0 + i % kc);
-        for (int i = tid; i < nrows * kc; i += NT)
-          cp_async4(bs + (i / kc) * kNtSB + i % kc, B + int64_t(i / kc) * ldb + k0 + i % kc);
+        for (int i = lane; i < arows * kc; i += 32) {
+          const int r = i / kc, kk = i % kc;
+          cp_async4(as + kk * RPT + r, A + int64_t(r) * lda + k0 + kk);
+        }
+        for (int i = lane; i < nrows * kc; i += 32)
+          cp_async4(bs + (i / kc) * kNwSB + i % kc, B + int64_t(i / kc) * ldb + k0 + i % kc);
       }
     }
     cp_async_commit();  // one group per tile slot, possibly empty
   };
 
-  float* out = live ? ((ones && CBb) ? CBb + c * c_cs + n : C + int64_t(m) * ldc + n) : nullptr;
-  float acc = live ? *out : 0.0f;
+  constexpr int NP = RPT / 2;
+  float acc[RPT];
+  float* outp[RPT];
 #pragma unroll
-  for (int s = 0; s < kNtStages - 1; ++s) load(s);
-  for (int tile = 0; tile < ntiles; ++tile) {
-    cp_async_wait<kNtStages - 2>();
-    __syncthreads();  // tile landed for everyone; everyone is past tile-1
-    load(tile + kNtStages - 1);
-    const int st = tile % kNtStages, kc = min(kNtBK, K - tile * kNtBK);
-    const float* as = As + (st * MR + mr) * kNtBK;
-    const float* bs = Bs + (st * kNtCols + col) * kNtSB;
-    if (live) {
-      if (kc == kNtBK) {
-        if (ones) {
+  for (int r = 0; r < RPT; ++r) {
+    const int m = m0 + r;
+    const bool live = m <= M && n < N;
+    outp[r] = live ? ((m == M && pp.cb) ? pp.cb + c * pp.c_cs + n : pp.C + c * pp.c_cs + int64_t(m) * ldc + n)
+                   : nullptr;
+    acc[r] = live ? *outp[r] : 0.0f;
+  }
+  f2_t acc2[NP > 0 ? NP : 1];
 #pragma unroll
-          for (int kk = 0; kk < kNtBK; kk += 4) {
-            const float4 b = *reinterpret_cast<const float4*>(bs + kk);
-            acc = fadd(acc, b.x);  // 1.0f * b == b exactly
-            acc = fadd(acc, b.y);
-            acc = fadd(acc, b.z);
-            acc = fadd(acc, b.w);
-          }
-        } else {
+  for (int i = 0; i < NP; ++i) acc2[i] = f2_pack(acc[2 * i], acc[2 * i + 1]);
+
+  auto step = [&](const float* ak, float bq) {
+    if constexpr (RPT == 1) {
+      acc[0] = mac(acc[0], ak[0], bq);
+    } else {
+      const f2_t bb = f2_bcast(bq);
+      if constexpr (RPT >= 4) {
 #pragma unroll
-          for (int kk = 0; kk < kNtBK; kk += 4) {
-            const float4 a = *reinterpret_cast<const float4*>(as + kk);
-            const float4 b = *reinterpret_cast<const float4*>(bs + kk);
-            acc = mac(acc, a.x, b.x);
-            acc = mac(acc, a.y, b.y);
-            acc = mac(acc, a.z, b.z);
-            acc = mac(acc, a.w, b.w);
-          }
+        for (int i = 0; i < RPT / 4; ++i) {
+          const float4 a4 = *reinterpret_cast<const float4*>(ak + 4 * i);
+          acc2[2 * i] = f2_mac(acc2[2 * i], f2_pack(a4.x, a4.y), bb);
+          acc2[2 * i + 1] = f2_mac(acc2[2 * i + 1], f2_pack(a4.z, a4.w), bb);
         }
       } else {
-        for (int kk = 0; kk < kc; ++kk) acc = ones ? fadd(acc, bs[kk]) : mac(acc, as[kk], bs[kk]);
+        const float2 a2 = *reinterpret_cast<const float2*>(ak);
+        acc2[0] = f2_mac(acc2[0], f2_pack(a2.x, a2.y), bb);
       }
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < kNwStages - 1; ++s) load(s);
+  for (int tile = 0; tile < ntiles; ++tile) {
+    cp_async_wait<kNwStages - 2>();
+    __syncwarp();  // tile landed for all lanes; all lanes are past tile-1
+    load(tile + kNwStages - 1);
+    const int st = tile % kNwStages, kc = min(kNwBK, K - tile * kNwBK);
+    const float* as = As + st * kNwBK * RPT;
+    const float* bs = Bs + (st * 32 + lane) * kNwSB;
+    if (kc == kNwBK) {
+#pragma unroll
+      for (int kk = 0; kk < kNwBK; kk += 4) {
+        const float4 b = *reinterpret_cast<const float4*>(bs + kk);
+        step(as + (kk + 0) * RPT, b.x);
+        step(as + (kk + 1) * RPT, b.y);
+        step(as + (kk + 2) * RPT, b.z);
+        step(as + (kk + 3) * RPT, b.w);
+      }
+    } else {
+      for (int kk = 0; kk < kc; ++kk) step(as + kk * RPT, bs[kk]);
     }
   }
   cp_async_wait<0>();
-  if (live) *out = acc;
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    acc[2 * i] = f2_lo(acc2[i]);
+    acc[2 * i + 1] = f2_hi(acc2[i]);
+  }
+#pragma unroll
+  for (int r = 0; r < RPT; ++r)
+    if (outp[r]) *outp[r] = acc[r];
 }
 
 // ------------------------------------------------------------------ embed
@@ -729,88 +809,161 @@ __global__ void __launch_bounds__(kEmbWarps * 32) k_emb_bwd(
 }
 
 // Sort-based embedding gradient (the default when a chunk's R*t positions and
-// the vocabulary fit in shared memory): stable counting sort of the positions
-// by token (histogram, scan, warp match-any ranks keep (r,t) order), then one
-// thread per (token, column) walks its contiguous list in order with 16 loads
-// in flight. Same per-element order as Embedding::backward (layers.cpp:117-125).
+// the vocabulary fit in shared memory). Three phases, one block per chunk:
+//  1. stable counting sort of the positions by token: warp w owns the
+//     contiguous span [w*RT/32, (w+1)*RT/32), counts it with match-any, the
+//     block scans (token-major, warp-minor) and each warp then places its span
+//     in order, so equal tokens keep ascending (r,t) order;
+//  2. all threads gather dx (+ the last-position dxl term) in sorted order into
+//     shared memory, a slab of positions at a time (independent loads);
+//  3. one thread per (token, column) adds its contiguous run from shared
+//     memory, carrying the sum across slabs.
+// The per-element order is Embedding::backward's (layers.cpp:117-125).
 constexpr int kSortThreads = 1024;
+constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortMaxPos = 10240;
 constexpr int kSortMaxV = 256;
+constexpr int kSortAcc = 4;                 // (token, column) outputs per thread
+constexpr int kSortVals = 36 * 1024;        // staged floats per slab
+constexpr size_t kSortSmem = size_t(kSortVals) * 4 + size_t(kSortMaxPos) * 2 +
+                             size_t(kSortWarps) * kSortMaxV * 2 + size_t(kSortMaxV + 1) * 4;
 __global__ void __launch_bounds__(kSortThreads) k_emb_bwd_sorted(
     const uint32_t* __restrict__ ctx, int64_t ctx_cs, const float* __restrict__ dx, int64_t dx_cs,
     const float* __restrict__ dxl, int64_t dxl_cs, float* grads, int64_t g_cs, int64_t off_emb,
     DmDims d, const TickDesc* __restrict__ td) {
-  __shared__ uint16_t sorted[kSortMaxPos];
-  __shared__ int cnt[kSortMaxV], off[kSortMaxV + 1], run[kSortMaxV];
-  __shared__ uint16_t wc[32][kSortMaxV];  // per-warp counts of each token in the current slab
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* vals = reinterpret_cast<float*>(smem_raw);
+  uint16_t* sorted = reinterpret_cast<uint16_t*>(vals + kSortVals);
+  uint16_t* wc = sorted + kSortMaxPos;                       // [warp][V] counts, then cursors
+  int* off = reinterpret_cast<int*>(wc + kSortWarps * kSortMaxV);  // [V+1]
   if (blockIdx.x >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int V = d.V, RT = d.R * d.T;
+  const int V = d.V, E = d.E, RT = d.R * d.T;
   const uint32_t* cp = ctx + c * ctx_cs;
-  for (int v = tid; v < V; v += kSortThreads) {
-    cnt[v] = 0;
-    run[v] = 0;
+  const int span = (RT + kSortWarps - 1) / kSortWarps;
+  const int p0 = w * span, p1 = min(RT, p0 + span);
+  const unsigned lt = (1u << lane) - 1u;
+  // phase 1a: per-warp token counts
+  for (int v = lane; v < V; v += 32) wc[w * V + v] = 0;
+  __syncwarp();
+  for (int base = p0; base < p1; base += 32) {
+    const int p = base + lane;
+    const uint32_t v = p < p1 ? cp[p] : 0xffffffffu;
+    const unsigned m = __match_any_sync(0xffffffffu, v);
+    if (p < p1 && (m & lt) == 0) wc[w * V + v] = uint16_t(wc[w * V + v] + __popc(m));
+    __syncwarp();
   }
   __syncthreads();
-  for (int p = tid; p < RT; p += kSortThreads) atomicAdd(&cnt[cp[p]], 1);
-  __syncthreads();
-  if (tid == 0) {
-    int a = 0;
-    for (int v = 0; v < V; ++v) {
-      off[v] = a;
-      a += cnt[v];
-    }
-    off[V] = a;
-  }
-  __syncthreads();
-  for (int base = 0; base < RT; base += kSortThreads) {
-    for (int i = tid; i < 32 * V; i += kSortThreads) wc[i / V][i % V] = 0;
-    __syncthreads();
-    const int p = base + tid;
-    const bool ok = p < RT;
-    const uint32_t v = ok ? cp[p] : 0xffffffffu;
-    const unsigned mask = __match_any_sync(0xffffffffu, v);
-    const int rank_w = __popc(mask & ((1u << lane) - 1u));
-    if (ok && rank_w == 0) wc[w][v] = uint16_t(__popc(mask));
-    __syncthreads();
-    if (ok) {
-      int before = 0;
-      for (int ww = 0; ww < w; ++ww) before += wc[ww][v];
-      sorted[off[v] + run[v] + before + rank_w] = uint16_t(p);
-    }
-    __syncthreads();
-    for (int vv = tid; vv < V; vv += kSortThreads) {
+  // phase 1b: exclusive scan in (token, warp) order; wc becomes each warp's cursor
+  if (w == 0) {
+    int carry = 0;
+    for (int v0 = 0; v0 < V; v0 += 32) {
+      const int v = v0 + lane;
       int tot = 0;
-      for (int ww = 0; ww < 32; ++ww) tot += wc[ww][vv];
-      run[vv] += tot;
+      if (v < V)
+        for (int ww = 0; ww < kSortWarps; ++ww) tot += wc[ww * V + v];
+      int inc = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      if (v < V) {
+        int a = carry + inc - tot;
+        off[v] = a;
+        for (int ww = 0; ww < kSortWarps; ++ww) {
+          const int n = wc[ww * V + v];
+          wc[ww * V + v] = uint16_t(a);
+          a += n;
+        }
+      }
+      carry += __shfl_sync(0xffffffffu, inc, 31);
     }
-    __syncthreads();
+    if (lane == 0) off[V] = carry;
   }
+  __syncthreads();
+  // phase 1c: stable placement
+  for (int base = p0; base < p1; base += 32) {
+    const int p = base + lane;
+    const uint32_t v = p < p1 ? cp[p] : 0xffffffffu;
+    const unsigned m = __match_any_sync(0xffffffffu, v);
+    if (p < p1) {
+      const int cur = wc[w * V + v];
+      sorted[cur + __popc(m & lt)] = uint16_t(p);
+    }
+    __syncwarp();
+    if (p < p1 && (m & lt) == 0) wc[w * V + v] = uint16_t(wc[w * V + v] + __popc(m));
+    __syncwarp();
+  }
+  __syncthreads();
+  // phases 2+3
   const float* xp = dx + c * dx_cs;
   const float* lp = dxl ? dxl + c * dxl_cs : nullptr;
-  for (int o = tid; o < V * d.E; o += kSortThreads) {
-    const int v = o / d.E, j = o % d.E;
-    float* g = grads + c * g_cs + off_emb + o;
-    float acc = *g;
-    const int b0 = off[v], b1 = off[v + 1];
-    constexpr int kB = 16;
-    for (int h0 = b0; h0 < b1; h0 += kB) {
-      float x[kB];
+  float* gp = grads + c * g_cs + off_emb;
+  const int VE = V * E;
+  float acc[kSortAcc];
 #pragma unroll
-      for (int b = 0; b < kB; ++b) {
-        const int h = h0 + b < b1 ? h0 + b : b0;
-        const int pp = sorted[h];
-        float val = __ldg(xp + int64_t(pp) * d.E + j);
-        if (lp && pp % d.T == d.T - 1) val = fadd(val, __ldg(lp + int64_t(pp / d.T) * d.E + j));
-        x[b] = val;
-      }
-#pragma unroll
-      for (int b = 0; b < kB; ++b)
-        if (h0 + b < b1) acc = fadd(acc, x[b]);
-    }
-    *g = acc;
+  for (int q = 0; q < kSortAcc; ++q) {
+    const int o = tid + q * kSortThreads;
+    acc[q] = o < VE ? gp[o] : 0.f;
   }
+  const int slab = kSortVals / E;
+  for (int s0 = 0; s0 < RT; s0 += slab) {
+    const int s1 = min(RT, s0 + slab);
+    const int n = (s1 - s0) * E;
+    for (int i = tid; i < n; i += kSortThreads) {
+      const int h = s0 + i / E, j = i % E;
+      const int pp = sorted[h];
+      float val = __ldg(xp + int64_t(pp) * E + j);
+      if (lp && pp % d.T == d.T - 1) val = fadd(val, __ldg(lp + int64_t(pp / d.T) * E + j));
+      vals[i] = val;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kSortAcc; ++q) {
+      const int o = tid + q * kSortThreads;
+      if (o < VE) {
+        const int v = o / E, j = o % E;
+        const int b0 = max(off[v], s0), b1 = min(off[v + 1], s1);
+        float a = acc[q];
+        int h = b0;
+        for (; h + 8 <= b1; h += 8) {
+          float x[8];
+#pragma unroll
+          for (int b = 0; b < 8; ++b) x[b] = vals[(h + b - s0) * E + j];
+#pragma unroll
+          for (int b = 0; b < 8; ++b) a = fadd(a, x[b]);
+        }
+        for (; h < b1; ++h) a = fadd(a, vals[(h - s0) * E + j]);
+        acc[q] = a;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < kSortAcc; ++q) {
+    const int o = tid + q * kSortThreads;
+    if (o < VE) gp[o] = acc[q];
+  }
+}
+
+static bool sorted_emb_ok(const DmDims& d) {
+  return d.R * d.T <= kSortMaxPos && d.V <= kSortMaxV && d.V * d.E <= kSortThreads * kSortAcc &&
+         d.E <= kSortVals / 64;
+}
+static void launch_sorted_emb(const uint32_t* ctx, int64_t ctx_cs, const float* dx, int64_t dx_cs,
+                              const float* dxl, int64_t dxl_cs, float* grads, int64_t g_cs,
+                              int64_t off_emb, DmDims d, const TickDesc* td, int max_active,
+                              cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_emb_bwd_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kSortSmem));
+    attr = true;
+  }
+  k_emb_bwd_sorted<<<max_active, kSortThreads, kSortSmem, st>>>(ctx, ctx_cs, dx, dx_cs, dxl, dxl_cs,
+                                                                grads, g_cs, off_emb, d, td);
 }
 
 // ------------------------------------------------------------------ Adam
@@ -884,44 +1037,56 @@ void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int m
   if (max_active <= 0 || nprob <= 0) return;
   auto al = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
   bool vec = true;
-  int maxn = 0;
   for (int i = 0; i < nprob; ++i) {
     const NtP& p = probs[i];
-    vec = vec && p.K % 4 == 0 && p.lda % 4 == 0 && p.ldb % 4 == 0 && p.a_cs % 4 == 0 &&
-          p.b_cs % 4 == 0 && al(p.A) && al(p.B);
-    maxn = std::max(maxn, p.N);
+    vec = vec && p.K % 4 == 0 && p.ldb % 4 == 0 && p.b_cs % 4 == 0 && al(p.B);
   }
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_gemm_nt<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(nt_smem(1)));
-    cudaFuncSetAttribute(k_gemm_nt<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(nt_smem(1)));
-    cudaFuncSetAttribute(k_gemm_nt<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(nt_smem(4)));
-    cudaFuncSetAttribute(k_gemm_nt<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(nt_smem(4)));
+#define PMKLC_NT_ATTR(V, R, S) \
+  cudaFuncSetAttribute(k_gemm_nt<V, R, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                       int(kNwWarps * nw_warp_floats(R, S) * sizeof(float)))
+    PMKLC_NT_ATTR(true, 8, 3); PMKLC_NT_ATTR(false, 8, 3); PMKLC_NT_ATTR(true, 4, 3);
+    PMKLC_NT_ATTR(false, 4, 3); PMKLC_NT_ATTR(true, 2, 3); PMKLC_NT_ATTR(false, 2, 3);
+    PMKLC_NT_ATTR(true, 2, 8); PMKLC_NT_ATTR(false, 2, 8);
+#undef PMKLC_NT_ATTR
     attr_set = true;
   }
-  const int nx = (maxn + kNtCols - 1) / kNtCols;
-  auto build = [&](int mr, NtBatch& nb) {
+  auto build = [&](int rpt, NtBatch& nb) {
     nb.n = nprob;
-    nb.first_block[0] = 0;
+    nb.first_task[0] = 0;
     for (int i = 0; i < nprob; ++i) {
       nb.p[i] = probs[i];
-      nb.first_block[i + 1] = nb.first_block[i] + (probs[i].M + 1 + mr - 1) / mr;
+      nb.colgroups[i] = (probs[i].N + 31) / 32;
+      nb.first_task[i + 1] = nb.first_task[i] + (probs[i].M + 1 + rpt - 1) / rpt * nb.colgroups[i];
     }
-    return nb.first_block[nprob];
+    return nb.first_task[nprob];
   };
+  // Rows per thread: 8 (B read once per 8 rows) while that still gives ~8
+  // warps per SM, else 4 while that gives ~4; a launch that cannot fill the chip
+  // is bound by the k chain (4 cycles per step), which 2 paired rows per thread
+  // still meet, with a deep ring so the few warps do not wait on L2.
   NtBatch nb;
-  const int rows1 = build(1, nb);
-  // one-row blocks while the launch cannot fill the chip, else 4-row blocks
-  if (int64_t(nx) * rows1 * max_active < 2 * 148) {
-    dim3 grid(nx, rows1, max_active);
-    if (vec) k_gemm_nt<true, 1><<<grid, kNtCols, nt_smem(1), st>>>(nb, td);
-    else k_gemm_nt<false, 1><<<grid, kNtCols, nt_smem(1), st>>>(nb, td);
+  int rpt = 8;
+  if (int64_t(build(8, nb)) * max_active < 148 * 8) rpt = 4;
+  if (rpt == 4 && int64_t(build(4, nb)) * max_active < 148 * 4) rpt = 2;
+  const int tasks = build(rpt, nb);
+  const int stages = (rpt == 2 && int64_t(tasks) * max_active < 148 * 2) ? 8 : 3;
+  const dim3 grid(unsigned((tasks + kNwWarps - 1) / kNwWarps), unsigned(max_active));
+  const size_t smem = size_t(kNwWarps) * nw_warp_floats(rpt, stages) * sizeof(float);
+#define PMKLC_NT_LAUNCH(R, S)                                                                  \
+  if (vec) k_gemm_nt<true, R, S><<<grid, kNwWarps * 32, smem, st>>>(nb, td);                  \
+  else k_gemm_nt<false, R, S><<<grid, kNwWarps * 32, smem, st>>>(nb, td);
+  if (rpt == 8) {
+    PMKLC_NT_LAUNCH(8, 3)
+  } else if (rpt == 4) {
+    PMKLC_NT_LAUNCH(4, 3)
+  } else if (stages == 3) {
+    PMKLC_NT_LAUNCH(2, 3)
   } else {
-    const int rows4 = build(4, nb);
-    dim3 grid(nx, rows4, max_active);
-    if (vec) k_gemm_nt<true, 4><<<grid, kNtCols * 4, nt_smem(4), st>>>(nb, td);
-    else k_gemm_nt<false, 4><<<grid, kNtCols * 4, nt_smem(4), st>>>(nb, td);
+    PMKLC_NT_LAUNCH(2, 8)
   }
+#undef PMKLC_NT_LAUNCH
 }
 
 void launch_gemm_nt(const NtP& p0, const NtP* p1, const TickDesc* td, int max_active,
@@ -987,9 +1152,8 @@ void launch_emb_grad(const uint32_t* ctx, int64_t ctx_cs, const float* dx, int64
                      float* grads, int64_t g_cs, int64_t off_emb, DmDims d, const TickDesc* td,
                      int max_active, cudaStream_t st) {
   if (max_active <= 0) return;
-  if (d.R * d.T <= kSortMaxPos && d.V <= kSortMaxV) {
-    k_emb_bwd_sorted<<<max_active, kSortThreads, 0, st>>>(ctx, ctx_cs, dx, dx_cs, nullptr, 0, grads,
-                                                         g_cs, off_emb, d, td);
+  if (sorted_emb_ok(d)) {
+    launch_sorted_emb(ctx, ctx_cs, dx, dx_cs, nullptr, 0, grads, g_cs, off_emb, d, td, max_active, st);
     return;
   }
   dim3 g2(unsigned((d.V + kEmbWarps - 1) / kEmbWarps), max_active);
@@ -1004,6 +1168,11 @@ void launch_embed_bwd(const uint32_t* ctx, int64_t ctx_cs, const float* dx, int6
   if (max_active <= 0) return;
   dim3 g1(unsigned((d.T * d.E + 255) / 256), max_active);
   k_pos_bwd<<<g1, 256, 0, st>>>(dx, dx_cs, dxl, dxl_cs, grads, g_cs, off_pos, d, td);
+  if (sorted_emb_ok(d)) {
+    launch_sorted_emb(ctx, ctx_cs, dx, dx_cs, dxl, dxl_cs, grads, g_cs, off_emb, d, td, max_active,
+                      st);
+    return;
+  }
   dim3 g2(unsigned((d.V + kEmbWarps - 1) / kEmbWarps), max_active);
   k_emb_bwd<<<g2, kEmbWarps * 32, 0, st>>>(ctx, ctx_cs, dx, dx_cs, dxl, dxl_cs, grads, g_cs, off_emb, d,
                                 td);

@@ -122,6 +122,96 @@ __global__ void __launch_bounds__(256) k_sprm_fwd(SprmP s, const uint32_t* __res
   if (act) fin[int64_t(r) * 2 * H + d * H + j] = sh[wl][cur][j];  // final_state (layers.cpp:389-399)
 }
 
+// H == 32 forward: two rows per warp as paired chains (rows r0, r0+1), the
+// three gate chains interleaved, next step's token and table values prefetched.
+// Same per-element operations and order as k_sprm_fwd.
+__global__ void __launch_bounds__(256) k_sprm_fwd32(SprmP s, const uint32_t* __restrict__ ctx,
+                                                    const float* __restrict__ tab, float* tape,
+                                                    float* fin) {
+  constexpr int H = 32;
+  __shared__ __align__(16) float sh[8][2][H][2];  // [warp][cur][q][row]
+  __shared__ __align__(16) float sw[3][H][H];
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = blockIdx.x & 1;
+  const int r0 = ((blockIdx.x >> 1) * 8 + wl) * 2;
+  const int T = s.T, R = s.R, V = s.V;
+  const float* W = s.w;
+  for (int i = threadIdx.x; i < 3 * H * H; i += blockDim.x) {
+    const int gate = i / (H * H), rem = i % (H * H);
+    sw[gate][rem / H][rem % H] = W[goff(s.offs, d, WHR + gate) + rem];
+  }
+  __syncthreads();
+  if (r0 >= R) return;
+  const bool ok1 = r0 + 1 < R;
+  const int r1 = ok1 ? r0 + 1 : r0;
+  const int j = lane;
+  const float bhr = W[goff(s.offs, d, BHR) + j], bhz = W[goff(s.offs, d, BHZ) + j],
+              bhn = W[goff(s.offs, d, BHN) + j];
+  const float* t0 = tab + int64_t(d) * 3 * V * H;
+  const int64_t TRH = int64_t(T) * R * H;
+  float* tr = tape + (int64_t(0 * 2 + d) * TRH);
+  float* tz = tape + (int64_t(1 * 2 + d) * TRH);
+  float* tn = tape + (int64_t(2 * 2 + d) * TRH);
+  float* th = tape + (int64_t(3 * 2 + d) * TRH);
+  float* to = tape + (int64_t(4 * 2 + d) * TRH);
+  *reinterpret_cast<float2*>(&sh[wl][0][j][0]) = make_float2(0.f, 0.f);
+  auto fetch = [&](int t, float (&x)[2][3]) {
+    const int src_t = d ? (T - 1 - t) : t;
+    const int64_t k0 = ctx[int64_t(r0) * T + src_t], k1 = ctx[int64_t(r1) * T + src_t];
+    x[0][0] = t0[k0 * H + j];
+    x[0][1] = t0[int64_t(V) * H + k0 * H + j];
+    x[0][2] = t0[2 * int64_t(V) * H + k0 * H + j];
+    x[1][0] = t0[k1 * H + j];
+    x[1][1] = t0[int64_t(V) * H + k1 * H + j];
+    x[1][2] = t0[2 * int64_t(V) * H + k1 * H + j];
+  };
+  float xc[2][3], xn[2][3];
+  fetch(0, xc);
+  __syncwarp();
+  int cur = 0;
+  for (int t = 0; t < T; ++t) {
+    if (t + 1 < T) fetch(t + 1, xn);
+    f2_t ar = f2_pack(fadd(xc[0][0], bhr), fadd(xc[1][0], bhr));
+    f2_t az = f2_pack(fadd(xc[0][1], bhz), fadd(xc[1][1], bhz));
+    f2_t hh = f2_bcast(bhn);
+#pragma unroll
+    for (int q = 0; q < H; ++q) {
+      const float2 hv = *reinterpret_cast<const float2*>(&sh[wl][cur][q][0]);
+      const f2_t hq = f2_pack(hv.x, hv.y);
+      ar = f2_mac(ar, hq, f2_bcast(sw[0][q][j]));
+      az = f2_mac(az, hq, f2_bcast(sw[1][q][j]));
+      hh = f2_mac(hh, hq, f2_bcast(sw[2][q][j]));
+    }
+    const float2 hp = *reinterpret_cast<const float2*>(&sh[wl][cur][j][0]);
+    const float arv[2] = {f2_lo(ar), f2_hi(ar)}, azv[2] = {f2_lo(az), f2_hi(az)};
+    const float hhv[2] = {f2_lo(hh), f2_hi(hh)}, hpv[2] = {hp.x, hp.y};
+    float hn[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const float rv = det_sigmoid(arv[u]), zv = det_sigmoid(azv[u]);
+      const float nv = det_tanh(fadd(xc[u][2], fmul(rv, hhv[u])));
+      hn[u] = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, hpv[u]));
+      if (u == 0 || ok1) {
+        const int64_t o = (int64_t(t) * R + r0 + u) * H + j;
+        tr[o] = rv;
+        tz[o] = zv;
+        tn[o] = nv;
+        th[o] = hhv[u];
+        to[o] = hn[u];
+      }
+    }
+    *reinterpret_cast<float2*>(&sh[wl][cur ^ 1][j][0]) = make_float2(hn[0], hn[1]);
+    __syncwarp();
+    cur ^= 1;
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int g = 0; g < 3; ++g) xc[u][g] = xn[u][g];
+  }
+  fin[int64_t(r0) * 2 * H + d * H + j] = sh[wl][cur][j][0];  // final_state (layers.cpp:389-399)
+  if (ok1) fin[int64_t(r0 + 1) * 2 * H + d * H + j] = sh[wl][cur][j][1];
+}
+
 // g = det_softmax(logits) ; loss term ; g[tgt] -= 1   (training.cpp:28-34)
 __global__ void k_sprm_ce(SprmP s, const uint32_t* __restrict__ tokens,
                           const int64_t* __restrict__ pos, const float* __restrict__ logits,
@@ -233,6 +323,98 @@ __global__ void __launch_bounds__(256) k_sprm_bptt(SprmP s, const float* __restr
   }
 }
 
+// H == 32 BPTT: two rows per warp as one paired dh chain, the step's tape values
+// prefetched one step ahead. Same per-element operations and order as k_sprm_bptt.
+__global__ void __launch_bounds__(256) k_sprm_bptt32(SprmP s, const float* __restrict__ tape,
+                                                     const float* __restrict__ dfin, float* Gt) {
+  constexpr int H = 32;
+  __shared__ float swt[3][H][H + 1];                // [gate][q][j] = W_h{gate}[j][q]
+  __shared__ __align__(16) float sg[8][3][H][2];    // dhh, dar, daz of this step, per row
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = blockIdx.x & 1;
+  const int r0 = ((blockIdx.x >> 1) * 8 + wl) * 2;
+  const int T = s.T, R = s.R;
+  const float* W = s.w;
+  for (int i = threadIdx.x; i < 3 * H * H; i += blockDim.x) {
+    const int gate = i / (H * H), rem = i % (H * H), jj = rem / H, q = rem % H;
+    const float* Wg = W + goff(s.offs, d, gate == 0 ? WHN : gate == 1 ? WHR : WHZ);
+    swt[gate][q][jj] = Wg[int64_t(jj) * H + q];
+  }
+  __syncthreads();
+  if (r0 >= R) return;
+  const bool ok1 = r0 + 1 < R;
+  const int j = lane;
+  const int64_t TRH = int64_t(T) * R * H;
+  const float* tp[5];
+#pragma unroll
+  for (int g = 0; g < 5; ++g) tp[g] = tape + (int64_t(g * 2 + d) * TRH);
+  float* gan = Gt + int64_t(0 * 2 + d) * TRH;
+  float* gar = Gt + int64_t(1 * 2 + d) * TRH;
+  float* gaz = Gt + int64_t(2 * 2 + d) * TRH;
+  float* ghh = Gt + int64_t(3 * 2 + d) * TRH;
+  float* ghp = Gt + int64_t(4 * 2 + d) * TRH;
+  const int rr[2] = {r0, ok1 ? r0 + 1 : r0};
+  float dlast[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) dlast[u] = fadd(0.0f, dfin[int64_t(rr[u]) * 2 * H + d * H + j]);
+  // tape values of step t for both rows: r, z, n, hh, hprev
+  auto fetch = [&](int t, float (&x)[2][5]) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t o = (int64_t(t) * R + rr[u]) * H + j;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) x[u][g] = tp[g][o];
+      x[u][4] = t == 0 ? 0.0f : tp[4][o - int64_t(R) * H];
+    }
+  };
+  float xc[2][5], xn[2][5];
+  fetch(T - 1, xc);
+  float dh[2] = {0.0f, 0.0f};
+  for (int t = T - 1; t >= 0; --t) {
+    if (t > 0) fetch(t - 1, xn);
+    float dn[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      dh[u] = fadd(dh[u], t == T - 1 ? dlast[u] : 0.0f);  // gather_add_step(dout, t, dh)
+      const float rv = xc[u][0], zv = xc[u][1], nv = xc[u][2], hhv = xc[u][3], hprev = xc[u][4];
+      const float dzv = fmul(dh[u], fsub(hprev, nv));
+      const float danv = fmul(fmul(dh[u], fsub(1.0f, zv)), fsub(1.0f, fmul(nv, nv)));
+      const float dar = fmul(fmul(fmul(danv, hhv), rv), fsub(1.0f, rv));
+      const float daz = fmul(fmul(dzv, zv), fsub(1.0f, zv));
+      const float dhh = fmul(danv, rv);
+      dn[u] = fmul(dh[u], zv);
+      if (u == 0 || ok1) {
+        const int64_t o = (int64_t(t) * R + rr[u]) * H + j;
+        gan[o] = danv;
+        gar[o] = dar;
+        gaz[o] = daz;
+        ghh[o] = dhh;
+        ghp[o] = hprev;
+      }
+      sg[wl][0][j][u] = dhh;
+      sg[wl][1][j][u] = dar;
+      sg[wl][2][j][u] = daz;
+    }
+    __syncwarp();
+    // dh_next = dh*z + dhh.W_hn^T + dar.W_hr^T + daz.W_hz^T  (layers.cpp:306-308)
+    f2_t acc = f2_pack(dn[0], dn[1]);
+#pragma unroll
+    for (int g = 0; g < 3; ++g)
+#pragma unroll
+      for (int q = 0; q < H; ++q) {
+        const float2 v = *reinterpret_cast<const float2*>(&sg[wl][g][q][0]);
+        acc = f2_mac(acc, f2_pack(v.x, v.y), f2_bcast(swt[g][q][j]));
+      }
+    __syncwarp();
+    dh[0] = f2_lo(acc);
+    dh[1] = f2_hi(acc);
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int g = 0; g < 5; ++g) xc[u][g] = xn[u][g];
+  }
+}
+
 // Gt[g][d][t][r][j] -> G[g][d][j][k], k = (T-1-t)*R + r (32x32 smem tiles)
 __global__ void k_sprm_transpose(SprmP s, const float* __restrict__ Gt, float* G) {
   __shared__ float tile[32][33];
@@ -328,6 +510,10 @@ void launch_sprm_prep(const uint32_t* tokens, const int64_t* pos, const SprmP& s
 }
 void launch_sprm_fwd(const SprmP& s, const uint32_t* ctx, const float* tab, float* tape, float* fin,
                      cudaStream_t st) {
+  if (s.H == 32) {
+    k_sprm_fwd32<<<unsigned(2 * ((s.R + 15) / 16)), 256, 0, st>>>(s, ctx, tab, tape, fin);
+    return;
+  }
   k_sprm_fwd<<<unsigned(2 * ((s.R + 7) / 8)), 256, 0, st>>>(s, ctx, tab, tape, fin);
 }
 void launch_sprm_ce(const SprmP& s, const uint32_t* tokens, const int64_t* pos, const float* logits,
@@ -339,7 +525,10 @@ void launch_sprm_tanh_grad(float* dbact, const float* bact, int64_t n, cudaStrea
 }
 void launch_sprm_bptt(const SprmP& s, const float* tape, const float* dfin, float* Gt, float* G,
                       cudaStream_t st) {
-  k_sprm_bptt<<<unsigned(2 * ((s.R + 7) / 8)), 256, 0, st>>>(s, tape, dfin, Gt);
+  if (s.H == 32)
+    k_sprm_bptt32<<<unsigned(2 * ((s.R + 15) / 16)), 256, 0, st>>>(s, tape, dfin, Gt);
+  else
+    k_sprm_bptt<<<unsigned(2 * ((s.R + 7) / 8)), 256, 0, st>>>(s, tape, dfin, Gt);
   const int64_t RT = int64_t(s.R) * s.T;
   dim3 grid(unsigned((RT + 31) / 32), unsigned((s.H + 31) / 32), 10);
   k_sprm_transpose<<<grid, dim3(32, 8), 0, st>>>(s, Gt, G);
