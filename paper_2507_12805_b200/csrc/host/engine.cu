@@ -92,6 +92,43 @@ struct Stream {
   }
 };
 
+// A second stream that forks from / joins into the engine stream by events
+// (works both eagerly and under stream capture, where it becomes graph branches).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  std::vector<cudaEvent_t> evs;
+  size_t next = 0;
+  SideStream() { CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  ~SideStream() {
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+  }
+  // events are reused from tick to tick (rewind()); a wait binds to the
+  // record that precedes it, so reuse after the wait was enqueued is safe
+  cudaEvent_t ev() {
+    if (next == evs.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      evs.push_back(e);
+    }
+    return evs[next++];
+  }
+  void rewind() { next = 0; }
+  void wait_for(cudaStream_t main) {  // side continues after main's work so far
+    cudaEvent_t e = ev();
+    CK(cudaEventRecord(e, main));
+    CK(cudaStreamWaitEvent(s, e, 0));
+  }
+  void join_into(cudaStream_t main) {  // main continues after side's work so far
+    cudaEvent_t e = ev();
+    CK(cudaEventRecord(e, s));
+    CK(cudaStreamWaitEvent(main, e, 0));
+  }
+};
+
 struct Event {
   cudaEvent_t e = nullptr;
   Event() { CK(cudaEventCreate(&e)); }
@@ -427,8 +464,16 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   const int nh = int(max_hand);
   const TickDesc* act = d_td.p;
   uint64_t tick_launches = 0;
+  // Side stream for the work of a tick that is independent of the main chain:
+  // the static predictors (need only ctx) run beside the DM forward, and each
+  // weight-gradient product runs beside the data-gradient chain once its input
+  // exists. Fork/join by events, so the captured graph gets parallel branches.
+  SideStream side;
+  auto to_side = [&]() { side.wait_for(st); };
+  auto from_side = [&]() { side.join_into(st); };
   auto enqueue_tick = [&](int64_t probe_tick) {
     const uint64_t l0 = run.launches;
+    side.rewind();
     launch_tick_advance(d_td.p, d_act_ptr.p, d_act.p, d_hand_ptr.p, d_hand.p, sch.ticks, st);
     ++run.launches;
     if (nh > 0) {
@@ -443,6 +488,18 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     launch_embed(d_tokens, geo, w.p, P, oE, oP, ctx.p, s_ctx, x.p, s_x, xl.p, s_re, dd, act, na,
                  st);
     ++run.launches;
+    // ---------------- static predictors (side stream, beside the DM forward)
+    if (run.flags & 3) {
+      to_side();
+      if (run.flags & 1) {
+        run.launches += launch_bigru_predict(run.pub->params(R), ctx.p, s_ctx, bwork.p, s_bw, lu.p,
+                                             s_rv, act, na, side.s);
+      }
+      if (run.flags & 2) {
+        run.launches += launch_bigru_predict(run.priv->params(R), ctx.p, s_ctx, bwork.p, s_bw, lr.p,
+                                             s_rv, act, na, side.s);
+      }
+    }
     GemmP gp{};
     // K, V over all R*T rows, q over the last position (layers.cpp:437-445)
     // x is feature-major: A(row, e) = xT[e*RT + row]
@@ -470,15 +527,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     gemm(GemmP{fo.p, s_rh, H, W_(DmLayout::HW), P, V, lm.p, s_rv, V, W_(DmLayout::HB), P, nullptr,
                0, 0, R, V, H, 0, 1, 0},
          false, false);
-    // ---------------- static predictors
-    if (run.flags & 1) {
-      launch_bigru_predict(run.pub->params(R), ctx.p, s_ctx, bwork.p, s_bw, lu.p, s_rv, act, na, st);
-      run.launches += 3 * run.pub->host.layers + 1;
-    }
-    if (run.flags & 2) {
-      launch_bigru_predict(run.priv->params(R), ctx.p, s_ctx, bwork.p, s_bw, lr.p, s_rv, act, na, st);
-      run.launches += 3 * run.priv->host.layers + 1;
-    }
+    if (run.flags & 3) from_side();
     // ---------------- mix + quantize + code
     MixP mp{lu.p, lr.p, lm.p, s_rv, probs.p, freq.p, cum.p, s_rv, s_cum, w.p, P, oA, sc.p,
             int(run.flags), R, V, err.p};
@@ -503,28 +552,39 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     launch_bc_dlm(bp, act, na, st);
     launch_alpha_step(bp, act, na, st);
     run.launches += 2;
-    // head, ffn, attention output projection (Linear::backward, layers.cpp:176-183)
-    gemm(GemmP{fo.p, s_rh, H, dlm.p, s_rv, V, G_(DmLayout::HW), P, V, nullptr, 0, nullptr, 0, 0, H,
-               V, R, 1, 2, 0},
-         true, false);
+    // head, ffn, attention output projection (Linear::backward, layers.cpp:176-183).
+    // Data gradients stay on the main stream; each weight gradient goes to the
+    // side stream as soon as its operands exist (they write disjoint slices of
+    // g that nothing reads before Adam).
+    auto side_gemm = [&](GemmP p, bool at, bool bt) {
+      launch_gemm(p, at, bt, act, na, side.s);
+      ++run.launches;
+    };
+    to_side();
+    side_gemm(GemmP{fo.p, s_rh, H, dlm.p, s_rv, V, G_(DmLayout::HW), P, V, nullptr, 0, nullptr, 0, 0,
+                    H, V, R, 1, 2, 0},
+              true, false);
     gemm(GemmP{dlm.p, s_rv, V, W_(DmLayout::HW), P, V, dffn.p, s_rh, H, nullptr, 0, nullptr, 0, 0,
                R, H, V, 0, 0, 0},
          false, true);
-    gemm(GemmP{pre.p, s_rf, F, dffn.p, s_rh, H, G_(DmLayout::UW), P, H, nullptr, 0, nullptr, 0, 0,
-               F, H, R, 1, 2, 1},
-         true, false);
+    to_side();
+    side_gemm(GemmP{pre.p, s_rf, F, dffn.p, s_rh, H, G_(DmLayout::UW), P, H, nullptr, 0, nullptr, 0,
+                    0, F, H, R, 1, 2, 1},
+              true, false);
     gemm(GemmP{dffn.p, s_rh, H, W_(DmLayout::UW), P, H, dact.p, s_rf, F, nullptr, 0, pre.p, s_rf, F,
                R, F, H, 0, 0, 0},
          false, true);
-    gemm(GemmP{ao.p, s_rh, H, dact.p, s_rf, F, G_(DmLayout::IW), P, F, nullptr, 0, nullptr, 0, 0, H,
-               F, R, 1, 2, 0},
-         true, false);
+    to_side();
+    side_gemm(GemmP{ao.p, s_rh, H, dact.p, s_rf, F, G_(DmLayout::IW), P, F, nullptr, 0, nullptr, 0,
+                    0, H, F, R, 1, 2, 0},
+              true, false);
     gemm(GemmP{dact.p, s_rf, F, W_(DmLayout::IW), P, F, datt.p, s_rh, H, nullptr, 0, nullptr, 0, 0,
                R, H, F, 0, 0, 0},
          false, true);
-    gemm(GemmP{cx.p, s_rh, H, datt.p, s_rh, H, G_(DmLayout::OW), P, H, nullptr, 0, nullptr, 0, 0, H,
-               H, R, 1, 2, 0},
-         true, false);
+    to_side();
+    side_gemm(GemmP{cx.p, s_rh, H, datt.p, s_rh, H, G_(DmLayout::OW), P, H, nullptr, 0, nullptr, 0,
+                    0, H, H, R, 1, 2, 0},
+              true, false);
     gemm(GemmP{datt.p, s_rh, H, W_(DmLayout::OW), P, H, dctx.p, s_rh, H, nullptr, 0, nullptr, 0, 0,
                R, H, H, 0, 0, 0},
          false, true);
@@ -533,17 +593,18 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     ++run.launches;
     // q/k/v projections: weight+bias grads, then dx = dk Wk^T + dv Wv^T, dxl = dq Wq^T
     // dWk|dbk and dWv|dbv: reductions over all R*T rows of feature-major x, dk, dv
+    to_side();
     {
       const NtP pk{x.p, dk.p, G_(DmLayout::KW), s_x, s_kv, P, RT, RT, H, E, H, int(RT)};
       NtP pv = pk;
       pv.B = dv.p;
       pv.C = G_(DmLayout::VW);
-      launch_gemm_nt(pk, &pv, act, na, st);
+      launch_gemm_nt(pk, &pv, act, na, side.s);
       ++run.launches;
     }
-    gemm(GemmP{xl.p, s_re, E, dq.p, s_rh, H, G_(DmLayout::QW), P, H, nullptr, 0, nullptr, 0, 0, E,
-               H, R, 1, 2, 0},
-         true, false);
+    side_gemm(GemmP{xl.p, s_re, E, dq.p, s_rh, H, G_(DmLayout::QW), P, H, nullptr, 0, nullptr, 0, 0,
+                    E, H, R, 1, 2, 0},
+              true, false);
     // dx = dk Wk^T + dv Wv^T (k terms then v terms), dk/dv feature-major
     gemm(GemmP{dk.p, s_kv, RT, W_(DmLayout::KW), P, H, dx.p, s_x, E, nullptr, 0, nullptr, 0, 0,
                R * T, E, H, 0, 0, 0},
@@ -556,6 +617,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
          false, true);
     launch_embed_bwd(ctx.p, s_ctx, dx.p, s_x, dxl.p, s_re, g.p, P, oE, oP, dd, act, na, st);
     run.launches += 2;
+    from_side();
     // Adam over every DM parameter (alpha was updated by k_alpha_step)
     launch_adam(w.p, g.p, m.p, v.p, P, P - 1, sc.p, act, na, st);
     ++run.launches;

@@ -133,6 +133,139 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
   }
 }
 
+__device__ __forceinline__ void rec_cp_async4(float* smem, const float* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+
+// Layer >= 1 with the input projection fused in (Hs == 32, input width 64):
+// per step each lane forms xi_g = b_ig + in . W_ig (k ascending, exactly the
+// GEMM's chain) for its unit and the warp's 4 rows, then runs the recurrence
+// as k_bigru_rec<32>. The step's input rows (the previous layer's output at
+// the direction's time index) are prefetched one step ahead by cp.async into a
+// per-warp [k][row] buffer, so one broadcast LDS.128 feeds two row pairs.
+// No xi buffer round trip through HBM; `out` may be null (last layer: only
+// the final state is consumed).
+constexpr int kFuseHs = 32, kFuseIn = 64;
+constexpr size_t kFuseSmem =
+    sizeof(float) * (size_t(3) * kFuseHs * kFuseHs + size_t(3) * kFuseIn * kFuseHs +
+                     size_t(kRecWarps) * 2 * 32 * kRPW + size_t(kRecWarps) * 2 * kFuseIn * kRPW);
+__global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec_fused(
+    BiGruP p, int l, const float* __restrict__ in, float* out, float* fin, int64_t work_cs,
+    const TickDesc* __restrict__ td) {
+  constexpr int HS = kFuseHs, IN = kFuseIn;
+  extern __shared__ __align__(16) float fsm[];
+  float (*sw)[HS][HS] = reinterpret_cast<float (*)[HS][HS]>(fsm);                    // [3][q][j]
+  float (*swi)[IN][HS] = reinterpret_cast<float (*)[IN][HS]>(fsm + 3 * HS * HS);     // [3][k][j]
+  float (*sh)[2][32][kRPW] =
+      reinterpret_cast<float (*)[2][32][kRPW]>(fsm + 3 * HS * HS + 3 * IN * HS);     // [w][cur][q][u]
+  float (*sin)[2][IN][kRPW] = reinterpret_cast<float (*)[2][IN][kRPW]>(
+      fsm + 3 * HS * HS + 3 * IN * HS + kRecWarps * 2 * 32 * kRPW);                 // [w][buf][k][u]
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int dir = blockIdx.x & 1;
+  const int grp = (blockIdx.x >> 1) * kRecWarps + wl;
+  const int T = p.T;
+  const float* W = p.w;
+  for (int i = threadIdx.x; i < 3 * HS * HS; i += blockDim.x) {
+    const int gate = i / (HS * HS), rem = i % (HS * HS);
+    sw[gate][rem / HS][rem % HS] = W[poff(p.offs, l, dir, WHR + gate) + rem];
+  }
+  for (int i = threadIdx.x; i < 3 * IN * HS; i += blockDim.x) {
+    const int gate = i / (IN * HS), rem = i % (IN * HS);
+    swi[gate][rem / HS][rem % HS] = W[poff(p.offs, l, dir, WIR + gate) + rem];
+  }
+  __syncthreads();
+  const int r0 = grp * kRPW;
+  if (r0 >= p.R) return;
+  const int j = lane;
+  const float bhr = W[poff(p.offs, l, dir, BHR) + j], bhz = W[poff(p.offs, l, dir, BHZ) + j],
+              bhn = W[poff(p.offs, l, dir, BHN) + j];
+  const float bir = W[poff(p.offs, l, dir, BIR) + j], biz = W[poff(p.offs, l, dir, BIZ) + j],
+              bin = W[poff(p.offs, l, dir, BIN) + j];
+  bool rv_ok[kRPW];
+  int rr[kRPW];
+#pragma unroll
+  for (int u = 0; u < kRPW; ++u) {
+    rv_ok[u] = r0 + u < p.R;
+    rr[u] = rv_ok[u] ? r0 + u : r0;
+  }
+  const float* inc = in + c * work_cs;
+  auto prefetch = [&](int step, int buf) {
+    const int tt = dir ? (T - 1 - step) : step;
+#pragma unroll
+    for (int i = 0; i < 2 * kRPW; ++i) {
+      const int u = i >> 1, k = lane + 32 * (i & 1);
+      rec_cp_async4(&sin[wl][buf][k][u], inc + (int64_t(rr[u]) * T + tt) * IN + k);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  *reinterpret_cast<float4*>(&sh[wl][0][j][0]) = make_float4(0.f, 0.f, 0.f, 0.f);  // h0 = 0
+  prefetch(0, 0);
+  int cur = 0;
+  for (int step = 0; step < T; ++step) {
+    const int tt = dir ? (T - 1 - step) : step;
+    const int buf = step & 1;
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncwarp();  // this step's inputs and h landed for every lane
+    if (step + 1 < T) prefetch(step + 1, buf ^ 1);
+    // input projections (GEMM chain order: bias, then k ascending)
+    f2_t xr01 = f2_bcast(bir), xr23 = f2_bcast(bir), xz01 = f2_bcast(biz), xz23 = f2_bcast(biz);
+    f2_t xn01 = f2_bcast(bin), xn23 = f2_bcast(bin);
+#pragma unroll 8
+    for (int k = 0; k < IN; ++k) {
+      const float4 iv = *reinterpret_cast<const float4*>(&sin[wl][buf][k][0]);
+      const f2_t i01 = f2_pack(iv.x, iv.y), i23 = f2_pack(iv.z, iv.w);
+      const f2_t wr = f2_bcast(swi[0][k][j]), wz = f2_bcast(swi[1][k][j]), wn = f2_bcast(swi[2][k][j]);
+      xr01 = f2_mac(xr01, i01, wr);
+      xr23 = f2_mac(xr23, i23, wr);
+      xz01 = f2_mac(xz01, i01, wz);
+      xz23 = f2_mac(xz23, i23, wz);
+      xn01 = f2_mac(xn01, i01, wn);
+      xn23 = f2_mac(xn23, i23, wn);
+    }
+    f2_t ar01 = f2_add(xr01, f2_bcast(bhr)), ar23 = f2_add(xr23, f2_bcast(bhr));
+    f2_t az01 = f2_add(xz01, f2_bcast(bhz)), az23 = f2_add(xz23, f2_bcast(bhz));
+    f2_t hh01 = f2_bcast(bhn), hh23 = f2_bcast(bhn);
+#pragma unroll 8
+    for (int q = 0; q < HS; ++q) {
+      const float4 hv = *reinterpret_cast<const float4*>(&sh[wl][cur][q][0]);
+      const f2_t h01 = f2_pack(hv.x, hv.y), h23 = f2_pack(hv.z, hv.w);
+      const f2_t wr = f2_bcast(sw[0][q][j]), wz = f2_bcast(sw[1][q][j]);
+      const f2_t wn = f2_bcast(sw[2][q][j]);
+      ar01 = f2_mac(ar01, h01, wr);
+      ar23 = f2_mac(ar23, h23, wr);
+      az01 = f2_mac(az01, h01, wz);
+      az23 = f2_mac(az23, h23, wz);
+      hh01 = f2_mac(hh01, h01, wn);
+      hh23 = f2_mac(hh23, h23, wn);
+    }
+    const float arv[kRPW] = {f2_lo(ar01), f2_hi(ar01), f2_lo(ar23), f2_hi(ar23)};
+    const float azv[kRPW] = {f2_lo(az01), f2_hi(az01), f2_lo(az23), f2_hi(az23)};
+    const float hhv[kRPW] = {f2_lo(hh01), f2_hi(hh01), f2_lo(hh23), f2_hi(hh23)};
+    const float anv[kRPW] = {f2_lo(xn01), f2_hi(xn01), f2_lo(xn23), f2_hi(xn23)};
+    const float4 hp = *reinterpret_cast<const float4*>(&sh[wl][cur][j][0]);
+    const float hprev[kRPW] = {hp.x, hp.y, hp.z, hp.w};
+    float hn[kRPW];
+#pragma unroll
+    for (int u = 0; u < kRPW; ++u) {
+      const float rv = det_sigmoid(arv[u]), zv = det_sigmoid(azv[u]);
+      const float nv = det_tanh(fadd(anv[u], fmul(rv, hhv[u])));
+      hn[u] = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, hprev[u]));
+      if (out && rv_ok[u]) out[c * work_cs + (int64_t(r0 + u) * T + tt) * 2 * HS + dir * HS + j] = hn[u];
+    }
+    *reinterpret_cast<float4*>(&sh[wl][cur ^ 1][j][0]) = make_float4(hn[0], hn[1], hn[2], hn[3]);
+    cur ^= 1;
+  }
+  __syncwarp();
+  if (fin) {
+#pragma unroll
+    for (int u = 0; u < kRPW; ++u)
+      if (rv_ok[u]) fin[c * work_cs + int64_t(r0 + u) * 2 * HS + dir * HS + j] = sh[wl][cur][j][u];
+  }
+}
+
 // Generic recurrence (any Hs; lane owns units j, j+32, ...; weights via L1).
 __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec_generic(
     BiGruP p, int l, const uint32_t* __restrict__ ctx, int64_t ctx_cs, const float* __restrict__ xi,
@@ -214,10 +347,11 @@ size_t bigru_work_floats(const BiGruP& p) {
   return 6 * RT * p.Hs + 2 * RT * 2 * p.Hs + size_t(p.R) * 2 * p.Hs + size_t(p.R) * p.B;
 }
 
-void launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, float* work,
+int launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, float* work,
                           int64_t work_cs, float* logits, int64_t lg_cs, const TickDesc* td,
                           int max_active, cudaStream_t st) {
-  if (max_active <= 0) return;
+  if (max_active <= 0) return 0;
+  int launches = 0;
   const int64_t RT = int64_t(p.R) * p.T, H = p.Hs;
   float* xi = work;
   float* outs[2] = {xi + 6 * RT * H, xi + 6 * RT * H + RT * 2 * H};
@@ -226,7 +360,26 @@ void launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, 
   const dim3 rgrid(unsigned((p.R * 2 + kRecWarps - 1) / kRecWarps), max_active);
   const int ngroups = (p.R + kRPW - 1) / kRPW;
   const dim3 rgrid2(unsigned(2 * ((ngroups + kRecWarps - 1) / kRecWarps)), max_active);
+  const bool fuse = p.Hs == kFuseHs;
+  if (fuse) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_bigru_rec_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(kFuseSmem));
+      attr = true;
+    }
+  }
   for (int l = 0; l < p.layers; ++l) {
+    const bool last = l == p.layers - 1;
+    float* f = last ? fin : nullptr;
+    if (l > 0 && fuse) {
+      // projection fused into the recurrence; the last layer's per-step
+      // outputs are never read (the head consumes the final state only)
+      k_bigru_rec_fused<<<rgrid2, kRecWarps * 32, kFuseSmem, st>>>(
+          p, l, outs[(l - 1) & 1], last ? nullptr : outs[l & 1], f, work_cs, td);
+      ++launches;
+      continue;
+    }
     float* out = outs[l & 1];
     if (l > 0) {
       // x-projections of layer l for every position: 3 gates per direction,
@@ -253,9 +406,9 @@ void launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, 
         gp.c_ps = RT * H;
         gp.bias_ps = H;               // b_ir, b_iz, b_in consecutive
         launch_gemm(gp, false, false, td, max_active, st);
+        ++launches;
       }
     }
-    float* f = (l == p.layers - 1) ? fin : nullptr;
     const float* xl = l == 0 ? nullptr : xi;
     if (p.Hs == 32)
       k_bigru_rec<32><<<rgrid2, kRecWarps * 32, 0, st>>>(p, l, ctx, ctx_cs, xl, out, f, work_cs, td);
@@ -266,6 +419,7 @@ void launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, 
     else
       k_bigru_rec_generic<<<rgrid, kRecWarps * 32, kRecWarps * 2 * p.Hs * sizeof(float), st>>>(
           p, l, ctx, ctx_cs, xl, out, f, work_cs, td);
+    ++launches;
   }
   // bott = tanh(bott.b + fin . bott.w);  logits = out.b + bott . out.w
   const int b0 = 1 + p.layers * 2 * NG;
@@ -301,6 +455,7 @@ void launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, 
   g2.K = p.B;
   g2.init = 1;
   launch_gemm(g2, false, false, td, max_active, st);
+  return launches + 3;  // + bottleneck GEMM, tanh, output GEMM
 }
 
 }  // namespace pmklc_b200

@@ -192,7 +192,8 @@ struct BiGruP {
   const float* xi0;     // device table [2][3][V][Hs]
   int layers, V, T, Es, Hs, B, R;
 };
-void launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, float* work,
+// returns the number of kernels launched
+int launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, float* work,
                           int64_t work_cs, float* logits, int64_t lg_cs, const TickDesc* td,
                           int max_active, cudaStream_t st);
 size_t bigru_work_floats(const BiGruP& p);
