@@ -239,11 +239,11 @@ def main():
             if rank == 0:
                 assert len(out) == n
         c_ms, d_ms = e0.elapsed_time(e1), e1b.elapsed_time(e2)
-        return blob, c_ms, d_ms, tm_c.kernel_launches + tm_d.kernel_launches
+        return blob, c_ms, d_ms, tm_c.kernel_launches + tm_d.kernel_launches, (tm_c, tm_d)
 
     clk = Clocks(dev).start()
     # correctness of the measured path: lossless round trip
-    blob, _, _, _ = run_step(False)
+    blob, _, _, _, _ = run_step(False)
     if ctx is None:
         assert P.decompress(blob, spum, device=dev) == raw, "round trip mismatch"
     else:
@@ -256,10 +256,16 @@ def main():
 
     ct = dt = 0.0
     launches = 0
+    hot = {"ms": 0.0, "launches": 0, "units": 0, "flops": 0.0}
     with clk:
         for _ in range(args.steps):
             flush_l2(torch, flush)
-            blob, c_ms, d_ms, l = run_step(True)
+            blob, c_ms, d_ms, l, tms = run_step(True)
+            for tm in tms:  # dominant kernel, timed on the device inside the timed region
+                hot["ms"] += tm.hot_ms
+                hot["launches"] += tm.hot_launches
+                hot["units"] += tm.hot_units
+                hot["flops"] += tm.hot_flops_per_unit * tm.hot_units
             if world > 1:  # max over ranks, per phase
                 tt = torch.tensor([c_ms, d_ms], dtype=torch.float64)
                 torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -297,21 +303,49 @@ def main():
 
     line = None
     if rank == 0:
-        # roofline: top kernel of the launch list (k_gemm_nt, dWk|dWv over R*t rows),
-        # live CUDA-event timing at the workload's concurrency, against the
-        # measured non-FMA FP32 issue peak (MEASURED_PEAKS.json has no FP32 figure)
-        chunks = min(args.workers, 64)
-        k_ms, k_fl, k_by = P.bench_kernel("gemm_nt", chunks, iters=10, device=dev)
+        # roofline of the dominant kernel. With the public model (the default
+        # workload) that is the SPuM layer-1 fused BiGRU recurrence, timed on
+        # the device around every launch inside the timed steps (stamp kernels
+        # on its own stream; in-situ, so co-running DM kernels are included).
+        # Bound: exact non-FMA FP32 issue (no tensor cores in EXACT mode); the
+        # peak is a live FP32 microbenchmark (MEASURED_PEAKS.json has no FP32
+        # figure).
         p_ms, p_fl, _ = P.bench_kernel("fp32_peak", 1, iters=10, device=dev)
         peak_tf = p_fl / (p_ms / 1000.0) / 1e12
-        ach_tf = k_fl / (k_ms / 1000.0) / 1e12
         traffic = None
-        tf = ROOT / "profiles" / "roofline_traffic.json"
-        if tf.exists():
+        tfile = ROOT / "profiles" / "roofline_traffic.json"
+        tjson = {}
+        if tfile.exists():
             try:
-                traffic = json.loads(tf.read_text()).get("gemm_nt_dram_bytes_per_launch")
+                tjson = json.loads(tfile.read_text())
             except Exception:
-                traffic = None
+                tjson = {}
+        if hot["launches"]:
+            ach_tf = hot["flops"] / (hot["ms"] / 1000.0) / 1e12
+            units_per_launch = hot["units"] / hot["launches"]
+            t = tjson.get("k_bigru_rec_fused")
+            if t and t.get("units"):  # DRAM bytes per chunk-launch x this run's chunks per launch
+                traffic = t["dram_bytes_per_launch"] / t["units"] * units_per_launch
+            roof = {"kernel": "k_bigru_rec_fused (SPuM BiGRU layer 1: input projection + "
+                              "recurrence, R=320 rows x 2 dirs x t=32 steps per chunk)",
+                    "bound": "fp32", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                    "frac": ach_tf / peak_tf, "traffic": traffic,
+                    "timing": "in-situ %globaltimer stamps around every launch in the timed steps",
+                    "avg_launch_ms": hot["ms"] / hot["launches"],
+                    "chunks_per_launch": units_per_launch,
+                    "flops_per_launch": hot["flops"] / hot["launches"],
+                    "flops_per_chunk_launch": hot["flops"] / max(hot["units"], 1),
+                    "peak_source": "live non-FMA FP32 microbenchmark (MEASURED_PEAKS.json has no "
+                                   "FP32 figure); EXACT mode cannot use tensor cores"}
+        else:  # DM only: the weight-gradient reduction, microbenchmarked live
+            chunks = min(args.workers, 64)
+            k_ms, k_fl, k_by = P.bench_kernel("gemm_nt", chunks, iters=10, device=dev)
+            ach_tf = k_fl / (k_ms / 1000.0) / 1e12
+            roof = {"kernel": f"k_gemm_nt (dWk|dbk + dWv|dbv over R*t=10240 rows, {chunks} chunks)",
+                    "bound": "fp32", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                    "frac": ach_tf / peak_tf, "traffic": tjson.get("gemm_nt_dram_bytes_per_launch"),
+                    "avg_launch_ms": k_ms, "flops_per_launch": k_fl,
+                    "peak_source": "live non-FMA FP32 microbenchmark"}
         cpu = None
         if not args.skip_cpu and world == 1:
             threads = min(os.cpu_count() or 1, 256, args.workers)
@@ -333,13 +367,7 @@ def main():
             "decompress_MBps": n * args.steps / 1e6 / (dt / 1000.0),
             "bits_per_base": 8.0 * len(blob) / n,
             "container_bytes": len(blob),
-            "roofline": {"kernel": "k_gemm_nt (dWk|dbk + dWv|dbv over R*t=10240 rows, "
-                                   f"{chunks} chunks)",
-                         "bound": "fp32", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": ach_tf / peak_tf, "traffic": traffic,
-                         "peak_source": "live non-FMA FP32 microbenchmark (MEASURED_PEAKS.json "
-                                        "has no FP32 figure); EXACT mode cannot use tensor cores",
-                         "avg_launch_ms": k_ms, "flops_per_launch": k_fl},
+            "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "MB/s", "h2d_bytes_per_step": n + len(blob),
                     "d2h_bytes_per_step": len(blob) + n},

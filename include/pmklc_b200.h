@@ -56,6 +56,12 @@ typedef struct pmklc_stats {
 typedef struct pmklc_timing {  /* CUDA-event times of the last call, ms */
   double total_ms, h2d_ms, tokenize_ms, warmup_ms, model_ms, d2h_ms;
   uint64_t ticks, kernel_launches, chunks, h2d_bytes, d2h_bytes;
+  /* dominant kernel (SPuM layer-1 fused BiGRU recurrence), timed on the device
+   * around every launch of the call: total ms, launches, chunk-launches
+   * processed, algorithmic FLOPs per chunk-launch (0 when not run) */
+  double hot_ms;
+  uint64_t hot_launches, hot_units;
+  double hot_flops_per_unit;
 } pmklc_timing;
 
 /* CompressConfig{} defaults: s=k=3, t=32, bs=320, workers=1, threshold 5e8,

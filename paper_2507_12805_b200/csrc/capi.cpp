@@ -75,8 +75,10 @@ void copy_stats(const std::vector<ChunkStats>& st, pmklc_stats* out, size_t cap)
 
 void copy_timing(const Timing& t, pmklc_timing* out) {
   if (!out) return;
-  *out = pmklc_timing{t.total_ms, t.h2d_ms, t.tokenize_ms, t.warmup_ms, t.model_ms, t.d2h_ms,
-                      t.ticks,    t.kernel_launches, t.chunks, t.h2d_bytes, t.d2h_bytes};
+  *out = pmklc_timing{t.total_ms,  t.h2d_ms,       t.tokenize_ms,     t.warmup_ms,
+                      t.model_ms,  t.d2h_ms,       t.ticks,           t.kernel_launches,
+                      t.chunks,    t.h2d_bytes,    t.d2h_bytes,       t.hot_ms,
+                      t.hot_launches, t.hot_units, t.hot_flops_per_unit};
 }
 
 int do_compress(const uint8_t* h, const uint8_t* d, size_t n, const pmklc_cfg* c, uint8_t** out,

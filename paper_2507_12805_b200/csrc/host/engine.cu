@@ -267,7 +267,20 @@ struct ChunkRun {
   std::vector<ChunkStats> stats;
   uint64_t launches = 0;
   double warm_ms = 0, model_ms = 0;
+  HotTimer hot{};  // in-situ timing of the SPuM fused recurrence
 };
+
+// Algorithmic work of one chunk-launch of k_bigru_rec_fused: R rows x 2
+// directions x t steps x 3 gates x Hs units x (2Hs input + Hs recurrent) MACs.
+void fill_hot(Timing& tm, const ChunkRun& run) {
+  tm.hot_ms = double(run.hot.ns) * 1e-6;
+  tm.hot_launches = run.hot.launches;
+  tm.hot_units = run.hot.units;
+  if (run.pub && run.hot.launches) {
+    const double H = double(run.pub->host.d.sh);
+    tm.hot_flops_per_unit = 2.0 * double(run.R) * 2.0 * double(run.t) * 3.0 * H * (2.0 * H + H);
+  }
+}
 
 // Host snapshot of a device state slot (for stats / snapshot hashes).
 DmState fetch_state(const DmLayout& L, const float* w, const float* m, const float* v,
@@ -355,6 +368,8 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   DBuf<float> lu((run.flags & 1) ? TW * s_rv : 0), lr((run.flags & 2) ? TW * s_rv : 0);
   int64_t s_bw = 0;
   DBuf<float> bwork;
+  DBuf<HotTimer> d_hot(1);
+  CK(cudaMemsetAsync(d_hot.p, 0, sizeof(HotTimer), st));
   if (run.flags & 3) {
     size_t mx = 0;
     if (run.pub) mx = std::max(mx, bigru_work_floats(run.pub->params(R)));
@@ -493,7 +508,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
       to_side();
       if (run.flags & 1) {
         run.launches += launch_bigru_predict(run.pub->params(R), ctx.p, s_ctx, bwork.p, s_bw, lu.p,
-                                             s_rv, act, na, side.s);
+                                             s_rv, act, na, side.s, d_hot.p);
       }
       if (run.flags & 2) {
         run.launches += launch_bigru_predict(run.priv->params(R), ctx.p, s_ctx, bwork.p, s_bw, lr.p,
@@ -684,6 +699,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   CK(cudaStreamSynchronize(st));
   run.warm_ms = Event::ms(e0, e1);
   run.model_ms = Event::ms(e1, e2);
+  CK(cudaMemcpy(&run.hot, d_hot.p, sizeof(HotTimer), cudaMemcpyDeviceToHost));
 
   int h_err = 0;
   CK(cudaMemcpy(&h_err, err.p, sizeof h_err, cudaMemcpyDeviceToHost));
@@ -1117,6 +1133,7 @@ Bytes compress_impl(const uint8_t* h_raw, const uint8_t* d_raw_in, size_t n, con
     tm.ticks = uint64_t(run.sch.ticks);
     tm.kernel_launches = run.launches + sprm_launches + 3;
     tm.chunks = W;
+    fill_hot(tm, run);
     tm.h2d_bytes = h2d;
     tm.d2h_bytes = out.size();
   }
@@ -1281,6 +1298,7 @@ void decompress_impl(const uint8_t* blob, size_t n, const std::string& pub_path,
     tm.ticks = uint64_t(run.sch.ticks);
     tm.kernel_launches = run.launches + 1;
     tm.chunks = W;
+    fill_hot(tm, run);
     tm.h2d_bytes = n;
   }
 }

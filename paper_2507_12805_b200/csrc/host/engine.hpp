@@ -35,6 +35,9 @@ struct Timing {
   double total_ms = 0, h2d_ms = 0, tokenize_ms = 0, warmup_ms = 0, model_ms = 0, d2h_ms = 0;
   uint64_t ticks = 0, kernel_launches = 0, chunks = 0;
   uint64_t h2d_bytes = 0, d2h_bytes = 0;
+  // dominant kernel (k_bigru_rec_fused, SPuM layer 1), timed in situ
+  double hot_ms = 0, hot_flops_per_unit = 0;
+  uint64_t hot_launches = 0, hot_units = 0;
 };
 
 struct CallOptions {

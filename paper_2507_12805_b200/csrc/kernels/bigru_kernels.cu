@@ -347,9 +347,27 @@ size_t bigru_work_floats(const BiGruP& p) {
   return 6 * RT * p.Hs + 2 * RT * 2 * p.Hs + size_t(p.R) * 2 * p.Hs + size_t(p.R) * p.B;
 }
 
+namespace {
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__global__ void k_hot_begin(HotTimer* h) { h->t0 = global_ns(); }
+__global__ void k_hot_end(HotTimer* h, const TickDesc* __restrict__ td) {
+  h->ns += global_ns() - h->t0;
+  h->units += unsigned(td->n_act);
+  h->launches += 1;
+}
+}  // namespace
+void launch_hot_begin(HotTimer* h, cudaStream_t st) { k_hot_begin<<<1, 1, 0, st>>>(h); }
+void launch_hot_end(HotTimer* h, const TickDesc* td, cudaStream_t st) {
+  k_hot_end<<<1, 1, 0, st>>>(h, td);
+}
+
 int launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, float* work,
                           int64_t work_cs, float* logits, int64_t lg_cs, const TickDesc* td,
-                          int max_active, cudaStream_t st) {
+                          int max_active, cudaStream_t st, HotTimer* hot) {
   if (max_active <= 0) return 0;
   int launches = 0;
   const int64_t RT = int64_t(p.R) * p.T, H = p.Hs;
@@ -375,9 +393,17 @@ int launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, f
     if (l > 0 && fuse) {
       // projection fused into the recurrence; the last layer's per-step
       // outputs are never read (the head consumes the final state only)
+      if (hot) {
+        launch_hot_begin(hot, st);
+        ++launches;
+      }
       k_bigru_rec_fused<<<rgrid2, kRecWarps * 32, kFuseSmem, st>>>(
           p, l, outs[(l - 1) & 1], last ? nullptr : outs[l & 1], f, work_cs, td);
       ++launches;
+      if (hot) {
+        launch_hot_end(hot, td, st);
+        ++launches;
+      }
       continue;
     }
     float* out = outs[l & 1];

@@ -192,10 +192,19 @@ struct BiGruP {
   const float* xi0;     // device table [2][3][V][Hs]
   int layers, V, T, Es, Hs, B, R;
 };
-// returns the number of kernels launched
+// In-situ timer for the dominant kernel: stamp kernels around its launch
+// accumulate %globaltimer nanoseconds and the active chunks it processed, over
+// every tick of a call (graph replays included).
+struct HotTimer {
+  unsigned long long t0, ns, units, launches;
+};
+void launch_hot_begin(HotTimer* h, cudaStream_t st);
+void launch_hot_end(HotTimer* h, const TickDesc* td, cudaStream_t st);
+// returns the number of kernels launched; `hot` (nullable) times the fused
+// layer >= 1 recurrence
 int launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, float* work,
                           int64_t work_cs, float* logits, int64_t lg_cs, const TickDesc* td,
-                          int max_active, cudaStream_t st);
+                          int max_active, cudaStream_t st, HotTimer* hot = nullptr);
 size_t bigru_work_floats(const BiGruP& p);
 
 // SPrM pre-pass (pretrain_private / train_pass, training.cpp:8-83): one-layer
