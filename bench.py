@@ -18,6 +18,7 @@ same workload.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -41,7 +42,9 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--mb", type=float, default=100.0, help="workload size in 10^6 bytes")
     ap.add_argument("--workers", type=int, default=128, help="data blocks W")
-    ap.add_argument("--no-spum", action="store_true", help="dynamic model only (flags 4)")
+    ap.add_argument("--no-spum", action="store_true", help="no public model")
+    ap.add_argument("--no-sprm-branch", action="store_true",
+                    help="skip the threshold-lowered SPrM+DM (flags 6) run of config 3")
     ap.add_argument("--skip-cpu", action="store_true", help="skip the cpu_baseline leg")
     return ap.parse_args()
 
@@ -56,9 +59,9 @@ def workload(args, tmpdir):
         spum = str(Path(tmpdir) / "spum_k3_t32_s4.bin")
         P.write_bigru(spum, 3, 32, 4, 0xACE3, layers=2)
         cfg.pub_model_path = spum
+    models = "DM only (flags 4)" if args.no_spum else "SPuM(seeded)+DM (flags 5, default selector)"
     desc = (f"config3: {n/1e6:g} MB synthetic genome (10 order-k Markov segments k=2..5 + 1% "
-            f"repeats), PMKLC-S W={args.workers} blocks, "
-            f"{'DM only (flags 4)' if args.no_spum else 'SPuM(seeded)+DM (flags 5)'}, "
+            f"repeats), PMKLC-S W={args.workers} blocks, {models}, "
             f"s=k=3 t=32 bs=320 scale=4 smp=0.05")
     return raw, cfg, spum, desc
 
@@ -126,36 +129,50 @@ def flush_l2(torch, buf):
     buf.add_(1)  # 256 MiB write > 126 MB L2, between timed steps (not timed)
 
 
+def cpu_sample(raw, cfg, threads):
+    """Bounded sample of the workload for the host-CPU reference: `chunks`
+    blocks of `steps` batch steps (32 warm-up + the rest model steps). With the
+    private model the reference pre-trains it sequentially over the whole
+    sample (~130 ms per 320-token step on one core), so that sample is smaller
+    (2 blocks x 48 steps: ~100 pre-pass steps) to keep a step within ~30 s."""
+    if cfg.selector_threshold == 0:
+        chunks, steps = 2, 48
+    else:
+        chunks, steps = threads, 64
+    n = min(len(raw), chunks * 320 * 3 * steps)
+    return raw[:n], chunks, steps
+
+
 def cpu_reference(raw, cfg, spum, threads, reps, warm):
     """The reference library (oracle/_ref) on host cores over a bounded sample."""
     sys.path.insert(0, str(ROOT / "tests"))
     import oracles as O
     R = O.ref() if O.REF_SO.exists() else O.port()
     kind = "reference" if O.REF_SO.exists() else "port"
-    # sample: `threads` chunks of 64 batch steps each (same per-step cost as
-    # the full run: 32 warm-up + 32 model steps per chunk)
-    per_chunk = 320 * 3 * 64
-    n = min(len(raw), threads * per_chunk)
-    sample = raw[:n]
-    c = O.make_cfg(workers=threads, pub_path=spum or None)
+    sample, chunks, steps = cpu_sample(raw, cfg, threads)
+    n = len(sample)
+    c = O.make_cfg(workers=chunks, pub_path=spum or None, threshold=int(cfg.selector_threshold))
     times = []
     blob = b""
     for i in range(warm + reps):
         t0 = time.perf_counter()
         blob = R.compress(sample, c)
         t1 = time.perf_counter()
-        out = R.decompress(blob, pub_path=spum or None, workers=threads)
+        out = R.decompress(blob, pub_path=spum or None, workers=chunks)
         t2 = time.perf_counter()
         assert out == sample
         if i >= warm:
             times.append((t1 - t0, t2 - t1))
     ct = sum(t[0] for t in times) / len(times)
     dt = sum(t[1] for t in times) / len(times)
-    return {"value": n / 1e6 / (ct + dt), "unit": "MB/s", "cores": threads, "kind": kind,
-            "sample": f"first {n} B of the workload, W={threads} blocks x 64 batch steps, "
-                      f"{'SPuM+DM' if spum else 'DM'}; compress {ct:.2f} s + decompress {dt:.2f} s",
+    flags = blob[5] if len(blob) > 5 else 0
+    return {"value": n / 1e6 / (ct + dt), "unit": "MB/s", "cores": chunks, "kind": kind,
+            "sample": f"first {n} B of the workload, W={chunks} blocks x {steps} batch steps, "
+                      f"container flags {flags}; compress {ct:.2f} s + decompress {dt:.2f} s "
+                      f"(one host thread per block; the SPrM pre-pass is sequential)",
             "compress_MBps": n / 1e6 / ct, "decompress_MBps": n / 1e6 / dt,
-            "bits_per_base": 8.0 * len(blob) / n}
+            "bits_per_base": 8.0 * len(blob) / n,
+            "n": n}
 
 
 def main():
@@ -173,7 +190,7 @@ def main():
         r = cpu_reference(raw, cfg, spum, threads, args.steps, args.warmup)
         line = {"metric": METRIC, "value": r["value"], "unit": "MB/s", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1000.0 * (r["value"] and (len(raw[:threads * 320 * 3 * 64]) / 1e6 / r["value"])),
+                "ms_per_step": 1000.0 * (r["n"] / 1e6 / r["value"]) if r["value"] else None,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "impl": "reference",
                 "config": {"workload": desc, "parallelism": f"{threads} host threads"},
@@ -207,7 +224,7 @@ def main():
         torch.distributed.broadcast_object_list(obj, src=0)
         return obj[0]
 
-    def run_step(timed):
+    def run_step(cfg):
         """compress (device-resident input) + decompress; PMKLC-M over all ranks."""
         tm_c, tm_d = P.Timing(), P.Timing()
         if world > 1:
@@ -241,40 +258,50 @@ def main():
         c_ms, d_ms = e0.elapsed_time(e1), e1b.elapsed_time(e2)
         return blob, c_ms, d_ms, tm_c.kernel_launches + tm_d.kernel_launches, (tm_c, tm_d)
 
+    def measure(cfg, warmup, steps):
+        # correctness of the measured path: lossless round trip (first warm-up)
+        blob, _, _, _, _ = run_step(cfg)
+        if ctx is None:
+            assert P.decompress(blob, spum, device=dev) == raw, "round trip mismatch"
+        else:
+            out = ctx.decompress(blob, spum)
+            if rank == 0:
+                assert out == raw, "round trip mismatch"
+        for _ in range(max(warmup - 1, 0)):
+            run_step(cfg)
+        res = {"ct": 0.0, "dt": 0.0, "launches": 0, "flags": blob[5],
+               "hot": {"ms": 0.0, "launches": 0, "units": 0, "flops": 0.0},
+               "brk": {"sprm_prepass_ms": 0.0, "compress_ticks_ms": 0.0, "decompress_ticks_ms": 0.0}}
+        hot, brk = res["hot"], res["brk"]
+        with clk:
+            for _ in range(steps):
+                flush_l2(torch, flush)
+                blob, c_ms, d_ms, l, tms = run_step(cfg)
+                brk["sprm_prepass_ms"] += tms[0].sprm_ms / steps
+                brk["compress_ticks_ms"] += tms[0].model_ms / steps
+                brk["decompress_ticks_ms"] += tms[1].model_ms / steps
+                for tm in tms:  # dominant kernel, timed on the device inside the timed region
+                    hot["ms"] += tm.hot_ms
+                    hot["launches"] += tm.hot_launches
+                    hot["units"] += tm.hot_units
+                    hot["flops"] += tm.hot_flops_per_unit * tm.hot_units
+                if world > 1:  # max over ranks, per phase
+                    tt = torch.tensor([c_ms, d_ms], dtype=torch.float64)
+                    torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+                    c_ms, d_ms = float(tt[0]), float(tt[1])
+                res["ct"] += c_ms
+                res["dt"] += d_ms
+                res["launches"] += l
+        res["blob"] = blob
+        res["value"] = n * steps / 1e6 / ((res["ct"] + res["dt"]) / 1000.0)
+        return res
+
     clk = Clocks(dev).start()
-    # correctness of the measured path: lossless round trip
-    blob, _, _, _, _ = run_step(False)
-    if ctx is None:
-        assert P.decompress(blob, spum, device=dev) == raw, "round trip mismatch"
-    else:
-        out = ctx.decompress(blob, spum)
-        if rank == 0:
-            assert out == raw, "round trip mismatch"
-
-    for _ in range(max(args.warmup - 1, 0)):
-        run_step(False)
-
-    ct = dt = 0.0
-    launches = 0
-    hot = {"ms": 0.0, "launches": 0, "units": 0, "flops": 0.0}
-    with clk:
-        for _ in range(args.steps):
-            flush_l2(torch, flush)
-            blob, c_ms, d_ms, l, tms = run_step(True)
-            for tm in tms:  # dominant kernel, timed on the device inside the timed region
-                hot["ms"] += tm.hot_ms
-                hot["launches"] += tm.hot_launches
-                hot["units"] += tm.hot_units
-                hot["flops"] += tm.hot_flops_per_unit * tm.hot_units
-            if world > 1:  # max over ranks, per phase
-                tt = torch.tensor([c_ms, d_ms], dtype=torch.float64)
-                torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-                c_ms, d_ms = float(tt[0]), float(tt[1])
-            ct += c_ms
-            dt += d_ms
-            launches += l
+    main_run = measure(cfg, args.warmup, args.steps)
+    ct, dt, launches = main_run["ct"], main_run["dt"], main_run["launches"]
+    hot, brk, blob = main_run["hot"], main_run["brk"], main_run["blob"]
     tot_ms = ct + dt
-    value = n * args.steps / 1e6 / (tot_ms / 1000.0)
+    value = main_run["value"]
 
     # e2e through the public host API (host buffers, H2D/D2H inside)
     e_times = []
@@ -300,6 +327,15 @@ def main():
         if rank == 0:
             assert back == raw
     e2e_val = n / 1e6 / (sum(e_times) / len(e_times))
+
+    # config 3's other selector branch: threshold lowered so the private model
+    # is pre-trained on the input inside compress (flags 6, SURVEY §8 config 3;
+    # the reference never enables SPuM and SPrM together, mixer.cpp:9-12).
+    # One warm-up step (the engine paths are already warm from the main run).
+    sprm = None
+    if not args.no_sprm_branch:
+        cfg6 = dataclasses.replace(cfg, selector_threshold=0)
+        sprm = measure(cfg6, 1, args.steps)
 
     line = None
     if rank == 0:
@@ -346,15 +382,33 @@ def main():
                     "frac": ach_tf / peak_tf, "traffic": tjson.get("gemm_nt_dram_bytes_per_launch"),
                     "avg_launch_ms": k_ms, "flops_per_launch": k_fl,
                     "peak_source": "live non-FMA FP32 microbenchmark"}
-        cpu = None
+        cpu = cpu6 = None
         if not args.skip_cpu and world == 1:
             threads = min(os.cpu_count() or 1, 256, args.workers)
-            try:
-                cpu_full = cpu_reference(raw, cfg, spum, threads, 1, 0)
-                cpu = {k: cpu_full[k] for k in ("value", "unit", "cores", "kind", "sample")}
-            except Exception as e:  # report, do not hide
-                cpu = {"value": None, "unit": "MB/s", "cores": threads, "kind": "reference",
-                       "sample": f"failed: {e}"}
+            def cpu_leg(c):
+                try:
+                    full = cpu_reference(raw, c, spum, threads, 1, 0)
+                    return {k: full[k] for k in ("value", "unit", "cores", "kind", "sample")}
+                except Exception as e:  # report, do not hide
+                    return {"value": None, "unit": "MB/s", "cores": threads, "kind": "reference",
+                            "sample": f"failed: {e}"}
+            cpu = cpu_leg(cfg)
+            if sprm is not None:
+                cpu6 = cpu_leg(dataclasses.replace(cfg, selector_threshold=0))
+        sprm_line = None
+        if sprm is not None:
+            sprm_line = {
+                "workload": desc.replace("SPuM(seeded)+DM (flags 5, default selector)",
+                                         "SPrM(pre-trained on the input inside compress)+DM "
+                                         "(flags 6, selector_threshold=0)"),
+                "container_flags": sprm["flags"], "value": sprm["value"], "unit": "MB/s",
+                "warmup": 1, "steps": args.steps,
+                "ms_per_step": (sprm["ct"] + sprm["dt"]) / args.steps,
+                "compress_MBps": n * args.steps / 1e6 / (sprm["ct"] / 1000.0),
+                "decompress_MBps": n * args.steps / 1e6 / (sprm["dt"] / 1000.0),
+                "bits_per_base": 8.0 * len(sprm["blob"]) / n,
+                "step_breakdown_ms": sprm["brk"], "gpu_launches": sprm["launches"],
+                "cpu_baseline": cpu6}
         line = {
             "metric": METRIC, "value": value, "unit": "MB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
@@ -366,9 +420,11 @@ def main():
             "compress_MBps": n * args.steps / 1e6 / (ct / 1000.0),
             "decompress_MBps": n * args.steps / 1e6 / (dt / 1000.0),
             "bits_per_base": 8.0 * len(blob) / n,
+            "step_breakdown_ms": brk,
             "container_bytes": len(blob),
             "roofline": roof,
             "cpu_baseline": cpu,
+            "sprm_branch": sprm_line,
             "e2e": {"value": e2e_val, "unit": "MB/s", "h2d_bytes_per_step": n + len(blob),
                     "d2h_bytes_per_step": len(blob) + n},
             "clocks": clk.summary(),

@@ -62,6 +62,7 @@ typedef struct pmklc_timing {  /* CUDA-event times of the last call, ms */
   double hot_ms;
   uint64_t hot_launches, hot_units;
   double hot_flops_per_unit;
+  double sprm_ms; /* SPrM pre-pass (training.cpp:8-83) inside compress, ms */
 } pmklc_timing;
 
 /* CompressConfig{} defaults: s=k=3, t=32, bs=320, workers=1, threshold 5e8,

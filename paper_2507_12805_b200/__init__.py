@@ -59,7 +59,7 @@ class Timing(C.Structure):
                 ("ticks", C.c_uint64), ("kernel_launches", C.c_uint64), ("chunks", C.c_uint64),
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("hot_ms", C.c_double), ("hot_launches", C.c_uint64), ("hot_units", C.c_uint64),
-                ("hot_flops_per_unit", C.c_double)]
+                ("hot_flops_per_unit", C.c_double), ("sprm_ms", C.c_double)]
 
 
 # Every symbol include/pmklc_b200.h declares (checked by tests/test_capi.py).

@@ -78,7 +78,7 @@ void copy_timing(const Timing& t, pmklc_timing* out) {
   *out = pmklc_timing{t.total_ms,  t.h2d_ms,       t.tokenize_ms,     t.warmup_ms,
                       t.model_ms,  t.d2h_ms,       t.ticks,           t.kernel_launches,
                       t.chunks,    t.h2d_bytes,    t.d2h_bytes,       t.hot_ms,
-                      t.hot_launches, t.hot_units, t.hot_flops_per_unit};
+                      t.hot_launches, t.hot_units, t.hot_flops_per_unit, t.sprm_ms};
 }
 
 int do_compress(const uint8_t* h, const uint8_t* d, size_t n, const pmklc_cfg* c, uint8_t** out,

@@ -850,6 +850,7 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
   auto G_ = [&](int i) { return g.p + hoffs[size_t(i)]; };
   const int b0 = model.bott();
   uint64_t nl = 0;
+  SideStream side;
   auto step = [&](int rows) {
     SprmP sp{w.p, offs.p, rows, T, Es, H, V, B};
     const int64_t rt = int64_t(rows) * T;
@@ -876,16 +877,24 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
     g4.M = rows; g4.N = B; g4.K = V; g4.init = 0;
     launch_gemm(g4, false, true, td.p, 1, st);
     launch_sprm_tanh_grad(dbact.p, bact.p, int64_t(rows) * B, st);
+    // Branches of the step DAG run on a side stream where nothing on the main
+    // chain reads their results before Adam: the bottleneck weight gradient,
+    // then (after BPTT) the gradient transpose and the 12 weight-gradient
+    // reductions, beside dx -> embedding gradient.
+    side.rewind();
+    side.wait_for(st);
     GemmP g5{};
     g5.A = fin.p; g5.lda = 2 * H; g5.B = dbact.p; g5.ldb = B; g5.C = G_(b0); g5.ldc = B;
     g5.M = 2 * H; g5.N = B; g5.K = rows; g5.ones_row = 1; g5.init = 2;
-    launch_gemm(g5, true, false, td.p, 1, st);
+    launch_gemm(g5, true, false, td.p, 1, side.s);
     GemmP g6{};
     g6.A = dbact.p; g6.lda = B; g6.B = W_(b0); g6.ldb = B; g6.C = dfin.p; g6.ldc = 2 * H;
     g6.M = rows; g6.N = 2 * H; g6.K = B; g6.init = 0;
     launch_gemm(g6, false, true, td.p, 1, st);
     // backward through time, then the weight-gradient reductions over (t desc, rows asc)
-    launch_sprm_bptt(sp, tape.p, dfin.p, Gt.p, G.p, st);
+    launch_sprm_bptt(sp, tape.p, dfin.p, Gt.p, st);
+    side.wait_for(st);
+    launch_sprm_transpose(sp, Gt.p, G.p, side.s);
     NtP probs[12];
     for (int d = 0; d < 2; ++d) {
       const float* Gan = G.p + (int64_t(0 * 2 + d) * H) * rt;
@@ -904,10 +913,12 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
       const NtP six[6] = {a1, a2, a3, a4, a5, a6};
       for (int u = 0; u < 6; ++u) probs[d * 6 + u] = six[u];
     }
-    launch_gemm_nt_batch(probs, 12, td.p, 1, st);
-    launch_sprm_dx(sp, G.p, dx.p, st);
+    launch_gemm_nt_batch(probs, 12, td.p, 1, side.s);
+    if (!sprm_dx_time_major(sp)) side.join_into(st);  // the generic dx reads the transposed G
+    launch_sprm_dx(sp, G.p, Gt.p, dx.p, st);
     const DmDims ed{rows, T, Es, H, 0, V, 0};
     launch_emb_grad(ctx.p, 0, dx.p, 0, g.p, 0, int64_t(hoffs[0]), ed, td.p, 1, st);
+    side.join_into(st);
     launch_adam_scalars(sc.p, st);
     launch_adam(w.p, g.p, mo.p, vo.p, 0, P, sc.p, td.p, 1, st);
     launch_pos_advance(pos.p, batch, st);
@@ -1005,11 +1016,16 @@ Bytes compress_impl(const uint8_t* h_raw, const uint8_t* d_raw_in, size_t n, con
   if ((flags & 2) && m < uint64_t(cfg.t) + 1) flags = 4;
   BiGru priv_model;
   uint64_t sprm_launches = 0;
+  double sprm_ms = 0;
   if (flags & 2) {
+    Event p0, p1;
+    p0.record(st);
     priv_model = pretrain_private_gpu(d_tok.p, m, models.has_pub ? &models.pub.host : nullptr, dims,
                                       cfg.t, cfg.bs, sprm_seed, st, &sprm_launches);
+    p1.record(st);
     models.priv.upload(priv_model, st);
     models.has_priv = true;
+    sprm_ms = Event::ms(p0, p1);
   }
 
   const uint16_t myriad = uint16_t(std::lround(double(cfg.smp_fraction) * 10000.0));
@@ -1132,6 +1148,7 @@ Bytes compress_impl(const uint8_t* h_raw, const uint8_t* d_raw_in, size_t n, con
     tm.model_ms = run.model_ms;
     tm.ticks = uint64_t(run.sch.ticks);
     tm.kernel_launches = run.launches + sprm_launches + 3;
+    tm.sprm_ms = sprm_ms;
     tm.chunks = W;
     fill_hot(tm, run);
     tm.h2d_bytes = h2d;

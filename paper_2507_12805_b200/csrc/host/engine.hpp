@@ -38,6 +38,7 @@ struct Timing {
   // dominant kernel (k_bigru_rec_fused, SPuM layer 1), timed in situ
   double hot_ms = 0, hot_flops_per_unit = 0;
   uint64_t hot_launches = 0, hot_units = 0;
+  double sprm_ms = 0;  // SPrM pre-pass (compress, flags & 2)
 };
 
 struct CallOptions {

@@ -251,10 +251,10 @@ __device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
 // column; A is staged interleaved [k][row] so one broadcast LDS.128 yields row
 // pairs for the paired FP32 chains; B is read once per RPT rows. Row M of a
 // problem is the bias row (A == 1, so 1*b == b exactly: the plain sum).
-constexpr int kNwBK = 32, kNwWarps = 2;
-constexpr int kNwSB = kNwBK + 4;  // padded B row: LDS.128 of 32 rows is conflict-free
-__host__ __device__ constexpr int nw_warp_floats(int rpt, int stages) {
-  return stages * (rpt * kNwBK + 32 * kNwSB);
+constexpr int kNwWarps = 2;
+// padded B row (BK + 4 floats): LDS.128 of 32 rows is conflict-free
+__host__ __device__ constexpr int nw_warp_floats(int rpt, int stages, int bk) {
+  return stages * (rpt * bk + 32 * (bk + 4));
 }
 
 struct NtBatch {
@@ -264,12 +264,74 @@ struct NtBatch {
   int n;
 };
 
+// In-order building blocks for the latency-bound NT tile: ptxas keeps asm
+// volatile statements in program order, so the software pipeline written in
+// nt_tile_rpt2 is the one that issues (plain loads get sunk next to their
+// uses, which exposes the shared-memory latency on the add chain).
+__device__ __forceinline__ float4 lds128_v(const float* p) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+  return v;
+}
+__device__ __forceinline__ f2_t f2_mul_v(f2_t a, f2_t b) {
+  f2_t r;
+  asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c_negzero2));
+  return r;
+}
+__device__ __forceinline__ f2_t f2_add_v(f2_t a, f2_t b) {
+  f2_t r;
+  asm volatile("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// One full tile of the 2-row paired chain: acc += a(k) * b(k), k ascending.
+// Groups of 16 k: shared loads two groups ahead, products one group ahead,
+// one chain add per k with the independent work issued in its latency gaps.
+// as: [BK][2] (row pair per k), bs: this lane's B row.
+template <int BK>
+__device__ __forceinline__ f2_t nt_tile_rpt2(f2_t acc, const float* as, const float* bs) {
+  constexpr int KG = 16, NG = BK / KG, NL = KG / 4 + KG / 2;  // 12 LDS.128 per group
+  float4 L[2][NL];  // loaded operands: [0..3] B (4 k each), [4..11] A (2 k each)
+  f2_t Pp[2][KG];   // products
+  auto ld = [&](int g, int i) -> float4 {
+    return i < KG / 4 ? lds128_v(bs + g * KG + 4 * i) : lds128_v(as + g * KG * 2 + 4 * (i - KG / 4));
+  };
+  auto prod = [&](const float4 (&l)[NL], int k) -> f2_t {
+    const float4 b4 = l[k / 4];
+    const float b = (k & 3) == 0 ? b4.x : (k & 3) == 1 ? b4.y : (k & 3) == 2 ? b4.z : b4.w;
+    const float4 a4 = l[KG / 4 + k / 2];
+    const f2_t a = (k & 1) ? f2_pack(a4.z, a4.w) : f2_pack(a4.x, a4.y);
+    return f2_mul_v(a, f2_bcast(b));
+  };
+#pragma unroll
+  for (int i = 0; i < NL; ++i) L[0][i] = ld(0, i);
+  if (NG > 1) {
+#pragma unroll
+    for (int i = 0; i < NL; ++i) L[1][i] = ld(1, i);
+  }
+#pragma unroll
+  for (int k = 0; k < KG; ++k) Pp[0][k] = prod(L[0], k);
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    const int cb = g & 1, nb = cb ^ 1;
+#pragma unroll
+    for (int k = 0; k < KG; ++k) {
+      acc = f2_add_v(acc, Pp[cb][k]);
+      if (g + 1 < NG) Pp[nb][k] = prod(L[nb], k);
+      if (g + 2 < NG && k < NL) L[cb][k] = ld(g + 2, k);
+    }
+  }
+  return acc;
+}
+
 // VEC: B rows 16-byte aligned and K a multiple of 4 (host-checked).
 // STAGES: ring depth; 3 when the chip is full of warps, 8 when a few warps must
 // cover the L2 latency alone.
-template <bool VEC, int RPT, int STAGES>
+template <bool VEC, int RPT, int STAGES, int BK>
 __global__ void __launch_bounds__(kNwWarps * 32) k_gemm_nt(NtBatch nb, const TickDesc* __restrict__ td) {
-  constexpr int kNwStages = STAGES;
+  constexpr int kNwStages = STAGES, kNwBK = BK, kNwSB = BK + 4;
   extern __shared__ __align__(128) float sm[];
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
@@ -286,7 +348,7 @@ __global__ void __launch_bounds__(kNwWarps * 32) k_gemm_nt(NtBatch nb, const Tic
   const int m0 = rg * RPT, n0 = cg * 32, n = n0 + lane;
   const int arows = max(0, min(RPT, M - m0));  // rows with A data; the rest are 1 (bias) or 0
   const int nrows = min(32, N - n0);
-  float* As = sm + w * nw_warp_floats(RPT, STAGES);  // [stage][BK][RPT]
+  float* As = sm + w * nw_warp_floats(RPT, STAGES, BK);  // [stage][BK][RPT]
   float* Bs = As + kNwStages * RPT * kNwBK;  // [stage][32][SB]
   const float* A = pp.A + c * pp.a_cs + int64_t(m0) * lda;
   const float* B = pp.B + c * pp.b_cs + int64_t(n0) * ldb;
@@ -295,11 +357,12 @@ __global__ void __launch_bounds__(kNwWarps * 32) k_gemm_nt(NtBatch nb, const Tic
     for (int i = lane; i < kNwStages * kNwBK; i += 32) As[i * RPT + r] = v;
   }
   const int ntiles = (K + kNwBK - 1) / kNwBK;
-  // full tiles: lane copies A[r][k0 + lane] for each row (BK == 32) and the
-  // 16-byte chunk (lane & 7) of B rows (lane >> 3) + 4j, j < 8
-  static_assert(kNwBK == 32, "one A element and one B chunk column per lane");
-  const float* bl = B + int64_t(lane >> 3) * ldb + 4 * (lane & 7);
-  const int bsl = (lane >> 3) * kNwSB + 4 * (lane & 7);
+  // full tiles: lane copies A[r][k0 + lane + 32e] for each row and the 16-byte
+  // chunk (lane % CPR) of B rows lane / CPR + RPI*j (CPR = BK/4 chunks per row)
+  static_assert(kNwBK == 32 || kNwBK == 64, "tile depth");
+  constexpr int CPR = kNwBK / 4, RPI = 32 / CPR, BJ = 32 / RPI;
+  const float* bl = B + int64_t(lane / CPR) * ldb + 4 * (lane % CPR);
+  const int bsl = (lane / CPR) * kNwSB + 4 * (lane % CPR);
   auto load = [&](int tile) {
     if (tile < ntiles) {
       const int st = tile % kNwStages, k0 = tile * kNwBK, kc = min(kNwBK, K - k0);
@@ -308,11 +371,15 @@ __global__ void __launch_bounds__(kNwWarps * 32) k_gemm_nt(NtBatch nb, const Tic
       if (kc == kNwBK) {
 #pragma unroll
         for (int r = 0; r < RPT; ++r)
-          if (r < arows) cp_async4(as + lane * RPT + r, A + int64_t(r) * lda + k0 + lane);
+          if (r < arows) {
+#pragma unroll
+            for (int e = 0; e < kNwBK / 32; ++e)
+              cp_async4(as + (lane + 32 * e) * RPT + r, A + int64_t(r) * lda + k0 + lane + 32 * e);
+          }
         if (VEC && nrows == 32) {
           const float* src = bl + k0;
 #pragma unroll
-          for (int j = 0; j < 8; ++j, src += 4 * ldb) cp_async16(bs + bsl + j * 4 * kNwSB, src);
+          for (int j = 0; j < BJ; ++j, src += RPI * ldb) cp_async16(bs + bsl + j * RPI * kNwSB, src);
         } else {
           for (int i = lane; i < nrows * kNwBK; i += 32)
             cp_async4(bs + (i / kNwBK) * kNwSB + i % kNwBK, B + int64_t(i / kNwBK) * ldb + k0 + i % kNwBK);
@@ -371,7 +438,9 @@ __global__ void __launch_bounds__(kNwWarps * 32) k_gemm_nt(NtBatch nb, const Tic
     const int st = tile % kNwStages, kc = min(kNwBK, K - tile * kNwBK);
     const float* as = As + st * kNwBK * RPT;
     const float* bs = Bs + (st * 32 + lane) * kNwSB;
-    if (kc == kNwBK) {
+    if (kc == kNwBK && RPT == 2) {
+      acc2[0] = nt_tile_rpt2<kNwBK>(acc2[0], as, bs);
+    } else if (kc == kNwBK) {
 #pragma unroll
       for (int kk = 0; kk < kNwBK; kk += 4) {
         const float4 b = *reinterpret_cast<const float4*>(bs + kk);
@@ -836,20 +905,32 @@ __global__ void __launch_bounds__(kSortThreads) k_emb_bwd_sorted(
   uint16_t* sorted = reinterpret_cast<uint16_t*>(vals + kSortVals);
   uint16_t* wc = sorted + kSortMaxPos;                       // [warp][V] counts, then cursors
   int* off = reinterpret_cast<int*>(wc + kSortWarps * kSortMaxV);  // [V+1]
-  if (blockIdx.x >= unsigned(td->n_act)) return;
-  const int c = td->act[blockIdx.x];
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int V = d.V, E = d.E, RT = d.R * d.T;
+  // token group of this block: tokens [v0, v1) (every block sorts redundantly)
+  const int v0 = int(int64_t(V) * blockIdx.x / gridDim.x);
+  const int v1 = int(int64_t(V) * (blockIdx.x + 1) / gridDim.x);
   const uint32_t* cp = ctx + c * ctx_cs;
   const int span = (RT + kSortWarps - 1) / kSortWarps;
   const int p0 = w * span, p1 = min(RT, p0 + span);
   const unsigned lt = (1u << lane) - 1u;
+  // the warp's span of tokens, loaded once (independent loads in flight)
+  constexpr int kSpanIt = (kSortMaxPos + kSortThreads - 1) / kSortThreads;
+  uint32_t tokv[kSpanIt];
+#pragma unroll
+  for (int it = 0; it < kSpanIt; ++it) {
+    const int p = p0 + it * 32 + lane;
+    tokv[it] = p < p1 ? __ldg(cp + p) : 0xffffffffu;
+  }
   // phase 1a: per-warp token counts
   for (int v = lane; v < V; v += 32) wc[w * V + v] = 0;
   __syncwarp();
-  for (int base = p0; base < p1; base += 32) {
-    const int p = base + lane;
-    const uint32_t v = p < p1 ? cp[p] : 0xffffffffu;
+#pragma unroll
+  for (int it = 0; it < kSpanIt; ++it) {
+    const int p = p0 + it * 32 + lane;
+    const uint32_t v = tokv[it];
     const unsigned m = __match_any_sync(0xffffffffu, v);
     if (p < p1 && (m & lt) == 0) wc[w * V + v] = uint16_t(wc[w * V + v] + __popc(m));
     __syncwarp();
@@ -884,9 +965,10 @@ __global__ void __launch_bounds__(kSortThreads) k_emb_bwd_sorted(
   }
   __syncthreads();
   // phase 1c: stable placement
-  for (int base = p0; base < p1; base += 32) {
-    const int p = base + lane;
-    const uint32_t v = p < p1 ? cp[p] : 0xffffffffu;
+#pragma unroll
+  for (int it = 0; it < kSpanIt; ++it) {
+    const int p = p0 + it * 32 + lane;
+    const uint32_t v = tokv[it];
     const unsigned m = __match_any_sync(0xffffffffu, v);
     if (p < p1) {
       const int cur = wc[w * V + v];
@@ -897,34 +979,52 @@ __global__ void __launch_bounds__(kSortThreads) k_emb_bwd_sorted(
     __syncwarp();
   }
   __syncthreads();
-  // phases 2+3
+  // phases 2+3 over this block's tokens: sorted range [off[v0], off[v1])
   const float* xp = dx + c * dx_cs;
   const float* lp = dxl ? dxl + c * dxl_cs : nullptr;
   float* gp = grads + c * g_cs + off_emb;
-  const int VE = V * E;
+  const int o0 = v0 * E, VE = (v1 - v0) * E;
+  const int r0 = off[v0], r1 = off[v1];
   float acc[kSortAcc];
 #pragma unroll
   for (int q = 0; q < kSortAcc; ++q) {
     const int o = tid + q * kSortThreads;
-    acc[q] = o < VE ? gp[o] : 0.f;
+    acc[q] = o < VE ? gp[o0 + o] : 0.0f;
   }
   const int slab = kSortVals / E;
-  for (int s0 = 0; s0 < RT; s0 += slab) {
-    const int s1 = min(RT, s0 + slab);
+  for (int s0 = r0; s0 < r1; s0 += slab) {
+    const int s1 = min(r1, s0 + slab);
     const int n = (s1 - s0) * E;
-    for (int i = tid; i < n; i += kSortThreads) {
-      const int h = s0 + i / E, j = i % E;
-      const int pp = sorted[h];
-      float val = __ldg(xp + int64_t(pp) * E + j);
-      if (lp && pp % d.T == d.T - 1) val = fadd(val, __ldg(lp + int64_t(pp / d.T) * E + j));
-      vals[i] = val;
+    constexpr int kG = 8;  // loads in flight per thread
+    for (int i0 = tid; i0 < n; i0 += kG * kSortThreads) {
+      float val[kG], lv[kG];
+      bool last[kG];
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        const int i = i0 + u * kSortThreads;
+        val[u] = 0.0f;
+        lv[u] = 0.0f;
+        last[u] = false;
+        if (i < n) {
+          const int h = s0 + i / E, j = i % E;
+          const int pp = sorted[h];
+          val[u] = __ldg(xp + int64_t(pp) * E + j);
+          last[u] = lp && pp % d.T == d.T - 1;
+          if (last[u]) lv[u] = __ldg(lp + int64_t(pp / d.T) * E + j);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kG; ++u) {
+        const int i = i0 + u * kSortThreads;
+        if (i < n) vals[i] = last[u] ? fadd(val[u], lv[u]) : val[u];
+      }
     }
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < kSortAcc; ++q) {
       const int o = tid + q * kSortThreads;
       if (o < VE) {
-        const int v = o / E, j = o % E;
+        const int v = v0 + o / E, j = o % E;
         const int b0 = max(off[v], s0), b1 = min(off[v + 1], s1);
         float a = acc[q];
         int h = b0;
@@ -944,7 +1044,7 @@ __global__ void __launch_bounds__(kSortThreads) k_emb_bwd_sorted(
 #pragma unroll
   for (int q = 0; q < kSortAcc; ++q) {
     const int o = tid + q * kSortThreads;
-    if (o < VE) gp[o] = acc[q];
+    if (o < VE) gp[o0 + o] = acc[q];
   }
 }
 
@@ -962,8 +1062,11 @@ static void launch_sorted_emb(const uint32_t* ctx, int64_t ctx_cs, const float* 
                          int(kSortSmem));
     attr = true;
   }
-  k_emb_bwd_sorted<<<max_active, kSortThreads, kSortSmem, st>>>(ctx, ctx_cs, dx, dx_cs, dxl, dxl_cs,
-                                                                grads, g_cs, off_emb, d, td);
+  // split the vocabulary over several blocks per chunk while chunks alone
+  // cannot fill the chip (each block re-sorts; the gather and walk split)
+  const int groups = std::max(1, std::min(std::min(8, d.V), 148 / std::max(1, max_active)));
+  k_emb_bwd_sorted<<<dim3(unsigned(groups), unsigned(max_active)), kSortThreads, kSortSmem, st>>>(
+      ctx, ctx_cs, dx, dx_cs, dxl, dxl_cs, grads, g_cs, off_emb, d, td);
 }
 
 // ------------------------------------------------------------------ Adam
@@ -1043,12 +1146,12 @@ void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int m
   }
   static bool attr_set = false;
   if (!attr_set) {
-#define PMKLC_NT_ATTR(V, R, S) \
-  cudaFuncSetAttribute(k_gemm_nt<V, R, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                       int(kNwWarps * nw_warp_floats(R, S) * sizeof(float)))
-    PMKLC_NT_ATTR(true, 8, 3); PMKLC_NT_ATTR(false, 8, 3); PMKLC_NT_ATTR(true, 4, 3);
-    PMKLC_NT_ATTR(false, 4, 3); PMKLC_NT_ATTR(true, 2, 3); PMKLC_NT_ATTR(false, 2, 3);
-    PMKLC_NT_ATTR(true, 2, 8); PMKLC_NT_ATTR(false, 2, 8);
+#define PMKLC_NT_ATTR(V, R, S, K) \
+  cudaFuncSetAttribute(k_gemm_nt<V, R, S, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                       int(kNwWarps * nw_warp_floats(R, S, K) * sizeof(float)))
+    PMKLC_NT_ATTR(true, 8, 3, 32); PMKLC_NT_ATTR(false, 8, 3, 32); PMKLC_NT_ATTR(true, 4, 3, 32);
+    PMKLC_NT_ATTR(false, 4, 3, 32); PMKLC_NT_ATTR(true, 2, 3, 32); PMKLC_NT_ATTR(false, 2, 3, 32);
+    PMKLC_NT_ATTR(true, 2, 6, 64); PMKLC_NT_ATTR(false, 2, 6, 64);
 #undef PMKLC_NT_ATTR
     attr_set = true;
   }
@@ -1065,26 +1168,28 @@ void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int m
   // Rows per thread: 8 (B read once per 8 rows) while that still gives ~8
   // warps per SM, else 4 while that gives ~4; a launch that cannot fill the chip
   // is bound by the k chain (4 cycles per step), which 2 paired rows per thread
-  // still meet, with a deep ring so the few warps do not wait on L2.
+  // still meet, with deep 64-k tiles so the few warps neither wait on L2 nor
+  // spend their issue slots on per-tile bookkeeping.
   NtBatch nb;
   int rpt = 8;
   if (int64_t(build(8, nb)) * max_active < 148 * 8) rpt = 4;
   if (rpt == 4 && int64_t(build(4, nb)) * max_active < 148 * 4) rpt = 2;
   const int tasks = build(rpt, nb);
-  const int stages = (rpt == 2 && int64_t(tasks) * max_active < 148 * 2) ? 8 : 3;
+  const bool deep = rpt == 2 && int64_t(tasks) * max_active < 148 * 2;
+  const int stages = deep ? 6 : 3, bk = deep ? 64 : 32;
   const dim3 grid(unsigned((tasks + kNwWarps - 1) / kNwWarps), unsigned(max_active));
-  const size_t smem = size_t(kNwWarps) * nw_warp_floats(rpt, stages) * sizeof(float);
-#define PMKLC_NT_LAUNCH(R, S)                                                                  \
-  if (vec) k_gemm_nt<true, R, S><<<grid, kNwWarps * 32, smem, st>>>(nb, td);                  \
-  else k_gemm_nt<false, R, S><<<grid, kNwWarps * 32, smem, st>>>(nb, td);
+  const size_t smem = size_t(kNwWarps) * nw_warp_floats(rpt, stages, bk) * sizeof(float);
+#define PMKLC_NT_LAUNCH(R, S, K)                                                               \
+  if (vec) k_gemm_nt<true, R, S, K><<<grid, kNwWarps * 32, smem, st>>>(nb, td);               \
+  else k_gemm_nt<false, R, S, K><<<grid, kNwWarps * 32, smem, st>>>(nb, td);
   if (rpt == 8) {
-    PMKLC_NT_LAUNCH(8, 3)
+    PMKLC_NT_LAUNCH(8, 3, 32)
   } else if (rpt == 4) {
-    PMKLC_NT_LAUNCH(4, 3)
-  } else if (stages == 3) {
-    PMKLC_NT_LAUNCH(2, 3)
+    PMKLC_NT_LAUNCH(4, 3, 32)
+  } else if (!deep) {
+    PMKLC_NT_LAUNCH(2, 3, 32)
   } else {
-    PMKLC_NT_LAUNCH(2, 8)
+    PMKLC_NT_LAUNCH(2, 6, 64)
   }
 #undef PMKLC_NT_LAUNCH
 }

@@ -222,9 +222,13 @@ void launch_sprm_ce(const SprmP& s, const uint32_t* tokens, const int64_t* pos, 
                     float* g, cudaStream_t st);
 void launch_sprm_tanh_grad(float* dbact, const float* bact, int64_t n, cudaStream_t st);
 // BPTT + transpose: G = [5 (an, ar, az, hh, hprev)][2][Hs][R*T] feature-major
-void launch_sprm_bptt(const SprmP& s, const float* tape, const float* dfin, float* Gt, float* G,
+void launch_sprm_bptt(const SprmP& s, const float* tape, const float* dfin, float* Gt,
                       cudaStream_t st);
-void launch_sprm_dx(const SprmP& s, const float* G, float* dx, cudaStream_t st);
+// Gt[g][d][t][r][j] -> G[g][d][j][k] (feature-major, k = (t-1-t')*R + r)
+void launch_sprm_transpose(const SprmP& s, const float* Gt, float* G, cudaStream_t st);
+// true: launch_sprm_dx reads the time-major Gt (no dependency on the transpose)
+bool sprm_dx_time_major(const SprmP& s);
+void launch_sprm_dx(const SprmP& s, const float* G, const float* Gt, float* dx, cudaStream_t st);
 void launch_sprm_emb_grad(const SprmP& s, const uint32_t* ctx, const float* dx, float* grad_emb,
                           cudaStream_t st);
 void launch_tanh_vec(float* x, int64_t n, cudaStream_t st);

@@ -122,29 +122,35 @@ __global__ void __launch_bounds__(256) k_sprm_fwd(SprmP s, const uint32_t* __res
   if (act) fin[int64_t(r) * 2 * H + d * H + j] = sh[wl][cur][j];  // final_state (layers.cpp:389-399)
 }
 
-// H == 32 forward: two rows per warp as paired chains (rows r0, r0+1), the
-// three gate chains interleaved, next step's token and table values prefetched.
-// Same per-element operations and order as k_sprm_fwd.
-__global__ void __launch_bounds__(256) k_sprm_fwd32(SprmP s, const uint32_t* __restrict__ ctx,
-                                                    const float* __restrict__ tab, float* tape,
-                                                    float* fin) {
+// H == 32 forward, one row per warp (640 row-directions spread over every
+// SM scheduler: the step loop is latency-bound, so one warp per scheduler).
+// Each lane keeps its three W_h columns in registers for the whole sequence
+// (96 floats), so a step reads only h (8 broadcast LDS.128); the r and z gates
+// run as one paired chain, n as a scalar chain; next step's token and table
+// values are prefetched. Same per-element operations and order as k_sprm_fwd.
+constexpr int kFwdWarps = 4;
+__global__ void __launch_bounds__(kFwdWarps * 32) k_sprm_fwd32(SprmP s, const uint32_t* __restrict__ ctx,
+                                                               const float* __restrict__ tab, float* tape,
+                                                               float* fin) {
   constexpr int H = 32;
-  __shared__ __align__(16) float sh[8][2][H][2];  // [warp][cur][q][row]
-  __shared__ __align__(16) float sw[3][H][H];
+  __shared__ __align__(16) float sh[kFwdWarps][2][H];
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = blockIdx.x & 1;
-  const int r0 = ((blockIdx.x >> 1) * 8 + wl) * 2;
+  const int r = (blockIdx.x >> 1) * kFwdWarps + wl;
   const int T = s.T, R = s.R, V = s.V;
+  if (r >= R) return;
   const float* W = s.w;
-  for (int i = threadIdx.x; i < 3 * H * H; i += blockDim.x) {
-    const int gate = i / (H * H), rem = i % (H * H);
-    sw[gate][rem / H][rem % H] = W[goff(s.offs, d, WHR + gate) + rem];
-  }
-  __syncthreads();
-  if (r0 >= R) return;
-  const bool ok1 = r0 + 1 < R;
-  const int r1 = ok1 ? r0 + 1 : r0;
   const int j = lane;
+  const float* wr = W + goff(s.offs, d, WHR) + j;
+  const float* wz = W + goff(s.offs, d, WHZ) + j;
+  const float* wn = W + goff(s.offs, d, WHN) + j;
+  f2_t wrz[H];
+  float wnr[H];
+#pragma unroll
+  for (int q = 0; q < H; ++q) {
+    wrz[q] = f2_pack(__ldg(wr + q * H), __ldg(wz + q * H));
+    wnr[q] = __ldg(wn + q * H);
+  }
   const float bhr = W[goff(s.offs, d, BHR) + j], bhz = W[goff(s.offs, d, BHZ) + j],
               bhn = W[goff(s.offs, d, BHN) + j];
   const float* t0 = tab + int64_t(d) * 3 * V * H;
@@ -154,62 +160,49 @@ __global__ void __launch_bounds__(256) k_sprm_fwd32(SprmP s, const uint32_t* __r
   float* tn = tape + (int64_t(2 * 2 + d) * TRH);
   float* th = tape + (int64_t(3 * 2 + d) * TRH);
   float* to = tape + (int64_t(4 * 2 + d) * TRH);
-  *reinterpret_cast<float2*>(&sh[wl][0][j][0]) = make_float2(0.f, 0.f);
-  auto fetch = [&](int t, float (&x)[2][3]) {
+  sh[wl][0][j] = 0.0f;
+  auto fetch = [&](int t, float (&x)[3]) {
     const int src_t = d ? (T - 1 - t) : t;
-    const int64_t k0 = ctx[int64_t(r0) * T + src_t], k1 = ctx[int64_t(r1) * T + src_t];
-    x[0][0] = t0[k0 * H + j];
-    x[0][1] = t0[int64_t(V) * H + k0 * H + j];
-    x[0][2] = t0[2 * int64_t(V) * H + k0 * H + j];
-    x[1][0] = t0[k1 * H + j];
-    x[1][1] = t0[int64_t(V) * H + k1 * H + j];
-    x[1][2] = t0[2 * int64_t(V) * H + k1 * H + j];
+    const int64_t k0 = ctx[int64_t(r) * T + src_t];
+    x[0] = t0[k0 * H + j];
+    x[1] = t0[int64_t(V) * H + k0 * H + j];
+    x[2] = t0[2 * int64_t(V) * H + k0 * H + j];
   };
-  float xc[2][3], xn[2][3];
+  float xc[3], xn[3];
   fetch(0, xc);
   __syncwarp();
   int cur = 0;
   for (int t = 0; t < T; ++t) {
     if (t + 1 < T) fetch(t + 1, xn);
-    f2_t ar = f2_pack(fadd(xc[0][0], bhr), fadd(xc[1][0], bhr));
-    f2_t az = f2_pack(fadd(xc[0][1], bhz), fadd(xc[1][1], bhz));
-    f2_t hh = f2_bcast(bhn);
+    f2_t arz = f2_pack(fadd(xc[0], bhr), fadd(xc[1], bhz));
+    float hh = bhn;
+    const float* h = sh[wl][cur];
 #pragma unroll
-    for (int q = 0; q < H; ++q) {
-      const float2 hv = *reinterpret_cast<const float2*>(&sh[wl][cur][q][0]);
-      const f2_t hq = f2_pack(hv.x, hv.y);
-      ar = f2_mac(ar, hq, f2_bcast(sw[0][q][j]));
-      az = f2_mac(az, hq, f2_bcast(sw[1][q][j]));
-      hh = f2_mac(hh, hq, f2_bcast(sw[2][q][j]));
-    }
-    const float2 hp = *reinterpret_cast<const float2*>(&sh[wl][cur][j][0]);
-    const float arv[2] = {f2_lo(ar), f2_hi(ar)}, azv[2] = {f2_lo(az), f2_hi(az)};
-    const float hhv[2] = {f2_lo(hh), f2_hi(hh)}, hpv[2] = {hp.x, hp.y};
-    float hn[2];
+    for (int q4 = 0; q4 < H / 4; ++q4) {
+      const float4 hv = *reinterpret_cast<const float4*>(h + 4 * q4);
+      const float hq[4] = {hv.x, hv.y, hv.z, hv.w};
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const float rv = det_sigmoid(arv[u]), zv = det_sigmoid(azv[u]);
-      const float nv = det_tanh(fadd(xc[u][2], fmul(rv, hhv[u])));
-      hn[u] = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, hpv[u]));
-      if (u == 0 || ok1) {
-        const int64_t o = (int64_t(t) * R + r0 + u) * H + j;
-        tr[o] = rv;
-        tz[o] = zv;
-        tn[o] = nv;
-        th[o] = hhv[u];
-        to[o] = hn[u];
+      for (int u = 0; u < 4; ++u) {
+        arz = f2_mac(arz, f2_bcast(hq[u]), wrz[4 * q4 + u]);
+        hh = mac(hh, hq[u], wnr[4 * q4 + u]);
       }
     }
-    *reinterpret_cast<float2*>(&sh[wl][cur ^ 1][j][0]) = make_float2(hn[0], hn[1]);
+    const float rv = det_sigmoid(f2_lo(arz)), zv = det_sigmoid(f2_hi(arz));
+    const float nv = det_tanh(fadd(xc[2], fmul(rv, hh)));
+    const float hv = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, h[j]));
+    const int64_t o = (int64_t(t) * R + r) * H + j;
+    tr[o] = rv;
+    tz[o] = zv;
+    tn[o] = nv;
+    th[o] = hh;
+    to[o] = hv;
+    sh[wl][cur ^ 1][j] = hv;
     __syncwarp();
     cur ^= 1;
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-      for (int g = 0; g < 3; ++g) xc[u][g] = xn[u][g];
+    for (int g = 0; g < 3; ++g) xc[g] = xn[g];
   }
-  fin[int64_t(r0) * 2 * H + d * H + j] = sh[wl][cur][j][0];  // final_state (layers.cpp:389-399)
-  if (ok1) fin[int64_t(r0 + 1) * 2 * H + d * H + j] = sh[wl][cur][j][1];
+  fin[int64_t(r) * 2 * H + d * H + j] = sh[wl][cur][j];  // final_state (layers.cpp:389-399)
 }
 
 // g = det_softmax(logits) ; loss term ; g[tgt] -= 1   (training.cpp:28-34)
@@ -323,27 +316,37 @@ __global__ void __launch_bounds__(256) k_sprm_bptt(SprmP s, const float* __restr
   }
 }
 
-// H == 32 BPTT: two rows per warp as one paired dh chain, the step's tape values
-// prefetched one step ahead. Same per-element operations and order as k_sprm_bptt.
-__global__ void __launch_bounds__(256) k_sprm_bptt32(SprmP s, const float* __restrict__ tape,
-                                                     const float* __restrict__ dfin, float* Gt) {
+// H == 32 BPTT, one row per warp (the dh chain of 3*H MACs per step is the
+// latency floor; one warp per scheduler). Each lane keeps its W_h rows in
+// registers (96 floats); a step reads only the gate gradients (broadcast
+// LDS.128); the step's tape values are prefetched one step ahead. Same
+// per-element operations and order as k_sprm_bptt.
+constexpr int kBpttWarps = 4;
+__global__ void __launch_bounds__(kBpttWarps * 32) k_sprm_bptt32(SprmP s, const float* __restrict__ tape,
+                                                                 const float* __restrict__ dfin, float* Gt) {
   constexpr int H = 32;
-  __shared__ float swt[3][H][H + 1];                // [gate][q][j] = W_h{gate}[j][q]
-  __shared__ __align__(16) float sg[8][3][H][2];    // dhh, dar, daz of this step, per row
+  __shared__ __align__(16) float sg[kBpttWarps][3][H];  // dhh, dar, daz of this step
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = blockIdx.x & 1;
-  const int r0 = ((blockIdx.x >> 1) * 8 + wl) * 2;
+  const int r = (blockIdx.x >> 1) * kBpttWarps + wl;
   const int T = s.T, R = s.R;
+  if (r >= R) return;
   const float* W = s.w;
-  for (int i = threadIdx.x; i < 3 * H * H; i += blockDim.x) {
-    const int gate = i / (H * H), rem = i % (H * H), jj = rem / H, q = rem % H;
-    const float* Wg = W + goff(s.offs, d, gate == 0 ? WHN : gate == 1 ? WHR : WHZ);
-    swt[gate][q][jj] = Wg[int64_t(jj) * H + q];
-  }
-  __syncthreads();
-  if (r0 >= R) return;
-  const bool ok1 = r0 + 1 < R;
   const int j = lane;
+  // wt[g][q] = W_h{n,r,z}[j][q] (row j of each gate matrix)
+  float wt[3][H];
+#pragma unroll
+  for (int g = 0; g < 3; ++g) {
+    const float* Wg = W + goff(s.offs, d, g == 0 ? WHN : g == 1 ? WHR : WHZ) + int64_t(j) * H;
+#pragma unroll
+    for (int q4 = 0; q4 < H / 4; ++q4) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(Wg) + q4);
+      wt[g][4 * q4 + 0] = v.x;
+      wt[g][4 * q4 + 1] = v.y;
+      wt[g][4 * q4 + 2] = v.z;
+      wt[g][4 * q4 + 3] = v.w;
+    }
+  }
   const int64_t TRH = int64_t(T) * R * H;
   const float* tp[5];
 #pragma unroll
@@ -353,65 +356,53 @@ __global__ void __launch_bounds__(256) k_sprm_bptt32(SprmP s, const float* __res
   float* gaz = Gt + int64_t(2 * 2 + d) * TRH;
   float* ghh = Gt + int64_t(3 * 2 + d) * TRH;
   float* ghp = Gt + int64_t(4 * 2 + d) * TRH;
-  const int rr[2] = {r0, ok1 ? r0 + 1 : r0};
-  float dlast[2];
+  // only the GRU's last own step receives the final-state gradient
+  // (final_state_backward, layers.cpp:401-413), as 0 + dfin
+  const float dlast = fadd(0.0f, dfin[int64_t(r) * 2 * H + d * H + j]);
+  auto fetch = [&](int t, float (&x)[5]) {
+    const int64_t o = (int64_t(t) * R + r) * H + j;
 #pragma unroll
-  for (int u = 0; u < 2; ++u) dlast[u] = fadd(0.0f, dfin[int64_t(rr[u]) * 2 * H + d * H + j]);
-  // tape values of step t for both rows: r, z, n, hh, hprev
-  auto fetch = [&](int t, float (&x)[2][5]) {
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int64_t o = (int64_t(t) * R + rr[u]) * H + j;
-#pragma unroll
-      for (int g = 0; g < 4; ++g) x[u][g] = tp[g][o];
-      x[u][4] = t == 0 ? 0.0f : tp[4][o - int64_t(R) * H];
-    }
+    for (int g = 0; g < 4; ++g) x[g] = tp[g][o];
+    x[4] = t == 0 ? 0.0f : tp[4][o - int64_t(R) * H];
   };
-  float xc[2][5], xn[2][5];
+  float xc[5], xn[5];
   fetch(T - 1, xc);
-  float dh[2] = {0.0f, 0.0f};
+  float dh = 0.0f;
   for (int t = T - 1; t >= 0; --t) {
     if (t > 0) fetch(t - 1, xn);
-    float dn[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      dh[u] = fadd(dh[u], t == T - 1 ? dlast[u] : 0.0f);  // gather_add_step(dout, t, dh)
-      const float rv = xc[u][0], zv = xc[u][1], nv = xc[u][2], hhv = xc[u][3], hprev = xc[u][4];
-      const float dzv = fmul(dh[u], fsub(hprev, nv));
-      const float danv = fmul(fmul(dh[u], fsub(1.0f, zv)), fsub(1.0f, fmul(nv, nv)));
-      const float dar = fmul(fmul(fmul(danv, hhv), rv), fsub(1.0f, rv));
-      const float daz = fmul(fmul(dzv, zv), fsub(1.0f, zv));
-      const float dhh = fmul(danv, rv);
-      dn[u] = fmul(dh[u], zv);
-      if (u == 0 || ok1) {
-        const int64_t o = (int64_t(t) * R + rr[u]) * H + j;
-        gan[o] = danv;
-        gar[o] = dar;
-        gaz[o] = daz;
-        ghh[o] = dhh;
-        ghp[o] = hprev;
-      }
-      sg[wl][0][j][u] = dhh;
-      sg[wl][1][j][u] = dar;
-      sg[wl][2][j][u] = daz;
-    }
+    dh = fadd(dh, t == T - 1 ? dlast : 0.0f);  // gather_add_step(dout, t, dh)
+    const float rv = xc[0], zv = xc[1], nv = xc[2], hhv = xc[3], hprev = xc[4];
+    const float dzv = fmul(dh, fsub(hprev, nv));
+    const float danv = fmul(fmul(dh, fsub(1.0f, zv)), fsub(1.0f, fmul(nv, nv)));
+    const float dar = fmul(fmul(fmul(danv, hhv), rv), fsub(1.0f, rv));
+    const float daz = fmul(fmul(dzv, zv), fsub(1.0f, zv));
+    const float dhh = fmul(danv, rv);
+    float dn = fmul(dh, zv);
+    const int64_t o = (int64_t(t) * R + r) * H + j;
+    gan[o] = danv;
+    gar[o] = dar;
+    gaz[o] = daz;
+    ghh[o] = dhh;
+    ghp[o] = hprev;
+    sg[wl][0][j] = dhh;
+    sg[wl][1][j] = dar;
+    sg[wl][2][j] = daz;
     __syncwarp();
     // dh_next = dh*z + dhh.W_hn^T + dar.W_hr^T + daz.W_hz^T  (layers.cpp:306-308)
-    f2_t acc = f2_pack(dn[0], dn[1]);
 #pragma unroll
     for (int g = 0; g < 3; ++g)
 #pragma unroll
-      for (int q = 0; q < H; ++q) {
-        const float2 v = *reinterpret_cast<const float2*>(&sg[wl][g][q][0]);
-        acc = f2_mac(acc, f2_pack(v.x, v.y), f2_bcast(swt[g][q][j]));
+      for (int q4 = 0; q4 < H / 4; ++q4) {
+        const float4 v = *reinterpret_cast<const float4*>(&sg[wl][g][4 * q4]);
+        dn = mac(dn, v.x, wt[g][4 * q4 + 0]);
+        dn = mac(dn, v.y, wt[g][4 * q4 + 1]);
+        dn = mac(dn, v.z, wt[g][4 * q4 + 2]);
+        dn = mac(dn, v.w, wt[g][4 * q4 + 3]);
       }
     __syncwarp();
-    dh[0] = f2_lo(acc);
-    dh[1] = f2_hi(acc);
+    dh = dn;
 #pragma unroll
-    for (int u = 0; u < 2; ++u)
-#pragma unroll
-      for (int g = 0; g < 5; ++g) xc[u][g] = xn[u][g];
+    for (int g = 0; g < 5; ++g) xc[g] = xn[g];
   }
 }
 
@@ -469,6 +460,54 @@ __global__ void k_sprm_dx(SprmP s, const float* __restrict__ Gr, float* dx) {
   dx[idx] = fadd(fadd(0.0f, part[0]), fadd(0.0f, part[1]));  // dx += dx_rev (both from zero)
 }
 
+// dx from the time-major gradients Gt[g][d][t][r][j] (H == 32, Es <= 8): the
+// 3*H terms of one (row, step, direction) are three contiguous 128-byte
+// vectors, read with LDG.128 and shared by the Es threads of the position;
+// the input weights sit in shared memory. Same chain order as k_sprm_dx.
+__global__ void __launch_bounds__(256) k_sprm_dx_t(SprmP s, const float* __restrict__ Gt, float* dx) {
+  constexpr int H = 32;
+  __shared__ __align__(16) float sw[2][3][8][H];  // [d][gate n,r,z][i][q]
+  const int R = s.R, T = s.T, Es = s.Es;
+  const float* W = s.w;
+  const int gates[3] = {WIN, WIR, WIZ};
+  for (int e = threadIdx.x; e < 2 * 3 * Es * H; e += blockDim.x) {
+    const int d = e / (3 * Es * H), rem = e % (3 * Es * H), u = rem / (Es * H), iq = rem % (Es * H);
+    sw[d][u][iq / H][iq % H] = W[goff(s.offs, d, gates[u]) + iq];
+  }
+  __syncthreads();
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t RT = int64_t(R) * T;
+  if (idx >= RT * Es) return;
+  const int i = int(idx % Es);
+  const int64_t rt = idx / Es;
+  const int r = int(rt / T), t = int(rt % T);
+  const int64_t TRH = RT * H;
+  float part[2];
+#pragma unroll
+  for (int d = 0; d < 2; ++d) {
+    const int own_t = d ? (T - 1 - t) : t;
+    float acc = 0.0f;
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const float4* gp =
+          reinterpret_cast<const float4*>(Gt + int64_t(u * 2 + d) * TRH + (int64_t(own_t) * R + r) * H);
+      float4 g4[H / 4];
+#pragma unroll
+      for (int q4 = 0; q4 < H / 4; ++q4) g4[q4] = __ldg(gp + q4);
+      const float* w = sw[d][u][i];
+#pragma unroll
+      for (int q4 = 0; q4 < H / 4; ++q4) {
+        acc = mac(acc, g4[q4].x, w[4 * q4 + 0]);
+        acc = mac(acc, g4[q4].y, w[4 * q4 + 1]);
+        acc = mac(acc, g4[q4].z, w[4 * q4 + 2]);
+        acc = mac(acc, g4[q4].w, w[4 * q4 + 3]);
+      }
+    }
+    part[d] = acc;
+  }
+  dx[idx] = fadd(fadd(0.0f, part[0]), fadd(0.0f, part[1]));  // dx += dx_rev (both from zero)
+}
+
 // emb grad: grad[tok][j] += dx[r][t][j], (r,t) row-major order (layers.cpp:117-125)
 __global__ void k_sprm_emb_grad(SprmP s, const uint32_t* __restrict__ ctx,
                                 const float* __restrict__ dx, float* grad_emb) {
@@ -511,7 +550,8 @@ void launch_sprm_prep(const uint32_t* tokens, const int64_t* pos, const SprmP& s
 void launch_sprm_fwd(const SprmP& s, const uint32_t* ctx, const float* tab, float* tape, float* fin,
                      cudaStream_t st) {
   if (s.H == 32) {
-    k_sprm_fwd32<<<unsigned(2 * ((s.R + 15) / 16)), 256, 0, st>>>(s, ctx, tab, tape, fin);
+    k_sprm_fwd32<<<unsigned(2 * ((s.R + kFwdWarps - 1) / kFwdWarps)), kFwdWarps * 32, 0, st>>>(
+        s, ctx, tab, tape, fin);
     return;
   }
   k_sprm_fwd<<<unsigned(2 * ((s.R + 7) / 8)), 256, 0, st>>>(s, ctx, tab, tape, fin);
@@ -523,18 +563,26 @@ void launch_sprm_ce(const SprmP& s, const uint32_t* tokens, const int64_t* pos, 
 void launch_sprm_tanh_grad(float* dbact, const float* bact, int64_t n, cudaStream_t st) {
   k_sprm_tanh_grad<<<unsigned((n + 255) / 256), 256, 0, st>>>(dbact, bact, n);
 }
-void launch_sprm_bptt(const SprmP& s, const float* tape, const float* dfin, float* Gt, float* G,
+void launch_sprm_bptt(const SprmP& s, const float* tape, const float* dfin, float* Gt,
                       cudaStream_t st) {
   if (s.H == 32)
-    k_sprm_bptt32<<<unsigned(2 * ((s.R + 15) / 16)), 256, 0, st>>>(s, tape, dfin, Gt);
+    k_sprm_bptt32<<<unsigned(2 * ((s.R + kBpttWarps - 1) / kBpttWarps)), kBpttWarps * 32, 0, st>>>(
+        s, tape, dfin, Gt);
   else
     k_sprm_bptt<<<unsigned(2 * ((s.R + 7) / 8)), 256, 0, st>>>(s, tape, dfin, Gt);
+}
+void launch_sprm_transpose(const SprmP& s, const float* Gt, float* G, cudaStream_t st) {
   const int64_t RT = int64_t(s.R) * s.T;
   dim3 grid(unsigned((RT + 31) / 32), unsigned((s.H + 31) / 32), 10);
   k_sprm_transpose<<<grid, dim3(32, 8), 0, st>>>(s, Gt, G);
 }
-void launch_sprm_dx(const SprmP& s, const float* G, float* dx, cudaStream_t st) {
+bool sprm_dx_time_major(const SprmP& s) { return s.H == 32 && s.Es <= 8; }
+void launch_sprm_dx(const SprmP& s, const float* G, const float* Gt, float* dx, cudaStream_t st) {
   const int64_t n = int64_t(s.R) * s.T * s.Es;
+  if (sprm_dx_time_major(s) && Gt) {
+    k_sprm_dx_t<<<unsigned((n + 255) / 256), 256, 0, st>>>(s, Gt, dx);
+    return;
+  }
   k_sprm_dx<<<unsigned((n + 255) / 256), 256, 0, st>>>(s, G, dx);
 }
 void launch_sprm_emb_grad(const SprmP& s, const uint32_t* ctx, const float* dx, float* grad_emb,

@@ -7,4 +7,6 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 400_000
 raw = P.synth("genome", n, 5, 10)
 st = P.PipelineStats()
 b = P.compress(raw, P.CompressConfig(workers=4, selector_threshold=0), st)
-print("flags", b[5], "launches", st.timing.kernel_launches, "total_ms", round(st.timing.total_ms, 1))
+t = st.timing
+print("flags", b[5], "launches", t.kernel_launches, "total_ms", round(t.total_ms, 1), "sprm_ms",
+      round(t.sprm_ms, 1), "model_ms", round(t.model_ms, 1))
