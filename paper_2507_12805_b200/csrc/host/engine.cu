@@ -603,8 +603,9 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     gemm(GemmP{datt.p, s_rh, H, W_(DmLayout::OW), P, H, dctx.p, s_rh, H, nullptr, 0, nullptr, 0, 0,
                R, H, H, 0, 0, 0},
          false, true);
-    launch_attn_bwd(q.p, kk.p, vv.p, wts.p, dctx.p, dq.p, dk.p, dv.p, s_rh, s_kv, s_w, dd, inv_hd,
-                    act, na, st);
+    const AttnDx fx{W_(DmLayout::KW), W_(DmLayout::VW), P, dx.p, s_x};
+    const bool dx_fused = launch_attn_bwd(q.p, kk.p, vv.p, wts.p, dctx.p, dq.p, dk.p, dv.p, s_rh,
+                                          s_kv, s_w, dd, inv_hd, fx, act, na, st);
     ++run.launches;
     // q/k/v projections: weight+bias grads, then dx = dk Wk^T + dv Wv^T, dxl = dq Wq^T
     // dWk|dbk and dWv|dbv: reductions over all R*T rows of feature-major x, dk, dv
@@ -621,12 +622,15 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
                     E, H, R, 1, 2, 0},
               true, false);
     // dx = dk Wk^T + dv Wv^T (k terms then v terms), dk/dv feature-major
-    gemm(GemmP{dk.p, s_kv, RT, W_(DmLayout::KW), P, H, dx.p, s_x, E, nullptr, 0, nullptr, 0, 0,
-               R * T, E, H, 0, 0, 0},
-         true, true);
-    gemm(GemmP{dv.p, s_kv, RT, W_(DmLayout::VW), P, H, dx.p, s_x, E, nullptr, 0, nullptr, 0, 0,
-               R * T, E, H, 0, 2, 0},
-         true, true);
+    // (formed inside the attention backward when it could stage them)
+    if (!dx_fused) {
+      gemm(GemmP{dk.p, s_kv, RT, W_(DmLayout::KW), P, H, dx.p, s_x, E, nullptr, 0, nullptr, 0, 0,
+                 R * T, E, H, 0, 0, 0},
+           true, true);
+      gemm(GemmP{dv.p, s_kv, RT, W_(DmLayout::VW), P, H, dx.p, s_x, E, nullptr, 0, nullptr, 0, 0,
+                 R * T, E, H, 0, 2, 0},
+           true, true);
+    }
     gemm(GemmP{dq.p, s_rh, H, W_(DmLayout::QW), P, H, dxl.p, s_re, E, nullptr, 0, nullptr, 0, 0, R,
                E, H, 0, 0, 0},
          false, true);

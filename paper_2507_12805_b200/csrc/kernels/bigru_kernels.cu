@@ -109,19 +109,20 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
       hh01 = f2_mac(hh01, h01, wn);
       hh23 = f2_mac(hh23, h23, wn);
     }
-    const float arv[kRPW] = {f2_lo(ar01), f2_hi(ar01), f2_lo(ar23), f2_hi(ar23)};
-    const float azv[kRPW] = {f2_lo(az01), f2_hi(az01), f2_lo(az23), f2_hi(az23)};
-    const float hhv[kRPW] = {f2_lo(hh01), f2_hi(hh01), f2_lo(hh23), f2_hi(hh23)};
+    // gates of row pairs (0,1), (2,3) through the paired det functions
     const float4 hp = *reinterpret_cast<const float4*>(&sh[wl][cur][jj][0]);
-    const float hprev[kRPW] = {hp.x, hp.y, hp.z, hp.w};
-    float hn[kRPW];
+    const f2_t an01 = f2_pack(an[0], an[1]), an23 = f2_pack(an[2], an[3]);
+    const f2_t rv01 = det_sigmoid2(ar01), rv23 = det_sigmoid2(ar23);
+    const f2_t zv01 = det_sigmoid2(az01), zv23 = det_sigmoid2(az23);
+    const f2_t nv01 = det_tanh2(f2_add(an01, f2_mul(rv01, hh01)));
+    const f2_t nv23 = det_tanh2(f2_add(an23, f2_mul(rv23, hh23)));
+    const f2_t one = f2_bcast(1.0f);
+    const f2_t hn01 = f2_add(f2_mul(f2_sub(one, zv01), nv01), f2_mul(zv01, f2_pack(hp.x, hp.y)));
+    const f2_t hn23 = f2_add(f2_mul(f2_sub(one, zv23), nv23), f2_mul(zv23, f2_pack(hp.z, hp.w)));
+    const float hn[kRPW] = {f2_lo(hn01), f2_hi(hn01), f2_lo(hn23), f2_hi(hn23)};
 #pragma unroll
-    for (int u = 0; u < kRPW; ++u) {
-      const float rv = det_sigmoid(arv[u]), zv = det_sigmoid(azv[u]);
-      const float nv = det_tanh(fadd(an[u], fmul(rv, hhv[u])));
-      hn[u] = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, hprev[u]));
+    for (int u = 0; u < kRPW; ++u)
       if (act && rv_ok[u]) out[c * work_cs + (int64_t(r0 + u) * T + tt) * 2 * H + dir * H + j] = hn[u];
-    }
     if (act) *reinterpret_cast<float4*>(&sh[wl][cur ^ 1][j][0]) = make_float4(hn[0], hn[1], hn[2], hn[3]);
     __syncwarp();
     cur ^= 1;
@@ -241,20 +242,18 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec_fused(
       hh01 = f2_mac(hh01, h01, wn);
       hh23 = f2_mac(hh23, h23, wn);
     }
-    const float arv[kRPW] = {f2_lo(ar01), f2_hi(ar01), f2_lo(ar23), f2_hi(ar23)};
-    const float azv[kRPW] = {f2_lo(az01), f2_hi(az01), f2_lo(az23), f2_hi(az23)};
-    const float hhv[kRPW] = {f2_lo(hh01), f2_hi(hh01), f2_lo(hh23), f2_hi(hh23)};
-    const float anv[kRPW] = {f2_lo(xn01), f2_hi(xn01), f2_lo(xn23), f2_hi(xn23)};
     const float4 hp = *reinterpret_cast<const float4*>(&sh[wl][cur][j][0]);
-    const float hprev[kRPW] = {hp.x, hp.y, hp.z, hp.w};
-    float hn[kRPW];
+    const f2_t rv01 = det_sigmoid2(ar01), rv23 = det_sigmoid2(ar23);
+    const f2_t zv01 = det_sigmoid2(az01), zv23 = det_sigmoid2(az23);
+    const f2_t nv01 = det_tanh2(f2_add(xn01, f2_mul(rv01, hh01)));
+    const f2_t nv23 = det_tanh2(f2_add(xn23, f2_mul(rv23, hh23)));
+    const f2_t one = f2_bcast(1.0f);
+    const f2_t hn01 = f2_add(f2_mul(f2_sub(one, zv01), nv01), f2_mul(zv01, f2_pack(hp.x, hp.y)));
+    const f2_t hn23 = f2_add(f2_mul(f2_sub(one, zv23), nv23), f2_mul(zv23, f2_pack(hp.z, hp.w)));
+    const float hn[kRPW] = {f2_lo(hn01), f2_hi(hn01), f2_lo(hn23), f2_hi(hn23)};
 #pragma unroll
-    for (int u = 0; u < kRPW; ++u) {
-      const float rv = det_sigmoid(arv[u]), zv = det_sigmoid(azv[u]);
-      const float nv = det_tanh(fadd(anv[u], fmul(rv, hhv[u])));
-      hn[u] = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, hprev[u]));
+    for (int u = 0; u < kRPW; ++u)
       if (out && rv_ok[u]) out[c * work_cs + (int64_t(r0 + u) * T + tt) * 2 * HS + dir * HS + j] = hn[u];
-    }
     *reinterpret_cast<float4*>(&sh[wl][cur ^ 1][j][0]) = make_float4(hn[0], hn[1], hn[2], hn[3]);
     cur ^= 1;
   }

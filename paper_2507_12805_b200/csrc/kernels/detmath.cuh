@@ -100,4 +100,57 @@ __device__ __forceinline__ float det_tanh(float x) {
   return x < 0.0f ? -t : t;
 }
 
+// ---- paired forms: two independent lanes through exactly the scalar
+// functions' operation sequences (arithmetic on f32x2; the clamps, floor,
+// int conversion, exponent assembly, sign tests and the correctly rounded
+// divisions per lane), so each half is bit-identical to the scalar result.
+__device__ __forceinline__ f2_t f2_sub(f2_t a, f2_t b) {
+  f2_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+__device__ __forceinline__ f2_t det_exp2(f2_t x2) {
+  float xl = f2_lo(x2), xh = f2_hi(x2);
+  if (xl > 87.0f) xl = 87.0f;
+  if (xl < -87.0f) xl = -87.0f;
+  if (xh > 87.0f) xh = 87.0f;
+  if (xh < -87.0f) xh = -87.0f;
+  const f2_t x = f2_pack(xl, xh);
+  const f2_t t = f2_add(f2_mul(x, f2_bcast(1.4426950408889634f)), f2_bcast(0.5f));
+  const float nfl = floorf(f2_lo(t)), nfh = floorf(f2_hi(t));
+  const int nl = int(nfl), nh = int(nfh);
+  const f2_t nf = f2_pack(nfl, nfh);
+  f2_t f = f2_sub(x, f2_mul(nf, f2_bcast(0.693359375f)));
+  f = f2_sub(f, f2_mul(nf, f2_bcast(-2.12194440e-4f)));
+  f2_t p = f2_bcast(1.0f / 720.0f);
+  p = f2_add(f2_mul(p, f), f2_bcast(1.0f / 120.0f));
+  p = f2_add(f2_mul(p, f), f2_bcast(1.0f / 24.0f));
+  p = f2_add(f2_mul(p, f), f2_bcast(1.0f / 6.0f));
+  p = f2_add(f2_mul(p, f), f2_bcast(0.5f));
+  p = f2_add(f2_mul(p, f), f2_bcast(1.0f));
+  p = f2_add(f2_mul(p, f), f2_bcast(1.0f));
+  return f2_mul(p, f2_pack(__uint_as_float(uint32_t(nl + 127) << 23),
+                           __uint_as_float(uint32_t(nh + 127) << 23)));
+}
+
+__device__ __forceinline__ f2_t det_sigmoid2(f2_t x) {
+  const float xl = f2_lo(x), xh = f2_hi(x);
+  const bool pl = xl >= 0.0f, ph = xh >= 0.0f;
+  const f2_t e = det_exp2(f2_pack(pl ? -xl : xl, ph ? -xh : xh));
+  const f2_t den = f2_add(f2_bcast(1.0f), e);
+  return f2_pack(fdiv(pl ? 1.0f : f2_lo(e), f2_lo(den)), fdiv(ph ? 1.0f : f2_hi(e), f2_hi(den)));
+}
+
+__device__ __forceinline__ f2_t det_tanh2(f2_t x) {
+  const float xl = f2_lo(x), xh = f2_hi(x);
+  float al = xl < 0.0f ? -xl : xl, ah = xh < 0.0f ? -xh : xh;
+  if (al > 9.0f) al = 9.0f;
+  if (ah > 9.0f) ah = 9.0f;
+  const f2_t den = f2_add(det_exp2(f2_mul(f2_bcast(2.0f), f2_pack(al, ah))), f2_bcast(1.0f));
+  const f2_t t = f2_sub(f2_bcast(1.0f), f2_pack(fdiv(2.0f, f2_lo(den)), fdiv(2.0f, f2_hi(den))));
+  const float tl = f2_lo(t), th = f2_hi(t);
+  return f2_pack(xl < 0.0f ? -tl : tl, xh < 0.0f ? -th : th);
+}
+
 }  // namespace pmklc_b200

@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_fwd_row(
 __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
     const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
     const float* __restrict__ wts, const float* __restrict__ dctx, float* dq, float* dkT,
-    float* dvT, int64_t cs_q, int64_t cs_kv, int64_t cs_w, DmDims d, float inv,
+    float* dvT, int64_t cs_q, int64_t cs_kv, int64_t cs_w, DmDims d, float inv, AttnDx fx,
     const TickDesc* __restrict__ td) {
   extern __shared__ __align__(128) float sm[];
   if (blockIdx.y >= unsigned(td->n_act)) return;
@@ -710,12 +710,26 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
   float* Ds = Vs + T * HP;    // [NH][T]: ds_t per head
   float* Qs = Ds + d.NH * T;  // [H]
   float* Cs = Qs + H;         // dctx row [H]
+  // fused dx (fx.dx set, NH == warps): this row's dk, dv [T][H+1] and Wk, Wv [E][H+1]
+  const bool fuse = fx.dx != nullptr;
+  float* Dk = Cs + H;
+  float* Dv = Dk + T * (H + 1);
+  float* Wks = Dv + T * (H + 1);
+  float* Wvs = Wks + d.E * (H + 1);
   const int64_t ko = c * cs_kv + int64_t(r) * T * H;
   stage_rows(Ks, k + ko, T, H);
   stage_rows(Vs, v + ko, T, H);
   for (int i = threadIdx.x; i < H; i += blockDim.x) {
     Qs[i] = q[c * cs_q + int64_t(r) * H + i];
     Cs[i] = dctx[c * cs_q + int64_t(r) * H + i];
+  }
+  if (fuse) {  // transposed: Wks[h][e] = W_k[e][h] (e pairs adjacent for LDS.64)
+    const float* wk = fx.wk + c * fx.w_cs;
+    const float* wv = fx.wv + c * fx.w_cs;
+    for (int i = threadIdx.x; i < d.E * H; i += blockDim.x) {
+      Wks[(i % H) * d.E + i / H] = __ldg(wk + i);
+      Wvs[(i % H) * d.E + i / H] = __ldg(wv + i);
+    }
   }
   __syncthreads();
   if (h >= d.NH) return;
@@ -733,7 +747,9 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
       const float* vr = Vs + t * HP + h * HD;
       float acc = 0.0f;
       for (int dd = 0; dd < HD; ++dd) {
-        dvT[to + int64_t(dd) * RT + t] = fadd(0.0f, fmul(wt, dc[dd]));
+        const float dvv = fadd(0.0f, fmul(wt, dc[dd]));
+        dvT[to + int64_t(dd) * RT + t] = dvv;
+        if (fuse) Dv[t * (H + 1) + h * HD + dd] = dvv;
         acc = mac(acc, dc[dd], vr[dd]);
       }
       dsw[t] = acc;  // dwt_t, turned into ds_t below
@@ -746,7 +762,11 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
   for (int t = lane; t < T; t += 32) {
     const float ds = fmul(fmul(w[t], fsub(dsw[t], dot)), inv);
     dsw[t] = ds;
-    for (int dd = 0; dd < HD; ++dd) dkT[to + int64_t(dd) * RT + t] = fadd(0.0f, fmul(ds, Qs[h * HD + dd]));
+    for (int dd = 0; dd < HD; ++dd) {
+      const float dkv = fadd(0.0f, fmul(ds, Qs[h * HD + dd]));
+      dkT[to + int64_t(dd) * RT + t] = dkv;
+      if (fuse) Dk[t * (H + 1) + h * HD + dd] = dkv;
+    }
   }
   __syncwarp();
   // dq[d] = 0 + sum_t ds_t*k_t[d]
@@ -754,6 +774,31 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
     float acc = 0.0f;
     for (int t = 0; t < T; ++t) acc = mac(acc, dsw[t], Ks[t * HP + h * HD + lane]);
     dq[c * cs_q + int64_t(r) * H + h * HD + lane] = acc;
+  }
+  if (!fuse) return;
+  // dx[r][t][e] = (0 + dk_t . W_k[e]) then + dv_t . W_v[e], h ascending: the
+  // chain of the two accumulating GEMMs it replaces (Linear::backward x2,
+  // layers.cpp:176-183; K terms first, layers.cpp:505-512)
+  __syncthreads();
+  // thread = (t, e pair): the two chains of a pair run as one paired chain
+  float* dxr = fx.dx + c * fx.dx_cs + int64_t(r) * T * d.E;
+  const int EP = d.E / 2;
+  for (int o = threadIdx.x; o < T * EP; o += blockDim.x) {
+    const int t = o / EP, e = 2 * (o % EP);
+    const float* dkr = Dk + t * (H + 1);
+    const float* dvr = Dv + t * (H + 1);
+    f2_t acc = 0;
+#pragma unroll 8
+    for (int hh = 0; hh < H; ++hh) {
+      const float2 w2 = *reinterpret_cast<const float2*>(Wks + hh * d.E + e);
+      acc = f2_mac(acc, f2_bcast(dkr[hh]), f2_pack(w2.x, w2.y));
+    }
+#pragma unroll 8
+    for (int hh = 0; hh < H; ++hh) {
+      const float2 w2 = *reinterpret_cast<const float2*>(Wvs + hh * d.E + e);
+      acc = f2_mac(acc, f2_bcast(dvr[hh]), f2_pack(w2.x, w2.y));
+    }
+    *reinterpret_cast<float2*>(dxr + t * d.E + e) = make_float2(f2_lo(acc), f2_hi(acc));
   }
 }
 
@@ -1231,26 +1276,33 @@ void launch_attn_fwd(const float* q, const float* k, const float* v, float* wts,
   k_attn_fwd<<<grid, 256, 0, st>>>(q, k, v, wts, cx, cs_q, cs_kv, cs_w, d, inv, td);
 }
 
-void launch_attn_bwd(const float* q, const float* k, const float* v, const float* wts,
+bool launch_attn_bwd(const float* q, const float* k, const float* v, const float* wts,
                      const float* dctx, float* dq, float* dk, float* dv, int64_t cs_q,
-                     int64_t cs_kv, int64_t cs_w, DmDims d, float inv, const TickDesc* td,
-                     int max_active, cudaStream_t st) {
-  if (max_active <= 0) return;
-  const size_t smem = attn_row_smem(d) + d.H * sizeof(float);
-  if (d.NH <= 8 && d.H % 4 == 0 && smem <= 200 * 1024) {
+                     int64_t cs_kv, int64_t cs_w, DmDims d, float inv, const AttnDx& fx,
+                     const TickDesc* td, int max_active, cudaStream_t st) {
+  if (max_active <= 0) return fx.dx != nullptr;
+  const size_t base = attn_row_smem(d) + d.H * sizeof(float);
+  const size_t extra = (size_t(2) * d.T * (d.H + 1) + size_t(2) * d.E * (d.H + 1)) * sizeof(float);
+  if (d.NH <= 8 && d.H % 4 == 0 && base <= 200 * 1024) {
+    const bool fuse = fx.dx && d.NH * 32 == kRowThreads && d.E % 2 == 0 &&
+                      base + extra <= 200 * 1024;
+    const size_t smem = base + (fuse ? extra : 0);
     static size_t attr = 0;
     if (smem > attr) {
       cudaFuncSetAttribute(k_attn_bwd_row, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       attr = smem;
     }
+    AttnDx f = fx;
+    if (!fuse) f.dx = nullptr;
     k_attn_bwd_row<<<dim3(d.R, max_active), kRowThreads, smem, st>>>(
-        q, k, v, wts, dctx, dq, dk, dv, cs_q, cs_kv, cs_w, d, inv, td);
-    return;
+        q, k, v, wts, dctx, dq, dk, dv, cs_q, cs_kv, cs_w, d, inv, f, td);
+    return fuse;
   }
   const int64_t warps = int64_t(d.R) * d.NH;
   dim3 grid(unsigned((warps * 32 + 255) / 256), max_active);
   k_attn_bwd<<<grid, 256, 0, st>>>(q, k, v, wts, dctx, dq, dk, dv, cs_q, cs_kv, cs_w, d, inv,
                                    td);
+  return false;
 }
 
 void launch_emb_grad(const uint32_t* ctx, int64_t ctx_cs, const float* dx, int64_t dx_cs,

@@ -106,11 +106,17 @@ void launch_embed(const uint32_t* tokens, ChunkGeo geo, const float* params,
 void launch_attn_fwd(const float* q, const float* k, const float* v, float* wts, float* cx,
                      int64_t cs_q, int64_t cs_kv, int64_t cs_w, DmDims d, float inv,
                      const TickDesc* td, int max_active, cudaStream_t st);
-// Attention backward core (layers.cpp:480-512)
-void launch_attn_bwd(const float* q, const float* k, const float* v, const float* wts,
+// Attention backward core (layers.cpp:480-512). With fx.dx set it also forms
+// dx = dk W_k^T + dv W_v^T for the row's positions (the two projection-input
+// gradient GEMMs, same chain) and returns true; false: the caller runs them.
+struct AttnDx {
+  const float* wk; const float* wv; int64_t w_cs;  // W_k, W_v [E][H] per chunk
+  float* dx; int64_t dx_cs;                        // dx [R*T][E] per chunk, or nullptr
+};
+bool launch_attn_bwd(const float* q, const float* k, const float* v, const float* wts,
                      const float* dctx, float* dq, float* dk, float* dv, int64_t cs_q,
-                     int64_t cs_kv, int64_t cs_w, DmDims d, float inv, const TickDesc* td,
-                     int max_active, cudaStream_t st);
+                     int64_t cs_kv, int64_t cs_w, DmDims d, float inv, const AttnDx& fx,
+                     const TickDesc* td, int max_active, cudaStream_t st);
 // PositionalEmbedding + Embedding backward (layers.cpp:117-125,147-155)
 void launch_embed_bwd(const uint32_t* ctx, int64_t ctx_cs, const float* dx, int64_t dx_cs,
                       const float* dxl, int64_t dxl_cs, float* grads, int64_t g_cs,

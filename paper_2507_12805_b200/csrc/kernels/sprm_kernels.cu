@@ -187,7 +187,8 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_sprm_fwd32(SprmP s, const ui
         hh = mac(hh, hq[u], wnr[4 * q4 + u]);
       }
     }
-    const float rv = det_sigmoid(f2_lo(arz)), zv = det_sigmoid(f2_hi(arz));
+    const f2_t rz = det_sigmoid2(arz);
+    const float rv = f2_lo(rz), zv = f2_hi(rz);
     const float nv = det_tanh(fadd(xc[2], fmul(rv, hh)));
     const float hv = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, h[j]));
     const int64_t o = (int64_t(t) * R + r) * H + j;
