@@ -630,10 +630,10 @@ __host__ __device__ inline size_t attn_row_smem(const DmDims& d) {
 __device__ __forceinline__ void stage_rows(float* dst, const float* src, int T, int H) {
   // src [T][H] contiguous (H multiple of 4) -> dst rows of H+4
   const int nv = T * (H / 4);
+  // by cp.async (no per-copy stall); the caller commits, waits and syncs
   for (int i = threadIdx.x; i < nv; i += blockDim.x) {
     const int t = i / (H / 4), v4 = i % (H / 4);
-    *reinterpret_cast<float4*>(dst + t * (H + 4) + 4 * v4) =
-        __ldg(reinterpret_cast<const float4*>(src + int64_t(t) * H + 4 * v4));
+    cp_async16(dst + t * (H + 4) + 4 * v4, src + int64_t(t) * H + 4 * v4);
   }
 }
 
@@ -653,7 +653,9 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_fwd_row(
   const int64_t ko = c * cs_kv + int64_t(r) * T * H;
   stage_rows(Ks, k + ko, T, H);
   stage_rows(Vs, v + ko, T, H);
+  cp_async_commit();
   for (int i = threadIdx.x; i < H; i += blockDim.x) Qs[i] = q[c * cs_q + int64_t(r) * H + i];
+  cp_async_wait<0>();
   __syncthreads();
   if (h >= d.NH) return;
   const float* qh = Qs + h * HD;
@@ -662,7 +664,13 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_fwd_row(
   for (int t = lane; t < T; t += 32) {
     const float* kr = Ks + t * HP + h * HD;
     float s = 0.0f;
-    for (int dd = 0; dd < HD; ++dd) s = mac(s, qh[dd], kr[dd]);
+    for (int d0 = 0; d0 < HD; d0 += 4) {  // LDS.128 per 4 dims: conflict-free across t
+      const float4 k4 = *reinterpret_cast<const float4*>(kr + d0);
+      const float kv[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (d0 + u < HD) s = mac(s, qh[d0 + u], kv[u]);
+    }
     s = fmul(s, inv);
     wrow[t] = s;
     mx = fmaxf(mx, s);
@@ -712,10 +720,11 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
   float* Cs = Qs + H;         // dctx row [H]
   // fused dx (fx.dx set, NH == warps): this row's dk, dv [T][H+1] and Wk, Wv [E][H+1]
   const bool fuse = fx.dx != nullptr;
-  float* Dk = Cs + H;
-  float* Dv = Dk + T * (H + 1);
-  float* Wks = Dv + T * (H + 1);
-  float* Wvs = Wks + d.E * (H + 1);
+  const int DP = (T * (H + 1) + 3) & ~3;  // 16-byte aligned regions
+  float* Dk = Cs + ((H + 3) & ~3);
+  float* Dv = Dk + DP;
+  float* Wks = Dv + DP;  // [H][E]
+  float* Wvs = Wks + ((d.E * H + 3) & ~3);
   const int64_t ko = c * cs_kv + int64_t(r) * T * H;
   stage_rows(Ks, k + ko, T, H);
   stage_rows(Vs, v + ko, T, H);
@@ -723,14 +732,16 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
     Qs[i] = q[c * cs_q + int64_t(r) * H + i];
     Cs[i] = dctx[c * cs_q + int64_t(r) * H + i];
   }
-  if (fuse) {  // transposed: Wks[h][e] = W_k[e][h] (e pairs adjacent for LDS.64)
+  if (fuse) {  // transposed: Wks[h][e] = W_k[e][h] (e runs contiguous for LDS.128)
     const float* wk = fx.wk + c * fx.w_cs;
     const float* wv = fx.wv + c * fx.w_cs;
     for (int i = threadIdx.x; i < d.E * H; i += blockDim.x) {
-      Wks[(i % H) * d.E + i / H] = __ldg(wk + i);
-      Wvs[(i % H) * d.E + i / H] = __ldg(wv + i);
+      cp_async4(Wks + (i % H) * d.E + i / H, wk + i);
+      cp_async4(Wvs + (i % H) * d.E + i / H, wv + i);
     }
   }
+  cp_async_commit();
+  cp_async_wait<0>();
   __syncthreads();
   if (h >= d.NH) return;
   const float* w = wts + c * cs_w + (int64_t(r) * d.NH + h) * T;
@@ -746,11 +757,19 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
       const float wt = w[t];
       const float* vr = Vs + t * HP + h * HD;
       float acc = 0.0f;
-      for (int dd = 0; dd < HD; ++dd) {
-        const float dvv = fadd(0.0f, fmul(wt, dc[dd]));
-        dvT[to + int64_t(dd) * RT + t] = dvv;
-        if (fuse) Dv[t * (H + 1) + h * HD + dd] = dvv;
-        acc = mac(acc, dc[dd], vr[dd]);
+      for (int d0 = 0; d0 < HD; d0 += 4) {
+        // one LDS.128 per 4 dims (rows 272 B apart: conflict-free), then the chain
+        const float4 v4 = *reinterpret_cast<const float4*>(vr + d0);
+        const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int dd = d0 + u;
+          if (dd >= HD) break;
+          const float dvv = fadd(0.0f, fmul(wt, dc[dd]));
+          dvT[to + int64_t(dd) * RT + t] = dvv;
+          if (fuse) Dv[t * (H + 1) + h * HD + dd] = dvv;
+          acc = mac(acc, dc[dd], vv[u]);
+        }
       }
       dsw[t] = acc;  // dwt_t, turned into ds_t below
       prod = fmul(wt, acc);
@@ -780,25 +799,33 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
   // chain of the two accumulating GEMMs it replaces (Linear::backward x2,
   // layers.cpp:176-183; K terms first, layers.cpp:505-512)
   __syncthreads();
-  // thread = (t, e pair): the two chains of a pair run as one paired chain
+  // lane = t, warp = a block of 8 e (4 paired chains per lane): W rows are
+  // broadcast LDS.128 reads, the dk/dv row one conflict-free LDS per h
   float* dxr = fx.dx + c * fx.dx_cs + int64_t(r) * T * d.E;
-  const int EP = d.E / 2;
-  for (int o = threadIdx.x; o < T * EP; o += blockDim.x) {
-    const int t = o / EP, e = 2 * (o % EP);
-    const float* dkr = Dk + t * (H + 1);
-    const float* dvr = Dv + t * (H + 1);
-    f2_t acc = 0;
-#pragma unroll 8
-    for (int hh = 0; hh < H; ++hh) {
-      const float2 w2 = *reinterpret_cast<const float2*>(Wks + hh * d.E + e);
-      acc = f2_mac(acc, f2_bcast(dkr[hh]), f2_pack(w2.x, w2.y));
+  for (int eb = h * 8; eb < d.E; eb += d.NH * 8) {
+    for (int t = lane; t < T; t += 32) {
+      const float* dkr = Dk + t * (H + 1);
+      const float* dvr = Dv + t * (H + 1);
+      f2_t acc[4] = {0, 0, 0, 0};
+      auto chain = [&](const float* dr, const float* Ws) {
+#pragma unroll 4
+        for (int hh = 0; hh < H; ++hh) {
+          const f2_t dv2 = f2_bcast(dr[hh]);
+          const float4 wa = *reinterpret_cast<const float4*>(Ws + hh * d.E + eb);
+          const float4 wb = *reinterpret_cast<const float4*>(Ws + hh * d.E + eb + 4);
+          acc[0] = f2_mac(acc[0], dv2, f2_pack(wa.x, wa.y));
+          acc[1] = f2_mac(acc[1], dv2, f2_pack(wa.z, wa.w));
+          acc[2] = f2_mac(acc[2], dv2, f2_pack(wb.x, wb.y));
+          acc[3] = f2_mac(acc[3], dv2, f2_pack(wb.z, wb.w));
+        }
+      };
+      chain(dkr, Wks);
+      chain(dvr, Wvs);
+      float* o = dxr + t * d.E + eb;
+      *reinterpret_cast<float4*>(o) = make_float4(f2_lo(acc[0]), f2_hi(acc[0]), f2_lo(acc[1]), f2_hi(acc[1]));
+      *reinterpret_cast<float4*>(o + 4) =
+          make_float4(f2_lo(acc[2]), f2_hi(acc[2]), f2_lo(acc[3]), f2_hi(acc[3]));
     }
-#pragma unroll 8
-    for (int hh = 0; hh < H; ++hh) {
-      const float2 w2 = *reinterpret_cast<const float2*>(Wvs + hh * d.E + e);
-      acc = f2_mac(acc, f2_bcast(dvr[hh]), f2_pack(w2.x, w2.y));
-    }
-    *reinterpret_cast<float2*>(dxr + t * d.E + e) = make_float2(f2_lo(acc), f2_hi(acc));
   }
 }
 
@@ -1282,9 +1309,10 @@ bool launch_attn_bwd(const float* q, const float* k, const float* v, const float
                      const TickDesc* td, int max_active, cudaStream_t st) {
   if (max_active <= 0) return fx.dx != nullptr;
   const size_t base = attn_row_smem(d) + d.H * sizeof(float);
-  const size_t extra = (size_t(2) * d.T * (d.H + 1) + size_t(2) * d.E * (d.H + 1)) * sizeof(float);
+  const size_t extra = (size_t(2) * (d.T * (d.H + 1) + 3) + size_t(2) * (d.E * d.H + 3) + 8) *
+                       sizeof(float);
   if (d.NH <= 8 && d.H % 4 == 0 && base <= 200 * 1024) {
-    const bool fuse = fx.dx && d.NH * 32 == kRowThreads && d.E % 2 == 0 &&
+    const bool fuse = fx.dx && d.NH * 32 == kRowThreads && d.E % 8 == 0 &&
                       base + extra <= 200 * 1024;
     const size_t smem = base + (fuse ? extra : 0);
     static size_t attr = 0;
