@@ -326,6 +326,33 @@ __device__ __forceinline__ f2_t nt_tile_rpt2(f2_t acc, const float* as, const fl
   return acc;
 }
 
+// Bias row of a ones_row GEMM: C[M][n] = init + sum_k 1*B(k, n), k ascending
+// (exactly the GEMM's chain for its ones row: 1*b == b). Thread per column,
+// 16 loads in flight per batch.
+template <bool BT>
+__global__ void __launch_bounds__(128) k_bias_row(GemmP p, const TickDesc* __restrict__ td) {
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= p.N) return;
+  const float* B = p.B + c * p.b_cs;
+  float* Cr = p.C + c * p.c_cs + int64_t(p.M) * p.ldc;
+  float acc = p.init == 1 ? p.bias[c * p.bias_cs + n] : p.init == 2 ? Cr[n] : 0.0f;
+  const int64_t ks = BT ? 1 : p.ldb;
+  const float* b = B + (BT ? int64_t(n) * p.ldb : n);
+  constexpr int kB = 16;
+  int k = 0;
+  for (; k + kB <= p.K; k += kB) {
+    float v[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) v[u] = __ldg(b + (k + u) * ks);
+#pragma unroll
+    for (int u = 0; u < kB; ++u) acc = fadd(acc, v[u]);
+  }
+  for (; k < p.K; ++k) acc = fadd(acc, __ldg(b + k * ks));
+  Cr[n] = acc;
+}
+
 // VEC: B rows 16-byte aligned and K a multiple of 4 (host-checked).
 // STAGES: ring depth; 3 when the chip is full of warps, 8 when a few warps must
 // cover the L2 latency alone.
@@ -1201,6 +1228,18 @@ __global__ void k_tick_advance(TickDesc* td, const uint32_t* __restrict__ act_pt
 void launch_gemm(const GemmP& p, bool at, bool bt, const TickDesc* td, int max_active,
                  cudaStream_t st) {
   if (max_active <= 0 || p.N <= 0 || p.M + p.ones_row <= 0) return;
+  // A bias row on top of a tile-aligned M (weight gradient + bias gradient,
+  // M = fan-in) would cost a whole extra row of tiles for one row: run the M
+  // rows as a GEMM and the bias row as its own column-sum chain.
+  if (p.ones_row && p.M > 0 && p.M % 64 == 0 && p.nprob <= 1 && !p.mask) {
+    GemmP q = p;
+    q.ones_row = 0;
+    launch_gemm(q, at, bt, td, max_active, st);
+    const dim3 grid(unsigned((p.N + 127) / 128), unsigned(max_active));
+    if (bt) k_bias_row<true><<<grid, 128, 0, st>>>(p, td);
+    else k_bias_row<false><<<grid, 128, 0, st>>>(p, td);
+    return;
+  }
   if (at && bt) gemm_dispatch<true, true>(p, td, max_active, st);
   else if (at) gemm_dispatch<true, false>(p, td, max_active, st);
   else if (bt) gemm_dispatch<false, true>(p, td, max_active, st);
