@@ -206,6 +206,29 @@ def test_encode_chunks_matches_reference_standalone(P, checker):
         assert got[i] == want
 
 
+@pytest.mark.parametrize("flags", [4, 5])
+def test_throughput_regime_matches_reference(P, checker, tmp_path, flags):
+    # 128 independent chunks at the default widths (scale 4, t=32, bs=320) in
+    # one batch: every kernel runs its many-chunk variant (NT reduction with 8
+    # rows per thread, one token group per chunk, fused dx, fused BiGRU layer
+    # 1, ...). Chunks 0, 63 and 127 against the reference's standalone chunk
+    # encoder (4 model steps each after the 32 warm-up steps).
+    spum = ""
+    if flags & 1:
+        spum = str(tmp_path / "spum_s4.bin")
+        P.write_bigru(spum, 3, 32, 4, 0xACE3, layers=2)
+    W, n = 128, 320 * 36
+    raw = P.synth("genome", W * n * 3 + 64, 77, 10)
+    tok, _ = checker.skmer_encode(codes_of(raw), 3, 3)
+    tok = np.ascontiguousarray(tok[:W * n], dtype=np.uint32)
+    got = P.encode_chunks(tok, [n] * W, [b""] * W, flags, 3, 32, 320, 4, 0x5EED,
+                          pub_model_path=spum)
+    for i in (0, 63, 127):
+        want, _, _ = checker.dump_chunk(tok[i * n:(i + 1) * n], flags, 3, 32, 320, 4, 0x5EED,
+                                        pub_path=spum or None)
+        assert got[i] == want, i
+
+
 # ------------------------------------------------------------------ edge cases / errors
 def test_degenerate_inputs(P, checker):
     for raw in [b"", b"A", b"AC", b"ACG", b"NNNN", b"acgt", bytes(range(256)), b"ACGT" * 3]:
