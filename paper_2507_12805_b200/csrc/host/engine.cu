@@ -486,9 +486,32 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   SideStream side;
   auto to_side = [&]() { side.wait_for(st); };
   auto from_side = [&]() { side.join_into(st); };
+  // Cross-tick pipeline of the static predictors: their input is only the
+  // context tokens, which for tick tau+1 are final once tick tau's coder has
+  // run (decode included). So tick tau's graph computes tick tau+1's
+  // predictions on a second side stream, beside tau's DM backward and Adam,
+  // straight into lu/lr (tau's mixer and trainer have consumed them by then).
+  // A prologue computes tick 0's before the first tick.
+  const bool statics = (run.flags & 3) != 0;
+  SideStream pred;
+  DBuf<TickDesc> d_td_next(1);
+  DBuf<uint32_t> ctx_next;
+  if (statics) ctx_next.alloc(TW * s_ctx);
+  auto predict_next = [&](cudaStream_t s2) {
+    launch_tick_peek(d_td.p, d_td_next.p, d_act_ptr.p, d_act.p, sch.ticks, s2);
+    launch_ctx_gather(d_tokens, geo, ctx_next.p, s_ctx, dd, d_td_next.p, na, s2);
+    run.launches += 2;
+    if (run.flags & 1)
+      run.launches += launch_bigru_predict(run.pub->params(R), ctx_next.p, s_ctx, bwork.p, s_bw,
+                                           lu.p, s_rv, d_td_next.p, na, s2, d_hot.p);
+    if (run.flags & 2)
+      run.launches += launch_bigru_predict(run.priv->params(R), ctx_next.p, s_ctx, bwork.p, s_bw,
+                                           lr.p, s_rv, d_td_next.p, na, s2);
+  };
   auto enqueue_tick = [&](int64_t probe_tick) {
     const uint64_t l0 = run.launches;
     side.rewind();
+    pred.rewind();
     launch_tick_advance(d_td.p, d_act_ptr.p, d_act.p, d_hand_ptr.p, d_hand.p, sch.ticks, st);
     ++run.launches;
     if (nh > 0) {
@@ -503,18 +526,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     launch_embed(d_tokens, geo, w.p, P, oE, oP, ctx.p, s_ctx, x.p, s_x, xl.p, s_re, dd, act, na,
                  st);
     ++run.launches;
-    // ---------------- static predictors (side stream, beside the DM forward)
-    if (run.flags & 3) {
-      to_side();
-      if (run.flags & 1) {
-        run.launches += launch_bigru_predict(run.pub->params(R), ctx.p, s_ctx, bwork.p, s_bw, lu.p,
-                                             s_rv, act, na, side.s, d_hot.p);
-      }
-      if (run.flags & 2) {
-        run.launches += launch_bigru_predict(run.priv->params(R), ctx.p, s_ctx, bwork.p, s_bw, lr.p,
-                                             s_rv, act, na, side.s);
-      }
-    }
+    // (static predictors of this tick: computed during the previous tick)
     GemmP gp{};
     // K, V over all R*T rows, q over the last position (layers.cpp:437-445)
     // x is feature-major: A(row, e) = xT[e*RT + row]
@@ -542,7 +554,6 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     gemm(GemmP{fo.p, s_rh, H, W_(DmLayout::HW), P, V, lm.p, s_rv, V, W_(DmLayout::HB), P, nullptr,
                0, 0, R, V, H, 0, 1, 0},
          false, false);
-    if (run.flags & 3) from_side();
     // ---------------- mix + quantize + code
     MixP mp{lu.p, lr.p, lm.p, s_rv, probs.p, freq.p, cum.p, s_rv, s_cum, w.p, P, oA, sc.p,
             int(run.flags), R, V, err.p};
@@ -567,6 +578,11 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     launch_bc_dlm(bp, act, na, st);
     launch_alpha_step(bp, act, na, st);
     run.launches += 2;
+    // next tick's static predictions, beside this tick's backward
+    if (statics) {
+      pred.wait_for(st);
+      predict_next(pred.s);
+    }
     // head, ffn, attention output projection (Linear::backward, layers.cpp:176-183).
     // Data gradients stay on the main stream; each weight gradient goes to the
     // side stream as soon as its operands exist (they write disjoint slices of
@@ -640,9 +656,11 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     // Adam over every DM parameter (alpha was updated by k_alpha_step)
     launch_adam(w.p, g.p, m.p, v.p, P, P - 1, sc.p, act, na, st);
     ++run.launches;
+    if (statics) pred.join_into(st);
     check_launch();
     tick_launches = run.launches - l0;
   };
+  if (statics && sch.ticks > 0) predict_next(st);  // prologue: tick 0's predictions
 
   // cross-rank SMP handoffs due at a tick: grouped point-to-point transfers
   // of the whole state slot (w, m, v, Adam scalars) on the engine stream,

@@ -1223,7 +1223,51 @@ __global__ void k_tick_advance(TickDesc* td, const uint32_t* __restrict__ act_pt
   }
 }
 
+// Descriptor of the tick after `cur` (act list only): the static predictors of
+// tick tau+1 run inside tick tau's graph (cross-tick pipeline).
+__global__ void k_tick_peek(const TickDesc* __restrict__ cur, TickDesc* next,
+                            const uint32_t* __restrict__ act_ptr, const int* __restrict__ act_all,
+                            int64_t ticks) {
+  const int64_t t = cur->tick + 1;
+  next->tick = t;
+  next->hand = nullptr;
+  next->n_hand = 0;
+  if (t >= 0 && t < ticks) {
+    next->act = act_all + act_ptr[t];
+    next->n_act = int(act_ptr[t + 1] - act_ptr[t]);
+  } else {
+    next->act = act_all;
+    next->n_act = 0;
+  }
+}
+
+// Context tokens of every active chunk's coded rows (k_embed's ctx gather alone)
+__global__ void k_ctx_gather(const uint32_t* __restrict__ tokens, ChunkGeo geo, uint32_t* ctx,
+                             int64_t ctx_cs, DmDims d, const TickDesc* __restrict__ td) {
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
+  const int64_t RT = int64_t(d.R) * d.T;
+  const int64_t rt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (rt >= RT) return;
+  const int t = int(rt % d.T), r = int(rt / d.T);
+  const uint64_t L = geo.L[c];
+  const uint64_t jstep = uint64_t(d.T) + uint64_t(td->tick - geo.offset[c]);
+  ctx[c * ctx_cs + rt] = tokens[geo.start[c] + uint64_t(r) * L + (jstep - d.T) + t] & uint32_t(d.V - 1);
+}
+
 }  // namespace
+
+void launch_tick_peek(const TickDesc* cur, TickDesc* next, const uint32_t* act_ptr,
+                      const int* act_all, int64_t ticks, cudaStream_t st) {
+  k_tick_peek<<<1, 1, 0, st>>>(cur, next, act_ptr, act_all, ticks);
+}
+void launch_ctx_gather(const uint32_t* tokens, ChunkGeo geo, uint32_t* ctx, int64_t ctx_cs,
+                       DmDims d, const TickDesc* td, int max_active, cudaStream_t st) {
+  if (max_active <= 0) return;
+  const int64_t RT = int64_t(d.R) * d.T;
+  k_ctx_gather<<<dim3(unsigned((RT + 255) / 256), max_active), 256, 0, st>>>(tokens, geo, ctx, ctx_cs,
+                                                                             d, td);
+}
 
 void launch_gemm(const GemmP& p, bool at, bool bt, const TickDesc* td, int max_active,
                  cudaStream_t st) {

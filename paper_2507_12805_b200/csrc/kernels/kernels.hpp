@@ -97,6 +97,12 @@ void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int m
 
 struct DmDims { int R, T, E, H, F, V, NH; };
 
+// cross-tick pipeline: next = the tick after cur (act list only), and the
+// context tokens of that tick's coded rows
+void launch_tick_peek(const TickDesc* cur, TickDesc* next, const uint32_t* act_ptr,
+                      const int* act_all, int64_t ticks, cudaStream_t st);
+void launch_ctx_gather(const uint32_t* tokens, ChunkGeo geo, uint32_t* ctx, int64_t ctx_cs,
+                       DmDims d, const TickDesc* td, int max_active, cudaStream_t st);
 // ctx gather (pipeline.cpp:180-182) + Embedding/PositionalEmbedding forward
 void launch_embed(const uint32_t* tokens, ChunkGeo geo, const float* params,
                   int64_t p_cs, int64_t off_emb, int64_t off_pos, uint32_t* ctx, int64_t ctx_cs,
