@@ -360,8 +360,10 @@ def main():
             ach_tf = hot["flops"] / (hot["ms"] / 1000.0) / 1e12
             units_per_launch = hot["units"] / hot["launches"]
             t = tjson.get("k_bigru_rec_fused")
+            fma_busy = None
             if t and t.get("units"):  # DRAM bytes per chunk-launch x this run's chunks per launch
                 traffic = t["dram_bytes_per_launch"] / t["units"] * units_per_launch
+                fma_busy = t.get("fma_pipe_busy_pct")
             roof = {"kernel": "k_bigru_rec_fused (SPuM BiGRU layer 1: input projection + "
                               "recurrence, R=320 rows x 2 dirs x t=32 steps per chunk)",
                     "bound": "fp32", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
@@ -371,6 +373,9 @@ def main():
                     "chunks_per_launch": units_per_launch,
                     "flops_per_launch": hot["flops"] / hot["launches"],
                     "flops_per_chunk_launch": hot["flops"] / max(hot["units"], 1),
+                    "fma_pipe_busy_pct_ncu": fma_busy,
+                    "note": "achieved counts MAC flops only; the FP32 pipe also runs the exact "
+                            "det-math epilogue and 2 instructions per exact (non-FMA) MAC pair",
                     "peak_source": "live non-FMA FP32 microbenchmark (MEASURED_PEAKS.json has no "
                                    "FP32 figure); EXACT mode cannot use tensor cores"}
         else:  # DM only: the weight-gradient reduction, microbenchmarked live
