@@ -34,6 +34,12 @@ __device__ __forceinline__ void cp_async4(float* smem, const float* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
 }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -56,26 +62,62 @@ __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc*
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int ntiles = (p.K + BK - 1) / BK;
 
+  // 16-byte copies where the global side runs along the smem row (A^T: m,
+  // B: n) and is 16-byte aligned (chunk slots of the parameter array are only
+  // 4-byte aligned, so this is decided per block)
+  auto al16 = [](const float* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  const bool va = AT && BM % 4 == 0 && p.lda % 4 == 0 && al16(A);
+  const bool vb = !BT && BN % 4 == 0 && p.ldb % 4 == 0 && al16(B);
   auto load = [&](int tile) {
     if (tile < ntiles) {
       const int stage = tile % STAGES, k0 = tile * BK;
-      for (int idx = threadIdx.x; idx < BM * BK; idx += NT) {
-        int mm, kk;
-        if (AT) { mm = idx % BM; kk = idx / BM; }  // global contiguous in m
-        else    { kk = idx % BK; mm = idx / BK; }  // global contiguous in k
-        const int m = m0 + mm, k = k0 + kk;
-        if (k < p.K) {
-          if (m < p.M) cp_async4(&As[stage][kk][mm], AT ? A + int64_t(k) * p.lda + m : A + int64_t(m) * p.lda + k);
-          else if (m == p.M && p.ones_row) As[stage][kk][mm] = 1.0f;
+      if (va) {
+        for (int idx = threadIdx.x; idx < BM * BK / 4; idx += NT) {
+          const int mm = (idx % (BM / 4)) * 4, kk = idx / (BM / 4);
+          const int m = m0 + mm, k = k0 + kk;
+          if (k >= p.K) continue;
+          if (m + 3 < p.M) {
+            cp_async16(&As[stage][kk][mm], A + int64_t(k) * p.lda + m);
+          } else {
+            for (int u = 0; u < 4; ++u) {
+              if (m + u < p.M) cp_async4(&As[stage][kk][mm + u], A + int64_t(k) * p.lda + m + u);
+              else if (m + u == p.M && p.ones_row) As[stage][kk][mm + u] = 1.0f;
+            }
+          }
+        }
+      } else {
+        for (int idx = threadIdx.x; idx < BM * BK; idx += NT) {
+          int mm, kk;
+          if (AT) { mm = idx % BM; kk = idx / BM; }  // global contiguous in m
+          else    { kk = idx % BK; mm = idx / BK; }  // global contiguous in k
+          const int m = m0 + mm, k = k0 + kk;
+          if (k < p.K) {
+            if (m < p.M) cp_async4(&As[stage][kk][mm], AT ? A + int64_t(k) * p.lda + m : A + int64_t(m) * p.lda + k);
+            else if (m == p.M && p.ones_row) As[stage][kk][mm] = 1.0f;
+          }
         }
       }
-      for (int idx = threadIdx.x; idx < BN * BK; idx += NT) {
-        int nn, kk;
-        if (BT) { kk = idx % BK; nn = idx / BK; }
-        else    { nn = idx % BN; kk = idx / BN; }
-        const int n = n0 + nn, k = k0 + kk;
-        if (k < p.K && n < p.N)
-          cp_async4(&Bs[stage][kk][nn], BT ? B + int64_t(n) * p.ldb + k : B + int64_t(k) * p.ldb + n);
+      if (vb) {
+        for (int idx = threadIdx.x; idx < BN * BK / 4; idx += NT) {
+          const int nn = (idx % (BN / 4)) * 4, kk = idx / (BN / 4);
+          const int n = n0 + nn, k = k0 + kk;
+          if (k >= p.K) continue;
+          if (n + 3 < p.N) {
+            cp_async16(&Bs[stage][kk][nn], B + int64_t(k) * p.ldb + n);
+          } else {
+            for (int u = 0; u < 4; ++u)
+              if (n + u < p.N) cp_async4(&Bs[stage][kk][nn + u], B + int64_t(k) * p.ldb + n + u);
+          }
+        }
+      } else {
+        for (int idx = threadIdx.x; idx < BN * BK; idx += NT) {
+          int nn, kk;
+          if (BT) { kk = idx % BK; nn = idx / BK; }
+          else    { nn = idx % BN; kk = idx / BN; }
+          const int n = n0 + nn, k = k0 + kk;
+          if (k < p.K && n < p.N)
+            cp_async4(&Bs[stage][kk][nn], BT ? B + int64_t(n) * p.ldb + k : B + int64_t(k) * p.ldb + n);
+        }
       }
     }
     cp_async_commit();  // one group per tile slot, possibly empty
@@ -180,6 +222,19 @@ __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc*
       }
   }
 
+  if constexpr (TN == 4) {  // 16-byte stores of a thread's 4 columns when possible
+    const int n = n0 + tx * TN;
+    if (!p.mask && p.ldc % 4 == 0 && al16(C) && n + 3 < p.N) {
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const int m = m0 + ty * TM + i;
+        if (m < Mx)
+          *reinterpret_cast<float4*>(C + int64_t(m) * p.ldc + n) =
+              make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+      }
+      return;
+    }
+  }
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -228,12 +283,6 @@ void gemm_dispatch(const GemmP& p, const TickDesc* td, int max_active, cudaStrea
 
 // ------------------------------------------------------------------ NT reduction
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem));
-}
 
 // Block = MR output rows x 64 columns (64*MR threads, one output each).
 // K-tiles of 64 are staged by 16-byte cp.async into a 4-deep ring; one staged
