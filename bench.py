@@ -364,8 +364,17 @@ def main():
             if t and t.get("units"):  # DRAM bytes per chunk-launch x this run's chunks per launch
                 traffic = t["dram_bytes_per_launch"] / t["units"] * units_per_launch
                 fma_busy = t.get("fma_pipe_busy_pct")
+            # the same kernel alone on the GPU (no co-running DM branch), same stamps
+            chunks_iso = max(1, int(round(units_per_launch)))
+            i_ms, i_fl, _ = P.bench_kernel("bigru_fused", chunks_iso, iters=10, device=dev)
+            iso_tf = i_fl / (i_ms / 1000.0) / 1e12 if i_ms > 0 else None
             roof = {"kernel": "k_bigru_rec_fused (SPuM BiGRU layer 1: input projection + "
                               "recurrence, R=320 rows x 2 dirs x t=32 steps per chunk)",
+                    "achieved_isolated": iso_tf,
+                    "frac_isolated": iso_tf / peak_tf if iso_tf else None,
+                    "isolated": f"bench_kernel('bigru_fused', {chunks_iso} chunks): the kernel "
+                                "alone; in situ it shares the SMs with the previous tick's DM "
+                                "backward (cross-tick pipeline)",
                     "bound": "fp32", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
                     "frac": ach_tf / peak_tf, "traffic": traffic,
                     "timing": "in-situ %globaltimer stamps around every launch in the timed steps",

@@ -1576,6 +1576,36 @@ KernelBench bench_kernel(const std::string& name, int device, uint32_t chunks, u
     launch = [=]() { launch_gemm(gp, false, false, tdp, int(chunks), st); };
     kb.flops = 2.0 * double(R) * H * F * chunks;
     kb.bytes = (double(R) * F + double(F) * H + double(R) * H) * 4.0 * chunks;
+  } else if (name == "bigru_fused") {
+    // the SPuM predictor (seeded 2-layer model at these widths) over `chunks`
+    // chunks of random contexts; the fused layer-1 recurrence is timed by the
+    // same device stamps the engine uses (HotTimer), alone on the GPU
+    const Dims gd = Dims::make(64, t, scale);
+    DevBiGru pub;
+    pub.upload(BiGru::seeded(gd, 2, 0xACE3), st);
+    const BiGruP bp = pub.params(int(R));
+    std::vector<uint32_t> hc(size_t(chunks) * RT);
+    Rng rng(12345);
+    for (auto& v : hc) v = uint32_t(rng.next_below(64));
+    DBuf<uint32_t> dctx(hc.size());
+    dctx.upload(hc.data(), hc.size(), st);
+    const int64_t wcs = int64_t(bigru_work_floats(bp));
+    DBuf<float> work(size_t(chunks) * wcs), lg(size_t(chunks) * R * 64);
+    DBuf<HotTimer> hot(1);
+    launch_bigru_predict(bp, dctx.p, RT, work.p, wcs, lg.p, int64_t(R) * 64, tdp, int(chunks), st);
+    CK(cudaMemsetAsync(hot.p, 0, sizeof(HotTimer), st));
+    for (int i = 0; i < iters; ++i)
+      launch_bigru_predict(bp, dctx.p, RT, work.p, wcs, lg.p, int64_t(R) * 64, tdp, int(chunks), st,
+                           hot.p);
+    check_launch();
+    HotTimer h{};
+    CK(cudaMemcpyAsync(&h, hot.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    kb.avg_ms = h.launches ? double(h.ns) * 1e-6 / double(h.launches) : 0.0;
+    const double Hs = double(gd.sh);
+    kb.flops = 2.0 * double(R) * 2.0 * double(t) * 3.0 * Hs * (3.0 * Hs) * chunks;
+    kb.bytes = double(RT) * 2.0 * Hs * 4.0 * chunks;
+    return kb;
   } else {
     raise(errc::config_invalid, "unknown kernel " + name);
   }
