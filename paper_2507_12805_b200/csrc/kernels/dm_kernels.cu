@@ -548,24 +548,42 @@ __global__ void k_embed(const uint32_t* __restrict__ tokens, ChunkGeo geo,
                         const float* __restrict__ params, int64_t p_cs, int64_t off_emb,
                         int64_t off_pos, uint32_t* ctx, int64_t ctx_cs, float* xT, int64_t x_cs,
                         float* xl, int64_t xl_cs, DmDims d, const TickDesc* __restrict__ td) {
+  // thread per coded position (r, t): one token gather, all E features
+  // (x[j] = emb[tok][j] + pos[t][j], feature-major stores coalesced over rt)
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
   const int64_t RT = int64_t(d.R) * d.T;
-  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // = j*RT + rt
-  if (idx >= RT * d.E) return;
-  const int64_t rt = idx % RT;
-  const int j = int(idx / RT);
+  const int64_t rt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (rt >= RT) return;
   const int t = int(rt % d.T), r = int(rt / d.T);
   const uint64_t L = geo.L[c];
   const uint64_t jstep = uint64_t(d.T) + uint64_t(td->tick - geo.offset[c]);  // coded position
   // tokens are < V = 4^k by construction; the mask only guards memory after a
   // decode error (slots past a truncated codestream are never written)
   const uint32_t tok = tokens[geo.start[c] + uint64_t(r) * L + (jstep - d.T) + t] & uint32_t(d.V - 1);
-  if (j == 0) ctx[c * ctx_cs + rt] = tok;
+  ctx[c * ctx_cs + rt] = tok;
   const float* P = params + c * p_cs;
-  const float xv = fadd(P[off_emb + int64_t(tok) * d.E + j], P[off_pos + int64_t(t) * d.E + j]);
-  xT[c * x_cs + idx] = xv;
-  if (t == d.T - 1) xl[c * xl_cs + int64_t(r) * d.E + j] = xv;
+  const float* er = P + off_emb + int64_t(tok) * d.E;
+  const float* pr = P + off_pos + int64_t(t) * d.E;
+  float* xo = xT + c * x_cs + rt;
+  float* lo = t == d.T - 1 ? xl + c * xl_cs + int64_t(r) * d.E : nullptr;
+  constexpr int kU = 8;
+  for (int j0 = 0; j0 < d.E; j0 += kU) {
+    float e[kU], q[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const bool ok = j0 + u < d.E;
+      e[u] = ok ? __ldg(er + j0 + u) : 0.0f;
+      q[u] = ok ? __ldg(pr + j0 + u) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (j0 + u >= d.E) break;
+      const float xv = fadd(e[u], q[u]);
+      xo[int64_t(j0 + u) * RT] = xv;
+      if (lo) lo[j0 + u] = xv;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ attention
@@ -1409,7 +1427,7 @@ void launch_embed(const uint32_t* tokens, ChunkGeo geo, const float* params,
                   float* x, int64_t x_cs, float* xl, int64_t xl_cs, DmDims d, const TickDesc* td,
                   int max_active, cudaStream_t st) {
   if (max_active <= 0) return;
-  const int64_t total = int64_t(d.R) * d.T * d.E;
+  const int64_t total = int64_t(d.R) * d.T;  // one thread per coded position
   dim3 grid(unsigned((total + 255) / 256), max_active);
   k_embed<<<grid, 256, 0, st>>>(tokens, geo, params, p_cs, off_emb, off_pos, ctx, ctx_cs, x,
                                 x_cs, xl, xl_cs, d, td);
