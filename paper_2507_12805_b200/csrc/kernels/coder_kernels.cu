@@ -114,7 +114,28 @@ __global__ void k_mix_quantize(MixP p, const TickDesc* __restrict__ td) {
   assigned = warp_sum_u32(assigned);
   const int64_t deficit = int64_t(kTotal) - int64_t(assigned);
   __syncwarp();
-  if (deficit > 0) {
+  if (deficit > 0 && V <= 64) {
+    // stable_sort by (rem desc, idx asc), then +1 cyclically (coder.cpp:57-66).
+    // V <= 64: each lane holds the remainders of i = lane, lane + 32; the rank
+    // of element i = #{j : r_j > r_i or (r_j == r_i and j < i)} is counted
+    // with two ballots per i (r_i broadcast by shuffle).
+    const uint32_t full = uint32_t(deficit / V), part = uint32_t(deficit % V);
+    const bool h0 = lane < V, h1 = lane + 32 < V;
+    uint32_t f0 = 0, f1 = 0;
+    const double r0 = h0 ? rem_of(pr[lane], f0) : 0.0;
+    const double r1 = h1 ? rem_of(pr[lane + 32], f1) : 0.0;
+    uint32_t rk0 = 0, rk1 = 0;
+    for (int i = 0; i < V; ++i) {
+      const double ri = i < 32 ? __shfl_sync(0xffffffffu, r0, i) : __shfl_sync(0xffffffffu, r1, i - 32);
+      const bool c0 = h0 && (r0 > ri || (r0 == ri && lane < i));
+      const bool c1 = h1 && (r1 > ri || (r1 == ri && lane + 32 < i));
+      const uint32_t rank = __popc(__ballot_sync(0xffffffffu, c0)) + __popc(__ballot_sync(0xffffffffu, c1));
+      if (i == lane) rk0 = rank;
+      if (i == lane + 32) rk1 = rank;
+    }
+    if (h0) fq[lane] = f0 + full + (rk0 < part ? 1u : 0u);
+    if (h1) fq[lane + 32] = f1 + full + (rk1 < part ? 1u : 0u);
+  } else if (deficit > 0) {
     // stable_sort by (rem desc, idx asc), then +1 cyclically (coder.cpp:57-66)
     const uint32_t full = uint32_t(deficit / V), part = uint32_t(deficit % V);
     for (int i = lane; i < V; i += 32) {
