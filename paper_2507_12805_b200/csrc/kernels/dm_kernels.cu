@@ -829,9 +829,12 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
   if (fuse) {  // transposed: Wks[h][e] = W_k[e][h] (e runs contiguous for LDS.128)
     const float* wk = fx.wk + c * fx.w_cs;
     const float* wv = fx.wv + c * fx.w_cs;
+    // destination-ordered (consecutive lanes, consecutive banks); the
+    // strided side is the 4 KB global read, L2-resident
     for (int i = threadIdx.x; i < d.E * H; i += blockDim.x) {
-      cp_async4(Wks + (i % H) * d.E + i / H, wk + i);
-      cp_async4(Wvs + (i % H) * d.E + i / H, wv + i);
+      const int hh = i / d.E, e = i % d.E;
+      cp_async4(Wks + i, wk + e * H + hh);
+      cp_async4(Wvs + i, wv + e * H + hh);
     }
   }
   cp_async_commit();
