@@ -3,10 +3,11 @@
 // skmer encode (reference: core/src/skmer.cpp:16-24, token j = base-4 number of
 // bases [j*s, j*s+k), most significant digit first) is HBM-bound: per base it
 // reads 2 bits (packed) or 1 byte (ASCII) and writes 4*m/n bytes of u32 tokens.
-// Each CTA stages the packed window covering its 2048 tokens in shared memory
-// with 128-bit coalesced loads (halo of k-1 bases included), then every thread
-// extracts 8 consecutive tokens with two 32-bit shared loads + a funnel shift +
-// a 2-bit digit reversal (__brev), and writes them as two 128-bit stores.
+// Each CTA stages the packed window covering its 8192 (s <= 2: 16384) tokens in
+// shared memory with 128-bit coalesced loads (halo of k-1 bases included);
+// every token is two 32-bit shared loads + a funnel shift + a 2-bit digit
+// reversal (__brev), and each warp writes 128-token slabs as lane-contiguous
+// 16-byte stores (512 contiguous bytes per store instruction).
 #include <cstdint>
 
 #include "kernels.hpp"
@@ -16,10 +17,12 @@ namespace pmklc_b200 {
 namespace {
 
 constexpr int kTokThreads = 256;
-constexpr int kTokPerThread = 8;
-constexpr int kTokPerBlock = kTokThreads * kTokPerThread;  // 2048
-// bases per block <= 2047*8 + 8 = 16384 -> 4096 packed bytes; +32 B slack
-constexpr int kStageBytes = (kTokPerBlock * 8 + 8) / 4 + 48;
+// tokens per thread: 64 for strides s <= 2 (larger tiles, fewer blocks),
+// 32 otherwise (a 64-token tile at stride 8 needs 32 KB of staging and leaves
+// too few blocks in flight); both stage <= 16 KB + slack
+constexpr int kTpt = 32, kTptSmallStride = 64;
+constexpr int kStageBytes = (kTokThreads * kTpt * 8 + 16) / 4 + 48;
+static_assert(kTokThreads * kTptSmallStride * 2 <= kTokThreads * kTpt * 8, "staging bound");
 
 __device__ __forceinline__ uint32_t ascii_code(uint32_t c) { return ((c >> 1) ^ (c >> 2)) & 3u; }
 
@@ -31,36 +34,44 @@ __device__ __forceinline__ uint32_t digits_to_token(uint32_t f, uint32_t k) {
   return x >> (32u - 2u * k);
 }
 
-// Extract tokens [j0, j0+2048) from a packed shared-memory window whose first
-// byte holds base `sbase`.
+// Extract tokens [j0, j0 + 256*kTokPerThread) from a packed shared-memory window whose first
+// byte holds base `sbase`. Warp w owns 32*kTokPerThread consecutive tokens as
+// slabs of 128; lane l makes tokens 4l..4l+3 of each slab and writes them
+// with one 16-byte store, so every warp store covers 512 contiguous bytes.
+template <int kTokPerThread>
 __device__ __forceinline__ void emit_tokens(const uint32_t* sw, uint64_t sbase, uint64_t j0,
                                             uint32_t s, uint32_t k, uint32_t* tokens, uint64_t m) {
-  const uint64_t jt = j0 + uint64_t(threadIdx.x) * kTokPerThread;
-  if (jt >= m) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t jw = j0 + uint64_t(w) * 32 * kTokPerThread;
+  if (jw >= m) return;
   const uint32_t mask = (k == 16) ? 0xffffffffu : ((1u << (2u * k)) - 1u);
-  uint32_t out[kTokPerThread];
 #pragma unroll
-  for (int q = 0; q < kTokPerThread; ++q) {
-    const uint64_t bit = ((jt + q) * s - sbase) * 2;  // bit offset in window
-    const uint32_t wi = uint32_t(bit >> 5), sh = uint32_t(bit & 31);
-    const uint32_t lo = sw[wi], hi = sw[wi + 1];
-    const uint32_t f = __funnelshift_r(lo, hi, sh) & mask;
-    out[q] = digits_to_token(f, k);
-  }
-  if (jt + kTokPerThread <= m) {
-    uint4* dst = reinterpret_cast<uint4*>(tokens + jt);
-    dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
-    dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
-  } else {
-    for (int q = 0; q < kTokPerThread && jt + q < m; ++q) tokens[jt + q] = out[q];
+  for (int slab = 0; slab < kTokPerThread / 4; ++slab) {
+    const uint64_t jt = jw + uint64_t(slab) * 128 + uint64_t(lane) * 4;
+    uint32_t out[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t bit = ((jt + q) * s - sbase) * 2;  // bit offset in window
+      const uint32_t wi = uint32_t(bit >> 5), sh = uint32_t(bit & 31);
+      const uint32_t lo = sw[wi], hi = sw[wi + 1];
+      const uint32_t f = __funnelshift_r(lo, hi, sh) & mask;
+      out[q] = digits_to_token(f, k);
+    }
+    if (jt + 4 <= m) {
+      *reinterpret_cast<uint4*>(tokens + jt) = make_uint4(out[0], out[1], out[2], out[3]);
+    } else {
+      for (int q = 0; q < 4 && jt + q < m; ++q) tokens[jt + q] = out[q];
+    }
   }
 }
 
+template <int kTokPerThread>
 __global__ void __launch_bounds__(kTokThreads) k_skmer_packed(const uint8_t* __restrict__ packed,
                                                               uint64_t n, uint32_t s, uint32_t k,
                                                               uint32_t* __restrict__ tokens,
                                                               uint64_t m) {
   __shared__ __align__(16) uint32_t sw[kStageBytes / 4];
+  constexpr int kTokPerBlock = kTokThreads * kTokPerThread;
   const uint64_t j0 = uint64_t(blockIdx.x) * kTokPerBlock;
   const uint64_t jlast = min(j0 + kTokPerBlock, m) - 1;
   const uint64_t b_first = j0 * s, b_end = jlast * s + k;  // bases needed [b_first, b_end)
@@ -75,16 +86,17 @@ __global__ void __launch_bounds__(kTokThreads) k_skmer_packed(const uint8_t* __r
   for (uint64_t i = nvec * 16 + threadIdx.x; i < nbytes + 8; i += kTokThreads)
     sb[i] = i < nbytes ? packed[byte0 + i] : 0;
   __syncthreads();
-  emit_tokens(sw, byte0 * 4, j0, s, k, tokens, m);
+  emit_tokens<kTokPerThread>(sw, byte0 * 4, j0, s, k, tokens, m);
 }
 
 // ASCII / code input: stage 16 bytes per step, pack to 2-bit on the way in.
-template <bool kAscii>
+template <bool kAscii, int kTokPerThread>
 __global__ void __launch_bounds__(kTokThreads) k_skmer_bytes(const uint8_t* __restrict__ in,
                                                              uint64_t n, uint32_t s, uint32_t k,
                                                              uint32_t* __restrict__ tokens,
                                                              uint64_t m) {
   __shared__ __align__(16) uint32_t sw[kStageBytes / 4];
+  constexpr int kTokPerBlock = kTokThreads * kTokPerThread;
   const uint64_t j0 = uint64_t(blockIdx.x) * kTokPerBlock;
   const uint64_t jlast = min(j0 + kTokPerBlock, m) - 1;
   const uint64_t b_first = j0 * s, b_end = jlast * s + k;
@@ -114,7 +126,7 @@ __global__ void __launch_bounds__(kTokThreads) k_skmer_bytes(const uint8_t* __re
   }
   if (threadIdx.x == 0) sw[nwords] = 0;
   __syncthreads();
-  emit_tokens(sw, base0, j0, s, k, tokens, m);
+  emit_tokens<kTokPerThread>(sw, base0, j0, s, k, tokens, m);
 }
 
 // ------------------------------------------------------------ canonicalize
@@ -244,20 +256,25 @@ __global__ void k_detok_restore(const uint32_t* __restrict__ tokens, uint64_t m,
 void launch_skmer_encode_packed(const uint8_t* packed, uint64_t n, uint32_t s, uint32_t k,
                                 uint32_t* tokens, uint64_t m, cudaStream_t st) {
   if (!m) return;
-  const uint64_t blocks = (m + kTokPerBlock - 1) / kTokPerBlock;
-  k_skmer_packed<<<unsigned(blocks), kTokThreads, 0, st>>>(packed, n, s, k, tokens, m);
+  if (s <= 2) {
+    const uint64_t blocks = (m + kTokThreads * kTptSmallStride - 1) / (kTokThreads * kTptSmallStride);
+    k_skmer_packed<kTptSmallStride><<<unsigned(blocks), kTokThreads, 0, st>>>(packed, n, s, k, tokens, m);
+  } else {
+    const uint64_t blocks = (m + kTokThreads * kTpt - 1) / (kTokThreads * kTpt);
+    k_skmer_packed<kTpt><<<unsigned(blocks), kTokThreads, 0, st>>>(packed, n, s, k, tokens, m);
+  }
 }
 void launch_skmer_encode_ascii(const uint8_t* ascii, uint64_t n, uint32_t s, uint32_t k,
                                uint32_t* tokens, uint64_t m, cudaStream_t st) {
   if (!m) return;
-  const uint64_t blocks = (m + kTokPerBlock - 1) / kTokPerBlock;
-  k_skmer_bytes<true><<<unsigned(blocks), kTokThreads, 0, st>>>(ascii, n, s, k, tokens, m);
+  const uint64_t blocks = (m + kTokThreads * kTpt - 1) / (kTokThreads * kTpt);
+  k_skmer_bytes<true, kTpt><<<unsigned(blocks), kTokThreads, 0, st>>>(ascii, n, s, k, tokens, m);
 }
 void launch_skmer_encode_codes(const uint8_t* codes, uint64_t n, uint32_t s, uint32_t k,
                                uint32_t* tokens, uint64_t m, cudaStream_t st) {
   if (!m) return;
-  const uint64_t blocks = (m + kTokPerBlock - 1) / kTokPerBlock;
-  k_skmer_bytes<false><<<unsigned(blocks), kTokThreads, 0, st>>>(codes, n, s, k, tokens, m);
+  const uint64_t blocks = (m + kTokThreads * kTpt - 1) / (kTokThreads * kTpt);
+  k_skmer_bytes<false, kTpt><<<unsigned(blocks), kTokThreads, 0, st>>>(codes, n, s, k, tokens, m);
 }
 uint32_t canon_blocks(uint64_t n) { return uint32_t((n + kCanonPerBlock - 1) / kCanonPerBlock); }
 void launch_canon_count(const uint8_t* raw, uint64_t n, uint32_t* counts, cudaStream_t st) {
