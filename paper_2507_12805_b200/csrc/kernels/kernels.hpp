@@ -241,8 +241,6 @@ void launch_sprm_transpose(const SprmP& s, const float* Gt, float* G, cudaStream
 // true: launch_sprm_dx reads the time-major Gt (no dependency on the transpose)
 bool sprm_dx_time_major(const SprmP& s);
 void launch_sprm_dx(const SprmP& s, const float* G, const float* Gt, float* dx, cudaStream_t st);
-void launch_sprm_emb_grad(const SprmP& s, const uint32_t* ctx, const float* dx, float* grad_emb,
-                          cudaStream_t st);
 void launch_tanh_vec(float* x, int64_t n, cudaStream_t st);
 void launch_adam_scalars(AdamScalars* sc, cudaStream_t st);
 void launch_pos_advance(int64_t* pos, int64_t by, cudaStream_t st);

@@ -509,20 +509,6 @@ __global__ void __launch_bounds__(256) k_sprm_dx_t(SprmP s, const float* __restr
   dx[idx] = fadd(fadd(0.0f, part[0]), fadd(0.0f, part[1]));  // dx += dx_rev (both from zero)
 }
 
-// emb grad: grad[tok][j] += dx[r][t][j], (r,t) row-major order (layers.cpp:117-125)
-__global__ void k_sprm_emb_grad(SprmP s, const uint32_t* __restrict__ ctx,
-                                const float* __restrict__ dx, float* grad_emb) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= s.V * s.Es) return;
-  const uint32_t tok = uint32_t(idx / s.Es);
-  const int j = idx % s.Es;
-  float acc = grad_emb[idx];
-  const int64_t RT = int64_t(s.R) * s.T;
-  for (int64_t p = 0; p < RT; ++p)
-    if (ctx[p] == tok) acc = fadd(acc, dx[p * s.Es + j]);
-  grad_emb[idx] = acc;
-}
-
 __global__ void k_tanh_vec(float* x, int64_t n) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) x[i] = det_tanh(x[i]);
@@ -585,10 +571,6 @@ void launch_sprm_dx(const SprmP& s, const float* G, const float* Gt, float* dx, 
     return;
   }
   k_sprm_dx<<<unsigned((n + 255) / 256), 256, 0, st>>>(s, G, dx);
-}
-void launch_sprm_emb_grad(const SprmP& s, const uint32_t* ctx, const float* dx, float* grad_emb,
-                          cudaStream_t st) {
-  k_sprm_emb_grad<<<unsigned((s.V * s.Es + 127) / 128), 128, 0, st>>>(s, ctx, dx, grad_emb);
 }
 void launch_tanh_vec(float* x, int64_t n, cudaStream_t st) {
   k_tanh_vec<<<unsigned((n + 255) / 256), 256, 0, st>>>(x, n);
