@@ -555,7 +555,7 @@ __global__ void k_embed(const uint32_t* __restrict__ tokens, ChunkGeo geo,
   const int64_t RT = int64_t(d.R) * d.T;
   const int64_t rt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (rt >= RT) return;
-  const int t = int(rt % d.T), r = int(rt / d.T);
+  const int t = int(uint32_t(rt) % uint32_t(d.T)), r = int(uint32_t(rt) / uint32_t(d.T));  // RT < 2^31
   const uint64_t L = geo.L[c];
   const uint64_t jstep = uint64_t(d.T) + uint64_t(td->tick - geo.offset[c]);  // coded position
   // tokens are < V = 4^k by construction; the mask only guards memory after a
@@ -1319,7 +1319,7 @@ __global__ void k_ctx_gather(const uint32_t* __restrict__ tokens, ChunkGeo geo, 
   const int64_t RT = int64_t(d.R) * d.T;
   const int64_t rt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (rt >= RT) return;
-  const int t = int(rt % d.T), r = int(rt / d.T);
+  const int t = int(uint32_t(rt) % uint32_t(d.T)), r = int(uint32_t(rt) / uint32_t(d.T));  // RT < 2^31
   const uint64_t L = geo.L[c];
   const uint64_t jstep = uint64_t(d.T) + uint64_t(td->tick - geo.offset[c]);
   ctx[c * ctx_cs + rt] = tokens[geo.start[c] + uint64_t(r) * L + (jstep - d.T) + t] & uint32_t(d.V - 1);
@@ -1345,7 +1345,9 @@ void launch_gemm(const GemmP& p, bool at, bool bt, const TickDesc* td, int max_a
   // A bias row on top of a tile-aligned M (weight gradient + bias gradient,
   // M = fan-in) would cost a whole extra row of tiles for one row: run the M
   // rows as a GEMM and the bias row as its own column-sum chain.
-  if (p.ones_row && p.M > 0 && p.M % 64 == 0 && p.nprob <= 1 && !p.mask) {
+  // (only with many chunks in flight: for one chunk the extra tile row is
+  // cheap and the separate chain launch would sit on the critical path)
+  if (p.ones_row && p.M > 0 && p.M % 64 == 0 && p.nprob <= 1 && !p.mask && max_active >= 8) {
     GemmP q = p;
     q.ones_row = 0;
     launch_gemm(q, at, bt, td, max_active, st);

@@ -407,29 +407,50 @@ __global__ void __launch_bounds__(kBpttWarps * 32) k_sprm_bptt32(SprmP s, const 
   }
 }
 
-// Gt[g][d][t][r][j] -> G[g][d][j][k], k = (T-1-t)*R + r (32x32 smem tiles)
-__global__ void k_sprm_transpose(SprmP s, const float* __restrict__ Gt, float* G) {
+// Gt[g][d][t][r][j] -> G[g][d][j][k], k = (T-1-t)*R + r (32x32 smem tiles).
+// A block owns one (k, j) tile position for all 10 gate/direction slabs: every
+// load is issued up front (40 per thread in flight), then the slabs go through
+// the shared tile one after another -- one memory latency per block instead
+// of one per tile.
+constexpr int kTrSlabs = 10;
+__global__ void __launch_bounds__(256) k_sprm_transpose(SprmP s, const float* __restrict__ Gt, float* G) {
   __shared__ float tile[32][33];
   const int T = s.T, H = s.H, R = s.R;
   const int64_t RT = int64_t(R) * T;
-  const int gd = blockIdx.z;  // gate*2 + d
   const int64_t k0 = int64_t(blockIdx.x) * 32;
   const int j0 = blockIdx.y * 32;
-  const float* src = Gt + int64_t(gd) * RT * H;
-  float* dst = G + int64_t(gd) * H * RT;
-  for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
-    const int64_t k = k0 + yy;
-    const int j = j0 + threadIdx.x;
-    if (k < RT && j < H) {
-      const int t = int(T - 1 - k / R), r = int(k % R);
-      tile[yy][threadIdx.x] = src[(int64_t(t) * R + r) * H + j];
-    }
+  // source offsets of this thread's 4 rows (the same in every slab)
+  int64_t so[4];
+  bool ok[4];
+  const int j = j0 + threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t k = uint32_t(k0) + threadIdx.y + 8 * u;
+    ok[u] = k < uint64_t(RT) && j < H;
+    const uint32_t t = uint32_t(T - 1) - k / uint32_t(R), r = k % uint32_t(R);
+    so[u] = (int64_t(t) * R + r) * H + j;
   }
-  __syncthreads();
-  for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
-    const int j = j0 + yy;
-    const int64_t k = k0 + threadIdx.x;
-    if (k < RT && j < H) dst[int64_t(j) * RT + k] = tile[threadIdx.x][yy];
+  float v[kTrSlabs][4];
+#pragma unroll
+  for (int gd = 0; gd < kTrSlabs; ++gd) {
+    const float* src = Gt + int64_t(gd) * RT * H;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[gd][u] = ok[u] ? __ldg(src + so[u]) : 0.0f;
+  }
+#pragma unroll
+  for (int gd = 0; gd < kTrSlabs; ++gd) {
+    float* dst = G + int64_t(gd) * H * RT;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) tile[threadIdx.y + 8 * u][threadIdx.x] = v[gd][u];
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int yy = threadIdx.y + 8 * u;
+      const int jj = j0 + yy;
+      const int64_t k = k0 + threadIdx.x;
+      if (k < RT && jj < H) dst[int64_t(jj) * RT + k] = tile[threadIdx.x][yy];
+    }
+    __syncthreads();
   }
 }
 
@@ -440,9 +461,10 @@ __global__ void k_sprm_dx(SprmP s, const float* __restrict__ Gr, float* dx) {
   const int R = s.R, T = s.T, Es = s.Es, H = s.H;
   const int64_t RT = int64_t(R) * T;
   if (idx >= RT * Es) return;
-  const int i = int(idx % Es);
-  const int64_t rt = idx / Es;
-  const int r = int(rt / T), t = int(rt % T);
+  const uint32_t ui = uint32_t(idx);  // R*T*Es < 2^31
+  const int i = int(ui % uint32_t(Es));
+  const uint32_t rt = ui / uint32_t(Es);
+  const int r = int(rt / uint32_t(T)), t = int(rt % uint32_t(T));
   const float* W = s.w;
   float part[2];
   for (int d = 0; d < 2; ++d) {
@@ -479,9 +501,10 @@ __global__ void __launch_bounds__(256) k_sprm_dx_t(SprmP s, const float* __restr
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t RT = int64_t(R) * T;
   if (idx >= RT * Es) return;
-  const int i = int(idx % Es);
-  const int64_t rt = idx / Es;
-  const int r = int(rt / T), t = int(rt % T);
+  const uint32_t ui = uint32_t(idx);  // R*T*Es < 2^31
+  const int i = int(ui % uint32_t(Es));
+  const uint32_t rt = ui / uint32_t(Es);
+  const int r = int(rt / uint32_t(T)), t = int(rt % uint32_t(T));
   const int64_t TRH = RT * H;
   float part[2];
 #pragma unroll
@@ -560,7 +583,7 @@ void launch_sprm_bptt(const SprmP& s, const float* tape, const float* dfin, floa
 }
 void launch_sprm_transpose(const SprmP& s, const float* Gt, float* G, cudaStream_t st) {
   const int64_t RT = int64_t(s.R) * s.T;
-  dim3 grid(unsigned((RT + 31) / 32), unsigned((s.H + 31) / 32), 10);
+  dim3 grid(unsigned((RT + 31) / 32), unsigned((s.H + 31) / 32));
   k_sprm_transpose<<<grid, dim3(32, 8), 0, st>>>(s, Gt, G);
 }
 bool sprm_dx_time_major(const SprmP& s) { return s.H == 32 && s.Es <= 8; }
