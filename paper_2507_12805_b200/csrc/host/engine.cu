@@ -494,6 +494,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   // A prologue computes tick 0's before the first tick.
   const bool statics = (run.flags & 3) != 0;
   SideStream pred;
+  SideStream cod;  // encode: the range coder runs beside the trainer (nothing reads its output)
   DBuf<TickDesc> d_td_next(1);
   DBuf<uint32_t> ctx_next;
   if (statics) ctx_next.alloc(TW * s_ctx);
@@ -512,6 +513,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     const uint64_t l0 = run.launches;
     side.rewind();
     pred.rewind();
+    cod.rewind();
     launch_tick_advance(d_td.p, d_act_ptr.p, d_act.p, d_hand_ptr.p, d_hand.p, sch.ticks, st);
     ++run.launches;
     if (nh > 0) {
@@ -569,20 +571,26 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
                            cudaMemcpyDeviceToHost, st));
       }
     }
+    // encode: the coded symbols are known, and only the payload depends on the
+    // coder, so it runs on its own stream; decode: it produces the tokens the
+    // trainer and the next tick's contexts need, so it stays on the chain
+    if (!run.decode) cod.wait_for(st);
     launch_range_step(d_tokens, geo, int(run.t), R, V, freq.p, cum.p, s_rv, s_cum, payload.p,
-                      d_pay_off.p, d_pay_len.p, cstate.p, act, na, run.decode, st);
+                      d_pay_off.p, d_pay_len.p, cstate.p, act, na, run.decode,
+                      run.decode ? st : cod.s);
     ++run.launches;
     // ---------------- backward controller (OnlineTrainer::step, mixer.cpp:57-97)
     BcP bp{probs.p, lu.p, lr.p, lm.p, s_rv, d_tokens, geo, d_td.p, int(run.t), w.p, m.p, v.p, P, oA,
            dlm.p, aterm.p, lterm.p, R, sc.p, warm_loss.p, d_warm.p, int(run.flags), R, V};
     launch_bc_dlm(bp, act, na, st);
-    launch_alpha_step(bp, act, na, st);
-    run.launches += 2;
-    // next tick's static predictions, beside this tick's backward
-    if (statics) {
-      pred.wait_for(st);
-      predict_next(pred.s);
-    }
+    run.launches += 1;
+    // the mixing weight's own step (alpha is not in Adam's range and nothing
+    // in this tick reads it), then the next tick's static predictions (they
+    // overwrite lu/lr, which the alpha step reads), beside the DM backward
+    pred.wait_for(st);
+    launch_alpha_step(bp, act, na, pred.s);
+    run.launches += 1;
+    if (statics) predict_next(pred.s);
     // head, ffn, attention output projection (Linear::backward, layers.cpp:176-183).
     // Data gradients stay on the main stream; each weight gradient goes to the
     // side stream as soon as its operands exist (they write disjoint slices of
@@ -656,7 +664,8 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     // Adam over every DM parameter (alpha was updated by k_alpha_step)
     launch_adam(w.p, g.p, m.p, v.p, P, P - 1, sc.p, act, na, st);
     ++run.launches;
-    if (statics) pred.join_into(st);
+    pred.join_into(st);
+    if (!run.decode) cod.join_into(st);
     check_launch();
     tick_launches = run.launches - l0;
   };
