@@ -532,12 +532,14 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     GemmP gp{};
     // K, V over all R*T rows, q over the last position (layers.cpp:437-445)
     // x is feature-major: A(row, e) = xT[e*RT + row]
+    // K and V in one launch: two problems over the same x tiles
     gp = GemmP{x.p, s_x, RT, W_(DmLayout::KW), P, H, kk.p, s_kv, H, W_(DmLayout::KB), P,
                nullptr, 0, 0, R * T, H, E, 0, 1, 0};
-    gemm(gp, true, false);
-    gp.B = W_(DmLayout::VW);
-    gp.bias = W_(DmLayout::VB);
-    gp.C = vv.p;
+    gp.nprob = 2;
+    gp.a_ps = 0;
+    gp.b_ps = int64_t(lay.off(DmLayout::VW)) - int64_t(lay.off(DmLayout::KW));
+    gp.c_ps = vv.p - kk.p;
+    gp.bias_ps = int64_t(lay.off(DmLayout::VB)) - int64_t(lay.off(DmLayout::KB));
     gemm(gp, true, false);
     gp = GemmP{xl.p, s_re, E, W_(DmLayout::QW), P, H, q.p, s_rh, H, W_(DmLayout::QB), P, nullptr, 0,
                0, R, H, E, 0, 1, 0};
