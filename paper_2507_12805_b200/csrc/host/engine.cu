@@ -479,10 +479,11 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   const int nh = int(max_hand);
   const TickDesc* act = d_td.p;
   uint64_t tick_launches = 0;
-  // Side stream for the work of a tick that is independent of the main chain:
-  // the static predictors (need only ctx) run beside the DM forward, and each
-  // weight-gradient product runs beside the data-gradient chain once its input
-  // exists. Fork/join by events, so the captured graph gets parallel branches.
+  // Side streams for the work of a tick that is off the main chain (fork/join
+  // by events, so the captured graph gets parallel branches): `side` takes each
+  // weight-gradient product as soon as its operands exist, beside the
+  // data-gradient chain; `pred` (below) the mixing-weight step and the next
+  // tick's static predictions; `cod` (below) the encoder's range coder.
   SideStream side;
   auto to_side = [&]() { side.wait_for(st); };
   auto from_side = [&]() { side.join_into(st); };
