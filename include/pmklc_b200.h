@@ -118,6 +118,10 @@ int pmklc_skmer_encode(const uint8_t* codes, uint64_t n, uint32_t s, uint32_t k,
  * byte i/4, 16-byte aligned) -> u32 tokens; `stream` is a cudaStream_t */
 int pmklc_skmer_encode_packed_device(const uint8_t* d_packed, uint64_t n_bases, uint32_t s,
                                      uint32_t k, uint32_t* d_tokens, void* stream);
+/* same with u16 tokens (k <= 8): SURVEY config 2's 2-byte layout, half the
+ * written bytes; values identical to the u32 tokens (skmer.cpp:16-24) */
+int pmklc_skmer_encode_packed_device_u16(const uint8_t* d_packed, uint64_t n_bases, uint32_t s,
+                                         uint32_t k, uint16_t* d_tokens, void* stream);
 
 /* host logic of PMKLC-M block partitioning: plan_chunks (pipeline.cpp:32-52)
  * and snapshot_step (pipeline.cpp:26-30); arrays of capacity `cap` */

@@ -66,7 +66,7 @@ class Timing(C.Structure):
 EXPORTS = [
     "pmklc_cfg_default", "pmklc_compress", "pmklc_compress_device", "pmklc_decompress",
     "pmklc_decompress_to_device", "pmklc_encode_chunks", "pmklc_dump_chunk", "pmklc_skmer_encode",
-    "pmklc_skmer_encode_packed_device", "pmklc_free", "pmklc_device_free", "pmklc_last_error",
+    "pmklc_skmer_encode_packed_device", "pmklc_skmer_encode_packed_device_u16", "pmklc_free", "pmklc_device_free", "pmklc_last_error",
     "pmklc_errc_name", "pmklc_version", "pmklc_synth_markov3", "pmklc_synth_uniform",
     "pmklc_synth_genome", "pmklc_synth_species", "pmklc_synth_packed_codes", "pmklc_plan_chunks",
     "pmklc_schedule", "pmklc_quantize", "pmklc_write_bigru", "pmklc_bench_kernel",
@@ -256,9 +256,11 @@ def skmer_encode(codes: bytes, s: int, k: int, device: int = 0):
 
 
 def skmer_encode_packed_device(d_packed: int, n_bases: int, s: int, k: int, d_tokens: int,
-                               stream: int = 0) -> None:
-    _check(lib().pmklc_skmer_encode_packed_device(C.c_void_p(d_packed), C.c_uint64(n_bases), s, k,
-                                                  C.c_void_p(d_tokens), C.c_void_p(stream)))
+                               stream: int = 0, u16: bool = False) -> None:
+    """Device tokenizer; u16=True writes 2-byte tokens (k <= 8)."""
+    f = lib().pmklc_skmer_encode_packed_device_u16 if u16 else lib().pmklc_skmer_encode_packed_device
+    _check(f(C.c_void_p(d_packed), C.c_uint64(n_bases), s, k, C.c_void_p(d_tokens),
+             C.c_void_p(stream)))
 
 
 def plan_chunks(m: int, workers: int, bs: int, t: int, smp_per_myriad: int):

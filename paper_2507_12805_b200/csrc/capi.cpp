@@ -219,6 +219,11 @@ int pmklc_skmer_encode_packed_device(const uint8_t* d_packed, uint64_t n_bases, 
   return guard([&] { skmer_encode_packed_device(d_packed, n_bases, s, k, d_tokens, stream); });
 }
 
+int pmklc_skmer_encode_packed_device_u16(const uint8_t* d_packed, uint64_t n_bases, uint32_t s,
+                                         uint32_t k, uint16_t* d_tokens, void* stream) {
+  return guard([&] { skmer_encode_packed_device16(d_packed, n_bases, s, k, d_tokens, stream); });
+}
+
 int pmklc_plan_chunks(uint64_t m, uint32_t workers, uint32_t bs, uint32_t t, uint16_t myriad,
                       uint64_t* starts, uint64_t* lens, uint64_t* snaps, size_t cap, size_t* count,
                       uint32_t* bs_out) {

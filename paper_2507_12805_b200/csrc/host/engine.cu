@@ -1505,6 +1505,15 @@ void skmer_encode_packed_device(const uint8_t* d_packed, uint64_t n_bases, uint3
   check_launch();
 }
 
+void skmer_encode_packed_device16(const uint8_t* d_packed, uint64_t n_bases, uint32_t s, uint32_t k,
+                                  uint16_t* d_tokens, void* stream) {
+  if (!(s >= 1 && s <= k && k <= 8)) raise(errc::config_invalid, "invalid (s,k) parameters");
+  const uint64_t m = token_count(n_bases, s, k);
+  launch_skmer_encode_packed16(d_packed, n_bases, s, k, d_tokens, m,
+                               static_cast<cudaStream_t>(stream));
+  check_launch();
+}
+
 Bytes seeded_bigru_file(uint32_t k, uint32_t t, uint32_t scale, int layers, uint64_t seed) {
   if (k < 1 || k > 8) raise(errc::config_invalid, "k out of range");
   const Dims d = Dims::make(uint32_t(1) << (2 * k), t, scale);

@@ -100,6 +100,8 @@ std::vector<uint32_t> skmer_encode_codes(const uint8_t* codes, uint64_t n, uint3
 // Tokenizer on device buffers: packed 2-bit bases -> u32 tokens (bench config 2)
 void skmer_encode_packed_device(const uint8_t* d_packed, uint64_t n_bases, uint32_t s, uint32_t k,
                                 uint32_t* d_tokens, void* stream);
+void skmer_encode_packed_device16(const uint8_t* d_packed, uint64_t n_bases, uint32_t s, uint32_t k,
+                                  uint16_t* d_tokens, void* stream);
 
 // PMKW bytes of a seeded (untrained) BiGRU predictor (BiGruModel ctor +
 // serialize_model, models.cpp:38-51,159-173): the SPuM file the reference

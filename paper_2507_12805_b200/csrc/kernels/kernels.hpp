@@ -19,6 +19,9 @@ namespace pmklc_b200 {
 // Input: 2-bit packed bases, base i at bits 2*(i%4) of byte i/4.
 void launch_skmer_encode_packed(const uint8_t* packed, uint64_t n_bases, uint32_t s, uint32_t k,
                                 uint32_t* tokens, uint64_t m, cudaStream_t st);
+// same, u16 tokens (k <= 8; SURVEY config 2's 2-byte token layout)
+void launch_skmer_encode_packed16(const uint8_t* packed, uint64_t n_bases, uint32_t s, uint32_t k,
+                                  uint16_t* tokens, uint64_t m, cudaStream_t st);
 // Input: one byte per base, ASCII "ACGT" (pure input, no exception bytes).
 void launch_skmer_encode_ascii(const uint8_t* ascii, uint64_t n_bases, uint32_t s, uint32_t k,
                                uint32_t* tokens, uint64_t m, cudaStream_t st);

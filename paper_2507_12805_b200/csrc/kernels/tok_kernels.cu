@@ -9,6 +9,7 @@
 // reversal (__brev), and each warp writes 128-token slabs as lane-contiguous
 // 16-byte stores (512 contiguous bytes per store instruction).
 #include <cstdint>
+#include <cstring>
 
 #include "kernels.hpp"
 
@@ -26,49 +27,55 @@ static_assert(kTokThreads * kTptSmallStride * 2 <= kTokThreads * kTpt * 8, "stag
 
 __device__ __forceinline__ uint32_t ascii_code(uint32_t c) { return ((c >> 1) ^ (c >> 2)) & 3u; }
 
-// Reverse the order of the 2-bit digits of a 2k-bit field whose digit i sits
-// at bits 2i (first base lowest) into the token's MSB-first order.
-__device__ __forceinline__ uint32_t digits_to_token(uint32_t f, uint32_t k) {
-  uint32_t x = __brev(f);
-  x = ((x >> 1) & 0x55555555u) | ((x & 0x55555555u) << 1);
-  return x >> (32u - 2u * k);
+// Staged windows hold the bases MSB-first: base i of a 32-bit word at bits
+// 31-2i..30-2i, so a token (k bases, first base most significant,
+// skmer.cpp:16-24) is one contiguous 2k-bit field of the stream. msb_first
+// turns a word of the packed input layout (base i at bits 2i..2i+1) into that
+// form: bit reversal, then swap the two bits of every digit back.
+__device__ __forceinline__ uint32_t msb_first(uint32_t w) {
+  const uint32_t x = __brev(w);
+  return ((x >> 1) & 0x55555555u) | ((x & 0x55555555u) << 1);
 }
 
-// Extract tokens [j0, j0 + 256*kTokPerThread) from a packed shared-memory window whose first
-// byte holds base `sbase`. Warp w owns 32*kTokPerThread consecutive tokens as
-// slabs of 128; lane l makes tokens 4l..4l+3 of each slab and writes them
-// with one 16-byte store, so every warp store covers 512 contiguous bytes.
-template <int kTokPerThread>
+// Extract tokens [j0, j0 + 256*kTokPerThread) from a packed shared-memory
+// window whose first byte holds base `sbase`. Warp w owns 32*kTokPerThread
+// consecutive tokens as slabs of 32*PER (PER = 16 bytes / token size: 4 u32 or
+// 8 u16 tokens); lane l makes tokens PER*l .. PER*l+PER-1 of each slab and
+// writes them with one 16-byte store, so every warp store covers 512
+// contiguous bytes.
+template <int kTokPerThread, typename TokT>
 __device__ __forceinline__ void emit_tokens(const uint32_t* sw, uint64_t sbase, uint64_t j0,
-                                            uint32_t s, uint32_t k, uint32_t* tokens, uint64_t m) {
+                                            uint32_t s, uint32_t k, TokT* tokens, uint64_t m) {
+  constexpr int PER = 16 / int(sizeof(TokT));
+  static_assert(kTokPerThread % PER == 0, "whole slabs per thread");
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint64_t jw = j0 + uint64_t(w) * 32 * kTokPerThread;
   if (jw >= m) return;
-  const uint32_t mask = (k == 16) ? 0xffffffffu : ((1u << (2u * k)) - 1u);
+  const uint32_t rsh = 32u - 2u * k;  // k <= 16
 #pragma unroll
-  for (int slab = 0; slab < kTokPerThread / 4; ++slab) {
-    const uint64_t jt = jw + uint64_t(slab) * 128 + uint64_t(lane) * 4;
-    uint32_t out[4];
+  for (int slab = 0; slab < kTokPerThread / PER; ++slab) {
+    const uint64_t jt = jw + uint64_t(slab) * 32 * PER + uint64_t(lane) * PER;
+    uint32_t b = uint32_t(jt * s - sbase);  // base offset in the window (< 2^17)
+    TokT out[PER];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint64_t bit = ((jt + q) * s - sbase) * 2;  // bit offset in window
-      const uint32_t wi = uint32_t(bit >> 5), sh = uint32_t(bit & 31);
-      const uint32_t lo = sw[wi], hi = sw[wi + 1];
-      const uint32_t f = __funnelshift_r(lo, hi, sh) & mask;
-      out[q] = digits_to_token(f, k);
+    for (int q = 0; q < PER; ++q, b += s) {
+      const uint32_t wi = b >> 4, o = b & 15u;
+      out[q] = TokT(__funnelshift_l(sw[wi + 1], sw[wi], 2u * o) >> rsh);
     }
-    if (jt + 4 <= m) {
-      *reinterpret_cast<uint4*>(tokens + jt) = make_uint4(out[0], out[1], out[2], out[3]);
+    if (jt + PER <= m) {
+      uint4 v;
+      memcpy(&v, out, 16);
+      *reinterpret_cast<uint4*>(tokens + jt) = v;
     } else {
-      for (int q = 0; q < 4 && jt + q < m; ++q) tokens[jt + q] = out[q];
+      for (int q = 0; q < PER && jt + q < m; ++q) tokens[jt + q] = out[q];
     }
   }
 }
 
-template <int kTokPerThread>
+template <int kTokPerThread, typename TokT>
 __global__ void __launch_bounds__(kTokThreads) k_skmer_packed(const uint8_t* __restrict__ packed,
                                                               uint64_t n, uint32_t s, uint32_t k,
-                                                              uint32_t* __restrict__ tokens,
+                                                              TokT* __restrict__ tokens,
                                                               uint64_t m) {
   __shared__ __align__(16) uint32_t sw[kStageBytes / 4];
   constexpr int kTokPerBlock = kTokThreads * kTokPerThread;
@@ -86,7 +93,9 @@ __global__ void __launch_bounds__(kTokThreads) k_skmer_packed(const uint8_t* __r
   for (uint64_t i = nvec * 16 + threadIdx.x; i < nbytes + 8; i += kTokThreads)
     sb[i] = i < nbytes ? packed[byte0 + i] : 0;
   __syncthreads();
-  emit_tokens<kTokPerThread>(sw, byte0 * 4, j0, s, k, tokens, m);
+  for (uint32_t i = threadIdx.x; i < uint32_t((nbytes + 8 + 3) / 4); i += kTokThreads) sw[i] = msb_first(sw[i]);
+  __syncthreads();
+  emit_tokens<kTokPerThread, TokT>(sw, byte0 * 4, j0, s, k, tokens, m);
 }
 
 // ASCII / code input: stage 16 bytes per step, pack to 2-bit on the way in.
@@ -114,19 +123,19 @@ __global__ void __launch_bounds__(kTokThreads) k_skmer_bytes(const uint8_t* __re
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const uint32_t byte = (wv[q] >> (8 * c)) & 0xffu;
-          packed |= (kAscii ? ascii_code(byte) : (byte & 3u)) << (2 * (q * 4 + c));
+          packed |= (kAscii ? ascii_code(byte) : (byte & 3u)) << (30 - 2 * (q * 4 + c));  // MSB-first
         }
     } else {
       for (int c = 0; c < 16; ++c) {
         const uint32_t byte = (b + c < n) ? in[b + c] : 0u;
-        packed |= (kAscii ? ascii_code(byte) : (byte & 3u)) << (2 * c);
+        packed |= (kAscii ? ascii_code(byte) : (byte & 3u)) << (30 - 2 * c);
       }
     }
     sw[w] = packed;
   }
   if (threadIdx.x == 0) sw[nwords] = 0;
   __syncthreads();
-  emit_tokens<kTokPerThread>(sw, base0, j0, s, k, tokens, m);
+  emit_tokens<kTokPerThread, uint32_t>(sw, base0, j0, s, k, tokens, m);
 }
 
 // ------------------------------------------------------------ canonicalize
@@ -253,17 +262,28 @@ __global__ void k_detok_restore(const uint32_t* __restrict__ tokens, uint64_t m,
 
 }  // namespace
 
-void launch_skmer_encode_packed(const uint8_t* packed, uint64_t n, uint32_t s, uint32_t k,
-                                uint32_t* tokens, uint64_t m, cudaStream_t st) {
-  if (!m) return;
+template <typename TokT>
+static void launch_packed(const uint8_t* packed, uint64_t n, uint32_t s, uint32_t k, TokT* tokens,
+                          uint64_t m, cudaStream_t st) {
+  if (m == 0) return;
   if (s <= 2) {
     const uint64_t blocks = (m + kTokThreads * kTptSmallStride - 1) / (kTokThreads * kTptSmallStride);
-    k_skmer_packed<kTptSmallStride><<<unsigned(blocks), kTokThreads, 0, st>>>(packed, n, s, k, tokens, m);
+    k_skmer_packed<kTptSmallStride, TokT><<<unsigned(blocks), kTokThreads, 0, st>>>(packed, n, s, k,
+                                                                                  tokens, m);
   } else {
     const uint64_t blocks = (m + kTokThreads * kTpt - 1) / (kTokThreads * kTpt);
-    k_skmer_packed<kTpt><<<unsigned(blocks), kTokThreads, 0, st>>>(packed, n, s, k, tokens, m);
+    k_skmer_packed<kTpt, TokT><<<unsigned(blocks), kTokThreads, 0, st>>>(packed, n, s, k, tokens, m);
   }
 }
+void launch_skmer_encode_packed(const uint8_t* packed, uint64_t n, uint32_t s, uint32_t k,
+                                uint32_t* tokens, uint64_t m, cudaStream_t st) {
+  launch_packed(packed, n, s, k, tokens, m, st);
+}
+void launch_skmer_encode_packed16(const uint8_t* packed, uint64_t n, uint32_t s, uint32_t k,
+                                  uint16_t* tokens, uint64_t m, cudaStream_t st) {
+  launch_packed(packed, n, s, k, tokens, m, st);
+}
+
 void launch_skmer_encode_ascii(const uint8_t* ascii, uint64_t n, uint32_t s, uint32_t k,
                                uint32_t* tokens, uint64_t m, cudaStream_t st) {
   if (!m) return;

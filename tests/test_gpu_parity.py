@@ -49,13 +49,19 @@ def test_tokenizer_packed_large(P, checker):
     codes = np.unpackbits(np.frombuffer(packed, np.uint8)[:, None], axis=1, bitorder="little")
     codes = (codes[:, 0::2] | (codes[:, 1::2] << 1)).reshape(-1).astype(np.uint8)
     dp = torch.frombuffer(bytearray(packed), dtype=torch.uint8).cuda()
-    for s, k in [(3, 3), (1, 8), (8, 8), (2, 5), (1, 1)]:
-        m = (n - k) // s + 1
-        dt = torch.zeros(m, dtype=torch.int32, device="cuda")
-        P.skmer_encode_packed_device(dp.data_ptr(), n, s, k, dt.data_ptr())
-        torch.cuda.synchronize()
-        want, _ = checker.skmer_encode(codes.tobytes(), s, k)
-        assert np.array_equal(dt.cpu().numpy().view(np.uint32), want), (s, k)
+    for nb in (n, n - 37):  # full and ragged (tail slabs, partial last byte)
+        for s, k in [(3, 3), (1, 8), (8, 8), (2, 5), (1, 1)]:
+            m = (nb - k) // s + 1
+            want, _ = checker.skmer_encode(codes[:nb].tobytes(), s, k)
+            dt = torch.zeros(m, dtype=torch.int32, device="cuda")
+            P.skmer_encode_packed_device(dp.data_ptr(), nb, s, k, dt.data_ptr())
+            torch.cuda.synchronize()
+            assert np.array_equal(dt.cpu().numpy().view(np.uint32), want), (nb, s, k)
+            # 2-byte token layout (config 2), same values
+            d16 = torch.zeros(m, dtype=torch.int16, device="cuda")
+            P.skmer_encode_packed_device(dp.data_ptr(), nb, s, k, d16.data_ptr(), u16=True)
+            torch.cuda.synchronize()
+            assert np.array_equal(d16.cpu().numpy().view(np.uint16).astype(np.uint32), want), (nb, s, k)
 
 
 # ------------------------------------------------------------------ quantizer

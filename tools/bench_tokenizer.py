@@ -33,32 +33,40 @@ def main():
     pre = np.frombuffer(packed[: 1 << 16], np.uint8)
     codes = np.unpackbits(pre[:, None], axis=1, bitorder="little")
     codes = (codes[:, 0::2] | (codes[:, 1::2] << 1)).reshape(-1).astype(np.uint8).tobytes()
+    out16 = torch.empty((nbases + 16), dtype=torch.int16, device="cuda")
     results = []
     for s, k in PAIRS:
         m = (nbases - k) // s + 1
-        P.skmer_encode_packed_device(d_in.data_ptr(), nbases, s, k, out.data_ptr())
-        torch.cuda.synchronize()
         want, _ = chk.skmer_encode(codes, s, k)
-        got = out[: len(want)].cpu().numpy().view(np.uint32)
-        ok = bool(np.array_equal(got, want))
-        ts = []
-        for _ in range(iters):
-            flush.add_(1)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            P.skmer_encode_packed_device(d_in.data_ptr(), nbases, s, k, out.data_ptr())
-            e1.record()
+        for tw in (4, 2):  # u32 (the reference layout) and u16 tokens
+            buf = out if tw == 4 else out16
+            run = lambda: P.skmer_encode_packed_device(d_in.data_ptr(), nbases, s, k, buf.data_ptr(),
+                                                       u16=(tw == 2))
+            run()
             torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1))
-        ms = sorted(ts)[len(ts) // 2]
-        byts = (nbases + 3) // 4 + 4 * m
-        gbs = byts / (ms / 1e3) / 1e9
-        r = {"s": s, "k": k, "tokens": m, "ms": ms, "GB/s": gbs, "frac": gbs / peak,
-             "bases_per_s": nbases / (ms / 1e3), "parity_prefix_ok": ok}
-        results.append(r)
-        print(json.dumps(r), flush=True)
+            got = buf[: len(want)].cpu().numpy().view(np.uint32 if tw == 4 else np.uint16)
+            ok = bool(np.array_equal(got.astype(np.uint32), want))
+            ts = []
+            for _ in range(iters):
+                flush.add_(1)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                run()
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            ms = sorted(ts)[len(ts) // 2]
+            byts = (nbases + 3) // 4 + tw * m
+            gbs = byts / (ms / 1e3) / 1e9
+            r = {"s": s, "k": k, "token_bytes": tw, "tokens": m, "ms": ms, "GB/s": gbs,
+                 "frac": gbs / peak, "bases_per_s": nbases / (ms / 1e3), "parity_prefix_ok": ok}
+            results.append(r)
+            print(json.dumps(r), flush=True)
     print(json.dumps({"summary": "tokenizer sweep", "n_bases": nbases, "peak_gbs": peak,
-                      "mean_frac": sum(r["frac"] for r in results) / len(results),
+                      "mean_frac_u32": sum(r["frac"] for r in results if r["token_bytes"] == 4)
+                      / max(1, sum(1 for r in results if r["token_bytes"] == 4)),
+                      "mean_frac_u16": sum(r["frac"] for r in results if r["token_bytes"] == 2)
+                      / max(1, sum(1 for r in results if r["token_bytes"] == 2)),
                       "all_parity_ok": all(r["parity_prefix_ok"] for r in results)}))
 
 
