@@ -522,8 +522,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
       ++run.launches;
     }
     auto gemm = [&](GemmP p, bool at, bool bt) {
-      launch_gemm(p, at, bt, act, na, st);
-      ++run.launches;
+      run.launches += launch_gemm(p, at, bt, act, na, st);
     };
     // ---------------- forward (AttentionModel::forward, models.cpp:122-136)
     launch_embed(d_tokens, geo, w.p, P, oE, oP, ctx.p, s_ctx, x.p, s_x, xl.p, s_re, dd, act, na,
@@ -599,8 +598,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     // side stream as soon as its operands exist (they write disjoint slices of
     // g that nothing reads before Adam).
     auto side_gemm = [&](GemmP p, bool at, bool bt) {
-      launch_gemm(p, at, bt, act, na, side.s);
-      ++run.launches;
+      run.launches += launch_gemm(p, at, bt, act, na, side.s);
     };
     to_side();
     side_gemm(GemmP{fo.p, s_rh, H, dlm.p, s_rv, V, G_(DmLayout::HW), P, V, nullptr, 0, nullptr, 0, 0,

@@ -1339,9 +1339,9 @@ void launch_ctx_gather(const uint32_t* tokens, ChunkGeo geo, uint32_t* ctx, int6
                                                                              d, td);
 }
 
-void launch_gemm(const GemmP& p, bool at, bool bt, const TickDesc* td, int max_active,
-                 cudaStream_t st) {
-  if (max_active <= 0 || p.N <= 0 || p.M + p.ones_row <= 0) return;
+int launch_gemm(const GemmP& p, bool at, bool bt, const TickDesc* td, int max_active,
+                cudaStream_t st) {
+  if (max_active <= 0 || p.N <= 0 || p.M + p.ones_row <= 0) return 0;
   // A bias row on top of a tile-aligned M (weight gradient + bias gradient,
   // M = fan-in) would cost a whole extra row of tiles for one row: run the M
   // rows as a GEMM and the bias row as its own column-sum chain.
@@ -1350,16 +1350,17 @@ void launch_gemm(const GemmP& p, bool at, bool bt, const TickDesc* td, int max_a
   if (p.ones_row && p.M > 0 && p.M % 64 == 0 && p.nprob <= 1 && !p.mask && max_active >= 8) {
     GemmP q = p;
     q.ones_row = 0;
-    launch_gemm(q, at, bt, td, max_active, st);
+    const int n = launch_gemm(q, at, bt, td, max_active, st);
     const dim3 grid(unsigned((p.N + 127) / 128), unsigned(max_active));
     if (bt) k_bias_row<true><<<grid, 128, 0, st>>>(p, td);
     else k_bias_row<false><<<grid, 128, 0, st>>>(p, td);
-    return;
+    return n + 1;
   }
   if (at && bt) gemm_dispatch<true, true>(p, td, max_active, st);
   else if (at) gemm_dispatch<true, false>(p, td, max_active, st);
   else if (bt) gemm_dispatch<false, true>(p, td, max_active, st);
   else gemm_dispatch<false, false>(p, td, max_active, st);
+  return 1;
 }
 
 void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int max_active,

@@ -77,7 +77,8 @@ struct GemmP {
   int nprob;
   int64_t a_ps, b_ps, c_ps, bias_ps;
 };
-void launch_gemm(const GemmP& p, bool at, bool bt, const TickDesc* td, int max_active,
+// returns the number of kernels launched (2 when the bias row is split off)
+int launch_gemm(const GemmP& p, bool at, bool bt, const TickDesc* td, int max_active,
                  cudaStream_t st);
 // Long-reduction "NT" product for weight gradients over many rows:
 // C[m][n] += sum_{k ascending} A[m][k] * B[n][k] (+ row M: sum_k B[n][k]),
