@@ -366,6 +366,9 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
       dctx(TW * s_rh), dq(TW * s_rh), dk(TW * s_kv), dv(TW * s_kv), dx(TW * s_x), dxl(TW * s_re),
       xl(TW * s_re);
   DBuf<float> lu((run.flags & 1) ? TW * s_rv : 0), lr((run.flags & 2) ? TW * s_rv : 0);
+  // static predictions of the next tick (cross-tick pipeline), moved into
+  // lu/lr at the start of each tick
+  DBuf<float> lu_p((run.flags & 1) ? TW * s_rv : 0), lr_p((run.flags & 2) ? TW * s_rv : 0);
   int64_t s_bw = 0;
   DBuf<float> bwork;
   DBuf<HotTimer> d_hot(1);
@@ -495,7 +498,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   // A prologue computes tick 0's before the first tick.
   const bool statics = (run.flags & 3) != 0;
   SideStream pred;
-  SideStream cod;  // encode: the range coder runs beside the trainer (nothing reads its output)
+  SideStream cod;  // the encoder's range coder and the mixing-weight step, beside the trainer
   DBuf<TickDesc> d_td_next(1);
   DBuf<uint32_t> ctx_next;
   if (statics) ctx_next.alloc(TW * s_ctx);
@@ -505,10 +508,10 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     run.launches += 2;
     if (run.flags & 1)
       run.launches += launch_bigru_predict(run.pub->params(R), ctx_next.p, s_ctx, bwork.p, s_bw,
-                                           lu.p, s_rv, d_td_next.p, na, s2, d_hot.p);
+                                           lu_p.p, s_rv, d_td_next.p, na, s2, d_hot.p);
     if (run.flags & 2)
       run.launches += launch_bigru_predict(run.priv->params(R), ctx_next.p, s_ctx, bwork.p, s_bw,
-                                           lr.p, s_rv, d_td_next.p, na, s2);
+                                           lr_p.p, s_rv, d_td_next.p, na, s2);
   };
   auto enqueue_tick = [&](int64_t probe_tick) {
     const uint64_t l0 = run.launches;
@@ -520,6 +523,18 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     if (nh > 0) {
       launch_state_copy(w.p, m.p, v.p, sc.p, P, P, d_td.p, nh, st);
       ++run.launches;
+    }
+    if (statics) {
+      // this tick's static predictions (made during the previous tick) into
+      // lu/lr; the next tick's then go to lu_p/lr_p, concurrently with every
+      // reader of lu/lr in this tick. Encoding: the next tick's contexts are
+      // known now, so the predictors run beside this whole tick.
+      if (run.flags & 1) CK(cudaMemcpyAsync(lu.p, lu_p.p, lu.n * 4, cudaMemcpyDeviceToDevice, st));
+      if (run.flags & 2) CK(cudaMemcpyAsync(lr.p, lr_p.p, lr.n * 4, cudaMemcpyDeviceToDevice, st));
+      if (!run.decode) {
+        pred.wait_for(st);
+        predict_next(pred.s);
+      }
     }
     auto gemm = [&](GemmP p, bool at, bool bt) {
       run.launches += launch_gemm(p, at, bt, act, na, st);
@@ -581,18 +596,20 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
                       d_pay_off.p, d_pay_len.p, cstate.p, act, na, run.decode,
                       run.decode ? st : cod.s);
     ++run.launches;
+    if (statics && run.decode) {  // decoding: the next contexts exist once this tick's tokens do
+      pred.wait_for(st);
+      predict_next(pred.s);
+    }
     // ---------------- backward controller (OnlineTrainer::step, mixer.cpp:57-97)
     BcP bp{probs.p, lu.p, lr.p, lm.p, s_rv, d_tokens, geo, d_td.p, int(run.t), w.p, m.p, v.p, P, oA,
            dlm.p, aterm.p, lterm.p, R, sc.p, warm_loss.p, d_warm.p, int(run.flags), R, V};
     launch_bc_dlm(bp, act, na, st);
     run.launches += 1;
-    // the mixing weight's own step (alpha is not in Adam's range and nothing
-    // in this tick reads it), then the next tick's static predictions (they
-    // overwrite lu/lr, which the alpha step reads), beside the DM backward
-    pred.wait_for(st);
-    launch_alpha_step(bp, act, na, pred.s);
+    // the mixing weight's own step: alpha is not in Adam's range and only the
+    // next tick's mixer reads it, so it runs beside the DM backward
+    cod.wait_for(st);
+    launch_alpha_step(bp, act, na, cod.s);
     run.launches += 1;
-    if (statics) predict_next(pred.s);
     // head, ffn, attention output projection (Linear::backward, layers.cpp:176-183).
     // Data gradients stay on the main stream; each weight gradient goes to the
     // side stream as soon as its operands exist (they write disjoint slices of
@@ -665,8 +682,8 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     // Adam over every DM parameter (alpha was updated by k_alpha_step)
     launch_adam(w.p, g.p, m.p, v.p, P, P - 1, sc.p, act, na, st);
     ++run.launches;
-    pred.join_into(st);
-    if (!run.decode) cod.join_into(st);
+    if (statics) pred.join_into(st);
+    cod.join_into(st);
     check_launch();
     tick_launches = run.launches - l0;
   };
