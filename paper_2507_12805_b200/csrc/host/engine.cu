@@ -12,6 +12,7 @@
 #include <memory>
 
 #include "../kernels/kernels.hpp"
+#include "../kernels/launch.cuh"
 #include "container.hpp"
 #include "nccl_loader.hpp"
 #include "plan.hpp"
@@ -302,6 +303,9 @@ DmState fetch_state(const DmLayout& L, const float* w, const float* m, const flo
 }
 
 void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
+  // programmatic dependent launch on the tick's chain, unless a predictor
+  // branch runs beside it (early-scheduled blocks would hold SMs it needs)
+  const PdlScope pdl((run.flags & 3) ? nullptr : st);
   const size_t W = run.start.size();
   const Dims& d = run.dims;
   const DmLayout lay(d);
@@ -854,6 +858,7 @@ void canonicalize_device(const uint8_t* d_raw, uint64_t n, Canon& out, cudaStrea
 BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, const Dims& dims,
                            uint32_t t, uint32_t batch, uint64_t seed, cudaStream_t st,
                            uint64_t* launches) {
+  const PdlScope pdl(st);  // programmatic dependent launch along the train step
   if (m < uint64_t(t) + 1) raise(errc::target_too_short, "target shorter than t+1 tokens");
   BiGru model = BiGru::seeded(dims, 1, seed);
   if (pub && pub->fits(dims)) {

@@ -15,6 +15,7 @@
 
 #include "detmath.cuh"
 #include "kernels.hpp"
+#include "launch.cuh"
 
 namespace pmklc_b200 {
 
@@ -37,6 +38,7 @@ template <int HS>
 __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
     BiGruP p, int l, const uint32_t* __restrict__ ctx, int64_t ctx_cs, const float* __restrict__ xi,
     float* out, float* fin, int64_t work_cs, const TickDesc* __restrict__ td) {
+  pdl_wait();
   static_assert(kRPW == 4, "rows are paired (0,1),(2,3)");
   __shared__ __align__(16) float sw[3][HS][HS];
   __shared__ __align__(16) float sh[kRecWarps][2][32][kRPW];  // h[q][row] per warp
@@ -154,6 +156,7 @@ constexpr size_t kFuseSmem =
 __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec_fused(
     BiGruP p, int l, const float* __restrict__ in, float* out, float* fin, int64_t work_cs,
     const TickDesc* __restrict__ td) {
+  pdl_wait();
   constexpr int HS = kFuseHs, IN = kFuseIn;
   extern __shared__ __align__(16) float fsm[];
   float (*sw)[HS][HS] = reinterpret_cast<float (*)[HS][HS]>(fsm);                    // [3][q][j]
@@ -269,6 +272,7 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec_fused(
 __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec_generic(
     BiGruP p, int l, const uint32_t* __restrict__ ctx, int64_t ctx_cs, const float* __restrict__ xi,
     float* out, float* fin, int64_t work_cs, const TickDesc* __restrict__ td) {
+  pdl_wait();
   extern __shared__ __align__(16) float shd[];  // [kRecWarps][2][Hs]
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
@@ -331,6 +335,7 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec_generic(
 }
 
 __global__ void k_tanh_inplace(float* x, int64_t n, int64_t cs, const TickDesc* __restrict__ td) {
+  pdl_wait();
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -352,16 +357,18 @@ __device__ __forceinline__ unsigned long long global_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-__global__ void k_hot_begin(HotTimer* h) { h->t0 = global_ns(); }
+__global__ void k_hot_begin(HotTimer* h) {
+  pdl_wait(); h->t0 = global_ns(); }
 __global__ void k_hot_end(HotTimer* h, const TickDesc* __restrict__ td) {
+  pdl_wait();
   h->ns += global_ns() - h->t0;
   h->units += unsigned(td->n_act);
   h->launches += 1;
 }
 }  // namespace
-void launch_hot_begin(HotTimer* h, cudaStream_t st) { k_hot_begin<<<1, 1, 0, st>>>(h); }
+void launch_hot_begin(HotTimer* h, cudaStream_t st) { launch_pdl(k_hot_begin, dim3(1), dim3(1), 0, st, h); }
 void launch_hot_end(HotTimer* h, const TickDesc* td, cudaStream_t st) {
-  k_hot_end<<<1, 1, 0, st>>>(h, td);
+  launch_pdl(k_hot_end, dim3(1), dim3(1), 0, st, h, td);
 }
 
 int launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, float* work,
@@ -396,7 +403,7 @@ int launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, f
         launch_hot_begin(hot, st);
         ++launches;
       }
-      k_bigru_rec_fused<<<rgrid2, kRecWarps * 32, kFuseSmem, st>>>(
+      launch_pdl(k_bigru_rec_fused, dim3(rgrid2), dim3(kRecWarps * 32), kFuseSmem, st, 
           p, l, outs[(l - 1) & 1], last ? nullptr : outs[l & 1], f, work_cs, td);
       ++launches;
       if (hot) {
@@ -436,13 +443,13 @@ int launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, f
     }
     const float* xl = l == 0 ? nullptr : xi;
     if (p.Hs == 32)
-      k_bigru_rec<32><<<rgrid2, kRecWarps * 32, 0, st>>>(p, l, ctx, ctx_cs, xl, out, f, work_cs, td);
+      launch_pdl(k_bigru_rec<32>, dim3(rgrid2), dim3(kRecWarps * 32), 0, st, p, l, ctx, ctx_cs, xl, out, f, work_cs, td);
     else if (p.Hs == 16)
-      k_bigru_rec<16><<<rgrid2, kRecWarps * 32, 0, st>>>(p, l, ctx, ctx_cs, xl, out, f, work_cs, td);
+      launch_pdl(k_bigru_rec<16>, dim3(rgrid2), dim3(kRecWarps * 32), 0, st, p, l, ctx, ctx_cs, xl, out, f, work_cs, td);
     else if (p.Hs == 8)
-      k_bigru_rec<8><<<rgrid2, kRecWarps * 32, 0, st>>>(p, l, ctx, ctx_cs, xl, out, f, work_cs, td);
+      launch_pdl(k_bigru_rec<8>, dim3(rgrid2), dim3(kRecWarps * 32), 0, st, p, l, ctx, ctx_cs, xl, out, f, work_cs, td);
     else
-      k_bigru_rec_generic<<<rgrid, kRecWarps * 32, kRecWarps * 2 * p.Hs * sizeof(float), st>>>(
+      launch_pdl(k_bigru_rec_generic, dim3(rgrid), dim3(kRecWarps * 32), kRecWarps * 2 * p.Hs * sizeof(float), st, 
           p, l, ctx, ctx_cs, xl, out, f, work_cs, td);
     ++launches;
   }
@@ -464,7 +471,7 @@ int launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, f
   g1.init = 1;
   launch_gemm(g1, false, false, td, max_active, st);
   const int64_t nb = int64_t(p.R) * p.B;
-  k_tanh_inplace<<<dim3(unsigned((nb + 255) / 256), max_active), 256, 0, st>>>(bott, nb, work_cs, td);
+  launch_pdl(k_tanh_inplace, dim3(dim3(unsigned((nb + 255) / 256), max_active)), dim3(256), 0, st, bott, nb, work_cs, td);
   GemmP g2{};
   g2.A = bott;
   g2.a_cs = work_cs;

@@ -14,6 +14,7 @@
 
 #include "detmath.cuh"
 #include "kernels.hpp"
+#include "launch.cuh"
 
 namespace pmklc_b200 {
 
@@ -37,6 +38,7 @@ __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t x) {
 }
 
 __global__ void k_mix_quantize(MixP p, const TickDesc* __restrict__ td) {
+  pdl_wait();
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -215,6 +217,7 @@ __global__ void k_mix_quantize(MixP p, const TickDesc* __restrict__ td) {
 }
 
 __global__ void k_bc_dlm(BcP p, const TickDesc* __restrict__ td) {
+  pdl_wait();
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -243,6 +246,7 @@ __global__ void k_bc_dlm(BcP p, const TickDesc* __restrict__ td) {
 // 1 lane 0 runs the (short) loss chain.
 constexpr int kAlphaBatch = 4096;
 __global__ void __launch_bounds__(256) k_alpha_step(BcP p, const TickDesc* __restrict__ td) {
+  pdl_wait();
   __shared__ __align__(16) float buf[2][kAlphaBatch];
   if (blockIdx.x >= unsigned(p.td->n_act)) return;
   const int c = p.td->act[blockIdx.x];
@@ -357,6 +361,7 @@ __device__ __forceinline__ uint32_t dec_sym(uint64_t& code, uint64_t& range, con
 __global__ void k_range_uniform(uint32_t* tokens, ChunkGeo geo, int t, int R, int V,
                                 uint8_t* payload, const uint64_t* pay_off, const uint64_t* pay_len,
                                 CoderState* cs, int n_chunks, bool decode) {
+  pdl_wait();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n_chunks) return;
   const uint64_t L = geo.L[c], start = geo.start[c];
@@ -417,6 +422,7 @@ __global__ void __launch_bounds__(kCoderWarps * 32) k_range_step(
     const uint32_t* __restrict__ freq, const uint32_t* __restrict__ cum, int64_t cs_f,
     int64_t cs_c, uint8_t* payload, const uint64_t* pay_off, const uint64_t* pay_len,
     CoderState* cs, const TickDesc* __restrict__ td, bool decode) {
+  pdl_wait();
   __shared__ uint32_t sc_[kCoderWarps][32], sf_[kCoderWarps][32];
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wi = blockIdx.x * kCoderWarps + wl;
@@ -506,6 +512,7 @@ __global__ void __launch_bounds__(kCoderWarps * 32) k_range_step(
 }
 
 __global__ void k_range_finish(uint8_t* payload, const uint64_t* pay_off, CoderState* cs, int n) {
+  pdl_wait();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= n) return;
   CoderState s = cs[c];
@@ -522,25 +529,25 @@ __global__ void k_range_finish(uint8_t* payload, const uint64_t* pay_off, CoderS
 void launch_mix_quantize(const MixP& p, const TickDesc* td, int max_active, cudaStream_t st) {
   if (max_active <= 0) return;
   dim3 grid(unsigned((int64_t(p.R) * 32 + 255) / 256), max_active);
-  k_mix_quantize<<<grid, 256, 0, st>>>(p, td);
+  launch_pdl(k_mix_quantize, dim3(grid), dim3(256), 0, st, p, td);
 }
 
 void launch_bc_dlm(const BcP& p, const TickDesc* td, int max_active, cudaStream_t st) {
   if (max_active <= 0) return;
   dim3 grid(unsigned((int64_t(p.R) * p.V + 255) / 256), max_active);
-  k_bc_dlm<<<grid, 256, 0, st>>>(p, td);
+  launch_pdl(k_bc_dlm, dim3(grid), dim3(256), 0, st, p, td);
 }
 
 void launch_alpha_step(const BcP& p, const TickDesc* td, int max_active, cudaStream_t st) {
   if (max_active <= 0) return;
-  k_alpha_step<<<unsigned(max_active), 256, 0, st>>>(p, td);
+  launch_pdl(k_alpha_step, dim3(unsigned(max_active)), dim3(256), 0, st, p, td);
 }
 
 void launch_range_uniform(uint32_t* tokens, ChunkGeo geo, int t, int R, int V, uint8_t* payload,
                           const uint64_t* pay_off, const uint64_t* pay_len, CoderState* cs,
                           int n_chunks, bool decode, cudaStream_t st) {
   if (n_chunks <= 0) return;
-  k_range_uniform<<<unsigned((n_chunks + 63) / 64), 64, 0, st>>>(tokens, geo, t, R, V, payload,
+  launch_pdl(k_range_uniform, dim3(unsigned((n_chunks + 63) / 64)), dim3(64), 0, st, tokens, geo, t, R, V, payload,
                                                                  pay_off, pay_len, cs, n_chunks,
                                                                  decode);
 }
@@ -551,7 +558,7 @@ void launch_range_step(uint32_t* tokens, ChunkGeo geo, int t, int R, int V,
                        CoderState* cs, const TickDesc* td, int max_active, bool decode,
                        cudaStream_t st) {
   if (max_active <= 0) return;
-  k_range_step<<<unsigned((max_active + kCoderWarps - 1) / kCoderWarps), kCoderWarps * 32, 0, st>>>(tokens, geo, t, R, V, freq, cum,
+  launch_pdl(k_range_step, dim3(unsigned((max_active + kCoderWarps - 1) / kCoderWarps)), dim3(kCoderWarps * 32), 0, st, tokens, geo, t, R, V, freq, cum,
                                                               cs_f, cs_c, payload, pay_off, pay_len,
                                                               cs, td, decode);
 }
@@ -559,7 +566,7 @@ void launch_range_step(uint32_t* tokens, ChunkGeo geo, int t, int R, int V,
 void launch_range_finish(uint8_t* payload, const uint64_t* pay_off, CoderState* cs, int n_chunks,
                          cudaStream_t st) {
   if (n_chunks <= 0) return;
-  k_range_finish<<<unsigned((n_chunks + 63) / 64), 64, 0, st>>>(payload, pay_off, cs, n_chunks);
+  launch_pdl(k_range_finish, dim3(unsigned((n_chunks + 63) / 64)), dim3(64), 0, st, payload, pay_off, cs, n_chunks);
 }
 
 }  // namespace pmklc_b200

@@ -15,6 +15,7 @@
 
 #include "detmath.cuh"
 #include "kernels.hpp"
+#include "launch.cuh"
 
 namespace pmklc_b200 {
 
@@ -46,6 +47,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 template <bool AT, bool BT, int TM, int TN, int BK, int STAGES, int TX, int TY>
 __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc* __restrict__ td) {
+  pdl_wait();
   constexpr int NT = TX * TY, BM = TY * TM, BN = TX * TN;
   __shared__ __align__(16) float As[STAGES][BK][BM + 4];
   __shared__ __align__(16) float Bs[STAGES][BK][BN + 4];
@@ -253,7 +255,7 @@ void gemm_launch(const GemmP& p, const TickDesc* td, int max_active, cudaStream_
   const int Mx = p.M + (p.ones_row ? 1 : 0);
   const int np = p.nprob > 1 ? p.nprob : 1;
   dim3 grid((p.N + TX * TN - 1) / (TX * TN), (Mx + TY * TM - 1) / (TY * TM), max_active * np);
-  k_gemm_tiled<AT, BT, TM, TN, BK, STAGES, TX, TY><<<grid, TX * TY, 0, st>>>(p, td);
+  launch_pdl(k_gemm_tiled<AT, BT, TM, TN, BK, STAGES, TX, TY>, dim3(grid), dim3(TX * TY), 0, st, p, td);
 }
 
 template <bool AT, bool BT>
@@ -380,6 +382,7 @@ __device__ __forceinline__ f2_t nt_tile_rpt2(f2_t acc, const float* as, const fl
 // 16 loads in flight per batch.
 template <bool BT>
 __global__ void __launch_bounds__(128) k_bias_row(GemmP p, const TickDesc* __restrict__ td) {
+  pdl_wait();
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
@@ -407,6 +410,7 @@ __global__ void __launch_bounds__(128) k_bias_row(GemmP p, const TickDesc* __res
 // cover the L2 latency alone.
 template <bool VEC, int RPT, int STAGES, int BK>
 __global__ void __launch_bounds__(kNwWarps * 32) k_gemm_nt(NtBatch nb, const TickDesc* __restrict__ td) {
+  pdl_wait();
   constexpr int kNwStages = STAGES, kNwBK = BK, kNwSB = BK + 4;
   extern __shared__ __align__(128) float sm[];
   if (blockIdx.y >= unsigned(td->n_act)) return;
@@ -548,6 +552,7 @@ __global__ void k_embed(const uint32_t* __restrict__ tokens, ChunkGeo geo,
                         const float* __restrict__ params, int64_t p_cs, int64_t off_emb,
                         int64_t off_pos, uint32_t* ctx, int64_t ctx_cs, float* xT, int64_t x_cs,
                         float* xl, int64_t xl_cs, DmDims d, const TickDesc* __restrict__ td) {
+  pdl_wait();
   // thread per coded position (r, t): one token gather, all E features
   // (x[j] = emb[tok][j] + pos[t][j], feature-major stores coalesced over rt)
   if (blockIdx.y >= unsigned(td->n_act)) return;
@@ -594,6 +599,7 @@ __global__ void k_attn_fwd(const float* __restrict__ q, const float* __restrict_
                            const float* __restrict__ v, float* wts, float* cx, int64_t cs_q,
                            int64_t cs_kv, int64_t cs_w, DmDims d, float inv,
                            const TickDesc* __restrict__ td) {
+  pdl_wait();
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -645,6 +651,7 @@ __global__ void __launch_bounds__(256) k_attn_bwd(const float* __restrict__ q, c
                            const float* __restrict__ dctx, float* dq, float* dkT, float* dvT,
                            int64_t cs_q, int64_t cs_kv, int64_t cs_w, DmDims d, float inv,
                            const TickDesc* __restrict__ td) {
+  pdl_wait();
   __shared__ float sds[8][kAttnMaxT];
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
@@ -735,6 +742,7 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_fwd_row(
     const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
     float* wts, float* cx, int64_t cs_q, int64_t cs_kv, int64_t cs_w, DmDims d, float inv,
     const TickDesc* __restrict__ td) {
+  pdl_wait();
   extern __shared__ __align__(128) float sm[];
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
@@ -801,6 +809,7 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
     const float* __restrict__ wts, const float* __restrict__ dctx, float* dq, float* dkT,
     float* dvT, int64_t cs_q, int64_t cs_kv, int64_t cs_w, DmDims d, float inv, AttnDx fx,
     const TickDesc* __restrict__ td) {
+  pdl_wait();
   extern __shared__ __align__(128) float sm[];
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
@@ -935,6 +944,7 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
 __global__ void k_pos_bwd(const float* __restrict__ dx, int64_t dx_cs, const float* __restrict__ dxl,
                           int64_t dxl_cs, float* grads, int64_t g_cs, int64_t off_pos, DmDims d,
                           const TickDesc* __restrict__ td) {
+  pdl_wait();
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -976,6 +986,7 @@ __global__ void __launch_bounds__(kEmbWarps * 32) k_emb_bwd(
     const uint32_t* __restrict__ ctx, int64_t ctx_cs, const float* __restrict__ dx, int64_t dx_cs,
     const float* __restrict__ dxl, int64_t dxl_cs, float* grads, int64_t g_cs, int64_t off_emb,
     DmDims d, const TickDesc* __restrict__ td) {
+  pdl_wait();
   __shared__ uint32_t sctx[kEmbSeg];
   __shared__ uint16_t hits[kEmbWarps][kEmbSeg];
   if (blockIdx.y >= unsigned(td->n_act)) return;
@@ -1069,6 +1080,7 @@ __global__ void __launch_bounds__(kSortThreads) k_emb_bwd_sorted(
     const uint32_t* __restrict__ ctx, int64_t ctx_cs, const float* __restrict__ dx, int64_t dx_cs,
     const float* __restrict__ dxl, int64_t dxl_cs, float* grads, int64_t g_cs, int64_t off_emb,
     DmDims d, const TickDesc* __restrict__ td) {
+  pdl_wait();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* vals = reinterpret_cast<float*>(smem_raw);
   uint16_t* sorted = reinterpret_cast<uint16_t*>(vals + kSortVals);
@@ -1234,7 +1246,7 @@ static void launch_sorted_emb(const uint32_t* ctx, int64_t ctx_cs, const float* 
   // split the vocabulary over several blocks per chunk while chunks alone
   // cannot fill the chip (each block re-sorts; the gather and walk split)
   const int groups = std::max(1, std::min(std::min(8, d.V), 148 / std::max(1, max_active)));
-  k_emb_bwd_sorted<<<dim3(unsigned(groups), unsigned(max_active)), kSortThreads, kSortSmem, st>>>(
+  launch_pdl(k_emb_bwd_sorted, dim3(dim3(unsigned(groups), unsigned(max_active))), dim3(kSortThreads), kSortSmem, st, 
       ctx, ctx_cs, dx, dx_cs, dxl, dxl_cs, grads, g_cs, off_emb, d, td);
 }
 
@@ -1242,6 +1254,7 @@ static void launch_sorted_emb(const uint32_t* ctx, int64_t ctx_cs, const float* 
 __global__ void k_adam(float* __restrict__ w, float* __restrict__ g, float* __restrict__ m,
                        float* __restrict__ v, int64_t p_cs, int64_t n,
                        const AdamScalars* __restrict__ sc, const TickDesc* __restrict__ td) {
+  pdl_wait();
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
   const float bc1 = sc[c].bc1, bc2 = sc[c].bc2;
@@ -1265,6 +1278,7 @@ __global__ void k_adam(float* __restrict__ w, float* __restrict__ g, float* __re
 
 __global__ void k_state_copy(float* w, float* m, float* v, AdamScalars* sc, int64_t p_cs, int64_t n,
                              const TickDesc* __restrict__ td) {
+  pdl_wait();
   if (blockIdx.y >= unsigned(td->n_hand)) return;
   const int2 pr = td->hand[blockIdx.y];  // x = src, y = dst
   const int64_t so = pr.x * p_cs, dof = pr.y * p_cs;
@@ -1280,6 +1294,7 @@ __global__ void k_state_copy(float* w, float* m, float* v, AdamScalars* sc, int6
 __global__ void k_tick_advance(TickDesc* td, const uint32_t* __restrict__ act_ptr,
                                const int* __restrict__ act_all, const uint32_t* __restrict__ hand_ptr,
                                const int2* __restrict__ hand_all, int64_t ticks) {
+  pdl_wait();
   const int64_t t = td->tick + 1;
   td->tick = t;
   if (t < ticks) {
@@ -1298,6 +1313,7 @@ __global__ void k_tick_advance(TickDesc* td, const uint32_t* __restrict__ act_pt
 __global__ void k_tick_peek(const TickDesc* __restrict__ cur, TickDesc* next,
                             const uint32_t* __restrict__ act_ptr, const int* __restrict__ act_all,
                             int64_t ticks) {
+  pdl_wait();
   const int64_t t = cur->tick + 1;
   next->tick = t;
   next->hand = nullptr;
@@ -1314,6 +1330,7 @@ __global__ void k_tick_peek(const TickDesc* __restrict__ cur, TickDesc* next,
 // Context tokens of every active chunk's coded rows (k_embed's ctx gather alone)
 __global__ void k_ctx_gather(const uint32_t* __restrict__ tokens, ChunkGeo geo, uint32_t* ctx,
                              int64_t ctx_cs, DmDims d, const TickDesc* __restrict__ td) {
+  pdl_wait();
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
   const int64_t RT = int64_t(d.R) * d.T;
@@ -1329,13 +1346,13 @@ __global__ void k_ctx_gather(const uint32_t* __restrict__ tokens, ChunkGeo geo, 
 
 void launch_tick_peek(const TickDesc* cur, TickDesc* next, const uint32_t* act_ptr,
                       const int* act_all, int64_t ticks, cudaStream_t st) {
-  k_tick_peek<<<1, 1, 0, st>>>(cur, next, act_ptr, act_all, ticks);
+  launch_pdl(k_tick_peek, dim3(1), dim3(1), 0, st, cur, next, act_ptr, act_all, ticks);
 }
 void launch_ctx_gather(const uint32_t* tokens, ChunkGeo geo, uint32_t* ctx, int64_t ctx_cs,
                        DmDims d, const TickDesc* td, int max_active, cudaStream_t st) {
   if (max_active <= 0) return;
   const int64_t RT = int64_t(d.R) * d.T;
-  k_ctx_gather<<<dim3(unsigned((RT + 255) / 256), max_active), 256, 0, st>>>(tokens, geo, ctx, ctx_cs,
+  launch_pdl(k_ctx_gather, dim3(dim3(unsigned((RT + 255) / 256), max_active)), dim3(256), 0, st, tokens, geo, ctx, ctx_cs,
                                                                              d, td);
 }
 
@@ -1352,8 +1369,8 @@ int launch_gemm(const GemmP& p, bool at, bool bt, const TickDesc* td, int max_ac
     q.ones_row = 0;
     const int n = launch_gemm(q, at, bt, td, max_active, st);
     const dim3 grid(unsigned((p.N + 127) / 128), unsigned(max_active));
-    if (bt) k_bias_row<true><<<grid, 128, 0, st>>>(p, td);
-    else k_bias_row<false><<<grid, 128, 0, st>>>(p, td);
+    if (bt) launch_pdl(k_bias_row<true>, dim3(grid), dim3(128), 0, st, p, td);
+    else launch_pdl(k_bias_row<false>, dim3(grid), dim3(128), 0, st, p, td);
     return n + 1;
   }
   if (at && bt) gemm_dispatch<true, true>(p, td, max_active, st);
@@ -1408,8 +1425,8 @@ void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int m
   const dim3 grid(unsigned((tasks + kNwWarps - 1) / kNwWarps), unsigned(max_active));
   const size_t smem = size_t(kNwWarps) * nw_warp_floats(rpt, stages, bk) * sizeof(float);
 #define PMKLC_NT_LAUNCH(R, S, K)                                                               \
-  if (vec) k_gemm_nt<true, R, S, K><<<grid, kNwWarps * 32, smem, st>>>(nb, td);               \
-  else k_gemm_nt<false, R, S, K><<<grid, kNwWarps * 32, smem, st>>>(nb, td);
+  if (vec) launch_pdl(k_gemm_nt<true, R, S, K>, dim3(grid), dim3(kNwWarps * 32), smem, st, nb, td);               \
+  else launch_pdl(k_gemm_nt<false, R, S, K>, dim3(grid), dim3(kNwWarps * 32), smem, st, nb, td);
   if (rpt == 8) {
     PMKLC_NT_LAUNCH(8, 3, 32)
   } else if (rpt == 4) {
@@ -1435,7 +1452,7 @@ void launch_embed(const uint32_t* tokens, ChunkGeo geo, const float* params,
   if (max_active <= 0) return;
   const int64_t total = int64_t(d.R) * d.T;  // one thread per coded position
   dim3 grid(unsigned((total + 255) / 256), max_active);
-  k_embed<<<grid, 256, 0, st>>>(tokens, geo, params, p_cs, off_emb, off_pos, ctx, ctx_cs, x,
+  launch_pdl(k_embed, dim3(grid), dim3(256), 0, st, tokens, geo, params, p_cs, off_emb, off_pos, ctx, ctx_cs, x,
                                 x_cs, xl, xl_cs, d, td);
 }
 
@@ -1450,13 +1467,13 @@ void launch_attn_fwd(const float* q, const float* k, const float* v, float* wts,
       cudaFuncSetAttribute(k_attn_fwd_row, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       attr = smem;
     }
-    k_attn_fwd_row<<<dim3(d.R, max_active), kRowThreads, smem, st>>>(q, k, v, wts, cx, cs_q, cs_kv,
+    launch_pdl(k_attn_fwd_row, dim3(dim3(d.R, max_active)), dim3(kRowThreads), smem, st, q, k, v, wts, cx, cs_q, cs_kv,
                                                                       cs_w, d, inv, td);
     return;
   }
   const int64_t warps = int64_t(d.R) * d.NH;
   dim3 grid(unsigned((warps * 32 + 255) / 256), max_active);
-  k_attn_fwd<<<grid, 256, 0, st>>>(q, k, v, wts, cx, cs_q, cs_kv, cs_w, d, inv, td);
+  launch_pdl(k_attn_fwd, dim3(grid), dim3(256), 0, st, q, k, v, wts, cx, cs_q, cs_kv, cs_w, d, inv, td);
 }
 
 bool launch_attn_bwd(const float* q, const float* k, const float* v, const float* wts,
@@ -1478,13 +1495,13 @@ bool launch_attn_bwd(const float* q, const float* k, const float* v, const float
     }
     AttnDx f = fx;
     if (!fuse) f.dx = nullptr;
-    k_attn_bwd_row<<<dim3(d.R, max_active), kRowThreads, smem, st>>>(
+    launch_pdl(k_attn_bwd_row, dim3(dim3(d.R, max_active)), dim3(kRowThreads), smem, st, 
         q, k, v, wts, dctx, dq, dk, dv, cs_q, cs_kv, cs_w, d, inv, f, td);
     return fuse;
   }
   const int64_t warps = int64_t(d.R) * d.NH;
   dim3 grid(unsigned((warps * 32 + 255) / 256), max_active);
-  k_attn_bwd<<<grid, 256, 0, st>>>(q, k, v, wts, dctx, dq, dk, dv, cs_q, cs_kv, cs_w, d, inv,
+  launch_pdl(k_attn_bwd, dim3(grid), dim3(256), 0, st, q, k, v, wts, dctx, dq, dk, dv, cs_q, cs_kv, cs_w, d, inv,
                                    td);
   return false;
 }
@@ -1498,7 +1515,7 @@ void launch_emb_grad(const uint32_t* ctx, int64_t ctx_cs, const float* dx, int64
     return;
   }
   dim3 g2(unsigned((d.V + kEmbWarps - 1) / kEmbWarps), max_active);
-  k_emb_bwd<<<g2, kEmbWarps * 32, 0, st>>>(ctx, ctx_cs, dx, dx_cs, nullptr, 0, grads, g_cs, off_emb,
+  launch_pdl(k_emb_bwd, dim3(g2), dim3(kEmbWarps * 32), 0, st, ctx, ctx_cs, dx, dx_cs, nullptr, 0, grads, g_cs, off_emb,
                                            d, td);
 }
 
@@ -1508,14 +1525,14 @@ void launch_embed_bwd(const uint32_t* ctx, int64_t ctx_cs, const float* dx, int6
                       cudaStream_t st) {
   if (max_active <= 0) return;
   dim3 g1(unsigned((d.T * d.E + 255) / 256), max_active);
-  k_pos_bwd<<<g1, 256, 0, st>>>(dx, dx_cs, dxl, dxl_cs, grads, g_cs, off_pos, d, td);
+  launch_pdl(k_pos_bwd, dim3(g1), dim3(256), 0, st, dx, dx_cs, dxl, dxl_cs, grads, g_cs, off_pos, d, td);
   if (sorted_emb_ok(d)) {
     launch_sorted_emb(ctx, ctx_cs, dx, dx_cs, dxl, dxl_cs, grads, g_cs, off_emb, d, td, max_active,
                       st);
     return;
   }
   dim3 g2(unsigned((d.V + kEmbWarps - 1) / kEmbWarps), max_active);
-  k_emb_bwd<<<g2, kEmbWarps * 32, 0, st>>>(ctx, ctx_cs, dx, dx_cs, dxl, dxl_cs, grads, g_cs, off_emb, d,
+  launch_pdl(k_emb_bwd, dim3(g2), dim3(kEmbWarps * 32), 0, st, ctx, ctx_cs, dx, dx_cs, dxl, dxl_cs, grads, g_cs, off_emb, d,
                                 td);
 }
 
@@ -1524,7 +1541,7 @@ void launch_adam(float* w, float* g, float* m, float* v, int64_t p_cs, int64_t n
   if (max_active <= 0 || n <= 0) return;
   const int64_t per = (n + 255) / 256;
   dim3 grid(unsigned(per < 64 ? per : 64), max_active);
-  k_adam<<<grid, 256, 0, st>>>(w, g, m, v, p_cs, n, sc, td);
+  launch_pdl(k_adam, dim3(grid), dim3(256), 0, st, w, g, m, v, p_cs, n, sc, td);
 }
 
 void launch_state_copy(float* w, float* m, float* v, AdamScalars* sc, int64_t p_cs, int64_t n,
@@ -1532,13 +1549,13 @@ void launch_state_copy(float* w, float* m, float* v, AdamScalars* sc, int64_t p_
   if (max_pairs <= 0) return;
   const int64_t per = (n + 255) / 256;
   dim3 grid(unsigned(per < 64 ? per : 64), max_pairs);
-  k_state_copy<<<grid, 256, 0, st>>>(w, m, v, sc, p_cs, n, td);
+  launch_pdl(k_state_copy, dim3(grid), dim3(256), 0, st, w, m, v, sc, p_cs, n, td);
 }
 
 void launch_tick_advance(TickDesc* td, const uint32_t* act_ptr, const int* act_all,
                          const uint32_t* hand_ptr, const int2* hand_all, int64_t ticks,
                          cudaStream_t st) {
-  k_tick_advance<<<1, 1, 0, st>>>(td, act_ptr, act_all, hand_ptr, hand_all, ticks);
+  launch_pdl(k_tick_advance, dim3(1), dim3(1), 0, st, td, act_ptr, act_all, hand_ptr, hand_all, ticks);
 }
 
 }  // namespace pmklc_b200

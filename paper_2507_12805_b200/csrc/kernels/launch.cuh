@@ -1,0 +1,49 @@
+// Programmatic dependent launch (PDL). Kernels are launched with programmatic
+// stream serialization, so a kernel's blocks can be scheduled while its stream
+// predecessor drains (also inside captured graphs); every kernel starts with
+// pdl_wait() -- griddepcontrol.wait, a no-op when launched without the
+// attribute -- which returns once the predecessor grid has completed and its
+// memory is visible, so no kernel touches memory before its inputs exist.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <utility>
+
+namespace pmklc_b200 {
+
+__device__ __forceinline__ void pdl_wait() {
+#if defined(__CUDA_ARCH__)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+// The attribute is used only on the stream registered here (the engine's
+// critical chain): on a side stream that runs concurrently with other work,
+// early-scheduled blocks idle at the wait while holding SM slots.
+inline cudaStream_t& pdl_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  return s;
+}
+struct PdlScope {  // registers `s` as the PDL stream for the scope
+  cudaStream_t prev;
+  explicit PdlScope(cudaStream_t s) : prev(pdl_stream()) { pdl_stream() = s; }
+  ~PdlScope() { pdl_stream() = prev; }
+};
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (st != nullptr && st == pdl_stream()) ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+}  // namespace pmklc_b200

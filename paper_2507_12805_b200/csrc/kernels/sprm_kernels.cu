@@ -14,6 +14,7 @@
 
 #include "detmath.cuh"
 #include "kernels.hpp"
+#include "launch.cuh"
 
 namespace pmklc_b200 {
 
@@ -28,6 +29,7 @@ __device__ __forceinline__ int64_t goff(const int64_t* offs, int dir, int t) {
 // the GRU inputs X[d][i][k] and the per-token layer-0 projection table.
 __global__ void k_sprm_prep(const uint32_t* __restrict__ tokens, const int64_t* __restrict__ pos,
                             SprmP s, uint32_t* ctx, float* X, float* tab) {
+  pdl_wait();
   const int64_t p = *pos;
   const int R = s.R, T = s.T, Es = s.Es, H = s.H, V = s.V;
   const int64_t RT = int64_t(R) * T;
@@ -66,6 +68,7 @@ __global__ void k_sprm_prep(const uint32_t* __restrict__ tokens, const int64_t* 
 __global__ void __launch_bounds__(256) k_sprm_fwd(SprmP s, const uint32_t* __restrict__ ctx,
                                                   const float* __restrict__ tab, float* tape,
                                                   float* fin) {
+  pdl_wait();
   __shared__ __align__(16) float sh[8][2][32];
   __shared__ float sw[3][32][32];  // [gate][q][j] = W_h{r,z,n}[q][j]
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -132,6 +135,7 @@ constexpr int kFwdWarps = 4;
 __global__ void __launch_bounds__(kFwdWarps * 32) k_sprm_fwd32(SprmP s, const uint32_t* __restrict__ ctx,
                                                                const float* __restrict__ tab, float* tape,
                                                                float* fin) {
+  pdl_wait();
   constexpr int H = 32;
   __shared__ __align__(16) float sh[kFwdWarps][2][H];
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -210,6 +214,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_sprm_fwd32(SprmP s, const ui
 __global__ void k_sprm_ce(SprmP s, const uint32_t* __restrict__ tokens,
                           const int64_t* __restrict__ pos, const float* __restrict__ logits,
                           float* g) {
+  pdl_wait();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= s.R) return;
   const int V = s.V;
@@ -241,6 +246,7 @@ __global__ void k_sprm_ce(SprmP s, const uint32_t* __restrict__ tokens,
 
 // dbact *= (1 - a*a)   (models.cpp:81-84)
 __global__ void k_sprm_tanh_grad(float* dbact, const float* __restrict__ bact, int64_t n) {
+  pdl_wait();
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) {
     const float a = bact[i];
@@ -255,6 +261,7 @@ __global__ void k_sprm_tanh_grad(float* dbact, const float* __restrict__ bact, i
 // transposed afterwards into the feature-major reduction operands.
 __global__ void __launch_bounds__(256) k_sprm_bptt(SprmP s, const float* __restrict__ tape,
                                                    const float* __restrict__ dfin, float* Gt) {
+  pdl_wait();
   __shared__ float swt[3][32][33];              // [gate][q][j] = W_h{gate}[j][q]
   __shared__ __align__(16) float sg[8][3][32];  // dhh, dar, daz of this step
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -325,6 +332,7 @@ __global__ void __launch_bounds__(256) k_sprm_bptt(SprmP s, const float* __restr
 constexpr int kBpttWarps = 4;
 __global__ void __launch_bounds__(kBpttWarps * 32) k_sprm_bptt32(SprmP s, const float* __restrict__ tape,
                                                                  const float* __restrict__ dfin, float* Gt) {
+  pdl_wait();
   constexpr int H = 32;
   __shared__ __align__(16) float sg[kBpttWarps][3][H];  // dhh, dar, daz of this step
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -414,6 +422,7 @@ __global__ void __launch_bounds__(kBpttWarps * 32) k_sprm_bptt32(SprmP s, const 
 // of one per tile.
 constexpr int kTrSlabs = 10;
 __global__ void __launch_bounds__(256) k_sprm_transpose(SprmP s, const float* __restrict__ Gt, float* G) {
+  pdl_wait();
   __shared__ float tile[32][33];
   const int T = s.T, H = s.H, R = s.R;
   const int64_t RT = int64_t(R) * T;
@@ -457,6 +466,7 @@ __global__ void __launch_bounds__(256) k_sprm_transpose(SprmP s, const float* __
 // dx[r][t][i] = (0 + dxt_fwd(t)) + (0 + dxt_bwd(T-1-t)),
 // dxt(t) = 0 + dan.W_in^T + dar.W_ir^T + daz.W_iz^T   (layers.cpp:300-304, 384-386)
 __global__ void k_sprm_dx(SprmP s, const float* __restrict__ Gr, float* dx) {
+  pdl_wait();
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int R = s.R, T = s.T, Es = s.Es, H = s.H;
   const int64_t RT = int64_t(R) * T;
@@ -488,6 +498,7 @@ __global__ void k_sprm_dx(SprmP s, const float* __restrict__ Gr, float* dx) {
 // vectors, read with LDG.128 and shared by the Es threads of the position;
 // the input weights sit in shared memory. Same chain order as k_sprm_dx.
 __global__ void __launch_bounds__(256) k_sprm_dx_t(SprmP s, const float* __restrict__ Gt, float* dx) {
+  pdl_wait();
   constexpr int H = 32;
   __shared__ __align__(16) float sw[2][3][8][H];  // [d][gate n,r,z][i][q]
   const int R = s.R, T = s.T, Es = s.Es;
@@ -533,11 +544,13 @@ __global__ void __launch_bounds__(256) k_sprm_dx_t(SprmP s, const float* __restr
 }
 
 __global__ void k_tanh_vec(float* x, int64_t n) {
+  pdl_wait();
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) x[i] = det_tanh(x[i]);
 }
 
 __global__ void k_adam_scalars(AdamScalars* sc) {
+  pdl_wait();
   AdamScalars a = *sc;
   a.step += 1;
   a.b1p = fmul(a.b1p, 0.9f);
@@ -547,7 +560,8 @@ __global__ void k_adam_scalars(AdamScalars* sc) {
   *sc = a;
 }
 
-__global__ void k_pos_advance(int64_t* pos, int64_t by) { *pos += by; }
+__global__ void k_pos_advance(int64_t* pos, int64_t by) {
+  pdl_wait(); *pos += by; }
 
 }  // namespace
 
@@ -555,52 +569,52 @@ void launch_sprm_prep(const uint32_t* tokens, const int64_t* pos, const SprmP& s
                       float* X, float* tab, cudaStream_t st) {
   const int64_t n = std::max<int64_t>(std::max<int64_t>(int64_t(s.R) * s.T, 6ll * s.V * s.H),
                                       2ll * s.Es * s.R * s.T);
-  k_sprm_prep<<<unsigned((n + 255) / 256), 256, 0, st>>>(tokens, pos, s, ctx, X, tab);
+  launch_pdl(k_sprm_prep, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, tokens, pos, s, ctx, X, tab);
 }
 void launch_sprm_fwd(const SprmP& s, const uint32_t* ctx, const float* tab, float* tape, float* fin,
                      cudaStream_t st) {
   if (s.H == 32) {
-    k_sprm_fwd32<<<unsigned(2 * ((s.R + kFwdWarps - 1) / kFwdWarps)), kFwdWarps * 32, 0, st>>>(
+    launch_pdl(k_sprm_fwd32, dim3(unsigned(2 * ((s.R + kFwdWarps - 1) / kFwdWarps))), dim3(kFwdWarps * 32), 0, st, 
         s, ctx, tab, tape, fin);
     return;
   }
-  k_sprm_fwd<<<unsigned(2 * ((s.R + 7) / 8)), 256, 0, st>>>(s, ctx, tab, tape, fin);
+  launch_pdl(k_sprm_fwd, dim3(unsigned(2 * ((s.R + 7) / 8))), dim3(256), 0, st, s, ctx, tab, tape, fin);
 }
 void launch_sprm_ce(const SprmP& s, const uint32_t* tokens, const int64_t* pos, const float* logits,
                     float* g, cudaStream_t st) {
-  k_sprm_ce<<<unsigned((s.R * 32 + 255) / 256), 256, 0, st>>>(s, tokens, pos, logits, g);
+  launch_pdl(k_sprm_ce, dim3(unsigned((s.R * 32 + 255) / 256)), dim3(256), 0, st, s, tokens, pos, logits, g);
 }
 void launch_sprm_tanh_grad(float* dbact, const float* bact, int64_t n, cudaStream_t st) {
-  k_sprm_tanh_grad<<<unsigned((n + 255) / 256), 256, 0, st>>>(dbact, bact, n);
+  launch_pdl(k_sprm_tanh_grad, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, dbact, bact, n);
 }
 void launch_sprm_bptt(const SprmP& s, const float* tape, const float* dfin, float* Gt,
                       cudaStream_t st) {
   if (s.H == 32)
-    k_sprm_bptt32<<<unsigned(2 * ((s.R + kBpttWarps - 1) / kBpttWarps)), kBpttWarps * 32, 0, st>>>(
+    launch_pdl(k_sprm_bptt32, dim3(unsigned(2 * ((s.R + kBpttWarps - 1) / kBpttWarps))), dim3(kBpttWarps * 32), 0, st, 
         s, tape, dfin, Gt);
   else
-    k_sprm_bptt<<<unsigned(2 * ((s.R + 7) / 8)), 256, 0, st>>>(s, tape, dfin, Gt);
+    launch_pdl(k_sprm_bptt, dim3(unsigned(2 * ((s.R + 7) / 8))), dim3(256), 0, st, s, tape, dfin, Gt);
 }
 void launch_sprm_transpose(const SprmP& s, const float* Gt, float* G, cudaStream_t st) {
   const int64_t RT = int64_t(s.R) * s.T;
   dim3 grid(unsigned((RT + 31) / 32), unsigned((s.H + 31) / 32));
-  k_sprm_transpose<<<grid, dim3(32, 8), 0, st>>>(s, Gt, G);
+  launch_pdl(k_sprm_transpose, dim3(grid), dim3(dim3(32, 8)), 0, st, s, Gt, G);
 }
 bool sprm_dx_time_major(const SprmP& s) { return s.H == 32 && s.Es <= 8; }
 void launch_sprm_dx(const SprmP& s, const float* G, const float* Gt, float* dx, cudaStream_t st) {
   const int64_t n = int64_t(s.R) * s.T * s.Es;
   if (sprm_dx_time_major(s) && Gt) {
-    k_sprm_dx_t<<<unsigned((n + 255) / 256), 256, 0, st>>>(s, Gt, dx);
+    launch_pdl(k_sprm_dx_t, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, s, Gt, dx);
     return;
   }
-  k_sprm_dx<<<unsigned((n + 255) / 256), 256, 0, st>>>(s, G, dx);
+  launch_pdl(k_sprm_dx, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, s, G, dx);
 }
 void launch_tanh_vec(float* x, int64_t n, cudaStream_t st) {
-  k_tanh_vec<<<unsigned((n + 255) / 256), 256, 0, st>>>(x, n);
+  launch_pdl(k_tanh_vec, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, x, n);
 }
-void launch_adam_scalars(AdamScalars* sc, cudaStream_t st) { k_adam_scalars<<<1, 1, 0, st>>>(sc); }
+void launch_adam_scalars(AdamScalars* sc, cudaStream_t st) { launch_pdl(k_adam_scalars, dim3(1), dim3(1), 0, st, sc); }
 void launch_pos_advance(int64_t* pos, int64_t by, cudaStream_t st) {
-  k_pos_advance<<<1, 1, 0, st>>>(pos, by);
+  launch_pdl(k_pos_advance, dim3(1), dim3(1), 0, st, pos, by);
 }
 
 }  // namespace pmklc_b200

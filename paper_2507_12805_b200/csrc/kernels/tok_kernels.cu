@@ -12,6 +12,7 @@
 #include <cstring>
 
 #include "kernels.hpp"
+#include "launch.cuh"
 
 namespace pmklc_b200 {
 
@@ -77,6 +78,7 @@ __global__ void __launch_bounds__(kTokThreads) k_skmer_packed(const uint8_t* __r
                                                               uint64_t n, uint32_t s, uint32_t k,
                                                               TokT* __restrict__ tokens,
                                                               uint64_t m) {
+  pdl_wait();
   __shared__ __align__(16) uint32_t sw[kStageBytes / 4];
   constexpr int kTokPerBlock = kTokThreads * kTokPerThread;
   const uint64_t j0 = uint64_t(blockIdx.x) * kTokPerBlock;
@@ -104,6 +106,7 @@ __global__ void __launch_bounds__(kTokThreads) k_skmer_bytes(const uint8_t* __re
                                                              uint64_t n, uint32_t s, uint32_t k,
                                                              uint32_t* __restrict__ tokens,
                                                              uint64_t m) {
+  pdl_wait();
   __shared__ __align__(16) uint32_t sw[kStageBytes / 4];
   constexpr int kTokPerBlock = kTokThreads * kTokPerThread;
   const uint64_t j0 = uint64_t(blockIdx.x) * kTokPerBlock;
@@ -148,6 +151,7 @@ __device__ __forceinline__ bool is_acgt(uint32_t c) {
 }
 
 __global__ void k_canon_count(const uint8_t* __restrict__ raw, uint64_t n, uint32_t* counts) {
+  pdl_wait();
   const uint64_t b0 = uint64_t(blockIdx.x) * kCanonPerBlock + threadIdx.x * kCanonPerThread;
   uint32_t c = 0;
   for (int i = 0; i < kCanonPerThread; ++i)
@@ -168,6 +172,7 @@ __global__ void k_canon_count(const uint8_t* __restrict__ raw, uint64_t n, uint3
 __global__ void k_canon_scatter(const uint8_t* __restrict__ raw, uint64_t n,
                                 const uint64_t* __restrict__ block_exc, uint8_t* codes,
                                 uint64_t* exc_pos, uint8_t* exc_byte) {
+  pdl_wait();
   const uint64_t b0 = uint64_t(blockIdx.x) * kCanonPerBlock + threadIdx.x * kCanonPerThread;
   uint32_t c = 0;
   uint8_t v[kCanonPerThread];
@@ -207,6 +212,7 @@ __global__ void k_detok_restore(const uint32_t* __restrict__ tokens, uint64_t m,
                                 const uint64_t* __restrict__ exc_pos,
                                 const uint8_t* __restrict__ exc_byte, uint64_t n_exc,
                                 uint8_t* __restrict__ out, uint64_t out_len, int* err) {
+  pdl_wait();
   constexpr int kPer = 16;
   const uint64_t o0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * kPer;
   if (o0 >= out_len) return;
@@ -268,11 +274,11 @@ static void launch_packed(const uint8_t* packed, uint64_t n, uint32_t s, uint32_
   if (m == 0) return;
   if (s <= 2) {
     const uint64_t blocks = (m + kTokThreads * kTptSmallStride - 1) / (kTokThreads * kTptSmallStride);
-    k_skmer_packed<kTptSmallStride, TokT><<<unsigned(blocks), kTokThreads, 0, st>>>(packed, n, s, k,
+    launch_pdl(k_skmer_packed<kTptSmallStride, TokT>, dim3(unsigned(blocks)), dim3(kTokThreads), 0, st, packed, n, s, k,
                                                                                   tokens, m);
   } else {
     const uint64_t blocks = (m + kTokThreads * kTpt - 1) / (kTokThreads * kTpt);
-    k_skmer_packed<kTpt, TokT><<<unsigned(blocks), kTokThreads, 0, st>>>(packed, n, s, k, tokens, m);
+    launch_pdl(k_skmer_packed<kTpt, TokT>, dim3(unsigned(blocks)), dim3(kTokThreads), 0, st, packed, n, s, k, tokens, m);
   }
 }
 void launch_skmer_encode_packed(const uint8_t* packed, uint64_t n, uint32_t s, uint32_t k,
@@ -288,23 +294,23 @@ void launch_skmer_encode_ascii(const uint8_t* ascii, uint64_t n, uint32_t s, uin
                                uint32_t* tokens, uint64_t m, cudaStream_t st) {
   if (!m) return;
   const uint64_t blocks = (m + kTokThreads * kTpt - 1) / (kTokThreads * kTpt);
-  k_skmer_bytes<true, kTpt><<<unsigned(blocks), kTokThreads, 0, st>>>(ascii, n, s, k, tokens, m);
+  launch_pdl(k_skmer_bytes<true, kTpt>, dim3(unsigned(blocks)), dim3(kTokThreads), 0, st, ascii, n, s, k, tokens, m);
 }
 void launch_skmer_encode_codes(const uint8_t* codes, uint64_t n, uint32_t s, uint32_t k,
                                uint32_t* tokens, uint64_t m, cudaStream_t st) {
   if (!m) return;
   const uint64_t blocks = (m + kTokThreads * kTpt - 1) / (kTokThreads * kTpt);
-  k_skmer_bytes<false, kTpt><<<unsigned(blocks), kTokThreads, 0, st>>>(codes, n, s, k, tokens, m);
+  launch_pdl(k_skmer_bytes<false, kTpt>, dim3(unsigned(blocks)), dim3(kTokThreads), 0, st, codes, n, s, k, tokens, m);
 }
 uint32_t canon_blocks(uint64_t n) { return uint32_t((n + kCanonPerBlock - 1) / kCanonPerBlock); }
 void launch_canon_count(const uint8_t* raw, uint64_t n, uint32_t* counts, cudaStream_t st) {
   if (!n) return;
-  k_canon_count<<<canon_blocks(n), kCanonThreads, 0, st>>>(raw, n, counts);
+  launch_pdl(k_canon_count, dim3(canon_blocks(n)), dim3(kCanonThreads), 0, st, raw, n, counts);
 }
 void launch_canon_scatter(const uint8_t* raw, uint64_t n, const uint64_t* block_exc,
                           uint8_t* codes, uint64_t* exc_pos, uint8_t* exc_byte, cudaStream_t st) {
   if (!n) return;
-  k_canon_scatter<<<canon_blocks(n), kCanonThreads, 0, st>>>(raw, n, block_exc, codes, exc_pos,
+  launch_pdl(k_canon_scatter, dim3(canon_blocks(n)), dim3(kCanonThreads), 0, st, raw, n, block_exc, codes, exc_pos,
                                                              exc_byte);
 }
 void launch_detokenize_restore(const uint32_t* tokens, uint64_t m, uint32_t s, uint32_t k,
@@ -313,7 +319,7 @@ void launch_detokenize_restore(const uint32_t* tokens, uint64_t m, uint32_t s, u
                                uint64_t out_len, int* err, cudaStream_t st) {
   if (!out_len) return;
   const uint64_t threads = (out_len + 15) / 16;
-  k_detok_restore<<<unsigned((threads + 255) / 256), 256, 0, st>>>(
+  launch_pdl(k_detok_restore, dim3(unsigned((threads + 255) / 256)), dim3(256), 0, st, 
       tokens, m, s, k, residual, n_res, exc_pos, exc_byte, n_exc, out, out_len, err);
 }
 
