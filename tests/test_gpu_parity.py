@@ -235,6 +235,32 @@ def test_throughput_regime_matches_reference(P, checker, tmp_path, flags):
         assert got[i] == want, i
 
 
+@pytest.mark.parametrize("kw,n", [
+    (dict(t=8, bs=8, scale=1), 3000),                    # paper widths (E=64, H=256, F=4096)
+    (dict(t=8, bs=8, scale=2, workers=2, smp=0.3), 6000),
+    (dict(s=5, k=5, t=4, bs=16, scale=16), 40000),       # V=1024: general quantizer ranks
+    (dict(s=3, k=6, t=4, bs=16, scale=16, workers=2), 30000),  # V=4096
+])
+def test_containers_more_widths_and_vocabularies(P, checker, kw, n):
+    raw = P.synth("markov3", n, 97)
+    pkw = {("smp_fraction" if k == "smp" else k): v for k, v in kw.items()}
+    blob = P.compress(raw, P.CompressConfig(**pkw))
+    assert blob == checker.compress(raw, O.make_cfg(**kw))
+    assert P.decompress(blob) == raw
+
+
+def test_spum_paper_widths(P, checker, tmp_path):
+    # SPuM at scale 1 (Hs=128: the generic recurrence, no fused layer 1)
+    path = str(tmp_path / "spum_s1.bin")
+    P.write_bigru(path, 3, 8, 1, 0xBEEF, layers=2)
+    raw = P.synth("markov3", 2400, 98)
+    kw = dict(t=8, bs=8, scale=1)
+    blob = P.compress(raw, P.CompressConfig(pub_model_path=path, **kw))
+    assert blob[5] == 5
+    assert blob == checker.compress(raw, O.make_cfg(pub_path=path, **kw))
+    assert P.decompress(blob, path) == raw
+
+
 # ------------------------------------------------------------------ edge cases / errors
 def test_degenerate_inputs(P, checker):
     for raw in [b"", b"A", b"AC", b"ACG", b"NNNN", b"acgt", bytes(range(256)), b"ACGT" * 3]:
