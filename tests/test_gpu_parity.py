@@ -249,6 +249,20 @@ def test_containers_more_widths_and_vocabularies(P, checker, kw, n):
     assert P.decompress(blob) == raw
 
 
+def test_k8_invalid_distribution_like_reference(P, checker):
+    # k=8 (V=65,536): the reference's float32 softmax sum drifts past the
+    # quantizer's 1e-5 check and compress throws InvalidDistribution
+    # (SURVEY 8(a) a8); the exact GPU path must throw the same error.
+    raw = P.synth("markov3", 200000, 99)
+    kw = dict(s=8, k=8, t=4, bs=16, scale=16)
+    with pytest.raises(O.CheckerError) as want:
+        checker.compress(raw, O.make_cfg(**kw))
+    with pytest.raises(P.PmklcError) as got:
+        P.compress(raw, P.CompressConfig(**kw))
+    assert want.value.errc == "InvalidDistribution"
+    assert got.value.errc == want.value.errc
+
+
 def test_spum_paper_widths(P, checker, tmp_path):
     # SPuM at scale 1 (Hs=128: the generic recurrence, no fused layer 1)
     path = str(tmp_path / "spum_s1.bin")
