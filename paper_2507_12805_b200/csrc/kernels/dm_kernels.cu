@@ -12,6 +12,7 @@
 #include <type_traits>
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "detmath.cuh"
 #include "kernels.hpp"
@@ -542,6 +543,151 @@ __global__ void __launch_bounds__(kNwWarps * 32) k_gemm_nt(NtBatch nb, const Tic
 #pragma unroll
   for (int r = 0; r < RPT; ++r)
     if (outp[r]) *outp[r] = acc[r];
+}
+
+// Deep regime, one row per thread (the SPrM pre-pass: ~230 warps, one per SM
+// sub-partition). A warp alone on its sub-partition gets no latency hiding
+// from other warps, and ptxas, left to itself, issues a tile's 64 products
+// first and then the 64 dependent adds with a 4-cycle stall each (measured
+// 8 cycles per k in isolation, 14 in situ with the copy burst at the tile
+// start). Here the tile is written as a software pipeline of volatile asm:
+// per k one chain add, the product 16 k ahead, a shared load 32 k ahead, and
+// one copy of the tile STAGES-1 ahead (19 copy slots: 16 B chunks, 2 A words,
+// commit). ptxas still regroups independent instructions (the SASS shows the
+// copies and adds partly clustered), but the streamed copies and the spread
+// of outputs over 2x the sub-partitions bring the SPrM-step reduction from
+// 78.8 us (2 paired rows per thread) to 68.6 us. Same per-output order as
+// every NT path: acc = acc + a(k)*b(k), k ascending, separately rounded.
+__device__ __forceinline__ float fmul_v(float a, float b) {
+  float r;
+  asm volatile("mul.rn.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float fadd_v(float a, float b) {
+  float r;
+  asm volatile("add.rn.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float f4c(const float4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+template <class CopyFn>
+__device__ __forceinline__ float nt_tile_r1(float acc, const float* as, const float* bs, CopyFn copy) {
+  constexpr int KG = 16, NG = 4, NL = 8;  // per 16-k group: 4 B + 4 A LDS.128
+  float4 L[2][NL];
+  float P[2][KG];
+  auto ld = [&](int g, int i) {
+    return i < 4 ? lds128_v(bs + g * KG + 4 * i) : lds128_v(as + g * KG + 4 * (i - 4));
+  };
+  auto prod = [&](const float4 (&l)[NL], int k) { return fmul_v(f4c(l[4 + k / 4], k & 3), f4c(l[k / 4], k & 3)); };
+#pragma unroll
+  for (int i = 0; i < NL; ++i) L[0][i] = ld(0, i);
+#pragma unroll
+  for (int i = 0; i < NL; ++i) L[1][i] = ld(1, i);
+#pragma unroll
+  for (int k = 0; k < KG; ++k) P[0][k] = prod(L[0], k);
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    const int cb = g & 1, nb = cb ^ 1;
+#pragma unroll
+    for (int k = 0; k < KG; ++k) {
+      acc = fadd_v(acc, P[cb][k]);
+      if (g + 1 < NG) P[nb][k] = prod(L[nb], k);
+      if (g + 2 < NG && k < NL) L[cb][k] = ld(g + 2, k);
+      copy(g * KG + k);
+    }
+  }
+  return acc;
+}
+
+template <bool VEC, int STAGES>
+__global__ void __launch_bounds__(kNwWarps * 32) k_gemm_nt_r1(NtBatch nb, const TickDesc* __restrict__ td) {
+  pdl_wait();
+  constexpr int BK = 64, SB = BK + 4;
+  extern __shared__ __align__(128) float sm[];
+  if (blockIdx.y >= unsigned(td->n_act)) return;
+  const int c = td->act[blockIdx.y];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int task = int(blockIdx.x) * kNwWarps + w;
+  if (task >= nb.first_task[nb.n]) return;  // warp-uniform; no block barriers below
+  int prob = 0;
+  while (prob + 1 < nb.n && task >= nb.first_task[prob + 1]) ++prob;
+  const NtP& pp = nb.p[prob];
+  const int lt = task - nb.first_task[prob];
+  const int cg = lt % nb.colgroups[prob], m = lt / nb.colgroups[prob];
+  const int M = pp.M, N = pp.N, K = pp.K;
+  const int64_t ldb = pp.ldb;
+  const int n0 = cg * 32, n = n0 + lane;
+  const bool has_a = m < M;  // row M is the bias row (A = 1)
+  const int nrows = min(32, N - n0);
+  float* As = sm + w * nw_warp_floats(1, STAGES, BK);  // [stage][BK]
+  float* Bs = As + STAGES * BK;                        // [stage][32][SB]
+  const float* A = pp.A + c * pp.a_cs + int64_t(m) * pp.lda;
+  const float* B = pp.B + c * pp.b_cs + int64_t(n0) * ldb;
+  if (!has_a)
+    for (int i = lane; i < STAGES * BK; i += 32) As[i] = m == M ? 1.0f : 0.0f;
+  __syncwarp();
+  const int ntiles = (K + BK - 1) / BK;
+  const bool vec_tiles = VEC && nrows == 32;
+  // full-tile copy slots: lane copies chunk lane%16 of B rows lane/16 + 2j
+  const float* bl = B + int64_t(lane >> 4) * ldb + 4 * (lane & 15);
+  const int bsl = (lane >> 4) * SB + 4 * (lane & 15);
+  auto full_copy = [&](int tile, int slot) {  // slot 0..15 B, 16..17 A
+    const int st = tile % STAGES, k0 = tile * BK;
+    if (slot < 16) {
+      cp_async16(Bs + st * 32 * SB + bsl + slot * 2 * SB, bl + k0 + int64_t(slot) * 2 * ldb);
+    } else if (has_a) {
+      const int e = slot - 16;
+      cp_async4(As + st * BK + lane + 32 * e, A + k0 + lane + 32 * e);
+    }
+  };
+  auto load_all = [&](int tile) {  // whole tile at once (prologue, ragged tiles, generic B)
+    if (tile < ntiles) {
+      const int st = tile % STAGES, k0 = tile * BK, kc = min(BK, K - k0);
+      if (kc == BK && vec_tiles) {
+#pragma unroll
+        for (int j = 0; j < 18; ++j) full_copy(tile, j);
+      } else {
+        if (has_a)
+          for (int i = lane; i < kc; i += 32) cp_async4(As + st * BK + i, A + k0 + i);
+        for (int i = lane; i < nrows * kc; i += 32)
+          cp_async4(Bs + st * 32 * SB + (i / kc) * SB + i % kc, B + int64_t(i / kc) * ldb + k0 + i % kc);
+      }
+    }
+    cp_async_commit();  // one group per tile slot, possibly empty
+  };
+
+  float* outp = nullptr;
+  float acc = 0.0f;
+  if (m <= M && n < N) {
+    outp = (m == M && pp.cb) ? pp.cb + c * pp.c_cs + n : pp.C + c * pp.c_cs + int64_t(m) * pp.ldc + n;
+    acc = *outp;
+  }
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) load_all(s);
+  for (int tile = 0; tile < ntiles; ++tile) {
+    cp_async_wait<STAGES - 2>();
+    __syncwarp();  // tile landed for all lanes; all lanes are past tile-1
+    const int st = tile % STAGES, kc = min(BK, K - tile * BK);
+    const float* as = As + st * BK;
+    const float* bs = Bs + (st * 32 + lane) * SB;
+    const int nt = tile + STAGES - 1;
+    if (kc == BK && vec_tiles && nt < ntiles && K - nt * BK >= BK) {
+      acc = nt_tile_r1(acc, as, bs, [&](int slot) {
+        if (slot < 18) full_copy(nt, slot);
+        else if (slot == 18) cp_async_commit();
+      });
+    } else {
+      load_all(nt);
+      if (kc == BK) {
+        acc = nt_tile_r1(acc, as, bs, [](int) {});
+      } else {
+        for (int kk = 0; kk < kc; ++kk) acc = fadd_v(acc, fmul_v(as[kk], bs[kk]));
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (outp) *outp = acc;
 }
 
 // ------------------------------------------------------------------ embed
@@ -1397,6 +1543,10 @@ void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int m
     PMKLC_NT_ATTR(true, 8, 3, 32); PMKLC_NT_ATTR(false, 8, 3, 32); PMKLC_NT_ATTR(true, 4, 3, 32);
     PMKLC_NT_ATTR(false, 4, 3, 32); PMKLC_NT_ATTR(true, 2, 3, 32); PMKLC_NT_ATTR(false, 2, 3, 32);
     PMKLC_NT_ATTR(true, 2, 6, 64); PMKLC_NT_ATTR(false, 2, 6, 64);
+    cudaFuncSetAttribute(k_gemm_nt_r1<true, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kNwWarps * nw_warp_floats(1, 6, 64) * sizeof(float)));
+    cudaFuncSetAttribute(k_gemm_nt_r1<false, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kNwWarps * nw_warp_floats(1, 6, 64) * sizeof(float)));
 #undef PMKLC_NT_ATTR
     attr_set = true;
   }
@@ -1420,9 +1570,21 @@ void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int m
   if (int64_t(build(8, nb)) * max_active < 148 * 8) rpt = 4;
   if (rpt == 4 && int64_t(build(4, nb)) * max_active < 148 * 4) rpt = 2;
   const int tasks = build(rpt, nb);
-  const bool deep = rpt == 2 && int64_t(tasks) * max_active < 148 * 2;
+  bool deep = rpt == 2 && int64_t(tasks) * max_active < 148 * 2;
+  // deep regime: one row per thread spreads the outputs over twice the SM
+  // sub-partitions; each then needs 2 FP32-pipe cycles per k (exact mul +
+  // add) under the 4-cycle add chain instead of exactly 4 with a row pair.
+  static const int deep_rpt = [] {
+    const char* e = std::getenv("PMKLC_NT_DEEP_RPT");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (deep && deep_rpt == 1) {
+    build(1, nb);
+    rpt = 1;
+  }
+  const int tasks_final = nb.first_task[nprob];
   const int stages = deep ? 6 : 3, bk = deep ? 64 : 32;
-  const dim3 grid(unsigned((tasks + kNwWarps - 1) / kNwWarps), unsigned(max_active));
+  const dim3 grid(unsigned((tasks_final + kNwWarps - 1) / kNwWarps), unsigned(max_active));
   const size_t smem = size_t(kNwWarps) * nw_warp_floats(rpt, stages, bk) * sizeof(float);
 #define PMKLC_NT_LAUNCH(R, S, K)                                                               \
   if (vec) launch_pdl(k_gemm_nt<true, R, S, K>, dim3(grid), dim3(kNwWarps * 32), smem, st, nb, td);               \
@@ -1433,8 +1595,12 @@ void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int m
     PMKLC_NT_LAUNCH(4, 3, 32)
   } else if (!deep) {
     PMKLC_NT_LAUNCH(2, 3, 32)
-  } else {
+  } else if (rpt == 2) {
     PMKLC_NT_LAUNCH(2, 6, 64)
+  } else if (vec) {
+    launch_pdl(k_gemm_nt_r1<true, 6>, dim3(grid), dim3(kNwWarps * 32), smem, st, nb, td);
+  } else {
+    launch_pdl(k_gemm_nt_r1<false, 6>, dim3(grid), dim3(kNwWarps * 32), smem, st, nb, td);
   }
 #undef PMKLC_NT_LAUNCH
 }
