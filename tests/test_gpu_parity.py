@@ -362,6 +362,24 @@ def test_sprm_prepass_branch(P, checker, spum_k3, with_pub):
     assert checker.decompress(blob, pub_path=spum_k3 if with_pub else None) == raw
 
 
+@pytest.mark.parametrize("kw", [
+    dict(t=32, bs=99),             # K = 3168: 49 full 64-k tiles + a ragged one, 16-byte B rows
+    dict(t=8, bs=50, scale=16),    # K = 400, N < 32: the generic copy path of the NT reduction
+])
+def test_sprm_prepass_ragged_k(P, checker, kw):
+    # the pre-pass weight-gradient reductions run K = bs*t long chains in the
+    # deep (one row per thread) NT kernel; a K that is not a multiple of its
+    # 64-k tile exercises the ragged last tile and the end of the copy stream
+    raw = P.synth("markov3", 60000, 63)
+    full = dict(kw, workers=2, threshold=0)
+    ckw = dict(full)
+    thr = ckw.pop("threshold")
+    blob = P.compress(raw, P.CompressConfig(**_cfgs(ckw), selector_threshold=thr))
+    assert blob[5] == 6
+    assert blob == checker.compress(raw, O.make_cfg(**full))
+    assert P.decompress(blob) == raw
+
+
 def test_sprm_prepass_default_widths(P, checker):
     # scale 4, t = 32, bs = 320: the widths of BASELINE configs 4/5
     raw = P.synth("markov3", 150000, 62)
