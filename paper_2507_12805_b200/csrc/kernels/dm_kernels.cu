@@ -673,9 +673,21 @@ __global__ void __launch_bounds__(kNwWarps * 32) k_gemm_nt_r1(NtBatch nb, const 
     const float* bs = Bs + (st * 32 + lane) * SB;
     const int nt = tile + STAGES - 1;
     if (kc == BK && vec_tiles && nt < ntiles && K - nt * BK >= BK) {
+      // streamed copies of tile nt: one running B pointer (rows lane/16 + 2j)
+      // and immediate shared offsets, so a copy costs one 64-bit add
+      const int sn = nt % STAGES;
+      const float* bsrc = bl + int64_t(nt) * BK;
+      float* bdst = Bs + sn * 32 * SB + bsl;
+      const int64_t bstep = 2 * ldb;
       acc = nt_tile_r1(acc, as, bs, [&](int slot) {
-        if (slot < 18) full_copy(nt, slot);
-        else if (slot == 18) cp_async_commit();
+        if (slot < 16) {
+          cp_async16(bdst + slot * 2 * SB, bsrc);
+          bsrc += bstep;
+        } else if (slot < 18) {
+          if (has_a) cp_async4(As + sn * BK + lane + 32 * (slot - 16), A + int64_t(nt) * BK + lane + 32 * (slot - 16));
+        } else if (slot == 18) {
+          cp_async_commit();
+        }
       });
     } else {
       load_all(nt);
