@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -74,13 +75,35 @@ struct DBuf {
   }
 };
 
+// Stream priorities: the engine stream and its fork/join branches (the DM
+// chain of a tick, the coder) get the device's greatest priority; the next
+// tick's static predictions, which only have to finish within the tick, the
+// least, so the block scheduler hands freed SM slots to the critical chain
+// first. PMKLC_PRIO=0 keeps every stream at the default priority.
+static int prio_mode() {
+  static const int m = [] {
+    const char* e = std::getenv("PMKLC_PRIO");
+    return e ? std::atoi(e) : 1;
+  }();
+  return m;
+}
+// level 2: highest, 1: middle, 0: least
+static int stream_prio(int level) {
+  if (prio_mode() == 0) return 0;
+  int least = 0, greatest = 0;
+  if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) return 0;
+  if (level >= 2) return greatest;
+  if (level == 1) return prio_mode() == 2 ? (least + greatest) / 2 : greatest;
+  return least;
+}
+
 struct Stream {
   cudaStream_t s = nullptr;
   cudaStream_t prev = nullptr;
   explicit Stream(int device) {
     CK(cudaSetDevice(device));
     configure_pool(device);
-    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, stream_prio(2)));
     prev = g_alloc_stream;
     g_alloc_stream = s;
   }
@@ -99,7 +122,9 @@ struct SideStream {
   cudaStream_t s = nullptr;
   std::vector<cudaEvent_t> evs;
   size_t next = 0;
-  SideStream() { CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  explicit SideStream(int level = 2) {
+    CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, stream_prio(level)));
+  }
   ~SideStream() {
     if (s) {
       cudaStreamSynchronize(s);
@@ -491,7 +516,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   // weight-gradient product as soon as its operands exist, beside the
   // data-gradient chain; `pred` (below) the mixing-weight step and the next
   // tick's static predictions; `cod` (below) the encoder's range coder.
-  SideStream side;
+  SideStream side(1);  // weight gradients: joined before Adam
   auto to_side = [&]() { side.wait_for(st); };
   auto from_side = [&]() { side.join_into(st); };
   // Cross-tick pipeline of the static predictors: their input is only the
@@ -501,7 +526,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   // straight into lu/lr (tau's mixer and trainer have consumed them by then).
   // A prologue computes tick 0's before the first tick.
   const bool statics = (run.flags & 3) != 0;
-  SideStream pred;
+  SideStream pred(0);  // next tick's predictions: lowest priority
   SideStream cod;  // the encoder's range coder and the mixing-weight step, beside the trainer
   DBuf<TickDesc> d_td_next(1);
   DBuf<uint32_t> ctx_next;

@@ -30,6 +30,19 @@ struct PdlScope {  // registers `s` as the PDL stream for the scope
   ~PdlScope() { pdl_stream() = prev; }
 };
 
+// cached cudaStreamGetPriority (launches repeat on a handful of streams)
+inline int stream_priority(cudaStream_t st) {
+  thread_local cudaStream_t last = nullptr;
+  thread_local int prio = 0;
+  if (st != last || st == nullptr) {
+    int p = 0;
+    if (st != nullptr && cudaStreamGetPriority(st, &p) != cudaSuccess) p = 0;
+    last = st;
+    prio = p;
+  }
+  return prio;
+}
+
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        Args&&... args) {
@@ -38,11 +51,21 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (st != nullptr && st == pdl_stream()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  // the stream's scheduling priority, stamped on the launch so that it also
+  // holds inside captured graphs (the DM chain of a tick outranks the next
+  // tick's static predictions running beside it)
+  attr[na].id = cudaLaunchAttributePriority;
+  attr[na].val.priority = stream_priority(st);
+  ++na;
   cfg.attrs = attr;
-  cfg.numAttrs = (st != nullptr && st == pdl_stream()) ? 1 : 0;
+  cfg.numAttrs = na;
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
