@@ -50,8 +50,11 @@ template <bool AT, bool BT, int TM, int TN, int BK, int STAGES, int TX, int TY>
 __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc* __restrict__ td) {
   pdl_wait();
   constexpr int NT = TX * TY, BM = TY * TM, BN = TX * TN;
-  __shared__ __align__(16) float As[STAGES][BK][BM + 4];
-  __shared__ __align__(16) float Bs[STAGES][BK][BN + 4];
+  // dynamic shared memory: the ring is [STAGES][BK][BM+4] A then [STAGES][BK][BN+4] B
+  // (3+ stages of the 64x64 tile exceed the 48 KB static limit)
+  extern __shared__ __align__(16) float g_sm[];
+  auto As = reinterpret_cast<float (*)[BK][BM + 4]>(g_sm);
+  auto Bs = reinterpret_cast<float (*)[BK][BN + 4]>(g_sm + STAGES * BK * (BM + 4));
   const int np = p.nprob > 1 ? p.nprob : 1;
   const int slot = blockIdx.z / np, prob = blockIdx.z % np;
   if (slot >= td->n_act) return;
@@ -64,6 +67,13 @@ __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc*
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int ntiles = (p.K + BK - 1) / BK;
+  // Output column of a thread's j-th accumulator. TN = 8 splits the thread's
+  // columns into two groups of 4 interleaved across the block (group g at
+  // g*TX*4 + tx*4), so each LDS.128 of a B row covers a contiguous 128 B per
+  // 8 lanes (one wavefront); TN <= 4 keeps the thread's columns contiguous.
+  auto col = [&](int j) {
+    return TN % 4 == 0 ? n0 + (j / 4) * (TX * 4) + tx * 4 + j % 4 : n0 + tx * TN + j;
+  };
 
   // 16-byte copies where the global side runs along the smem row (A^T: m,
   // B: n) and is 16-byte aligned (chunk slots of the parameter array are only
@@ -136,7 +146,7 @@ __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc*
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
-      const int m = m0 + ty * TM + i, n = n0 + tx * TN + j;
+      const int m = m0 + ty * TM + i, n = col(j);
       float v = 0.0f;
       if (m < Mx && n < p.N) {
         if (p.init == 1) v = bias[n];
@@ -164,7 +174,7 @@ __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc*
       // each thread's TM (TN) operands are contiguous: one vector shared load each
       float a[TM], b[TN];
       const float* ap = &As[stage][kk][ty * TM];
-      const float* bp = &Bs[stage][kk][tx * TN];
+      const float* bp = &Bs[stage][kk][TN % 4 == 0 ? tx * 4 : tx * TN];
       if constexpr (TM == 4) {
         const float4 v = *reinterpret_cast<const float4*>(ap);
         a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w;
@@ -175,9 +185,12 @@ __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc*
 #pragma unroll
         for (int i = 0; i < TM; ++i) a[i] = ap[i];
       }
-      if constexpr (TN == 4) {
-        const float4 v = *reinterpret_cast<const float4*>(bp);
-        b[0] = v.x; b[1] = v.y; b[2] = v.z; b[3] = v.w;
+      if constexpr (TN % 4 == 0) {
+#pragma unroll
+        for (int g = 0; g < TN / 4; ++g) {
+          const float4 v = *reinterpret_cast<const float4*>(bp + g * TX * 4);
+          b[4 * g] = v.x; b[4 * g + 1] = v.y; b[4 * g + 2] = v.z; b[4 * g + 3] = v.w;
+        }
       } else if constexpr (TN == 2) {
         const float2 v = *reinterpret_cast<const float2*>(bp);
         b[0] = v.x; b[1] = v.y;
@@ -225,15 +238,17 @@ __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc*
       }
   }
 
-  if constexpr (TN == 4) {  // 16-byte stores of a thread's 4 columns when possible
-    const int n = n0 + tx * TN;
-    if (!p.mask && p.ldc % 4 == 0 && al16(C) && n + 3 < p.N) {
+  if constexpr (TN % 4 == 0) {  // 16-byte stores of each group of 4 columns when possible
+    if (!p.mask && p.ldc % 4 == 0 && al16(C) && col(TN - 1) < p.N) {
 #pragma unroll
       for (int i = 0; i < TM; ++i) {
         const int m = m0 + ty * TM + i;
-        if (m < Mx)
-          *reinterpret_cast<float4*>(C + int64_t(m) * p.ldc + n) =
-              make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        if (m < Mx) {
+#pragma unroll
+          for (int g = 0; g < TN / 4; ++g)
+            *reinterpret_cast<float4*>(C + int64_t(m) * p.ldc + col(4 * g)) =
+                make_float4(acc[i][4 * g], acc[i][4 * g + 1], acc[i][4 * g + 2], acc[i][4 * g + 3]);
+        }
       }
       return;
     }
@@ -242,7 +257,7 @@ __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc*
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
-      const int m = m0 + ty * TM + i, n = n0 + tx * TN + j;
+      const int m = m0 + ty * TM + i, n = col(j);
       if (m < Mx && n < p.N) {
         float v = acc[i][j];
         if (p.mask && p.mask[c * p.mask_cs + int64_t(m) * p.ldm + n] <= 0.0f) v = 0.0f;
@@ -251,12 +266,36 @@ __global__ void __launch_bounds__(TX * TY) k_gemm_tiled(GemmP p, const TickDesc*
     }
 }
 
+// The 64x64 tile of the throughput regime: 4x8 outputs per thread (128 threads,
+// interleaved column groups) through a 3-deep ring of 32-k tiles. Measured
+// against 4x4 x 256 threads with 2-4 stages and BK 16-64 by
+// tools/x2/gemm_variants.py: -2.2% model time on a 20 MB SPuM+DM compress,
+// identical container (the ring depth and tile shape change no reduction order).
+#ifndef PMKLC_G44_STAGES
+#define PMKLC_G44_STAGES 3
+#endif
+#ifndef PMKLC_G44_BK
+#define PMKLC_G44_BK 32
+#endif
+#ifndef PMKLC_G44_WIDE
+#define PMKLC_G44_WIDE 1
+#endif
+
 template <bool AT, bool BT, int TM, int TN, int BK, int STAGES, int TX = 16, int TY = 16>
 void gemm_launch(const GemmP& p, const TickDesc* td, int max_active, cudaStream_t st) {
   const int Mx = p.M + (p.ones_row ? 1 : 0);
   const int np = p.nprob > 1 ? p.nprob : 1;
   dim3 grid((p.N + TX * TN - 1) / (TX * TN), (Mx + TY * TM - 1) / (TY * TM), max_active * np);
-  launch_pdl(k_gemm_tiled<AT, BT, TM, TN, BK, STAGES, TX, TY>, dim3(grid), dim3(TX * TY), 0, st, p, td);
+  constexpr int smem = STAGES * BK * (TY * TM + 4 + TX * TN + 4) * int(sizeof(float));
+  auto* kern = k_gemm_tiled<AT, BT, TM, TN, BK, STAGES, TX, TY>;
+  if constexpr (smem > 48 * 1024) {
+    static bool attr = false;  // per instantiation, as for the other opt-in kernels
+    if (!attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+  }
+  launch_pdl(kern, dim3(grid), dim3(TX * TY), smem, st, p, td);
 }
 
 template <bool AT, bool BT>
@@ -271,7 +310,11 @@ void gemm_dispatch(const GemmP& p, const TickDesc* td, int max_active, cudaStrea
   // dependent chains spread over as many SMs as possible.
   constexpr int64_t kFill = 2 * 148;
   if (blocks(64, 64) >= kFill && p.N >= 48 && Mx >= 48)
-    gemm_launch<AT, BT, 4, 4, 32, 2>(p, td, max_active, st);
+#if PMKLC_G44_WIDE
+    gemm_launch<AT, BT, 4, 8, PMKLC_G44_BK, PMKLC_G44_STAGES, 8, 16>(p, td, max_active, st);
+#else
+    gemm_launch<AT, BT, 4, 4, PMKLC_G44_BK, PMKLC_G44_STAGES>(p, td, max_active, st);
+#endif
   else if (blocks(64, 16) >= kFill && p.N <= 16 && Mx >= 48)
     gemm_launch<AT, BT, 4, 1, 32, 2>(p, td, max_active, st);
   else if (blocks(64, 32) >= kFill && p.N <= 32 && Mx >= 48)
