@@ -1462,18 +1462,38 @@ __global__ void k_adam(float* __restrict__ w, float* __restrict__ g, float* __re
   const float b1 = 0.9f, b2 = 0.999f, lr = 5e-4f, eps = 1e-8f;
   const float omb1 = fsub(1.0f, b1), omb2 = fsub(1.0f, b2);
   const int64_t base = c * p_cs;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t o = base + i;
-    const float gi = g[o];
-    const float mi = fadd(fmul(b1, m[o]), fmul(omb1, gi));
-    const float vi = fadd(fmul(b2, v[o]), fmul(fmul(omb2, gi), gi));
-    const float mhat = fdiv(mi, bc1);
-    const float vhat = fdiv(vi, bc2);
-    w[o] = fsub(w[o], fdiv(fmul(lr, mhat), fadd(__fsqrt_rn(vhat), eps)));
-    m[o] = mi;
-    v[o] = vi;
-    g[o] = 0.0f;
+  // U elements per thread per round, all loads issued before the math: the
+  // update is latency-bound on its HBM reads, not on the IEEE divides
+  constexpr int U = 4;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    float gi[U], mo[U], vo[U], wo[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n) {
+        const int64_t o = base + i;
+        gi[u] = g[o];
+        mo[u] = m[o];
+        vo[u] = v[o];
+        wo[u] = w[o];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n) {
+        const int64_t o = base + i;
+        const float mi = fadd(fmul(b1, mo[u]), fmul(omb1, gi[u]));
+        const float vi = fadd(fmul(b2, vo[u]), fmul(fmul(omb2, gi[u]), gi[u]));
+        const float mhat = fdiv(mi, bc1);
+        const float vhat = fdiv(vi, bc2);
+        w[o] = fsub(wo[u], fdiv(fmul(lr, mhat), fadd(__fsqrt_rn(vhat), eps)));
+        m[o] = mi;
+        v[o] = vi;
+        g[o] = 0.0f;
+      }
+    }
   }
 }
 
