@@ -346,7 +346,17 @@ void gemm_dispatch(const GemmP& p, const TickDesc* td, int max_active, cudaStrea
 // column; A is staged interleaved [k][row] so one broadcast LDS.128 yields row
 // pairs for the paired FP32 chains; B is read once per RPT rows. Row M of a
 // problem is the bias row (A == 1, so 1*b == b exactly: the plain sum).
-constexpr int kNwWarps = 2;
+#ifndef PMKLC_NW_WARPS
+#define PMKLC_NW_WARPS 2
+#endif
+constexpr int kNwWarps = PMKLC_NW_WARPS;  // independent warps per NT block (no block barriers)
+// ring depth and k-tile of the throughput-regime (8 rows per thread) NT launch
+#ifndef PMKLC_NT8_S
+#define PMKLC_NT8_S 3
+#endif
+#ifndef PMKLC_NT8_BK
+#define PMKLC_NT8_BK 32
+#endif
 // padded B row (BK + 4 floats): LDS.128 of 32 rows is conflict-free
 __host__ __device__ constexpr int nw_warp_floats(int rpt, int stages, int bk) {
   return stages * (rpt * bk + 32 * (bk + 4));
@@ -1615,7 +1625,7 @@ void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int m
 #define PMKLC_NT_ATTR(V, R, S, K) \
   cudaFuncSetAttribute(k_gemm_nt<V, R, S, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                        int(kNwWarps * nw_warp_floats(R, S, K) * sizeof(float)))
-    PMKLC_NT_ATTR(true, 8, 3, 32); PMKLC_NT_ATTR(false, 8, 3, 32); PMKLC_NT_ATTR(true, 4, 3, 32);
+    PMKLC_NT_ATTR(true, 8, PMKLC_NT8_S, PMKLC_NT8_BK); PMKLC_NT_ATTR(false, 8, PMKLC_NT8_S, PMKLC_NT8_BK); PMKLC_NT_ATTR(true, 4, 3, 32);
     PMKLC_NT_ATTR(false, 4, 3, 32); PMKLC_NT_ATTR(true, 2, 3, 32); PMKLC_NT_ATTR(false, 2, 3, 32);
     PMKLC_NT_ATTR(true, 2, 6, 64); PMKLC_NT_ATTR(false, 2, 6, 64);
     cudaFuncSetAttribute(k_gemm_nt_r1<true, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1658,14 +1668,14 @@ void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int m
     rpt = 1;
   }
   const int tasks_final = nb.first_task[nprob];
-  const int stages = deep ? 6 : 3, bk = deep ? 64 : 32;
+  const int stages = deep ? 6 : rpt == 8 ? PMKLC_NT8_S : 3, bk = deep ? 64 : rpt == 8 ? PMKLC_NT8_BK : 32;
   const dim3 grid(unsigned((tasks_final + kNwWarps - 1) / kNwWarps), unsigned(max_active));
   const size_t smem = size_t(kNwWarps) * nw_warp_floats(rpt, stages, bk) * sizeof(float);
 #define PMKLC_NT_LAUNCH(R, S, K)                                                               \
   if (vec) launch_pdl(k_gemm_nt<true, R, S, K>, dim3(grid), dim3(kNwWarps * 32), smem, st, nb, td);               \
   else launch_pdl(k_gemm_nt<false, R, S, K>, dim3(grid), dim3(kNwWarps * 32), smem, st, nb, td);
   if (rpt == 8) {
-    PMKLC_NT_LAUNCH(8, 3, 32)
+    PMKLC_NT_LAUNCH(8, PMKLC_NT8_S, PMKLC_NT8_BK)
   } else if (rpt == 4) {
     PMKLC_NT_LAUNCH(4, 3, 32)
   } else if (!deep) {
