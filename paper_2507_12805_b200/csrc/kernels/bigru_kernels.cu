@@ -150,10 +150,14 @@ __device__ __forceinline__ void rec_cp_async4(float* smem, const float* gmem) {
 // No xi buffer round trip through HBM; `out` may be null (last layer: only
 // the final state is consumed).
 constexpr int kFuseHs = 32, kFuseIn = 64;
+#ifndef PMKLC_FUSE_WARPS
+#define PMKLC_FUSE_WARPS 8
+#endif
+constexpr int kFuseWarps = PMKLC_FUSE_WARPS;  // warps (row groups) per fused block
 constexpr size_t kFuseSmem =
     sizeof(float) * (size_t(3) * kFuseHs * kFuseHs + size_t(3) * kFuseIn * kFuseHs +
-                     size_t(kRecWarps) * 2 * 32 * kRPW + size_t(kRecWarps) * 2 * kFuseIn * kRPW);
-__global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec_fused(
+                     size_t(kFuseWarps) * 2 * 32 * kRPW + size_t(kFuseWarps) * 2 * kFuseIn * kRPW);
+__global__ void __launch_bounds__(kFuseWarps * 32) k_bigru_rec_fused(
     BiGruP p, int l, const float* __restrict__ in, float* out, float* fin, int64_t work_cs,
     const TickDesc* __restrict__ td) {
   pdl_wait();
@@ -164,12 +168,12 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec_fused(
   float (*sh)[2][32][kRPW] =
       reinterpret_cast<float (*)[2][32][kRPW]>(fsm + 3 * HS * HS + 3 * IN * HS);     // [w][cur][q][u]
   float (*sin)[2][IN][kRPW] = reinterpret_cast<float (*)[2][IN][kRPW]>(
-      fsm + 3 * HS * HS + 3 * IN * HS + kRecWarps * 2 * 32 * kRPW);                 // [w][buf][k][u]
+      fsm + 3 * HS * HS + 3 * IN * HS + kFuseWarps * 2 * 32 * kRPW);                 // [w][buf][k][u]
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int dir = blockIdx.x & 1;
-  const int grp = (blockIdx.x >> 1) * kRecWarps + wl;
+  const int grp = (blockIdx.x >> 1) * kFuseWarps + wl;
   const int T = p.T;
   const float* W = p.w;
   for (int i = threadIdx.x; i < 3 * HS * HS; i += blockDim.x) {
@@ -403,7 +407,8 @@ int launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, f
         launch_hot_begin(hot, st);
         ++launches;
       }
-      launch_pdl(k_bigru_rec_fused, dim3(rgrid2), dim3(kRecWarps * 32), kFuseSmem, st, 
+      const dim3 fgrid(unsigned(2 * ((ngroups + kFuseWarps - 1) / kFuseWarps)), max_active);
+      launch_pdl(k_bigru_rec_fused, fgrid, dim3(kFuseWarps * 32), kFuseSmem, st, 
           p, l, outs[(l - 1) & 1], last ? nullptr : outs[l & 1], f, work_cs, td);
       ++launches;
       if (hot) {
