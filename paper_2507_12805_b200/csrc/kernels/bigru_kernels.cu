@@ -22,7 +22,10 @@ namespace pmklc_b200 {
 namespace {
 
 enum { WIR, WIZ, WIN, WHR, WHZ, WHN, BIR, BIZ, BIN, BHR, BHZ, BHN, NG };
-constexpr int kRecWarps = 8;
+#ifndef PMKLC_REC_WARPS
+#define PMKLC_REC_WARPS 4
+#endif
+constexpr int kRecWarps = PMKLC_REC_WARPS;
 
 __device__ __forceinline__ int64_t poff(const int64_t* offs, int l, int dir, int t) {
   return offs[1 + (l * 2 + dir) * NG + t];
