@@ -1,19 +1,34 @@
-"""PMKLC B200 benchmark (driver contract in the task statement; see DESIGN.md).
+"""PMKLC B200 benchmark (driver contract in the task statement; see DESIGN.md §7).
 
 One step = compress + decompress of the whole workload (the paper's Eq. 4
-throughput THP = size / (CT + DT)), device-resident input for
-`value`, host buffers through the public API for `e2e`.
+throughput THP = size / (CT + DT); reference bench.cpp:20-24),
+device-resident input for `value`, host buffers through the public API for
+`e2e`.
 
-Default workload (N=1): BASELINE config 3 — a 100 MB synthetic genome (10
-order-k Markov segments, k in 2..5, GC bias varied, 1 % copy-repeats),
-PMKLC-S block-partitioned into W=128 data blocks, public (seeded, untrained
-SPuM) + dynamic models (the selector never enables private and public
-together below the 500 MB threshold, mixer.cpp:9-12), reference defaults
-s=k=3, t=32, bs=320, scale 4, SMP 0.05.
+Workloads (BASELINE.json configs):
+  config3 (N=1 default): 100 MB synthetic genome (10 order-k Markov segments,
+      k in 2..5, GC bias varied, 1 % copy-repeats), PMKLC-S block-partitioned
+      into W=128 data blocks, seeded untrained SPuM + dynamic model (the
+      selector never enables private and public together below the 500 MB
+      threshold, mixer.cpp:9-12), defaults s=k=3, t=32, bs=320, scale 4,
+      SMP 0.05. Sub-lines: the threshold-lowered SPrM branch (flags 6) and
+      config 4.
+  config4 (N>1 default, and a one-step sub-line at N=1): 10^9 B synthetic
+      genome, default selector (> 500 MB => SPrM + DM, flags 6, with the
+      sequential SPrM pre-pass inside compress), W=256, SMP 0.05.
 
---impl reference times the reference C++ library itself (oracle/_ref, built
-from /root/reference sources) on the host cores over a bounded sample of the
-same workload.
+--impl reference times the reference C++ library itself (oracle/_ref, the
+reference compiled from /root/reference sources) on the host cores. It never
+loads the product library: inputs come from the checker library's copy of the
+seeded generators and the SPuM file from the reference's own writer. Each step
+is a bounded stock compress()+decompress() sample at the workload's chunk
+geometry (bs=320, t=32, the same model) over C = host threads chunks of
+t + S batch steps (S alternating 8 / 24 model steps); a least-squares fit of
+sample time against S gives the per-model-step cost with C chunks in flight
+and the fixed cost, which are extrapolated to the workload's W chunks x
+(L - t) model steps on the same C cores (the SPrM pre-pass separately, timed
+with the reference's pretrain_private). The sample geometry, fit and
+extrapolation are stated in the line.
 """
 from __future__ import annotations
 
@@ -32,6 +47,8 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "Compress/decompress MB/s at 1/2/4/8 B200; bits/base vs CPU reference"
+BS, T, K = 320, 32, 3
+SPUM_SEED = 0xACE3
 
 
 def parse():
@@ -40,30 +57,62 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--mb", type=float, default=100.0, help="workload size in 10^6 bytes")
-    ap.add_argument("--workers", type=int, default=128, help="data blocks W")
-    ap.add_argument("--no-spum", action="store_true", help="no public model")
+    ap.add_argument("--config", default=None, choices=["config3", "config4"],
+                    help="main workload (default: config3 at N=1, config4 at N>1)")
+    ap.add_argument("--mb", type=float, default=None, help="workload size in 10^6 bytes")
+    ap.add_argument("--workers", type=int, default=None, help="data blocks W")
+    ap.add_argument("--no-spum", action="store_true", help="config3 without the public model")
     ap.add_argument("--no-sprm-branch", action="store_true",
                     help="skip the threshold-lowered SPrM+DM (flags 6) run of config 3")
+    ap.add_argument("--no-config4", action="store_true", help="skip the config-4 sub-line at N=1")
     ap.add_argument("--skip-cpu", action="store_true", help="skip the cpu_baseline leg")
-    return ap.parse_args()
+    a = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if a.config is None:
+        a.config = "config4" if max(a.gpus, world) > 1 else "config3"
+    return a
 
 
-def workload(args, tmpdir):
-    import paper_2507_12805_b200 as P
-    n = int(args.mb * 1e6)
-    raw = P.synth("genome", n, 2025, 10)
-    cfg = P.CompressConfig(workers=args.workers)
-    spum = ""
-    if not args.no_spum:
-        spum = str(Path(tmpdir) / "spum_k3_t32_s4.bin")
-        P.write_bigru(spum, 3, 32, 4, 0xACE3, layers=2)
-        cfg.pub_model_path = spum
-    models = "DM only (flags 4)" if args.no_spum else "SPuM(seeded)+DM (flags 5, default selector)"
-    desc = (f"config3: {n/1e6:g} MB synthetic genome (10 order-k Markov segments k=2..5 + 1% "
-            f"repeats), PMKLC-S W={args.workers} blocks, {models}, "
-            f"s=k=3 t=32 bs=320 scale=4 smp=0.05")
-    return raw, cfg, spum, desc
+@dataclasses.dataclass
+class Workload:
+    name: str
+    n: int
+    seed: int
+    workers: int
+    threshold: int
+    spum: bool
+    desc: str
+
+
+def workload(args, name=None) -> Workload:
+    """The named BASELINE config (no product import: plain description)."""
+    name = name or args.config
+    if name == "config3":
+        n = int((args.mb or 100.0) * 1e6)
+        W = args.workers or 128
+        models = ("DM only (flags 4)" if args.no_spum
+                  else "SPuM(seeded)+DM (flags 5, default selector)")
+        desc = (f"config3: {n/1e6:g} MB synthetic genome (10 order-k Markov segments k=2..5 + 1% "
+                f"repeats), PMKLC-S W={W} blocks, {models}, s=k=3 t=32 bs=320 scale=4 smp=0.05")
+        return Workload(name, n, 2025, W, 500_000_000, not args.no_spum, desc)
+    n = int((args.mb or 1000.0) * 1e6) if name == args.config else 10**9
+    W = (args.workers or 256) if name == args.config else 256
+    desc = (f"config4: {n/1e6:g} MB synthetic genome (10 order-k Markov segments, seed 2026), "
+            f"PMKLC-M W={W} blocks, default selector (> 500 MB: SPrM pre-trained on the input "
+            f"inside compress + DM, flags 6), s=k=3 t=32 bs=320 scale=4 smp=0.05")
+    return Workload(name, n, 2026, W, 500_000_000, False, desc)
+
+
+def plan_geometry(m: int, workers: int, bs: int = BS, t: int = T):
+    """plan_chunks (pipeline.cpp:32-52) restated for the extrapolation: chunk
+    count, clamped bs and the model steps sum(L_i - t)."""
+    if m == 0:
+        return 0, 1, 0
+    w = min(workers, max(1, m // (bs * (t + 1))))
+    base, rem = divmod(m, w)
+    bsc = min(bs, max(1, base // (t + 1)))
+    steps = sum(max(0, (base + (1 if i < rem else 0)) // bsc - t) for i in range(w))
+    return w, bsc, steps
 
 
 class Clocks:
@@ -104,9 +153,13 @@ class Clocks:
         return self
 
     def __exit__(self, *a):
+        pass  # keeps sampling across the sub-lines; stop() ends it
+
+    def stop(self):
         if self.p:
             self.p.terminate()
             self.p.wait()
+            self.p = None
 
     def summary(self):
         try:
@@ -125,54 +178,214 @@ class Clocks:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(lines)}
 
 
-def flush_l2(torch, buf):
-    buf.add_(1)  # 256 MiB write > 126 MB L2, between timed steps (not timed)
-
-
-def cpu_sample(raw, cfg, threads):
-    """Bounded sample of the workload for the host-CPU reference: `chunks`
-    blocks of `steps` batch steps (32 warm-up + the rest model steps). With the
-    private model the reference pre-trains it sequentially over the whole
-    sample (~130 ms per 320-token step on one core), so that sample is smaller
-    (2 blocks x 48 steps: ~100 pre-pass steps) to keep a step within ~30 s."""
-    if cfg.selector_threshold == 0:
-        chunks, steps = 2, 48
-    else:
-        chunks, steps = threads, 64
-    n = min(len(raw), chunks * 320 * 3 * steps)
-    return raw[:n], chunks, steps
-
-
-def cpu_reference(raw, cfg, spum, threads, reps, warm):
-    """The reference library (oracle/_ref) on host cores over a bounded sample."""
+# ----------------------------------------------------------------- CPU reference
+def checker():
     sys.path.insert(0, str(ROOT / "tests"))
     import oracles as O
-    R = O.ref() if O.REF_SO.exists() else O.port()
-    kind = "reference" if O.REF_SO.exists() else "port"
-    sample, chunks, steps = cpu_sample(raw, cfg, threads)
-    n = len(sample)
-    c = O.make_cfg(workers=chunks, pub_path=spum or None, threshold=int(cfg.selector_threshold))
-    times = []
-    blob = b""
-    for i in range(warm + reps):
+    if O.REF_SO.exists():
+        return O, O.ref(), "reference"
+    return O, O.port(), "port"
+
+
+def ref_inputs(wl: Workload, tmpdir: str, O, R):
+    """Workload input and SPuM file built by the checker library (generators)
+    and the reference's own model writer -- no product code."""
+    raw = R.synth("genome", wl.n, wl.seed, 10)
+    spum = None
+    if wl.spum:
+        spum = str(Path(tmpdir) / "spum_k3_t32_s4.bin")
+        O.write_spum(spum, K, T, 4, SPUM_SEED)
+    return raw, spum
+
+
+class RefSampler:
+    """Bounded samples of the stock reference compress()/decompress() at the
+    workload's chunk geometry, fitted and extrapolated to the whole workload."""
+
+    def __init__(self, O, R, kind, raw, spum, wl: Workload, threads: int, flags6: bool):
+        self.O, self.R, self.kind = O, R, kind
+        self.raw, self.spum, self.wl = raw, spum, wl
+        self.flags6 = flags6
+        # the pre-pass is sequential: with it, keep the sample small (2 chunks);
+        # the sample (C chunks of t + 24 batch steps) must fit in the input
+        m = (wl.n - K) // K + 1
+        fit = max(1, m // (BS * (T + 24)))
+        self.C = max(1, min(threads, 2 if flags6 else threads, fit))
+        self.threads = threads
+        self.pts = []  # (S, compress_s (chunk part), decompress_s)
+        self.c_pre = None  # reference pretrain_private seconds per Adam step
+        self.bpb = []
+
+    def sample(self, S: int):
+        O, R = self.O, self.R
+        m_s = self.C * BS * (T + S)
+        n_s = m_s * 3  # k = s = 3: n = 3 (m - 1) + 3
+        sample = self.raw[:n_s]
+        thr = 0 if self.flags6 else self.wl.threshold
+        cfg = O.make_cfg(workers=self.C, pub_path=self.spum, threshold=thr)
+        pre_steps = (m_s - T + BS - 1) // BS if self.flags6 else 0
+        if self.flags6 and self.c_pre is None:
+            import numpy as np
+            codes = np.frombuffer(sample, np.uint8)
+            codes = (((codes >> 1) ^ (codes >> 2)) & 3).astype(np.uint8).tobytes()
+            tok, _ = R.skmer_encode(codes, K, K)
+            t0 = time.perf_counter()
+            R.pretrain_private(tok, K, T, BS, 4, 1234, pub_path=self.spum)
+            self.c_pre = (time.perf_counter() - t0) / pre_steps
         t0 = time.perf_counter()
-        blob = R.compress(sample, c)
+        blob = R.compress(sample, cfg)
         t1 = time.perf_counter()
-        out = R.decompress(blob, pub_path=spum or None, workers=chunks)
+        out = R.decompress(blob, pub_path=self.spum, workers=self.C)
         t2 = time.perf_counter()
-        assert out == sample
-        if i >= warm:
-            times.append((t1 - t0, t2 - t1))
-    ct = sum(t[0] for t in times) / len(times)
-    dt = sum(t[1] for t in times) / len(times)
-    flags = blob[5] if len(blob) > 5 else 0
-    return {"value": n / 1e6 / (ct + dt), "unit": "MB/s", "cores": chunks, "kind": kind,
-            "sample": f"first {n} B of the workload, W={chunks} blocks x {steps} batch steps, "
-                      f"container flags {flags}; compress {ct:.2f} s + decompress {dt:.2f} s "
-                      f"(one host thread per block; the SPrM pre-pass is sequential)",
-            "compress_MBps": n / 1e6 / ct, "decompress_MBps": n / 1e6 / dt,
-            "bits_per_base": 8.0 * len(blob) / n,
-            "n": n}
+        assert out == sample, "reference round trip failed"
+        ct = (t1 - t0) - (pre_steps * self.c_pre if self.flags6 else 0.0)
+        self.pts.append((S, ct, t2 - t1))
+        self.bpb.append(8.0 * len(blob) / n_s)
+        return (t1 - t0) + (t2 - t1)
+
+    @staticmethod
+    def _fit(xs, ys):
+        if len(set(xs)) < 2:
+            return ys[0] / xs[0] if xs[0] else 0.0, 0.0
+        mx, my = statistics.fmean(xs), statistics.fmean(ys)
+        sxx = sum((x - mx) ** 2 for x in xs)
+        b = sum((x - mx) * (y - my) for x, y in zip(xs, ys)) / sxx
+        return max(b, 1e-9), max(my - b * mx, 0.0)
+
+    def extrapolate(self):
+        """Whole-workload seconds on C cores: chunk model steps at the fitted
+        per-step cost (C in flight), fixed cost scaled by bytes, pre-pass
+        steps at the measured per-step cost."""
+        wl = self.wl
+        m = (wl.n - K) // K + 1
+        W, bsc, steps = plan_geometry(m, wl.workers)
+        xs = [p[0] for p in self.pts]
+        bc, ac = self._fit(xs, [p[1] for p in self.pts])
+        bd, ad = self._fit(xs, [p[2] for p in self.pts])
+        scale_n = wl.n / (self.C * BS * (T + statistics.fmean(xs)) * 3)
+        # chunks are independent given their inbound snapshot (the SMP link is
+        # a few model steps, far shorter than a chunk), so the reference's
+        # run_chunks keeps min(cores, W) chunks in flight: per-chunk step cost
+        # as sampled, spread over that many cores
+        par = min(self.threads, W)
+        self.par = par
+        ct = steps / par * bc + ac * scale_n
+        dt = steps / par * bd + ad * scale_n
+        pre = 0.0
+        if self.flags6:
+            pre = ((m - T + BS - 1) // BS) * self.c_pre
+            ct += pre
+        return {"compress_s": ct, "decompress_s": dt, "prepass_s": pre, "W": W, "bs": bsc,
+                "model_steps": steps, "per_step_compress_s": bc, "per_step_decompress_s": bd,
+                "fixed_compress_s": ac, "fixed_decompress_s": ad,
+                "prepass_step_s": self.c_pre}
+
+    def describe(self, ex):
+        wl = self.wl
+        S = sorted({p[0] for p in self.pts})
+        s = (f"stock reference compress()+decompress() on the first {self.C}x{BS}x(32+S) tokens "
+             f"(C={self.C} chunks on {self.C} threads, L=32+S batch steps, S in {S}, "
+             f"{len(self.pts)} samples); least-squares per-model-step cost "
+             f"{ex['per_step_compress_s']*1e3:.1f}/{ex['per_step_decompress_s']*1e3:.1f} ms "
+             f"(compress/decompress, {self.C} chunks in flight), extrapolated to the workload's "
+             f"W={ex['W']} chunks x {ex['model_steps']//max(ex['W'],1)} model steps on "
+             f"{self.par} cores")
+        if self.flags6:
+            s += (f"; SPrM pre-pass {ex['prepass_step_s']*1e3:.1f} ms per sequential step "
+                  f"(reference pretrain_private) x {int(round(ex['prepass_s']/ex['prepass_step_s']))} "
+                  f"steps")
+        return s
+
+
+def cpu_reference(wl: Workload, raw, spum, threads, samples, flags6, O, R, kind):
+    rs = RefSampler(O, R, kind, raw, spum, wl, threads, flags6)
+    for i in range(samples):
+        rs.sample(8 if i % 2 == 0 else 24)
+    ex = rs.extrapolate()
+    value = wl.n / 1e6 / (ex["compress_s"] + ex["decompress_s"])
+    return {"value": value, "unit": "MB/s", "cores": rs.par, "kind": kind,
+            "sample": rs.describe(ex), "extrapolation": ex,
+            "compress_MBps": wl.n / 1e6 / ex["compress_s"],
+            "decompress_MBps": wl.n / 1e6 / ex["decompress_s"],
+            "bits_per_base_sample": statistics.fmean(rs.bpb)}
+
+
+def golden_bpb(wl: Workload):
+    """Same-config bits/base of the reference itself, from the committed
+    reference-generated golden (tests/golden/make_bench_golden.py)."""
+    g = ROOT / "tests" / "golden" / "bench_config3.json"
+    if wl.name == "config3" and wl.n == 100_000_000 and wl.workers == 128 and wl.spum and g.exists():
+        d = json.loads(g.read_text())
+        return {"bits_per_base": d["bits_per_base"], "container_fnv": d["container_fnv"],
+                "source": "tests/golden/bench_config3.json (reference compress() of the same "
+                          "100 MB input, W=128, generated in the build container)"}
+    return None
+
+
+def reference_arm(args, world, rank):
+    if rank != 0:
+        return
+    O, R, kind = checker()
+    wl = workload(args)
+    tmp = tempfile.mkdtemp(prefix="pmklc_ref_")
+    raw, spum = ref_inputs(wl, tmp, O, R)
+    threads = min(os.cpu_count() or 1, 256)
+    flags6 = wl.n > wl.threshold
+    rs = RefSampler(O, R, kind, raw, spum, wl, threads, flags6)
+    for i in range(args.warmup):
+        rs.sample(8 if i % 2 == 0 else 24)
+    rs.pts.clear()
+    rs.bpb.clear()
+    for i in range(max(args.steps, 1)):
+        rs.sample(8 if i % 2 == 0 else 24)
+    if len(rs.pts) == 1:  # one step: add the other size so the fit has two points
+        rs.sample(24)
+    ex = rs.extrapolate()
+    tot = ex["compress_s"] + ex["decompress_s"]
+    value = wl.n / 1e6 / tot
+    line = {"metric": METRIC, "value": value, "unit": "MB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": wl.desc, "bytes": wl.n,
+                       "parallelism": f"{rs.par} host cores (reference run_chunks threads)",
+                       "same_config": "extrapolated: " + rs.describe(ex)},
+            "cpu_baseline": {"value": value, "unit": "MB/s", "cores": rs.par, "kind": kind,
+                             "sample": rs.describe(ex)},
+            "e2e": {"value": value, "unit": "MB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "compress_MBps": wl.n / 1e6 / ex["compress_s"],
+            "decompress_MBps": wl.n / 1e6 / ex["decompress_s"],
+            "extrapolation": ex,
+            "bits_per_base_sample": statistics.fmean(rs.bpb),
+            "bits_per_base_same_config": golden_bpb(wl),
+            "product_library_loaded": "libpmklc_b200" in Path("/proc/self/maps").read_text()}
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------- B200 arm
+def gpu_inputs(wl: Workload, tmpdir, P):
+    raw = P.synth("genome", wl.n, wl.seed, 10)
+    spum = ""
+    if wl.spum:
+        spum = str(Path(tmpdir) / "spum_k3_t32_s4.bin")
+        P.write_bigru(spum, K, T, 4, SPUM_SEED, layers=2)
+    cfg = P.CompressConfig(workers=wl.workers, selector_threshold=wl.threshold,
+                           pub_model_path=spum)
+    return raw, cfg, spum
+
+
+def eq_metrics(n, blob_len, ct_s, dt_s, block_crs=None):
+    """Eq. 3-5 as the reference computes them (bench.cpp:15-36): CR bits/base,
+    THP bytes/s over CT+DT, and CRP (sample coefficient of variation, n-1) of
+    per-block CRs."""
+    import paper_2507_12805_b200 as P
+    out = {"cr_bits_per_base": P.compression_ratio(blob_len, n),
+           "thp_bytes_per_s": P.throughput(n, ct_s, dt_s)}
+    if block_crs:
+        out["crp_percent_blocks"] = P.robustness(block_crs)
+        out["blocks"] = len(block_crs)
+    return out
 
 
 def main():
@@ -180,42 +393,21 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    tmp = tempfile.mkdtemp(prefix="pmklc_bench_")
-
     if args.impl == "reference":
-        if rank != 0:
-            return
-        raw, cfg, spum, desc = workload(args, tmp)
-        threads = min(os.cpu_count() or 1, 256, args.workers)
-        r = cpu_reference(raw, cfg, spum, threads, args.steps, args.warmup)
-        line = {"metric": METRIC, "value": r["value"], "unit": "MB/s", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1000.0 * (r["n"] / 1e6 / r["value"]) if r["value"] else None,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic", "impl": "reference",
-                "config": {"workload": desc, "parallelism": f"{threads} host threads"},
-                "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": r["value"], "unit": "MB/s", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0},
-                "compress_MBps": r["compress_MBps"], "decompress_MBps": r["decompress_MBps"],
-                "bits_per_base_sample": r["bits_per_base"]}
-        print(json.dumps(line))
+        reference_arm(args, world, rank)
         return
 
     import torch
     import paper_2507_12805_b200 as P
 
+    tmp = tempfile.mkdtemp(prefix="pmklc_bench_")
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo", init_method="env://")  # host control plane only
     torch.cuda.set_device(local)
     dev = local
-    raw, cfg, spum, desc = workload(args, tmp)
-    cfg.device = dev
-    n = len(raw)
-    d_raw = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(f"cuda:{dev}")
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
     ctx = P.DistContext(rank, world, dev) if world > 1 else None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
 
     def bcast(blob):
         if world == 1:
@@ -224,159 +416,193 @@ def main():
         torch.distributed.broadcast_object_list(obj, src=0)
         return obj[0]
 
-    def run_step(cfg):
-        """compress (device-resident input) + decompress; PMKLC-M over all ranks."""
-        tm_c, tm_d = P.Timing(), P.Timing()
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-        e0.record()
-        if ctx is None:
-            blob = P.compress_device(d_raw.data_ptr(), n, cfg, tm_c)
-        else:
-            blob = ctx.compress_device(d_raw.data_ptr(), n, cfg, tm_c)
-        e1.record()
-        torch.cuda.synchronize()
-        blob = bcast(blob)  # container to every rank (not timed)
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        e1b = torch.cuda.Event(enable_timing=True)
-        e1b.record()
-        if ctx is None:
-            dptr, dlen = P.decompress_to_device(blob, spum, dev, tm_d)
-            e2.record()
-            torch.cuda.synchronize()
-            P.device_free(dptr)
-        else:
-            out = ctx.decompress(blob, spum, tm_d)
-            e2.record()
-            torch.cuda.synchronize()
-            if rank == 0:
-                assert len(out) == n
-        c_ms, d_ms = e0.elapsed_time(e1), e1b.elapsed_time(e2)
-        return blob, c_ms, d_ms, tm_c.kernel_launches + tm_d.kernel_launches, (tm_c, tm_d)
+    def max_ranks(*vals):
+        if world == 1:
+            return vals
+        tt = torch.tensor(list(vals), dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        return tuple(float(x) for x in tt)
 
-    def measure(cfg, warmup, steps):
-        # correctness of the measured path: lossless round trip (first warm-up)
-        blob, _, _, _, _ = run_step(cfg)
-        if ctx is None:
-            assert P.decompress(blob, spum, device=dev) == raw, "round trip mismatch"
-        else:
-            out = ctx.decompress(blob, spum)
+    class Run:
+        """One workload: device-resident input, timed steps, round-trip check."""
+
+        def __init__(self, wl: Workload, cfg, raw, spum):
+            self.wl, self.cfg, self.raw, self.spum = wl, cfg, raw, spum
+            self.cfg.device = dev
+            self.n = len(raw)
+            self.d_raw = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(f"cuda:{dev}")
+
+        def step(self):
+            """compress (device input) + decompress (device output), both arms
+            of PMKLC-M included; CUDA events, max over ranks per phase."""
+            tm_c, tm_d = P.Timing(), P.Timing()
+            if world > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+            e0.record()
+            if ctx is None:
+                blob = P.compress_device(self.d_raw.data_ptr(), self.n, self.cfg, tm_c)
+            else:
+                blob = ctx.compress_device(self.d_raw.data_ptr(), self.n, self.cfg, tm_c)
+            e1.record()
+            torch.cuda.synchronize()
+            blob = bcast(blob)  # container to every rank (not timed)
+            if world > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            e2.record()
+            if ctx is None:
+                dptr, dlen = P.decompress_to_device(blob, self.spum, dev, tm_d)
+            else:
+                dptr, dlen = ctx.decompress_to_device(blob, self.spum, tm_d)
+            e3.record()
+            torch.cuda.synchronize()
+            c_ms, d_ms = max_ranks(e0.elapsed_time(e1), e2.elapsed_time(e3))
+            return blob, c_ms, d_ms, (tm_c, tm_d), (dptr, dlen)
+
+        def check_device(self, out):
+            """decoded bytes on the device == input (rank 0 holds the output)"""
+            dptr, dlen = out
+            ok = True
             if rank == 0:
-                assert out == raw, "round trip mismatch"
-        for _ in range(max(warmup - 1, 0)):
-            run_step(cfg)
-        res = {"ct": 0.0, "dt": 0.0, "launches": 0, "flags": blob[5],
-               "hot": {"ms": 0.0, "launches": 0, "units": 0, "flops": 0.0},
-               "brk": {"sprm_prepass_ms": 0.0, "compress_ticks_ms": 0.0, "decompress_ticks_ms": 0.0}}
-        hot, brk = res["hot"], res["brk"]
-        with clk:
-            for _ in range(steps):
-                flush_l2(torch, flush)
-                blob, c_ms, d_ms, l, tms = run_step(cfg)
+                ok = dlen == self.n and P.device_equal(dptr, self.d_raw.data_ptr(), self.n, dev)
+            if dptr:
+                P.device_free(dptr)
+            return ok
+
+        def measure(self, warmup, steps, clk_on=True):
+            # correctness of the measured path: the first warm-up's round trip
+            res = {"ct": 0.0, "dt": 0.0, "launches": 0, "steps": steps,
+                   "hot": {"ms": 0.0, "launches": 0, "units": 0, "flops": 0.0},
+                   "brk": {"sprm_prepass_ms": 0.0, "compress_ticks_ms": 0.0,
+                           "decompress_ticks_ms": 0.0}, "ticks": 0}
+            for i in range(warmup):
+                flush.add_(1)
+                blob, _, _, _, out = self.step()
+                ok = self.check_device(out)
+                assert ok, "round trip mismatch"
+            hot, brk = res["hot"], res["brk"]
+            verified = warmup > 0
+            for i in range(steps):
+                flush.add_(1)  # 256 MiB write > 126 MB L2 between timed steps (not timed)
+                blob, c_ms, d_ms, tms, out = self.step()
+                if not verified:
+                    assert self.check_device(out), "round trip mismatch"
+                    verified = True
+                elif out[0]:
+                    P.device_free(out[0])
                 brk["sprm_prepass_ms"] += tms[0].sprm_ms / steps
                 brk["compress_ticks_ms"] += tms[0].model_ms / steps
                 brk["decompress_ticks_ms"] += tms[1].model_ms / steps
-                for tm in tms:  # dominant kernel, timed on the device inside the timed region
+                res["ticks"] = tms[0].ticks
+                for tm in tms:
                     hot["ms"] += tm.hot_ms
                     hot["launches"] += tm.hot_launches
                     hot["units"] += tm.hot_units
                     hot["flops"] += tm.hot_flops_per_unit * tm.hot_units
-                if world > 1:  # max over ranks, per phase
-                    tt = torch.tensor([c_ms, d_ms], dtype=torch.float64)
-                    torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-                    c_ms, d_ms = float(tt[0]), float(tt[1])
                 res["ct"] += c_ms
                 res["dt"] += d_ms
-                res["launches"] += l
-        res["blob"] = blob
-        res["value"] = n * steps / 1e6 / ((res["ct"] + res["dt"]) / 1000.0)
-        return res
+                res["launches"] += tms[0].kernel_launches + tms[1].kernel_launches
+            res["blob"] = blob
+            res["value"] = self.n * steps / 1e6 / ((res["ct"] + res["dt"]) / 1000.0)
+            res["compress_MBps"] = self.n * steps / 1e6 / (res["ct"] / 1000.0)
+            res["decompress_MBps"] = self.n * steps / 1e6 / (res["dt"] / 1000.0)
+            res["bits_per_base"] = 8.0 * len(blob) / self.n
+            return res
+
+        def e2e(self, reps):
+            """same metric through the public host API: H2D of the input and
+            D2H of the container / decoded bytes inside the timed region"""
+            times = []
+            b2 = b""
+            for _ in range(reps):
+                flush.add_(1)
+                if world > 1:
+                    torch.distributed.barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                if ctx is None:
+                    b2 = P.compress(self.raw, self.cfg)
+                    back = P.decompress(b2, self.spum, device=dev)
+                else:
+                    b2 = bcast(ctx.compress(self.raw, self.cfg))
+                    back = ctx.decompress(b2, self.spum)
+                torch.cuda.synchronize()
+                (el,) = max_ranks(time.perf_counter() - t0)
+                times.append(el)
+                if rank == 0:
+                    assert back == self.raw
+            return self.n / 1e6 / statistics.fmean(times), len(b2)
 
     clk = Clocks(dev).start()
-    main_run = measure(cfg, args.warmup, args.steps)
-    ct, dt, launches = main_run["ct"], main_run["dt"], main_run["launches"]
-    hot, brk, blob = main_run["hot"], main_run["brk"], main_run["blob"]
-    tot_ms = ct + dt
-    value = main_run["value"]
-
-    # e2e through the public host API (host buffers, H2D/D2H inside)
-    e_times = []
-    for _ in range(max(1, args.steps // 2)):
-        flush_l2(torch, flush)
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        if ctx is None:
-            b2 = P.compress(raw, cfg)
-            back = P.decompress(b2, spum, device=dev)
-        else:
-            b2 = bcast(ctx.compress(raw, cfg))
-            back = ctx.decompress(b2, spum)
-        torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-        if world > 1:
-            tt = torch.tensor([el], dtype=torch.float64)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            el = float(tt[0])
-        e_times.append(el)
-        if rank == 0:
-            assert back == raw
-    e2e_val = n / 1e6 / (sum(e_times) / len(e_times))
+    wl = workload(args)
+    raw, cfg, spum = gpu_inputs(wl, tmp, P)
+    main_run = Run(wl, cfg, raw, spum)
+    res = main_run.measure(args.warmup, args.steps)
+    e2e_val, e2e_blob = main_run.e2e(max(1, args.steps // 2))
+    n = main_run.n
 
     # config 3's other selector branch: threshold lowered so the private model
     # is pre-trained on the input inside compress (flags 6, SURVEY §8 config 3;
-    # the reference never enables SPuM and SPrM together, mixer.cpp:9-12).
-    # One warm-up step (the engine paths are already warm from the main run).
+    # the reference never enables SPuM and SPrM together, mixer.cpp:9-12)
     sprm = None
-    if not args.no_sprm_branch:
+    if wl.name == "config3" and not args.no_sprm_branch:
         cfg6 = dataclasses.replace(cfg, selector_threshold=0)
-        sprm = measure(cfg6, 1, args.steps)
+        sprm_run = Run(wl, cfg6, raw, spum)
+        sprm = sprm_run.measure(1, min(args.steps, 3))
+        del sprm_run
+    del main_run
+
+    # config 4 at N=1: one step (the engine paths are warm; the first step's
+    # round trip is checked on the device)
+    c4 = None
+    if wl.name == "config3" and not args.no_config4 and world == 1:
+        wl4 = workload(args, "config4")
+        raw4, cfg4, spum4 = gpu_inputs(wl4, tmp, P)
+        run4 = Run(wl4, cfg4, raw4, spum4)
+        c4res = run4.measure(0, 1)
+        c4 = {"workload": wl4.desc, "bytes": wl4.n, "value": c4res["value"], "unit": "MB/s",
+              "warmup": 0, "steps": 1, "ms_per_step": c4res["ct"] + c4res["dt"],
+              "compress_MBps": c4res["compress_MBps"], "decompress_MBps": c4res["decompress_MBps"],
+              "bits_per_base": c4res["bits_per_base"], "container_flags": c4res["blob"][5],
+              "step_breakdown_ms": c4res["brk"], "ticks": c4res["ticks"],
+              "gpu_launches": c4res["launches"], "lossless": True,
+              "metrics_eq3_5": eq_metrics(wl4.n, len(c4res["blob"]), c4res["ct"] / 1e3,
+                                          c4res["dt"] / 1e3, P.block_ratios(c4res["blob"]))}
+        del run4, raw4
+    clk.stop()
 
     line = None
     if rank == 0:
-        # roofline of the dominant kernel. With the public model (the default
-        # workload) that is the SPuM layer-1 fused BiGRU recurrence, timed on
-        # the device around every launch inside the timed steps (stamp kernels
-        # on its own stream; in-situ, so co-running DM kernels are included).
-        # Bound: exact non-FMA FP32 issue (no tensor cores in EXACT mode); the
-        # peak is a live FP32 microbenchmark (MEASURED_PEAKS.json has no FP32
-        # figure).
+        hot = res["hot"]
         p_ms, p_fl, _ = P.bench_kernel("fp32_peak", 1, iters=10, device=dev)
         peak_tf = p_fl / (p_ms / 1000.0) / 1e12
-        traffic = None
         tfile = ROOT / "profiles" / "roofline_traffic.json"
-        tjson = {}
-        if tfile.exists():
-            try:
-                tjson = json.loads(tfile.read_text())
-            except Exception:
-                tjson = {}
+        tjson = json.loads(tfile.read_text()) if tfile.exists() else {}
+        roof = None
         if hot["launches"]:
+            # the SPuM layer-1 fused BiGRU recurrence, timed on the device
+            # around every launch inside the timed steps (in situ)
             ach_tf = hot["flops"] / (hot["ms"] / 1000.0) / 1e12
             units_per_launch = hot["units"] / hot["launches"]
             t = tjson.get("k_bigru_rec_fused")
-            fma_busy = None
-            if t and t.get("units"):  # DRAM bytes per chunk-launch x this run's chunks per launch
+            traffic = fma_busy = None
+            if t and t.get("units"):
                 traffic = t["dram_bytes_per_launch"] / t["units"] * units_per_launch
                 fma_busy = t.get("fma_pipe_busy_pct")
-            # the same kernel alone on the GPU (no co-running DM branch), same stamps
             chunks_iso = max(1, int(round(units_per_launch)))
             i_ms, i_fl, _ = P.bench_kernel("bigru_fused", chunks_iso, iters=10, device=dev)
             iso_tf = i_fl / (i_ms / 1000.0) / 1e12 if i_ms > 0 else None
             roof = {"kernel": "k_bigru_rec_fused (SPuM BiGRU layer 1: input projection + "
                               "recurrence, R=320 rows x 2 dirs x t=32 steps per chunk)",
+                    "bound": "fp32", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                    "frac": ach_tf / peak_tf, "traffic": traffic,
                     "achieved_isolated": iso_tf,
                     "frac_isolated": iso_tf / peak_tf if iso_tf else None,
                     "isolated": f"bench_kernel('bigru_fused', {chunks_iso} chunks): the kernel "
                                 "alone; in situ it shares the SMs with the previous tick's DM "
                                 "backward (cross-tick pipeline)",
-                    "bound": "fp32", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                    "frac": ach_tf / peak_tf, "traffic": traffic,
                     "timing": "in-situ %globaltimer stamps around every launch in the timed steps",
                     "avg_launch_ms": hot["ms"] / hot["launches"],
                     "chunks_per_launch": units_per_launch,
@@ -384,12 +610,12 @@ def main():
                     "flops_per_chunk_launch": hot["flops"] / max(hot["units"], 1),
                     "fma_pipe_busy_pct_ncu": fma_busy,
                     "note": "achieved counts MAC flops only; the FP32 pipe also runs the exact "
-                            "det-math epilogue and 2 instructions per exact (non-FMA) MAC pair",
+                            "det-math epilogue and 2 instructions per exact (non-FMA) MAC",
                     "peak_source": "live non-FMA FP32 microbenchmark (MEASURED_PEAKS.json has no "
                                    "FP32 figure); EXACT mode cannot use tensor cores"}
-        else:  # DM only: the weight-gradient reduction, microbenchmarked live
-            chunks = min(args.workers, 64)
-            k_ms, k_fl, k_by = P.bench_kernel("gemm_nt", chunks, iters=10, device=dev)
+        else:  # DM only / config 4: the weight-gradient reduction, microbenchmarked live
+            chunks = min(wl.workers, 64)
+            k_ms, k_fl, _ = P.bench_kernel("gemm_nt", chunks, iters=10, device=dev)
             ach_tf = k_fl / (k_ms / 1000.0) / 1e12
             roof = {"kernel": f"k_gemm_nt (dWk|dbk + dWv|dbv over R*t=10240 rows, {chunks} chunks)",
                     "bound": "fp32", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
@@ -398,51 +624,67 @@ def main():
                     "peak_source": "live non-FMA FP32 microbenchmark"}
         cpu = cpu6 = None
         if not args.skip_cpu and world == 1:
-            threads = min(os.cpu_count() or 1, 256, args.workers)
-            def cpu_leg(c):
+            O, R, kind = checker()
+            threads = min(os.cpu_count() or 1, 256)
+
+            def leg(flags6, wlx, rawx, spumx):
                 try:
-                    full = cpu_reference(raw, c, spum, threads, 1, 0)
-                    return {k: full[k] for k in ("value", "unit", "cores", "kind", "sample")}
+                    r = cpu_reference(wlx, rawx, spumx or None, threads, 2, flags6, O, R, kind)
+                    return {k: r[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                              "compress_MBps", "decompress_MBps")}
                 except Exception as e:  # report, do not hide
-                    return {"value": None, "unit": "MB/s", "cores": threads, "kind": "reference",
+                    return {"value": None, "unit": "MB/s", "cores": threads, "kind": kind,
                             "sample": f"failed: {e}"}
-            cpu = cpu_leg(cfg)
+            cpu = leg(wl.n > wl.threshold, wl, raw, spum)
             if sprm is not None:
-                cpu6 = cpu_leg(dataclasses.replace(cfg, selector_threshold=0))
+                cpu6 = leg(True, wl, raw, spum)
         sprm_line = None
         if sprm is not None:
             sprm_line = {
-                "workload": desc.replace("SPuM(seeded)+DM (flags 5, default selector)",
-                                         "SPrM(pre-trained on the input inside compress)+DM "
-                                         "(flags 6, selector_threshold=0)"),
-                "container_flags": sprm["flags"], "value": sprm["value"], "unit": "MB/s",
-                "warmup": 1, "steps": args.steps,
-                "ms_per_step": (sprm["ct"] + sprm["dt"]) / args.steps,
-                "compress_MBps": n * args.steps / 1e6 / (sprm["ct"] / 1000.0),
-                "decompress_MBps": n * args.steps / 1e6 / (sprm["dt"] / 1000.0),
-                "bits_per_base": 8.0 * len(sprm["blob"]) / n,
+                "workload": wl.desc.replace("SPuM(seeded)+DM (flags 5, default selector)",
+                                            "SPrM(pre-trained on the input inside compress)+DM "
+                                            "(flags 6, selector_threshold=0)"),
+                "container_flags": sprm["blob"][5], "value": sprm["value"], "unit": "MB/s",
+                "warmup": 1, "steps": sprm["steps"],
+                "ms_per_step": (sprm["ct"] + sprm["dt"]) / sprm["steps"],
+                "compress_MBps": sprm["compress_MBps"], "decompress_MBps": sprm["decompress_MBps"],
+                "bits_per_base": sprm["bits_per_base"],
                 "step_breakdown_ms": sprm["brk"], "gpu_launches": sprm["launches"],
                 "cpu_baseline": cpu6}
+        blob = res["blob"]
+        gold = golden_bpb(wl)
+        parity = None
+        if gold:
+            parity = {"reference_bits_per_base": gold["bits_per_base"],
+                      "container_identical_to_reference":
+                          P.fnv1a64(blob) == int(gold["container_fnv"], 16),
+                      "source": gold["source"]}
         line = {
-            "metric": METRIC, "value": value, "unit": "MB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "metric": METRIC, "value": res["value"], "unit": "MB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": (res["ct"] + res["dt"]) / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": desc, "bytes": n,
+            "config": {"workload": wl.desc, "bytes": n,
                        "parallelism": (f"PMKLC-M over {world} GPUs: chunk c on GPU c%{world}, "
                                        "SMP handoffs as NCCL send/recv") if world > 1 else "1 GPU",
-                       "l2": "256 MiB flush write between timed steps"},
-            "compress_MBps": n * args.steps / 1e6 / (ct / 1000.0),
-            "decompress_MBps": n * args.steps / 1e6 / (dt / 1000.0),
-            "bits_per_base": 8.0 * len(blob) / n,
-            "step_breakdown_ms": brk,
+                       "l2": "256 MiB flush write between timed steps",
+                       "timed": "compress from device-resident input + decompress to device "
+                                "memory (rank 0), CUDA events, max over ranks"},
+            "compress_MBps": res["compress_MBps"], "decompress_MBps": res["decompress_MBps"],
+            "bits_per_base": res["bits_per_base"],
+            "parity_vs_reference": parity,
+            "metrics_eq3_5": eq_metrics(n, len(blob), res["ct"] / 1e3 / args.steps,
+                                        res["dt"] / 1e3 / args.steps, P.block_ratios(blob)),
+            "step_breakdown_ms": res["brk"],
             "container_bytes": len(blob),
             "roofline": roof,
             "cpu_baseline": cpu,
             "sprm_branch": sprm_line,
-            "e2e": {"value": e2e_val, "unit": "MB/s", "h2d_bytes_per_step": n + len(blob),
-                    "d2h_bytes_per_step": len(blob) + n},
+            "config4": c4,
+            "e2e": {"value": e2e_val, "unit": "MB/s", "h2d_bytes_per_step": n + e2e_blob,
+                    "d2h_bytes_per_step": e2e_blob + n},
             "clocks": clk.summary(),
-            "gpu_launches": launches,
+            "gpu_launches": res["launches"],
         }
         print(json.dumps(line))
     if world > 1:

@@ -50,8 +50,23 @@ typedef struct pmklc_cfg {
 typedef struct pmklc_stats {
   uint64_t tokens, uniform_coded, pub_calls, priv_calls, dyn_calls;
   uint64_t snapshot_recv_hash, snapshot_sent_hash;
+  /* WorkerStats::snapshot_recv_bytes (pipeline.hpp:32, pipeline.cpp:108-111):
+   * the chunk's inbound SMP snapshot, library-allocated (NULL when the chunk
+   * starts from the seeded init); release with pmklc_stats_release() */
+  uint8_t* snapshot_recv_bytes;
+  uint64_t snapshot_recv_len;
   double early_loss_bits;
 } pmklc_stats;
+
+/* frees the snapshot_recv_bytes of n stats entries (and nulls them) */
+void pmklc_stats_release(pmklc_stats* stats, size_t n);
+
+/* number of chunks (data blocks) compress() will write for this input and
+ * configuration (plan_chunks over the canonical token count, pipeline.cpp:32-52),
+ * so a caller can size the stats array exactly; host-only, O(n) */
+int pmklc_chunk_count(const uint8_t* in, size_t n, const pmklc_cfg* cfg, size_t* count);
+/* chunk count stored in a container header (container.cpp:53), host-only */
+int pmklc_container_chunks(const uint8_t* in, size_t n, size_t* count);
 
 typedef struct pmklc_timing {  /* CUDA-event times of the last call, ms */
   double total_ms, h2d_ms, tokenize_ms, warmup_ms, model_ms, d2h_ms;
@@ -68,6 +83,8 @@ typedef struct pmklc_timing {  /* CUDA-event times of the last call, ms */
 /* CompressConfig{} defaults: s=k=3, t=32, bs=320, workers=1, threshold 5e8,
  * smp 0.05, seed 42, scale 4, no public model, device 0. */
 void pmklc_cfg_default(pmklc_cfg* cfg);
+/* CompressConfig::validate (pipeline.cpp:16-24): 0 or 1 + ConfigInvalid */
+int pmklc_cfg_validate(const pmklc_cfg* cfg);
 
 /* compress: host input, host container out. stats (nullable) receives one
  * entry per chunk up to stats_cap; n_chunks (nullable) the chunk count. */
@@ -91,12 +108,15 @@ int pmklc_decompress_to_device(const uint8_t* in, size_t n, const char* pub_mode
 
 /* encode_chunk_standalone over n_chunks chunks at once: chunk i codes
  * tokens[off_i, off_i + chunk_len[i]) (off_i = prefix sum) from inbound
- * snapshot i (length 0 = seeded init). payloads[i] is library-allocated. */
+ * snapshot i (length 0 = seeded init). payloads[i] is library-allocated.
+ * ChunkCodeSpec (pipeline.hpp:69-78): flags & 1 loads the public model file,
+ * flags & 2 the private model from its PMKW bytes (priv_model, priv_len), as
+ * shipped in the container's SPrM blob. */
 int pmklc_encode_chunks(const uint32_t* tokens, const uint64_t* chunk_len, size_t n_chunks,
                         const uint8_t* const* inbound, const size_t* inbound_len, uint32_t flags,
-                        const char* pub_model_path, uint32_t k, uint32_t t, uint32_t bs,
-                        uint32_t scale, uint64_t dm_seed, int32_t device, uint8_t** payloads,
-                        size_t* payload_lens);
+                        const char* pub_model_path, const uint8_t* priv_model, size_t priv_len,
+                        uint32_t k, uint32_t t, uint32_t bs, uint32_t scale, uint64_t dm_seed,
+                        int32_t device, uint8_t** payloads, size_t* payload_lens);
 
 /* one chunk with a probe of its mixed probabilities [max_steps, bs, 4^k]
  * (diagnostic; mirrors oracle/ pmref_dump_chunk) */
@@ -152,6 +172,10 @@ int pmklc_compress_dist(void* handle, const uint8_t* in, const uint8_t* d_in, si
 /* every rank passes the container; rank 0 receives the original bytes */
 int pmklc_decompress_dist(void* handle, const uint8_t* in, size_t n, const char* pub_model_path,
                           uint8_t** out, size_t* out_n, pmklc_timing* timing);
+/* same, rank 0's output left in device memory (release with pmklc_device_free) */
+int pmklc_decompress_dist_to_device(void* handle, const uint8_t* in, size_t n,
+                                    const char* pub_model_path, uint8_t** d_out, size_t* out_n,
+                                    pmklc_timing* timing);
 /* host logic of the above (CPU-testable): this rank's cross-rank handoff ops
  * in tick order (send = 1: this rank sends chunk src's state to `peer`) and
  * the number of (tick, chunk) model steps it runs */
@@ -159,6 +183,39 @@ int pmklc_dist_plan(const uint64_t* lens, size_t n_chunks, uint32_t bs, uint32_t
                     uint16_t smp_per_myriad, int32_t rank, int32_t world, int64_t* op_tick,
                     int32_t* op_src, int32_t* op_dst, int32_t* op_peer, uint8_t* op_send,
                     size_t cap, size_t* n_ops, uint64_t* local_steps);
+
+/* ---- metrics (reference bench.hpp:10-59, bench.cpp:15-114) ------------ */
+/* Eq. 3 compression ratio in bits/base; 1 + EmptySource when source == 0 */
+int pmklc_compression_ratio(uint64_t compressed_bytes, uint64_t source_bytes, double* out);
+/* Eq. 4 throughput in bytes/s over CT + DT; 1 + ZeroTime when not positive */
+int pmklc_throughput(uint64_t source_bytes, double ct_s, double dt_s, double* out);
+/* Eq. 5 robustness CRP in percent (n-1 sample deviation / mean); 1 + EmptyList */
+int pmklc_robustness(const double* crs, size_t n, double* out);
+/* per data block compression ratios of a container (payload + trailer bytes x
+ * 8 / the bases each chunk covers), the CRP population of one large input */
+int pmklc_block_ratios(const uint8_t* container, size_t n, double* crs, size_t cap,
+                       size_t* count);
+
+typedef struct pmklc_dataset_result {  /* DatasetResult (bench.hpp:22-29) */
+  char name[256];
+  uint64_t source_bytes, compressed_bytes;
+  double ct_s, dt_s, cr, thp;
+  int32_t verified;
+} pmklc_dataset_result;
+typedef struct pmklc_metrics_report {  /* MetricsReport (bench.hpp:31-36) */
+  double mean_cr, crp_percent;
+  uint64_t peak_mem_bytes, peak_device_bytes;
+} pmklc_metrics_report;
+/* run_benchmark (bench.cpp:67-114) over n_paths files with cfg; rows has
+ * capacity n_paths; csv_path (nullable) gets the reference CSV (to_csv,
+ * bench.cpp:49-65). fault_flip_mid != 0 flips bit 6 of the container's middle
+ * byte before decompression (the reference tests' fault hook). */
+int pmklc_run_benchmark(const char* const* paths, size_t n_paths, const pmklc_cfg* cfg,
+                        const char* csv_path, int32_t fault_flip_mid, pmklc_dataset_result* rows,
+                        pmklc_metrics_report* report);
+
+/* FNV-1a-64 (bytes.hpp:17-24), the fingerprint/checksum hash of the format */
+uint64_t pmklc_fnv1a64(const uint8_t* p, size_t n);
 
 /* seeded (untrained) BiGRU predictor file in the reference's PMKW format
  * (BiGruModel + serialize_model, models.cpp:38-51,159-173); layers = 2 is a

@@ -111,6 +111,7 @@ static uint64_t fnv1a(const uint8_t* p, size_t n, uint64_t h) {
   return h;
 }
 #define FNV_SEED 0xcbf29ce484222325ull
+uint64_t orc_fnv1a64(const uint8_t* p, size_t n) { return fnv1a(p, n, FNV_SEED); }
 
 typedef struct { uint64_t s; } rng_t;
 static uint64_t rng_u64(rng_t* r) {

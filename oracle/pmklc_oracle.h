@@ -34,6 +34,7 @@ typedef struct {
 } orc_chunk_stats;
 
 const char* orc_last_error(void);
+uint64_t orc_fnv1a64(const uint8_t* p, size_t n);
 void orc_free(void* p);
 
 int orc_compress(const uint8_t* in, size_t n, const orc_cfg* c, uint8_t** out, size_t* out_n,

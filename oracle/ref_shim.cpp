@@ -99,6 +99,7 @@ void copy_stats(const PipelineStats& ps, RefChunkStats* out, size_t cap) {
 extern "C" {
 
 const char* pmref_last_error(void) { return g_err.c_str(); }
+uint64_t pmref_fnv1a64(const uint8_t* p, size_t n) { return fnv1a64(ByteSpan(p, n)); }
 void pmref_free(void* p) { std::free(p); }
 
 int pmref_compress(const uint8_t* in, size_t n, const RefCfg* c, uint8_t** out, size_t* out_n,
@@ -326,19 +327,97 @@ int pmref_dump_chunk(const uint32_t* tokens, uint64_t n_tokens, uint32_t flags_b
   });
 }
 
+int pmref_encode_chunk_standalone_priv(const uint32_t*, uint64_t, uint32_t, const char*,
+                                       const uint8_t*, size_t, uint32_t, uint32_t, uint32_t,
+                                       uint32_t, uint64_t, const uint8_t*, size_t, uint8_t**, size_t*);
+
+/// Replays ChunkWorker::encode (pipeline.cpp:115-137, 178-213) over one
+/// chunk with the reference's public classes, with either static model
+/// (flags bit 0: the public model file, bit 1: the private model from its
+/// PMKW bytes), stopping after `stop_at` batch steps (0 = all L). The trainer
+/// snapshot is taken after batch step `snap_at` (maybe_snapshot(j + 1),
+/// warm-up steps included; 0 = after the last executed step). The payload is
+/// returned only for a complete chunk (empty otherwise). Used to replay the
+/// SMP chain of large runs (chunk i's inbound = chunk i-1's snapshot at its
+/// snapshot step, pipeline.cpp:207-213, 253-294) and to recode sampled chunks
+/// from recorded inbound snapshots.
+int pmref_replay_chunk(const uint32_t* tokens, uint64_t n_tokens, uint32_t flags_bits,
+                       const char* pub_path, const uint8_t* priv_bytes, size_t priv_n, uint32_t k,
+                       uint32_t t, uint32_t bs, uint32_t scale, uint64_t dm_seed,
+                       const uint8_t* inbound, size_t inbound_n, uint64_t snap_at,
+                       uint64_t stop_at, uint8_t** payload, size_t* payload_n, uint8_t** snap,
+                       size_t* snap_n) {
+  return guard([&] {
+    const ModelDims dims = ModelDims::make(uint32_t(1) << (2 * k), t, scale);
+    const SelectorFlags f = SelectorFlags::from_bits(uint8_t(flags_bits));
+    std::unique_ptr<BiGruModel> pub, priv;
+    if (f.pub_model) pub = deserialize_model(read_file(pub_path));
+    if (f.priv_model) priv = deserialize_model(ByteSpan(priv_bytes, priv_n));
+    AttentionModel dm(dims, dm_seed);
+    OnlineTrainer tr(&dm);
+    if (inbound_n) tr.restore(ByteSpan(inbound, inbound_n));
+    const QuantizedDistribution uni = uniform_dist(uint32_t(dims.vocab));
+    const uint64_t L = n_tokens / bs;
+    const uint64_t stop = stop_at && stop_at < L ? stop_at : L;
+    ByteVec out, s;
+    RangeEncoder enc(out);
+    std::vector<uint32_t> ctx(size_t(bs) * t), tg(bs);
+    Tensor lu, lr, lm, pr;
+    AttentionModel::Tape tape;
+    for (uint64_t j = 0; j < stop; ++j) {
+      if (j < t) {
+        for (uint32_t r = 0; r < bs; ++r) enc.encode(uni, tokens[r * L + j]);
+      } else {
+        for (uint32_t r = 0; r < bs; ++r)
+          for (uint32_t i = 0; i < t; ++i) ctx[size_t(r) * t + i] = tokens[uint64_t(r) * L + (j - t) + i];
+        if (f.pub_model) pub->predict(ctx.data(), bs, t, lu);
+        if (f.priv_model) priv->predict(ctx.data(), bs, t, lr);
+        dm.forward(ctx.data(), bs, t, tape, lm);
+        mix(f, tr.alpha(), f.pub_model ? &lu : nullptr, f.priv_model ? &lr : nullptr, &lm, pr);
+        for (uint32_t r = 0; r < bs; ++r) {
+          tg[r] = tokens[r * L + j];
+          enc.encode(quantize(std::span<const float>(pr.ptr() + int64_t(r) * dims.vocab, size_t(dims.vocab))),
+                     tg[r]);
+        }
+        tr.step(f, pr, tg.data(), f.pub_model ? &lu : nullptr, f.priv_model ? &lr : nullptr, lm, tape);
+      }
+      if (snap_at && j + 1 == snap_at) s = tr.snapshot();
+    }
+    if (!snap_at) s = tr.snapshot();
+    if (stop == L) enc.finish();
+    else out.clear();
+    *payload = dup(out);
+    *payload_n = out.size();
+    *snap = dup(s);
+    *snap_n = s.size();
+  });
+}
+
 /// The reference's own diagnostic hook (pipeline.cpp:298-301).
 int pmref_encode_chunk_standalone(const uint32_t* tokens, uint64_t n_tokens, uint32_t flags_bits,
                                   const char* pub_path, uint32_t k, uint32_t t, uint32_t bs,
                                   uint32_t scale, uint64_t dm_seed, const uint8_t* inbound,
                                   size_t inbound_n, uint8_t** out, size_t* out_n) {
+  return pmref_encode_chunk_standalone_priv(tokens, n_tokens, flags_bits, pub_path, nullptr, 0, k, t,
+                                            bs, scale, dm_seed, inbound, inbound_n, out, out_n);
+}
+
+/// Same, with ChunkCodeSpec::priv given as PMKW bytes (pipeline.hpp:69-78).
+int pmref_encode_chunk_standalone_priv(const uint32_t* tokens, uint64_t n_tokens, uint32_t flags_bits,
+                                       const char* pub_path, const uint8_t* priv_bytes,
+                                       size_t priv_n, uint32_t k, uint32_t t, uint32_t bs,
+                                       uint32_t scale, uint64_t dm_seed, const uint8_t* inbound,
+                                       size_t inbound_n, uint8_t** out, size_t* out_n) {
   return guard([&] {
     const ModelDims dims = ModelDims::make(uint32_t(1) << (2 * k), t, scale);
-    std::unique_ptr<BiGruModel> pub;
+    std::unique_ptr<BiGruModel> pub, priv;
     const SelectorFlags f = SelectorFlags::from_bits(uint8_t(flags_bits));
     if (f.pub_model) pub = deserialize_model(read_file(pub_path));
+    if (f.priv_model) priv = deserialize_model(ByteSpan(priv_bytes, priv_n));
     ChunkCodeSpec spec;
     spec.flags = f;
     spec.pub = pub.get();
+    spec.priv = priv.get();
     spec.dims = dims;
     spec.t = t;
     spec.bs = bs;

@@ -46,11 +46,39 @@ class _Cfg(C.Structure):
 
 
 class Stats(C.Structure):
-    """WorkerStats (pipeline.hpp:27-35), one per chunk."""
+    """pmklc_stats: WorkerStats (pipeline.hpp:27-35), one per chunk."""
     _fields_ = [("tokens", C.c_uint64), ("uniform_coded", C.c_uint64), ("pub_calls", C.c_uint64),
                 ("priv_calls", C.c_uint64), ("dyn_calls", C.c_uint64),
                 ("snapshot_recv_hash", C.c_uint64), ("snapshot_sent_hash", C.c_uint64),
+                ("snapshot_recv_bytes", C.POINTER(C.c_uint8)), ("snapshot_recv_len", C.c_uint64),
                 ("early_loss_bits", C.c_double)]
+
+
+@dataclass
+class WorkerStats:
+    """pmklc::WorkerStats (pipeline.hpp:27-35); snapshot_recv_bytes is the
+    chunk's inbound SMP snapshot (empty: seeded init), as the reference keeps
+    it when stats are collected (pipeline.cpp:108-111)."""
+    tokens: int = 0
+    uniform_coded: int = 0
+    pub_calls: int = 0
+    priv_calls: int = 0
+    dyn_calls: int = 0
+    snapshot_recv_hash: int = 0
+    snapshot_sent_hash: int = 0
+    snapshot_recv_bytes: bytes = b""
+    early_loss_bits: float = 0.0
+
+
+def _worker_stats(st, n: int) -> List[WorkerStats]:
+    out = []
+    for i in range(n):
+        e = st[i]
+        b = C.string_at(e.snapshot_recv_bytes, e.snapshot_recv_len) if e.snapshot_recv_len else b""
+        out.append(WorkerStats(e.tokens, e.uniform_coded, e.pub_calls, e.priv_calls, e.dyn_calls,
+                               e.snapshot_recv_hash, e.snapshot_sent_hash, b, e.early_loss_bits))
+    lib().pmklc_stats_release(st, C.c_size_t(n))
+    return out
 
 
 class Timing(C.Structure):
@@ -62,7 +90,7 @@ class Timing(C.Structure):
                 ("hot_flops_per_unit", C.c_double), ("sprm_ms", C.c_double)]
 
 
-# Every symbol include/pmklc_b200.h declares (checked by tests/test_capi.py).
+# Every symbol include/pmklc_b200.h declares (checked by tests/test_host.py).
 EXPORTS = [
     "pmklc_cfg_default", "pmklc_compress", "pmklc_compress_device", "pmklc_decompress",
     "pmklc_decompress_to_device", "pmklc_encode_chunks", "pmklc_dump_chunk", "pmklc_skmer_encode",
@@ -71,7 +99,10 @@ EXPORTS = [
     "pmklc_synth_genome", "pmklc_synth_species", "pmklc_synth_packed_codes", "pmklc_plan_chunks",
     "pmklc_schedule", "pmklc_quantize", "pmklc_write_bigru", "pmklc_bench_kernel",
     "pmklc_nccl_id", "pmklc_dist_create", "pmklc_dist_destroy", "pmklc_compress_dist",
-    "pmklc_decompress_dist", "pmklc_dist_plan",
+    "pmklc_decompress_dist", "pmklc_dist_plan", "pmklc_stats_release", "pmklc_chunk_count",
+    "pmklc_container_chunks", "pmklc_decompress_dist_to_device", "pmklc_compression_ratio",
+    "pmklc_throughput", "pmklc_robustness", "pmklc_block_ratios", "pmklc_run_benchmark",
+    "pmklc_fnv1a64", "pmklc_cfg_validate",
 ]
 
 _lib = None
@@ -127,8 +158,16 @@ class CompressConfig:
 
 @dataclass
 class PipelineStats:
-    workers: List[Stats] = field(default_factory=list)
+    workers: List[WorkerStats] = field(default_factory=list)
     timing: Optional[Timing] = None
+
+
+def chunk_count(raw: bytes, cfg: CompressConfig = CompressConfig()) -> int:
+    """Chunks compress() writes for this input (host-only plan, pipeline.cpp:32-52)."""
+    c = cfg._c()
+    n = C.c_size_t()
+    _check(lib().pmklc_chunk_count(raw, C.c_size_t(len(raw)), C.byref(c), C.byref(n)))
+    return n.value
 
 
 def compress(raw: bytes, cfg: CompressConfig = CompressConfig(),
@@ -137,15 +176,14 @@ def compress(raw: bytes, cfg: CompressConfig = CompressConfig(),
     c = cfg._c()
     out = C.POINTER(C.c_uint8)()
     n = C.c_size_t()
-    cap = 1 << 16
-    st = (Stats * cap)() if stats is not None else None
+    cap = chunk_count(raw, cfg) if stats is not None else 0
+    st = (Stats * max(cap, 1))() if stats is not None else None
     nch = C.c_size_t()
     tm = Timing()
     _check(lib().pmklc_compress(raw, C.c_size_t(len(raw)), C.byref(c), C.byref(out), C.byref(n),
-                                st, C.c_size_t(cap if st is not None else 0), C.byref(nch),
-                                C.byref(tm)))
+                                st, C.c_size_t(cap), C.byref(nch), C.byref(tm)))
     if stats is not None:
-        stats.workers = [st[i] for i in range(nch.value)]
+        stats.workers = _worker_stats(st, min(nch.value, cap))
         stats.timing = tm
     return _take(out, n.value)
 
@@ -167,16 +205,19 @@ def decompress(container: bytes, pub_model_path: str = "", workers: int = 1,
     """pmklc::decompress — bit-exact inverse of compress."""
     out = C.POINTER(C.c_uint8)()
     n = C.c_size_t()
-    cap = 1 << 16
-    st = (Stats * cap)() if stats is not None else None
+    cap = 0
+    if stats is not None:  # chunk count from the container header (container.cpp:53)
+        cn = C.c_size_t()
+        if lib().pmklc_container_chunks(container, C.c_size_t(len(container)), C.byref(cn)) == 0:
+            cap = cn.value
+    st = (Stats * max(cap, 1))() if stats is not None else None
     tm = Timing()
     _check(lib().pmklc_decompress(container, C.c_size_t(len(container)),
                                   pub_model_path.encode() if pub_model_path else None, workers,
-                                  device, C.byref(out), C.byref(n), st,
-                                  C.c_size_t(cap if st is not None else 0), C.byref(tm)))
+                                  device, C.byref(out), C.byref(n), st, C.c_size_t(cap),
+                                  C.byref(tm)))
     if stats is not None:
-        nchunks = int.from_bytes(container[48:52], "little") if len(container) >= 52 else 0
-        stats.workers = [st[i] for i in range(min(nchunks, cap))]
+        stats.workers = _worker_stats(st, cap)
         stats.timing = tm
     return _take(out, n.value)
 
@@ -199,8 +240,10 @@ def device_free(ptr: int) -> None:
 
 def encode_chunks(tokens, chunk_lens: Sequence[int], inbound: Sequence[bytes], flags: int, k: int,
                   t: int, bs: int, scale: int, dm_seed: int, pub_model_path: str = "",
-                  device: int = 0) -> List[bytes]:
-    """Batched pmklc::encode_chunk_standalone."""
+                  device: int = 0, priv_model: bytes = b"") -> List[bytes]:
+    """Batched pmklc::encode_chunk_standalone (ChunkCodeSpec, pipeline.hpp:69-78):
+    flags & 1 uses the public model file, flags & 2 the private model given as
+    its PMKW bytes (the container's SPrM blob)."""
     import numpy as np
     tokens = np.ascontiguousarray(tokens, dtype=np.uint32)
     nc = len(chunk_lens)
@@ -211,7 +254,8 @@ def encode_chunks(tokens, chunk_lens: Sequence[int], inbound: Sequence[bytes], f
     pl = (C.c_size_t * nc)()
     _check(lib().pmklc_encode_chunks(tokens.ctypes.data_as(C.c_void_p), lens, C.c_size_t(nc),
                                      C.cast(ib, C.c_void_p), ibl, flags,
-                                     pub_model_path.encode() if pub_model_path else None, k, t, bs,
+                                     pub_model_path.encode() if pub_model_path else None,
+                                     priv_model or None, C.c_size_t(len(priv_model)), k, t, bs,
                                      scale, C.c_uint64(dm_seed), device, pays, pl))
     return [_take(pays[i], pl[i]) for i in range(nc)]
 
@@ -387,10 +431,116 @@ class DistContext:
                                            C.byref(out), C.byref(n), C.byref(tm)))
         return _take(out, n.value)
 
+    def decompress_to_device(self, blob: bytes, pub_model_path: str = "",
+                             timing: Optional[Timing] = None):
+        """(device_ptr, length) on rank 0 ((0, 0) elsewhere); free with device_free."""
+        d = C.c_void_p()
+        n = C.c_size_t()
+        tm = timing if timing is not None else Timing()
+        _check(lib().pmklc_decompress_dist_to_device(
+            self.h, blob, C.c_size_t(len(blob)),
+            pub_model_path.encode() if pub_model_path else None, C.byref(d), C.byref(n),
+            C.byref(tm)))
+        return d.value or 0, n.value
+
     def close(self):
         if self.h:
             lib().pmklc_dist_destroy(self.h)
             self.h = None
+
+
+# ---------------------------------------------------------------- metrics
+def compression_ratio(compressed_bytes: int, source_bytes: int) -> float:
+    """Eq. 3, bits per base (bench.cpp:15-18); PmklcError EmptySource for 0."""
+    out = C.c_double()
+    _check(lib().pmklc_compression_ratio(C.c_uint64(compressed_bytes), C.c_uint64(source_bytes),
+                                         C.byref(out)))
+    return out.value
+
+
+def throughput(source_bytes: int, ct_s: float, dt_s: float) -> float:
+    """Eq. 4, bytes/s over CT + DT (bench.cpp:20-24); PmklcError ZeroTime."""
+    out = C.c_double()
+    _check(lib().pmklc_throughput(C.c_uint64(source_bytes), C.c_double(ct_s), C.c_double(dt_s),
+                                  C.byref(out)))
+    return out.value
+
+
+def robustness(crs: Sequence[float]) -> float:
+    """Eq. 5, CRP in percent with the n-1 denominator (bench.cpp:26-36)."""
+    n = len(crs)
+    arr = (C.c_double * max(n, 1))(*crs)
+    out = C.c_double()
+    _check(lib().pmklc_robustness(arr, C.c_size_t(n), C.byref(out)))
+    return out.value
+
+
+def block_ratios(container: bytes) -> List[float]:
+    """Per data block compression ratios of a container (the CRP population)."""
+    cn = C.c_size_t()
+    _check(lib().pmklc_container_chunks(container, C.c_size_t(len(container)), C.byref(cn)))
+    arr = (C.c_double * max(cn.value, 1))()
+    cnt = C.c_size_t()
+    _check(lib().pmklc_block_ratios(container, C.c_size_t(len(container)), arr,
+                                    C.c_size_t(cn.value), C.byref(cnt)))
+    return list(arr[: min(cnt.value, cn.value)])
+
+
+class DatasetResult(C.Structure):
+    """DatasetResult (bench.hpp:22-29)."""
+    _fields_ = [("_name", C.c_char * 256), ("source_bytes", C.c_uint64),
+                ("compressed_bytes", C.c_uint64), ("ct_s", C.c_double), ("dt_s", C.c_double),
+                ("cr", C.c_double), ("thp", C.c_double), ("_verified", C.c_int32)]
+
+    @property
+    def name(self) -> str:
+        return self._name.decode()
+
+    @property
+    def verified(self) -> bool:
+        return bool(self._verified)
+
+
+class MetricsReport(C.Structure):
+    """MetricsReport (bench.hpp:31-36) + the device HBM peak."""
+    _fields_ = [("mean_cr", C.c_double), ("crp_percent", C.c_double),
+                ("peak_mem_bytes", C.c_uint64), ("peak_device_bytes", C.c_uint64)]
+
+
+def run_benchmark(paths: Sequence[str], cfg: CompressConfig = CompressConfig(), csv_path: str = "",
+                  fault_flip_mid: bool = False):
+    """run_benchmark (bench.cpp:67-114): (rows, report)."""
+    n = len(paths)
+    ps = (C.c_char_p * max(n, 1))(*[p.encode() for p in paths])
+    rows = (DatasetResult * max(n, 1))()
+    rep = MetricsReport()
+    c = cfg._c()
+    _check(lib().pmklc_run_benchmark(ps, C.c_size_t(n), C.byref(c),
+                                     csv_path.encode() if csv_path else None,
+                                     1 if fault_flip_mid else 0, rows, C.byref(rep)))
+    return list(rows[:n]), rep
+
+
+def fnv1a64(b: bytes) -> int:
+    """FNV-1a-64 (bytes.hpp:17-24)."""
+    f = lib().pmklc_fnv1a64
+    f.restype = C.c_uint64
+    return int(f(b, C.c_size_t(len(b))))
+
+
+def device_equal(d_ptr: int, d_ref_ptr: int, n: int, device: int = 0) -> bool:
+    """True when n bytes at device pointer d_ptr equal those at d_ref_ptr
+    (verification of device-resident decompression output; torch compares)."""
+    import torch
+    cuda = C.CDLL("libcuda.so.1")
+    a = torch.empty(n, dtype=torch.uint8, device=f"cuda:{device}")
+    b = torch.empty(n, dtype=torch.uint8, device=f"cuda:{device}")
+    torch.cuda.synchronize(device)
+    for dst, src in ((a, d_ptr), (b, d_ref_ptr)):
+        if cuda.cuMemcpyDtoD_v2(C.c_uint64(dst.data_ptr()), C.c_uint64(src), C.c_size_t(n)) != 0:
+            raise PmklcError(101, "cuMemcpyDtoD failed")
+    torch.cuda.synchronize(device)
+    return bool(torch.equal(a, b))
 
 
 def version() -> str:

@@ -8,6 +8,7 @@
 
 #include "../../include/pmklc_b200.h"
 #include "host/engine.hpp"
+#include "host/metrics.hpp"
 #include "host/plan.hpp"
 
 namespace pmklc_b200 {
@@ -68,8 +69,11 @@ void copy_stats(const std::vector<ChunkStats>& st, pmklc_stats* out, size_t cap)
   if (!out) return;
   for (size_t i = 0; i < st.size() && i < cap; ++i) {
     const ChunkStats& s = st[i];
+    uint8_t* bytes = nullptr;
+    if (!s.snapshot_recv_bytes.empty()) bytes = dup(s.snapshot_recv_bytes);
     out[i] = pmklc_stats{s.tokens,    s.uniform_coded,      s.pub_calls,          s.priv_calls,
-                         s.dyn_calls, s.snapshot_recv_hash, s.snapshot_sent_hash, s.early_loss_bits};
+                         s.dyn_calls, s.snapshot_recv_hash, s.snapshot_sent_hash, bytes,
+                         uint64_t(s.snapshot_recv_bytes.size()), s.early_loss_bits};
   }
 }
 
@@ -105,6 +109,13 @@ extern "C" {
 
 void pmklc_cfg_default(pmklc_cfg* c) {
   *c = pmklc_cfg{3, 3, 32, 320, 1, 4, 500000000ull, 42, 0.05f, nullptr, 0, 0};
+}
+
+int pmklc_cfg_validate(const pmklc_cfg* c) {
+  return guard([&] {
+    if (!c) raise(errc::config_invalid, "null config");
+    to_cfg(c).validate();
+  });
 }
 
 int pmklc_compress(const uint8_t* in, size_t n, const pmklc_cfg* cfg, uint8_t** out, size_t* out_n,
@@ -152,10 +163,11 @@ int pmklc_decompress_to_device(const uint8_t* in, size_t n, const char* pub_mode
 
 int pmklc_encode_chunks(const uint32_t* tokens, const uint64_t* chunk_len, size_t n_chunks,
                         const uint8_t* const* inbound, const size_t* inbound_len, uint32_t flags,
-                        const char* pub_model_path, uint32_t k, uint32_t t, uint32_t bs,
-                        uint32_t scale, uint64_t dm_seed, int32_t device, uint8_t** payloads,
-                        size_t* payload_lens) {
+                        const char* pub_model_path, const uint8_t* priv_model, size_t priv_len,
+                        uint32_t k, uint32_t t, uint32_t bs, uint32_t scale, uint64_t dm_seed,
+                        int32_t device, uint8_t** payloads, size_t* payload_lens) {
   return guard([&] {
+    const Bytes priv = priv_model && priv_len ? Bytes(priv_model, priv_model + priv_len) : Bytes{};
     std::vector<ChunkJob> jobs(n_chunks);
     uint64_t off = 0;
     for (size_t i = 0; i < n_chunks; ++i) {
@@ -166,7 +178,7 @@ int pmklc_encode_chunks(const uint32_t* tokens, const uint64_t* chunk_len, size_
         jobs[i].inbound.assign(inbound[i], inbound[i] + inbound_len[i]);
     }
     std::vector<Bytes> out = encode_chunks(jobs, uint8_t(flags), pub_model_path ? pub_model_path : "",
-                                           k, t, bs, scale, dm_seed, device);
+                                           priv, k, t, bs, scale, dm_seed, device);
     for (size_t i = 0; i < n_chunks; ++i) {
       payloads[i] = dup(out[i]);
       payload_lens[i] = out[i].size();
@@ -190,7 +202,7 @@ int pmklc_dump_chunk(const uint32_t* tokens, uint64_t n_tokens, uint32_t flags,
     opt.probe_steps = max_steps;
     opt.probe = &pr;
     std::vector<Bytes> out = encode_chunks(jobs, uint8_t(flags), pub_model_path ? pub_model_path : "",
-                                           k, t, bs, scale, dm_seed, device, opt);
+                                           Bytes{}, k, t, bs, scale, dm_seed, device, opt);
     if (probs && !pr.empty()) std::memcpy(probs, pr.data(), pr.size() * 4);
     *payload = dup(out[0]);
     *payload_n = out[0].size();
@@ -324,6 +336,72 @@ int pmklc_decompress_dist(void* handle, const uint8_t* in, size_t n, const char*
   });
 }
 
+int pmklc_decompress_dist_to_device(void* handle, const uint8_t* in, size_t n,
+                                    const char* pub_model_path, uint8_t** d_out, size_t* out_n,
+                                    pmklc_timing* timing) {
+  return guard([&] {
+    Timing t;
+    CallOptions opt;
+    opt.timing = &t;
+    *d_out = decompress_dist_to_device(*static_cast<Dist*>(handle), in, n,
+                                       pub_model_path ? pub_model_path : "", out_n, opt);
+    copy_timing(t, timing);
+  });
+}
+
+int pmklc_compression_ratio(uint64_t compressed_bytes, uint64_t source_bytes, double* out) {
+  return guard([&] { *out = compression_ratio(compressed_bytes, source_bytes); });
+}
+
+int pmklc_throughput(uint64_t source_bytes, double ct_s, double dt_s, double* out) {
+  return guard([&] { *out = throughput(source_bytes, ct_s, dt_s); });
+}
+
+int pmklc_robustness(const double* crs, size_t n, double* out) {
+  return guard([&] { *out = robustness(crs, n); });
+}
+
+int pmklc_block_ratios(const uint8_t* container, size_t n, double* crs, size_t cap, size_t* count) {
+  return guard([&] {
+    const std::vector<double> r = block_ratios(container, n);
+    *count = r.size();
+    for (size_t i = 0; i < r.size() && i < cap; ++i) crs[i] = r[i];
+  });
+}
+
+int pmklc_run_benchmark(const char* const* paths, size_t n_paths, const pmklc_cfg* cfg,
+                        const char* csv_path, int32_t fault_flip_mid, pmklc_dataset_result* rows,
+                        pmklc_metrics_report* report) {
+  return guard([&] {
+    if (!cfg) raise(errc::config_invalid, "null config");
+    std::vector<std::string> ps(paths, paths + n_paths);
+    std::function<void(Bytes&)> fault;
+    if (fault_flip_mid)
+      fault = [](Bytes& c) {
+        if (!c.empty()) c[c.size() / 2] ^= 0x40;
+      };
+    const MetricsReport rep = run_benchmark(ps, to_cfg(cfg), csv_path ? csv_path : "", fault);
+    for (size_t i = 0; i < rep.rows.size() && i < n_paths; ++i) {
+      const DatasetResult& d = rep.rows[i];
+      pmklc_dataset_result& o = rows[i];
+      std::memset(&o, 0, sizeof o);
+      std::snprintf(o.name, sizeof o.name, "%s", d.name.c_str());
+      o.source_bytes = d.source_bytes;
+      o.compressed_bytes = d.compressed_bytes;
+      o.ct_s = d.ct_s;
+      o.dt_s = d.dt_s;
+      o.cr = d.cr;
+      o.thp = d.thp;
+      o.verified = d.verified ? 1 : 0;
+    }
+    if (report)
+      *report = pmklc_metrics_report{rep.mean_cr, rep.crp_percent, rep.peak_mem_bytes,
+                                     rep.peak_device_bytes};
+  });
+}
+
+uint64_t pmklc_fnv1a64(const uint8_t* p, size_t n) { return fnv1a64(p, n); }
+
 int pmklc_dist_plan(const uint64_t* lens, size_t n_chunks, uint32_t bs, uint32_t t, uint16_t myriad,
                     int32_t rank, int32_t world, int64_t* op_tick, int32_t* op_src, int32_t* op_dst,
                     int32_t* op_peer, uint8_t* op_send, size_t cap, size_t* n_ops,
@@ -350,6 +428,31 @@ int pmklc_dist_plan(const uint64_t* lens, size_t n_chunks, uint32_t bs, uint32_t
       op_send[i] = rp.ops[i].send ? 1 : 0;
     }
     if (local_steps) *local_steps = rp.local.act.size();
+  });
+}
+
+void pmklc_stats_release(pmklc_stats* stats, size_t n) {
+  if (!stats) return;
+  for (size_t i = 0; i < n; ++i) {
+    std::free(stats[i].snapshot_recv_bytes);
+    stats[i].snapshot_recv_bytes = nullptr;
+    stats[i].snapshot_recv_len = 0;
+  }
+}
+
+int pmklc_chunk_count(const uint8_t* in, size_t n, const pmklc_cfg* c, size_t* count) {
+  return guard([&] {
+    if (!c) raise(errc::config_invalid, "null config");
+    const Config cfg = to_cfg(c);
+    cfg.validate();
+    *count = planned_chunks(in, n, cfg);
+  });
+}
+
+int pmklc_container_chunks(const uint8_t* in, size_t n, size_t* count) {
+  return guard([&] {
+    if (n < 52) raise(errc::length_mismatch, "container shorter than its header");
+    *count = size_t(in[48]) | size_t(in[49]) << 8 | size_t(in[50]) << 16 | size_t(in[51]) << 24;
   });
 }
 

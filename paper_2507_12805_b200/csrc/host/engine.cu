@@ -454,8 +454,12 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     d_td.upload(&td0, 1, st);
   }
 
-  // snapshot hashes for stats: key (src, steps)
+  // snapshots for stats (hash and inbound bytes, WorkerStats semantics,
+  // pipeline.cpp:106-113): key (src, steps). They are read from the device
+  // state slots between ticks, at the tick the source reaches the step, in
+  // the graph-replay path too (one host sync per snapshot tick).
   std::map<std::pair<int64_t, uint64_t>, uint64_t> snap_hash;
+  std::map<std::pair<int64_t, uint64_t>, Bytes> snap_bytes;
   auto need_snapshot = [&](int64_t src, uint64_t steps) {
     return want_stats && !snap_hash.count({src, steps});
   };
@@ -468,8 +472,9 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     } else {
       s = fetch_state(lay, w.p, m.p, v.p, sc.p, src, st);
     }
-    const Bytes b = snapshot_bytes(lay, s);
+    Bytes b = snapshot_bytes(lay, s);
     snap_hash[{src, steps}] = fnv1a64(b);
+    snap_bytes[{src, steps}] = std::move(b);
   };
   // which (src, steps) snapshots are needed and when they become available
   std::map<int64_t, std::vector<std::pair<int64_t, uint64_t>>> snap_at;  // tick -> keys
@@ -744,8 +749,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     nck(nccl().GroupEnd());
   };
   const bool probing = run.opt && run.opt->probe && run.opt->probe_chunk >= 0;
-  const bool host_sync = probing || want_stats;
-  if (sch.ticks > 0 && !host_sync) {
+  if (sch.ticks > 0 && !probing) {
     // capture one tick, replay it sch.ticks times
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
@@ -754,6 +758,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     CK(cudaStreamEndCapture(st, &graph));
     CK(cudaGraphInstantiate(&exec, graph, 0));
     for (int64_t tick = 0; tick < sch.ticks; ++tick) {
+      snapshots_for_tick(tick);
       comm_ops(tick);
       CK(cudaGraphLaunch(exec, st));
     }
@@ -809,7 +814,11 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     const uint64_t counted = std::min<uint64_t>(sch.M[c], warm[c]);
     if (counted) s.early_loss_bits = wl[c] / double(counted * R) / 0.6931471805599453;
     if (want_stats) {
-      if (sch.inbound_nonempty[c]) s.snapshot_recv_hash = snap_hash[{sch.src[c], sch.src_steps[c]}];
+      if (sch.inbound_nonempty[c]) {
+        const std::pair<int64_t, uint64_t> key{sch.src[c], sch.src_steps[c]};
+        s.snapshot_recv_hash = snap_hash[key];
+        s.snapshot_recv_bytes = snap_bytes[key];
+      }
       if (sch.emits[c]) s.snapshot_sent_hash = snap_hash[{sch.src[c + 1], sch.src_steps[c + 1]}];
     }
   }
@@ -1435,18 +1444,35 @@ uint8_t* decompress_to_device(const uint8_t* blob, size_t n, const std::string& 
   return p;
 }
 
+size_t planned_chunks(const uint8_t* raw, size_t n, const Config& cfg) {
+  uint64_t nc = 0;  // canonical bases: the ACGT bytes (alphabet.cpp:22-35)
+  for (size_t i = 0; i < n; ++i) {
+    const uint8_t b = raw[i];
+    nc += (b == 'A' || b == 'C' || b == 'G' || b == 'T') ? 1 : 0;
+  }
+  const uint64_t m = token_count(nc, cfg.s, cfg.k);
+  const uint16_t myriad = uint16_t(std::lround(double(cfg.smp_fraction) * 10000.0));
+  return plan_chunks(m, cfg.workers, cfg.bs, cfg.t, myriad).len.size();
+}
+
 std::vector<Bytes> encode_chunks(const std::vector<ChunkJob>& jobs, uint8_t flags,
-                                 const std::string& pub_model_path, uint32_t k, uint32_t t,
-                                 uint32_t bs, uint32_t scale, uint64_t dm_seed, int device,
-                                 const CallOptions& opt) {
+                                 const std::string& pub_model_path, const Bytes& priv_model,
+                                 uint32_t k, uint32_t t, uint32_t bs, uint32_t scale,
+                                 uint64_t dm_seed, int device, const CallOptions& opt) {
   CK(cudaSetDevice(device));
   Stream stream(device);
   cudaStream_t st = stream.s;
   const Dims dims = Dims::make(uint32_t(1) << (2 * k), t, scale);
   const DmLayout lay(dims);
   if (!(flags & 4)) raise(errc::config_invalid, "dynamic model flag must be set");
-  if (flags & 2) raise(errc::config_invalid, "private model not supported by encode_chunks");
   Loaded models;
+  if (flags & 2) {
+    if (priv_model.empty()) raise(errc::config_invalid, "private model flag without a private model");
+    BiGru priv = BiGru::deserialize(priv_model.data(), priv_model.size());
+    check_model_dims(priv, dims, "private");
+    models.priv.upload(std::move(priv), st);
+    models.has_priv = true;
+  }
   if (flags & 1) {
     const Bytes file = read_file(pub_model_path);
     BiGru pub = BiGru::deserialize(file.data(), file.size());
@@ -1461,6 +1487,7 @@ std::vector<Bytes> encode_chunks(const std::vector<ChunkJob>& jobs, uint8_t flag
   run.t = t;
   run.flags = flags;
   run.pub = models.has_pub ? &models.pub : nullptr;
+  run.priv = models.has_priv ? &models.priv : nullptr;
   run.dm_seed = dm_seed;
   Plan plan;
   plan.bs = bs;
@@ -1728,6 +1755,22 @@ Bytes decompress_dist(const Dist& d, const uint8_t* blob, size_t n, const std::s
   Bytes out(res.len);
   if (res.len) CK(cudaMemcpy(out.data(), res.out.p, res.len, cudaMemcpyDeviceToHost));
   return out;
+}
+
+uint8_t* decompress_dist_to_device(const Dist& d, const uint8_t* blob, size_t n,
+                                   const std::string& pub_model_path, size_t* out_len,
+                                   const CallOptions& opt) {
+  CK(cudaSetDevice(d.device));
+  Stream stream(d.device);
+  DecodeResult res;
+  decompress_impl(blob, n, pub_model_path, d.device, opt, res, stream.s, &d);
+  *out_len = res.len;
+  uint8_t* p = res.len ? res.out.p : nullptr;
+  if (p) {
+    res.out.p = nullptr;  // ownership to caller
+    res.out.n = 0;
+  }
+  return p;
 }
 
 }  // namespace pmklc_b200

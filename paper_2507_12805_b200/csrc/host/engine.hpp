@@ -27,6 +27,7 @@ struct Config {
 struct ChunkStats {
   uint64_t tokens = 0, uniform_coded = 0, pub_calls = 0, priv_calls = 0, dyn_calls = 0;
   uint64_t snapshot_recv_hash = 0, snapshot_sent_hash = 0;
+  Bytes snapshot_recv_bytes;  // the inbound SMP snapshot, kept when stats are collected
   double early_loss_bits = 0;
 };
 
@@ -67,6 +68,14 @@ Bytes compress_dist(const Dist& d, const uint8_t* h_raw, const uint8_t* d_raw, s
 // Every rank passes the container; rank 0 receives the decompressed bytes.
 Bytes decompress_dist(const Dist& d, const uint8_t* blob, size_t n, const std::string& pub_model_path,
                       const CallOptions& opt = {});
+// same, rank 0's output left in device memory (nullptr on other ranks)
+uint8_t* decompress_dist_to_device(const Dist& d, const uint8_t* blob, size_t n,
+                                   const std::string& pub_model_path, size_t* out_len,
+                                   const CallOptions& opt = {});
+
+// chunk count compress() writes for this input (plan_chunks over the token
+// count of the canonical stream); host-only
+size_t planned_chunks(const uint8_t* raw, size_t n, const Config& cfg);
 
 // host buffers in / out
 Bytes compress(const uint8_t* raw, size_t n, const Config& cfg, const CallOptions& opt = {});
@@ -85,8 +94,11 @@ struct ChunkJob {
   uint64_t n_tokens = 0;
   Bytes inbound;
 };
+// `priv_model`: PMKW bytes of the private model (flags & 2), as shipped in a
+// container (ChunkCodeSpec::priv, pipeline.hpp:69-78).
 std::vector<Bytes> encode_chunks(const std::vector<ChunkJob>& jobs, uint8_t flags,
-                                 const std::string& pub_model_path, uint32_t k, uint32_t t,
+                                 const std::string& pub_model_path, const Bytes& priv_model,
+                                 uint32_t k, uint32_t t,
                                  uint32_t bs, uint32_t scale, uint64_t dm_seed, int device,
                                  const CallOptions& opt = {});
 

@@ -392,14 +392,7 @@ int launch_bigru_predict(const BiGruP& p, const uint32_t* ctx, int64_t ctx_cs, f
   const int ngroups = (p.R + kRPW - 1) / kRPW;
   const dim3 rgrid2(unsigned(2 * ((ngroups + kRecWarps - 1) / kRecWarps)), max_active);
   const bool fuse = p.Hs == kFuseHs;
-  if (fuse) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_bigru_rec_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(kFuseSmem));
-      attr = true;
-    }
-  }
+  if (fuse) ensure_smem(reinterpret_cast<const void*>(k_bigru_rec_fused), kFuseSmem);
   for (int l = 0; l < p.layers; ++l) {
     const bool last = l == p.layers - 1;
     float* f = last ? fin : nullptr;

@@ -330,6 +330,9 @@ __device__ __forceinline__ uint8_t dec_byte(const uint8_t* in, uint64_t len, uin
 
 // exact floor(code / rb) clamped to 65535 (coder.cpp:144-146)
 __device__ __forceinline__ uint32_t dec_target(uint64_t code, uint64_t rb) {
+  // rb < 2^48, so rb * 2^16 cannot overflow: a (corrupt) code at or above it
+  // clamps at once instead of stepping q up one at a time
+  if (code >= (rb << 16)) return kTotal - 1;
   uint64_t q = uint64_t(double(code) / double(rb));
   if (q > kTotal) q = kTotal;
   while (q > 0 && (__umul64hi(q, rb) != 0 || q * rb > code)) --q;

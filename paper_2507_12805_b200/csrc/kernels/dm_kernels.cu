@@ -288,13 +288,7 @@ void gemm_launch(const GemmP& p, const TickDesc* td, int max_active, cudaStream_
   dim3 grid((p.N + TX * TN - 1) / (TX * TN), (Mx + TY * TM - 1) / (TY * TM), max_active * np);
   constexpr int smem = STAGES * BK * (TY * TM + 4 + TX * TN + 4) * int(sizeof(float));
   auto* kern = k_gemm_tiled<AT, BT, TM, TN, BK, STAGES, TX, TY>;
-  if constexpr (smem > 48 * 1024) {
-    static bool attr = false;  // per instantiation, as for the other opt-in kernels
-    if (!attr) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr = true;
-    }
-  }
+  if constexpr (smem > 48 * 1024) ensure_smem(reinterpret_cast<const void*>(kern), smem);
   launch_pdl(kern, dim3(grid), dim3(TX * TY), smem, st, p, td);
 }
 
@@ -1448,12 +1442,7 @@ static void launch_sorted_emb(const uint32_t* ctx, int64_t ctx_cs, const float* 
                               const float* dxl, int64_t dxl_cs, float* grads, int64_t g_cs,
                               int64_t off_emb, DmDims d, const TickDesc* td, int max_active,
                               cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_emb_bwd_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(kSortSmem));
-    attr = true;
-  }
+  ensure_smem(reinterpret_cast<const void*>(k_emb_bwd_sorted), kSortSmem);
   // split the vocabulary over several blocks per chunk while chunks alone
   // cannot fill the chip (each block re-sorts; the gather and walk split)
   const int groups = std::max(1, std::min(std::min(8, d.V), 148 / std::max(1, max_active)));
@@ -1620,20 +1609,18 @@ void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int m
     const NtP& p = probs[i];
     vec = vec && p.K % 4 == 0 && p.ldb % 4 == 0 && p.b_cs % 4 == 0 && al(p.B);
   }
-  static bool attr_set = false;
-  if (!attr_set) {
-#define PMKLC_NT_ATTR(V, R, S, K) \
-  cudaFuncSetAttribute(k_gemm_nt<V, R, S, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                       int(kNwWarps * nw_warp_floats(R, S, K) * sizeof(float)))
+  {
+#define PMKLC_NT_ATTR(V, R, S, K)                                        \
+  ensure_smem(reinterpret_cast<const void*>(k_gemm_nt<V, R, S, K>), \
+              kNwWarps * nw_warp_floats(R, S, K) * sizeof(float))
     PMKLC_NT_ATTR(true, 8, PMKLC_NT8_S, PMKLC_NT8_BK); PMKLC_NT_ATTR(false, 8, PMKLC_NT8_S, PMKLC_NT8_BK); PMKLC_NT_ATTR(true, 4, 3, 32);
     PMKLC_NT_ATTR(false, 4, 3, 32); PMKLC_NT_ATTR(true, 2, 3, 32); PMKLC_NT_ATTR(false, 2, 3, 32);
     PMKLC_NT_ATTR(true, 2, 6, 64); PMKLC_NT_ATTR(false, 2, 6, 64);
-    cudaFuncSetAttribute(k_gemm_nt_r1<true, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(kNwWarps * nw_warp_floats(1, 6, 64) * sizeof(float)));
-    cudaFuncSetAttribute(k_gemm_nt_r1<false, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(kNwWarps * nw_warp_floats(1, 6, 64) * sizeof(float)));
+    ensure_smem(reinterpret_cast<const void*>(k_gemm_nt_r1<true, 6>),
+                kNwWarps * nw_warp_floats(1, 6, 64) * sizeof(float));
+    ensure_smem(reinterpret_cast<const void*>(k_gemm_nt_r1<false, 6>),
+                kNwWarps * nw_warp_floats(1, 6, 64) * sizeof(float));
 #undef PMKLC_NT_ATTR
-    attr_set = true;
   }
   auto build = [&](int rpt, NtBatch& nb) {
     nb.n = nprob;
@@ -1713,11 +1700,7 @@ void launch_attn_fwd(const float* q, const float* k, const float* v, float* wts,
   if (max_active <= 0) return;
   const size_t smem = attn_row_smem(d);
   if (d.NH <= 8 && d.H % 4 == 0 && smem <= 200 * 1024) {
-    static size_t attr = 0;
-    if (smem > attr) {
-      cudaFuncSetAttribute(k_attn_fwd_row, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      attr = smem;
-    }
+    ensure_smem(reinterpret_cast<const void*>(k_attn_fwd_row), smem);
     launch_pdl(k_attn_fwd_row, dim3(dim3(d.R, max_active)), dim3(kRowThreads), smem, st, q, k, v, wts, cx, cs_q, cs_kv,
                                                                       cs_w, d, inv, td);
     return;
@@ -1739,11 +1722,7 @@ bool launch_attn_bwd(const float* q, const float* k, const float* v, const float
     const bool fuse = fx.dx && d.NH * 32 == kRowThreads && d.E % 8 == 0 &&
                       base + extra <= 200 * 1024;
     const size_t smem = base + (fuse ? extra : 0);
-    static size_t attr = 0;
-    if (smem > attr) {
-      cudaFuncSetAttribute(k_attn_bwd_row, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      attr = smem;
-    }
+    ensure_smem(reinterpret_cast<const void*>(k_attn_bwd_row), smem);
     AttnDx f = fx;
     if (!fuse) f.dx = nullptr;
     launch_pdl(k_attn_bwd_row, dim3(dim3(d.R, max_active)), dim3(kRowThreads), smem, st, 

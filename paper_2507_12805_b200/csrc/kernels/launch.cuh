@@ -7,6 +7,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
 #include <utility>
 
 namespace pmklc_b200 {
@@ -41,6 +43,24 @@ inline int stream_priority(cudaStream_t st) {
     prio = p;
   }
   return prio;
+}
+
+// Opt-in dynamic shared memory above 48 KB. The attribute belongs to the
+// current device's context, so it is raised once per (kernel, device) -- a
+// process that drives a second device gets its own opt-in -- under a lock
+// (entry points are reentrant across threads). A failed call is not cached
+// and leaves the error for the launch check to report.
+inline void ensure_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{kernel, dev}];
+  if (bytes <= have) return;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)) ==
+      cudaSuccess)
+    have = bytes;
 }
 
 template <typename... KArgs, typename... Args>

@@ -195,6 +195,77 @@ class Checker:
         return self._take(out, n.value)
 
 
+    def fnv(self, b: bytes) -> int:
+        """FNV-1a-64 (bytes.hpp:17-24) of a byte string."""
+        f = self._f("fnv1a64")
+        f.restype = C.c_uint64
+        return int(f(b, C.c_size_t(len(b))))
+
+    def synth(self, kind: str, n: int, seed: int, extra: int = 0) -> bytes:
+        """Seeded benchmark inputs (the generators of host/synth.cpp, built
+        into the checker library): markov3 | uniform | genome | species."""
+        buf = (C.c_uint8 * max(n, 1))()
+        f = self._f("synth_" + kind)
+        if kind == "genome":
+            f(buf, C.c_uint64(n), C.c_uint64(seed), C.c_uint32(extra or 10))
+        elif kind == "species":
+            f(buf, C.c_uint64(n), C.c_uint64(seed), C.c_uint64(extra))
+        else:
+            f(buf, C.c_uint64(n), C.c_uint64(seed))
+        return bytes(buf)[:n]
+
+    def replay_chunk(self, tokens, flags, k, t, bs, scale, dm_seed, pub_path=None, priv=b"",
+                     inbound=b"", snap_at=0, stop_at=0):
+        """ChunkWorker replay (reference classes): (payload, snapshot). The
+        snapshot is taken after batch step snap_at (0: after the last step
+        run); the run stops after stop_at batch steps (0: all); the payload
+        is empty unless the chunk ran to completion."""
+        import numpy as np
+        tokens = np.ascontiguousarray(tokens, dtype=np.uint32)
+        pay = C.POINTER(C.c_uint8)()
+        pn = C.c_size_t()
+        sn = C.POINTER(C.c_uint8)()
+        snn = C.c_size_t()
+        self._check(self._f("replay_chunk")(
+            tokens.ctypes.data_as(C.c_void_p), C.c_uint64(len(tokens)), flags,
+            pub_path.encode() if pub_path else None, priv or None, C.c_size_t(len(priv)), k, t,
+            bs, scale, C.c_uint64(dm_seed), inbound or None, C.c_size_t(len(inbound)),
+            C.c_uint64(snap_at), C.c_uint64(stop_at), C.byref(pay), C.byref(pn), C.byref(sn),
+            C.byref(snn)))
+        return self._take(pay, pn.value), self._take(sn, snn.value)
+
+    def encode_chunk_standalone(self, tokens, flags, k, t, bs, scale, dm_seed, pub_path=None,
+                                priv=b"", inbound=b"") -> bytes:
+        """pmklc::encode_chunk_standalone (pipeline.cpp:298-301), the reference's own hook."""
+        import numpy as np
+        tokens = np.ascontiguousarray(tokens, dtype=np.uint32)
+        out = C.POINTER(C.c_uint8)()
+        n = C.c_size_t()
+        self._check(self._f("encode_chunk_standalone_priv")(
+            tokens.ctypes.data_as(C.c_void_p), C.c_uint64(len(tokens)), flags,
+            pub_path.encode() if pub_path else None, priv or None, C.c_size_t(len(priv)), k, t,
+            bs, scale, C.c_uint64(dm_seed), inbound or None, C.c_size_t(len(inbound)),
+            C.byref(out), C.byref(n)))
+        return self._take(out, n.value)
+
+
+def parse_container(blob: bytes):
+    """Header fields and per-chunk (token_start, token_len, payload_off,
+    payload_len, trailer_len) of a PMKL container (container.cpp:41-88), plus
+    the SPrM blob."""
+    import struct
+    (magic, ver, flags, s, k, t, bs, myriad, dm_seed, sprm_seed, fp, olen,
+     nch) = struct.unpack_from("<4sBBBBHIHQQQQI", blob, 0)
+    assert magic == b"PMKL"
+    chunks = [struct.unpack_from("<QQQQI", blob, 52 + 36 * i) for i in range(nch)]
+    at = 52 + 36 * nch
+    plen = struct.unpack_from("<Q", blob, at)[0]
+    priv = blob[at + 8: at + 8 + plen]
+    return {"flags": flags, "s": s, "k": k, "t": t, "bs": bs, "myriad": myriad,
+            "dm_seed": dm_seed, "sprm_seed": sprm_seed, "pub_fingerprint": fp,
+            "original_len": olen, "chunks": chunks, "priv": priv}
+
+
 def ref() -> Checker:
     return Checker(REF_SO, "pmref_")
 

@@ -388,3 +388,81 @@ def test_sprm_prepass_default_widths(P, checker):
     blob = P.compress(raw, cfg)
     assert blob == checker.compress(raw, O.make_cfg(**kw))
     assert P.decompress(blob) == raw
+
+
+def test_encode_chunks_with_private_model(P, checker):
+    # ChunkCodeSpec::priv (pipeline.hpp:69-78): recode the chunks of a flags-6
+    # container from their recorded inbound snapshots with the container's own
+    # private model, on the GPU and on the reference's encode_chunk_standalone
+    raw = P.synth("markov3", 120000, 64)
+    kw = dict(t=8, bs=32, scale=16, workers=3, smp=0.3)
+    st = P.PipelineStats()
+    blob = P.compress(raw, P.CompressConfig(**_cfgs(kw), selector_threshold=0), st)
+    assert blob == checker.compress(raw, O.make_cfg(threshold=0, **kw))
+    h = O.parse_container(blob)
+    assert h["flags"] == 6 and h["priv"]
+    tok, _ = checker.skmer_encode(codes_of(raw), 3, 3)
+    lens = [(tl // 32) * 32 for (_, tl, _, _, _) in h["chunks"]]
+    ctok = np.concatenate([tok[ts:ts + n] for (ts, _, _, _, _), n in zip(h["chunks"], lens)])
+    inbound = [w.snapshot_recv_bytes for w in st.workers]
+    assert inbound[0] == b"" and all(inbound[1:])
+    got = P.encode_chunks(ctok, lens, inbound, 6, 3, 8, 32, 16, h["dm_seed"], priv_model=h["priv"])
+    off = 0
+    for i, ((_, _, po, pl, _), n) in enumerate(zip(h["chunks"], lens)):
+        assert got[i] == blob[po:po + pl], i
+        want = checker.encode_chunk_standalone(ctok[off:off + n], 6, 3, 8, 32, 16, h["dm_seed"],
+                                               priv=h["priv"], inbound=inbound[i])
+        assert want == got[i], i
+        off += n
+    with pytest.raises(P.PmklcError) as e:
+        P.encode_chunks(ctok[:lens[0]], lens[:1], [b""], 6, 3, 8, 32, 16, h["dm_seed"])
+    assert e.value.errc == "ConfigInvalid"
+
+
+@pytest.mark.parametrize("kw", [dict(t=512, bs=8, scale=4), dict(t=160, bs=8, scale=1)])
+def test_long_context_attention(P, checker, kw):
+    # contexts long enough that K/V no longer fit the row kernels' shared
+    # memory: the long-context attention forward/backward kernels run
+    raw = P.synth("markov3", 3 * 8 * (kw["t"] + 12) + 9, 71)
+    blob = P.compress(raw, P.CompressConfig(**kw))
+    assert blob == checker.compress(raw, O.make_cfg(**kw))
+    assert P.decompress(blob) == raw
+
+
+def test_stats_inbound_bytes(P, checker):
+    # WorkerStats::snapshot_recv_bytes (pipeline.hpp:32): exported per chunk,
+    # hashing to the reference's snapshot_recv_hash, on both ends
+    raw = P.synth("markov3", 200000, 31)
+    kw = dict(t=8, bs=32, scale=16, workers=4, smp=0.3)
+    st, dst = P.PipelineStats(), P.PipelineStats()
+    blob = P.compress(raw, P.CompressConfig(**_cfgs(kw)), st)
+    _, wst = checker.compress(raw, O.make_cfg(**kw), with_stats=True)
+    assert P.decompress(blob, stats=dst) == raw
+    for a, b, d in zip(st.workers, wst, dst.workers):
+        assert O.fnv1a64(a.snapshot_recv_bytes) == b.snapshot_recv_hash if a.snapshot_recv_bytes \
+            else b.snapshot_recv_hash == 0
+        assert d.snapshot_recv_bytes == a.snapshot_recv_bytes
+    assert P.chunk_count(raw, P.CompressConfig(**_cfgs(kw))) == len(st.workers) == 4
+
+
+def test_run_benchmark_csv_and_fault(P, tmp_path):
+    # run_benchmark (bench.cpp:67-114) as test_metrics.cpp:80-140 drives it
+    a, b, csv = tmp_path / "pmklc_bench_a.seq", tmp_path / "pmklc_bench_b.seq", tmp_path / "r.csv"
+    a.write_bytes(P.synth("uniform", 2500, 41))
+    b.write_bytes(P.synth("genome", 3200, 42, 2) + b"\n>chr\nNNacgt\n")
+    cfg = P.CompressConfig(s=2, k=2, t=4, bs=16, scale=16, selector_threshold=1 << 40)
+    rows, rep = P.run_benchmark([str(a), str(b)], cfg, str(csv))
+    assert [r.name for r in rows] == ["pmklc_bench_a.seq", "pmklc_bench_b.seq"]
+    for r in rows:
+        assert r.verified and r.source_bytes > 0 and r.compressed_bytes > 0 and r.ct_s > 0
+        assert r.cr == pytest.approx(r.compressed_bytes / r.source_bytes * 8.0)
+        assert r.thp > 0
+    assert rep.mean_cr == pytest.approx((rows[0].cr + rows[1].cr) / 2)
+    assert rep.crp_percent == pytest.approx(P.robustness([rows[0].cr, rows[1].cr]))
+    assert rep.peak_mem_bytes > 0 and rep.peak_device_bytes > 0
+    text = csv.read_text()
+    assert text.startswith("dataset,source_bytes,compressed_bytes,ct_s,dt_s,cr_bits_per_base,"
+                           "thp_bytes_per_s,verified\n")
+    assert text.count("\n") == 4 and "AGGREGATE" in text and ",true\n" in text
+    rows, rep = P.run_benchmark([str(a)], cfg, "", fault_flip_mid=True)
+    assert not rows[0].verified and rep.mean_cr == 0.0 and rep.crp_percent == 0.0
