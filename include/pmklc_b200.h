@@ -78,6 +78,8 @@ typedef struct pmklc_timing {  /* CUDA-event times of the last call, ms */
   uint64_t hot_launches, hot_units;
   double hot_flops_per_unit;
   double sprm_ms; /* SPrM pre-pass (training.cpp:8-83) inside compress, ms */
+  uint64_t slots;          /* state/tape slots held (peak chunks in flight)   */
+  uint64_t dev_peak_bytes; /* peak device bytes of the call's buffers         */
 } pmklc_timing;
 
 /* CompressConfig{} defaults: s=k=3, t=32, bs=320, workers=1, threshold 5e8,
@@ -155,6 +157,13 @@ int pmklc_plan_chunks(uint64_t m, uint32_t workers, uint32_t bs, uint32_t t, uin
 int pmklc_schedule(const uint64_t* lens, size_t n_chunks, uint32_t bs, uint32_t t,
                    uint16_t smp_per_myriad, int64_t* offset, int64_t* src, uint64_t* src_steps,
                    uint64_t* model_steps, int64_t* ticks);
+
+/* host logic: the state/tape slot of every chunk (assign_slots: device memory
+ * by chunks in flight, not by chunk count) on `rank` of `world` (1 = single
+ * GPU); slot[c] = -1 for chunks that never step or live on another rank */
+int pmklc_schedule_slots(const uint64_t* lens, size_t n_chunks, uint32_t bs, uint32_t t,
+                         uint16_t smp_per_myriad, int32_t rank, int32_t world, int32_t* slot,
+                         int32_t* n_slots);
 
 /* ---- PMKLC-M across GPUs (one process per GPU) -------------------------
  * Chunk c runs on rank c % world; an SMP handoff between chunks on different

@@ -87,7 +87,8 @@ class Timing(C.Structure):
                 ("ticks", C.c_uint64), ("kernel_launches", C.c_uint64), ("chunks", C.c_uint64),
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
                 ("hot_ms", C.c_double), ("hot_launches", C.c_uint64), ("hot_units", C.c_uint64),
-                ("hot_flops_per_unit", C.c_double), ("sprm_ms", C.c_double)]
+                ("hot_flops_per_unit", C.c_double), ("sprm_ms", C.c_double),
+                ("slots", C.c_uint64), ("dev_peak_bytes", C.c_uint64)]
 
 
 # Every symbol include/pmklc_b200.h declares (checked by tests/test_host.py).
@@ -102,7 +103,7 @@ EXPORTS = [
     "pmklc_decompress_dist", "pmklc_dist_plan", "pmklc_stats_release", "pmklc_chunk_count",
     "pmklc_container_chunks", "pmklc_decompress_dist_to_device", "pmklc_compression_ratio",
     "pmklc_throughput", "pmklc_robustness", "pmklc_block_ratios", "pmklc_run_benchmark",
-    "pmklc_fnv1a64", "pmklc_cfg_validate",
+    "pmklc_fnv1a64", "pmklc_cfg_validate", "pmklc_schedule_slots",
 ]
 
 _lib = None
@@ -334,6 +335,18 @@ def schedule(lens: Sequence[int], bs: int, t: int, smp_per_myriad: int):
     _check(lib().pmklc_schedule(L, C.c_size_t(nc), bs, t, C.c_uint16(smp_per_myriad), off, src, ss,
                                 ms, C.byref(ticks)))
     return list(off), list(src), list(ss), list(ms), ticks.value
+
+
+def schedule_slots(lens: Sequence[int], bs: int, t: int, smp_per_myriad: int, rank: int = 0,
+                   world: int = 1):
+    """State/tape slot per chunk (-1: never steps / other rank) and the slot count."""
+    nc = len(lens)
+    L = (C.c_uint64 * max(nc, 1))(*lens)
+    sl = (C.c_int32 * max(nc, 1))()
+    ns = C.c_int32()
+    _check(lib().pmklc_schedule_slots(L, C.c_size_t(nc), bs, t, C.c_uint16(smp_per_myriad), rank,
+                                      world, sl, C.byref(ns)))
+    return list(sl[:nc]), ns.value
 
 
 def synth(kind: str, n: int, seed: int, extra: int = 0) -> bytes:

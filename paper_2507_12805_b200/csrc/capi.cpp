@@ -82,7 +82,8 @@ void copy_timing(const Timing& t, pmklc_timing* out) {
   *out = pmklc_timing{t.total_ms,  t.h2d_ms,       t.tokenize_ms,     t.warmup_ms,
                       t.model_ms,  t.d2h_ms,       t.ticks,           t.kernel_launches,
                       t.chunks,    t.h2d_bytes,    t.d2h_bytes,       t.hot_ms,
-                      t.hot_launches, t.hot_units, t.hot_flops_per_unit, t.sprm_ms};
+                      t.hot_launches, t.hot_units, t.hot_flops_per_unit, t.sprm_ms,
+                      t.slots,     t.dev_peak_bytes};
 }
 
 int do_compress(const uint8_t* h, const uint8_t* d, size_t n, const pmklc_cfg* c, uint8_t** out,
@@ -273,6 +274,33 @@ int pmklc_schedule(const uint64_t* lens, size_t n, uint32_t bs, uint32_t t, uint
       model_steps[i] = sc.M[i];
     }
     *ticks = sc.ticks;
+  });
+}
+
+int pmklc_schedule_slots(const uint64_t* lens, size_t n, uint32_t bs, uint32_t t, uint16_t myriad,
+                         int32_t rank, int32_t world, int32_t* slot, int32_t* n_slots) {
+  return guard([&] {
+    if (world < 1 || rank < 0 || rank >= world) raise(errc::config_invalid, "rank/world");
+    Plan p;
+    p.bs = bs;
+    p.t = t;
+    p.myriad = myriad;
+    uint64_t s = 0;
+    for (size_t i = 0; i < n; ++i) {
+      p.start.push_back(s);
+      p.len.push_back(lens[i]);
+      s += lens[i];
+    }
+    const Schedule sc = make_schedule(p, myriad > 0);
+    Slots sl;
+    if (world > 1) {
+      const RankPlan rp = plan_rank(sc, rank, world);
+      sl = assign_slots(rp.local, &rp.mine);
+    } else {
+      sl = assign_slots(sc);
+    }
+    for (size_t i = 0; i < n; ++i) slot[i] = sl.of[i];
+    *n_slots = sl.count;
   });
 }
 

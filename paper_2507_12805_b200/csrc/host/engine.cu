@@ -45,6 +45,8 @@ void configure_pool(int device) {
 }
 
 thread_local cudaStream_t g_alloc_stream = nullptr;  // the calling engine's stream
+// device bytes held by this thread's engine buffers (current, peak of the call)
+thread_local uint64_t g_dev_bytes = 0, g_dev_peak = 0;
 
 template <class T>
 struct DBuf {
@@ -57,10 +59,17 @@ struct DBuf {
     free();
     n = count;
     st = g_alloc_stream;
-    if (count) CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), st));
+    if (count) {
+      CK(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), st));
+      g_dev_bytes += count * sizeof(T);
+      g_dev_peak = std::max(g_dev_peak, g_dev_bytes);
+    }
   }
   void free() {
-    if (p) cudaFreeAsync(p, st);
+    if (p) {
+      cudaFreeAsync(p, st);
+      g_dev_bytes -= n * sizeof(T);
+    }
     p = nullptr;
     n = 0;
   }
@@ -294,6 +303,7 @@ struct ChunkRun {
   uint64_t launches = 0;
   double warm_ms = 0, model_ms = 0;
   HotTimer hot{};  // in-situ timing of the SPuM fused recurrence
+  uint32_t slots = 0;  // state/tape slots (peak chunks in flight incl. pending sources)
 };
 
 // Algorithmic work of one chunk-launch of k_bigru_rec_fused: R rows x 2
@@ -351,43 +361,52 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   d_off.upload(sch.offset.data(), W, st);
   const ChunkGeo geo{d_start.p, d_L.p, d_off.p};
 
-  // ---- model state slots (one per chunk)
-  DBuf<float> w(W * P), g(W * P), m(W * P), v(W * P);
-  DBuf<AdamScalars> sc(W);
+  // ---- slots: model state and tapes per chunk in flight (assign_slots); with
+  // several ranks only this rank's chunks hold one
+  const Schedule& lsch = run.rplan ? run.rplan->local : sch;
+  const Slots slots = assign_slots(lsch, run.rplan ? &run.rplan->mine : nullptr);
+  const size_t S = size_t(slots.count);
+  run.slots = uint32_t(S);
+  auto slot_of = [&](int64_t c) { return int64_t(slots.of[size_t(c)]); };
+
+  // ---- model state slots: chunks starting from the seeded init (or a given
+  // inbound state) all start at tick 0 and are written here; the others get
+  // their state by the SMP handoff copy at their first tick
+  DBuf<float> w(S * P), g(S * P), m(S * P), v(S * P);
+  DBuf<AdamScalars> sc(std::max<size_t>(S, 1));
   g.zero(st);
   {
     const std::vector<float> seeded = lay.seeded(run.dm_seed);
     DBuf<float> init(P);
     init.upload(seeded.data(), P, st);
-    std::vector<AdamScalars> hsc(W);
+    std::vector<AdamScalars> hsc(std::max<size_t>(S, 1), AdamScalars{0, 1.0f, 1.0f, 0.0f, 0.0f, {0, 0}});
     for (size_t c = 0; c < W; ++c) {
+      const int64_t sl = slots.of[c];
+      if (sl < 0 || sch.src[c] >= 0) continue;
       const DmState* s0 = run.init_state.empty() ? nullptr : run.init_state[c];
-      hsc[c] = AdamScalars{0, 1.0f, 1.0f, 0.0f, 0.0f, {0, 0}};
       if (s0) {
-        w.upload(s0->w.data(), P, st, c * P);
-        m.upload(s0->m.data(), P, st, c * P);
-        v.upload(s0->v.data(), P, st, c * P);
-        hsc[c].step = s0->step;
-        hsc[c].b1p = s0->b1p;
-        hsc[c].b2p = s0->b2p;
+        w.upload(s0->w.data(), P, st, sl * P);
+        m.upload(s0->m.data(), P, st, sl * P);
+        v.upload(s0->v.data(), P, st, sl * P);
+        hsc[size_t(sl)].step = s0->step;
+        hsc[size_t(sl)].b1p = s0->b1p;
+        hsc[size_t(sl)].b2p = s0->b2p;
       } else {
-        CK(cudaMemcpyAsync(w.p + c * P, init.p, P * 4, cudaMemcpyDeviceToDevice, st));
-        CK(cudaMemsetAsync(m.p + c * P, 0, P * 4, st));
-        CK(cudaMemsetAsync(v.p + c * P, 0, P * 4, st));
+        CK(cudaMemcpyAsync(w.p + sl * P, init.p, P * 4, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemsetAsync(m.p + sl * P, 0, P * 4, st));
+        CK(cudaMemsetAsync(v.p + sl * P, 0, P * 4, st));
       }
     }
-    sc.upload(hsc.data(), W, st);
+    sc.upload(hsc.data(), hsc.size(), st);
     CK(cudaStreamSynchronize(st));
   }
 
-  // ---- tapes (one per chunk that ever steps)
+  // ---- tapes (one per slot)
   const int64_t RT = int64_t(R) * T;
   const int64_t s_ctx = int64_t(R) * T, s_x = int64_t(R) * T * E, s_kv = int64_t(R) * T * H,
                 s_rh = int64_t(R) * H, s_w = int64_t(R) * NH * T, s_rf = int64_t(R) * F,
                 s_rv = int64_t(R) * V, s_cum = int64_t(R) * (V + 1), s_re = int64_t(R) * E;
-  uint32_t n_step_chunks = 0;
-  for (size_t c = 0; c < W; ++c) n_step_chunks += sch.M[c] ? 1 : 0;
-  const size_t TW = n_step_chunks ? W : 0;  // tapes indexed by chunk id
+  const size_t TW = S;  // tapes indexed by slot
   DBuf<uint32_t> ctx(TW * s_ctx), freq(TW * s_rv), cum(TW * s_cum);
   DBuf<float> x(TW * s_x), kk(TW * s_kv), vv(TW * s_kv), q(TW * s_rh), wts(TW * s_w),
       cx(TW * s_rh), ao(TW * s_rh), pre(TW * s_rf), fo(TW * s_rh), lm(TW * s_rv),
@@ -434,14 +453,24 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   DBuf<double> warm_loss(W);
   warm_loss.zero(st);
 
-  // ---- schedule lists (CSR per tick) + the device tick descriptor; with
-  // several ranks the lists are this rank's (its chunks, local handoffs)
-  const Schedule& lsch = run.rplan ? run.rplan->local : sch;
-  DBuf<int> d_act(std::max<size_t>(lsch.act.size(), 1));
-  if (!lsch.act.empty()) d_act.upload(reinterpret_cast<const int*>(lsch.act.data()), lsch.act.size(), st);
-  DBuf<int2> d_hand(std::max<size_t>(lsch.hand.size() / 2, 1));
-  if (!lsch.hand.empty())
-    d_hand.upload(reinterpret_cast<const int2*>(lsch.hand.data()), lsch.hand.size() / 2, st);
+  // ---- schedule lists (CSR per tick: slots, chunk ids, slot handoff pairs)
+  // + the device tick descriptor; with several ranks the lists are this
+  // rank's (its chunks, local handoffs)
+  std::vector<int> act_slot(lsch.act.size()), act_chunk(lsch.act.size());
+  for (size_t i = 0; i < lsch.act.size(); ++i) {
+    act_chunk[i] = int(lsch.act[i]);
+    act_slot[i] = int(slot_of(lsch.act[i]));
+  }
+  std::vector<int> hand_slot(lsch.hand.size());
+  for (size_t i = 0; i < lsch.hand.size(); ++i) hand_slot[i] = int(slot_of(lsch.hand[i]));
+  DBuf<int> d_act(std::max<size_t>(act_slot.size(), 1)), d_act_chunk(std::max<size_t>(act_slot.size(), 1));
+  if (!act_slot.empty()) {
+    d_act.upload(act_slot.data(), act_slot.size(), st);
+    d_act_chunk.upload(act_chunk.data(), act_chunk.size(), st);
+  }
+  DBuf<int2> d_hand(std::max<size_t>(hand_slot.size() / 2, 1));
+  if (!hand_slot.empty())
+    d_hand.upload(reinterpret_cast<const int2*>(hand_slot.data()), hand_slot.size() / 2, st);
   DBuf<uint32_t> d_act_ptr(lsch.act_ptr.size()), d_hand_ptr(lsch.hand_ptr.size());
   d_act_ptr.upload(lsch.act_ptr.data(), lsch.act_ptr.size(), st);
   d_hand_ptr.upload(lsch.hand_ptr.data(), lsch.hand_ptr.size(), st);
@@ -470,7 +499,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
       s.m.assign(lay.total, 0.0f);
       s.v.assign(lay.total, 0.0f);
     } else {
-      s = fetch_state(lay, w.p, m.p, v.p, sc.p, src, st);
+      s = fetch_state(lay, w.p, m.p, v.p, sc.p, slot_of(src), st);
     }
     Bytes b = snapshot_bytes(lay, s);
     snap_hash[{src, steps}] = fnv1a64(b);
@@ -537,7 +566,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   DBuf<uint32_t> ctx_next;
   if (statics) ctx_next.alloc(TW * s_ctx);
   auto predict_next = [&](cudaStream_t s2) {
-    launch_tick_peek(d_td.p, d_td_next.p, d_act_ptr.p, d_act.p, sch.ticks, s2);
+    launch_tick_peek(d_td.p, d_td_next.p, d_act_ptr.p, d_act.p, d_act_chunk.p, sch.ticks, s2);
     launch_ctx_gather(d_tokens, geo, ctx_next.p, s_ctx, dd, d_td_next.p, na, s2);
     run.launches += 2;
     if (run.flags & 1)
@@ -552,7 +581,8 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     side.rewind();
     pred.rewind();
     cod.rewind();
-    launch_tick_advance(d_td.p, d_act_ptr.p, d_act.p, d_hand_ptr.p, d_hand.p, sch.ticks, st);
+    launch_tick_advance(d_td.p, d_act_ptr.p, d_act.p, d_act_chunk.p, d_hand_ptr.p, d_hand.p,
+                        sch.ticks, st);
     ++run.launches;
     if (nh > 0) {
       launch_state_copy(w.p, m.p, v.p, sc.p, P, P, d_td.p, nh, st);
@@ -618,7 +648,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
       if (sch.M[size_t(pc)] && ms >= 0 && uint64_t(ms) < sch.M[size_t(pc)] &&
           uint64_t(ms) < run.opt->probe_steps) {
         std::vector<float>& pr = *run.opt->probe;
-        CK(cudaMemcpyAsync(pr.data() + uint64_t(ms) * s_rv, probs.p + pc * s_rv, s_rv * 4,
+        CK(cudaMemcpyAsync(pr.data() + uint64_t(ms) * s_rv, probs.p + slot_of(pc) * s_rv, s_rv * 4,
                            cudaMemcpyDeviceToHost, st));
       }
     }
@@ -737,7 +767,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     nck(nccl().GroupStart());
     for (; op_i < ops.size() && ops[op_i].tick == tick; ++op_i) {
       const CommOp& o = ops[op_i];
-      const int64_t c = o.send ? o.src : o.dst;
+      const int64_t c = slot_of(o.send ? o.src : o.dst);
       float* bufs[3] = {w.p + c * P, m.p + c * P, v.p + c * P};
       for (float* b : bufs) {
         if (o.send) nck(nccl().Send(b, size_t(P), ncclFloat32, o.peer, run.comm, st));
@@ -907,7 +937,8 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
     }
   }
   const int Es = int(dims.se), H = int(dims.sh), B = int(dims.sb), V = int(dims.V), T = int(t);
-  if (H > 32) raise(errc::config_invalid, "SPrM pre-pass on the GPU supports sp_hidden <= 32 (scale >= 4)");
+  if (!(H <= 32 || H == 64 || H == 128))
+    raise(errc::config_invalid, "SPrM pre-pass on the GPU supports sp_hidden <= 32, 64 or 128");
   const int64_t P = int64_t(model.total);
   DBuf<float> w(P), g(P), mo(P), vo(P);
   w.upload(model.w.data(), P, st);
@@ -944,41 +975,25 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
     const int64_t rt = int64_t(rows) * T;
     launch_sprm_prep(d_tok, pos.p, sp, ctx.p, X.p, tab.p, st);
     launch_sprm_fwd(sp, ctx.p, tab.p, tape.p, fin.p, st);
-    // head: bact = tanh(bott.b + fin.bott.w); logits = out.b + bact.out.w
-    GemmP g1{};
-    g1.A = fin.p; g1.lda = 2 * H; g1.B = W_(b0); g1.ldb = B; g1.C = bact.p; g1.ldc = B;
-    g1.bias = W_(b0 + 1); g1.M = rows; g1.N = B; g1.K = 2 * H; g1.init = 1;
-    launch_gemm(g1, false, false, td.p, 1, st);
-    launch_tanh_vec(bact.p, int64_t(rows) * B, st);
-    GemmP g2{};
-    g2.A = bact.p; g2.lda = B; g2.B = W_(b0 + 2); g2.ldb = V; g2.C = logits.p; g2.ldc = V;
-    g2.bias = W_(b0 + 3); g2.M = rows; g2.N = V; g2.K = B; g2.init = 1;
-    launch_gemm(g2, false, false, td.p, 1, st);
-    launch_sprm_ce(sp, d_tok, pos.p, logits.p, gg.p, st);
-    // out.backward, tanh', bott.backward (models.cpp:75-86)
+    // head forward, CE gradient and head backward in one launch (models.cpp:67-86,
+    // training.cpp:28-34): bact, g, dbact and dfin
+    launch_sprm_head(sp, d_tok, pos.p, fin.p, W_(b0), W_(b0 + 1), W_(b0 + 2), W_(b0 + 3), bact.p,
+                     gg.p, dbact.p, dfin.p, st);
+    // Branches of the step DAG run on a side stream where nothing on the main
+    // chain reads their results before Adam: the head's weight gradients
+    // (out.backward / bott.backward reductions over rows), then (after BPTT)
+    // the gradient transpose and the 12 weight-gradient reductions, beside
+    // dx -> embedding gradient.
+    side.rewind();
+    side.wait_for(st);
     GemmP g3{};
     g3.A = bact.p; g3.lda = B; g3.B = gg.p; g3.ldb = V; g3.C = G_(b0 + 2); g3.ldc = V;
     g3.M = B; g3.N = V; g3.K = rows; g3.ones_row = 1; g3.init = 2;
-    launch_gemm(g3, true, false, td.p, 1, st);
-    GemmP g4{};
-    g4.A = gg.p; g4.lda = V; g4.B = W_(b0 + 2); g4.ldb = V; g4.C = dbact.p; g4.ldc = B;
-    g4.M = rows; g4.N = B; g4.K = V; g4.init = 0;
-    launch_gemm(g4, false, true, td.p, 1, st);
-    launch_sprm_tanh_grad(dbact.p, bact.p, int64_t(rows) * B, st);
-    // Branches of the step DAG run on a side stream where nothing on the main
-    // chain reads their results before Adam: the bottleneck weight gradient,
-    // then (after BPTT) the gradient transpose and the 12 weight-gradient
-    // reductions, beside dx -> embedding gradient.
-    side.rewind();
-    side.wait_for(st);
+    launch_gemm(g3, true, false, td.p, 1, side.s);
     GemmP g5{};
     g5.A = fin.p; g5.lda = 2 * H; g5.B = dbact.p; g5.ldb = B; g5.C = G_(b0); g5.ldc = B;
     g5.M = 2 * H; g5.N = B; g5.K = rows; g5.ones_row = 1; g5.init = 2;
     launch_gemm(g5, true, false, td.p, 1, side.s);
-    GemmP g6{};
-    g6.A = dbact.p; g6.lda = B; g6.B = W_(b0); g6.ldb = B; g6.C = dfin.p; g6.ldc = 2 * H;
-    g6.M = rows; g6.N = 2 * H; g6.K = B; g6.init = 0;
-    launch_gemm(g6, false, true, td.p, 1, st);
     // backward through time, then the weight-gradient reductions over (t desc, rows asc)
     launch_sprm_bptt(sp, tape.p, dfin.p, Gt.p, st);
     side.wait_for(st);
@@ -1010,7 +1025,7 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
     launch_adam_scalars(sc.p, st);
     launch_adam(w.p, g.p, mo.p, vo.p, 0, P, sc.p, td.p, 1, st);
     launch_pos_advance(pos.p, batch, st);
-    nl += 19;
+    nl += 14;
   };
   const uint64_t nsteps = (m - t + batch - 1) / batch;
   const uint64_t full = (m - t) / batch;
@@ -1022,7 +1037,7 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
     CK(cudaStreamEndCapture(st, &graph));
     CK(cudaGraphInstantiate(&exec, graph, 0));
     for (uint64_t i = 0; i < full; ++i) CK(cudaGraphLaunch(exec, st));
-    nl += 19 * (full - 1);
+    nl += 14 * (full - 1);
     CK(cudaGraphExecDestroy(exec));
     CK(cudaGraphDestroy(graph));
   }
@@ -1044,6 +1059,7 @@ Bytes compress_impl(const uint8_t* h_raw, const uint8_t* d_raw_in, size_t n, con
   CK(cudaSetDevice(cfg.device));
   Stream stream(cfg.device);
   cudaStream_t st = stream.s;
+  g_dev_peak = g_dev_bytes;
   Event t0, t1, t2, t3;
   t0.record(st);
   Rng master(cfg.seed);
@@ -1241,6 +1257,8 @@ Bytes compress_impl(const uint8_t* h_raw, const uint8_t* d_raw_in, size_t n, con
     fill_hot(tm, run);
     tm.h2d_bytes = h2d;
     tm.d2h_bytes = out.size();
+    tm.slots = run.slots;
+    tm.dev_peak_bytes = g_dev_peak;
   }
   return out;
 }
@@ -1253,6 +1271,7 @@ struct DecodeResult {
 void decompress_impl(const uint8_t* blob, size_t n, const std::string& pub_path, int device,
                      const CallOptions& opt, DecodeResult& res, cudaStream_t st,
                      const Dist* dist = nullptr) {
+  g_dev_peak = g_dev_bytes;
   Event t0, t1, t2, t3;
   t0.record(st);
   const Container c = read_container(blob, n);
@@ -1405,6 +1424,8 @@ void decompress_impl(const uint8_t* blob, size_t n, const std::string& pub_path,
     tm.chunks = W;
     fill_hot(tm, run);
     tm.h2d_bytes = n;
+    tm.slots = run.slots;
+    tm.dev_peak_bytes = g_dev_peak;
   }
 }
 

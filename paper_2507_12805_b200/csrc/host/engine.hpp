@@ -40,6 +40,8 @@ struct Timing {
   double hot_ms = 0, hot_flops_per_unit = 0;
   uint64_t hot_launches = 0, hot_units = 0;
   double sprm_ms = 0;  // SPrM pre-pass (compress, flags & 2)
+  uint64_t slots = 0;           // state/tape slots of the chunk engine (chunks in flight)
+  uint64_t dev_peak_bytes = 0;  // peak device bytes the call's buffers held
 };
 
 struct CallOptions {

@@ -1,6 +1,8 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <functional>
+#include <queue>
 
 namespace pmklc_b200 {
 
@@ -132,6 +134,47 @@ RankPlan plan_rank(const Schedule& s, int rank, int world) {
     l.hand_ptr.push_back(uint32_t(l.hand.size() / 2));
   }
   return rp;
+}
+
+Slots assign_slots(const Schedule& s, const std::vector<uint8_t>* mine) {
+  const size_t W = s.L.size();
+  Slots out;
+  out.of.assign(W, -1);
+  std::vector<int64_t> end(W, -1);
+  for (size_t c = 0; c < W; ++c)
+    if (s.M[c] && (!mine || (*mine)[c])) end[c] = s.offset[c] + int64_t(s.M[c]) - 1;
+  for (size_t c = 0; c < W; ++c) {  // handoff sources stay live until the copy
+    const int64_t src = s.src[c];
+    if (src >= 0 && s.M[c] && end[size_t(src)] >= 0)
+      end[size_t(src)] = std::max(end[size_t(src)], s.offset[c]);
+  }
+  std::vector<size_t> order;
+  for (size_t c = 0; c < W; ++c)
+    if (end[c] >= 0) order.push_back(c);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](size_t a, size_t b) { return s.offset[a] < s.offset[b]; });
+  // busy slots keyed by their last tick; a slot is free for an interval
+  // starting strictly after it
+  using E = std::pair<int64_t, int32_t>;
+  std::priority_queue<E, std::vector<E>, std::greater<E>> busy;
+  std::vector<int32_t> free_slots;
+  for (size_t c : order) {
+    while (!busy.empty() && busy.top().first < s.offset[c]) {
+      free_slots.push_back(busy.top().second);
+      busy.pop();
+    }
+    int32_t sl;
+    if (!free_slots.empty()) {
+      std::sort(free_slots.begin(), free_slots.end(), std::greater<int32_t>());
+      sl = free_slots.back();  // lowest free slot: deterministic
+      free_slots.pop_back();
+    } else {
+      sl = out.count++;
+    }
+    out.of[c] = sl;
+    busy.push({end[c], sl});
+  }
+  return out;
 }
 
 }  // namespace pmklc_b200

@@ -65,4 +65,17 @@ struct RankPlan {
 inline int owner_of(size_t chunk, int world) { return int(chunk % size_t(world)); }
 RankPlan plan_rank(const Schedule& s, int rank, int world);
 
+// Device memory by concurrency, not by chunk count: chunk c holds a state /
+// tape slot from its first model tick (where its inbound state is copied in)
+// through its last model tick, extended to the last tick at which its state
+// is the source of a handoff (local or, on the sending rank, remote). Slots
+// are assigned greedily by start tick, so their number is the peak number of
+// live chunks (max_active plus pending handoff sources). Chunks that never
+// step (or are not `mine`) get -1.
+struct Slots {
+  std::vector<int32_t> of;  // per chunk
+  int32_t count = 0;
+};
+Slots assign_slots(const Schedule& s, const std::vector<uint8_t>* mine = nullptr);
+
 }  // namespace pmklc_b200

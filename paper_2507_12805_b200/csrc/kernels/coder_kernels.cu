@@ -219,13 +219,13 @@ __global__ void k_mix_quantize(MixP p, const TickDesc* __restrict__ td) {
 __global__ void k_bc_dlm(BcP p, const TickDesc* __restrict__ td) {
   pdl_wait();
   if (blockIdx.y >= unsigned(td->n_act)) return;
-  const int c = td->act[blockIdx.y];
+  const int c = td->act[blockIdx.y], ch = td->chunk[blockIdx.y];
   const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int R = p.R, V = p.V;
   if (idx >= int64_t(R) * V) return;
   const int r = int(idx / V), i = int(idx % V);
-  const uint64_t jstep = uint64_t(p.t) + uint64_t(p.td->tick - p.geo.offset[c]);
-  const uint32_t tgt = p.tokens[p.geo.start[c] + uint64_t(r) * p.geo.L[c] + jstep];
+  const uint64_t jstep = uint64_t(p.t) + uint64_t(p.td->tick - p.geo.offset[ch]);
+  const uint32_t tgt = p.tokens[p.geo.start[ch] + uint64_t(r) * p.geo.L[ch] + jstep];
   const float a = det_sigmoid(p.w[c * p.p_cs + p.off_alpha]);
   const int64_t o = c * p.cs_p + idx;
   const float pv = p.probs[o];
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(256) k_alpha_step(BcP p, const TickDesc* __res
   pdl_wait();
   __shared__ __align__(16) float buf[2][kAlphaBatch];
   if (blockIdx.x >= unsigned(p.td->n_act)) return;
-  const int c = p.td->act[blockIdx.x];
+  const int c = p.td->act[blockIdx.x], ch = p.td->chunk[blockIdx.x];
   const int64_t n = int64_t(p.R) * p.V;
   const float* terms = p.aterm + c * p.cs_p;
   const int nb = int((n + kAlphaBatch - 1) / kAlphaBatch);
@@ -277,12 +277,12 @@ __global__ void __launch_bounds__(256) k_alpha_step(BcP p, const TickDesc* __res
     }
     __syncthreads();
   }
-  const uint64_t mstep = uint64_t(p.td->tick - p.geo.offset[c]);
-  if (tid == 32 && p.warm_loss && mstep < p.warm_steps[c]) {
+  const uint64_t mstep = uint64_t(p.td->tick - p.geo.offset[ch]);
+  if (tid == 32 && p.warm_loss && mstep < p.warm_steps[ch]) {
     const float* lt = p.lterm + c * p.cs_l;
     float loss = 0.0f;
     for (int r = 0; r < p.R; ++r) loss = fadd(loss, lt[r]);
-    p.warm_loss[c] += double(loss);
+    p.warm_loss[ch] += double(loss);
   }
   if (tid == 0) {
     const int64_t aoff = c * p.p_cs + p.off_alpha;
@@ -430,11 +430,11 @@ __global__ void __launch_bounds__(kCoderWarps * 32) k_range_step(
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wi = blockIdx.x * kCoderWarps + wl;
   if (wi >= td->n_act) return;
-  const int c = td->act[wi];
-  const uint64_t L = geo.L[c], start = geo.start[c];
-  const uint64_t jstep = uint64_t(t) + uint64_t(td->tick - geo.offset[c]);
-  uint8_t* buf = payload + pay_off[c];
-  CoderState s = cs[c];
+  const int c = td->act[wi], ch = td->chunk[wi];  // slot (freq/cum), chunk (codestream)
+  const uint64_t L = geo.L[ch], start = geo.start[ch];
+  const uint64_t jstep = uint64_t(t) + uint64_t(td->tick - geo.offset[ch]);
+  uint8_t* buf = payload + pay_off[ch];
+  CoderState s = cs[ch];
   if (s.err) return;
   const uint32_t* fq = freq + c * cs_f;
   const uint32_t* cm = cum + c * cs_c;
@@ -453,22 +453,22 @@ __global__ void __launch_bounds__(kCoderWarps * 32) k_range_step(
       }
       __syncwarp();
     }
-    if (lane == 0) cs[c] = s;
+    if (lane == 0) cs[ch] = s;
     return;
   }
   const int nq = (V + 1 + 31) / 32;  // cum[0..V] (cum[V] = 2^16) in registers
   if (nq > kMaxQ) {  // large alphabets: scalar path in lane 0
     if (lane == 0) {
       for (int r = 0; r < R && !s.err; ++r) {
-        const uint32_t sym = dec_sym(s.code, s.range, buf, pay_len[c], s.pos, cm + int64_t(r) * (V + 1),
+        const uint32_t sym = dec_sym(s.code, s.range, buf, pay_len[ch], s.pos, cm + int64_t(r) * (V + 1),
                                      fq + int64_t(r) * V, uint32_t(V), s.err);
         tokens[start + uint64_t(r) * L + jstep] = sym;
       }
-      cs[c] = s;
+      cs[ch] = s;
     }
     return;
   }
-  const uint64_t plen = pay_len[c];
+  const uint64_t plen = pay_len[ch];
   uint32_t cur[kMaxQ], nxt[kMaxQ];
 #pragma unroll
   for (int q = 0; q < kMaxQ; ++q) {
@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(kCoderWarps * 32) k_range_step(
 #pragma unroll
     for (int q = 0; q < kMaxQ; ++q) cur[q] = nxt[q];
   }
-  if (lane == 0) cs[c] = s;
+  if (lane == 0) cs[ch] = s;
 }
 
 __global__ void k_range_finish(uint8_t* payload, const uint64_t* pay_off, CoderState* cs, int n) {

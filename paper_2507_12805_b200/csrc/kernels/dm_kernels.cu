@@ -761,16 +761,16 @@ __global__ void k_embed(const uint32_t* __restrict__ tokens, ChunkGeo geo,
   // thread per coded position (r, t): one token gather, all E features
   // (x[j] = emb[tok][j] + pos[t][j], feature-major stores coalesced over rt)
   if (blockIdx.y >= unsigned(td->n_act)) return;
-  const int c = td->act[blockIdx.y];
+  const int c = td->act[blockIdx.y], ch = td->chunk[blockIdx.y];
   const int64_t RT = int64_t(d.R) * d.T;
   const int64_t rt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (rt >= RT) return;
   const int t = int(uint32_t(rt) % uint32_t(d.T)), r = int(uint32_t(rt) / uint32_t(d.T));  // RT < 2^31
-  const uint64_t L = geo.L[c];
-  const uint64_t jstep = uint64_t(d.T) + uint64_t(td->tick - geo.offset[c]);  // coded position
+  const uint64_t L = geo.L[ch];
+  const uint64_t jstep = uint64_t(d.T) + uint64_t(td->tick - geo.offset[ch]);  // coded position
   // tokens are < V = 4^k by construction; the mask only guards memory after a
-  // decode error (slots past a truncated codestream are never written)
-  const uint32_t tok = tokens[geo.start[c] + uint64_t(r) * L + (jstep - d.T) + t] & uint32_t(d.V - 1);
+  // decode error (positions past a truncated codestream are never written)
+  const uint32_t tok = tokens[geo.start[ch] + uint64_t(r) * L + (jstep - d.T) + t] & uint32_t(d.V - 1);
   ctx[c * ctx_cs + rt] = tok;
   const float* P = params + c * p_cs;
   const float* er = P + off_emb + int64_t(tok) * d.E;
@@ -1512,13 +1512,15 @@ __global__ void k_state_copy(float* w, float* m, float* v, AdamScalars* sc, int6
 }
 
 __global__ void k_tick_advance(TickDesc* td, const uint32_t* __restrict__ act_ptr,
-                               const int* __restrict__ act_all, const uint32_t* __restrict__ hand_ptr,
+                               const int* __restrict__ act_all, const int* __restrict__ chunk_all,
+                               const uint32_t* __restrict__ hand_ptr,
                                const int2* __restrict__ hand_all, int64_t ticks) {
   pdl_wait();
   const int64_t t = td->tick + 1;
   td->tick = t;
   if (t < ticks) {
     td->act = act_all + act_ptr[t];
+    td->chunk = chunk_all + act_ptr[t];
     td->n_act = int(act_ptr[t + 1] - act_ptr[t]);
     td->hand = hand_all + hand_ptr[t];
     td->n_hand = int(hand_ptr[t + 1] - hand_ptr[t]);
@@ -1532,7 +1534,7 @@ __global__ void k_tick_advance(TickDesc* td, const uint32_t* __restrict__ act_pt
 // tick tau+1 run inside tick tau's graph (cross-tick pipeline).
 __global__ void k_tick_peek(const TickDesc* __restrict__ cur, TickDesc* next,
                             const uint32_t* __restrict__ act_ptr, const int* __restrict__ act_all,
-                            int64_t ticks) {
+                            const int* __restrict__ chunk_all, int64_t ticks) {
   pdl_wait();
   const int64_t t = cur->tick + 1;
   next->tick = t;
@@ -1540,9 +1542,11 @@ __global__ void k_tick_peek(const TickDesc* __restrict__ cur, TickDesc* next,
   next->n_hand = 0;
   if (t >= 0 && t < ticks) {
     next->act = act_all + act_ptr[t];
+    next->chunk = chunk_all + act_ptr[t];
     next->n_act = int(act_ptr[t + 1] - act_ptr[t]);
   } else {
     next->act = act_all;
+    next->chunk = chunk_all;
     next->n_act = 0;
   }
 }
@@ -1552,21 +1556,21 @@ __global__ void k_ctx_gather(const uint32_t* __restrict__ tokens, ChunkGeo geo, 
                              int64_t ctx_cs, DmDims d, const TickDesc* __restrict__ td) {
   pdl_wait();
   if (blockIdx.y >= unsigned(td->n_act)) return;
-  const int c = td->act[blockIdx.y];
+  const int c = td->act[blockIdx.y], ch = td->chunk[blockIdx.y];
   const int64_t RT = int64_t(d.R) * d.T;
   const int64_t rt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (rt >= RT) return;
   const int t = int(uint32_t(rt) % uint32_t(d.T)), r = int(uint32_t(rt) / uint32_t(d.T));  // RT < 2^31
-  const uint64_t L = geo.L[c];
-  const uint64_t jstep = uint64_t(d.T) + uint64_t(td->tick - geo.offset[c]);
-  ctx[c * ctx_cs + rt] = tokens[geo.start[c] + uint64_t(r) * L + (jstep - d.T) + t] & uint32_t(d.V - 1);
+  const uint64_t L = geo.L[ch];
+  const uint64_t jstep = uint64_t(d.T) + uint64_t(td->tick - geo.offset[ch]);
+  ctx[c * ctx_cs + rt] = tokens[geo.start[ch] + uint64_t(r) * L + (jstep - d.T) + t] & uint32_t(d.V - 1);
 }
 
 }  // namespace
 
 void launch_tick_peek(const TickDesc* cur, TickDesc* next, const uint32_t* act_ptr,
-                      const int* act_all, int64_t ticks, cudaStream_t st) {
-  launch_pdl(k_tick_peek, dim3(1), dim3(1), 0, st, cur, next, act_ptr, act_all, ticks);
+                      const int* act_all, const int* chunk_all, int64_t ticks, cudaStream_t st) {
+  launch_pdl(k_tick_peek, dim3(1), dim3(1), 0, st, cur, next, act_ptr, act_all, chunk_all, ticks);
 }
 void launch_ctx_gather(const uint32_t* tokens, ChunkGeo geo, uint32_t* ctx, int64_t ctx_cs,
                        DmDims d, const TickDesc* td, int max_active, cudaStream_t st) {
@@ -1783,9 +1787,10 @@ void launch_state_copy(float* w, float* m, float* v, AdamScalars* sc, int64_t p_
 }
 
 void launch_tick_advance(TickDesc* td, const uint32_t* act_ptr, const int* act_all,
-                         const uint32_t* hand_ptr, const int2* hand_all, int64_t ticks,
-                         cudaStream_t st) {
-  launch_pdl(k_tick_advance, dim3(1), dim3(1), 0, st, td, act_ptr, act_all, hand_ptr, hand_all, ticks);
+                         const int* chunk_all, const uint32_t* hand_ptr, const int2* hand_all,
+                         int64_t ticks, cudaStream_t st) {
+  launch_pdl(k_tick_advance, dim3(1), dim3(1), 0, st, td, act_ptr, act_all, chunk_all, hand_ptr,
+             hand_all, ticks);
 }
 
 }  // namespace pmklc_b200

@@ -44,22 +44,29 @@ void launch_detokenize_restore(const uint32_t* tokens, uint64_t m, uint32_t s, u
                                uint64_t out_len, int* err, cudaStream_t st);
 
 // ---------------------------------------------------------------- chunk engine
-struct ChunkGeo {      // per-chunk constants, device arrays indexed by chunk id
+struct ChunkGeo {      // per-chunk constants, device arrays indexed by chunk id (TickDesc::chunk)
   const uint64_t* start;   // token offset of the chunk
   const uint64_t* L;       // batch steps (substream length)
   const int64_t* offset;   // tick of the chunk's first model step
 };
 
+// Per-chunk model state and the per-step tapes live in slots (host
+// assign_slots: a chunk holds one from its first model tick until its state
+// is no longer needed), so device memory scales with the number of chunks in
+// flight, not with the chunk count. Kernels index state / tape arrays by the
+// slot (act[i]) and the chunk's geometry, codestream and statistics by the
+// chunk id (chunk[i], same position).
 struct TickDesc {
   int64_t tick;       // -1 before the first advance
-  const int* act;     // chunk ids doing a model step at this tick
-  const int2* hand;   // (src, dst) state handoffs due before this tick's step
+  const int* act;     // slots of the chunks doing a model step at this tick
+  const int2* hand;   // (src, dst) slot pairs: state handoffs due before this tick's step
   int n_act, n_hand;
+  const int* chunk;   // chunk ids, parallel to act (nullptr where unused)
 };
-// tick += 1 and point act/hand at that tick's CSR slices (n = 0 past the end)
+// tick += 1 and point act/chunk/hand at that tick's CSR slices (n = 0 past the end)
 void launch_tick_advance(TickDesc* td, const uint32_t* act_ptr, const int* act_all,
-                         const uint32_t* hand_ptr, const int2* hand_all, int64_t ticks,
-                         cudaStream_t st);
+                         const int* chunk_all, const uint32_t* hand_ptr, const int2* hand_all,
+                         int64_t ticks, cudaStream_t st);
 
 // Exact-order GEMM: C[m][n] = init + sum_{k ascending} A(m,k) * B(k,n).
 struct GemmP {
@@ -104,7 +111,7 @@ struct DmDims { int R, T, E, H, F, V, NH; };
 // cross-tick pipeline: next = the tick after cur (act list only), and the
 // context tokens of that tick's coded rows
 void launch_tick_peek(const TickDesc* cur, TickDesc* next, const uint32_t* act_ptr,
-                      const int* act_all, int64_t ticks, cudaStream_t st);
+                      const int* act_all, const int* chunk_all, int64_t ticks, cudaStream_t st);
 void launch_ctx_gather(const uint32_t* tokens, ChunkGeo geo, uint32_t* ctx, int64_t ctx_cs,
                        DmDims d, const TickDesc* td, int max_active, cudaStream_t st);
 // ctx gather (pipeline.cpp:180-182) + Embedding/PositionalEmbedding forward
@@ -245,6 +252,11 @@ void launch_sprm_transpose(const SprmP& s, const float* Gt, float* G, cudaStream
 // true: launch_sprm_dx reads the time-major Gt (no dependency on the transpose)
 bool sprm_dx_time_major(const SprmP& s);
 void launch_sprm_dx(const SprmP& s, const float* G, const float* Gt, float* dx, cudaStream_t st);
+// model head forward + CE + head backward, warp per row (one launch): writes
+// bact [R][B], g [R][V], dbact [R][B] and dfin [R][2H]
+void launch_sprm_head(const SprmP& s, const uint32_t* tokens, const int64_t* pos, const float* fin,
+                      const float* w1, const float* b1, const float* w2, const float* b2, float* bact,
+                      float* g, float* dbact, float* dfin, cudaStream_t st);
 void launch_tanh_vec(float* x, int64_t n, cudaStream_t st);
 void launch_adam_scalars(AdamScalars* sc, cudaStream_t st);
 void launch_pos_advance(int64_t* pos, int64_t by, cudaStream_t st);

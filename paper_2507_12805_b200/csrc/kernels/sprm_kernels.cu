@@ -210,6 +210,282 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_sprm_fwd32(SprmP s, const ui
   fin[int64_t(r) * 2 * H + d * H + j] = sh[wl][cur][j];  // final_state (layers.cpp:389-399)
 }
 
+// Forward with tape for H = 32*U > 32 (scale 2: H = 64, scale 1: H = 128).
+// Block = one direction, kWideWarps rows (warp per row); lane owns units
+// j = lane + 32u. The direction's W_h{r,z,n} sit in shared memory as
+// [gate][q][32] pairs (W[q][lane + 64v], W[q][lane + 64v + 32]) so that units
+// u = 2v, 2v+1 of a lane run as one paired exact chain; h of the warp's row is
+// double-buffered in shared memory and read as a broadcast. Per element the
+// operations and their order are k_sprm_fwd's (Gru::forward, layers.cpp:229-258).
+constexpr int kWideWarps = 4;
+template <int U>
+__global__ void __launch_bounds__(kWideWarps * 32) k_sprm_fwd_wide(SprmP s, const uint32_t* __restrict__ ctx,
+                                                                   const float* __restrict__ tab, float* tape,
+                                                                   float* fin) {
+  pdl_wait();
+  constexpr int H = 32 * U, P2 = U / 2;
+  extern __shared__ __align__(16) float dyn[];
+  f2_t* sw = reinterpret_cast<f2_t*>(dyn);                 // [3][H][P2][32]
+  float* sh = dyn + 2 * (3 * H * P2 * 32);                 // [kWideWarps][2][H]
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = blockIdx.x & 1;
+  const int r = (blockIdx.x >> 1) * kWideWarps + wl;
+  const int T = s.T, R = s.R, V = s.V;
+  const float* W = s.w;
+  for (int i = threadIdx.x; i < 3 * H * P2 * 32; i += blockDim.x) {
+    const int g = i / (H * P2 * 32), rem = i % (H * P2 * 32), q = rem / (P2 * 32),
+              v = (rem / 32) % P2, l = rem % 32;
+    const float* Wg = W + goff(s.offs, d, WHR + g) + int64_t(q) * H;
+    sw[i] = f2_pack(Wg[l + 64 * v], Wg[l + 64 * v + 32]);
+  }
+  float* hb = sh + wl * 2 * H;
+  for (int j = lane; j < H; j += 32) hb[j] = 0.0f;
+  __syncthreads();
+  if (r >= R) return;
+  float bhr[U], bhz[U], bhn[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int j = lane + 32 * u;
+    bhr[u] = W[goff(s.offs, d, BHR) + j];
+    bhz[u] = W[goff(s.offs, d, BHZ) + j];
+    bhn[u] = W[goff(s.offs, d, BHN) + j];
+  }
+  const float* t0 = tab + int64_t(d) * 3 * V * H;
+  const int64_t TRH = int64_t(T) * R * H;
+  float* tr = tape + (int64_t(0 * 2 + d) * TRH);
+  float* tz = tape + (int64_t(1 * 2 + d) * TRH);
+  float* tn = tape + (int64_t(2 * 2 + d) * TRH);
+  float* th = tape + (int64_t(3 * 2 + d) * TRH);
+  float* to = tape + (int64_t(4 * 2 + d) * TRH);
+  __syncwarp();
+  int cur = 0;
+  for (int t = 0; t < T; ++t) {
+    const int src_t = d ? (T - 1 - t) : t;
+    const int64_t tok = ctx[int64_t(r) * T + src_t];
+    const float* h = hb + cur * H;
+    f2_t ar[P2], az[P2], hh[P2];
+#pragma unroll
+    for (int v = 0; v < P2; ++v) {
+      const int j0 = lane + 64 * v, j1 = j0 + 32;
+      ar[v] = f2_pack(fadd(t0[tok * H + j0], bhr[2 * v]), fadd(t0[tok * H + j1], bhr[2 * v + 1]));
+      az[v] = f2_pack(fadd(t0[int64_t(V) * H + tok * H + j0], bhz[2 * v]),
+                      fadd(t0[int64_t(V) * H + tok * H + j1], bhz[2 * v + 1]));
+      hh[v] = f2_pack(bhn[2 * v], bhn[2 * v + 1]);
+    }
+    for (int q = 0; q < H; ++q) {
+      const f2_t hq = f2_bcast(h[q]);
+#pragma unroll
+      for (int v = 0; v < P2; ++v) {
+        ar[v] = f2_mac(ar[v], hq, sw[((0 * H + q) * P2 + v) * 32 + lane]);
+        az[v] = f2_mac(az[v], hq, sw[((1 * H + q) * P2 + v) * 32 + lane]);
+        hh[v] = f2_mac(hh[v], hq, sw[((2 * H + q) * P2 + v) * 32 + lane]);
+      }
+    }
+    float hn[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int v = u >> 1, j = lane + 32 * u;
+      const float arv = (u & 1) ? f2_hi(ar[v]) : f2_lo(ar[v]);
+      const float azv = (u & 1) ? f2_hi(az[v]) : f2_lo(az[v]);
+      const float hhv = (u & 1) ? f2_hi(hh[v]) : f2_lo(hh[v]);
+      const float an = t0[2 * int64_t(V) * H + tok * H + j];
+      const float rv = det_sigmoid(arv), zv = det_sigmoid(azv);
+      const float nv = det_tanh(fadd(an, fmul(rv, hhv)));
+      hn[u] = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, h[j]));
+      const int64_t o = (int64_t(t) * R + r) * H + j;
+      tr[o] = rv;
+      tz[o] = zv;
+      tn[o] = nv;
+      th[o] = hhv;
+      to[o] = hn[u];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) hb[(cur ^ 1) * H + lane + 32 * u] = hn[u];
+    __syncwarp();
+    cur ^= 1;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u)  // final_state (layers.cpp:389-399)
+    fin[int64_t(r) * 2 * H + d * H + lane + 32 * u] = hb[cur * H + lane + 32 * u];
+}
+
+// BPTT for H = 32*U > 32: as k_sprm_bptt (same per-element operations and
+// order), lane owns units j = lane + 32u; the transposed W_h of the direction
+// in shared memory as pairs WT[gate][q][v][lane] = (W_g[j0][q], W_g[j1][q]),
+// j0 = lane + 64v, j1 = j0 + 32; this step's dhh/dar/daz of the warp's row in
+// shared memory, read as broadcasts.
+template <int U>
+__global__ void __launch_bounds__(kWideWarps * 32) k_sprm_bptt_wide(SprmP s, const float* __restrict__ tape,
+                                                                    const float* __restrict__ dfin, float* Gt) {
+  pdl_wait();
+  constexpr int H = 32 * U, P2 = U / 2;
+  extern __shared__ __align__(16) float dyn[];
+  f2_t* swt = reinterpret_cast<f2_t*>(dyn);  // [3 (n, r, z)][H][P2][32]
+  float* sg = dyn + 2 * (3 * H * P2 * 32);   // [kWideWarps][3][H]
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int d = blockIdx.x & 1;
+  const int r = (blockIdx.x >> 1) * kWideWarps + wl;
+  const int T = s.T, R = s.R;
+  const float* W = s.w;
+  for (int i = threadIdx.x; i < 3 * H * P2 * 32; i += blockDim.x) {
+    const int g = i / (H * P2 * 32), rem = i % (H * P2 * 32), q = rem / (P2 * 32),
+              v = (rem / 32) % P2, l = rem % 32;
+    const float* Wg = W + goff(s.offs, d, g == 0 ? WHN : g == 1 ? WHR : WHZ);
+    swt[i] = f2_pack(Wg[int64_t(l + 64 * v) * H + q], Wg[int64_t(l + 64 * v + 32) * H + q]);
+  }
+  __syncthreads();
+  if (r >= R) return;
+  float* sgw = sg + wl * 3 * H;
+  const int64_t TRH = int64_t(T) * R * H;
+  const float* tp[5];
+#pragma unroll
+  for (int g = 0; g < 5; ++g) tp[g] = tape + (int64_t(g * 2 + d) * TRH);
+  float* go[5];
+#pragma unroll
+  for (int g = 0; g < 5; ++g) go[g] = Gt + int64_t(g * 2 + d) * TRH;  // an, ar, az, hh, hprev
+  float dh[U], dlast[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    dh[u] = 0.0f;
+    dlast[u] = fadd(0.0f, dfin[int64_t(r) * 2 * H + d * H + lane + 32 * u]);
+  }
+  for (int t = T - 1; t >= 0; --t) {
+    float dn[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = lane + 32 * u;
+      dh[u] = fadd(dh[u], t == T - 1 ? dlast[u] : 0.0f);  // gather_add_step(dout, t, dh)
+      const int64_t o = (int64_t(t) * R + r) * H + j;
+      const float rv = tp[0][o], zv = tp[1][o], nv = tp[2][o], hhv = tp[3][o];
+      const float hprev = t == 0 ? 0.0f : tp[4][o - int64_t(R) * H];
+      const float dzv = fmul(dh[u], fsub(hprev, nv));
+      const float danv = fmul(fmul(dh[u], fsub(1.0f, zv)), fsub(1.0f, fmul(nv, nv)));
+      const float dar = fmul(fmul(fmul(danv, hhv), rv), fsub(1.0f, rv));
+      const float daz = fmul(fmul(dzv, zv), fsub(1.0f, zv));
+      const float dhh = fmul(danv, rv);
+      dn[u] = fmul(dh[u], zv);
+      go[0][o] = danv;
+      go[1][o] = dar;
+      go[2][o] = daz;
+      go[3][o] = dhh;
+      go[4][o] = hprev;
+      sgw[0 * H + j] = dhh;
+      sgw[1 * H + j] = dar;
+      sgw[2 * H + j] = daz;
+    }
+    __syncwarp();
+    // dh_next = dh*z + dhh.W_hn^T + dar.W_hr^T + daz.W_hz^T  (layers.cpp:306-308)
+    f2_t acc[P2];
+#pragma unroll
+    for (int v = 0; v < P2; ++v) acc[v] = f2_pack(dn[2 * v], dn[2 * v + 1]);
+#pragma unroll
+    for (int g = 0; g < 3; ++g)
+      for (int q = 0; q < H; ++q) {
+        const f2_t gq = f2_bcast(sgw[g * H + q]);
+#pragma unroll
+        for (int v = 0; v < P2; ++v) acc[v] = f2_mac(acc[v], gq, swt[((g * H + q) * P2 + v) * 32 + lane]);
+      }
+    __syncwarp();
+#pragma unroll
+    for (int v = 0; v < P2; ++v) {
+      dh[2 * v] = f2_lo(acc[v]);
+      dh[2 * v + 1] = f2_hi(acc[v]);
+    }
+  }
+}
+
+template <int U>
+size_t wide_smem(int extra_per_warp) {
+  return size_t(2 * 3 * 32 * U * (U / 2) * 32 + kWideWarps * extra_per_warp * 32 * U) * sizeof(float);
+}
+
+// The model head of one train step, forward and backward, warp per row
+// (BiGruModel::forward tail and backward head, models.cpp:67-72, 77-86, with
+// the CE gradient of training.cpp:28-34 between them):
+//   bact = tanh(bott.b + fin.bott.w)          (Linear::forward: bias, then ascending p)
+//   logits = out.b + bact.out.w
+//   g = det_softmax(logits); g[tgt] -= 1
+//   dbact = (0 + g.out.w^T) * (1 - bact^2)   (Linear::backward dx, ascending o)
+//   dfin = 0 + dbact.bott.w^T
+// The chains of every output are the reference's; only their placement
+// changes (one launch instead of seven). The weight gradients of bott/out
+// (reductions over rows) run afterwards on the side stream from bact, g,
+// dbact.
+constexpr int kHeadWarps = 4;
+__global__ void __launch_bounds__(kHeadWarps * 32) k_sprm_head(
+    SprmP s, const uint32_t* __restrict__ tokens, const int64_t* __restrict__ pos,
+    const float* __restrict__ fin, const float* __restrict__ w1, const float* __restrict__ b1,
+    const float* __restrict__ w2, const float* __restrict__ b2, float* bact_out, float* g_out,
+    float* dbact_out, float* dfin_out) {
+  pdl_wait();
+  extern __shared__ __align__(16) float hs[];
+  const int H2 = 2 * s.H, B = s.B, V = s.V;
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kHeadWarps + wl;
+  float* f = hs + wl * (H2 + 2 * B + V);  // fin row, bact, dbact, g
+  float* ba = f + H2;
+  float* db = ba + B;
+  float* gr = db + B;
+  if (r >= s.R) return;
+  for (int p = lane; p < H2; p += 32) f[p] = fin[int64_t(r) * H2 + p];
+  __syncwarp();
+  for (int j = lane; j < B; j += 32) {
+    float acc = b1[j];
+    for (int p = 0; p < H2; ++p) acc = mac(acc, f[p], w1[int64_t(p) * B + j]);
+    acc = det_tanh(acc);
+    ba[j] = acc;
+    bact_out[int64_t(r) * B + j] = acc;
+  }
+  __syncwarp();
+  float mx = -__int_as_float(0x7f800000);
+  for (int i = lane; i < V; i += 32) {
+    float acc = b2[i];
+    for (int q = 0; q < B; ++q) acc = mac(acc, ba[q], w2[int64_t(q) * V + i]);
+    gr[i] = acc;
+    mx = fmaxf(mx, acc);
+  }
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  __syncwarp();
+  // det_softmax (detmath.cpp:85-97): exp of the shifted logits, one sequential sum
+  float sum = 0.0f;
+  for (int i0 = 0; i0 < V; i0 += 32) {
+    const int i = i0 + lane;
+    float e = 0.0f;
+    if (i < V) {
+      e = det_exp(fsub(gr[i], mx));
+      gr[i] = e;
+    }
+    const int cnt = min(32, V - i0);
+    for (int l = 0; l < cnt; ++l) sum = fadd(sum, __shfl_sync(0xffffffffu, e, l));
+  }
+  const float inv = fdiv(1.0f, sum);
+  const uint32_t tgt = tokens[*pos + r] & uint32_t(V - 1);
+  __syncwarp();
+  for (int i = lane; i < V; i += 32) {
+    float v = fmul(gr[i], inv);
+    if (uint32_t(i) == tgt) v = fsub(v, 1.0f);
+    gr[i] = v;
+    g_out[int64_t(r) * V + i] = v;
+  }
+  __syncwarp();
+  for (int j = lane; j < B; j += 32) {
+    float acc = 0.0f;
+    const float* wr = w2 + int64_t(j) * V;
+    for (int o = 0; o < V; ++o) acc = mac(acc, gr[o], wr[o]);
+    const float a = ba[j];
+    acc = fmul(acc, fsub(1.0f, fmul(a, a)));
+    db[j] = acc;
+    dbact_out[int64_t(r) * B + j] = acc;
+  }
+  __syncwarp();
+  for (int p = lane; p < H2; p += 32) {
+    float acc = 0.0f;
+    const float* wr = w1 + int64_t(p) * B;
+    for (int j = 0; j < B; ++j) acc = mac(acc, db[j], wr[j]);
+    dfin_out[int64_t(r) * H2 + p] = acc;
+  }
+}
+
 // g = det_softmax(logits) ; loss term ; g[tgt] -= 1   (training.cpp:28-34)
 __global__ void k_sprm_ce(SprmP s, const uint32_t* __restrict__ tokens,
                           const int64_t* __restrict__ pos, const float* __restrict__ logits,
@@ -578,6 +854,19 @@ void launch_sprm_fwd(const SprmP& s, const uint32_t* ctx, const float* tab, floa
         s, ctx, tab, tape, fin);
     return;
   }
+  const dim3 wgrid(unsigned(2 * ((s.R + kWideWarps - 1) / kWideWarps)));
+  if (s.H == 64) {
+    const size_t sm = wide_smem<2>(2);
+    ensure_smem(reinterpret_cast<const void*>(k_sprm_fwd_wide<2>), sm);
+    launch_pdl(k_sprm_fwd_wide<2>, wgrid, dim3(kWideWarps * 32), sm, st, s, ctx, tab, tape, fin);
+    return;
+  }
+  if (s.H == 128) {
+    const size_t sm = wide_smem<4>(2);
+    ensure_smem(reinterpret_cast<const void*>(k_sprm_fwd_wide<4>), sm);
+    launch_pdl(k_sprm_fwd_wide<4>, wgrid, dim3(kWideWarps * 32), sm, st, s, ctx, tab, tape, fin);
+    return;
+  }
   launch_pdl(k_sprm_fwd, dim3(unsigned(2 * ((s.R + 7) / 8))), dim3(256), 0, st, s, ctx, tab, tape, fin);
 }
 void launch_sprm_ce(const SprmP& s, const uint32_t* tokens, const int64_t* pos, const float* logits,
@@ -592,7 +881,18 @@ void launch_sprm_bptt(const SprmP& s, const float* tape, const float* dfin, floa
   if (s.H == 32)
     launch_pdl(k_sprm_bptt32, dim3(unsigned(2 * ((s.R + kBpttWarps - 1) / kBpttWarps))), dim3(kBpttWarps * 32), 0, st, 
         s, tape, dfin, Gt);
-  else
+  else if (s.H == 64 || s.H == 128) {
+    const dim3 wgrid(unsigned(2 * ((s.R + kWideWarps - 1) / kWideWarps)));
+    if (s.H == 64) {
+      const size_t sm = wide_smem<2>(3);
+      ensure_smem(reinterpret_cast<const void*>(k_sprm_bptt_wide<2>), sm);
+      launch_pdl(k_sprm_bptt_wide<2>, wgrid, dim3(kWideWarps * 32), sm, st, s, tape, dfin, Gt);
+    } else {
+      const size_t sm = wide_smem<4>(3);
+      ensure_smem(reinterpret_cast<const void*>(k_sprm_bptt_wide<4>), sm);
+      launch_pdl(k_sprm_bptt_wide<4>, wgrid, dim3(kWideWarps * 32), sm, st, s, tape, dfin, Gt);
+    }
+  } else
     launch_pdl(k_sprm_bptt, dim3(unsigned(2 * ((s.R + 7) / 8))), dim3(256), 0, st, s, tape, dfin, Gt);
 }
 void launch_sprm_transpose(const SprmP& s, const float* Gt, float* G, cudaStream_t st) {
@@ -608,6 +908,14 @@ void launch_sprm_dx(const SprmP& s, const float* G, const float* Gt, float* dx, 
     return;
   }
   launch_pdl(k_sprm_dx, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, s, G, dx);
+}
+void launch_sprm_head(const SprmP& s, const uint32_t* tokens, const int64_t* pos, const float* fin,
+                      const float* w1, const float* b1, const float* w2, const float* b2, float* bact,
+                      float* g, float* dbact, float* dfin, cudaStream_t st) {
+  const size_t smem = size_t(kHeadWarps) * (2 * s.H + 2 * s.B + s.V) * sizeof(float);
+  ensure_smem(reinterpret_cast<const void*>(k_sprm_head), smem);
+  launch_pdl(k_sprm_head, dim3(unsigned((s.R + kHeadWarps - 1) / kHeadWarps)), dim3(kHeadWarps * 32), smem,
+             st, s, tokens, pos, fin, w1, b1, w2, b2, bact, g, dbact, dfin);
 }
 void launch_tanh_vec(float* x, int64_t n, cudaStream_t st) {
   launch_pdl(k_tanh_vec, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, x, n);

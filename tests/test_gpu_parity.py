@@ -466,3 +466,23 @@ def test_run_benchmark_csv_and_fault(P, tmp_path):
     assert text.count("\n") == 4 and "AGGREGATE" in text and ",true\n" in text
     rows, rep = P.run_benchmark([str(a)], cfg, "", fault_flip_mid=True)
     assert not rows[0].verified and rep.mean_cr == 0.0 and rep.crp_percent == 0.0
+
+
+@pytest.mark.parametrize("scale,with_pub", [(2, False), (2, True), (1, False)])
+def test_sprm_prepass_wide_scales(P, checker, tmp_path, scale, with_pub):
+    # SPrM pre-pass at the paper's widths (scale 1: Es=16, Hs=128, B=128) and
+    # scale 2 (Hs=64): the wide forward/BPTT kernels; flags-6 containers
+    # (which carry the trained private model) byte-identical to the reference
+    raw = P.synth("markov3", 9000, 65 + scale)
+    kw = dict(t=8, bs=16, scale=scale, workers=2, threshold=0)
+    if with_pub:
+        path = str(tmp_path / f"spum_s{scale}.bin")
+        P.write_bigru(path, 3, 8, scale, 0xD00D, layers=2)
+        kw["pub_path"] = path
+    ckw = dict(kw)
+    thr = ckw.pop("threshold")
+    blob = P.compress(raw, P.CompressConfig(**_cfgs(ckw), selector_threshold=thr))
+    want = checker.compress(raw, O.make_cfg(**kw))
+    assert blob[5] == 6
+    assert blob == want
+    assert P.decompress(blob, kw.get("pub_path", "")) == raw

@@ -93,3 +93,47 @@ def test_config_validation_matches_reference(P):
         with pytest.raises(P.PmklcError) as e:
             P.compress(b"ACGT", P.CompressConfig(**kw))
         assert e.value.errc == "ConfigInvalid", kw
+
+
+@pytest.mark.parametrize("W,L,smp,world", [(128, 813, 500, 1), (256, 4069, 500, 1), (64, 300, 3000, 1),
+                                           (256, 4069, 500, 4), (16, 40, 0, 1), (4096, 2543, 500, 8)])
+def test_slots_by_concurrency(P, W, L, smp, world):
+    """Device memory by chunks in flight (assign_slots): no two chunks whose
+    lifetimes (first model tick .. last tick, extended to the handoff ticks at
+    which they are the source) overlap share a slot, every handoff source is
+    live at its copy, and the slot count is far below W once SMP staggers
+    the chunks."""
+    bs, t = 320, 32
+    lens = [bs * L] * W
+    off, src, ss, ms, ticks = P.schedule(lens, bs, t, smp)
+    for rank in range(world):
+        slot, n = P.schedule_slots(lens, bs, t, smp, rank, world)
+        life = {}
+        for c in range(W):
+            mine = c % world == rank
+            if ms[c] and mine:
+                assert slot[c] >= 0
+                life[c] = [off[c], off[c] + ms[c] - 1]
+            else:
+                assert slot[c] == -1
+        for c in range(W):
+            if src[c] >= 0 and ms[c] and src[c] in life:
+                life[src[c]][1] = max(life[src[c]][1], off[c])
+        by_slot = {}
+        for c, (a, b) in life.items():
+            by_slot.setdefault(slot[c], []).append((a, b))
+        for iv in by_slot.values():
+            iv.sort()
+            for (a0, b0), (a1, b1) in zip(iv, iv[1:]):
+                assert a1 > b0, "overlapping lifetimes share a slot"
+        assert n == len(by_slot)
+        # greedy by start tick is optimal: slots == peak number of live chunks
+        ev = sorted([(a, 1) for a, _ in life.values()] + [(b + 1, -1) for _, b in life.values()],
+                    key=lambda e: (e[0], e[1]))
+        peak = cur = 0
+        for _, d in ev:
+            cur += d
+            peak = max(peak, cur)
+        assert n == peak
+        if smp and L > 640:  # SMP staggers chunks: fewer slots than chunks
+            assert n < len(life), (n, len(life))
