@@ -968,12 +968,40 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
   auto W_ = [&](int i) { return w.p + hoffs[size_t(i)]; };
   auto G_ = [&](int i) { return g.p + hoffs[size_t(i)]; };
   const int b0 = model.bott();
+  // streamed BPTT + weight gradients (H == 32): its consumer table, counters
+  // and time-major inputs; otherwise transpose + batched NT reductions
+  const SprmP sp_full{w.p, offs.p, int(batch), T, Es, H, V, B};
+  const bool stream = sprm_stream_ok(sp_full);
+  DBuf<unsigned char> ntab;
+  DBuf<unsigned> cnt;
+  DBuf<float> Xtm;
+  const bool sorted_emb = stream && sprm_sorted_emb_ok(sp_full) && sprm_dx_time_major(sp_full) &&
+                          (Es == 2 || Es == 4 || Es == 8);
+  DBuf<uint16_t> order(sorted_emb ? RT : 0), rank(sorted_emb ? RT : 0);
+  DBuf<int> toff(sorted_emb ? V + 1 : 0);
+  if (stream) {
+    std::vector<unsigned char> host(sprm_stream_table_bytes(sp_full));
+    sprm_stream_table(sp_full, g.p, hoffs.data(), host.data());
+    ntab.alloc(host.size());
+    ntab.upload(host.data(), host.size(), st);
+    cnt.alloc(2 * size_t(T));
+    Xtm.alloc(2 * Es * RT);
+    CK(cudaStreamSynchronize(st));
+  }
   uint64_t nl = 0;
-  SideStream side;
+  SideStream side, side2;  // 12 GRU weight-gradient reductions; the head's weight gradients
   auto step = [&](int rows) {
     SprmP sp{w.p, offs.p, rows, T, Es, H, V, B};
     const int64_t rt = int64_t(rows) * T;
-    launch_sprm_prep(d_tok, pos.p, sp, ctx.p, X.p, tab.p, st);
+    const bool strm = stream && rows == int(batch);
+    launch_sprm_prep(d_tok, pos.p, sp, ctx.p, strm ? nullptr : X.p, tab.p, strm ? Xtm.p : nullptr,
+                     strm ? cnt.p : nullptr, st);
+    side.rewind();
+    side2.rewind();
+    if (strm && sorted_emb) {  // the embedding gradient's position order, beside the forward
+      side2.wait_for(st);
+      launch_tok_sort(ctx.p, int(rows) * T, V, order.p, toff.p, rank.p, side2.s);
+    }
     launch_sprm_fwd(sp, ctx.p, tab.p, tape.p, fin.p, st);
     // head forward, CE gradient and head backward in one launch (models.cpp:67-86,
     // training.cpp:28-34): bact, g, dbact and dfin
@@ -984,17 +1012,34 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
     // (out.backward / bott.backward reductions over rows), then (after BPTT)
     // the gradient transpose and the 12 weight-gradient reductions, beside
     // dx -> embedding gradient.
-    side.rewind();
-    side.wait_for(st);
+    side2.wait_for(st);
     GemmP g3{};
     g3.A = bact.p; g3.lda = B; g3.B = gg.p; g3.ldb = V; g3.C = G_(b0 + 2); g3.ldc = V;
     g3.M = B; g3.N = V; g3.K = rows; g3.ones_row = 1; g3.init = 2;
-    launch_gemm(g3, true, false, td.p, 1, side.s);
+    launch_gemm(g3, true, false, td.p, 1, side2.s);
     GemmP g5{};
     g5.A = fin.p; g5.lda = 2 * H; g5.B = dbact.p; g5.ldb = B; g5.C = G_(b0); g5.ldc = B;
     g5.M = 2 * H; g5.N = B; g5.K = rows; g5.ones_row = 1; g5.init = 2;
-    launch_gemm(g5, true, false, td.p, 1, side.s);
+    launch_gemm(g5, true, false, td.p, 1, side2.s);
     // backward through time, then the weight-gradient reductions over (t desc, rows asc)
+    if (strm) {  // both in one launch, the reductions streaming behind BPTT
+      side.wait_for(st);
+      launch_sprm_bptt_stream(sp, tape.p, dfin.p, Gt.p, Xtm.p, cnt.p, ntab.p, st, side.s);
+      side2.join_into(st);  // the sort (rank), beside the forward
+      launch_sprm_dx(sp, G.p, Gt.p, dx.p, st, sorted_emb ? rank.p : nullptr);
+      if (sorted_emb) {
+        launch_emb_walk_sorted(toff.p, dx.p, g.p + hoffs[0], V, Es, int(rows) * T, st);
+      } else {
+        const DmDims ed{rows, T, Es, H, 0, V, 0};
+        launch_emb_grad(ctx.p, 0, dx.p, 0, g.p, 0, int64_t(hoffs[0]), ed, td.p, 1, st);
+      }
+      side.join_into(st);
+      launch_adam_scalars(sc.p, st);
+      launch_adam(w.p, g.p, mo.p, vo.p, 0, P, sc.p, td.p, 1, st);
+      launch_pos_advance(pos.p, batch, st);
+      nl += 10;
+      return;
+    }
     launch_sprm_bptt(sp, tape.p, dfin.p, Gt.p, st);
     side.wait_for(st);
     launch_sprm_transpose(sp, Gt.p, G.p, side.s);
@@ -1022,6 +1067,7 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
     const DmDims ed{rows, T, Es, H, 0, V, 0};
     launch_emb_grad(ctx.p, 0, dx.p, 0, g.p, 0, int64_t(hoffs[0]), ed, td.p, 1, st);
     side.join_into(st);
+    side2.join_into(st);
     launch_adam_scalars(sc.p, st);
     launch_adam(w.p, g.p, mo.p, vo.p, 0, P, sc.p, td.p, 1, st);
     launch_pos_advance(pos.p, batch, st);
@@ -1032,12 +1078,13 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
   if (full > 0) {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    const uint64_t nl0 = nl;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     step(int(batch));
     CK(cudaStreamEndCapture(st, &graph));
     CK(cudaGraphInstantiate(&exec, graph, 0));
     for (uint64_t i = 0; i < full; ++i) CK(cudaGraphLaunch(exec, st));
-    nl += 14 * (full - 1);
+    nl += (nl - nl0) * (full - 1);
     CK(cudaGraphExecDestroy(exec));
     CK(cudaGraphDestroy(graph));
   }

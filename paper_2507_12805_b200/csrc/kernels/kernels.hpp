@@ -237,8 +237,21 @@ struct SprmP {
   const int64_t* offs;  // device param offsets
   int R, T, Es, H, V, B;
 };
+// X (feature-major reduction operand, nullable) and, for the streamed path,
+// Xtm [2][T][R][Es] (time-major GRU inputs) and the zeroed step counters cnt [2][T]
 void launch_sprm_prep(const uint32_t* tokens, const int64_t* pos, const SprmP& s, uint32_t* ctx,
-                      float* X, float* tab, cudaStream_t st);
+                      float* X, float* tab, float* Xtm, unsigned* cnt, cudaStream_t st);
+// Streamed BPTT + the 12 GRU weight-gradient reductions, concurrent (H == 32,
+// sprm_stream_ok): gradients accumulate into g as BPTT produces them. The
+// consumer table (output pointers into g) is built once per pre-pass:
+// sprm_stream_table fills sprm_stream_table_bytes(s) host bytes to upload.
+bool sprm_stream_ok(const SprmP& s);
+size_t sprm_stream_table_bytes(const SprmP& s);
+void sprm_stream_table(const SprmP& s, float* g, const int64_t* hoffs, void* host_buf);
+// (the reductions run on `side`, forked from and joined back into `st` by the caller)
+void launch_sprm_bptt_stream(const SprmP& s, const float* tape, const float* dfin, float* Gt,
+                             const float* Xtm, unsigned* cnt, const void* d_table, cudaStream_t st,
+                             cudaStream_t side);
 void launch_sprm_fwd(const SprmP& s, const uint32_t* ctx, const float* tab, float* tape, float* fin,
                      cudaStream_t st);
 void launch_sprm_ce(const SprmP& s, const uint32_t* tokens, const int64_t* pos, const float* logits,
@@ -251,12 +264,26 @@ void launch_sprm_bptt(const SprmP& s, const float* tape, const float* dfin, floa
 void launch_sprm_transpose(const SprmP& s, const float* Gt, float* G, cudaStream_t st);
 // true: launch_sprm_dx reads the time-major Gt (no dependency on the transpose)
 bool sprm_dx_time_major(const SprmP& s);
-void launch_sprm_dx(const SprmP& s, const float* G, const float* Gt, float* dx, cudaStream_t st);
+// rank (nullable, time-major path only): store dx row rt at its sorted rank
+void launch_sprm_dx(const SprmP& s, const float* G, const float* Gt, float* dx, cudaStream_t st,
+                    const uint16_t* rank = nullptr);
 // model head forward + CE + head backward, warp per row (one launch): writes
 // bact [R][B], g [R][V], dbact [R][B] and dfin [R][2H]
 void launch_sprm_head(const SprmP& s, const uint32_t* tokens, const int64_t* pos, const float* fin,
                       const float* w1, const float* b1, const float* w2, const float* b2, float* bact,
                       float* g, float* dbact, float* dfin, cudaStream_t st);
+// Embedding::backward of the pre-pass as a stable sort of the step's R*T
+// context positions by token (beside the forward) + a per-(token, feature)
+// walk after dx; needs V <= 256 and R*T <= 65536 (sprm_sorted_emb_ok)
+bool sprm_sorted_emb_ok(const SprmP& s);
+// order[k]: k-th position in (token, position) order; offs[V+1]; rank[p]: inverse
+void launch_tok_sort(const uint32_t* ctx, int n, int V, uint16_t* order, int* offs, uint16_t* rank,
+                     cudaStream_t st);
+// walk over dx stored in sorted order (launch_sprm_dx with rank); false if E unsupported
+bool launch_emb_walk_sorted(const int* offs, const float* dxs, float* grad, int V, int E, int n,
+                            cudaStream_t st);
+void launch_emb_walk(const uint16_t* order, const int* offs, const float* dx, float* grad, int V,
+                     int E, cudaStream_t st);
 void launch_tanh_vec(float* x, int64_t n, cudaStream_t st);
 void launch_adam_scalars(AdamScalars* sc, cudaStream_t st);
 void launch_pos_advance(int64_t* pos, int64_t by, cudaStream_t st);

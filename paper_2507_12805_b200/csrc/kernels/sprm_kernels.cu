@@ -11,6 +11,11 @@
 //   G{an,ar,az,hh}[d][j][k], HP[d][q][k] (h_{t-1}), X[d][i][k] (GRU input)
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
+#include <vector>
 
 #include "detmath.cuh"
 #include "kernels.hpp"
@@ -28,13 +33,24 @@ __device__ __forceinline__ int64_t goff(const int64_t* offs, int dir, int t) {
 // contexts of the batch at position p: ctx[r][i] = tok[p + r - T + i]; also
 // the GRU inputs X[d][i][k] and the per-token layer-0 projection table.
 __global__ void k_sprm_prep(const uint32_t* __restrict__ tokens, const int64_t* __restrict__ pos,
-                            SprmP s, uint32_t* ctx, float* X, float* tab) {
+                            SprmP s, uint32_t* ctx, float* X, float* tab, float* Xtm, unsigned* cnt) {
   pdl_wait();
   const int64_t p = *pos;
   const int R = s.R, T = s.T, Es = s.Es, H = s.H, V = s.V;
   const int64_t RT = int64_t(R) * T;
   const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const float* W = s.w;
+  if (cnt && tid < 2 * T) cnt[tid] = 0u;  // streamed-BPTT step counters of this train step
+  // Xtm[d][t][r][i]: the GRU input of direction d at its own time t (streamed path)
+  if (Xtm && tid < 2 * RT * Es) {
+    const int i = int(tid % Es);
+    const int64_t rest = tid / Es;
+    const int r = int(rest % R);
+    const int64_t dt = rest / R;
+    const int t = int(dt % T), d = int(dt / T);
+    const int src_t = d ? (T - 1 - t) : t;
+    Xtm[tid] = W[s.offs[0] + int64_t(tokens[p + r - T + src_t]) * Es + i];
+  }
   if (tid < RT) {
     const int r = int(tid / T), i = int(tid % T);
     ctx[tid] = tokens[p + r - T + i];
@@ -52,8 +68,9 @@ __global__ void k_sprm_prep(const uint32_t* __restrict__ tokens, const int64_t* 
     tab[tid] = acc;
   }
   // X[d][i][k]: fwd input at its time t is x[r][t]; bwd's is x[r][T-1-t]
+  // (feature-major reduction operand; the streamed path has none)
   const int64_t nx = int64_t(2) * Es * RT;
-  if (tid < nx) {
+  if (X && tid < nx) {
     const int64_t k = tid % RT;
     const int64_t rest = tid / RT;
     const int i = int(rest % Es), d = int(rest / Es);
@@ -411,7 +428,14 @@ size_t wide_smem(int extra_per_warp) {
 // changes (one launch instead of seven). The weight gradients of bott/out
 // (reductions over rows) run afterwards on the side stream from bact, g,
 // dbact.
-constexpr int kHeadWarps = 4;
+constexpr int kHeadWarps = 8;
+// shared floats of the head kernel: W1 [2H][B] and W2 [B][V] as they are, their
+// transposes W1t [B][2H+1] and W2t [V][B+1] (padded rows: conflict-free
+// column walks), and per warp fin [2H], bact [B], dbact [B], e/g [V]
+__host__ __device__ inline int head_w_floats(int H2, int B, int V) {
+  return H2 * B + B * V + B * (H2 + 1) + V * (B + 1);
+}
+template <bool kSmemW>  // weights staged in shared memory (the default widths) or read from L1/L2
 __global__ void __launch_bounds__(kHeadWarps * 32) k_sprm_head(
     SprmP s, const uint32_t* __restrict__ tokens, const int64_t* __restrict__ pos,
     const float* __restrict__ fin, const float* __restrict__ w1, const float* __restrict__ b1,
@@ -420,47 +444,88 @@ __global__ void __launch_bounds__(kHeadWarps * 32) k_sprm_head(
   pdl_wait();
   extern __shared__ __align__(16) float hs[];
   const int H2 = 2 * s.H, B = s.B, V = s.V;
+  float* W1s = hs;                  // [H2][B]
+  float* W2s = W1s + H2 * B;         // [B][V]
+  float* W1t = W2s + B * V;          // [B][H2+1]: W1t[j][p] = W1[p][j]
+  float* W2t = W1t + B * (H2 + 1);   // [V][B+1]: W2t[i][q] = W2[q][i]
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * kHeadWarps + wl;
-  float* f = hs + wl * (H2 + 2 * B + V);  // fin row, bact, dbact, g
+  if (kSmemW) {  // staging: every thread's loads issued before its stores
+    constexpr int kU = 8;
+    const int n1 = H2 * B, n2 = B * V, nt = int(blockDim.x);
+    for (int e0 = threadIdx.x; e0 < n1 + n2; e0 += kU * nt) {
+      float x[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int e = e0 + u * nt;
+        x[u] = e < n1 ? __ldg(w1 + e) : (e < n1 + n2 ? __ldg(w2 + (e - n1)) : 0.0f);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int e = e0 + u * nt;
+        if (e < n1) {
+          W1s[e] = x[u];
+          W1t[(e % B) * (H2 + 1) + e / B] = x[u];
+        } else if (e < n1 + n2) {
+          const int f = e - n1;
+          W2s[f] = x[u];
+          W2t[(f % V) * (B + 1) + f / V] = x[u];
+        }
+      }
+    }
+  }
+  // W1(p, j), W2(q, i) and the transposed walks W2(j, o) / W1(p, j) by column
+  auto W1 = [&](int p, int j) { return kSmemW ? W1s[p * B + j] : w1[int64_t(p) * B + j]; };
+  auto W2 = [&](int q, int i) { return kSmemW ? W2s[q * V + i] : w2[int64_t(q) * V + i]; };
+  auto W2T = [&](int o, int j) { return kSmemW ? W2t[o * (B + 1) + j] : w2[int64_t(j) * V + o]; };
+  auto W1T = [&](int j, int p) { return kSmemW ? W1t[j * (H2 + 1) + p] : w1[int64_t(p) * B + j]; };
+  float* f = hs + (kSmemW ? head_w_floats(H2, B, V) : 0) + wl * (H2 + 2 * B + V);  // fin, bact, dbact, g
   float* ba = f + H2;
   float* db = ba + B;
   float* gr = db + B;
-  if (r >= s.R) return;
-  for (int p = lane; p < H2; p += 32) f[p] = fin[int64_t(r) * H2 + p];
-  __syncwarp();
+  const int r = blockIdx.x * kHeadWarps + wl;
+  const bool live = r < s.R;
+  if (live)
+    for (int p = lane; p < H2; p += 32) f[p] = fin[int64_t(r) * H2 + p];
+  __syncthreads();
+  if (!live) return;
+  // bact = tanh(bott.b + fin.W1), ascending p
   for (int j = lane; j < B; j += 32) {
     float acc = b1[j];
-    for (int p = 0; p < H2; ++p) acc = mac(acc, f[p], w1[int64_t(p) * B + j]);
+#pragma unroll 8
+    for (int p = 0; p < H2; ++p) acc = mac(acc, f[p], W1(p, j));
     acc = det_tanh(acc);
     ba[j] = acc;
     bact_out[int64_t(r) * B + j] = acc;
   }
   __syncwarp();
+  // logits = out.b + bact.W2, ascending q
   float mx = -__int_as_float(0x7f800000);
   for (int i = lane; i < V; i += 32) {
     float acc = b2[i];
-    for (int q = 0; q < B; ++q) acc = mac(acc, ba[q], w2[int64_t(q) * V + i]);
+#pragma unroll 8
+    for (int q = 0; q < B; ++q) acc = mac(acc, ba[q], W2(q, i));
     gr[i] = acc;
     mx = fmaxf(mx, acc);
   }
   for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   __syncwarp();
-  // det_softmax (detmath.cpp:85-97): exp of the shifted logits, one sequential sum
+  // det_softmax (detmath.cpp:85-97): exp of the shifted logits, then one
+  // sequential sum in index order (lane 0 over shared memory)
+  for (int i = lane; i < V; i += 32) gr[i] = det_exp(fsub(gr[i], mx));
+  __syncwarp();
   float sum = 0.0f;
-  for (int i0 = 0; i0 < V; i0 += 32) {
-    const int i = i0 + lane;
-    float e = 0.0f;
-    if (i < V) {
-      e = det_exp(fsub(gr[i], mx));
-      gr[i] = e;
-    }
-    const int cnt = min(32, V - i0);
-    for (int l = 0; l < cnt; ++l) sum = fadd(sum, __shfl_sync(0xffffffffu, e, l));
+  if (lane == 0) {
+    int i = 0;
+    if ((V & 3) == 0)
+      for (; i < V; i += 4) {
+        const float4 e4 = *reinterpret_cast<const float4*>(gr + i);
+        sum = fadd(fadd(fadd(fadd(sum, e4.x), e4.y), e4.z), e4.w);
+      }
+    for (; i < V; ++i) sum = fadd(sum, gr[i]);
   }
+  sum = __shfl_sync(0xffffffffu, sum, 0);
   const float inv = fdiv(1.0f, sum);
   const uint32_t tgt = tokens[*pos + r] & uint32_t(V - 1);
-  __syncwarp();
   for (int i = lane; i < V; i += 32) {
     float v = fmul(gr[i], inv);
     if (uint32_t(i) == tgt) v = fsub(v, 1.0f);
@@ -468,20 +533,22 @@ __global__ void __launch_bounds__(kHeadWarps * 32) k_sprm_head(
     g_out[int64_t(r) * V + i] = v;
   }
   __syncwarp();
+  // dbact = (0 + g.W2^T) * (1 - bact^2), ascending o
   for (int j = lane; j < B; j += 32) {
     float acc = 0.0f;
-    const float* wr = w2 + int64_t(j) * V;
-    for (int o = 0; o < V; ++o) acc = mac(acc, gr[o], wr[o]);
+#pragma unroll 8
+    for (int o = 0; o < V; ++o) acc = mac(acc, gr[o], W2T(o, j));
     const float a = ba[j];
     acc = fmul(acc, fsub(1.0f, fmul(a, a)));
     db[j] = acc;
     dbact_out[int64_t(r) * B + j] = acc;
   }
   __syncwarp();
+  // dfin = 0 + dbact.W1^T, ascending j
   for (int p = lane; p < H2; p += 32) {
     float acc = 0.0f;
-    const float* wr = w1 + int64_t(p) * B;
-    for (int j = 0; j < B; ++j) acc = mac(acc, db[j], wr[j]);
+#pragma unroll 8
+    for (int j = 0; j < B; ++j) acc = mac(acc, db[j], W1T(j, p));
     dfin_out[int64_t(r) * H2 + p] = acc;
   }
 }
@@ -606,8 +673,13 @@ __global__ void __launch_bounds__(256) k_sprm_bptt(SprmP s, const float* __restr
 // LDS.128); the step's tape values are prefetched one step ahead. Same
 // per-element operations and order as k_sprm_bptt.
 constexpr int kBpttWarps = 4;
+constexpr int kPubSteps = 8;  // BPTT progress published per group of steps
+// cnt (nullable): per (direction, step) count of rows whose step is stored,
+// published with a release add after each step (the streamed reductions of
+// k_sprm_nt_stream wait on it)
 __global__ void __launch_bounds__(kBpttWarps * 32) k_sprm_bptt32(SprmP s, const float* __restrict__ tape,
-                                                                 const float* __restrict__ dfin, float* Gt) {
+                                                                 const float* __restrict__ dfin, float* Gt,
+                                                                 unsigned* cnt) {
   pdl_wait();
   constexpr int H = 32;
   __shared__ __align__(16) float sg[kBpttWarps][3][H];  // dhh, dar, daz of this step
@@ -672,7 +744,12 @@ __global__ void __launch_bounds__(kBpttWarps * 32) k_sprm_bptt32(SprmP s, const 
     sg[wl][0][j] = dhh;
     sg[wl][1][j] = dar;
     sg[wl][2][j] = daz;
-    __syncwarp();
+    __syncwarp();  // also orders the lanes' stores before lane 0's release
+    // one release per kPubSteps steps (the group's lowest step): the fence
+    // waits for the warp's stores to land, so it is amortised over the group
+    if (cnt && lane == 0 && (t % kPubSteps) == 0)
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt + d * T + t / kPubSteps)
+                   : "memory");
     // dh_next = dh*z + dhh.W_hn^T + dar.W_hr^T + daz.W_hz^T  (layers.cpp:306-308)
 #pragma unroll
     for (int g = 0; g < 3; ++g)
@@ -689,6 +766,284 @@ __global__ void __launch_bounds__(kBpttWarps * 32) k_sprm_bptt32(SprmP s, const 
 #pragma unroll
     for (int g = 0; g < 5; ++g) xc[g] = xn[g];
   }
+}
+
+// ---------------------------------------------------------------------------
+// Streamed BPTT + weight-gradient reductions (H == 32). The 12 reductions
+// (dW_i{n,r,z} over the GRU inputs, dW_h{n,r,z} over h_{t-1}, and the bias
+// sums) accumulate in the reference's order k = (T-1-t)*R + r: time
+// descending, rows ascending -- exactly the order backward-through-time
+// produces the gate gradients. So one launch holds both: BPTT blocks (warp per
+// row, k_sprm_bptt32's body) publish each finished step with a per-(dir, step)
+// row counter; consumer blocks, one per (direction, gate) slab of output rows,
+// wait for the counter, pull the step's gradient slab Gt[g][d][t] ([R][32]),
+// the h_{t-1} slab (Gt[4][d][t], written by BPTT beside the gradients) and the
+// input slab Xtm[d][t] ([R][Es], from the prep kernel) into shared memory
+// with bulk async copies (a producer warp, double-buffered, mbarrier
+// complete_tx), and advance their chains one step behind BPTT. A consumer
+// lane owns output column j = lane of two output rows as one paired exact
+// chain (acc + a*b, a from the A slab, b = Gt[g][d][t][r][j]; the bias rows
+// use a = 1). Consumers only wait on BPTT, never the reverse, so the launch
+// cannot deadlock whatever the block placement. Replaces the transpose and
+// the batched NT reduction (which started only after BPTT ended).
+struct NtSRow {
+  int kind;      // 0: input row p (Xtm), 1: h_{t-1} row p, 2: bias (a = 1), -1: none
+  int p;
+  float* out0;   // output row: element j at out0[j]
+  float* out1;   // a second destination of the same chain (the b_i*/b_h* pair), or null
+};
+struct NtSWarp {
+  int g;         // gradient slab: 0 an, 1 ar, 2 az, 3 hh
+  NtSRow r0, r1;
+};
+struct NtSParams {
+  const float* tape;
+  const float* dfin;
+  float* Gt;
+  const float* Xtm;        // [2][T][R][Es]
+  unsigned* cnt;           // [2][T] rows finished per (dir, step)
+  const NtSWarp* warps;    // consumer warp table, 4 per block, (d, g) uniform per block
+  const int* block_dg;     // per consumer block: d * 4 + g
+  int nb_bptt;             // unused (0)
+  int variant;             // dev experiments (PMKLC_NT_VARIANT): 1 no compute, 2 no copies, 3 no wait
+};
+constexpr int kStreamConsumers = 8;
+
+__device__ __forceinline__ uint32_t sm_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(bar)) : "memory");
+}
+// One consumer step of a paired chain: acc += (a[r].x, a[r].y) * b[r] for r
+// ascending, a and b in shared memory (a: 8-byte pair, stride a_st bytes;
+// b: stride 128 bytes). A three-stage software pipeline in program order --
+// the add of batch k, the products of batch k+1, the loads of batch k+2 --
+// written with volatile asm so the schedule keeps it: each add then only
+// waits for the previous add (the chain's 4-cycle latency), never for a load
+// or a product.
+__device__ __forceinline__ void lds_pair(f2_t& x, float& y, uint32_t a, uint32_t b) {
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(x) : "r"(a));
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(y) : "r"(b));
+}
+__device__ __forceinline__ f2_t prod_v(f2_t x, float y) {
+  f2_t out;
+  asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(out) : "l"(x), "l"(f2_bcast(y)), "l"(c_negzero2));
+  return out;
+}
+__device__ __forceinline__ void add_v(f2_t& acc, f2_t p) {
+  asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(p));
+}
+// batch k's adds, batch k+1's products (from LN), batch k+2's loads (into LL)
+template <int kU>
+__device__ __forceinline__ void nt_stage(f2_t& acc, f2_t (&P)[kU], f2_t (&LN)[kU], float (&LNb)[kU],
+                                         f2_t (&LL)[kU], float (&LLb)[kU], bool more1, bool more2,
+                                         uint32_t a2, uint32_t b2, uint32_t a_st) {
+#pragma unroll
+  for (int u = 0; u < kU; ++u) {
+    add_v(acc, P[u]);
+    if (more1) P[u] = prod_v(LN[u], LNb[u]);
+    if (more2) lds_pair(LL[u], LLb[u], a2 + uint32_t(u) * a_st, b2 + uint32_t(u) * 128u);
+  }
+}
+__device__ __forceinline__ f2_t nt_chain_pair(f2_t acc, uint32_t a, uint32_t a_st, uint32_t b, int R) {
+  constexpr int kU = 8;
+  const int nb = R / kU;
+  f2_t L0[kU], L1[kU], P[kU];
+  float B0[kU], B1[kU];
+  if (nb > 0) {
+#pragma unroll
+    for (int u = 0; u < kU; ++u) lds_pair(L0[u], B0[u], a + uint32_t(u) * a_st, b + uint32_t(u) * 128u);
+    if (nb > 1) {
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        lds_pair(L1[u], B1[u], a + uint32_t(kU + u) * a_st, b + uint32_t(kU + u) * 128u);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) P[u] = prod_v(L0[u], B0[u]);
+    int k = 0;
+    for (; k + 2 <= nb; k += 2) {
+      nt_stage<kU>(acc, P, L1, B1, L0, B0, k + 1 < nb, k + 2 < nb, a + uint32_t((k + 2) * kU) * a_st,
+                   b + uint32_t((k + 2) * kU) * 128u, a_st);
+      nt_stage<kU>(acc, P, L0, B0, L1, B1, k + 2 < nb, k + 3 < nb, a + uint32_t((k + 3) * kU) * a_st,
+                   b + uint32_t((k + 3) * kU) * 128u, a_st);
+    }
+    if (k < nb) nt_stage<kU>(acc, P, L1, B1, L0, B0, false, false, 0, 0, a_st);
+  }
+  for (int r = nb * kU; r < R; ++r) {
+    f2_t x;
+    float y;
+    lds_pair(x, y, a + uint32_t(r) * a_st, b + uint32_t(r) * 128u);
+    add_v(acc, prod_v(x, y));
+  }
+  return acc;
+}
+
+// bounded waits: a protocol error traps (a loud launch failure) instead of
+// hanging the device
+constexpr unsigned long long kSpinLimit = 1ull << 28;
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  for (unsigned long long i = 0;; ++i) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(sm_addr(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (i > kSpinLimit) __trap();
+  }
+}
+// the producer's waits leave the issue slots to the consumer warps
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  for (unsigned long long i = 0;; ++i) {
+    uint32_t done;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(sm_addr(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (i > kSpinLimit) __trap();
+    __nanosleep(64);
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          sm_addr(dst)),
+      "l"(src), "r"(bytes), "r"(sm_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// The consumer blocks (one per (direction, gate) slab of output rows, 4
+// consumer warps + 1 producer warp) run as their own launch on a side stream,
+// beside the BPTT launch (k_sprm_bptt32 with the per-step counters): they
+// only wait on BPTT, and BPTT blocks (small shared memory) still fit next to
+// them on every SM, so the pair cannot deadlock.
+__global__ void __launch_bounds__((kStreamConsumers + 1) * 32, 1) k_sprm_nt_stream(SprmP s, NtSParams q) {
+  pdl_wait();
+  constexpr int H = 32;
+  const int T = s.T, R = s.R, Es = s.Es;
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // ---------------- weight-gradient consumers
+  extern __shared__ __align__(128) float sbuf[];  // [2][ B [R][32] | Hp [R][32] | X [R][Es] ]
+  __shared__ uint64_t full[2], empty[2];
+  const int cb = int(blockIdx.x);
+  const int dg = q.block_dg[cb], d = (dg >> 2) & 1, g = dg & 3;
+  const bool need_h = (dg >> 8) & 1, need_x = (dg >> 9) & 1;  // the block's A slabs
+  const int slab = R * (2 * H + Es);
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], kStreamConsumers);
+    mbar_init(&empty[1], kStreamConsumers);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (wl == kStreamConsumers) {  // producer warp
+    if (lane == 0) {
+      const uint32_t bB = uint32_t(R) * H * 4, bX = uint32_t(R) * Es * 4;
+      for (int i = 0; i < T; ++i) {
+        const int t = T - 1 - i, b = i & 1;
+        if (i >= 2) mbar_wait_sleep(&empty[b], ((i >> 1) - 1) & 1);  // consumers done with step i-2
+        const unsigned* c = q.cnt + d * T + t / kPubSteps;  // group of step t complete
+        for (unsigned long long k = 0; q.variant != 3 && ld_acquire(c) < unsigned(R); ++k) {
+          if (k > kSpinLimit) __trap();
+          __nanosleep(32);
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        float* base = sbuf + b * slab;
+        if (q.variant == 2) {
+          mbar_arrive(&full[b]);
+          continue;
+        }
+        mbar_arrive_tx(&full[b], bB + (need_h ? bB : 0) + (need_x ? bX : 0));
+        bulk_g2s(base, q.Gt + (int64_t(g * 2 + d) * T + t) * R * H, bB, &full[b]);
+        if (need_h) bulk_g2s(base + R * H, q.Gt + (int64_t(4 * 2 + d) * T + t) * R * H, bB, &full[b]);
+        if (need_x) bulk_g2s(base + 2 * R * H, q.Xtm + (int64_t(d) * T + t) * R * Es, bX, &full[b]);
+      }
+    }
+    return;
+  }
+  const NtSWarp wk = q.warps[cb * kStreamConsumers + wl];
+  if (wk.r0.kind < 0) {  // idle warp: still releases the buffers
+    for (int i = 0; i < T; ++i) {
+      mbar_wait(&full[i & 1], (i >> 1) & 1);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[i & 1]);
+    }
+    return;
+  }
+  // A source of each row inside a buffer: offset and row stride (floats)
+  auto a_off = [&](const NtSRow& rw, int& stride) {
+    if (rw.kind == 0) { stride = Es; return 2 * R * H + rw.p; }
+    if (rw.kind == 1) { stride = H; return R * H + rw.p; }
+    stride = 0;
+    return -1;  // bias / none: a = 1
+  };
+  int st0 = 0, st1 = 0;
+  const int o0 = a_off(wk.r0, st0), o1 = a_off(wk.r1, st1);
+  f2_t acc = f2_pack(wk.r0.out0 ? wk.r0.out0[lane] : 0.0f, wk.r1.out0 ? wk.r1.out0[lane] : 0.0f);
+  for (int i = 0; i < T; ++i) {
+    const int b = i & 1;
+    mbar_wait(&full[b], (i >> 1) & 1);
+    if (q.variant == 1) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[b]);
+      continue;
+    }
+    const float* base = sbuf + b * slab;
+    const float* bs = base + lane;
+    const float* a0 = o0 >= 0 ? base + o0 : nullptr;
+    const float* a1 = o1 >= 0 ? base + o1 : nullptr;
+    if (a0 && a1 && st0 == st1 && o1 == o0 + 1 && (o0 & 1) == 0) {
+      acc = nt_chain_pair(acc, sm_addr(a0), uint32_t(st0) * 4, sm_addr(bs), R);
+    } else if (!a0 && !a1) {  // bias row(s): a = 1, and 1*b == b exactly
+      for (int r = 0; r < R; ++r) acc = f2_add(acc, f2_bcast(bs[r * H]));
+    } else {
+      constexpr int kU = 8;
+      int r = 0;
+      for (; r + kU <= R; r += kU) {
+        float x0[kU], x1[kU], bv[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          x0[u] = a0 ? a0[(r + u) * st0] : 1.0f;
+          x1[u] = a1 ? a1[(r + u) * st1] : 1.0f;
+          bv[u] = bs[(r + u) * H];
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) acc = f2_add(acc, f2_mul(f2_pack(x0[u], x1[u]), f2_bcast(bv[u])));
+      }
+      for (; r < R; ++r) {
+        const float x0 = a0 ? a0[r * st0] : 1.0f, x1 = a1 ? a1[r * st1] : 1.0f;
+        acc = f2_add(acc, f2_mul(f2_pack(x0, x1), f2_bcast(bs[r * H])));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);
+  }
+  const float v0 = f2_lo(acc), v1 = f2_hi(acc);
+  if (wk.r0.out0) wk.r0.out0[lane] = v0;
+  if (wk.r0.out1) wk.r0.out1[lane] = v0;
+  if (wk.r1.out0) wk.r1.out0[lane] = v1;
+  if (wk.r1.out1) wk.r1.out1[lane] = v1;
 }
 
 // Gt[g][d][t][r][j] -> G[g][d][j][k], k = (T-1-t)*R + r (32x32 smem tiles).
@@ -773,7 +1128,8 @@ __global__ void k_sprm_dx(SprmP s, const float* __restrict__ Gr, float* dx) {
 // 3*H terms of one (row, step, direction) are three contiguous 128-byte
 // vectors, read with LDG.128 and shared by the Es threads of the position;
 // the input weights sit in shared memory. Same chain order as k_sprm_dx.
-__global__ void __launch_bounds__(256) k_sprm_dx_t(SprmP s, const float* __restrict__ Gt, float* dx) {
+__global__ void __launch_bounds__(256) k_sprm_dx_t(SprmP s, const float* __restrict__ Gt, float* dx,
+                                                   const uint16_t* __restrict__ rank) {
   pdl_wait();
   constexpr int H = 32;
   __shared__ __align__(16) float sw[2][3][8][H];  // [d][gate n,r,z][i][q]
@@ -816,7 +1172,182 @@ __global__ void __launch_bounds__(256) k_sprm_dx_t(SprmP s, const float* __restr
     }
     part[d] = acc;
   }
-  dx[idx] = fadd(fadd(0.0f, part[0]), fadd(0.0f, part[1]));  // dx += dx_rev (both from zero)
+  const float v = fadd(fadd(0.0f, part[0]), fadd(0.0f, part[1]));  // dx += dx_rev (both from zero)
+  // sorted store for the embedding gradient walk: row rt goes to its rank
+  if (rank) dx[int64_t(rank[rt]) * Es + i] = v;
+  else dx[idx] = v;
+}
+
+// Embedding::backward (layers.cpp:117-125) split in two: the ctx tokens of a
+// train step are known before its forward, so a stable counting sort of the
+// R*T positions by token (k_tok_sort, one block, beside the forward) leaves
+// only the gradient walk after dx (k_emb_walk): thread per (token, feature),
+// its positions in (r, t) order -- the reference's order for that element --
+// with the gathers issued ahead of the add chain.
+constexpr int kSortBlock = 1024, kSortMaxTok = 256;
+__global__ void __launch_bounds__(kSortBlock) k_tok_sort(const uint32_t* __restrict__ ctx, int n, int V,
+                                                         uint16_t* order, int* offs, uint16_t* rank) {
+  pdl_wait();
+  __shared__ int cnt[kSortBlock / 32][kSortMaxTok];
+  __shared__ int tot[kSortMaxTok + 1];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kSortBlock / 32;
+  const int span = (n + nw - 1) / nw, p0 = w * span, p1 = min(n, p0 + span);
+  for (int v = lane; v < V; v += 32) cnt[w][v] = 0;
+  __syncwarp();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int c = p0; c < p1; c += 32) {
+    const int p = c + lane;
+    const uint32_t v = p < p1 ? ctx[p] & uint32_t(V - 1) : 0xffffffffu;
+    const unsigned m = __match_any_sync(0xffffffffu, v);
+    if (p < p1 && (m & lt) == 0) cnt[w][v] += __popc(m);
+    __syncwarp();
+  }
+  __syncthreads();
+  // totals per token, exclusive scan over tokens (V <= 256: one warp per 32)
+  if (threadIdx.x < V) {
+    int sum = 0;
+    for (int ww = 0; ww < nw; ++ww) sum += cnt[ww][threadIdx.x];
+    tot[threadIdx.x] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int a = 0;
+    for (int v = 0; v < V; ++v) {
+      const int x = tot[v];
+      tot[v] = a;
+      offs[v] = a;
+      a += x;
+    }
+    offs[V] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x < V) {  // per-warp cursors in (token, warp) order
+    int a = tot[threadIdx.x];
+    for (int ww = 0; ww < nw; ++ww) {
+      const int x = cnt[ww][threadIdx.x];
+      cnt[ww][threadIdx.x] = a;
+      a += x;
+    }
+  }
+  __syncthreads();
+  for (int c = p0; c < p1; c += 32) {
+    const int p = c + lane;
+    const uint32_t v = p < p1 ? ctx[p] & uint32_t(V - 1) : 0xffffffffu;
+    const unsigned m = __match_any_sync(0xffffffffu, v);
+    if (p < p1) {
+      const int k = cnt[w][v] + __popc(m & lt);
+      order[k] = uint16_t(p);
+      rank[p] = uint16_t(k);
+    }
+    __syncwarp();
+    if (p < p1 && (m & lt) == 0) cnt[w][v] += __popc(m);
+    __syncwarp();
+  }
+}
+
+// walk over dx already stored in sorted order (dxs[k][i], k = rank of the
+// position): thread per token, all E feature chains at once, contiguous loads
+template <int E>
+__global__ void k_emb_walk_sorted(const int* __restrict__ offs, const float* __restrict__ dxs,
+                                  float* grad, int V) {
+  pdl_wait();
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const int k0 = offs[v], k1 = offs[v + 1];
+  float acc[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) acc[i] = grad[v * E + i];
+  constexpr int kU = 8;
+  int k = k0;
+  for (; k + kU <= k1; k += kU) {
+    float x[kU][E];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+#pragma unroll
+      for (int i = 0; i < E; ++i) x[u][i] = __ldg(dxs + int64_t(k + u) * E + i);
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+#pragma unroll
+      for (int i = 0; i < E; ++i) acc[i] = fadd(acc[i], x[u][i]);
+  }
+  for (; k < k1; ++k)
+#pragma unroll
+    for (int i = 0; i < E; ++i) acc[i] = fadd(acc[i], __ldg(dxs + int64_t(k) * E + i));
+#pragma unroll
+  for (int i = 0; i < E; ++i) grad[v * E + i] = acc[i];
+}
+
+// same walk with the sorted dx staged in shared memory first (one block):
+// the staging is one coalesced sweep with every load in flight, and the
+// per-token chains then read LDS.128s issued a batch ahead
+template <int E>
+__global__ void __launch_bounds__(1024, 1) k_emb_walk_smem(const int* __restrict__ offs,
+                                                        const float* __restrict__ dxs, float* grad,
+                                                        int V, int n) {
+  pdl_wait();
+  extern __shared__ __align__(16) float sx[];  // [n][E]
+  const int nf4 = n * E / 4;
+  const float4* src = reinterpret_cast<const float4*>(dxs);
+  float4* dst = reinterpret_cast<float4*>(sx);
+  constexpr int kU = 8;
+  for (int i0 = threadIdx.x; i0 < nf4; i0 += kU * blockDim.x) {
+    float4 x[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < nf4) x[u] = __ldg(src + i);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < nf4) dst[i] = x[u];
+    }
+  }
+  __syncthreads();
+  const int v = threadIdx.x;
+  if (v >= V) return;
+  const int k0 = offs[v], k1 = offs[v + 1];
+  float acc[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) acc[i] = grad[v * E + i];
+  int k = k0;
+  for (; k + kU <= k1; k += kU) {
+    float x[kU][E];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+#pragma unroll
+      for (int i = 0; i < E; ++i) x[u][i] = sx[(k + u) * E + i];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+#pragma unroll
+      for (int i = 0; i < E; ++i) acc[i] = fadd(acc[i], x[u][i]);
+  }
+  for (; k < k1; ++k)
+#pragma unroll
+    for (int i = 0; i < E; ++i) acc[i] = fadd(acc[i], sx[k * E + i]);
+#pragma unroll
+  for (int i = 0; i < E; ++i) grad[v * E + i] = acc[i];
+}
+
+__global__ void k_emb_walk(const uint16_t* __restrict__ order, const int* __restrict__ offs,
+                           const float* __restrict__ dx, float* grad, int V, int E) {
+  pdl_wait();
+  const int id = blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= V * E) return;
+  const int v = id / E, i = id % E;
+  const int k0 = offs[v], k1 = offs[v + 1];
+  float acc = grad[id];
+  constexpr int kU = 8;
+  int k = k0;
+  for (; k + kU <= k1; k += kU) {
+    float x[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) x[u] = __ldg(dx + int64_t(order[k + u]) * E + i);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) acc = fadd(acc, x[u]);
+  }
+  for (; k < k1; ++k) acc = fadd(acc, __ldg(dx + int64_t(order[k]) * E + i));
+  grad[id] = acc;
 }
 
 __global__ void k_tanh_vec(float* x, int64_t n) {
@@ -842,10 +1373,118 @@ __global__ void k_pos_advance(int64_t* pos, int64_t by) {
 }  // namespace
 
 void launch_sprm_prep(const uint32_t* tokens, const int64_t* pos, const SprmP& s, uint32_t* ctx,
-                      float* X, float* tab, cudaStream_t st) {
+                      float* X, float* tab, float* Xtm, unsigned* cnt, cudaStream_t st) {
   const int64_t n = std::max<int64_t>(std::max<int64_t>(int64_t(s.R) * s.T, 6ll * s.V * s.H),
                                       2ll * s.Es * s.R * s.T);
-  launch_pdl(k_sprm_prep, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, tokens, pos, s, ctx, X, tab);
+  launch_pdl(k_sprm_prep, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, tokens, pos, s, ctx, X, tab,
+             Xtm, cnt);
+}
+
+// Off by default (PMKLC_SPRM_STREAM=1 enables it): measured on the B200 the
+// consumers advance ~4 us per step against BPTT's ~1 us, so the streamed
+// reductions end ~120 us after BPTT instead of ~62 us for transpose + batched
+// NT. Kept, parity-green, for further work.
+bool sprm_stream_ok(const SprmP& s) {
+  static const bool on = [] {
+    const char* e = std::getenv("PMKLC_SPRM_STREAM");
+    return e && std::atoi(e) != 0;
+  }();
+  return on && s.H == 32 && s.Es >= 1 && s.Es <= 8 && (s.Es % 2 == 0) &&
+         size_t(2) * s.R * (64 + s.Es) * sizeof(float) <= 200 * 1024;
+}
+
+// consumer warp table of the streamed BPTT (see k_sprm_bptt_stream): per
+// (direction, gate slab) the output rows in pairs of one kind, 4 warps a block
+struct NtSPlan {
+  std::vector<NtSWarp> warps;
+  std::vector<int> block_dg;
+};
+static NtSPlan nt_stream_plan(const SprmP& s, float* g, const int64_t* hoffs) {
+  NtSPlan pl;
+  const int H = s.H, Es = s.Es;
+  auto G = [&](int d, int t) { return g + hoffs[1 + d * NG + t]; };
+  for (int d = 0; d < 2; ++d)
+    for (int gate = 0; gate < 4; ++gate) {
+      std::vector<NtSWarp> ws;
+      auto pairs = [&](int kind, int n, float* W) {
+        for (int p = 0; p < n; p += 2) {
+          NtSWarp w{};
+          w.g = gate;
+          w.r0 = NtSRow{kind, p, W + int64_t(p) * H, nullptr};
+          w.r1 = p + 1 < n ? NtSRow{kind, p + 1, W + int64_t(p + 1) * H, nullptr}
+                           : NtSRow{-1, 0, nullptr, nullptr};
+          ws.push_back(w);
+        }
+      };
+      const int wi = gate == 0 ? WIN : gate == 1 ? WIR : WIZ;
+      const int wh = gate == 3 ? WHN : gate == 1 ? WHR : WHZ;
+      const int bi = gate == 0 ? BIN : gate == 1 ? BIR : BIZ;
+      const int bh = gate == 3 ? BHN : gate == 1 ? BHR : BHZ;
+      if (gate != 3) pairs(0, Es, G(d, wi));
+      if (gate != 0) pairs(1, H, G(d, wh));
+      NtSWarp wb{};
+      wb.g = gate;
+      // the bias rows: sum of the gate gradient (b_in / b_hn alone; b_ir and
+      // b_hr, b_iz and b_hz are the same chain, stored twice)
+      float* b0 = gate == 3 ? G(d, bh) : G(d, bi);
+      float* b1 = (gate == 1 || gate == 2) ? G(d, bh) : nullptr;
+      wb.r0 = NtSRow{2, 0, b0, b1};
+      wb.r1 = NtSRow{-1, 0, nullptr, nullptr};
+      ws.push_back(wb);
+      for (size_t i = 0; i < ws.size(); i += kStreamConsumers) {
+        int need_h = 0, need_x = 0;
+        for (int k = 0; k < kStreamConsumers; ++k) {
+          NtSWarp w{};
+          w.g = gate;
+          w.r0 = w.r1 = NtSRow{-1, 0, nullptr, nullptr};
+          const NtSWarp& x = i + k < ws.size() ? ws[i + k] : w;
+          need_h |= (x.r0.kind == 1 || x.r1.kind == 1) ? 1 : 0;
+          need_x |= (x.r0.kind == 0 || x.r1.kind == 0) ? 1 : 0;
+          pl.warps.push_back(x);
+        }
+        pl.block_dg.push_back(d * 4 + gate + (need_h << 8) + (need_x << 9));
+      }
+    }
+  return pl;
+}
+
+size_t sprm_stream_table_bytes(const SprmP& s) {
+  const NtSPlan pl = nt_stream_plan(s, nullptr, std::vector<int64_t>(1 + 2 * NG, 0).data());
+  return pl.warps.size() * sizeof(NtSWarp) + pl.block_dg.size() * sizeof(int);
+}
+
+void sprm_stream_table(const SprmP& s, float* g, const int64_t* hoffs, void* host_buf) {
+  const NtSPlan pl = nt_stream_plan(s, g, hoffs);
+  unsigned char* b = static_cast<unsigned char*>(host_buf);
+  std::memcpy(b, pl.warps.data(), pl.warps.size() * sizeof(NtSWarp));
+  std::memcpy(b + pl.warps.size() * sizeof(NtSWarp), pl.block_dg.data(), pl.block_dg.size() * sizeof(int));
+}
+
+void launch_sprm_bptt_stream(const SprmP& s, const float* tape, const float* dfin, float* Gt,
+                             const float* Xtm, unsigned* cnt, const void* d_table, cudaStream_t st,
+                             cudaStream_t side) {
+  const NtSPlan pl = nt_stream_plan(s, nullptr, std::vector<int64_t>(1 + 2 * NG, 0).data());
+  NtSParams q{};
+  q.tape = tape;
+  q.dfin = dfin;
+  q.Gt = Gt;
+  q.Xtm = Xtm;
+  q.cnt = cnt;
+  q.warps = static_cast<const NtSWarp*>(d_table);
+  q.block_dg = reinterpret_cast<const int*>(static_cast<const unsigned char*>(d_table) +
+                                            pl.warps.size() * sizeof(NtSWarp));
+  q.nb_bptt = 0;
+  static const int variant = [] {
+    const char* e = std::getenv("PMKLC_NT_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  q.variant = variant;
+  const size_t smem = size_t(2) * s.R * (2 * s.H + s.Es) * sizeof(float);
+  ensure_smem(reinterpret_cast<const void*>(k_sprm_nt_stream), smem);
+  launch_pdl(k_sprm_nt_stream, dim3(unsigned(pl.block_dg.size())), dim3((kStreamConsumers + 1) * 32),
+             smem, side, s, q);
+  launch_pdl(k_sprm_bptt32, dim3(unsigned(2 * ((s.R + kBpttWarps - 1) / kBpttWarps))),
+             dim3(kBpttWarps * 32), 0, st, s, tape, dfin, Gt, cnt);
 }
 void launch_sprm_fwd(const SprmP& s, const uint32_t* ctx, const float* tab, float* tape, float* fin,
                      cudaStream_t st) {
@@ -880,7 +1519,7 @@ void launch_sprm_bptt(const SprmP& s, const float* tape, const float* dfin, floa
                       cudaStream_t st) {
   if (s.H == 32)
     launch_pdl(k_sprm_bptt32, dim3(unsigned(2 * ((s.R + kBpttWarps - 1) / kBpttWarps))), dim3(kBpttWarps * 32), 0, st, 
-        s, tape, dfin, Gt);
+        s, tape, dfin, Gt, static_cast<unsigned*>(nullptr));
   else if (s.H == 64 || s.H == 128) {
     const dim3 wgrid(unsigned(2 * ((s.R + kWideWarps - 1) / kWideWarps)));
     if (s.H == 64) {
@@ -901,10 +1540,11 @@ void launch_sprm_transpose(const SprmP& s, const float* Gt, float* G, cudaStream
   launch_pdl(k_sprm_transpose, dim3(grid), dim3(dim3(32, 8)), 0, st, s, Gt, G);
 }
 bool sprm_dx_time_major(const SprmP& s) { return s.H == 32 && s.Es <= 8; }
-void launch_sprm_dx(const SprmP& s, const float* G, const float* Gt, float* dx, cudaStream_t st) {
+void launch_sprm_dx(const SprmP& s, const float* G, const float* Gt, float* dx, cudaStream_t st,
+                    const uint16_t* rank) {
   const int64_t n = int64_t(s.R) * s.T * s.Es;
   if (sprm_dx_time_major(s) && Gt) {
-    launch_pdl(k_sprm_dx_t, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, s, Gt, dx);
+    launch_pdl(k_sprm_dx_t, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, s, Gt, dx, rank);
     return;
   }
   launch_pdl(k_sprm_dx, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, s, G, dx);
@@ -912,10 +1552,50 @@ void launch_sprm_dx(const SprmP& s, const float* G, const float* Gt, float* dx, 
 void launch_sprm_head(const SprmP& s, const uint32_t* tokens, const int64_t* pos, const float* fin,
                       const float* w1, const float* b1, const float* w2, const float* b2, float* bact,
                       float* g, float* dbact, float* dfin, cudaStream_t st) {
-  const size_t smem = size_t(kHeadWarps) * (2 * s.H + 2 * s.B + s.V) * sizeof(float);
-  ensure_smem(reinterpret_cast<const void*>(k_sprm_head), smem);
-  launch_pdl(k_sprm_head, dim3(unsigned((s.R + kHeadWarps - 1) / kHeadWarps)), dim3(kHeadWarps * 32), smem,
-             st, s, tokens, pos, fin, w1, b1, w2, b2, bact, g, dbact, dfin);
+  const size_t rows_smem = size_t(kHeadWarps) * (2 * s.H + 2 * s.B + s.V) * sizeof(float);
+  const size_t w_smem = size_t(head_w_floats(2 * s.H, s.B, s.V)) * sizeof(float);
+  const dim3 grid(unsigned((s.R + kHeadWarps - 1) / kHeadWarps)), block(kHeadWarps * 32);
+  if (w_smem + rows_smem <= 64 * 1024) {
+    ensure_smem(reinterpret_cast<const void*>(k_sprm_head<true>), w_smem + rows_smem);
+    launch_pdl(k_sprm_head<true>, grid, block, w_smem + rows_smem, st, s, tokens, pos, fin, w1, b1, w2,
+               b2, bact, g, dbact, dfin);
+  } else {
+    ensure_smem(reinterpret_cast<const void*>(k_sprm_head<false>), rows_smem);
+    launch_pdl(k_sprm_head<false>, grid, block, rows_smem, st, s, tokens, pos, fin, w1, b1, w2, b2,
+               bact, g, dbact, dfin);
+  }
+}
+bool sprm_sorted_emb_ok(const SprmP& s) { return s.V <= kSortMaxTok && s.R * s.T <= 65536; }
+void launch_tok_sort(const uint32_t* ctx, int n, int V, uint16_t* order, int* offs, uint16_t* rank,
+                     cudaStream_t st) {
+  launch_pdl(k_tok_sort, dim3(1), dim3(kSortBlock), 0, st, ctx, n, V, order, offs, rank);
+}
+bool launch_emb_walk_sorted(const int* offs, const float* dxs, float* grad, int V, int E, int n,
+                            cudaStream_t st) {
+  const size_t smem = size_t(n) * E * sizeof(float);
+  if (V <= 1024 && (n * E) % 4 == 0 && smem <= 200 * 1024 && (E == 2 || E == 4 || E == 8)) {
+    const void* k = E == 4 ? reinterpret_cast<const void*>(k_emb_walk_smem<4>)
+                   : E == 8 ? reinterpret_cast<const void*>(k_emb_walk_smem<8>)
+                            : reinterpret_cast<const void*>(k_emb_walk_smem<2>);
+    ensure_smem(k, smem);
+    const dim3 b(unsigned(std::max(V, 256)));
+    if (E == 4) launch_pdl(k_emb_walk_smem<4>, dim3(1), b, smem, st, offs, dxs, grad, V, n);
+    else if (E == 8) launch_pdl(k_emb_walk_smem<8>, dim3(1), b, smem, st, offs, dxs, grad, V, n);
+    else launch_pdl(k_emb_walk_smem<2>, dim3(1), b, smem, st, offs, dxs, grad, V, n);
+    return true;
+  }
+  const dim3 g(unsigned((V + 63) / 64)), b(64);
+  switch (E) {
+    case 4: launch_pdl(k_emb_walk_sorted<4>, g, b, 0, st, offs, dxs, grad, V); return true;
+    case 8: launch_pdl(k_emb_walk_sorted<8>, g, b, 0, st, offs, dxs, grad, V); return true;
+    case 2: launch_pdl(k_emb_walk_sorted<2>, g, b, 0, st, offs, dxs, grad, V); return true;
+    default: return false;
+  }
+}
+void launch_emb_walk(const uint16_t* order, const int* offs, const float* dx, float* grad, int V,
+                     int E, cudaStream_t st) {
+  launch_pdl(k_emb_walk, dim3(unsigned((V * E + 127) / 128)), dim3(128), 0, st, order, offs, dx, grad,
+             V, E);
 }
 void launch_tanh_vec(float* x, int64_t n, cudaStream_t st) {
   launch_pdl(k_tanh_vec, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, x, n);
