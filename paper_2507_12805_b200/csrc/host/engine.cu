@@ -408,6 +408,11 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
                 s_rv = int64_t(R) * V, s_cum = int64_t(R) * (V + 1), s_re = int64_t(R) * E;
   const size_t TW = S;  // tapes indexed by slot
   DBuf<uint32_t> ctx(TW * s_ctx), freq(TW * s_rv), cum(TW * s_cum);
+  // deduplicated K/V (bit-exact): the projections of the T*V distinct
+  // (position, token) inputs instead of all R*T coded positions
+  const bool kv_dedup = attn_rows_ok(dd) && V < R;
+  const int64_t s_xtab = kv_dedup ? int64_t(E) * T * V : 0;
+  DBuf<float> xtab(TW * s_xtab);
   DBuf<float> x(TW * s_x), kk(TW * s_kv), vv(TW * s_kv), q(TW * s_rh), wts(TW * s_w),
       cx(TW * s_rh), ao(TW * s_rh), pre(TW * s_rf), fo(TW * s_rh), lm(TW * s_rv),
       probs(TW * s_rv), dlm(TW * s_rv), aterm(TW * s_rv), lterm(TW * R), dffn(TW * s_rh), dact(TW * s_rf), datt(TW * s_rh),
@@ -605,15 +610,19 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     };
     // ---------------- forward (AttentionModel::forward, models.cpp:122-136)
     launch_embed(d_tokens, geo, w.p, P, oE, oP, ctx.p, s_ctx, x.p, s_x, xl.p, s_re, dd, act, na,
-                 st);
+                 st, kv_dedup ? xtab.p : nullptr, s_xtab);
     ++run.launches;
     // (static predictors of this tick: computed during the previous tick)
     GemmP gp{};
     // K, V over all R*T rows, q over the last position (layers.cpp:437-445)
     // x is feature-major: A(row, e) = xT[e*RT + row]
     // K and V in one launch: two problems over the same x tiles
-    gp = GemmP{x.p, s_x, RT, W_(DmLayout::KW), P, H, kk.p, s_kv, H, W_(DmLayout::KB), P,
-               nullptr, 0, 0, R * T, H, E, 0, 1, 0};
+    if (kv_dedup)  // the T*V table rows t*V + v
+      gp = GemmP{xtab.p, s_xtab, int64_t(T) * V, W_(DmLayout::KW), P, H, kk.p, s_kv, H,
+                 W_(DmLayout::KB), P, nullptr, 0, 0, T * V, H, E, 0, 1, 0};
+    else
+      gp = GemmP{x.p, s_x, RT, W_(DmLayout::KW), P, H, kk.p, s_kv, H, W_(DmLayout::KB), P,
+                 nullptr, 0, 0, R * T, H, E, 0, 1, 0};
     gp.nprob = 2;
     gp.a_ps = 0;
     gp.b_ps = int64_t(lay.off(DmLayout::VW)) - int64_t(lay.off(DmLayout::KW));
@@ -623,7 +632,8 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     gp = GemmP{xl.p, s_re, E, W_(DmLayout::QW), P, H, q.p, s_rh, H, W_(DmLayout::QB), P, nullptr, 0,
                0, R, H, E, 0, 1, 0};
     gemm(gp, false, false);
-    launch_attn_fwd(q.p, kk.p, vv.p, wts.p, cx.p, s_rh, s_kv, s_w, dd, inv_hd, act, na, st);
+    const KvTab kvt = kv_dedup ? KvTab{ctx.p, s_ctx} : KvTab{};
+    launch_attn_fwd(q.p, kk.p, vv.p, wts.p, cx.p, s_rh, s_kv, s_w, dd, inv_hd, act, na, st, kvt);
     ++run.launches;
     gemm(GemmP{cx.p, s_rh, H, W_(DmLayout::OW), P, H, ao.p, s_rh, H, W_(DmLayout::OB), P, nullptr,
                0, 0, R, H, H, 0, 1, 0},
@@ -711,7 +721,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
          false, true);
     const AttnDx fx{W_(DmLayout::KW), W_(DmLayout::VW), P, dx.p, s_x};
     const bool dx_fused = launch_attn_bwd(q.p, kk.p, vv.p, wts.p, dctx.p, dq.p, dk.p, dv.p, s_rh,
-                                          s_kv, s_w, dd, inv_hd, fx, act, na, st);
+                                          s_kv, s_w, dd, inv_hd, fx, act, na, st, kvt);
     ++run.launches;
     // q/k/v projections: weight+bias grads, then dx = dk Wk^T + dv Wv^T, dxl = dq Wq^T
     // dWk|dbk and dWv|dbv: reductions over all R*T rows of feature-major x, dk, dv

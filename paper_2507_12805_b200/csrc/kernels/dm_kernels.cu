@@ -756,7 +756,8 @@ __global__ void __launch_bounds__(kNwWarps * 32) k_gemm_nt_r1(NtBatch nb, const 
 __global__ void k_embed(const uint32_t* __restrict__ tokens, ChunkGeo geo,
                         const float* __restrict__ params, int64_t p_cs, int64_t off_emb,
                         int64_t off_pos, uint32_t* ctx, int64_t ctx_cs, float* xT, int64_t x_cs,
-                        float* xl, int64_t xl_cs, DmDims d, const TickDesc* __restrict__ td) {
+                        float* xl, int64_t xl_cs, DmDims d, const TickDesc* __restrict__ td,
+                        float* xtab, int64_t xtab_cs) {
   pdl_wait();
   // thread per coded position (r, t): one token gather, all E features
   // (x[j] = emb[tok][j] + pos[t][j], feature-major stores coalesced over rt)
@@ -764,6 +765,17 @@ __global__ void k_embed(const uint32_t* __restrict__ tokens, ChunkGeo geo,
   const int c = td->act[blockIdx.y], ch = td->chunk[blockIdx.y];
   const int64_t RT = int64_t(d.R) * d.T;
   const int64_t rt = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (xtab && rt >= RT && rt < RT + int64_t(d.T) * d.V) {
+    // the deduplicated K/V inputs: x for every (position t, token v) pair,
+    // row m = t*V + v of a feature-major [E][T*V] table (same adds as x)
+    const int64_t m = rt - RT, TV = int64_t(d.T) * d.V;
+    const int t = int(m / d.V), v = int(m % d.V);
+    const float* P = params + c * p_cs;
+    for (int j = 0; j < d.E; ++j)
+      xtab[c * xtab_cs + int64_t(j) * TV + m] =
+          fadd(__ldg(P + off_emb + int64_t(v) * d.E + j), __ldg(P + off_pos + int64_t(t) * d.E + j));
+    return;
+  }
   if (rt >= RT) return;
   const int t = int(uint32_t(rt) % uint32_t(d.T)), r = int(uint32_t(rt) / uint32_t(d.T));  // RT < 2^31
   const uint64_t L = geo.L[ch];
@@ -933,6 +945,18 @@ __host__ __device__ inline size_t attn_row_smem(const DmDims& d) {
   return (size_t(2) * d.T * (d.H + 4) + size_t(d.NH) * d.T + 2 * d.H) * sizeof(float);
 }
 
+// K/V rows of a coded row from the deduplicated tables: position t's row
+// is table row t*V + ctx[t] (the (position, token) pair it was computed for)
+__device__ __forceinline__ void stage_rows_tab(float* dst, const float* tab, const uint32_t* ctx_row,
+                                               int T, int H, int V) {
+  const int nv = T * (H / 4);
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    const int t = i / (H / 4), v4 = i % (H / 4);
+    const int64_t row = int64_t(t) * V + int64_t(ctx_row[t]);
+    cp_async16(dst + t * (H + 4) + 4 * v4, tab + row * H + 4 * v4);
+  }
+}
+
 __device__ __forceinline__ void stage_rows(float* dst, const float* src, int T, int H) {
   // src [T][H] contiguous (H multiple of 4) -> dst rows of H+4
   const int nv = T * (H / 4);
@@ -946,7 +970,7 @@ __device__ __forceinline__ void stage_rows(float* dst, const float* src, int T, 
 __global__ void __launch_bounds__(kRowThreads) k_attn_fwd_row(
     const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
     float* wts, float* cx, int64_t cs_q, int64_t cs_kv, int64_t cs_w, DmDims d, float inv,
-    const TickDesc* __restrict__ td) {
+    const TickDesc* __restrict__ td, KvTab kt) {
   pdl_wait();
   extern __shared__ __align__(128) float sm[];
   if (blockIdx.y >= unsigned(td->n_act)) return;
@@ -957,9 +981,15 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_fwd_row(
   float* Vs = Ks + T * HP;
   float* Ws = Vs + T * HP;   // [NH][T]
   float* Qs = Ws + d.NH * T; // [H]
-  const int64_t ko = c * cs_kv + int64_t(r) * T * H;
-  stage_rows(Ks, k + ko, T, H);
-  stage_rows(Vs, v + ko, T, H);
+  if (kt.ctx) {
+    const uint32_t* cr = kt.ctx + c * kt.ctx_cs + int64_t(r) * T;
+    stage_rows_tab(Ks, k + c * cs_kv, cr, T, H, d.V);
+    stage_rows_tab(Vs, v + c * cs_kv, cr, T, H, d.V);
+  } else {
+    const int64_t ko = c * cs_kv + int64_t(r) * T * H;
+    stage_rows(Ks, k + ko, T, H);
+    stage_rows(Vs, v + ko, T, H);
+  }
   cp_async_commit();
   for (int i = threadIdx.x; i < H; i += blockDim.x) Qs[i] = q[c * cs_q + int64_t(r) * H + i];
   cp_async_wait<0>();
@@ -1013,7 +1043,7 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
     const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
     const float* __restrict__ wts, const float* __restrict__ dctx, float* dq, float* dkT,
     float* dvT, int64_t cs_q, int64_t cs_kv, int64_t cs_w, DmDims d, float inv, AttnDx fx,
-    const TickDesc* __restrict__ td) {
+    const TickDesc* __restrict__ td, KvTab kt) {
   pdl_wait();
   extern __shared__ __align__(128) float sm[];
   if (blockIdx.y >= unsigned(td->n_act)) return;
@@ -1033,9 +1063,15 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
   float* Dv = Dk + DP;
   float* Wks = Dv + DP;  // [H][E]
   float* Wvs = Wks + ((d.E * H + 3) & ~3);
-  const int64_t ko = c * cs_kv + int64_t(r) * T * H;
-  stage_rows(Ks, k + ko, T, H);
-  stage_rows(Vs, v + ko, T, H);
+  if (kt.ctx) {
+    const uint32_t* cr = kt.ctx + c * kt.ctx_cs + int64_t(r) * T;
+    stage_rows_tab(Ks, k + c * cs_kv, cr, T, H, d.V);
+    stage_rows_tab(Vs, v + c * cs_kv, cr, T, H, d.V);
+  } else {
+    const int64_t ko = c * cs_kv + int64_t(r) * T * H;
+    stage_rows(Ks, k + ko, T, H);
+    stage_rows(Vs, v + ko, T, H);
+  }
   for (int i = threadIdx.x; i < H; i += blockDim.x) {
     Qs[i] = q[c * cs_q + int64_t(r) * H + i];
     Cs[i] = dctx[c * cs_q + int64_t(r) * H + i];
@@ -1690,23 +1726,28 @@ void launch_gemm_nt(const NtP& p0, const NtP* p1, const TickDesc* td, int max_ac
 void launch_embed(const uint32_t* tokens, ChunkGeo geo, const float* params,
                   int64_t p_cs, int64_t off_emb, int64_t off_pos, uint32_t* ctx, int64_t ctx_cs,
                   float* x, int64_t x_cs, float* xl, int64_t xl_cs, DmDims d, const TickDesc* td,
-                  int max_active, cudaStream_t st) {
+                  int max_active, cudaStream_t st, float* xtab, int64_t xtab_cs) {
   if (max_active <= 0) return;
-  const int64_t total = int64_t(d.R) * d.T;  // one thread per coded position
+  // one thread per coded position (+ one per (t, v) table row)
+  const int64_t total = int64_t(d.R) * d.T + (xtab ? int64_t(d.T) * d.V : 0);
   dim3 grid(unsigned((total + 255) / 256), max_active);
   launch_pdl(k_embed, dim3(grid), dim3(256), 0, st, tokens, geo, params, p_cs, off_emb, off_pos, ctx, ctx_cs, x,
-                                x_cs, xl, xl_cs, d, td);
+                                x_cs, xl, xl_cs, d, td, xtab, xtab_cs);
+}
+
+bool attn_rows_ok(const DmDims& d) {  // both row kernels (forward and backward) are used
+  return d.NH <= 8 && d.H % 4 == 0 && attn_row_smem(d) + d.H * sizeof(float) <= 200 * 1024;
 }
 
 void launch_attn_fwd(const float* q, const float* k, const float* v, float* wts, float* cx,
                      int64_t cs_q, int64_t cs_kv, int64_t cs_w, DmDims d, float inv,
-                     const TickDesc* td, int max_active, cudaStream_t st) {
+                     const TickDesc* td, int max_active, cudaStream_t st, const KvTab& kt) {
   if (max_active <= 0) return;
   const size_t smem = attn_row_smem(d);
   if (d.NH <= 8 && d.H % 4 == 0 && smem <= 200 * 1024) {
     ensure_smem(reinterpret_cast<const void*>(k_attn_fwd_row), smem);
     launch_pdl(k_attn_fwd_row, dim3(dim3(d.R, max_active)), dim3(kRowThreads), smem, st, q, k, v, wts, cx, cs_q, cs_kv,
-                                                                      cs_w, d, inv, td);
+                                                                      cs_w, d, inv, td, kt);
     return;
   }
   const int64_t warps = int64_t(d.R) * d.NH;
@@ -1717,7 +1758,7 @@ void launch_attn_fwd(const float* q, const float* k, const float* v, float* wts,
 bool launch_attn_bwd(const float* q, const float* k, const float* v, const float* wts,
                      const float* dctx, float* dq, float* dk, float* dv, int64_t cs_q,
                      int64_t cs_kv, int64_t cs_w, DmDims d, float inv, const AttnDx& fx,
-                     const TickDesc* td, int max_active, cudaStream_t st) {
+                     const TickDesc* td, int max_active, cudaStream_t st, const KvTab& kt) {
   if (max_active <= 0) return fx.dx != nullptr;
   const size_t base = attn_row_smem(d) + d.H * sizeof(float);
   const size_t extra = (size_t(2) * (d.T * (d.H + 1) + 3) + size_t(2) * (d.E * d.H + 3) + 8) *
@@ -1730,7 +1771,7 @@ bool launch_attn_bwd(const float* q, const float* k, const float* v, const float
     AttnDx f = fx;
     if (!fuse) f.dx = nullptr;
     launch_pdl(k_attn_bwd_row, dim3(dim3(d.R, max_active)), dim3(kRowThreads), smem, st, 
-        q, k, v, wts, dctx, dq, dk, dv, cs_q, cs_kv, cs_w, d, inv, f, td);
+        q, k, v, wts, dctx, dq, dk, dv, cs_q, cs_kv, cs_w, d, inv, f, td, kt);
     return fuse;
   }
   const int64_t warps = int64_t(d.R) * d.NH;

@@ -115,14 +115,26 @@ void launch_tick_peek(const TickDesc* cur, TickDesc* next, const uint32_t* act_p
 void launch_ctx_gather(const uint32_t* tokens, ChunkGeo geo, uint32_t* ctx, int64_t ctx_cs,
                        DmDims d, const TickDesc* td, int max_active, cudaStream_t st);
 // ctx gather (pipeline.cpp:180-182) + Embedding/PositionalEmbedding forward
+// xtab (nullable): also the K/V table inputs x(t, v) = emb[v] + pos[t],
+// feature-major [E][T*V] per chunk slot
 void launch_embed(const uint32_t* tokens, ChunkGeo geo, const float* params,
                   int64_t p_cs, int64_t off_emb, int64_t off_pos, uint32_t* ctx, int64_t ctx_cs,
                   float* xT, int64_t x_cs, float* xl, int64_t xl_cs, DmDims d, const TickDesc* td,
-                  int max_active, cudaStream_t st);
+                  int max_active, cudaStream_t st, float* xtab = nullptr, int64_t xtab_cs = 0);
+// Deduplicated K/V (bit-exact): the K/V row of coded position
+// (r, t) depends only on (t, token), so with ctx set the K/V buffers hold the
+// T*V table rows t*V + v (computed from launch_embed's xtab) and the row
+// kernels gather row t*V + ctx[r][t]; null: K/V hold all R*T rows.
+struct KvTab {
+  const uint32_t* ctx = nullptr;
+  int64_t ctx_cs = 0;
+};
+// the row-blocked attention kernels run (and so the K/V table may be used)
+bool attn_rows_ok(const DmDims& d);
 // Attention forward core: scores, det_softmax, context (layers.cpp:452-470)
 void launch_attn_fwd(const float* q, const float* k, const float* v, float* wts, float* cx,
                      int64_t cs_q, int64_t cs_kv, int64_t cs_w, DmDims d, float inv,
-                     const TickDesc* td, int max_active, cudaStream_t st);
+                     const TickDesc* td, int max_active, cudaStream_t st, const KvTab& kt = {});
 // Attention backward core (layers.cpp:480-512). With fx.dx set it also forms
 // dx = dk W_k^T + dv W_v^T for the row's positions (the two projection-input
 // gradient GEMMs, same chain) and returns true; false: the caller runs them.
@@ -133,7 +145,7 @@ struct AttnDx {
 bool launch_attn_bwd(const float* q, const float* k, const float* v, const float* wts,
                      const float* dctx, float* dq, float* dk, float* dv, int64_t cs_q,
                      int64_t cs_kv, int64_t cs_w, DmDims d, float inv, const AttnDx& fx,
-                     const TickDesc* td, int max_active, cudaStream_t st);
+                     const TickDesc* td, int max_active, cudaStream_t st, const KvTab& kt = {});
 // PositionalEmbedding + Embedding backward (layers.cpp:117-125,147-155)
 void launch_embed_bwd(const uint32_t* ctx, int64_t ctx_cs, const float* dx, int64_t dx_cs,
                       const float* dxl, int64_t dxl_cs, float* grads, int64_t g_cs,
