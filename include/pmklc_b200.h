@@ -226,6 +226,17 @@ int pmklc_run_benchmark(const char* const* paths, size_t n_paths, const pmklc_cf
 /* FNV-1a-64 (bytes.hpp:17-24), the fingerprint/checksum hash of the format */
 uint64_t pmklc_fnv1a64(const uint8_t* p, size_t n);
 
+/* pretrain_public (training.cpp:43-60; TrainConfig training.hpp:10-17) on the
+ * device: n_files corpus files (raw bytes; canonicalized and tokenized like
+ * compress), a seeded 2-layer BiGRU trained for `epochs` sequential passes of
+ * `batch`-row Adam steps over every file; PMKW bytes of the trained public
+ * model (SPuM) in *out (library-allocated). 1 + CorpusEmpty when no file
+ * yields a full context window. train_ms (nullable): device time. */
+int pmklc_pretrain_public(const uint8_t* const* files, const size_t* lens, size_t n_files,
+                          uint32_t s, uint32_t k, uint32_t t, uint32_t batch, uint32_t scale,
+                          uint32_t epochs, uint64_t seed, int32_t device, uint8_t** out,
+                          size_t* out_n, double* train_ms);
+
 /* seeded (untrained) BiGRU predictor file in the reference's PMKW format
  * (BiGruModel + serialize_model, models.cpp:38-51,159-173); layers = 2 is a
  * SPuM as the reference tests write it (acceptance.cpp:58-69). Host-only. */

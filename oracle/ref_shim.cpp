@@ -273,6 +273,26 @@ int pmref_pretrain_private(const uint32_t* tokens, uint64_t m, const char* pub_p
   });
 }
 
+/// pretrain_public (training.cpp:43-60) over n corpus files; PMKW bytes.
+int pmref_pretrain_public(const uint8_t* const* files, const size_t* lens, size_t n, uint32_t s,
+                          uint32_t k, uint32_t t, uint32_t batch, uint32_t scale, uint32_t epochs,
+                          uint64_t seed, uint8_t** out, size_t* out_n) {
+  return guard([&] {
+    std::vector<ByteVec> corpus;
+    for (size_t i = 0; i < n; ++i) corpus.emplace_back(files[i], files[i] + lens[i]);
+    TrainConfig tc;
+    tc.sk = SkParams{uint8_t(s), uint8_t(k)};
+    tc.t = t;
+    tc.batch = batch;
+    tc.scale = scale;
+    tc.epochs = epochs;
+    auto m = pretrain_public(corpus, tc, seed);
+    ByteVec v = serialize_model(*m);
+    *out = dup(v);
+    *out_n = v.size();
+  });
+}
+
 /// Replays ChunkWorker::encode (pipeline.cpp:115-137) over one chunk's tokens
 /// with the reference's public classes and records every model step's mixed
 /// probabilities [steps, bs, vocab] (probs may be null), the payload, and the

@@ -103,7 +103,7 @@ EXPORTS = [
     "pmklc_decompress_dist", "pmklc_dist_plan", "pmklc_stats_release", "pmklc_chunk_count",
     "pmklc_container_chunks", "pmklc_decompress_dist_to_device", "pmklc_compression_ratio",
     "pmklc_throughput", "pmklc_robustness", "pmklc_block_ratios", "pmklc_run_benchmark",
-    "pmklc_fnv1a64", "pmklc_cfg_validate", "pmklc_schedule_slots",
+    "pmklc_fnv1a64", "pmklc_cfg_validate", "pmklc_schedule_slots", "pmklc_pretrain_public",
 ]
 
 _lib = None
@@ -366,6 +366,26 @@ def synth(kind: str, n: int, seed: int, extra: int = 0) -> bytes:
     else:
         raise ValueError(kind)
     return bytes(buf)[:n]
+
+
+def pretrain_public(corpus: Sequence[bytes], s: int = 3, k: int = 3, t: int = 32, batch: int = 64,
+                    scale: int = 4, epochs: int = 2, seed: int = 0, device: int = 0,
+                    timing: Optional[list] = None) -> bytes:
+    """pmklc::pretrain_public (training.cpp:43-60, TrainConfig defaults): the
+    trained 2-layer public model (SPuM) as PMKW bytes, byte-identical to the
+    reference's serialize_model of its result."""
+    n = len(corpus)
+    files = (C.c_char_p * max(n, 1))(*[bytes(f) for f in corpus])
+    lens = (C.c_size_t * max(n, 1))(*[len(f) for f in corpus])
+    out = C.POINTER(C.c_uint8)()
+    on = C.c_size_t()
+    ms = C.c_double()
+    _check(lib().pmklc_pretrain_public(C.cast(files, C.c_void_p), lens, C.c_size_t(n), s, k, t, batch,
+                                       scale, epochs, C.c_uint64(seed), device, C.byref(out),
+                                       C.byref(on), C.byref(ms)))
+    if timing is not None:
+        timing.append(ms.value)
+    return _take(out, on.value)
 
 
 def write_bigru(path: str, k: int, t: int, scale: int, seed: int, layers: int = 2) -> int:

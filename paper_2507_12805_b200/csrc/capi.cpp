@@ -304,6 +304,19 @@ int pmklc_schedule_slots(const uint64_t* lens, size_t n, uint32_t bs, uint32_t t
   });
 }
 
+int pmklc_pretrain_public(const uint8_t* const* files, const size_t* lens, size_t n_files,
+                          uint32_t s, uint32_t k, uint32_t t, uint32_t batch, uint32_t scale,
+                          uint32_t epochs, uint64_t seed, int32_t device, uint8_t** out,
+                          size_t* out_n, double* train_ms) {
+  return guard([&] {
+    std::vector<std::pair<const uint8_t*, size_t>> corpus;
+    for (size_t i = 0; i < n_files; ++i) corpus.push_back({files[i], lens[i]});
+    const Bytes b = pretrain_public(corpus, s, k, t, batch, scale, epochs, seed, device, train_ms);
+    *out = dup(b);
+    *out_n = b.size();
+  });
+}
+
 int pmklc_write_bigru(const char* path, uint32_t k, uint32_t t, uint32_t scale, int32_t layers,
                       uint64_t seed, uint64_t* fingerprint) {
   return guard([&] {

@@ -1106,6 +1106,162 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
   return model;
 }
 
+// The 12 weight-gradient reductions of one BiGRU layer, over (t desc, rows
+// asc) (Gru::backward, layers.cpp:317-329): the input projections against the
+// layer input Xf (In rows), the recurrent ones against h_{t-1} (G slab 4), the
+// bias rows as sums of the gate gradients.
+void gru_layer_nt(const BiGru& model, int layer, float* g, const std::vector<int64_t>& hoffs,
+                  const float* Xf, int In, const float* G, int H, int64_t rt, const TickDesc* td,
+                  cudaStream_t st) {
+  NtP probs[12];
+  auto G_ = [&](int i) { return g + hoffs[size_t(i)]; };
+  for (int d = 0; d < 2; ++d) {
+    const float* Gan = G + (int64_t(0 * 2 + d) * H) * rt;
+    const float* Gar = G + (int64_t(1 * 2 + d) * H) * rt;
+    const float* Gaz = G + (int64_t(2 * 2 + d) * H) * rt;
+    const float* Ghh = G + (int64_t(3 * 2 + d) * H) * rt;
+    const float* Hd = G + (int64_t(4 * 2 + d) * H) * rt;
+    const float* Xd = Xf + int64_t(d) * In * rt;
+    auto idx = [&](int gt) { return model.idx(layer, d, gt); };
+    auto nt = [&](const float* A, int M, const float* Bm, int wg, int bg) {
+      return NtP{A, Bm, G_(idx(wg)), 0, 0, 0, rt, rt, H, M, H, int(rt), G_(idx(bg))};
+    };
+    const NtP six[6] = {nt(Xd, In, Gan, BiGru::WIN, BiGru::BIN), nt(Xd, In, Gar, BiGru::WIR, BiGru::BIR),
+                        nt(Xd, In, Gaz, BiGru::WIZ, BiGru::BIZ), nt(Hd, H, Ghh, BiGru::WHN, BiGru::BHN),
+                        nt(Hd, H, Gar, BiGru::WHR, BiGru::BHR), nt(Hd, H, Gaz, BiGru::WHZ, BiGru::BHZ)};
+    for (int u = 0; u < 6; ++u) probs[d * 6 + u] = six[u];
+  }
+  launch_gemm_nt_batch(probs, 12, td, 1, st);
+}
+
+// pretrain_public (training.cpp:43-60) on the device: a seeded 2-layer BiGRU
+// trained by train_pass (training.cpp:8-41) over every corpus token set, for
+// `epochs` passes, one Adam over all parameters. Per step: layer 0 forward
+// (token-table inputs), its outputs concatenated as layer 1's input
+// (BiGru::forward), layer 1's input projections as exact GEMMs, layer 1
+// forward, the head; backward: layer 1 BPTT from the final-state gradient,
+// its reductions and its input gradient dx1, then layer 0 BPTT with dx1 as
+// the per-step output gradient (gather_add_step), its reductions, dx and the
+// embedding gradient; Adam. Full batches of a set replay one captured graph.
+BiGru train_public_gpu(const std::vector<std::pair<const uint32_t*, uint64_t>>& sets,
+                       const Dims& dims, uint32_t t, uint32_t batch, uint32_t epochs, uint64_t seed,
+                       cudaStream_t st, uint64_t* launches) {
+  const PdlScope pdl(st);
+  BiGru model = BiGru::seeded(dims, 2, seed);
+  const int Es = int(dims.se), H = int(dims.sh), B = int(dims.sb), V = int(dims.V), T = int(t);
+  if (!(H <= 32 || H == 64 || H == 128))
+    raise(errc::config_invalid, "BiGRU training on the GPU supports sp_hidden <= 32, 64 or 128");
+  const int64_t P = int64_t(model.total);
+  DBuf<float> w(P), g(P), mo(P), vo(P);
+  w.upload(model.w.data(), P, st);
+  g.zero(st);
+  mo.zero(st);
+  vo.zero(st);
+  std::vector<int64_t> hoffs;
+  for (const ParamDesc& d : model.ps) hoffs.push_back(int64_t(d.off));
+  DBuf<int64_t> offs(hoffs.size());
+  offs.upload(hoffs.data(), hoffs.size(), st);
+  DBuf<AdamScalars> sc(1);
+  const AdamScalars s0{0, 1.0f, 1.0f, 0.0f, 0.0f, {0, 0}};
+  sc.upload(&s0, 1, st);
+  const int64_t R = batch, RT = R * T;
+  DBuf<uint32_t> ctx(RT);
+  DBuf<float> X0(2 * Es * RT), tab(6 * int64_t(V) * H), tape0(10 * RT * H), tape1(10 * RT * H),
+      fin(R * 2 * H), bact(R * B), gg(R * V), dbact(R * B), dfin(R * 2 * H), Gt0(10 * H * RT),
+      Gt1(10 * H * RT), G0(10 * H * RT), G1(10 * H * RT), x1(RT * 2 * H), xproj(6 * RT * H),
+      X1f(2 * 2 * H * RT), dx1(RT * 2 * H), dx0(RT * Es);
+  DBuf<int64_t> pos(1);
+  DBuf<int> act(1);
+  act.zero(st);
+  DBuf<TickDesc> td(1);
+  const TickDesc tdh{0, act.p, nullptr, 1, 0};
+  td.upload(&tdh, 1, st);
+  auto W_ = [&](int i) { return w.p + hoffs[size_t(i)]; };
+  auto G_ = [&](int i) { return g.p + hoffs[size_t(i)]; };
+  const int b0 = model.bott();
+  uint64_t nl = 0;
+  SideStream side2;
+  auto step = [&](const uint32_t* tok, int rows) {
+    const int64_t rt = int64_t(rows) * T;
+    SprmP sp0{w.p, offs.p, rows, T, Es, H, V, B};
+    SprmP sp1{w.p, offs.p + 2 * BiGru::NG, rows, T, 2 * H, H, V, B};
+    sp1.xproj = xproj.p;
+    // ---- forward (BiGruModel::forward, models.cpp:53-73)
+    launch_sprm_prep(tok, pos.p, sp0, ctx.p, X0.p, tab.p, nullptr, nullptr, st);
+    launch_sprm_fwd(sp0, ctx.p, tab.p, tape0.p, fin.p, st);
+    launch_bigru_concat(tape0.p, x1.p, rows, T, H, st);
+    for (int d = 0; d < 2; ++d)
+      for (int gi = 0; gi < 3; ++gi) {  // b_i + x1.W_i over 2H inputs, ascending (Linear order)
+        GemmP gp{};
+        gp.A = x1.p; gp.lda = 2 * H;
+        gp.B = W_(model.idx(1, d, BiGru::WIR + gi)); gp.ldb = H;
+        gp.C = xproj.p + int64_t(d * 3 + gi) * rt * H; gp.ldc = H;
+        gp.bias = W_(model.idx(1, d, BiGru::BIR + gi));
+        gp.M = int(rt); gp.N = H; gp.K = 2 * H; gp.init = 1;
+        nl += launch_gemm(gp, false, false, td.p, 1, st);
+      }
+    launch_sprm_fwd(sp1, ctx.p, tab.p, tape1.p, fin.p, st);
+    launch_sprm_head(sp0, tok, pos.p, fin.p, W_(b0), W_(b0 + 1), W_(b0 + 2), W_(b0 + 3), bact.p,
+                     gg.p, dbact.p, dfin.p, st);
+    side2.rewind();
+    side2.wait_for(st);
+    GemmP g3{};
+    g3.A = bact.p; g3.lda = B; g3.B = gg.p; g3.ldb = V; g3.C = G_(b0 + 2); g3.ldc = V;
+    g3.M = B; g3.N = V; g3.K = rows; g3.ones_row = 1; g3.init = 2;
+    nl += launch_gemm(g3, true, false, td.p, 1, side2.s);
+    GemmP g5{};
+    g5.A = fin.p; g5.lda = 2 * H; g5.B = dbact.p; g5.ldb = B; g5.C = G_(b0); g5.ldc = B;
+    g5.M = 2 * H; g5.N = B; g5.K = rows; g5.ones_row = 1; g5.init = 2;
+    nl += launch_gemm(g5, true, false, td.p, 1, side2.s);
+    // ---- layer 1 backward (BiGruModel::backward, models.cpp:75-96)
+    launch_sprm_bptt(sp1, tape1.p, dfin.p, Gt1.p, st);
+    launch_sprm_transpose(sp1, Gt1.p, G1.p, st);
+    launch_bigru_xf(x1.p, X1f.p, rows, T, 2 * H, st);
+    gru_layer_nt(model, 1, g.p, hoffs, X1f.p, 2 * H, G1.p, H, rt, td.p, st);
+    launch_sprm_dx(sp1, G1.p, nullptr, dx1.p, st);  // the gradient of layer 0's outputs
+    // ---- layer 0 backward: dx1 enters every step
+    SprmP sp0b = sp0;
+    sp0b.dout = dx1.p;
+    launch_sprm_bptt(sp0b, tape0.p, dfin.p, Gt0.p, st);
+    launch_sprm_transpose(sp0, Gt0.p, G0.p, st);
+    gru_layer_nt(model, 0, g.p, hoffs, X0.p, Es, G0.p, H, rt, td.p, st);
+    launch_sprm_dx(sp0, G0.p, Gt0.p, dx0.p, st);
+    const DmDims ed{rows, T, Es, H, 0, V, 0};
+    launch_emb_grad(ctx.p, 0, dx0.p, 0, g.p, 0, int64_t(hoffs[0]), ed, td.p, 1, st);
+    side2.join_into(st);
+    launch_adam_scalars(sc.p, st);
+    launch_adam(w.p, g.p, mo.p, vo.p, 0, P, sc.p, td.p, 1, st);
+    launch_pos_advance(pos.p, batch, st);
+    nl += 22;
+  };
+  for (uint32_t e = 0; e < epochs; ++e)
+    for (const auto& set : sets) {  // train_pass over one token set
+      const uint64_t m = set.second;
+      const int64_t p0 = t;
+      pos.upload(&p0, 1, st);
+      const uint64_t nsteps = (m - t + batch - 1) / batch, full = (m - t) / batch;
+      if (full > 0) {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        const uint64_t nl0 = nl;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        step(set.first, int(batch));
+        CK(cudaStreamEndCapture(st, &graph));
+        CK(cudaGraphInstantiate(&exec, graph, 0));
+        for (uint64_t i = 0; i < full; ++i) CK(cudaGraphLaunch(exec, st));
+        nl += (nl - nl0) * (full - 1);
+        CK(cudaGraphExecDestroy(exec));
+        CK(cudaGraphDestroy(graph));
+      }
+      if (nsteps > full) step(set.first, int((m - t) - full * batch));
+    }
+  check_launch();
+  CK(cudaMemcpyAsync(model.w.data(), w.p, P * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (launches) *launches += nl;
+  return model;
+}
+
 void nck(ncclResult_t r) {
   if (r != ncclSuccess) raise(errc::cuda_error, std::string("NCCL: ") + nccl().GetErrorString(r));
 }
@@ -1662,6 +1818,44 @@ void skmer_encode_packed_device16(const uint8_t* d_packed, uint64_t n_bases, uin
   launch_skmer_encode_packed16(d_packed, n_bases, s, k, d_tokens, m,
                                static_cast<cudaStream_t>(stream));
   check_launch();
+}
+
+Bytes pretrain_public(const std::vector<std::pair<const uint8_t*, size_t>>& corpus, uint32_t s,
+                      uint32_t k, uint32_t t, uint32_t batch, uint32_t scale, uint32_t epochs,
+                      uint64_t seed, int device, double* train_ms) {
+  if (!(s >= 1 && s <= k && k <= 8)) raise(errc::config_invalid, "window parameters need 1 <= s <= k <= 8");
+  if (batch < 1) raise(errc::config_invalid, "batch must be positive");
+  const Dims dims = Dims::make(uint32_t(1) << (2 * k), t, scale);
+  CK(cudaSetDevice(device));
+  Stream stream(device);
+  cudaStream_t st = stream.s;
+  // canonicalize + tokenize every file on the device (training.cpp:47-51);
+  // files shorter than one context window are skipped
+  std::vector<std::unique_ptr<DBuf<uint32_t>>> toks;
+  std::vector<std::pair<const uint32_t*, uint64_t>> sets;
+  for (const auto& f : corpus) {
+    DBuf<uint8_t> d_raw(f.second + 16);
+    d_raw.upload(f.first, f.second, st);
+    Canon canon;
+    canonicalize_device(d_raw.p, f.second, canon, st);
+    const uint64_t nc = canon.n_codes == 0 && canon.exc_pos.empty() ? f.second : canon.n_codes;
+    const uint64_t m = token_count(nc, s, k);
+    if (m < uint64_t(t) + 1) continue;
+    toks.push_back(std::make_unique<DBuf<uint32_t>>(m + 8));
+    if (canon.exc_pos.empty()) launch_skmer_encode_ascii(d_raw.p, nc, s, k, toks.back()->p, m, st);
+    else launch_skmer_encode_codes(canon.codes.p, nc, s, k, toks.back()->p, m, st);
+    check_launch();
+    CK(cudaStreamSynchronize(st));
+    sets.push_back({toks.back()->p, m});
+  }
+  if (sets.empty()) raise(errc::corpus_empty, "no corpus file yields a full context window");
+  Event e0, e1;
+  e0.record(st);
+  BiGru model = train_public_gpu(sets, dims, t, batch, epochs, seed, st, nullptr);
+  e1.record(st);
+  CK(cudaStreamSynchronize(st));
+  if (train_ms) *train_ms = Event::ms(e0, e1);
+  return model.serialize();
 }
 
 Bytes seeded_bigru_file(uint32_t k, uint32_t t, uint32_t scale, int layers, uint64_t seed) {

@@ -117,6 +117,13 @@ void skmer_encode_packed_device(const uint8_t* d_packed, uint64_t n_bases, uint3
 void skmer_encode_packed_device16(const uint8_t* d_packed, uint64_t n_bases, uint32_t s, uint32_t k,
                                   uint16_t* d_tokens, void* stream);
 
+// pretrain_public (training.cpp:43-60) on the device: the corpus files'
+// tokens, a seeded 2-layer BiGRU, train_pass over every set for `epochs`
+// passes; returns the PMKW bytes of the trained public model (SPuM)
+Bytes pretrain_public(const std::vector<std::pair<const uint8_t*, size_t>>& corpus, uint32_t s,
+                      uint32_t k, uint32_t t, uint32_t batch, uint32_t scale, uint32_t epochs,
+                      uint64_t seed, int device, double* train_ms = nullptr);
+
 // PMKW bytes of a seeded (untrained) BiGRU predictor (BiGruModel ctor +
 // serialize_model, models.cpp:38-51,159-173): the SPuM file the reference
 // tests and benchmarks use (acceptance.cpp:58-69). Host-only.

@@ -245,9 +245,19 @@ size_t bigru_work_floats(const BiGruP& p);
 // SPrM pre-pass (pretrain_private / train_pass, training.cpp:8-83): one-layer
 // BiGRU trained with Adam over the whole token stream, bs rows per step.
 struct SprmP {
-  const float* w;       // flat parameter array (BiGru layout, 1 layer)
-  const int64_t* offs;  // device param offsets
+  const float* w;       // flat parameter array (BiGru layout)
+  // device param offsets; for a deeper layer l the caller passes offs + 2*l*NG
+  // (NG = 12 GRU tensors per direction), so the kernels' gate lookups land on
+  // that layer (the embedding entry offs[0] is only read for layer 0)
+  const int64_t* offs;
   int R, T, Es, H, V, B;
+  // deeper layers of a multi-layer model (pretrain_public, training.cpp:43-60):
+  // xproj [2][3][R*T][H]: the gate input projections b_i + x.W_i per (row,
+  // position) instead of the per-token table; dout [R][T][2H]: the gradient
+  // of the layer's outputs, added into dh at every step (gather_add_step,
+  // layers.cpp:279) instead of the final-state gradient only
+  const float* xproj = nullptr;
+  const float* dout = nullptr;
 };
 // X (feature-major reduction operand, nullable) and, for the streamed path,
 // Xtm [2][T][R][Es] (time-major GRU inputs) and the zeroed step counters cnt [2][T]
@@ -296,6 +306,10 @@ bool launch_emb_walk_sorted(const int* offs, const float* dxs, float* grad, int 
                             cudaStream_t st);
 void launch_emb_walk(const uint16_t* order, const int* offs, const float* dx, float* grad, int V,
                      int E, cudaStream_t st);
+// 2-layer BiGRU training (pretrain_public): the layer-1 input x1 [R][T][2H]
+// from the layer-0 tape, and its feature-major reduction operand [2][2H][R*T]
+void launch_bigru_concat(const float* tape, float* x1, int R, int T, int H, cudaStream_t st);
+void launch_bigru_xf(const float* x1, float* Xf, int R, int T, int In, cudaStream_t st);
 void launch_tanh_vec(float* x, int64_t n, cudaStream_t st);
 void launch_adam_scalars(AdamScalars* sc, cudaStream_t st);
 void launch_pos_advance(int64_t* pos, int64_t by, cudaStream_t st);

@@ -113,17 +113,29 @@ __global__ void __launch_bounds__(256) k_sprm_fwd(SprmP s, const uint32_t* __res
   if (act) sh[wl][0][j] = 0.0f;
   __syncwarp();
   int cur = 0;
+  const int64_t RTH = int64_t(R) * T * H;
   for (int t = 0; t < T; ++t) {
     const int src_t = d ? (T - 1 - t) : t;
-    const int64_t tok = ctx[int64_t(r) * T + src_t];
     const float* h = sh[wl][cur];
-    float ar = fadd(t0[tok * H + j], bhr);
+    float xr, xz, xn;  // the gates' input projections b_i + x.W_i
+    if (s.xproj) {
+      const float* xp = s.xproj + int64_t(d) * 3 * RTH + (int64_t(r) * T + src_t) * H + j;
+      xr = xp[0];
+      xz = xp[RTH];
+      xn = xp[2 * RTH];
+    } else {
+      const int64_t tok = ctx[int64_t(r) * T + src_t];
+      xr = t0[tok * H + j];
+      xz = t0[int64_t(V) * H + tok * H + j];
+      xn = t0[2 * int64_t(V) * H + tok * H + j];
+    }
+    float ar = fadd(xr, bhr);
     for (int q = 0; q < H; ++q) ar = mac(ar, h[q], sw[0][q][j]);
-    float az = fadd(t0[int64_t(V) * H + tok * H + j], bhz);
+    float az = fadd(xz, bhz);
     for (int q = 0; q < H; ++q) az = mac(az, h[q], sw[1][q][j]);
     float hh = bhn;
     for (int q = 0; q < H; ++q) hh = mac(hh, h[q], sw[2][q][j]);
-    const float an = t0[2 * int64_t(V) * H + tok * H + j];
+    const float an = xn;
     const float rv = det_sigmoid(ar), zv = det_sigmoid(az);
     const float nv = det_tanh(fadd(an, fmul(rv, hh)));
     const float hv = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, h[j]));
@@ -182,8 +194,16 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_sprm_fwd32(SprmP s, const ui
   float* th = tape + (int64_t(3 * 2 + d) * TRH);
   float* to = tape + (int64_t(4 * 2 + d) * TRH);
   sh[wl][0][j] = 0.0f;
+  const int64_t RTH = int64_t(R) * T * H;
   auto fetch = [&](int t, float (&x)[3]) {
     const int src_t = d ? (T - 1 - t) : t;
+    if (s.xproj) {  // deeper layer: per-(row, position) input projections
+      const float* xp = s.xproj + int64_t(d) * 3 * RTH + (int64_t(r) * T + src_t) * H + j;
+      x[0] = xp[0];
+      x[1] = xp[RTH];
+      x[2] = xp[2 * RTH];
+      return;
+    }
     const int64_t k0 = ctx[int64_t(r) * T + src_t];
     x[0] = t0[k0 * H + j];
     x[1] = t0[int64_t(V) * H + k0 * H + j];
@@ -276,17 +296,20 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_sprm_fwd_wide(SprmP s, cons
   float* to = tape + (int64_t(4 * 2 + d) * TRH);
   __syncwarp();
   int cur = 0;
+  const int64_t RTH = int64_t(R) * T * H;
   for (int t = 0; t < T; ++t) {
     const int src_t = d ? (T - 1 - t) : t;
-    const int64_t tok = ctx[int64_t(r) * T + src_t];
+    // the gates' input projections: per-token table, or per-(row, position)
+    const float* xg = s.xproj ? s.xproj + int64_t(d) * 3 * RTH + (int64_t(r) * T + src_t) * H
+                              : t0 + int64_t(ctx[int64_t(r) * T + src_t]) * H;
+    const int64_t gs = s.xproj ? RTH : int64_t(V) * H;  // gate stride
     const float* h = hb + cur * H;
     f2_t ar[P2], az[P2], hh[P2];
 #pragma unroll
     for (int v = 0; v < P2; ++v) {
       const int j0 = lane + 64 * v, j1 = j0 + 32;
-      ar[v] = f2_pack(fadd(t0[tok * H + j0], bhr[2 * v]), fadd(t0[tok * H + j1], bhr[2 * v + 1]));
-      az[v] = f2_pack(fadd(t0[int64_t(V) * H + tok * H + j0], bhz[2 * v]),
-                      fadd(t0[int64_t(V) * H + tok * H + j1], bhz[2 * v + 1]));
+      ar[v] = f2_pack(fadd(xg[j0], bhr[2 * v]), fadd(xg[j1], bhr[2 * v + 1]));
+      az[v] = f2_pack(fadd(xg[gs + j0], bhz[2 * v]), fadd(xg[gs + j1], bhz[2 * v + 1]));
       hh[v] = f2_pack(bhn[2 * v], bhn[2 * v + 1]);
     }
     for (int q = 0; q < H; ++q) {
@@ -305,7 +328,7 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_sprm_fwd_wide(SprmP s, cons
       const float arv = (u & 1) ? f2_hi(ar[v]) : f2_lo(ar[v]);
       const float azv = (u & 1) ? f2_hi(az[v]) : f2_lo(az[v]);
       const float hhv = (u & 1) ? f2_hi(hh[v]) : f2_lo(hh[v]);
-      const float an = t0[2 * int64_t(V) * H + tok * H + j];
+      const float an = xg[2 * gs + j];
       const float rv = det_sigmoid(arv), zv = det_sigmoid(azv);
       const float nv = det_tanh(fadd(an, fmul(rv, hhv)));
       hn[u] = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, h[j]));
@@ -364,14 +387,17 @@ __global__ void __launch_bounds__(kWideWarps * 32) k_sprm_bptt_wide(SprmP s, con
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     dh[u] = 0.0f;
-    dlast[u] = fadd(0.0f, dfin[int64_t(r) * 2 * H + d * H + lane + 32 * u]);
+    dlast[u] = s.dout ? 0.0f : fadd(0.0f, dfin[int64_t(r) * 2 * H + d * H + lane + 32 * u]);
   }
   for (int t = T - 1; t >= 0; --t) {
     float dn[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = lane + 32 * u;
-      dh[u] = fadd(dh[u], t == T - 1 ? dlast[u] : 0.0f);  // gather_add_step(dout, t, dh)
+      // gather_add_step(dout, t, dh)
+      const float dadd = s.dout ? s.dout[(int64_t(r) * T + (d ? T - 1 - t : t)) * 2 * H + d * H + j]
+                                : (t == T - 1 ? dlast[u] : 0.0f);
+      dh[u] = fadd(dh[u], dadd);
       const int64_t o = (int64_t(t) * R + r) * H + j;
       const float rv = tp[0][o], zv = tp[1][o], nv = tp[2][o], hhv = tp[3][o];
       const float hprev = t == 0 ? 0.0f : tp[4][o - int64_t(R) * H];
@@ -634,10 +660,15 @@ __global__ void __launch_bounds__(256) k_sprm_bptt(SprmP s, const float* __restr
   float* ghp = Gt + int64_t(4 * 2 + d) * TRH;
   // only the GRU's last own step receives the final-state gradient
   // (final_state_backward, layers.cpp:401-413), as 0 + dfin
-  const float dlast = fadd(0.0f, dfin[int64_t(r) * 2 * H + d * H + j]);
+  const float dlast = s.dout ? 0.0f : fadd(0.0f, dfin[int64_t(r) * 2 * H + d * H + j]);
   float dh = 0.0f;
   for (int t = T - 1; t >= 0; --t) {
-    dh = fadd(dh, t == T - 1 ? dlast : 0.0f);  // gather_add_step(dout, t, dh)
+    // gather_add_step(dout, t, dh): the output gradient of this own step
+    // (a deeper layer's dx at position src_t, half d), else the final-state
+    // gradient at the last step
+    const float dadd = s.dout ? s.dout[(int64_t(r) * T + (d ? T - 1 - t : t)) * 2 * H + d * H + j]
+                              : (t == T - 1 ? dlast : 0.0f);
+    dh = fadd(dh, dadd);
     const int64_t o = (int64_t(t) * R + r) * H + j;
     const float rv = tr[o], zv = tz[o], nv = tn[o], hhv = th[o];
     const float hprev = t == 0 ? 0.0f : to[o - int64_t(R) * H];
@@ -715,7 +746,7 @@ __global__ void __launch_bounds__(kBpttWarps * 32) k_sprm_bptt32(SprmP s, const 
   float* ghp = Gt + int64_t(4 * 2 + d) * TRH;
   // only the GRU's last own step receives the final-state gradient
   // (final_state_backward, layers.cpp:401-413), as 0 + dfin
-  const float dlast = fadd(0.0f, dfin[int64_t(r) * 2 * H + d * H + j]);
+  const float dlast = s.dout ? 0.0f : fadd(0.0f, dfin[int64_t(r) * 2 * H + d * H + j]);
   auto fetch = [&](int t, float (&x)[5]) {
     const int64_t o = (int64_t(t) * R + r) * H + j;
 #pragma unroll
@@ -727,7 +758,11 @@ __global__ void __launch_bounds__(kBpttWarps * 32) k_sprm_bptt32(SprmP s, const 
   float dh = 0.0f;
   for (int t = T - 1; t >= 0; --t) {
     if (t > 0) fetch(t - 1, xn);
-    dh = fadd(dh, t == T - 1 ? dlast : 0.0f);  // gather_add_step(dout, t, dh)
+    // gather_add_step(dout, t, dh): a deeper layer's output gradient at
+    // position src_t (half d), else the final-state gradient at the last step
+    const float dadd = s.dout ? s.dout[(int64_t(r) * T + (d ? T - 1 - t : t)) * 2 * H + d * H + j]
+                              : (t == T - 1 ? dlast : 0.0f);
+    dh = fadd(dh, dadd);
     const float rv = xc[0], zv = xc[1], nv = xc[2], hhv = xc[3], hprev = xc[4];
     const float dzv = fmul(dh, fsub(hprev, nv));
     const float danv = fmul(fmul(dh, fsub(1.0f, zv)), fsub(1.0f, fmul(nv, nv)));
@@ -1350,6 +1385,37 @@ __global__ void k_emb_walk(const uint16_t* __restrict__ order, const int* __rest
   grad[id] = acc;
 }
 
+// Layer-1 input of a 2-layer BiGRU (BiGru::forward output concat,
+// layers.cpp:355-366): x1[r][pos] = [h_fwd(own time pos) | h_bwd(own time T-1-pos)]
+__global__ void k_bigru_concat(const float* __restrict__ tape, float* x1, int R, int T, int H) {
+  pdl_wait();
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t n = int64_t(R) * T * 2 * H;
+  if (i >= n) return;
+  const int j2 = int(i % (2 * H));
+  const int64_t rp = i / (2 * H);
+  const int r = int(rp / T), pos = int(rp % T);
+  const int d = j2 >= H ? 1 : 0, j = j2 - d * H;
+  const int t = d ? T - 1 - pos : pos;
+  const int64_t TRH = int64_t(T) * R * H;
+  x1[i] = tape[int64_t(4 * 2 + d) * TRH + (int64_t(t) * R + r) * H + j];
+}
+
+// feature-major reduction operand of a deeper layer's input: Xf[d][i][k],
+// k = (T-1-t)*R + r, = x1 at the direction's own time t (position src_t)
+__global__ void k_bigru_xf(const float* __restrict__ x1, float* Xf, int R, int T, int In) {
+  pdl_wait();
+  const int64_t RT = int64_t(R) * T;
+  const int64_t id = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (id >= 2 * In * RT) return;
+  const int64_t k = id % RT;
+  const int64_t rest = id / RT;
+  const int i = int(rest % In), d = int(rest / In);
+  const int t = int(T - 1 - k / R), r = int(k % R);
+  const int src_t = d ? (T - 1 - t) : t;
+  Xf[id] = x1[(int64_t(r) * T + src_t) * In + i];
+}
+
 __global__ void k_tanh_vec(float* x, int64_t n) {
   pdl_wait();
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1596,6 +1662,14 @@ void launch_emb_walk(const uint16_t* order, const int* offs, const float* dx, fl
                      int E, cudaStream_t st) {
   launch_pdl(k_emb_walk, dim3(unsigned((V * E + 127) / 128)), dim3(128), 0, st, order, offs, dx, grad,
              V, E);
+}
+void launch_bigru_concat(const float* tape, float* x1, int R, int T, int H, cudaStream_t st) {
+  const int64_t n = int64_t(R) * T * 2 * H;
+  launch_pdl(k_bigru_concat, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, tape, x1, R, T, H);
+}
+void launch_bigru_xf(const float* x1, float* Xf, int R, int T, int In, cudaStream_t st) {
+  const int64_t n = 2ll * In * R * T;
+  launch_pdl(k_bigru_xf, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, x1, Xf, R, T, In);
 }
 void launch_tanh_vec(float* x, int64_t n, cudaStream_t st) {
   launch_pdl(k_tanh_vec, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, x, n);

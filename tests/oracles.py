@@ -201,6 +201,18 @@ class Checker:
         f.restype = C.c_uint64
         return int(f(b, C.c_size_t(len(b))))
 
+    def pretrain_public(self, corpus, s=3, k=3, t=32, batch=64, scale=4, epochs=2, seed=0) -> bytes:
+        """pmklc::pretrain_public (training.cpp:43-60): PMKW bytes of the trained SPuM."""
+        n = len(corpus)
+        files = (C.c_char_p * max(n, 1))(*[bytes(f) for f in corpus])
+        lens = (C.c_size_t * max(n, 1))(*[len(f) for f in corpus])
+        out = C.POINTER(C.c_uint8)()
+        on = C.c_size_t()
+        self._check(self._f("pretrain_public")(C.cast(files, C.c_void_p), lens, C.c_size_t(n), s, k, t,
+                                               batch, scale, epochs, C.c_uint64(seed), C.byref(out),
+                                               C.byref(on)))
+        return self._take(out, on.value)
+
     def synth(self, kind: str, n: int, seed: int, extra: int = 0) -> bytes:
         """Seeded benchmark inputs (the generators of host/synth.cpp, built
         into the checker library): markov3 | uniform | genome | species."""

@@ -486,3 +486,25 @@ def test_sprm_prepass_wide_scales(P, checker, tmp_path, scale, with_pub):
     assert blob[5] == 6
     assert blob == want
     assert P.decompress(blob, kw.get("pub_path", "")) == raw
+
+
+@pytest.mark.parametrize("kw", [dict(t=8, batch=16, scale=16), dict(t=8, batch=24, scale=4),
+                                dict(t=6, batch=16, scale=2, epochs=1)])
+def test_pretrain_public_matches_reference(P, checker, tmp_path, kw):
+    # pretrain_public (training.cpp:43-60): the 2-layer public model trained on
+    # a corpus (a too-short file is skipped), byte-identical PMKW to the
+    # reference's; the trained SPuM then codes like the reference's
+    corpus = [P.synth("markov3", 4000, 81), P.synth("genome", 2500, 82, 2) + b"\n>x\nNNacgt\n",
+              b"ACGTACGT", P.synth("uniform", 1500, 83)]
+    want = checker.pretrain_public(corpus, seed=0x5EED, **kw)
+    got = P.pretrain_public(corpus, seed=0x5EED, **kw)
+    assert got == want
+    path = str(tmp_path / "trained.bin")
+    open(path, "wb").write(got)
+    raw = P.synth("markov3", 9000, 84)
+    ckw = dict(t=kw["t"], bs=16, scale=kw["scale"], workers=2)
+    blob = P.compress(raw, P.CompressConfig(pub_model_path=path, **ckw))
+    assert blob[5] == 5 and blob == checker.compress(raw, O.make_cfg(pub_path=path, **ckw))
+    with pytest.raises(P.PmklcError) as e:
+        P.pretrain_public([b"ACGT"], t=8, batch=16, scale=16)
+    assert e.value.errc == "CorpusEmpty"
