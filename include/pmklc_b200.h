@@ -108,6 +108,16 @@ int pmklc_decompress_to_device(const uint8_t* in, size_t n, const char* pub_mode
                                int32_t device, uint8_t** d_out, size_t* out_n,
                                pmklc_timing* timing);
 
+/* file to file with bounded host memory: the input streams
+ * from the file into HBM through a pinned double buffer of block_bytes (0 =
+ * 64 MiB; the read of one block overlaps the copy of the previous), the
+ * container is written to out_path; decompress streams the decoded bytes from
+ * HBM to out_path the same way. Same container as pmklc_compress. */
+int pmklc_compress_file(const char* in_path, const char* out_path, const pmklc_cfg* cfg,
+                        size_t block_bytes, pmklc_timing* timing);
+int pmklc_decompress_file(const char* in_path, const char* out_path, const char* pub_model_path,
+                          int32_t device, size_t block_bytes, pmklc_timing* timing);
+
 /* encode_chunk_standalone over n_chunks chunks at once: chunk i codes
  * tokens[off_i, off_i + chunk_len[i]) (off_i = prefix sum) from inbound
  * snapshot i (length 0 = seeded init). payloads[i] is library-allocated.

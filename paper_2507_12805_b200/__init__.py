@@ -104,6 +104,7 @@ EXPORTS = [
     "pmklc_container_chunks", "pmklc_decompress_dist_to_device", "pmklc_compression_ratio",
     "pmklc_throughput", "pmklc_robustness", "pmklc_block_ratios", "pmklc_run_benchmark",
     "pmklc_fnv1a64", "pmklc_cfg_validate", "pmklc_schedule_slots", "pmklc_pretrain_public",
+    "pmklc_compress_file", "pmklc_decompress_file",
 ]
 
 _lib = None
@@ -187,6 +188,25 @@ def compress(raw: bytes, cfg: CompressConfig = CompressConfig(),
         stats.workers = _worker_stats(st, min(nch.value, cap))
         stats.timing = tm
     return _take(out, n.value)
+
+
+def compress_file(in_path: str, out_path: str, cfg: CompressConfig = CompressConfig(),
+                  block_bytes: int = 0, timing: Optional[Timing] = None) -> None:
+    """File to file with bounded host memory: the input streams into HBM block
+    by block (pinned double buffer, read overlapping copy); same container."""
+    c = cfg._c()
+    tm = timing if timing is not None else Timing()
+    _check(lib().pmklc_compress_file(in_path.encode(), out_path.encode(), C.byref(c),
+                                     C.c_size_t(block_bytes), C.byref(tm)))
+
+
+def decompress_file(in_path: str, out_path: str, pub_model_path: str = "", device: int = 0,
+                    block_bytes: int = 0, timing: Optional[Timing] = None) -> None:
+    """Container file to original file, the output streamed out of HBM block by block."""
+    tm = timing if timing is not None else Timing()
+    _check(lib().pmklc_decompress_file(in_path.encode(), out_path.encode(),
+                                       pub_model_path.encode() if pub_model_path else None, device,
+                                       C.c_size_t(block_bytes), C.byref(tm)))
 
 
 def compress_device(d_ptr: int, n: int, cfg: CompressConfig = CompressConfig(),

@@ -162,6 +162,30 @@ int pmklc_decompress_to_device(const uint8_t* in, size_t n, const char* pub_mode
   });
 }
 
+int pmklc_compress_file(const char* in_path, const char* out_path, const pmklc_cfg* c,
+                        size_t block_bytes, pmklc_timing* timing) {
+  return guard([&] {
+    if (!c || !in_path || !out_path) raise(errc::config_invalid, "null argument");
+    Timing t;
+    CallOptions opt;
+    opt.timing = &t;
+    compress_file(in_path, out_path, to_cfg(c), opt, block_bytes);
+    copy_timing(t, timing);
+  });
+}
+
+int pmklc_decompress_file(const char* in_path, const char* out_path, const char* pub_model_path,
+                          int32_t device, size_t block_bytes, pmklc_timing* timing) {
+  return guard([&] {
+    if (!in_path || !out_path) raise(errc::config_invalid, "null argument");
+    Timing t;
+    CallOptions opt;
+    opt.timing = &t;
+    decompress_file(in_path, out_path, pub_model_path ? pub_model_path : "", device, opt, block_bytes);
+    copy_timing(t, timing);
+  });
+}
+
 int pmklc_encode_chunks(const uint32_t* tokens, const uint64_t* chunk_len, size_t n_chunks,
                         const uint8_t* const* inbound, const size_t* inbound_len, uint32_t flags,
                         const char* pub_model_path, const uint8_t* priv_model, size_t priv_len,

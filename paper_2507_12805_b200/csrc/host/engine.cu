@@ -2029,6 +2029,133 @@ Bytes decompress_dist(const Dist& d, const uint8_t* blob, size_t n, const std::s
   return out;
 }
 
+namespace {
+// pinned double buffer for the file <-> device streams
+struct Pinned {
+  uint8_t* p[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  size_t block = 0;
+  explicit Pinned(size_t b) : block(b) {
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaHostAlloc(reinterpret_cast<void**>(&p[i]), block, cudaHostAllocDefault));
+      CK(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+  }
+  ~Pinned() {
+    for (int i = 0; i < 2; ++i) {
+      if (ev[i]) cudaEventSynchronize(ev[i]), cudaEventDestroy(ev[i]);
+      if (p[i]) cudaFreeHost(p[i]);
+    }
+  }
+};
+struct File {
+  std::FILE* f = nullptr;
+  File(const std::string& path, const char* mode) : f(std::fopen(path.c_str(), mode)) {
+    if (!f) raise(errc::io_error, "cannot open " + path);
+  }
+  ~File() {
+    if (f) std::fclose(f);
+  }
+};
+}  // namespace
+
+void compress_file(const std::string& in_path, const std::string& out_path, const Config& cfg,
+                   const CallOptions& opt, size_t block) {
+  cfg.validate();
+  if (block == 0) block = size_t(64) << 20;
+  CK(cudaSetDevice(cfg.device));
+  Bytes out;
+  double io_ms = 0;
+  {
+    Stream stream(cfg.device);
+    cudaStream_t st = stream.s;
+    File in(in_path, "rb");
+    std::fseek(in.f, 0, SEEK_END);
+    const long ln = std::ftell(in.f);
+    std::fseek(in.f, 0, SEEK_SET);
+    if (ln < 0) raise(errc::io_error, "cannot size " + in_path);
+    const size_t n = size_t(ln);
+    // the input streams from the file into HBM block by block: the read of
+    // block i+1 overlaps the host-to-device copy of block i, and the host
+    // never holds more than two blocks of it
+    Event a, b;
+    a.record(st);
+    DBuf<uint8_t> d_raw(n + 16);
+    {
+      Pinned pin(std::min(block, std::max<size_t>(n, 1)));
+      size_t off = 0;
+      for (int i = 0; off < n; ++i) {
+        const int k = i & 1;
+        CK(cudaEventSynchronize(pin.ev[k]));  // the copy out of this buffer is done
+        const size_t len = std::min(pin.block, n - off);
+        if (std::fread(pin.p[k], 1, len, in.f) != len) raise(errc::io_error, "short read on " + in_path);
+        CK(cudaMemcpyAsync(d_raw.p + off, pin.p[k], len, cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(pin.ev[k], st));
+        off += len;
+      }
+      b.record(st);
+      CK(cudaStreamSynchronize(st));
+    }
+    io_ms = Event::ms(a, b);
+    out = compress_impl(nullptr, d_raw.p, n, cfg, opt);
+  }
+  File of(out_path, "wb");
+  if (!out.empty() && std::fwrite(out.data(), 1, out.size(), of.f) != out.size())
+    raise(errc::io_error, "short write on " + out_path);
+  if (opt.timing) {
+    opt.timing->h2d_ms = io_ms;  // file -> HBM, overlapped read + copy
+    opt.timing->d2h_bytes = out.size();
+  }
+}
+
+void decompress_file(const std::string& in_path, const std::string& out_path,
+                     const std::string& pub_model_path, int device, const CallOptions& opt,
+                     size_t block) {
+  if (block == 0) block = size_t(64) << 20;
+  const Bytes blob = read_file(in_path);
+  CK(cudaSetDevice(device));
+  Stream stream(device);
+  cudaStream_t st = stream.s;
+  DecodeResult res;
+  decompress_impl(blob.data(), blob.size(), pub_model_path, device, opt, res, stream.s);
+  // the decoded bytes stream from HBM to the file block by block: the copy
+  // of block i+1 overlaps the write of block i
+  File of(out_path, "wb");
+  Event a, b;
+  a.record(st);
+  {
+    Pinned pin(std::min(block, std::max<size_t>(res.len, 1)));
+    size_t off = 0, pending = 0, pending_len = 0;
+    bool have = false;
+    for (int i = 0; off < res.len; ++i) {
+      const int k = i & 1;
+      const size_t len = std::min(pin.block, res.len - off);
+      CK(cudaMemcpyAsync(pin.p[k], res.out.p + off, len, cudaMemcpyDeviceToHost, st));
+      CK(cudaEventRecord(pin.ev[k], st));
+      if (have) {  // write the previous block while this one copies
+        CK(cudaEventSynchronize(pin.ev[pending]));
+        if (std::fwrite(pin.p[pending], 1, pending_len, of.f) != pending_len)
+          raise(errc::io_error, "short write on " + out_path);
+      }
+      pending = size_t(k);
+      pending_len = len;
+      have = true;
+      off += len;
+    }
+    if (have) {
+      CK(cudaEventSynchronize(pin.ev[pending]));
+      if (std::fwrite(pin.p[pending], 1, pending_len, of.f) != pending_len)
+        raise(errc::io_error, "short write on " + out_path);
+    }
+    b.record(st);
+    CK(cudaStreamSynchronize(st));
+  }
+  if (opt.timing) {
+    opt.timing->d2h_ms = Event::ms(a, b);
+    opt.timing->d2h_bytes = res.len;
+  }
+}
+
 uint8_t* decompress_dist_to_device(const Dist& d, const uint8_t* blob, size_t n,
                                    const std::string& pub_model_path, size_t* out_len,
                                    const CallOptions& opt) {

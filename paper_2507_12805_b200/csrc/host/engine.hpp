@@ -89,6 +89,16 @@ Bytes compress_device(const uint8_t* d_raw, size_t n, const Config& cfg, const C
 uint8_t* decompress_to_device(const uint8_t* blob, size_t n, const std::string& pub_model_path,
                               int device, size_t* out_len, const CallOptions& opt = {});
 
+// File to file with bounded host memory: compress streams
+// the input file into HBM through a pinned double buffer of `block` bytes
+// (read of block i+1 overlapping the copy of block i; 0 = 64 MiB) and writes
+// the container; decompress streams the decoded bytes back out the same way.
+void compress_file(const std::string& in_path, const std::string& out_path, const Config& cfg,
+                   const CallOptions& opt = {}, size_t block = 0);
+void decompress_file(const std::string& in_path, const std::string& out_path,
+                     const std::string& pub_model_path, int device, const CallOptions& opt = {},
+                     size_t block = 0);
+
 // encode_chunk_standalone (pipeline.cpp:298-301), batched: every chunk is
 // coded independently from its own inbound snapshot (empty = seeded init).
 struct ChunkJob {

@@ -508,3 +508,22 @@ def test_pretrain_public_matches_reference(P, checker, tmp_path, kw):
     with pytest.raises(P.PmklcError) as e:
         P.pretrain_public([b"ACGT"], t=8, batch=16, scale=16)
     assert e.value.errc == "CorpusEmpty"
+
+
+def test_file_streaming(P, checker, tmp_path):
+    # file to file with bounded host memory: the input streams
+    # into HBM and the output out of it through small pinned blocks; the
+    # container is the same as the in-memory API's (and the reference's)
+    raw = P.synth("genome", 2_000_003, 91, 4) + b"\n>chr2\nNNNNacgtRY\n" + P.synth("markov3", 50_000, 92)
+    src, mid, dst = tmp_path / "in.fa", tmp_path / "c.pmkl", tmp_path / "out.fa"
+    src.write_bytes(raw)
+    kw = dict(t=8, bs=32, scale=16, workers=4)
+    tm = P.Timing()
+    P.compress_file(str(src), str(mid), P.CompressConfig(**kw), block_bytes=256 << 10, timing=tm)
+    blob = mid.read_bytes()
+    assert blob == P.compress(raw, P.CompressConfig(**kw)) == checker.compress(raw, O.make_cfg(**kw))
+    P.decompress_file(str(mid), str(dst), block_bytes=100_000)
+    assert dst.read_bytes() == raw
+    with pytest.raises(P.PmklcError) as e:
+        P.compress_file(str(tmp_path / "missing"), str(mid), P.CompressConfig(**kw))
+    assert e.value.errc == "IoError"

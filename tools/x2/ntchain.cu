@@ -75,8 +75,18 @@ __global__ void __launch_bounds__(128, 1) kbench(float* out, unsigned long long*
 #pragma unroll
         for (int u = 0; u < 8; ++u) acc = add2(acc, mul2(pk(av[u].x, av[u].y), pk(bv[u], bv[u])));
       }
-    } else {
+    } else if (V == 2) {
       acc = chain_v2(acc, sa(A + 2 * w), H * 4, sa(bs), R);
+    } else {  // v3: two scalar exact chains (FMUL + FADD), batched loads
+      float a0 = __uint_as_float(unsigned(acc)), a1 = __uint_as_float(unsigned(acc >> 32));
+      for (int r = 0; r < R; r += 8) {
+        float2 av[8]; float bv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { av[u] = ap[(r + u) * (H / 2)]; bv[u] = bs[(r + u) * H]; }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { a0 = __fadd_rn(a0, __fmul_rn(av[u].x, bv[u])); a1 = __fadd_rn(a1, __fmul_rn(av[u].y, bv[u])); }
+      }
+      acc = (f2_t)__float_as_uint(a0) | ((f2_t)__float_as_uint(a1) << 32);
     }
     __syncwarp();
   }
@@ -88,11 +98,12 @@ int main() {
   float* out; unsigned long long* cyc;
   cudaMalloc(&out, 4096); cudaMalloc(&cyc, 64);
   for (int rep = 0; rep < 2; ++rep) {
-    unsigned long long h[3][4];
+    unsigned long long h[4][4];
     kbench<0><<<1, 128>>>(out, cyc); cudaMemcpy(h[0], cyc, 32, cudaMemcpyDeviceToHost);
     kbench<1><<<1, 128>>>(out, cyc); cudaMemcpy(h[1], cyc, 32, cudaMemcpyDeviceToHost);
     kbench<2><<<1, 128>>>(out, cyc); cudaMemcpy(h[2], cyc, 32, cudaMemcpyDeviceToHost);
-    for (int v = 0; v < 3; ++v)
+    kbench<3><<<1, 128>>>(out, cyc); cudaMemcpy(h[3], cyc, 32, cudaMemcpyDeviceToHost);
+    for (int v = 0; v < 4; ++v)
       printf("v%d cycles/iteration: %.2f (warp 0), %.2f (warp 3)\n", v, h[v][0] / double(R * STEPS), h[v][3] / double(R * STEPS));
   }
   return 0;
