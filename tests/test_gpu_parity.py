@@ -527,3 +527,25 @@ def test_file_streaming(P, checker, tmp_path):
     with pytest.raises(P.PmklcError) as e:
         P.compress_file(str(tmp_path / "missing"), str(mid), P.CompressConfig(**kw))
     assert e.value.errc == "IoError"
+
+
+def test_flags7_public_and_private_chunks(P, checker, spum_k3):
+    # flags 7 (SPuM and SPrM together, mixer.cpp:14-42): the reference's
+    # compress never selects it, but its decoder and encode_chunk_standalone
+    # (ChunkCodeSpec with pub and priv) accept it -- chunk payloads identical
+    raw = P.synth("markov3", 60000, 93)
+    kw = dict(t=8, bs=16, scale=16, workers=1)
+    blob6 = P.compress(raw, P.CompressConfig(**kw, selector_threshold=0))
+    priv = O.parse_container(blob6)["priv"]
+    tok, _ = checker.skmer_encode(codes_of(raw), 3, 3)
+    n = 16 * 120
+    chunks = [tok[i * n:(i + 1) * n] for i in range(2)]
+    _, snap = checker.replay_chunk(chunks[0], 7, 3, 8, 16, 16, 4242, pub_path=spum_k3, priv=priv,
+                                   snap_at=50, stop_at=50)
+    inbound = [b"", snap]
+    got = P.encode_chunks(np.concatenate(chunks), [n] * 2, inbound, 7, 3, 8, 16, 16, 4242,
+                          pub_model_path=spum_k3, priv_model=priv)
+    for i in range(2):
+        want = checker.encode_chunk_standalone(chunks[i], 7, 3, 8, 16, 16, 4242, pub_path=spum_k3,
+                                               priv=priv, inbound=inbound[i])
+        assert got[i] == want, i
