@@ -24,10 +24,12 @@ import paper_2507_12805_b200 as P
 
 n = int(float(sys.argv[1]) * 1e6) if len(sys.argv) > 1 else 10**9
 W = int(sys.argv[2]) if len(sys.argv) > 2 else 256
-block = max(1, int((64 << 20) * n / 1e10))  # 160 source blocks, as in the 10 GB config
+# source block: 160 of them as in the 10 GB config (default), or a given size
+# (64 MiB = the 10 GB config's own blocks, for a contiguous 1/8 share)
+block = int(sys.argv[3]) if len(sys.argv) > 3 else max(1, int((64 << 20) * n / 1e10))
 t0 = time.time()
 raw = P.synth("species", n, 2026, block)
-cfg = P.CompressConfig(workers=W)
+cfg = P.CompressConfig(workers=W, max_workers=max(W, 256))
 d_raw = torch.frombuffer(bytearray(raw), dtype=torch.uint8).cuda()
 tc, td = P.Timing(), P.Timing()
 e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -69,13 +71,17 @@ for i in range(nchunks):
         norm_bits += 8 * (pl + tr)
         norm_bases += nb
 print(json.dumps({
-    "config": "config5 sample (N=1): species mixture, 160 source blocks of %d B, every 16th perturbed" % block,
+    "config": "config5 sample (N=1): species mixture, %d source blocks of %d B, every 16th perturbed"
+              % ((n + block - 1) // block, block),
     "bytes": n, "W": W, "container_flags": blob[5],
     "compress_MBps": n / 1e6 / (c_ms / 1e3), "decompress_MBps": n / 1e6 / (d_ms / 1e3),
     "round_trip_MBps": n / 1e6 / ((c_ms + d_ms) / 1e3), "bits_per_base": 8 * len(blob) / n,
     "bits_per_base_normal_chunks": norm_bits / max(norm_bases, 1),
     "bits_per_base_perturbed_chunks": pert_bits / max(pert_bases, 1),
     "chunks_normal_bases": norm_bases, "chunks_perturbed_bases": pert_bases,
+    "crp_percent_blocks": P.robustness(P.block_ratios(blob)),
+    "state_tape_slots": tc.slots, "device_peak_bytes_compress": tc.dev_peak_bytes,
+    "device_peak_bytes_decompress": td.dev_peak_bytes,
     "sprm_prepass_ms": tc.sprm_ms, "compress_ticks_ms": tc.model_ms,
     "decompress_ticks_ms": td.model_ms, "ticks": tc.ticks, "lossless": ok,
     "wall_s": time.time() - t0, "per_chunk_bits_per_base": per_chunk}))

@@ -94,6 +94,38 @@ __global__ void __launch_bounds__(128, 1) kbench(float* out, unsigned long long*
   if (lane == 0) cyc[w] = t1 - t0;
   out[threadIdx.x] = __uint_as_float(unsigned(acc));
 }
+// v4: feature-major operands (the layout the NT reduction reads): lane n's
+// B row [k] contiguous (row stride K+4: conflict-free LDS.128 along k), the two
+// A rows broadcast along k; one paired chain per lane; `warps` warps per block
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) kfm(float* out, unsigned long long* cyc) {
+  constexpr int K = 256, KS = K + 4;
+  __shared__ __align__(16) float B[32 * KS];
+  __shared__ __align__(16) float A[2 * K];
+  for (int i = threadIdx.x; i < 32 * KS; i += blockDim.x) B[i] = 1.0f + i * 1e-7f;
+  for (int i = threadIdx.x; i < 2 * K; i += blockDim.x) A[i] = 0.5f - i * 1e-7f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const float4* b4 = reinterpret_cast<const float4*>(B + lane * KS);
+  const float4* a0 = reinterpret_cast<const float4*>(A);
+  const float4* a1 = reinterpret_cast<const float4*>(A + K);
+  f2_t acc = 0;
+  const unsigned long long t0 = clock64();
+  for (int rep = 0; rep < 40; ++rep) {
+#pragma unroll 4
+    for (int k4 = 0; k4 < K / 4; ++k4) {
+      const float4 bb = b4[k4], x0 = a0[k4], x1 = a1[k4];
+      acc = add2(acc, mul2(pk(x0.x, x1.x), pk(bb.x, bb.x)));
+      acc = add2(acc, mul2(pk(x0.y, x1.y), pk(bb.y, bb.y)));
+      acc = add2(acc, mul2(pk(x0.z, x1.z), pk(bb.z, bb.z)));
+      acc = add2(acc, mul2(pk(x0.w, x1.w), pk(bb.w, bb.w)));
+    }
+  }
+  const unsigned long long t1 = clock64();
+  if (lane == 0) cyc[w] = t1 - t0;
+  out[threadIdx.x] = __uint_as_float(unsigned(acc));
+}
+
 int main() {
   float* out; unsigned long long* cyc;
   cudaMalloc(&out, 4096); cudaMalloc(&cyc, 64);
@@ -106,5 +138,12 @@ int main() {
     for (int v = 0; v < 4; ++v)
       printf("v%d cycles/iteration: %.2f (warp 0), %.2f (warp 3)\n", v, h[v][0] / double(R * STEPS), h[v][3] / double(R * STEPS));
   }
+  unsigned long long h[8];
+  kfm<1><<<1, 32>>>(out, cyc); cudaMemcpy(h, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("v4 feature-major, 1 warp/SM: %.2f cycles/k\n", h[0] / (40.0 * 256));
+  kfm<4><<<1, 128>>>(out, cyc); cudaMemcpy(h, cyc, 32, cudaMemcpyDeviceToHost);
+  printf("v4 feature-major, 4 warps/SM: %.2f cycles/k\n", h[0] / (40.0 * 256));
+  kfm<8><<<1, 256>>>(out, cyc); cudaMemcpy(h, cyc, 64, cudaMemcpyDeviceToHost);
+  printf("v4 feature-major, 8 warps/SM: %.2f cycles/k\n", h[0] / (40.0 * 256));
   return 0;
 }
