@@ -442,6 +442,10 @@ size_t wide_smem(int extra_per_warp) {
   return size_t(2 * 3 * 32 * U * (U / 2) * 32 + kWideWarps * extra_per_warp * 32 * U) * sizeof(float);
 }
 
+__device__ __forceinline__ uint32_t sm_addr_h(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 // The model head of one train step, forward and backward, warp per row
 // (BiGruModel::forward tail and backward head, models.cpp:67-72, 77-86, with
 // the CE gradient of training.cpp:28-34 between them):
@@ -455,11 +459,11 @@ size_t wide_smem(int extra_per_warp) {
 // (reductions over rows) run afterwards on the side stream from bact, g,
 // dbact.
 constexpr int kHeadWarps = 8;
-// shared floats of the head kernel: W1 [2H][B] and W2 [B][V] as they are, their
-// transposes W1t [B][2H+1] and W2t [V][B+1] (padded rows: conflict-free
-// column walks), and per warp fin [2H], bact [B], dbact [B], e/g [V]
+// shared floats of the head kernel: W1 [2H][B] and W2 [B][V] with padded rows
+// (B+1, V+1: the row walks and the column walks of the backward are both
+// conflict-free from one copy), and per warp fin [2H], bact [B], dbact [B], g [V]
 __host__ __device__ inline int head_w_floats(int H2, int B, int V) {
-  return H2 * B + B * V + B * (H2 + 1) + V * (B + 1);
+  return H2 * (B + 1) + B * (V + 1);
 }
 template <bool kSmemW>  // weights staged in shared memory (the default widths) or read from L1/L2
 __global__ void __launch_bounds__(kHeadWarps * 32) k_sprm_head(
@@ -470,40 +474,27 @@ __global__ void __launch_bounds__(kHeadWarps * 32) k_sprm_head(
   pdl_wait();
   extern __shared__ __align__(16) float hs[];
   const int H2 = 2 * s.H, B = s.B, V = s.V;
-  float* W1s = hs;                  // [H2][B]
-  float* W2s = W1s + H2 * B;         // [B][V]
-  float* W1t = W2s + B * V;          // [B][H2+1]: W1t[j][p] = W1[p][j]
-  float* W2t = W1t + B * (H2 + 1);   // [V][B+1]: W2t[i][q] = W2[q][i]
+  float* W1s = hs;                   // [H2][B+1]
+  float* W2s = W1s + H2 * (B + 1);   // [B][V+1]
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (kSmemW) {  // staging: every thread's loads issued before its stores
-    constexpr int kU = 8;
-    const int n1 = H2 * B, n2 = B * V, nt = int(blockDim.x);
-    for (int e0 = threadIdx.x; e0 < n1 + n2; e0 += kU * nt) {
-      float x[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int e = e0 + u * nt;
-        x[u] = e < n1 ? __ldg(w1 + e) : (e < n1 + n2 ? __ldg(w2 + (e - n1)) : 0.0f);
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int e = e0 + u * nt;
-        if (e < n1) {
-          W1s[e] = x[u];
-          W1t[(e % B) * (H2 + 1) + e / B] = x[u];
-        } else if (e < n1 + n2) {
-          const int f = e - n1;
-          W2s[f] = x[u];
-          W2t[(f % V) * (B + 1) + f / V] = x[u];
-        }
-      }
+  if (kSmemW) {  // element-wise async copies into the padded rows, all in flight at once
+    const int n1 = H2 * B, n2 = B * V;
+    for (int e = threadIdx.x; e < n1 + n2; e += blockDim.x) {
+      const bool one = e < n1;
+      const int f = one ? e : e - n1, w = one ? B : V;
+      float* dst = (one ? W1s : W2s) + (f / w) * (w + 1) + f % w;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sm_addr_h(dst)),
+                   "l"((one ? w1 : w2) + f)
+                   : "memory");
     }
+    asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
   }
-  // W1(p, j), W2(q, i) and the transposed walks W2(j, o) / W1(p, j) by column
-  auto W1 = [&](int p, int j) { return kSmemW ? W1s[p * B + j] : w1[int64_t(p) * B + j]; };
-  auto W2 = [&](int q, int i) { return kSmemW ? W2s[q * V + i] : w2[int64_t(q) * V + i]; };
-  auto W2T = [&](int o, int j) { return kSmemW ? W2t[o * (B + 1) + j] : w2[int64_t(j) * V + o]; };
-  auto W1T = [&](int j, int p) { return kSmemW ? W1t[j * (H2 + 1) + p] : w1[int64_t(p) * B + j]; };
+  // W1(p, j) = bott.w[p][j], W2(q, i) = out.w[q][i]; the backward walks the
+  // same copies by column
+  auto W1 = [&](int p, int j) { return kSmemW ? W1s[p * (B + 1) + j] : w1[int64_t(p) * B + j]; };
+  auto W2 = [&](int q, int i) { return kSmemW ? W2s[q * (V + 1) + i] : w2[int64_t(q) * V + i]; };
+  auto W2T = [&](int o, int j) { return W2(j, o); };
+  auto W1T = [&](int j, int p) { return W1(p, j); };
   float* f = hs + (kSmemW ? head_w_floats(H2, B, V) : 0) + wl * (H2 + 2 * B + V);  // fin, bact, dbact, g
   float* ba = f + H2;
   float* db = ba + B;

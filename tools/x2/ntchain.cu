@@ -126,6 +126,109 @@ __global__ void __launch_bounds__(WARPS * 32, 1) kfm(float* out, unsigned long l
   out[threadIdx.x] = __uint_as_float(unsigned(acc));
 }
 
+// v5: the same feature-major operands, two scalar exact chains per lane
+// (FMUL + FADD each), no packing
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) kfm_scalar(float* out, unsigned long long* cyc) {
+  constexpr int K = 256, KS = K + 4;
+  __shared__ __align__(16) float B[32 * KS];
+  __shared__ __align__(16) float A[2 * K];
+  for (int i = threadIdx.x; i < 32 * KS; i += blockDim.x) B[i] = 1.0f + i * 1e-7f;
+  for (int i = threadIdx.x; i < 2 * K; i += blockDim.x) A[i] = 0.5f - i * 1e-7f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const float4* b4 = reinterpret_cast<const float4*>(B + lane * KS);
+  const float4* a0 = reinterpret_cast<const float4*>(A);
+  const float4* a1 = reinterpret_cast<const float4*>(A + K);
+  float c0 = 0.f, c1 = 0.f;
+  const unsigned long long t0 = clock64();
+  for (int rep = 0; rep < 40; ++rep) {
+#pragma unroll 4
+    for (int k4 = 0; k4 < K / 4; ++k4) {
+      const float4 bb = b4[k4], x0 = a0[k4], x1 = a1[k4];
+      c0 = __fadd_rn(c0, __fmul_rn(x0.x, bb.x)); c1 = __fadd_rn(c1, __fmul_rn(x1.x, bb.x));
+      c0 = __fadd_rn(c0, __fmul_rn(x0.y, bb.y)); c1 = __fadd_rn(c1, __fmul_rn(x1.y, bb.y));
+      c0 = __fadd_rn(c0, __fmul_rn(x0.z, bb.z)); c1 = __fadd_rn(c1, __fmul_rn(x1.z, bb.z));
+      c0 = __fadd_rn(c0, __fmul_rn(x0.w, bb.w)); c1 = __fadd_rn(c1, __fmul_rn(x1.w, bb.w));
+    }
+  }
+  const unsigned long long t1 = clock64();
+  if (lane == 0) cyc[w] = t1 - t0;
+  out[threadIdx.x] = c0 + c1;
+}
+
+// v6: paired chain with the products of a 16-k block formed first (16
+// FFMA2 into registers), then the block's 16 dependent FADD2s
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) kfm_two_phase(float* out, unsigned long long* cyc) {
+  constexpr int K = 256, KS = K + 4;
+  __shared__ __align__(16) float B[32 * KS];
+  __shared__ __align__(16) float A[2 * K];
+  for (int i = threadIdx.x; i < 32 * KS; i += blockDim.x) B[i] = 1.0f + i * 1e-7f;
+  for (int i = threadIdx.x; i < 2 * K; i += blockDim.x) A[i] = 0.5f - i * 1e-7f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const float4* b4 = reinterpret_cast<const float4*>(B + lane * KS);
+  const float4* a0 = reinterpret_cast<const float4*>(A);
+  const float4* a1 = reinterpret_cast<const float4*>(A + K);
+  f2_t acc = 0;
+  const unsigned long long t0 = clock64();
+  for (int rep = 0; rep < 40; ++rep) {
+    for (int kb = 0; kb < K / 16; ++kb) {
+      f2_t P[16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 bb = b4[kb * 4 + q], x0 = a0[kb * 4 + q], x1 = a1[kb * 4 + q];
+        P[4 * q + 0] = mul2(pk(x0.x, x1.x), pk(bb.x, bb.x));
+        P[4 * q + 1] = mul2(pk(x0.y, x1.y), pk(bb.y, bb.y));
+        P[4 * q + 2] = mul2(pk(x0.z, x1.z), pk(bb.z, bb.z));
+        P[4 * q + 3] = mul2(pk(x0.w, x1.w), pk(bb.w, bb.w));
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc = add2(acc, P[u]);
+    }
+  }
+  const unsigned long long t1 = clock64();
+  if (lane == 0) cyc[w] = t1 - t0;
+  out[threadIdx.x] = __uint_as_float(unsigned(acc));
+}
+
+// v7: v6 with the two A rows interleaved in shared memory, (a0[k], a1[k])
+// adjacent, so an LDS.128 yields two k's ready-made register pairs
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) kfm_pairs(float* out, unsigned long long* cyc) {
+  constexpr int K = 256, KS = K + 4;
+  __shared__ __align__(16) float B[32 * KS];
+  __shared__ __align__(16) float A[2 * K];  // [k][2]
+  for (int i = threadIdx.x; i < 32 * KS; i += blockDim.x) B[i] = 1.0f + i * 1e-7f;
+  for (int i = threadIdx.x; i < 2 * K; i += blockDim.x) A[i] = 0.5f - i * 1e-7f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const float4* b4 = reinterpret_cast<const float4*>(B + lane * KS);
+  const ulonglong2* ap = reinterpret_cast<const ulonglong2*>(A);  // two (a0,a1) pairs
+  f2_t acc = 0;
+  const unsigned long long t0 = clock64();
+  for (int rep = 0; rep < 40; ++rep) {
+    for (int kb = 0; kb < K / 16; ++kb) {
+      f2_t P[16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 bb = b4[kb * 4 + q];
+        const ulonglong2 x01 = ap[kb * 8 + 2 * q], x23 = ap[kb * 8 + 2 * q + 1];
+        P[4 * q + 0] = mul2(x01.x, pk(bb.x, bb.x));
+        P[4 * q + 1] = mul2(x01.y, pk(bb.y, bb.y));
+        P[4 * q + 2] = mul2(x23.x, pk(bb.z, bb.z));
+        P[4 * q + 3] = mul2(x23.y, pk(bb.w, bb.w));
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc = add2(acc, P[u]);
+    }
+  }
+  const unsigned long long t1 = clock64();
+  if (lane == 0) cyc[w] = t1 - t0;
+  out[threadIdx.x] = __uint_as_float(unsigned(acc));
+}
+
 int main() {
   float* out; unsigned long long* cyc;
   cudaMalloc(&out, 4096); cudaMalloc(&cyc, 64);
@@ -145,5 +248,17 @@ int main() {
   printf("v4 feature-major, 4 warps/SM: %.2f cycles/k\n", h[0] / (40.0 * 256));
   kfm<8><<<1, 256>>>(out, cyc); cudaMemcpy(h, cyc, 64, cudaMemcpyDeviceToHost);
   printf("v4 feature-major, 8 warps/SM: %.2f cycles/k\n", h[0] / (40.0 * 256));
+  kfm_scalar<1><<<1, 32>>>(out, cyc); cudaMemcpy(h, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("v5 feature-major scalar x2, 1 warp/SM: %.2f cycles/k\n", h[0] / (40.0 * 256));
+  kfm_scalar<4><<<1, 128>>>(out, cyc); cudaMemcpy(h, cyc, 32, cudaMemcpyDeviceToHost);
+  printf("v5 feature-major scalar x2, 4 warps/SM: %.2f cycles/k\n", h[0] / (40.0 * 256));
+  kfm_two_phase<1><<<1, 32>>>(out, cyc); cudaMemcpy(h, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("v6 paired two-phase, 1 warp/SM: %.2f cycles/k\n", h[0] / (40.0 * 256));
+  kfm_two_phase<4><<<1, 128>>>(out, cyc); cudaMemcpy(h, cyc, 32, cudaMemcpyDeviceToHost);
+  printf("v6 paired two-phase, 4 warps/SM: %.2f cycles/k\n", h[0] / (40.0 * 256));
+  kfm_pairs<1><<<1, 32>>>(out, cyc); cudaMemcpy(h, cyc, 8, cudaMemcpyDeviceToHost);
+  printf("v7 paired, interleaved A, 1 warp/SM: %.2f cycles/k\n", h[0] / (40.0 * 256));
+  kfm_pairs<4><<<1, 128>>>(out, cyc); cudaMemcpy(h, cyc, 32, cudaMemcpyDeviceToHost);
+  printf("v7 paired, interleaved A, 4 warps/SM: %.2f cycles/k\n", h[0] / (40.0 * 256));
   return 0;
 }
