@@ -388,6 +388,47 @@ def eq_metrics(n, blob_len, ct_s, dt_s, block_crs=None):
     return out
 
 
+def config2_line(P, torch, dev, flush, reps=5):
+    """BASELINE config 2: the (s,k)-mer encoder over 2^30 packed synthetic bases
+    (Rng(1)) on one B200, u32 tokens (the reference layout) and u16; HBM-bound:
+    algorithmic bytes = ceil(n/4) read + token bytes written; median of `reps`
+    launches with an L2 flush before each (tokens bit-exact: tests/)."""
+    nb = 1 << 30
+    peaks = ROOT / "MEASURED_PEAKS.json"
+    peak, src = 6468.0, "B200_PROFILING.md fallback"
+    if peaks.exists():
+        peak, src = float(json.loads(peaks.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    packed = P.synth("packed", nb // 4, 1)
+    d_in = torch.frombuffer(bytearray(packed), dtype=torch.uint8).to(f"cuda:{dev}")
+    out32 = torch.empty(nb + 8, dtype=torch.int32, device=f"cuda:{dev}")
+    out16 = torch.empty(nb + 16, dtype=torch.int16, device=f"cuda:{dev}")
+    rows = []
+    for s_, k_ in [(1, 1), (2, 3), (3, 3), (4, 4), (1, 8), (8, 8)]:
+        m = (nb - k_) // s_ + 1
+        for tw, buf in ((4, out32), (2, out16)):
+            run = lambda: P.skmer_encode_packed_device(d_in.data_ptr(), nb, s_, k_, buf.data_ptr(),
+                                                       u16=(tw == 2))
+            run()
+            ts = []
+            for _ in range(reps):
+                flush.add_(1)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                run()
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            ms = sorted(ts)[len(ts) // 2]
+            gbs = ((nb + 3) // 4 + tw * m) / (ms / 1e3) / 1e9
+            rows.append({"s": s_, "k": k_, "token_bytes": tw, "ms": ms, "GB/s": gbs, "frac": gbs / peak})
+    del d_in, out32, out16
+    mean = lambda tw: statistics.fmean(r["frac"] for r in rows if r["token_bytes"] == tw)
+    return {"workload": "config2: (s,k)-mer encoder over 2^30 packed synthetic bases, 1 B200",
+            "bound": "hbm", "peak_gbs": peak, "peak_source": src, "results": rows,
+            "mean_frac_u32": mean(4), "mean_frac_u16": mean(2),
+            "gpu_launches": len(rows) * (reps + 1)}
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -554,6 +595,8 @@ def main():
         del sprm_run
     del main_run
 
+    c2 = config2_line(P, torch, dev, flush) if wl.name == "config3" and world == 1 else None
+
     # config 4 at N=1: one step (the engine paths are warm; the first step's
     # round trip is checked on the device)
     c4 = None
@@ -681,6 +724,7 @@ def main():
             "cpu_baseline": cpu,
             "sprm_branch": sprm_line,
             "config4": c4,
+            "config2": c2,
             "e2e": {"value": e2e_val, "unit": "MB/s", "h2d_bytes_per_step": n + e2e_blob,
                     "d2h_bytes_per_step": e2e_blob + n},
             "clocks": clk.summary(),

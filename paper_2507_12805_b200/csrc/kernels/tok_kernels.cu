@@ -10,6 +10,7 @@
 // 16-byte stores (512 contiguous bytes per store instruction).
 #include <cstdint>
 #include <cstring>
+#include <type_traits>
 
 #include "kernels.hpp"
 #include "launch.cuh"
@@ -44,7 +45,12 @@ __device__ __forceinline__ uint32_t msb_first(uint32_t w) {
 // 8 u16 tokens); lane l makes tokens PER*l .. PER*l+PER-1 of each slab and
 // writes them with one 16-byte store, so every warp store covers 512
 // contiguous bytes.
-template <int kTokPerThread, typename TokT>
+// kPad: the staged window has one padding word after every 32 (word w at
+// w + w/32). A lane's PER tokens span PER*s bases, so lanes read words PER*s/16
+// apart -- a 4-way bank conflict for 8 u16 tokens at s = 8; with the padding
+// the 32 lanes of such a stride land in 32 banks.
+__device__ __forceinline__ uint32_t padw(uint32_t w) { return w + (w >> 5); }
+template <int kTokPerThread, typename TokT, bool kPad = false>
 __device__ __forceinline__ void emit_tokens(const uint32_t* sw, uint64_t sbase, uint64_t j0,
                                             uint32_t s, uint32_t k, TokT* tokens, uint64_t m) {
   constexpr int PER = 16 / int(sizeof(TokT));
@@ -61,7 +67,8 @@ __device__ __forceinline__ void emit_tokens(const uint32_t* sw, uint64_t sbase, 
 #pragma unroll
     for (int q = 0; q < PER; ++q, b += s) {
       const uint32_t wi = b >> 4, o = b & 15u;
-      out[q] = TokT(__funnelshift_l(sw[wi + 1], sw[wi], 2u * o) >> rsh);
+      const uint32_t lo = kPad ? sw[padw(wi)] : sw[wi], hi = kPad ? sw[padw(wi + 1)] : sw[wi + 1];
+      out[q] = TokT(__funnelshift_l(hi, lo, 2u * o) >> rsh);
     }
     if (jt + PER <= m) {
       uint4 v;
@@ -73,13 +80,13 @@ __device__ __forceinline__ void emit_tokens(const uint32_t* sw, uint64_t sbase, 
   }
 }
 
-template <int kTokPerThread, typename TokT>
+template <int kTokPerThread, typename TokT, bool kPad = false>
 __global__ void __launch_bounds__(kTokThreads) k_skmer_packed(const uint8_t* __restrict__ packed,
                                                               uint64_t n, uint32_t s, uint32_t k,
                                                               TokT* __restrict__ tokens,
                                                               uint64_t m) {
   pdl_wait();
-  __shared__ __align__(16) uint32_t sw[kStageBytes / 4];
+  __shared__ __align__(16) uint32_t sw[kStageBytes / 4 + (kPad ? kStageBytes / 128 + 2 : 0)];
   constexpr int kTokPerBlock = kTokThreads * kTokPerThread;
   const uint64_t j0 = uint64_t(blockIdx.x) * kTokPerBlock;
   const uint64_t jlast = min(j0 + kTokPerBlock, m) - 1;
@@ -89,15 +96,36 @@ __global__ void __launch_bounds__(kTokThreads) k_skmer_packed(const uint8_t* __r
   const uint64_t nbytes = byte_end - byte0;
   const uint64_t nvec = nbytes / 16;
   const uint4* src = reinterpret_cast<const uint4*>(packed + byte0);
-  uint4* dst = reinterpret_cast<uint4*>(sw);
-  for (uint64_t i = threadIdx.x; i < nvec; i += kTokThreads) dst[i] = __ldg(src + i);
-  uint8_t* sb = reinterpret_cast<uint8_t*>(sw);
-  for (uint64_t i = nvec * 16 + threadIdx.x; i < nbytes + 8; i += kTokThreads)
-    sb[i] = i < nbytes ? packed[byte0 + i] : 0;
+  if (!kPad) {
+    uint4* dst = reinterpret_cast<uint4*>(sw);
+    for (uint64_t i = threadIdx.x; i < nvec; i += kTokThreads) dst[i] = __ldg(src + i);
+    uint8_t* sb = reinterpret_cast<uint8_t*>(sw);
+    for (uint64_t i = nvec * 16 + threadIdx.x; i < nbytes + 8; i += kTokThreads)
+      sb[i] = i < nbytes ? packed[byte0 + i] : 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < uint32_t((nbytes + 8 + 3) / 4); i += kTokThreads) sw[i] = msb_first(sw[i]);
+  } else {
+    // 16-byte loads, digit order fixed on the way in, padded word positions
+    for (uint64_t i = threadIdx.x; i < nvec; i += kTokThreads) {
+      const uint4 v = __ldg(src + i);
+      const uint32_t w0 = uint32_t(4 * i);
+      sw[padw(w0)] = msb_first(v.x);
+      sw[padw(w0 + 1)] = msb_first(v.y);
+      sw[padw(w0 + 2)] = msb_first(v.z);
+      sw[padw(w0 + 3)] = msb_first(v.w);
+    }
+    const uint32_t nw = uint32_t((nbytes + 8 + 3) / 4);
+    for (uint32_t wd = uint32_t(nvec * 4) + threadIdx.x; wd < nw; wd += kTokThreads) {
+      uint32_t x = 0;
+      for (int c = 0; c < 4; ++c) {
+        const uint64_t i = uint64_t(wd) * 4 + c;
+        x |= uint32_t(i < nbytes ? packed[byte0 + i] : 0) << (8 * c);
+      }
+      sw[padw(wd)] = msb_first(x);
+    }
+  }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < uint32_t((nbytes + 8 + 3) / 4); i += kTokThreads) sw[i] = msb_first(sw[i]);
-  __syncthreads();
-  emit_tokens<kTokPerThread, TokT>(sw, byte0 * 4, j0, s, k, tokens, m);
+  emit_tokens<kTokPerThread, TokT, kPad>(sw, byte0 * 4, j0, s, k, tokens, m);
 }
 
 // ASCII / code input: stage 16 bytes per step, pack to 2-bit on the way in.
@@ -285,9 +313,30 @@ void launch_skmer_encode_packed(const uint8_t* packed, uint64_t n, uint32_t s, u
                                 uint32_t* tokens, uint64_t m, cudaStream_t st) {
   launch_packed(packed, n, s, k, tokens, m, st);
 }
+// u16 tokens write half the bytes per token, so a block's staging phase
+// (window load, digit reversal, two barriers) is amortised over twice (s <= 4)
+// or four times (s <= 2) the tokens; the staged window stays <= 64 Ki bases
 void launch_skmer_encode_packed16(const uint8_t* packed, uint64_t n, uint32_t s, uint32_t k,
                                   uint16_t* tokens, uint64_t m, cudaStream_t st) {
-  launch_packed(packed, n, s, k, tokens, m, st);
+  if (m == 0) return;
+  auto go = [&](auto tpt_c, auto smax_c, auto pad_c) {
+    constexpr int tpt = decltype(tpt_c)::value, smax = decltype(smax_c)::value;
+    // the window of a block: tpt*256 tokens at stride <= smax, + k-1 halo, 16-byte aligned
+    static_assert(kTokThreads * tpt * smax / 4 + 32 <= kStageBytes, "staging bound");
+    const uint64_t blocks = (m + kTokThreads * tpt - 1) / (kTokThreads * tpt);
+    launch_pdl(k_skmer_packed<tpt, uint16_t, decltype(pad_c)::value>, dim3(unsigned(blocks)),
+               dim3(kTokThreads), 0, st, packed, n, s, k, tokens, m);
+  };
+  // measured (2^30 bases): the padded staging pays off only where a lane's 8
+  // tokens span >= 2.5 words (s > 4: 0.50 -> 0.69 of the copy peak at (8,8));
+  // at s <= 4 its scalar stores cost more than the 2-way conflicts it removes
+  using std::integral_constant;
+  if (s <= 2)
+    go(integral_constant<int, 2 * kTptSmallStride>{}, integral_constant<int, 2>{}, std::false_type{});
+  else if (s <= 4)
+    go(integral_constant<int, 2 * kTpt>{}, integral_constant<int, 4>{}, std::false_type{});
+  else
+    go(integral_constant<int, kTpt>{}, integral_constant<int, 8>{}, std::true_type{});
 }
 
 void launch_skmer_encode_ascii(const uint8_t* ascii, uint64_t n, uint32_t s, uint32_t k,
