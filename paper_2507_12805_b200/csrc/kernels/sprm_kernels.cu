@@ -11,7 +11,6 @@
 //   G{an,ar,az,hh}[d][j][k], HP[d][q][k] (h_{t-1}), X[d][i][k] (GRU input)
 #include <algorithm>
 #include <cstdint>
-#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -831,7 +830,6 @@ struct NtSParams {
   const NtSWarp* warps;    // consumer warp table, 4 per block, (d, g) uniform per block
   const int* block_dg;     // per consumer block: d * 4 + g
   int nb_bptt;             // unused (0)
-  int variant;             // dev experiments (PMKLC_NT_VARIANT): 1 no compute, 2 no copies, 3 no wait
 };
 constexpr int kStreamConsumers = 8;
 
@@ -990,16 +988,12 @@ __global__ void __launch_bounds__((kStreamConsumers + 1) * 32, 1) k_sprm_nt_stre
         const int t = T - 1 - i, b = i & 1;
         if (i >= 2) mbar_wait_sleep(&empty[b], ((i >> 1) - 1) & 1);  // consumers done with step i-2
         const unsigned* c = q.cnt + d * T + t / kPubSteps;  // group of step t complete
-        for (unsigned long long k = 0; q.variant != 3 && ld_acquire(c) < unsigned(R); ++k) {
+        for (unsigned long long k = 0; ld_acquire(c) < unsigned(R); ++k) {
           if (k > kSpinLimit) __trap();
           __nanosleep(32);
         }
         asm volatile("fence.proxy.async.global;" ::: "memory");
         float* base = sbuf + b * slab;
-        if (q.variant == 2) {
-          mbar_arrive(&full[b]);
-          continue;
-        }
         mbar_arrive_tx(&full[b], bB + (need_h ? bB : 0) + (need_x ? bX : 0));
         bulk_g2s(base, q.Gt + (int64_t(g * 2 + d) * T + t) * R * H, bB, &full[b]);
         if (need_h) bulk_g2s(base + R * H, q.Gt + (int64_t(4 * 2 + d) * T + t) * R * H, bB, &full[b]);
@@ -1030,11 +1024,6 @@ __global__ void __launch_bounds__((kStreamConsumers + 1) * 32, 1) k_sprm_nt_stre
   for (int i = 0; i < T; ++i) {
     const int b = i & 1;
     mbar_wait(&full[b], (i >> 1) & 1);
-    if (q.variant == 1) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[b]);
-      continue;
-    }
     const float* base = sbuf + b * slab;
     const float* bs = base + lane;
     const float* a0 = o0 >= 0 ? base + o0 : nullptr;
@@ -1531,11 +1520,6 @@ void launch_sprm_bptt_stream(const SprmP& s, const float* tape, const float* dfi
   q.block_dg = reinterpret_cast<const int*>(static_cast<const unsigned char*>(d_table) +
                                             pl.warps.size() * sizeof(NtSWarp));
   q.nb_bptt = 0;
-  static const int variant = [] {
-    const char* e = std::getenv("PMKLC_NT_VARIANT");
-    return e ? std::atoi(e) : 0;
-  }();
-  q.variant = variant;
   const size_t smem = size_t(2) * s.R * (2 * s.H + s.Es) * sizeof(float);
   ensure_smem(reinterpret_cast<const void*>(k_sprm_nt_stream), smem);
   launch_pdl(k_sprm_nt_stream, dim3(unsigned(pl.block_dg.size())), dim3((kStreamConsumers + 1) * 32),

@@ -549,3 +549,29 @@ def test_flags7_public_and_private_chunks(P, checker, spum_k3):
         want = checker.encode_chunk_standalone(chunks[i], 7, 3, 8, 16, 16, 4242, pub_path=spum_k3,
                                                priv=priv, inbound=inbound[i])
         assert got[i] == want, i
+
+
+def test_corrupt_container_fuzz(P, checker):
+    # structurally valid but mutated containers (checksum recomputed, so the
+    # reader's FNV check passes): every one must decode or raise a reference
+    # errc -- never crash, hang or return a CUDA failure
+    raw = P.synth("markov3", 30000, 94)
+    blob = P.compress(raw, P.CompressConfig(t=8, bs=16, scale=16, workers=2))
+    rng = np.random.default_rng(95)
+    outcomes = {}
+    for trial in range(60):
+        b = bytearray(blob[:-8])
+        for _ in range(int(rng.integers(1, 4))):
+            # past the header and chunk table (those are covered above): the
+            # SPrM/exception/residual sections, codestreams and trailers
+            at = int(rng.integers(52 + 36 * 2, len(b)))
+            b[at] ^= int(rng.integers(1, 256))
+        b += O.fnv1a64(bytes(b)).to_bytes(8, "little")
+        try:
+            out = P.decompress(bytes(b))
+            outcomes["decoded"] = outcomes.get("decoded", 0) + 1
+            assert isinstance(out, bytes)
+        except P.PmklcError as e:
+            assert e.errc != "CudaError", (trial, str(e))
+            outcomes[e.errc] = outcomes.get(e.errc, 0) + 1
+    assert sum(outcomes.values()) == 60
