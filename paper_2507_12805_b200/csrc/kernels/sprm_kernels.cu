@@ -460,53 +460,68 @@ __device__ __forceinline__ uint32_t sm_addr_h(const void* p) {
 constexpr int kHeadWarps = 8;
 // shared floats of the head kernel: W1 [2H][B] and W2 [B][V] with padded rows
 // (B+1, V+1: the row walks and the column walks of the backward are both
-// conflict-free from one copy), and per warp fin [2H], bact [B], dbact [B], g [V]
+// conflict-free from one copy), then b1 [B] and b2 [V], rounded up to whole
+// float4s; and per warp fin [2H], bact [B], dbact [B], g [V]
 __host__ __device__ inline int head_w_floats(int H2, int B, int V) {
-  return H2 * (B + 1) + B * (V + 1);
+  return (H2 * (B + 1) + B * (V + 1) + B + V + 3) & ~3;
 }
-template <bool kSmemW>  // weights staged in shared memory (the default widths) or read from L1/L2
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sm_addr_h(dst)), "l"(src) : "memory");
+}
+// kSmemW: weights and biases staged in shared memory (the default widths) or
+// read from L1/L2. cH2/cB/cV: the widths at compile time (0 = runtime), so the
+// default model's chains unroll fully and a lane's independent outputs
+// interleave.
+template <bool kSmemW, int cH2 = 0, int cB = 0, int cV = 0>
 __global__ void __launch_bounds__(kHeadWarps * 32) k_sprm_head(
     SprmP s, const uint32_t* __restrict__ tokens, const int64_t* __restrict__ pos,
     const float* __restrict__ fin, const float* __restrict__ w1, const float* __restrict__ b1,
     const float* __restrict__ w2, const float* __restrict__ b2, float* bact_out, float* g_out,
     float* dbact_out, float* dfin_out) {
-  pdl_wait();
   extern __shared__ __align__(16) float hs[];
-  const int H2 = 2 * s.H, B = s.B, V = s.V;
+  const int H2 = cH2 ? cH2 : 2 * s.H, B = cB ? cB : s.B, V = cV ? cV : s.V;
   float* W1s = hs;                   // [H2][B+1]
   float* W2s = W1s + H2 * (B + 1);   // [B][V+1]
+  float* b1s = W2s + B * (V + 1);
+  float* b2s = b1s + B;
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (kSmemW) {  // element-wise async copies into the padded rows, all in flight at once
+  const int r = blockIdx.x * kHeadWarps + wl;
+  const bool live = r < s.R;
+  float* f = hs + (kSmemW ? head_w_floats(H2, B, V) : 0) + wl * (H2 + 2 * B + V);  // fin, bact, dbact, g
+  float* ba = f + H2;
+  float* db = ba + B;
+  float* gr = db + B;
+  pdl_wait();
+  // every load of the step is issued before the first wait: the target token,
+  // the row's fin, and (kSmemW) the weights and biases, element-wise into the
+  // padded rows
+  const uint32_t tgt = live ? tokens[*pos + r] & uint32_t(V - 1) : 0u;
+  if (live)
+    for (int p = lane; p < H2; p += 32) cp_async4(f + p, fin + int64_t(r) * H2 + p);
+  if (kSmemW) {
     const int n1 = H2 * B, n2 = B * V;
-    for (int e = threadIdx.x; e < n1 + n2; e += blockDim.x) {
-      const bool one = e < n1;
-      const int f = one ? e : e - n1, w = one ? B : V;
-      float* dst = (one ? W1s : W2s) + (f / w) * (w + 1) + f % w;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sm_addr_h(dst)),
-                   "l"((one ? w1 : w2) + f)
-                   : "memory");
+    for (int e = threadIdx.x; e < n1 + n2 + B + V; e += blockDim.x) {
+      if (e < n1) cp_async4(W1s + (e / B) * (B + 1) + e % B, w1 + e);
+      else if (e < n1 + n2) cp_async4(W2s + ((e - n1) / V) * (V + 1) + (e - n1) % V, w2 + (e - n1));
+      else if (e < n1 + n2 + B) cp_async4(b1s + (e - n1 - n2), b1 + (e - n1 - n2));
+      else cp_async4(b2s + (e - n1 - n2 - B), b2 + (e - n1 - n2 - B));
     }
-    asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
   }
+  asm volatile("cp.async.commit_group;\n cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  if (!live) return;
   // W1(p, j) = bott.w[p][j], W2(q, i) = out.w[q][i]; the backward walks the
   // same copies by column
   auto W1 = [&](int p, int j) { return kSmemW ? W1s[p * (B + 1) + j] : w1[int64_t(p) * B + j]; };
   auto W2 = [&](int q, int i) { return kSmemW ? W2s[q * (V + 1) + i] : w2[int64_t(q) * V + i]; };
   auto W2T = [&](int o, int j) { return W2(j, o); };
   auto W1T = [&](int j, int p) { return W1(p, j); };
-  float* f = hs + (kSmemW ? head_w_floats(H2, B, V) : 0) + wl * (H2 + 2 * B + V);  // fin, bact, dbact, g
-  float* ba = f + H2;
-  float* db = ba + B;
-  float* gr = db + B;
-  const int r = blockIdx.x * kHeadWarps + wl;
-  const bool live = r < s.R;
-  if (live)
-    for (int p = lane; p < H2; p += 32) f[p] = fin[int64_t(r) * H2 + p];
-  __syncthreads();
-  if (!live) return;
+  auto B1 = [&](int j) { return kSmemW ? b1s[j] : b1[j]; };
+  auto B2 = [&](int i) { return kSmemW ? b2s[i] : b2[i]; };
   // bact = tanh(bott.b + fin.W1), ascending p
+#pragma unroll
   for (int j = lane; j < B; j += 32) {
-    float acc = b1[j];
+    float acc = B1(j);
 #pragma unroll 8
     for (int p = 0; p < H2; ++p) acc = mac(acc, f[p], W1(p, j));
     acc = det_tanh(acc);
@@ -516,8 +531,9 @@ __global__ void __launch_bounds__(kHeadWarps * 32) k_sprm_head(
   __syncwarp();
   // logits = out.b + bact.W2, ascending q
   float mx = -__int_as_float(0x7f800000);
+#pragma unroll
   for (int i = lane; i < V; i += 32) {
-    float acc = b2[i];
+    float acc = B2(i);
 #pragma unroll 8
     for (int q = 0; q < B; ++q) acc = mac(acc, ba[q], W2(q, i));
     gr[i] = acc;
@@ -527,12 +543,14 @@ __global__ void __launch_bounds__(kHeadWarps * 32) k_sprm_head(
   __syncwarp();
   // det_softmax (detmath.cpp:85-97): exp of the shifted logits, then one
   // sequential sum in index order (lane 0 over shared memory)
+#pragma unroll
   for (int i = lane; i < V; i += 32) gr[i] = det_exp(fsub(gr[i], mx));
   __syncwarp();
   float sum = 0.0f;
   if (lane == 0) {
     int i = 0;
-    if ((V & 3) == 0)
+    if ((V & 3) == 0 && ((H2 + 2 * B) & 3) == 0)  // gr is 16-byte aligned
+#pragma unroll 4
       for (; i < V; i += 4) {
         const float4 e4 = *reinterpret_cast<const float4*>(gr + i);
         sum = fadd(fadd(fadd(fadd(sum, e4.x), e4.y), e4.z), e4.w);
@@ -541,7 +559,7 @@ __global__ void __launch_bounds__(kHeadWarps * 32) k_sprm_head(
   }
   sum = __shfl_sync(0xffffffffu, sum, 0);
   const float inv = fdiv(1.0f, sum);
-  const uint32_t tgt = tokens[*pos + r] & uint32_t(V - 1);
+#pragma unroll
   for (int i = lane; i < V; i += 32) {
     float v = fmul(gr[i], inv);
     if (uint32_t(i) == tgt) v = fsub(v, 1.0f);
@@ -550,6 +568,7 @@ __global__ void __launch_bounds__(kHeadWarps * 32) k_sprm_head(
   }
   __syncwarp();
   // dbact = (0 + g.W2^T) * (1 - bact^2), ascending o
+#pragma unroll
   for (int j = lane; j < B; j += 32) {
     float acc = 0.0f;
 #pragma unroll 8
@@ -561,6 +580,7 @@ __global__ void __launch_bounds__(kHeadWarps * 32) k_sprm_head(
   }
   __syncwarp();
   // dfin = 0 + dbact.W1^T, ascending j
+#pragma unroll
   for (int p = lane; p < H2; p += 32) {
     float acc = 0.0f;
 #pragma unroll 8
@@ -1596,7 +1616,12 @@ void launch_sprm_head(const SprmP& s, const uint32_t* tokens, const int64_t* pos
   const size_t rows_smem = size_t(kHeadWarps) * (2 * s.H + 2 * s.B + s.V) * sizeof(float);
   const size_t w_smem = size_t(head_w_floats(2 * s.H, s.B, s.V)) * sizeof(float);
   const dim3 grid(unsigned((s.R + kHeadWarps - 1) / kHeadWarps)), block(kHeadWarps * 32);
-  if (w_smem + rows_smem <= 64 * 1024) {
+  if (s.H == 32 && s.B == 32 && s.V == 64) {  // the default SPrM widths
+    auto k = k_sprm_head<true, 64, 32, 64>;
+    ensure_smem(reinterpret_cast<const void*>(k), w_smem + rows_smem);
+    launch_pdl(k, grid, block, w_smem + rows_smem, st, s, tokens, pos, fin, w1, b1, w2, b2, bact, g,
+               dbact, dfin);
+  } else if (w_smem + rows_smem <= 64 * 1024) {
     ensure_smem(reinterpret_cast<const void*>(k_sprm_head<true>), w_smem + rows_smem);
     launch_pdl(k_sprm_head<true>, grid, block, w_smem + rows_smem, st, s, tokens, pos, fin, w1, b1, w2,
                b2, bact, g, dbact, dfin);

@@ -1,0 +1,2 @@
+export PATH=/usr/local/cuda/bin:$PATH
+PMKLC_FOLLOW_AFTER=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_gemm_nt_r1" -s 20 -c 1 -o gpurun_out/r2_nt_blk python tools/prof_sprm.py 400000 > gpurun_out/r2_ncu8.log 2>&1; echo "ncu rc=$?"
