@@ -960,6 +960,8 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
   DBuf<int64_t> offs(hoffs.size());
   offs.upload(hoffs.data(), hoffs.size(), st);
   DBuf<AdamScalars> sc(1);
+  DBuf<unsigned> adone(1);  // k_sprm_adam's block counter
+  adone.zero(st);
   const AdamScalars s0{0, 1.0f, 1.0f, 0.0f, 0.0f, {0, 0}};
   sc.upload(&s0, 1, st);
   const int64_t R = batch, RT = R * T;
@@ -1044,10 +1046,8 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
         launch_emb_grad(ctx.p, 0, dx.p, 0, g.p, 0, int64_t(hoffs[0]), ed, td.p, 1, st);
       }
       side.join_into(st);
-      launch_adam_scalars(sc.p, st);
-      launch_adam(w.p, g.p, mo.p, vo.p, 0, P, sc.p, td.p, 1, st);
-      launch_pos_advance(pos.p, batch, st);
-      nl += 10;
+      launch_sprm_adam(w.p, g.p, mo.p, vo.p, P, sc.p, pos.p, batch, adone.p, st);
+      nl += 8;
       return;
     }
     launch_sprm_bptt(sp, tape.p, dfin.p, Gt.p, st);
@@ -1078,26 +1078,31 @@ BiGru pretrain_private_gpu(const uint32_t* d_tok, uint64_t m, const BiGru* pub, 
     launch_emb_grad(ctx.p, 0, dx.p, 0, g.p, 0, int64_t(hoffs[0]), ed, td.p, 1, st);
     side.join_into(st);
     side2.join_into(st);
-    launch_adam_scalars(sc.p, st);
-    launch_adam(w.p, g.p, mo.p, vo.p, 0, P, sc.p, td.p, 1, st);
-    launch_pos_advance(pos.p, batch, st);
-    nl += 14;
+    launch_sprm_adam(w.p, g.p, mo.p, vo.p, P, sc.p, pos.p, batch, adone.p, st);
+    nl += 12;
   };
   const uint64_t nsteps = (m - t + batch - 1) / batch;
   const uint64_t full = (m - t) / batch;
-  if (full > 0) {
+  // Full steps replay a captured graph of kSteps steps (the steps chain by
+  // programmatic launches inside a graph; between graph launches the device
+  // idles ~2 us), then one graph of the remaining full steps.
+  auto replay = [&](uint64_t per, uint64_t reps) {
+    if (per == 0 || reps == 0) return;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     const uint64_t nl0 = nl;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    step(int(batch));
+    for (uint64_t i = 0; i < per; ++i) step(int(batch));
     CK(cudaStreamEndCapture(st, &graph));
     CK(cudaGraphInstantiate(&exec, graph, 0));
-    for (uint64_t i = 0; i < full; ++i) CK(cudaGraphLaunch(exec, st));
-    nl += (nl - nl0) * (full - 1);
+    for (uint64_t i = 0; i < reps; ++i) CK(cudaGraphLaunch(exec, st));
+    nl += (nl - nl0) * (reps - 1);
     CK(cudaGraphExecDestroy(exec));
     CK(cudaGraphDestroy(graph));
-  }
+  };
+  constexpr uint64_t kSteps = 8;
+  replay(kSteps, full / kSteps);
+  replay(full % kSteps, 1);
   if (nsteps > full) step(int((m - t) - full * batch));
   check_launch();
   CK(cudaMemcpyAsync(model.w.data(), w.p, P * 4, cudaMemcpyDeviceToHost, st));
@@ -1162,6 +1167,8 @@ BiGru train_public_gpu(const std::vector<std::pair<const uint32_t*, uint64_t>>& 
   DBuf<int64_t> offs(hoffs.size());
   offs.upload(hoffs.data(), hoffs.size(), st);
   DBuf<AdamScalars> sc(1);
+  DBuf<unsigned> adone(1);  // k_sprm_adam's block counter
+  adone.zero(st);
   const AdamScalars s0{0, 1.0f, 1.0f, 0.0f, 0.0f, {0, 0}};
   sc.upload(&s0, 1, st);
   const int64_t R = batch, RT = R * T;
@@ -1229,10 +1236,8 @@ BiGru train_public_gpu(const std::vector<std::pair<const uint32_t*, uint64_t>>& 
     const DmDims ed{rows, T, Es, H, 0, V, 0};
     launch_emb_grad(ctx.p, 0, dx0.p, 0, g.p, 0, int64_t(hoffs[0]), ed, td.p, 1, st);
     side2.join_into(st);
-    launch_adam_scalars(sc.p, st);
-    launch_adam(w.p, g.p, mo.p, vo.p, 0, P, sc.p, td.p, 1, st);
-    launch_pos_advance(pos.p, batch, st);
-    nl += 22;
+    launch_sprm_adam(w.p, g.p, mo.p, vo.p, P, sc.p, pos.p, batch, adone.p, st);
+    nl += 20;
   };
   for (uint32_t e = 0; e < epochs; ++e)
     for (const auto& set : sets) {  // train_pass over one token set

@@ -312,6 +312,10 @@ void launch_bigru_concat(const float* tape, float* x1, int R, int T, int H, cuda
 void launch_bigru_xf(const float* x1, float* Xf, int R, int T, int In, cudaStream_t st);
 void launch_tanh_vec(float* x, int64_t n, cudaStream_t st);
 void launch_adam_scalars(AdamScalars* sc, cudaStream_t st);
+// one model's Adam step + scalar update + pos += by, in one launch (the
+// trainers' k_adam_scalars -> k_adam -> k_pos_advance); done: a zeroed counter
+void launch_sprm_adam(float* w, float* g, float* m, float* v, int64_t n, AdamScalars* sc, int64_t* pos,
+                      int64_t by, unsigned* done, cudaStream_t st);
 void launch_pos_advance(int64_t* pos, int64_t by, cudaStream_t st);
 
 }  // namespace pmklc_b200

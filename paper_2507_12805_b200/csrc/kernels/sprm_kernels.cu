@@ -1433,6 +1433,65 @@ __global__ void k_adam_scalars(AdamScalars* sc) {
   *sc = a;
 }
 
+// Adam for the single-model trainers (SPrM pre-pass, pretrain_public) in one
+// launch: k_adam_scalars' bias-correction sequence formed by every thread
+// from the previous scalars (the same operations, so the same values), the
+// update of k_adam, then the last block to finish publishes the new scalars and
+// advances pos (every block has read the old scalars before it counts itself
+// done, so none reads the new ones).
+__global__ void __launch_bounds__(256) k_sprm_adam(float* __restrict__ w, float* __restrict__ g,
+                                                   float* __restrict__ m, float* __restrict__ v, int64_t n,
+                                                   AdamScalars* sc, int64_t* pos, int64_t by,
+                                                   unsigned* done) {
+  pdl_wait();
+  AdamScalars a = *sc;
+  a.step += 1;
+  a.b1p = fmul(a.b1p, 0.9f);
+  a.b2p = fmul(a.b2p, 0.999f);
+  a.bc1 = fsub(1.0f, a.b1p);
+  a.bc2 = fsub(1.0f, a.b2p);
+  const float b1 = 0.9f, b2 = 0.999f, lr = 5e-4f, eps = 1e-8f;
+  const float omb1 = fsub(1.0f, b1), omb2 = fsub(1.0f, b2);
+  constexpr int U = 4;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    float gi[U], mo[U], vo[U], wo[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n) {
+        gi[u] = g[i];
+        mo[u] = m[i];
+        vo[u] = v[i];
+        wo[u] = w[i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n) {
+        const float mi = fadd(fmul(b1, mo[u]), fmul(omb1, gi[u]));
+        const float vi = fadd(fmul(b2, vo[u]), fmul(fmul(omb2, gi[u]), gi[u]));
+        const float mhat = fdiv(mi, a.bc1);
+        const float vhat = fdiv(vi, a.bc2);
+        w[i] = fsub(wo[u], fdiv(fmul(lr, mhat), fadd(__fsqrt_rn(vhat), eps)));
+        m[i] = mi;
+        v[i] = vi;
+        g[i] = 0.0f;
+      }
+    }
+  }
+  __syncthreads();  // the block's reads of *sc are done
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done, 1u) == gridDim.x - 1) {
+      *sc = a;
+      *pos += by;
+      *done = 0u;
+    }
+  }
+}
+
 __global__ void k_pos_advance(int64_t* pos, int64_t by) {
   pdl_wait(); *pos += by; }
 
@@ -1673,6 +1732,12 @@ void launch_bigru_xf(const float* x1, float* Xf, int R, int T, int In, cudaStrea
 }
 void launch_tanh_vec(float* x, int64_t n, cudaStream_t st) {
   launch_pdl(k_tanh_vec, dim3(unsigned((n + 255) / 256)), dim3(256), 0, st, x, n);
+}
+void launch_sprm_adam(float* w, float* g, float* m, float* v, int64_t n, AdamScalars* sc, int64_t* pos,
+                      int64_t by, unsigned* done, cudaStream_t st) {
+  const int64_t per = (n + 255) / 256;
+  launch_pdl(k_sprm_adam, dim3(unsigned(per < 64 ? per : 64)), dim3(256), 0, st, w, g, m, v, n, sc, pos, by,
+             done);
 }
 void launch_adam_scalars(AdamScalars* sc, cudaStream_t st) { launch_pdl(k_adam_scalars, dim3(1), dim3(1), 0, st, sc); }
 void launch_pos_advance(int64_t* pos, int64_t by, cudaStream_t st) {
