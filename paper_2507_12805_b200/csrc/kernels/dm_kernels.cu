@@ -1039,6 +1039,7 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_fwd_row(
   }
 }
 
+template <int EB>  // fused dx: e per warp block (EB/2 paired chains per lane)
 __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
     const float* __restrict__ q, const float* __restrict__ k, const float* __restrict__ v,
     const float* __restrict__ wts, const float* __restrict__ dctx, float* dq, float* dkT,
@@ -1146,32 +1147,35 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
   // chain of the two accumulating GEMMs it replaces (Linear::backward x2,
   // layers.cpp:176-183; K terms first, layers.cpp:505-512)
   __syncthreads();
-  // lane = t, warp = a block of 8 e (4 paired chains per lane): W rows are
+  // lane = t, warp = a block of EB e (EB/2 paired chains per lane): W rows are
   // broadcast LDS.128 reads, the dk/dv row one conflict-free LDS per h
   float* dxr = fx.dx + c * fx.dx_cs + int64_t(r) * T * d.E;
-  for (int eb = h * 8; eb < d.E; eb += d.NH * 8) {
+  for (int eb = h * EB; eb < d.E; eb += d.NH * EB) {
     for (int t = lane; t < T; t += 32) {
       const float* dkr = Dk + t * (H + 1);
       const float* dvr = Dv + t * (H + 1);
-      f2_t acc[4] = {0, 0, 0, 0};
+      f2_t acc[EB / 2];
+#pragma unroll
+      for (int i = 0; i < EB / 2; ++i) acc[i] = 0;
       auto chain = [&](const float* dr, const float* Ws) {
 #pragma unroll 4
         for (int hh = 0; hh < H; ++hh) {
           const f2_t dv2 = f2_bcast(dr[hh]);
-          const float4 wa = *reinterpret_cast<const float4*>(Ws + hh * d.E + eb);
-          const float4 wb = *reinterpret_cast<const float4*>(Ws + hh * d.E + eb + 4);
-          acc[0] = f2_mac(acc[0], dv2, f2_pack(wa.x, wa.y));
-          acc[1] = f2_mac(acc[1], dv2, f2_pack(wa.z, wa.w));
-          acc[2] = f2_mac(acc[2], dv2, f2_pack(wb.x, wb.y));
-          acc[3] = f2_mac(acc[3], dv2, f2_pack(wb.z, wb.w));
+#pragma unroll
+          for (int i4 = 0; i4 < EB / 4; ++i4) {
+            const float4 wa = *reinterpret_cast<const float4*>(Ws + hh * d.E + eb + 4 * i4);
+            acc[2 * i4] = f2_mac(acc[2 * i4], dv2, f2_pack(wa.x, wa.y));
+            acc[2 * i4 + 1] = f2_mac(acc[2 * i4 + 1], dv2, f2_pack(wa.z, wa.w));
+          }
         }
       };
       chain(dkr, Wks);
       chain(dvr, Wvs);
       float* o = dxr + t * d.E + eb;
-      *reinterpret_cast<float4*>(o) = make_float4(f2_lo(acc[0]), f2_hi(acc[0]), f2_lo(acc[1]), f2_hi(acc[1]));
-      *reinterpret_cast<float4*>(o + 4) =
-          make_float4(f2_lo(acc[2]), f2_hi(acc[2]), f2_lo(acc[3]), f2_hi(acc[3]));
+#pragma unroll
+      for (int i4 = 0; i4 < EB / 4; ++i4)
+        *reinterpret_cast<float4*>(o + 4 * i4) = make_float4(f2_lo(acc[2 * i4]), f2_hi(acc[2 * i4]),
+                                                             f2_lo(acc[2 * i4 + 1]), f2_hi(acc[2 * i4 + 1]));
     }
   }
 }
@@ -1767,10 +1771,18 @@ bool launch_attn_bwd(const float* q, const float* k, const float* v, const float
     const bool fuse = fx.dx && d.NH * 32 == kRowThreads && d.E % 8 == 0 &&
                       base + extra <= 200 * 1024;
     const size_t smem = base + (fuse ? extra : 0);
-    ensure_smem(reinterpret_cast<const void*>(k_attn_bwd_row), smem);
     AttnDx f = fx;
     if (!fuse) f.dx = nullptr;
-    launch_pdl(k_attn_bwd_row, dim3(dim3(d.R, max_active)), dim3(kRowThreads), smem, st, 
+    // e per warp in the fused dx: 4 while the 8 warps still have e left to
+    // share (E <= 32), else 8
+    static const int eb_env = [] {
+      const char* e = std::getenv("PMKLC_ATTN_DX_EB");
+      return e ? std::atoi(e) : 0;
+    }();
+    const int eb = eb_env ? eb_env : (d.E <= 4 * d.NH ? 4 : 8);
+    const auto kern = eb == 4 ? k_attn_bwd_row<4> : k_attn_bwd_row<8>;
+    ensure_smem(reinterpret_cast<const void*>(kern), smem);
+    launch_pdl(kern, dim3(dim3(d.R, max_active)), dim3(kRowThreads), smem, st,
         q, k, v, wts, dctx, dq, dk, dv, cs_q, cs_kv, cs_w, d, inv, f, td, kt);
     return fuse;
   }

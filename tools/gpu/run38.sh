@@ -1,0 +1,5 @@
+timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -x -q 2>&1 | tail -2
+for eb in 8 4 8 4; do
+  echo "== EB=$eb"; PMKLC_ATTN_DX_EB=$eb timeout 600 python bench.py --steps 2 --warmup 1 --no-config4 --skip-cpu --no-sprm-branch 2>/dev/null | python -c "
+import sys,json; d=json.loads(sys.stdin.readlines()[-1]); print(d['value'], d['ms_per_step'], d['step_breakdown_ms'])"
+done
