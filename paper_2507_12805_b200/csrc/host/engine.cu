@@ -374,6 +374,7 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
   // their state by the SMP handoff copy at their first tick
   DBuf<float> w(S * P), g(S * P), m(S * P), v(S * P);
   DBuf<AdamScalars> sc(std::max<size_t>(S, 1));
+  DBuf<float> wkvT(std::max<size_t>(S, 1) * 2 * size_t(E) * H);  // attention backward's W_k^T, W_v^T
   g.zero(st);
   {
     const std::vector<float> seeded = lay.seeded(run.dm_seed);
@@ -719,10 +720,10 @@ void run_chunks(ChunkRun& run, uint32_t* d_tokens, cudaStream_t st) {
     gemm(GemmP{datt.p, s_rh, H, W_(DmLayout::OW), P, H, dctx.p, s_rh, H, nullptr, 0, nullptr, 0, 0,
                R, H, H, 0, 0, 0},
          false, true);
-    const AttnDx fx{W_(DmLayout::KW), W_(DmLayout::VW), P, dx.p, s_x};
+    const AttnDx fx{W_(DmLayout::KW), W_(DmLayout::VW), P, dx.p, s_x, wkvT.p};
     const bool dx_fused = launch_attn_bwd(q.p, kk.p, vv.p, wts.p, dctx.p, dq.p, dk.p, dv.p, s_rh,
                                           s_kv, s_w, dd, inv_hd, fx, act, na, st, kvt);
-    ++run.launches;
+    run.launches += dx_fused ? 2 : 1;  // + k_wkv_transpose
     // q/k/v projections: weight+bias grads, then dx = dk Wk^T + dv Wv^T, dxl = dq Wq^T
     // dWk|dbk and dWv|dbv: reductions over all R*T rows of feature-major x, dk, dv
     to_side();

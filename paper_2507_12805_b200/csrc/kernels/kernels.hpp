@@ -141,6 +141,9 @@ void launch_attn_fwd(const float* q, const float* k, const float* v, float* wts,
 struct AttnDx {
   const float* wk; const float* wv; int64_t w_cs;  // W_k, W_v [E][H] per chunk
   float* dx; int64_t dx_cs;                        // dx [R*T][E] per chunk, or nullptr
+  // scratch [slot][2][H][E] (nullable): W_k^T, W_v^T formed once per launch for
+  // every row block of the chunk to stage with 16-byte copies
+  float* wT = nullptr;
 };
 bool launch_attn_bwd(const float* q, const float* k, const float* v, const float* wts,
                      const float* dctx, float* dq, float* dk, float* dv, int64_t cs_q,

@@ -7,6 +7,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -87,6 +89,20 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   cfg.attrs = attr;
   cfg.numAttrs = na;
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  // PMKLC_DEBUG_SYNC=1: every launch synchronised and checked, naming the
+  // kernel that failed (a fault otherwise surfaces at the next checked call)
+  static const bool dbg = std::getenv("PMKLC_DEBUG_SYNC") != nullptr;
+  if (dbg) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    const cudaError_t e = cs == cudaStreamCaptureStatusNone ? cudaStreamSynchronize(st) : cudaGetLastError();
+    if (e != cudaSuccess) {
+      const char* name = nullptr;
+      cudaFuncGetName(&name, reinterpret_cast<const void*>(kernel));
+      std::fprintf(stderr, "PMKLC_DEBUG_SYNC: %s after %s\n", cudaGetErrorString(e), name ? name : "?");
+      std::abort();
+    }
+  }
 }
 
 }  // namespace pmklc_b200

@@ -1,0 +1,6 @@
+timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -x -q 2>&1 | tail -2
+for wt in 1 0 1 0; do
+  if [ $wt = 0 ]; then export PMKLC_ATTN_NO_WT=1; else unset PMKLC_ATTN_NO_WT; fi
+  echo "== WT=$wt"; timeout 600 python bench.py --steps 2 --warmup 1 --no-config4 --skip-cpu --no-sprm-branch 2>/dev/null | python -c "
+import sys,json; d=json.loads(sys.stdin.readlines()[-1]); print(d['value'], d['ms_per_step'], d['step_breakdown_ms'])"
+done
