@@ -1006,49 +1006,54 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_fwd_row(
   for (int i = threadIdx.x; i < H; i += blockDim.x) Qs[i] = q[c * cs_q + int64_t(r) * H + i];
   cp_async_wait<0>();
   __syncthreads();
-  if (h >= d.NH) return;
-  const float* qh = Qs + h * HD;
-  float* wrow = Ws + h * T;
-  const bool hd4 = (HD & 3) == 0;  // head slices 16-byte aligned
-  float mx = -__int_as_float(0x7f800000);
-  for (int t = lane; t < T; t += 32) {
-    const float* kr = Ks + t * HP + h * HD;
-    float s = 0.0f;
-    for (int d0 = 0; d0 < HD; d0 += 4) {  // LDS.128 per 4 dims: conflict-free across t
-      const float4 k4 = ld_head4(kr + d0, HD - d0, hd4);
-      const float kv[4] = {k4.x, k4.y, k4.z, k4.w};
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (d0 + u < HD) s = mac(s, qh[d0 + u], kv[u]);
+  if (h < d.NH) {  // scores and det_softmax, warp per head
+    const float* qh = Qs + h * HD;
+    float* wrow = Ws + h * T;
+    const bool hd4 = (HD & 3) == 0;  // head slices 16-byte aligned
+    float mx = -__int_as_float(0x7f800000);
+    for (int t = lane; t < T; t += 32) {
+      const float* kr = Ks + t * HP + h * HD;
+      float s = 0.0f;
+      for (int d0 = 0; d0 < HD; d0 += 4) {  // LDS.128 per 4 dims: conflict-free across t
+        const float4 k4 = ld_head4(kr + d0, HD - d0, hd4);
+        const float kv[4] = {k4.x, k4.y, k4.z, k4.w};
+  #pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (d0 + u < HD) s = mac(s, qh[d0 + u], kv[u]);
+      }
+      s = fmul(s, inv);
+      wrow[t] = s;
+      mx = fmaxf(mx, s);
     }
-    s = fmul(s, inv);
-    wrow[t] = s;
-    mx = fmaxf(mx, s);
-  }
-  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  float sum = 0.0f;
-  for (int t0 = 0; t0 < T; t0 += 32) {
-    const int t = t0 + lane;
-    float e = 0.0f;
-    if (t < T) {
-      e = det_exp(fsub(wrow[t], mx));
-      wrow[t] = e;
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.0f;
+    for (int t0 = 0; t0 < T; t0 += 32) {
+      const int t = t0 + lane;
+      float e = 0.0f;
+      if (t < T) {
+        e = det_exp(fsub(wrow[t], mx));
+        wrow[t] = e;
+      }
+      const int cnt = min(32, T - t0);
+      for (int i = 0; i < cnt; ++i) sum = fadd(sum, __shfl_sync(0xffffffffu, e, i));
     }
-    const int cnt = min(32, T - t0);
-    for (int i = 0; i < cnt; ++i) sum = fadd(sum, __shfl_sync(0xffffffffu, e, i));
+    const float invs = fdiv(1.0f, sum);
+    float* wg = wts + c * cs_w + (int64_t(r) * d.NH + h) * T;
+    for (int t = lane; t < T; t += 32) {
+      const float wv = fmul(wrow[t], invs);
+      wrow[t] = wv;
+      wg[t] = wv;
+    }
   }
-  const float invs = fdiv(1.0f, sum);
-  float* wg = wts + c * cs_w + (int64_t(r) * d.NH + h) * T;
-  for (int t = lane; t < T; t += 32) {
-    const float wv = fmul(wrow[t], invs);
-    wrow[t] = wv;
-    wg[t] = wv;
-  }
-  __syncwarp();
-  if (lane < HD) {
+  // context, one output per thread over the block (all heads' weights are in
+  // shared memory): cx[o] = 0 + sum_t w[o/HD][t] * v_t[o], t ascending -- a
+  // warp per head would leave all but HD of its lanes idle
+  __syncthreads();
+  for (int o = threadIdx.x; o < H; o += blockDim.x) {
+    const float* wr = Ws + (o / HD) * T;
     float acc = 0.0f;
-    for (int t = 0; t < T; ++t) acc = mac(acc, wrow[t], Vs[t * HP + h * HD + lane]);
-    cx[c * cs_q + int64_t(r) * H + h * HD + lane] = acc;
+    for (int t = 0; t < T; ++t) acc = mac(acc, wr[t], Vs[t * HP + o]);
+    cx[c * cs_q + int64_t(r) * H + o] = acc;
   }
 }
 
