@@ -1126,63 +1126,68 @@ __global__ void __launch_bounds__(kRowThreads) k_attn_bwd_row(
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
-  if (h >= d.NH) return;
-  const float* w = wts + c * cs_w + (int64_t(r) * d.NH + h) * T;
-  const float* dc = Cs + h * HD;
-  const int64_t to = c * cs_kv + int64_t(h) * HD * RT + int64_t(r) * T;  // feature-major dk, dv
-  float* dsw = Ds + h * T;
-  const bool hd4 = (HD & 3) == 0;  // head slices 16-byte aligned
-  // dv_t[d] = 0 + w_t*dc[d]; dwt_t = sum_d dc[d]*v_t[d]; dot = sum_t w_t*dwt_t
-  float dot = 0.0f;
-  for (int t0 = 0; t0 < T; t0 += 32) {
-    const int t = t0 + lane;
-    float prod = 0.0f;
-    if (t < T) {
-      const float wt = w[t];
-      const float* vr = Vs + t * HP + h * HD;
-      float acc = 0.0f;
-      for (int d0 = 0; d0 < HD; d0 += 4) {
-        // one LDS.128 per 4 dims (rows 272 B apart: conflict-free), then the chain
-        const float4 v4 = ld_head4(vr + d0, HD - d0, hd4);
-        const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+  if (h < d.NH) {  // warp per head: dv, the dot chain, ds and dk
+    const float* w = wts + c * cs_w + (int64_t(r) * d.NH + h) * T;
+    const float* dc = Cs + h * HD;
+    const int64_t to = c * cs_kv + int64_t(h) * HD * RT + int64_t(r) * T;  // feature-major dk, dv
+    float* dsw = Ds + h * T;
+    const bool hd4 = (HD & 3) == 0;  // head slices 16-byte aligned
+    // dv_t[d] = 0 + w_t*dc[d]; dwt_t = sum_d dc[d]*v_t[d]; dot = sum_t w_t*dwt_t
+    float dot = 0.0f;
+    for (int t0 = 0; t0 < T; t0 += 32) {
+      const int t = t0 + lane;
+      float prod = 0.0f;
+      if (t < T) {
+        const float wt = w[t];
+        const float* vr = Vs + t * HP + h * HD;
+        float acc = 0.0f;
+        for (int d0 = 0; d0 < HD; d0 += 4) {
+          // one LDS.128 per 4 dims (rows 272 B apart: conflict-free), then the chain
+          const float4 v4 = ld_head4(vr + d0, HD - d0, hd4);
+          const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int dd = d0 + u;
-          if (dd >= HD) break;
-          const float dvv = fadd(0.0f, fmul(wt, dc[dd]));
-          dvT[to + int64_t(dd) * RT + t] = dvv;
-          if (fuse) Dv[t * (H + 1) + h * HD + dd] = dvv;
-          acc = mac(acc, dc[dd], vv[u]);
+          for (int u = 0; u < 4; ++u) {
+            const int dd = d0 + u;
+            if (dd >= HD) break;
+            const float dvv = fadd(0.0f, fmul(wt, dc[dd]));
+            dvT[to + int64_t(dd) * RT + t] = dvv;
+            if (fuse) Dv[t * (H + 1) + h * HD + dd] = dvv;
+            acc = mac(acc, dc[dd], vv[u]);
+          }
         }
+        dsw[t] = acc;  // dwt_t, turned into ds_t below
+        prod = fmul(wt, acc);
       }
-      dsw[t] = acc;  // dwt_t, turned into ds_t below
-      prod = fmul(wt, acc);
+      const int cnt = min(32, T - t0);
+      for (int i = 0; i < cnt; ++i) dot = fadd(dot, __shfl_sync(0xffffffffu, prod, i));
     }
-    const int cnt = min(32, T - t0);
-    for (int i = 0; i < cnt; ++i) dot = fadd(dot, __shfl_sync(0xffffffffu, prod, i));
-  }
-  // ds_t = (w_t*(dwt_t - dot))*inv;  dk_t[d] = 0 + ds_t*q[d]
-  for (int t = lane; t < T; t += 32) {
-    const float ds = fmul(fmul(w[t], fsub(dsw[t], dot)), inv);
-    dsw[t] = ds;
-    for (int dd = 0; dd < HD; ++dd) {
-      const float dkv = fadd(0.0f, fmul(ds, Qs[h * HD + dd]));
-      dkT[to + int64_t(dd) * RT + t] = dkv;
-      if (fuse) Dk[t * (H + 1) + h * HD + dd] = dkv;
+    // ds_t = (w_t*(dwt_t - dot))*inv;  dk_t[d] = 0 + ds_t*q[d]
+    for (int t = lane; t < T; t += 32) {
+      const float ds = fmul(fmul(w[t], fsub(dsw[t], dot)), inv);
+      dsw[t] = ds;
+      for (int dd = 0; dd < HD; ++dd) {
+        const float dkv = fadd(0.0f, fmul(ds, Qs[h * HD + dd]));
+        dkT[to + int64_t(dd) * RT + t] = dkv;
+        if (fuse) Dk[t * (H + 1) + h * HD + dd] = dkv;
+      }
     }
   }
-  __syncwarp();
-  // dq[d] = 0 + sum_t ds_t*k_t[d]
-  if (lane < HD) {
-    float acc = 0.0f;
-    for (int t = 0; t < T; ++t) acc = mac(acc, dsw[t], Ks[t * HP + h * HD + lane]);
-    dq[c * cs_q + int64_t(r) * H + h * HD + lane] = acc;
-  }
+  __syncthreads();  // every head's ds (Ds) and, fused, dk/dv rows (Dk, Dv) in shared memory
+  // dq[o] = 0 + sum_t ds_t*k_t[o], t ascending: one output per thread on the
+  // warps the fused dx leaves idle (a warp per head would use HD lanes)
+  const int ndx = fuse ? min(d.NH, (d.E + EB - 1) / EB) : 0;
+  const int base = ndx * 32 < int(blockDim.x) ? ndx * 32 : 0;
+  if (int(threadIdx.x) >= base)
+    for (int o = int(threadIdx.x) - base; o < H; o += int(blockDim.x) - base) {
+      const float* dsr = Ds + (o / HD) * T;
+      float acc = 0.0f;
+      for (int t = 0; t < T; ++t) acc = mac(acc, dsr[t], Ks[t * HP + o]);
+      dq[c * cs_q + int64_t(r) * H + o] = acc;
+    }
   if (!fuse) return;
   // dx[r][t][e] = (0 + dk_t . W_k[e]) then + dv_t . W_v[e], h ascending: the
   // chain of the two accumulating GEMMs it replaces (Linear::backward x2,
   // layers.cpp:176-183; K terms first, layers.cpp:505-512)
-  __syncthreads();
   // lane = t, warp = a block of EB e (EB/2 paired chains per lane): W rows are
   // broadcast LDS.128 reads, the dk/dv row one conflict-free LDS per h
   float* dxr = fx.dx + c * fx.dx_cs + int64_t(r) * T * d.E;
