@@ -80,13 +80,56 @@ __device__ __forceinline__ void emit_tokens(const uint32_t* sw, uint64_t sbase, 
   }
 }
 
-template <int kTokPerThread, typename TokT, bool kPad = false>
+// The same extraction at a compile-time stride kS: a lane's PER tokens span
+// (PER-1)*kS + k bases from its first base, so it loads that span's NW words
+// once, aligns them to its first base with one runtime funnel shift per word,
+// and cuts every token out at compile-time word and bit offsets (u16, s = 3:
+// 4 shared loads per 8 tokens instead of 16).
+template <int kTokPerThread, typename TokT, int kS, bool kPad = false>
+__device__ __forceinline__ void emit_tokens_s(const uint32_t* sw, uint64_t sbase, uint64_t j0, uint32_t k,
+                                              TokT* tokens, uint64_t m) {
+  constexpr int PER = 16 / int(sizeof(TokT));
+  static_assert(kTokPerThread % PER == 0, "whole slabs per thread");
+  constexpr int NA = ((PER - 1) * kS) / 16 + 2;  // aligned words a lane's tokens touch
+  constexpr int NW = NA + 1;                     // staged words behind them
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t jw = j0 + uint64_t(w) * 32 * kTokPerThread;
+  if (jw >= m) return;
+  const uint32_t rsh = 32u - 2u * k;  // k <= 16
+#pragma unroll
+  for (int slab = 0; slab < kTokPerThread / PER; ++slab) {
+    const uint64_t jt = jw + uint64_t(slab) * 32 * PER + uint64_t(lane) * PER;
+    const uint32_t b = uint32_t(jt * kS - sbase);  // first base of the lane in the window
+    const uint32_t w0 = b >> 4, sh = 2u * (b & 15u);
+    uint32_t W[NW], A[NA];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) W[i] = kPad ? sw[padw(w0 + i)] : sw[w0 + i];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) A[i] = __funnelshift_l(W[i + 1], W[i], sh);
+    TokT out[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int qi = (q * kS) / 16, oo = (q * kS) % 16;
+      out[q] = TokT(__funnelshift_l(A[qi + 1], A[qi], 2u * oo) >> rsh);
+    }
+    if (jt + PER <= m) {
+      uint4 v;
+      memcpy(&v, out, 16);
+      *reinterpret_cast<uint4*>(tokens + jt) = v;
+    } else {
+      for (int q = 0; q < PER && jt + q < m; ++q) tokens[jt + q] = out[q];
+    }
+  }
+}
+
+// kS: the stride at compile time (1..8, the reference's range), 0 = runtime
+template <int kTokPerThread, typename TokT, bool kPad = false, int kS = 0>
 __global__ void __launch_bounds__(kTokThreads) k_skmer_packed(const uint8_t* __restrict__ packed,
                                                               uint64_t n, uint32_t s, uint32_t k,
                                                               TokT* __restrict__ tokens,
                                                               uint64_t m) {
   pdl_wait();
-  __shared__ __align__(16) uint32_t sw[kStageBytes / 4 + (kPad ? kStageBytes / 128 + 2 : 0)];
+  __shared__ __align__(16) uint32_t sw[kStageBytes / 4 + (kPad ? kStageBytes / 128 + 2 : 0) + 8];
   constexpr int kTokPerBlock = kTokThreads * kTokPerThread;
   const uint64_t j0 = uint64_t(blockIdx.x) * kTokPerBlock;
   const uint64_t jlast = min(j0 + kTokPerBlock, m) - 1;
@@ -125,7 +168,10 @@ __global__ void __launch_bounds__(kTokThreads) k_skmer_packed(const uint8_t* __r
     }
   }
   __syncthreads();
-  emit_tokens<kTokPerThread, TokT, kPad>(sw, byte0 * 4, j0, s, k, tokens, m);
+  if constexpr (kS > 0)
+    emit_tokens_s<kTokPerThread, TokT, kS, kPad>(sw, byte0 * 4, j0, k, tokens, m);
+  else
+    emit_tokens<kTokPerThread, TokT, kPad>(sw, byte0 * 4, j0, s, k, tokens, m);
 }
 
 // ASCII / code input: stage 16 bytes per step, pack to 2-bit on the way in.
@@ -296,18 +342,38 @@ __global__ void k_detok_restore(const uint32_t* __restrict__ tokens, uint64_t m,
 
 }  // namespace
 
+// f(integral_constant<int, s>) for the reference's strides 1..8, else f(<0>)
+template <typename F>
+static void with_stride(uint32_t s, F&& f) {
+  using std::integral_constant;
+  switch (s) {
+    case 1: f(integral_constant<int, 1>{}); break;
+    case 2: f(integral_constant<int, 2>{}); break;
+    case 3: f(integral_constant<int, 3>{}); break;
+    case 4: f(integral_constant<int, 4>{}); break;
+    case 5: f(integral_constant<int, 5>{}); break;
+    case 6: f(integral_constant<int, 6>{}); break;
+    case 7: f(integral_constant<int, 7>{}); break;
+    case 8: f(integral_constant<int, 8>{}); break;
+    default: f(integral_constant<int, 0>{}); break;
+  }
+}
 template <typename TokT>
 static void launch_packed(const uint8_t* packed, uint64_t n, uint32_t s, uint32_t k, TokT* tokens,
                           uint64_t m, cudaStream_t st) {
   if (m == 0) return;
-  if (s <= 2) {
-    const uint64_t blocks = (m + kTokThreads * kTptSmallStride - 1) / (kTokThreads * kTptSmallStride);
-    launch_pdl(k_skmer_packed<kTptSmallStride, TokT>, dim3(unsigned(blocks)), dim3(kTokThreads), 0, st, packed, n, s, k,
-                                                                                  tokens, m);
-  } else {
-    const uint64_t blocks = (m + kTokThreads * kTpt - 1) / (kTokThreads * kTpt);
-    launch_pdl(k_skmer_packed<kTpt, TokT>, dim3(unsigned(blocks)), dim3(kTokThreads), 0, st, packed, n, s, k, tokens, m);
-  }
+  with_stride(s, [&](auto s_c) {
+    constexpr int kS = decltype(s_c)::value;
+    if (s <= 2) {
+      const uint64_t blocks = (m + kTokThreads * kTptSmallStride - 1) / (kTokThreads * kTptSmallStride);
+      launch_pdl(k_skmer_packed<kTptSmallStride, TokT, false, kS>, dim3(unsigned(blocks)), dim3(kTokThreads), 0,
+                 st, packed, n, s, k, tokens, m);
+    } else {
+      const uint64_t blocks = (m + kTokThreads * kTpt - 1) / (kTokThreads * kTpt);
+      launch_pdl(k_skmer_packed<kTpt, TokT, false, kS>, dim3(unsigned(blocks)), dim3(kTokThreads), 0, st, packed,
+                 n, s, k, tokens, m);
+    }
+  });
 }
 void launch_skmer_encode_packed(const uint8_t* packed, uint64_t n, uint32_t s, uint32_t k,
                                 uint32_t* tokens, uint64_t m, cudaStream_t st) {
@@ -324,8 +390,10 @@ void launch_skmer_encode_packed16(const uint8_t* packed, uint64_t n, uint32_t s,
     // the window of a block: tpt*256 tokens at stride <= smax, + k-1 halo, 16-byte aligned
     static_assert(kTokThreads * tpt * smax / 4 + 32 <= kStageBytes, "staging bound");
     const uint64_t blocks = (m + kTokThreads * tpt - 1) / (kTokThreads * tpt);
-    launch_pdl(k_skmer_packed<tpt, uint16_t, decltype(pad_c)::value>, dim3(unsigned(blocks)),
-               dim3(kTokThreads), 0, st, packed, n, s, k, tokens, m);
+    with_stride(s, [&](auto s_c) {
+      launch_pdl(k_skmer_packed<tpt, uint16_t, decltype(pad_c)::value, decltype(s_c)::value>,
+                 dim3(unsigned(blocks)), dim3(kTokThreads), 0, st, packed, n, s, k, tokens, m);
+    });
   };
   // measured (2^30 bases): the padded staging pays off only where a lane's 8
   // tokens span >= 2.5 words (s > 4: 0.50 -> 0.69 of the copy peak at (8,8));
