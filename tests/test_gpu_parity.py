@@ -575,3 +575,38 @@ def test_corrupt_container_fuzz(P, checker):
             assert e.errc != "CudaError", (trial, str(e))
             outcomes[e.errc] = outcomes.get(e.errc, 0) + 1
     assert sum(outcomes.values()) == 60
+
+
+def _random_configs(n_cfg=24, seed=20261019):
+    # seeded draws over the geometry the kernels are specialised on: odd and
+    # even contexts and batch rows, several widths, vocabularies up to 4^6,
+    # 1-5 chunks with SMP, both input generators, a third with a seeded SPuM
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n_cfg):
+        k = int(rng.integers(1, 7))
+        s = int(rng.integers(1, k + 1))
+        kw = dict(s=s, k=k, t=int(rng.choice([2, 3, 5, 8, 13, 16])),
+                  bs=int(rng.choice([3, 4, 7, 8, 12, 16, 24])), scale=int(rng.choice([4, 8, 16])),
+                  workers=int(rng.choice([1, 2, 3, 5])), smp=float(rng.choice([0.05, 0.1, 0.3])))
+        n = int(rng.integers(4000, 24000))
+        kind = str(rng.choice(["markov3", "genome"]))
+        spum = bool(rng.random() < 0.34)
+        out.append((i, kind, n, kw, spum))
+    return out
+
+
+@pytest.mark.parametrize("case", _random_configs(), ids=lambda c: f"cfg{c[0]}")
+def test_random_geometry_sweep(P, checker, tmp_path, case):
+    # containers byte-identical to the reference's and lossless over seeded
+    # random geometries (the specialised kernel paths: head widths, odd t/bs,
+    # tile remainders, vocabulary sizes; flags 5 with a seeded SPuM)
+    i, kind, n, kw, spum = case
+    raw = P.synth(kind, n, 7000 + i, 10) if kind == "genome" else P.synth(kind, n, 7000 + i)
+    if spum:
+        path = str(tmp_path / "spum.bin")
+        O.write_spum(path, kw["k"], kw["t"], kw["scale"], 0xACE3 + i)
+        kw = dict(kw, pub_path=path)
+    blob = P.compress(raw, P.CompressConfig(**_cfgs(kw)))
+    assert blob == checker.compress(raw, O.make_cfg(**kw)), kw
+    assert P.decompress(blob, kw.get("pub_path", "")) == raw
