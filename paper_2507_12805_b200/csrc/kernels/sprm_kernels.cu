@@ -187,13 +187,15 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_sprm_fwd32(SprmP s, const ui
               bhn = W[goff(s.offs, d, BHN) + j];
   const float* t0 = tab + int64_t(d) * 3 * V * H;
   const int64_t TRH = int64_t(T) * R * H;
-  float* tr = tape + (int64_t(0 * 2 + d) * TRH);
-  float* tz = tape + (int64_t(1 * 2 + d) * TRH);
-  float* tn = tape + (int64_t(2 * 2 + d) * TRH);
-  float* th = tape + (int64_t(3 * 2 + d) * TRH);
-  float* to = tape + (int64_t(4 * 2 + d) * TRH);
+  // the step's tape slot (t*R + r)*H + j of slab g at tp + g*2*TRH, advanced by R*H
+  float* tp = tape + int64_t(d) * TRH + int64_t(r) * H + j;
+  const int64_t RH = int64_t(R) * H;
   sh[wl][0][j] = 0.0f;
   const int64_t RTH = int64_t(R) * T * H;
+  // the row's context tokens, one per lane (T <= 32): a step's token is a
+  // shuffle, so its table loads do not wait behind a dependent token load
+  const bool lane_tok = !s.xproj && T <= 32;
+  const uint32_t mytok = lane_tok && lane < T ? ctx[int64_t(r) * T + lane] : 0u;
   auto fetch = [&](int t, float (&x)[3]) {
     const int src_t = d ? (T - 1 - t) : t;
     if (s.xproj) {  // deeper layer: per-(row, position) input projections
@@ -203,17 +205,20 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_sprm_fwd32(SprmP s, const ui
       x[2] = xp[2 * RTH];
       return;
     }
-    const int64_t k0 = ctx[int64_t(r) * T + src_t];
+    const int64_t k0 = lane_tok ? int64_t(__shfl_sync(0xffffffffu, mytok, src_t))
+                                : int64_t(ctx[int64_t(r) * T + src_t]);
     x[0] = t0[k0 * H + j];
     x[1] = t0[int64_t(V) * H + k0 * H + j];
     x[2] = t0[2 * int64_t(V) * H + k0 * H + j];
   };
-  float xc[3], xn[3];
+  // input terms fetched two steps ahead
+  float xc[3], x1[3], x2[3];
   fetch(0, xc);
+  if (T > 1) fetch(1, x1);
   __syncwarp();
   int cur = 0;
   for (int t = 0; t < T; ++t) {
-    if (t + 1 < T) fetch(t + 1, xn);
+    if (t + 2 < T) fetch(t + 2, x2);
     f2_t arz = f2_pack(fadd(xc[0], bhr), fadd(xc[1], bhz));
     float hh = bhn;
     const float* h = sh[wl][cur];
@@ -231,17 +236,20 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_sprm_fwd32(SprmP s, const ui
     const float rv = f2_lo(rz), zv = f2_hi(rz);
     const float nv = det_tanh(fadd(xc[2], fmul(rv, hh)));
     const float hv = fadd(fmul(fsub(1.0f, zv), nv), fmul(zv, h[j]));
-    const int64_t o = (int64_t(t) * R + r) * H + j;
-    tr[o] = rv;
-    tz[o] = zv;
-    tn[o] = nv;
-    th[o] = hh;
-    to[o] = hv;
+    tp[0] = rv;
+    tp[2 * TRH] = zv;
+    tp[4 * TRH] = nv;
+    tp[6 * TRH] = hh;
+    tp[8 * TRH] = hv;
+    tp += RH;
     sh[wl][cur ^ 1][j] = hv;
     __syncwarp();
     cur ^= 1;
 #pragma unroll
-    for (int g = 0; g < 3; ++g) xc[g] = xn[g];
+    for (int g = 0; g < 3; ++g) {
+      xc[g] = x1[g];
+      x1[g] = x2[g];
+    }
   }
   fin[int64_t(r) * 2 * H + d * H + j] = sh[wl][cur][j];  // final_state (layers.cpp:389-399)
 }
