@@ -723,6 +723,11 @@ __global__ void __launch_bounds__(256) k_sprm_bptt(SprmP s, const float* __restr
 // per-element operations and order as k_sprm_bptt.
 constexpr int kBpttWarps = 4;
 constexpr int kPubSteps = 8;  // BPTT progress published per group of steps
+constexpr int kBpttAhead = 8;  // tape staging depth (steps)
+__device__ __forceinline__ void cp_async4_sp(float* smem, const float* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+               "l"(gmem));
+}
 // cnt (nullable): per (direction, step) count of rows whose step is stored,
 // published with a release add after each step (the streamed reductions of
 // k_sprm_nt_stream wait on it)
@@ -732,6 +737,7 @@ __global__ void __launch_bounds__(kBpttWarps * 32) k_sprm_bptt32(SprmP s, const 
   pdl_wait();
   constexpr int H = 32;
   __shared__ __align__(16) float sg[kBpttWarps][3][H];  // dhh, dar, daz of this step
+  __shared__ float stape[kBpttWarps][kBpttAhead][5][H];  // staged tape values
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d = blockIdx.x & 1;
   const int r = (blockIdx.x >> 1) * kBpttWarps + wl;
@@ -765,17 +771,30 @@ __global__ void __launch_bounds__(kBpttWarps * 32) k_sprm_bptt32(SprmP s, const 
   // only the GRU's last own step receives the final-state gradient
   // (final_state_backward, layers.cpp:401-413), as 0 + dfin
   const float dlast = s.dout ? 0.0f : fadd(0.0f, dfin[int64_t(r) * 2 * H + d * H + j]);
-  auto fetch = [&](int t, float (&x)[5]) {
-    const int64_t o = (int64_t(t) * R + r) * H + j;
+  // The step's tape values (r, z, n, hh and h_{t-1} for this lane's unit)
+  // are staged kBpttAhead steps ahead by per-lane 4-byte async copies into a
+  // per-warp shared ring (each lane copies and reads only its own unit, so
+  // no barrier), keeping global-load latency out of the step loop.
+  auto issue = [&](int t) {  // step t's five values into ring slot t % kBpttAhead
+    if (t >= 0) {
+      const int64_t o = (int64_t(t) * R + r) * H + j;
+      float* dst = &stape[wl][t % kBpttAhead][0][j];
 #pragma unroll
-    for (int g = 0; g < 4; ++g) x[g] = tp[g][o];
-    x[4] = t == 0 ? 0.0f : tp[4][o - int64_t(R) * H];
+      for (int g = 0; g < 4; ++g) cp_async4_sp(dst + g * H, tp[g] + o);
+      if (t > 0) cp_async4_sp(dst + 4 * H, tp[4] + o - int64_t(R) * H);
+      else dst[4 * H] = 0.0f;
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
   };
-  float xc[5], xn[5];
-  fetch(T - 1, xc);
+#pragma unroll
+  for (int i = 0; i < kBpttAhead - 1; ++i) issue(T - 1 - i);
+  float xc[5];
   float dh = 0.0f;
   for (int t = T - 1; t >= 0; --t) {
-    if (t > 0) fetch(t - 1, xn);
+    issue(t - (kBpttAhead - 1));
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kBpttAhead - 1));
+#pragma unroll
+    for (int g = 0; g < 5; ++g) xc[g] = stape[wl][t % kBpttAhead][g][j];
     // gather_add_step(dout, t, dh): a deeper layer's output gradient at
     // position src_t (half d), else the final-state gradient at the last step
     const float dadd = s.dout ? s.dout[(int64_t(r) * T + (d ? T - 1 - t : t)) * 2 * H + d * H + j]
@@ -816,8 +835,6 @@ __global__ void __launch_bounds__(kBpttWarps * 32) k_sprm_bptt32(SprmP s, const 
       }
     __syncwarp();
     dh = dn;
-#pragma unroll
-    for (int g = 0; g < 5; ++g) xc[g] = xn[g];
   }
 }
 
