@@ -333,11 +333,14 @@ __device__ __forceinline__ uint32_t dec_target(uint64_t code, uint64_t rb) {
   // rb < 2^48, so rb * 2^16 cannot overflow: a (corrupt) code at or above it
   // clamps at once instead of stepping q up one at a time
   if (code >= (rb << 16)) return kTotal - 1;
-  uint64_t q = uint64_t(double(code) / double(rb));
-  if (q > kTotal) q = kTotal;
-  while (q > 0 && (__umul64hi(q, rb) != 0 || q * rb > code)) --q;
-  while (code - q * rb >= rb) ++q;
-  return q >= kTotal ? kTotal - 1 : uint32_t(q);
+  // now code < rb * 2^16: the quotient is below 2^16. A single-precision
+  // estimate (relative error ~2^-22, so off by at most one) is made exact by
+  // the integer corrections; q * rb < 2^64 throughout.
+  uint32_t q = uint32_t(__fdividef(__ull2float_rn(code), __ull2float_rn(rb)));
+  if (q > kTotal - 1) q = kTotal - 1;
+  while (q > 0 && uint64_t(q) * rb > code) --q;
+  while (code - uint64_t(q) * rb >= rb) ++q;
+  return q;
 }
 
 __device__ __forceinline__ uint32_t dec_sym(uint64_t& code, uint64_t& range, const uint8_t* in,
@@ -413,13 +416,113 @@ __global__ void k_range_uniform(uint32_t* tokens, ChunkGeo geo, int t, int R, in
   cs[c] = s;
 }
 
+constexpr int kMaxQ = 8;  // V <= 256 in registers; larger V uses the scalar search
+constexpr int kCumAhead = 8;  // decode: cum rows staged this many rows ahead
+__device__ __forceinline__ void cp_async4_u32(uint32_t* smem, const uint32_t* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(smem))),
+               "l"(gmem));
+}
+
+// Decode of one chunk's R symbols of this tick by one warp (NQ = ceil((V+1)/32)
+// cum words per lane). Every lane carries the same coder state. The cum rows
+// are staged kCumAhead rows ahead by per-lane async copies into the warp's
+// shared ring (a lane copies and reads only its own entries); the symbol is a
+// warp ballot count over the row (the reference's binary search: the largest
+// i with cum[i] <= target); the payload is a register window (lane l holds
+// bytes [wb + 4l, wb + 4l + 4) of the current 128 bytes, the next 128 bytes
+// fetched when the window advances), so no byte read waits on memory.
+template <int NQ>
+__device__ __forceinline__ void range_decode_rows(CoderState& s, uint32_t* tokens, uint64_t start, uint64_t L,
+                                                  uint64_t jstep, int R, int V, const uint32_t* cm,
+                                                  const uint8_t* buf, uint64_t plen,
+                                                  uint32_t (*ring)[kMaxQ * 32], int lane) {
+  auto stage = [&](int r) {
+    if (r < R) {
+      uint32_t* dst = ring[r % kCumAhead];
+      const uint32_t* src = cm + int64_t(r) * (V + 1);
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int i = lane + 32 * q;
+        if (i <= V) cp_async4_u32(dst + i, src + i);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+#pragma unroll
+  for (int i = 0; i < kCumAhead - 1; ++i) stage(i);
+  auto word = [&](uint64_t at) -> uint32_t {  // aligned 4 bytes at `at`, bytes >= plen read as 0
+    if (at + 4 <= plen) return *reinterpret_cast<const uint32_t*>(buf + at);
+    uint32_t v = 0;
+    for (uint64_t b = at; b < plen && b < at + 4; ++b) v |= uint32_t(buf[b]) << (8 * (b - at));
+    return v;
+  };
+  uint64_t wb = s.pos & ~uint64_t(127);
+  uint32_t wa = word(wb + 4 * lane), wn = word(wb + 128 + 4 * lane);
+  uint64_t code = s.code, range = s.range, pos = s.pos;
+  for (int r = 0; r < R; ++r) {
+    stage(r + kCumAhead - 1);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kCumAhead - 1));
+    uint32_t cur[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int i = lane + 32 * q;
+      cur[q] = i <= V ? ring[r % kCumAhead][i] : 0xffffffffu;
+    }
+    const uint64_t rb = range >> 16;
+    // the reference's target is floor(code / rb) clamped to 65535 and the
+    // symbol the largest i < V with cum[i] <= target; for integers
+    // cum[i] <= floor(code / rb) <=> cum[i] * rb <= code (< 2^64: cum <= 2^16,
+    // rb < 2^48), and counting only i < V is the clamp. So no division: each
+    // lane compares its cum entries' products with code.
+    int count = 0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int i = lane + 32 * q;
+      count += __popc(__ballot_sync(0xffffffffu, i < V && uint64_t(cur[q]) * rb <= code));
+    }
+    const int sym = count - 1;
+    uint32_t p0 = cur[0], p1 = cur[0];
+#pragma unroll
+    for (int q = 1; q < NQ; ++q) {
+      if (q == (sym >> 5)) p0 = cur[q];
+      if (q == ((sym + 1) >> 5)) p1 = cur[q];
+    }
+    const uint32_t csym = __shfl_sync(0xffffffffu, p0, sym & 31);
+    const uint32_t cnext = __shfl_sync(0xffffffffu, p1, (sym + 1) & 31);
+    code -= rb * csym;
+    range = rb * (cnext - csym);  // freq = cum[s+1] - cum[s]
+    while (range < kRenorm) {  // dec_byte over the window
+      uint32_t byte = 0;
+      if (pos >= plen) {
+        s.err = 1;  // StreamExhausted
+      } else {
+        if (pos >= wb + 128) {
+          wb += 128;
+          wa = wn;
+          wn = word(wb + 128 + 4 * lane);
+        }
+        const uint32_t off = uint32_t(pos - wb);
+        byte = (__shfl_sync(0xffffffffu, wa, int(off >> 2)) >> (8 * (off & 3))) & 0xffu;
+        ++pos;
+      }
+      code = (code << 8) | byte;
+      range <<= 8;
+    }
+    if (lane == 0) tokens[start + uint64_t(r) * L + jstep] = uint32_t(sym);
+    if (s.err) break;
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  s.code = code;
+  s.range = range;
+  s.pos = pos;
+}
+
 // One warp per chunk. Encode: the warp gathers 32 rows' (cum, freq) of the
 // coded symbols into shared memory, lane 0 runs the 64-bit coder over them.
 // Decode: every lane carries the same coder state; the symbol search is a
 // warp ballot over the cum row held in registers (prefetched one row ahead),
 // which equals the reference binary search (largest i with cum[i] <= target).
 constexpr int kCoderWarps = 4;
-constexpr int kMaxQ = 8;  // V <= 256 in registers; larger V uses the scalar search
 __global__ void __launch_bounds__(kCoderWarps * 32) k_range_step(
     uint32_t* tokens, ChunkGeo geo, int t, int R, int V,
     const uint32_t* __restrict__ freq, const uint32_t* __restrict__ cum, int64_t cs_f,
@@ -427,6 +530,7 @@ __global__ void __launch_bounds__(kCoderWarps * 32) k_range_step(
     CoderState* cs, const TickDesc* __restrict__ td, bool decode) {
   pdl_wait();
   __shared__ uint32_t sc_[kCoderWarps][32], sf_[kCoderWarps][32];
+  __shared__ uint32_t scum[kCoderWarps][kCumAhead][kMaxQ * 32];  // decode: staged cum rows
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wi = blockIdx.x * kCoderWarps + wl;
   if (wi >= td->n_act) return;
@@ -468,48 +572,12 @@ __global__ void __launch_bounds__(kCoderWarps * 32) k_range_step(
     }
     return;
   }
-  const uint64_t plen = pay_len[ch];
-  uint32_t cur[kMaxQ], nxt[kMaxQ];
-#pragma unroll
-  for (int q = 0; q < kMaxQ; ++q) {
-    const int i = lane + 32 * q;
-    cur[q] = (q < nq && i <= V) ? cm[i] : 0xffffffffu;
-  }
-  for (int r = 0; r < R; ++r) {
-    if (r + 1 < R) {
-#pragma unroll
-      for (int q = 0; q < kMaxQ; ++q) {
-        const int i = lane + 32 * q;
-        nxt[q] = (q < nq && i <= V) ? cm[int64_t(r + 1) * (V + 1) + i] : 0xffffffffu;
-      }
-    }
-    const uint64_t rb = s.range >> 16;
-    const uint32_t tgt = dec_target(s.code, rb);
-    int count = 0;
-#pragma unroll
-    for (int q = 0; q < kMaxQ; ++q)
-      if (q < nq) count += __popc(__ballot_sync(0xffffffffu, cur[q] <= tgt));
-    // tgt <= 65535 < cum[V]: the count covers i < V only, so sym = count-1 in [0, V)
-    const int sym = count - 1;
-    uint32_t csym = 0, cnext = 0;
-#pragma unroll
-    for (int q = 0; q < kMaxQ; ++q) {
-      const uint32_t v0 = __shfl_sync(0xffffffffu, cur[q], sym & 31);
-      const uint32_t v1 = __shfl_sync(0xffffffffu, cur[q], (sym + 1) & 31);
-      if (q == (sym >> 5)) csym = v0;
-      if (q == ((sym + 1) >> 5)) cnext = v1;
-    }
-    const uint32_t fsym = cnext - csym;  // freq = cum[s+1] - cum[s]
-    s.code -= rb * csym;
-    s.range = rb * fsym;
-    while (s.range < kRenorm) {
-      s.code = (s.code << 8) | dec_byte(buf, plen, s.pos, s.err);
-      s.range <<= 8;
-    }
-    if (lane == 0) tokens[start + uint64_t(r) * L + jstep] = uint32_t(sym);
-    if (s.err) break;
-#pragma unroll
-    for (int q = 0; q < kMaxQ; ++q) cur[q] = nxt[q];
+  switch (nq) {
+    case 1: range_decode_rows<1>(s, tokens, start, L, jstep, R, V, cm, buf, pay_len[ch], scum[wl], lane); break;
+    case 2: range_decode_rows<2>(s, tokens, start, L, jstep, R, V, cm, buf, pay_len[ch], scum[wl], lane); break;
+    case 3: range_decode_rows<3>(s, tokens, start, L, jstep, R, V, cm, buf, pay_len[ch], scum[wl], lane); break;
+    case 4: range_decode_rows<4>(s, tokens, start, L, jstep, R, V, cm, buf, pay_len[ch], scum[wl], lane); break;
+    default: range_decode_rows<kMaxQ>(s, tokens, start, L, jstep, R, V, cm, buf, pay_len[ch], scum[wl], lane); break;
   }
   if (lane == 0) cs[ch] = s;
 }
