@@ -459,15 +459,21 @@ __device__ __forceinline__ void range_decode_rows(CoderState& s, uint32_t* token
   uint64_t wb = s.pos & ~uint64_t(127);
   uint32_t wa = word(wb + 4 * lane), wn = word(wb + 128 + 4 * lane);
   uint64_t code = s.code, range = s.range, pos = s.pos;
-  for (int r = 0; r < R; ++r) {
-    stage(r + kCumAhead - 1);
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(kCumAhead - 1));
-    uint32_t cur[NQ];
+  // row r's cum words in registers, row r+1's loaded during row r
+  uint32_t cur[NQ], nxt[NQ], mysym = 0;
+  auto load_row = [&](int r, uint32_t (&x)[NQ]) {
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int i = lane + 32 * q;
-      cur[q] = i <= V ? ring[r % kCumAhead][i] : 0xffffffffu;
+      x[q] = i <= V ? ring[r % kCumAhead][i] : 0xffffffffu;
     }
+  };
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(kCumAhead - 2));
+  load_row(0, cur);
+  for (int r = 0; r < R; ++r) {
+    stage(r + kCumAhead - 1);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(kCumAhead - 2));  // row r+1 landed
+    if (r + 1 < R) load_row(r + 1, nxt);
     const uint64_t rb = range >> 16;
     // the reference's target is floor(code / rb) clamped to 65535 and the
     // symbol the largest i < V with cum[i] <= target; for integers
@@ -481,35 +487,52 @@ __device__ __forceinline__ void range_decode_rows(CoderState& s, uint32_t* token
       count += __popc(__ballot_sync(0xffffffffu, i < V && uint64_t(cur[q]) * rb <= code));
     }
     const int sym = count - 1;
-    uint32_t p0 = cur[0], p1 = cur[0];
+    // cum[sym] and cum[sym+1]: shuffle every word column, select after (a
+    // register array indexed by sym would go through local memory)
+    uint32_t csym = 0, cnext = 0;
 #pragma unroll
-    for (int q = 1; q < NQ; ++q) {
-      if (q == (sym >> 5)) p0 = cur[q];
-      if (q == ((sym + 1) >> 5)) p1 = cur[q];
+    for (int q = 0; q < NQ; ++q) {
+      const uint32_t v0 = __shfl_sync(0xffffffffu, cur[q], sym & 31);
+      const uint32_t v1 = __shfl_sync(0xffffffffu, cur[q], (sym + 1) & 31);
+      if (q == (sym >> 5)) csym = v0;
+      if (q == ((sym + 1) >> 5)) cnext = v1;
     }
-    const uint32_t csym = __shfl_sync(0xffffffffu, p0, sym & 31);
-    const uint32_t cnext = __shfl_sync(0xffffffffu, p1, (sym + 1) & 31);
     code -= rb * csym;
     range = rb * (cnext - csym);  // freq = cum[s+1] - cum[s]
-    while (range < kRenorm) {  // dec_byte over the window
-      uint32_t byte = 0;
-      if (pos >= plen) {
-        s.err = 1;  // StreamExhausted
-      } else {
-        if (pos >= wb + 128) {
-          wb += 128;
-          wa = wn;
-          wn = word(wb + 128 + 4 * lane);
-        }
-        const uint32_t off = uint32_t(pos - wb);
-        byte = (__shfl_sync(0xffffffffu, wa, int(off >> 2)) >> (8 * (off & 3))) & 0xffu;
-        ++pos;
+    if (range < kRenorm) {
+      // the reference's byte loop (range < 2^56: range = range << 8 | next
+      // byte) runs once if range >= 2^48, else twice (range >= 2^40 since
+      // rb >= 2^40 and freq >= 1): both bytes come from the window at once
+      const bool two = range < (1ull << 48);
+      if (pos + (two ? 2 : 1) > plen) s.err = 1;  // StreamExhausted (bytes past the end read as 0)
+      if (pos >= wb + 128) {
+        wb += 128;
+        wa = wn;
+        wn = word(wb + 128 + 4 * lane);
       }
-      code = (code << 8) | byte;
-      range <<= 8;
+      const uint32_t off = uint32_t(pos - wb), off1 = off + 1;
+      const uint32_t w0 = __shfl_sync(0xffffffffu, wa, int(off >> 2));
+      const uint32_t w1 = __shfl_sync(0xffffffffu, off1 < 128 ? wa : wn, int((off1 >> 2) & 31));
+      const uint32_t b0 = (w0 >> (8 * (off & 3))) & 0xffu, b1 = (w1 >> (8 * (off1 & 3))) & 0xffu;
+      if (two) {
+        code = (code << 16) | (b0 << 8) | b1;
+        range <<= 16;
+        pos += 2;
+      } else {
+        code = (code << 8) | b0;
+        range <<= 8;
+        pos += 1;
+      }
     }
-    if (lane == 0) tokens[start + uint64_t(r) * L + jstep] = uint32_t(sym);
+    // the decoded symbols are stored 32 rows at a time (lane l keeps row r0+l's)
+    if (lane == (r & 31)) mysym = uint32_t(sym);
+    if ((r & 31) == 31 || r + 1 == R || s.err) {
+      const int r0 = r & ~31;
+      if (r0 + lane <= r) tokens[start + uint64_t(r0 + lane) * L + jstep] = mysym;
+    }
     if (s.err) break;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) cur[q] = nxt[q];
   }
   asm volatile("cp.async.wait_group 0;\n" ::);
   s.code = code;
