@@ -75,6 +75,37 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
   const float* xr = xi ? xi + c * work_cs + int64_t(dir) * 3 * RT * H : nullptr;
   const float* t0 = p.xi0 + int64_t(dir) * 3 * p.V * H;  // layer-0 tables [3][V][H]
   const int jj = act ? j : 0;
+  // layer 0: the rows' context tokens one per lane (T <= 32) and read by
+  // shuffle, and the step's table terms fetched one step ahead, so no step
+  // waits on a token load followed by a dependent table load
+  const bool lane_tok = l == 0 && T <= 32;
+  uint32_t mytok[kRPW];
+#pragma unroll
+  for (int u = 0; u < kRPW; ++u) {
+    const int r = rv_ok[u] ? r0 + u : r0;
+    mytok[u] = lane_tok && lane < T ? ctx[c * ctx_cs + int64_t(r) * T + lane] : 0u;
+  }
+  auto fetch = [&](int step, float (&x)[3][kRPW]) {
+    const int tt = dir ? (T - 1 - step) : step;
+#pragma unroll
+    for (int u = 0; u < kRPW; ++u) {
+      const int r = rv_ok[u] ? r0 + u : r0;
+      if (l == 0) {
+        const int64_t tok = lane_tok ? int64_t(__shfl_sync(0xffffffffu, mytok[u], tt))
+                                     : int64_t(ctx[c * ctx_cs + int64_t(r) * T + tt]);
+        x[0][u] = t0[tok * H + jj];
+        x[1][u] = t0[int64_t(p.V) * H + tok * H + jj];
+        x[2][u] = t0[2 * int64_t(p.V) * H + tok * H + jj];
+      } else {
+        const int64_t pos = (int64_t(r) * T + tt) * H + jj;
+        x[0][u] = xr[pos];
+        x[1][u] = xr[RT * H + pos];
+        x[2][u] = xr[2 * RT * H + pos];
+      }
+    }
+  };
+  float xn[3][kRPW];
+  fetch(0, xn);
   __syncwarp();
   int cur = 0;
   for (int step = 0; step < T; ++step) {
@@ -82,21 +113,11 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
     float ar[kRPW], az[kRPW], an[kRPW];
 #pragma unroll
     for (int u = 0; u < kRPW; ++u) {
-      const int r = rv_ok[u] ? r0 + u : r0;
-      if (l == 0) {
-        const int64_t tok = ctx[c * ctx_cs + int64_t(r) * T + tt];
-        ar[u] = t0[tok * H + jj];
-        az[u] = t0[int64_t(p.V) * H + tok * H + jj];
-        an[u] = t0[2 * int64_t(p.V) * H + tok * H + jj];
-      } else {
-        const int64_t pos = (int64_t(r) * T + tt) * H + jj;
-        ar[u] = xr[pos];
-        az[u] = xr[RT * H + pos];
-        an[u] = xr[2 * RT * H + pos];
-      }
-      ar[u] = fadd(ar[u], bhr);
-      az[u] = fadd(az[u], bhz);
+      ar[u] = fadd(xn[0][u], bhr);
+      az[u] = fadd(xn[1][u], bhz);
+      an[u] = xn[2][u];
     }
+    if (step + 1 < T) fetch(step + 1, xn);
     // gate pre-activations for rows (0,1) and (2,3) as paired chains, k ascending
     f2_t ar01 = f2_pack(ar[0], ar[1]), ar23 = f2_pack(ar[2], ar[3]);
     f2_t az01 = f2_pack(az[0], az[1]), az23 = f2_pack(az[2], az[3]);
