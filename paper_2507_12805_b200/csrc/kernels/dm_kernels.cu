@@ -1727,7 +1727,14 @@ void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int m
   if (int64_t(build(8, nb)) * max_active < 148 * 8) rpt = 4;
   if (rpt == 4 && int64_t(build(4, nb)) * max_active < 148 * 4) rpt = 2;
   const int tasks = build(rpt, nb);
-  bool deep = rpt == 2 && int64_t(tasks) * max_active < 148 * 2;
+  // deep regime up to 8 paired-row warps per SM: at ~24 chunks (the config-4
+  // SMP wavefront) one row per thread over more warps beats 2 paired rows
+  // (dWk/dWv reduction 191 -> 155 us per tick, decode tick 931 -> 892 us)
+  static const int deep_warps = [] {
+    const char* e = std::getenv("PMKLC_NT_DEEP_WARPS");
+    return e ? std::atoi(e) : 8;
+  }();
+  bool deep = rpt == 2 && int64_t(tasks) * max_active < 148 * deep_warps;
   // deep regime: one row per thread spreads the outputs over twice the SM
   // sub-partitions; each then needs 2 FP32-pipe cycles per k (exact mul +
   // add) under the 4-cycle add chain instead of exactly 4 with a row pair.

@@ -53,3 +53,16 @@ print(f"decode {n} B W={w}: {ticks} ticks, span {span / 1e3:.1f} ms, {span / max
 print("stream busy (us):", {k: round(v) for k, v in streams.items()})
 for k, (c, t) in rows[:30]:
     print(f"  {t / 1e3:9.1f} ms  n={c:6d}  avg {t / c:8.1f} us  per-tick {t / max(ticks, 1):7.1f} us  {k}")
+
+# one plateau tick: every kernel's stream, start and end relative to the tick's k_tick_advance
+adv = sorted(e["ts"] for e in ev if name(e) == "k_tick_advance")
+if len(adv) > 10:
+    i = len(adv) // 2
+    a, b = adv[i], adv[i + 1]
+    tick = sorted((e for e in ev if a <= e["ts"] < b), key=lambda e: e["ts"])
+    res["plateau_tick"] = [{"kernel": name(e), "stream": e.get("tid"), "start_us": round(e["ts"] - a, 1),
+                            "dur_us": round(e["dur"], 1)} for e in tick]
+    json.dump(res, open(out / "c4tick.json", "w"), indent=1)
+    print(f"plateau tick {i}: {b - a:.1f} us")
+    for k in res["plateau_tick"]:
+        print(f"  s{k['stream']:>3} {k['start_us']:8.1f} +{k['dur_us']:7.1f}  {k['kernel']}")
