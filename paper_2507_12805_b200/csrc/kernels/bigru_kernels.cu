@@ -36,6 +36,9 @@ __device__ __forceinline__ int64_t poff(const int64_t* offs, int l, int dir, int
 // Blocks are single-direction; the direction's W_h* (3 x Hs x Hs) sit in
 // shared memory, each warp runs kRPW rows so one weight read feeds kRPW
 // independent chains (and the register budget leaves room for 4+ blocks/SM).
+#ifndef PMKLC_REC_WREG
+#define PMKLC_REC_WREG 1
+#endif
 constexpr int kRPW = 4;
 template <int HS>
 __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
@@ -43,8 +46,12 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
     float* out, float* fin, int64_t work_cs, const TickDesc* __restrict__ td) {
   pdl_wait();
   static_assert(kRPW == 4, "rows are paired (0,1),(2,3)");
+#if PMKLC_REC_WREG
+  __shared__ __align__(16) float sh[kRecWarps][2][32][kRPW];  // h[q][row] per warp
+#else
   __shared__ __align__(16) float sw[3][HS][HS];
   __shared__ __align__(16) float sh[kRecWarps][2][32][kRPW];  // h[q][row] per warp
+#endif
   if (blockIdx.y >= unsigned(td->n_act)) return;
   const int c = td->act[blockIdx.y];
   const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -53,11 +60,13 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
   const int T = p.T, H = HS;
   const int64_t RT = int64_t(p.R) * T;
   const float* W = p.w;
+#if !PMKLC_REC_WREG
   for (int i = threadIdx.x; i < 3 * HS * HS; i += blockDim.x) {
     const int gate = i / (HS * HS), rem = i % (HS * HS);
     sw[gate][rem / HS][rem % HS] = W[poff(p.offs, l, dir, WHR + gate) + rem];
   }
   __syncthreads();
+#endif
   const int r0 = grp * kRPW;
   if (r0 >= p.R) return;
   const int j = lane;
@@ -75,6 +84,14 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
   const float* xr = xi ? xi + c * work_cs + int64_t(dir) * 3 * RT * H : nullptr;
   const float* t0 = p.xi0 + int64_t(dir) * 3 * p.V * H;  // layer-0 tables [3][V][H]
   const int jj = act ? j : 0;
+#if PMKLC_REC_WREG
+  // this lane's W_h columns (gate, q) in registers for the whole sequence
+  float wreg[3][HS];
+#pragma unroll
+  for (int g = 0; g < 3; ++g)
+#pragma unroll
+    for (int q = 0; q < HS; ++q) wreg[g][q] = __ldg(W + poff(p.offs, l, dir, WHR + g) + q * HS + jj);
+#endif
   // layer 0: the rows' context tokens one per lane (T <= 32) and read by
   // shuffle, and the step's table terms fetched one step ahead, so no step
   // waits on a token load followed by a dependent table load
@@ -122,12 +139,17 @@ __global__ void __launch_bounds__(kRecWarps * 32) k_bigru_rec(
     f2_t ar01 = f2_pack(ar[0], ar[1]), ar23 = f2_pack(ar[2], ar[3]);
     f2_t az01 = f2_pack(az[0], az[1]), az23 = f2_pack(az[2], az[3]);
     f2_t hh01 = f2_bcast(bhn), hh23 = f2_bcast(bhn);
-#pragma unroll 8
+#pragma unroll
     for (int q = 0; q < HS; ++q) {
       const float4 hv = *reinterpret_cast<const float4*>(&sh[wl][cur][q][0]);
       const f2_t h01 = f2_pack(hv.x, hv.y), h23 = f2_pack(hv.z, hv.w);
+#if PMKLC_REC_WREG
+      const f2_t wr = f2_bcast(wreg[0][q]), wz = f2_bcast(wreg[1][q]);
+      const f2_t wn = f2_bcast(wreg[2][q]);
+#else
       const f2_t wr = f2_bcast(sw[0][q][jj]), wz = f2_bcast(sw[1][q][jj]);
       const f2_t wn = f2_bcast(sw[2][q][jj]);
+#endif
       ar01 = f2_mac(ar01, h01, wr);
       ar23 = f2_mac(ar23, h23, wr);
       az01 = f2_mac(az01, h01, wz);
