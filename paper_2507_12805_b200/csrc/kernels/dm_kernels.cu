@@ -1726,6 +1726,11 @@ void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int m
   int rpt = 8;
   if (int64_t(build(8, nb)) * max_active < 148 * 8) rpt = 4;
   if (rpt == 4 && int64_t(build(4, nb)) * max_active < 148 * 4) rpt = 2;
+  static const int force_rpt = [] {  // PMKLC_NT_RPT=8|4|2: fixed rows per thread (experiments)
+    const char* e = std::getenv("PMKLC_NT_RPT");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (force_rpt == 8 || force_rpt == 4 || force_rpt == 2) rpt = force_rpt;
   const int tasks = build(rpt, nb);
   // deep regime up to 8 paired-row warps per SM: at ~24 chunks (the config-4
   // SMP wavefront) one row per thread over more warps beats 2 paired rows
@@ -1734,7 +1739,7 @@ void launch_gemm_nt_batch(const NtP* probs, int nprob, const TickDesc* td, int m
     const char* e = std::getenv("PMKLC_NT_DEEP_WARPS");
     return e ? std::atoi(e) : 8;
   }();
-  bool deep = rpt == 2 && int64_t(tasks) * max_active < 148 * deep_warps;
+  bool deep = !force_rpt && rpt == 2 && int64_t(tasks) * max_active < 148 * deep_warps;
   // deep regime: one row per thread spreads the outputs over twice the SM
   // sub-partitions; each then needs 2 FP32-pipe cycles per k (exact mul +
   // add) under the 4-cycle add chain instead of exactly 4 with a row pair.
