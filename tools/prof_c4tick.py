@@ -18,14 +18,23 @@ import paper_2507_12805_b200 as P
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 40_000_000
 w = int(sys.argv[2]) if len(sys.argv) > 2 else 256
-raw = P.synth("genome", n, 2026, 10)
-cfg = P.CompressConfig(workers=w, selector_threshold=0)
+spum = len(sys.argv) > 3 and sys.argv[3] == "spum"  # config-3 models (SPuM + DM, flags 5)
+if spum:
+    import tempfile
+    raw = P.synth("genome", n, 2025, 10)
+    pub = str(Path(tempfile.mkdtemp()) / "spum.bin")
+    P.write_bigru(pub, 3, 32, 4, 0xACE3, layers=2)
+    cfg = P.CompressConfig(workers=w, pub_model_path=pub)
+else:
+    pub = ""
+    raw = P.synth("genome", n, 2026, 10)
+    cfg = P.CompressConfig(workers=w, selector_threshold=0)
 blob = P.compress(raw, cfg)
-assert blob[5] == 6, blob[5]
-P.decompress(blob)  # warm
+assert blob[5] == (5 if spum else 6), blob[5]
+P.decompress(blob, pub)  # warm
 t0 = time.perf_counter()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
-    out_b = P.decompress(blob)
+    out_b = P.decompress(blob, pub)
     torch.cuda.synchronize()
 wall = (time.perf_counter() - t0) * 1e6
 assert out_b == raw
