@@ -121,22 +121,59 @@ __global__ void k_mix_quantize(MixP p, const TickDesc* __restrict__ td) {
     // V <= 64: each lane holds the remainders of i = lane, lane + 32; the rank
     // of element i = #{j : r_j > r_i or (r_j == r_i and j < i)} is counted
     // with two ballots per i (r_i broadcast by shuffle).
+    // The order is a total order on (remainder desc, index asc), so the ranks
+    // are the positions after sorting the 64 (key, index) pairs: a bitonic
+    // network over the warp (lane holds elements lane and lane + 32; key =
+    // the remainder's double bits mapped to an order-preserving unsigned,
+    // inverted for descending; absent elements sort last), then the first
+    // `part` sorted entries get the +1.
     const uint32_t full = uint32_t(deficit / V), part = uint32_t(deficit % V);
     const bool h0 = lane < V, h1 = lane + 32 < V;
     uint32_t f0 = 0, f1 = 0;
     const double r0 = h0 ? rem_of(pr[lane], f0) : 0.0;
     const double r1 = h1 ? rem_of(pr[lane + 32], f1) : 0.0;
-    uint32_t rk0 = 0, rk1 = 0;
-    for (int i = 0; i < V; ++i) {
-      const double ri = i < 32 ? __shfl_sync(0xffffffffu, r0, i) : __shfl_sync(0xffffffffu, r1, i - 32);
-      const bool c0 = h0 && (r0 > ri || (r0 == ri && lane < i));
-      const bool c1 = h1 && (r1 > ri || (r1 == ri && lane + 32 < i));
-      const uint32_t rank = __popc(__ballot_sync(0xffffffffu, c0)) + __popc(__ballot_sync(0xffffffffu, c1));
-      if (i == lane) rk0 = rank;
-      if (i == lane + 32) rk1 = rank;
+    auto key_of = [](double r, bool have) -> uint64_t {
+      if (!have) return ~0ull;
+      const uint64_t b = uint64_t(__double_as_longlong(r));
+      const uint64_t ord = (b >> 63) ? ~b : (b | (1ull << 63));  // ascending in r
+      return ~ord;                                                // descending in r
+    };
+    uint64_t ka = key_of(r0, h0), kb = key_of(r1, h1);
+    uint32_t ia = uint32_t(lane), ib = uint32_t(lane + 32);
+    auto less = [](uint64_t k1, uint32_t i1, uint64_t k2, uint32_t i2) {
+      return k1 < k2 || (k1 == k2 && i1 < i2);
+    };
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        if (j == 32) {  // partners lane and lane + 32 (k == 64: ascending)
+          if (less(kb, ib, ka, ia)) {
+            const uint64_t tk = ka;
+            const uint32_t ti = ia;
+            ka = kb; ia = ib; kb = tk; ib = ti;
+          }
+        } else {
+          const uint64_t pka = __shfl_xor_sync(0xffffffffu, ka, j);
+          const uint32_t pia = __shfl_xor_sync(0xffffffffu, ia, j);
+          const uint64_t pkb = __shfl_xor_sync(0xffffffffu, kb, j);
+          const uint32_t pib = __shfl_xor_sync(0xffffffffu, ib, j);
+          const bool lower = (lane & j) == 0;
+          // element e: ascending block iff (e & k) == 0; the lower index of a
+          // pair keeps the min in an ascending block, the max otherwise
+          const bool upa = (lane & k) == 0, upb = ((lane + 32) & k) == 0;
+          const bool mina = lower == upa, minb = lower == upb;
+          const bool pa_less = less(pka, pia, ka, ia), pb_less = less(pkb, pib, kb, ib);
+          if (mina == pa_less) { ka = pka; ia = pia; }
+          if (minb == pb_less) { kb = pkb; ib = pib; }
+        }
+      }
     }
-    if (h0) fq[lane] = f0 + full + (rk0 < part ? 1u : 0u);
-    if (h1) fq[lane + 32] = f1 + full + (rk1 < part ? 1u : 0u);
+    if (h0) fq[lane] = f0 + full;
+    if (h1) fq[lane + 32] = f1 + full;
+    __syncwarp();
+    if (uint32_t(lane) < part) fq[ia] += 1u;       // sorted position lane
+    if (uint32_t(lane + 32) < part) fq[ib] += 1u;  // sorted position lane + 32
   } else if (deficit > 0) {
     // stable_sort by (rem desc, idx asc), then +1 cyclically (coder.cpp:57-66)
     const uint32_t full = uint32_t(deficit / V), part = uint32_t(deficit % V);
