@@ -582,7 +582,7 @@ __device__ __forceinline__ void range_decode_rows(CoderState& s, uint32_t* token
 // Decode: every lane carries the same coder state; the symbol search is a
 // warp ballot over the cum row held in registers (prefetched one row ahead),
 // which equals the reference binary search (largest i with cum[i] <= target).
-constexpr int kCoderWarps = 4;
+constexpr int kCoderWarps = 1;
 __global__ void __launch_bounds__(kCoderWarps * 32) k_range_step(
     uint32_t* tokens, ChunkGeo geo, int t, int R, int V,
     const uint32_t* __restrict__ freq, const uint32_t* __restrict__ cum, int64_t cs_f,
