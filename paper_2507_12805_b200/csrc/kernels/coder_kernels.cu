@@ -53,6 +53,10 @@ __global__ void k_mix_quantize(MixP p, const TickDesc* __restrict__ td) {
   }
   if (row >= p.R) return;
   const int V = p.V;
+  // V <= 64: the serial sums read a per-warp shared copy
+  __shared__ __align__(16) float sbuf[8][64];
+  const bool small = V <= 64 && blockDim.x <= 256;
+  float* sb = sbuf[(threadIdx.x >> 5) & 7];
   const int64_t lo = c * p.cs_l + int64_t(row) * V;
   const float* lu = (p.flags & 1) ? p.lu + lo : nullptr;
   const float* lr = (p.flags & 2) ? p.lr + lo : nullptr;
@@ -83,9 +87,22 @@ __global__ void k_mix_quantize(MixP p, const TickDesc* __restrict__ td) {
       if (i < V) {
         e = det_exp(fsub(pr[i], mx));
         pr[i] = e;
+        if (small) sb[i] = e;
       }
-      const int cnt = min(32, V - i0);
-      for (int l = 0; l < cnt; ++l) sum = fadd(sum, __shfl_sync(0xffffffffu, e, l));
+      if (!small) {
+        const int cnt = min(32, V - i0);
+        for (int l = 0; l < cnt; ++l) sum = fadd(sum, __shfl_sync(0xffffffffu, e, l));
+      }
+    }
+    if (small) {  // the sequential sum over the warp's shared copy (broadcast LDS.128)
+      __syncwarp();
+      int i = 0;
+      for (; i + 4 <= V; i += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(sb + i);
+        sum = fadd(fadd(fadd(fadd(sum, v.x), v.y), v.z), v.w);
+      }
+      for (; i < V; ++i) sum = fadd(sum, sb[i]);
+      __syncwarp();
     }
     inv = fdiv(1.0f, sum);
   }
@@ -99,14 +116,29 @@ __global__ void k_mix_quantize(MixP p, const TickDesc* __restrict__ td) {
     if (i < V) {
       pv = p.probs_given ? pr[i] : fmul(pr[i], inv);
       pr[i] = pv;
+      if (small) sb[i] = pv;
       if (!(pv > 0.0f)) bad = true;
       uint32_t f;
       rem_of(pv, f);
       fq[i] = f;
       assigned += f;
     }
-    const int cnt = min(32, V - i0);
-    for (int l = 0; l < cnt; ++l) dsum = dsum + double(__shfl_sync(0xffffffffu, pv, l));
+    if (!small) {
+      const int cnt = min(32, V - i0);
+      for (int l = 0; l < cnt; ++l) dsum = dsum + double(__shfl_sync(0xffffffffu, pv, l));
+    }
+  }
+  if (small) {
+    __syncwarp();
+    int i = 0;
+    for (; i + 4 <= V; i += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(sb + i);
+      dsum = dsum + double(v.x);
+      dsum = dsum + double(v.y);
+      dsum = dsum + double(v.z);
+      dsum = dsum + double(v.w);
+    }
+    for (; i < V; ++i) dsum = dsum + double(sb[i]);
   }
   bad = __any_sync(0xffffffffu, bad);
   if (bad || fabs(dsum - 1.0) > 1e-5) {
