@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(256) k_sprm_fwd(SprmP s, const uint32_t* __res
 // (96 floats), so a step reads only h (8 broadcast LDS.128); the r and z gates
 // run as one paired chain, n as a scalar chain; next step's token and table
 // values are prefetched. Same per-element operations and order as k_sprm_fwd.
-constexpr int kFwdWarps = 4;
+constexpr int kFwdWarps = 2;
 __global__ void __launch_bounds__(kFwdWarps * 32) k_sprm_fwd32(SprmP s, const uint32_t* __restrict__ ctx,
                                                                const float* __restrict__ tab, float* tape,
                                                                float* fin) {
@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(256) k_sprm_bptt(SprmP s, const float* __restr
 // registers (96 floats); a step reads only the gate gradients (broadcast
 // LDS.128); the step's tape values are prefetched one step ahead. Same
 // per-element operations and order as k_sprm_bptt.
-constexpr int kBpttWarps = 4;
+constexpr int kBpttWarps = 2;
 constexpr int kPubSteps = 8;  // BPTT progress published per group of steps
 constexpr int kBpttAhead = 8;  // tape staging depth (steps)
 __device__ __forceinline__ void cp_async4_sp(float* smem, const float* gmem) {
